@@ -1,0 +1,321 @@
+/*
+ * nbg.h -- C ABI of the B200-native nonblocking GraphBLAS hot path (arxiv 2509.14211).
+ *
+ * The calls follow the paper's statement of the problem: GraphBLAS operations in program order
+ * define a DAG (Sec. 2); in NONBLOCKING mode an operation returns once its
+ * arguments are validated and the DAG is materialised at `wait` as fused GPU
+ * passes; in BLOCKING mode every operation is complete on return
+ * (PAPER.md:48, 255).  Results of both modes are equal up to floating-point rounding order
+ * (PAPER.md:52); this library keeps the blocking mode's rounding points in its fused kernels,
+ * so ranks agree bit for bit.
+ *
+ * Conventions (apply to every function):
+ *  - Return value: nbg_status.  NBG_SUCCESS = 0.  Validation errors (null handle, dimension or
+ *    domain mismatch, bad enum) are returned AT CALL TIME in both modes (PAPER.md:49,
+ *    SPEC.md:237).  Execution errors (a CUDA/NVRTC/NCCL failure, out of memory on the device)
+ *    are returned by the call that materialises the object (a wait, an export, a scalar read,
+ *    or any op in blocking mode) and latched on the context: nbg_last_error() returns the text.
+ *  - Handles (nbg_matrix, nbg_vector, nbg_scalar) are opaque and immutable: an operation never
+ *    modifies its inputs, it returns a NEW handle through its first out-parameter
+ *    (PAPER.md:113).  The caller owns every returned handle and releases it with
+ *    the matching nbg_*_free().  Freeing a handle that pending operations still reference is
+ *    safe: the library keeps the definition alive internally.
+ *  - Liveness: in nonblocking mode a pending node is materialised at wait iff it is requested
+ *    or the user still holds a handle to it; otherwise it is fused and elided.
+ *  - Memory spaces: NBG_HOST pointers are ordinary host memory (pinned or pageable);
+ *    NBG_DEVICE pointers are device memory of the context's GPU.  NBG_COPY copies the data;
+ *    NBG_BORROW keeps the device pointer (it must outlive the object and stay unmodified).
+ *  - All device work of a context is issued on the context's CUDA stream (config.stream, or a
+ *    library-owned stream when NULL).  Exports and scalar reads synchronise that stream.
+ *  - Index types: row pointers are int64, column indices int32 ("32 bit indices");
+ *    dimensions must be < 2^31 (NBG_INVALID_VALUE otherwise).
+ *  - A context is single-threaded: calls on one context must not run concurrently.
+ */
+#ifndef NBG_H
+#define NBG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status, types, modes */
+
+typedef enum {
+    NBG_SUCCESS = 0,
+    NBG_NULL_POINTER = 1,          /* a required pointer/handle argument is NULL */
+    NBG_INVALID_VALUE = 2,         /* bad enum, negative/oversized dimension, bad parameter */
+    NBG_DIMENSION_MISMATCH = 3,    /* operand lengths / matrix shape disagree */
+    NBG_DOMAIN_MISMATCH = 4,       /* operator not defined for the requested type */
+    NBG_INDEX_OUT_OF_BOUNDS = 5,   /* an index in user data is out of range */
+    NBG_INVALID_OBJECT = 6,        /* handle from another context, or an empty vector exported */
+    NBG_OUT_OF_MEMORY = 7,
+    NBG_NOT_IMPLEMENTED = 8,       /* valid request outside this subset (e.g. sparse vectors) */
+    NBG_PANIC = 9                  /* CUDA / NVRTC / NCCL failure; see nbg_last_error */
+} nbg_status;
+
+typedef enum { NBG_BOOL = 0, NBG_INT32 = 1, NBG_INT64 = 2, NBG_FP32 = 3, NBG_FP64 = 4 } nbg_type;
+
+typedef enum { NBG_BLOCKING = 0, NBG_NONBLOCKING = 1 } nbg_mode;
+
+typedef enum { NBG_HOST = 0, NBG_DEVICE = 1 } nbg_space;
+typedef enum { NBG_COPY = 0, NBG_BORROW = 1 } nbg_ownership;
+
+typedef struct nbg_ctx_s nbg_ctx;
+typedef struct nbg_matrix_s *nbg_matrix;
+typedef struct nbg_vector_s *nbg_vector;
+typedef struct nbg_scalar_s *nbg_scalar;
+
+typedef struct {
+    int mode;        /* nbg_mode; fixed for the context's lifetime */
+    int device;      /* CUDA device ordinal */
+    void *stream;    /* cudaStream_t to issue work on (borrowed), or NULL for a library stream */
+    int flags;       /* reserved, must be 0 */
+} nbg_config;
+
+/* ---------------------------------------------------------------- operators
+ * Operators are plain descriptors (no function pointers): the operation is inlined into the
+ * generated kernel per signature, as PAPER.md:227 specialises "the concrete operations".
+ * Every operator is evaluated in the OUTPUT type T of the operation that uses it: its inputs
+ * and constants are first converted to T (round to nearest for floating T, truncation toward
+ * zero for integer T; bool T computes in int64 and stores x != 0).  One IEEE round-to-nearest
+ * rounding per arithmetic step, no FMA contraction.                                          */
+
+typedef enum {
+    NBG_IDENTITY = 0,      /* x                                       */
+    NBG_AINV = 1,          /* -x                                      */
+    NBG_ABS = 2,           /* |x|                                     */
+    NBG_MINV = 3,          /* 1/x   (integer: 0 when x == 0)          */
+    NBG_ADD_C = 4,         /* x + c0        (Fig. 2: x -> x + 1)       */
+    NBG_MUL_C = 5,         /* x * c0                                  */
+    NBG_AXPB = 6,          /* (c0 * x) + c1, two roundings            */
+    NBG_ABS_SUB_C = 7,     /* |x - c0|                                */
+    NBG_RECIP_SCALED = 8,  /* x != 0 ? c0 / x : 0                     */
+    NBG_ISZERO = 9         /* x == 0 ? 1 : 0                          */
+} nbg_unop_code;
+
+typedef struct { int code; double c0; double c1; } nbg_unop;
+
+typedef enum {
+    NBG_PLUS = 0, NBG_MINUS = 1, NBG_TIMES = 2, NBG_DIV = 3, /* integer DIV: x/0 := 0 */
+    NBG_MIN = 4, NBG_MAX = 5,        /* IEEE minNum/maxNum (a NaN operand yields the other) */
+    NBG_FIRST = 6, NBG_SECOND = 7,   /* (x, y) -> x ; (x, y) -> y  (Fig. 6 mul "(_, x) -> x") */
+    NBG_ABSDIFF = 8,                 /* |x - y|       (Fig. 6)                      */
+    NBG_MAX_DIVX_C = 9               /* max(x / c0, y) (Fig. 6, c0 = damping)       */
+} nbg_binop_code;
+
+typedef struct { int code; double c0; } nbg_binop;
+
+/* Monoids (add of a semiring, reduce): NBG_PLUS (identity 0), NBG_MIN (+inf / INT_MAX),
+ * NBG_MAX (-inf / INT_MIN).  Floating PLUS folds accumulate in fp64. */
+typedef struct {
+    int add;        /* monoid: NBG_PLUS | NBG_MIN | NBG_MAX               (Fig. 3 `add`, `identity`) */
+    int mul;        /* any nbg_binop_code (Fig. 3 `mul`; x = A(i,j), y = u(j)) */
+    double mul_c0;  /* constant of `mul` when it takes one */
+} nbg_semiring;
+
+/* ---------------------------------------------------------------- context */
+
+/* Create a context on cfg->device.  Errors: NBG_NULL_POINTER, NBG_INVALID_VALUE (mode),
+ * NBG_PANIC (no CUDA device / driver error). */
+nbg_status nbg_init(nbg_ctx **ctx, const nbg_config *cfg);
+
+/* Destroy the context and every object still owned by it (outstanding handles become invalid). */
+nbg_status nbg_finalize(nbg_ctx *ctx);
+
+/* Copy the last latched error message (NUL-terminated, truncated to len) into buf. */
+nbg_status nbg_last_error(nbg_ctx *ctx, char *buf, size_t len);
+
+/* Block until all work issued on the context's stream has finished; returns a latched
+ * execution error if one occurred. */
+nbg_status nbg_sync(nbg_ctx *ctx);
+
+/* Planner / executor counters (SPEC.md:338-341 cache counters; PAPER.md:301-306 wait steps). */
+typedef struct {
+    uint64_t waits;                 /* regions materialised                                   */
+    uint64_t plans_built;           /* plan-cache misses (signature seen for the first time)  */
+    uint64_t plan_hits;             /* plan-cache hits (step 3 skipped)          */
+    uint64_t jit_compiles;          /* NVRTC compilations                       */
+    uint64_t kernels_launched;      /* kernels this library launched                          */
+    uint64_t vectors_materialized;  /* vector buffers written by kernels                      */
+    uint64_t intermediates_elided;  /* pending nodes computed in registers, never stored      */
+    uint64_t memo_hits;             /* pending nodes bound to an already computed result      */
+    uint64_t side_outputs;          /* speculative loop-carried outputs emitted               */
+    uint64_t bytes_materialized;    /* bytes of vector buffers written by kernels             */
+    uint64_t host_plan_ns;          /* host time spent planning (signature..launch)           */
+    double jit_ms;                  /* host time spent in NVRTC                               */
+} nbg_stats;
+
+nbg_status nbg_get_stats(nbg_ctx *ctx, nbg_stats *out);
+nbg_status nbg_reset_stats(nbg_ctx *ctx);
+
+/* Per-kernel-class device timing with CUDA events recorded on the context stream around every
+ * launch of that class (used by bench.py for the roofline).  Classes: "spmv" (any kernel with
+ * an mxv, fused or not), "ewise" (elementwise/reduce regions), "graph" (generation/CSR build).
+ * nbg_get_timing synchronises and returns the summed device milliseconds and launch count
+ * since the last nbg_set_timing(ctx, 1). */
+nbg_status nbg_set_timing(nbg_ctx *ctx, int enable);
+nbg_status nbg_get_timing(nbg_ctx *ctx, const char *kernel_class, double *total_ms, int64_t *launches);
+
+/* ---------------------------------------------------------------- matrices (CSR)
+ * A matrix is CSR with int64 row pointers and int32 column indices, columns strictly
+ * ascending within a row.  vals == NULL makes it iso-valued (every stored
+ * entry equals `iso`, PAPER.md:227 iso facet); otherwise vals has nnz entries of `type`. */
+nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64_t ncols, int64_t nnz,
+                               const int64_t *rowptr, const int32_t *colidx, const void *vals,
+                               int type, double iso, int space, int ownership);
+
+/* Build AT (edge u->v stored at AT[v,u], PAPER.md:266 `AT`) and the INT32 out-degree vector
+ * (`out_degree`) from an edge list of m edges (src[e] -> dst[e], ids in [0,n)).
+ * Self-loops are dropped and duplicate edges removed (BASELINE configs).  Runs on the GPU
+ * (radix sort by (dst, src), unique, histograms).  deg may be NULL.
+ * Errors: NBG_INDEX_OUT_OF_BOUNDS if an id is outside [0, n). */
+nbg_status nbg_matrix_from_edges(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, int64_t n, int64_t m,
+                                 const int32_t *src, const int32_t *dst, int space);
+
+/* Synthetic graphs (input recipe of DESIGN.md; BASELINE configs 1,3,4,5).
+ * kind NBG_GRAPH_RMAT: n = 2^scale, m = edge_factor * n, (a,b,c,d) = (0.57,0.19,0.19,0.05),
+ *   edge e level l draws u = SplitMix64(seed, e*64 + l) >> 11 (reading Q9).
+ * kind NBG_GRAPH_ER: n = 2^scale, m = edge_factor * n, src/dst = top scale bits of
+ *   SplitMix64(seed, 2e) / SplitMix64(seed, 2e+1) (reading Q11). */
+typedef enum { NBG_GRAPH_RMAT = 0, NBG_GRAPH_ER = 1 } nbg_graph_kind;
+typedef struct { int kind; int scale; int edge_factor; uint64_t seed; } nbg_graphgen;
+
+/* Write the m generated edges into src/dst (int32[m] each, in `space`). */
+nbg_status nbg_graph_edges(nbg_ctx *ctx, const nbg_graphgen *g, int32_t *src, int32_t *dst, int space);
+
+/* Generate on the device and build AT + out-degree (= nbg_graph_edges + nbg_matrix_from_edges
+ * without a host round trip). */
+nbg_status nbg_matrix_from_generator(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, const nbg_graphgen *g);
+
+nbg_status nbg_matrix_nrows(nbg_ctx *ctx, nbg_matrix A, int64_t *out);
+nbg_status nbg_matrix_ncols(nbg_ctx *ctx, nbg_matrix A, int64_t *out);
+nbg_status nbg_matrix_nnz(nbg_ctx *ctx, nbg_matrix A, int64_t *out);
+
+/* Copy the structure out (rowptr: nrows+1 int64, colidx: nnz int32) into `space`.  Synchronises. */
+nbg_status nbg_matrix_export_csr(nbg_ctx *ctx, nbg_matrix A, int64_t *rowptr, int32_t *colidx, int space);
+nbg_status nbg_matrix_free(nbg_ctx *ctx, nbg_matrix A);
+
+/* ---------------------------------------------------------------- vectors
+ * Representations in this subset: FULL (dense values), ISO full (one value, "iso
+ * value only once"), EMPTY (no stored entries).  Sparse/bitset vectors are
+ * outside the hot path and return NBG_NOT_IMPLEMENTED. */
+
+/* Empty vector of length n (Fig. 6 line 276 `GrBVector{Float32}(n)`). */
+nbg_status nbg_vector_new(nbg_ctx *ctx, nbg_vector *v, int type, int64_t n);
+
+/* Iso full vector, every entry = (type)value (Fig. 6 line 277 `GrBVector(n, 1/n)`). */
+nbg_status nbg_vector_new_const(nbg_ctx *ctx, nbg_vector *v, int type, int64_t n, double value);
+
+/* Full vector from n dense values of `type` in `space` (NBG_BORROW: device pointer kept). */
+nbg_status nbg_vector_from_dense(nbg_ctx *ctx, nbg_vector *v, int type, int64_t n, const void *data,
+                                 int space, int ownership);
+
+/* Materialise v (forces wait) and copy its n values (of v's type) to out in `space`.
+ * Errors: NBG_INVALID_OBJECT if v is empty.  Synchronises. */
+nbg_status nbg_vector_export_dense(nbg_ctx *ctx, nbg_vector v, void *out, int space);
+
+nbg_status nbg_vector_size(nbg_ctx *ctx, nbg_vector v, int64_t *n);
+nbg_status nbg_vector_type(nbg_ctx *ctx, nbg_vector v, int *type);
+/* Number of stored entries (n or 0); known at record time in this subset, no wait needed. */
+nbg_status nbg_vector_nvals(nbg_ctx *ctx, nbg_vector v, int64_t *nvals);
+/* 1 if v is currently materialised (FULL buffer, ISO or EMPTY), 0 if it is a pending node. */
+nbg_status nbg_vector_is_materialized(nbg_ctx *ctx, nbg_vector v, int *out);
+/* Materialise v and return the device address of its dense values (FULL vectors; an ISO vector
+ * is expanded once).  The pointer stays valid while v (or a handle to the same node) lives;
+ * the caller must not write through it (handles are immutable).  Used for zero-copy interop
+ * (e.g. torch) and to build row-block views for the multi-GPU driver. */
+nbg_status nbg_vector_device_ptr(nbg_ctx *ctx, nbg_vector v, void **ptr);
+nbg_status nbg_vector_free(nbg_ctx *ctx, nbg_vector v);
+
+/* ---------------------------------------------------------------- scalars */
+
+/* Materialised scalar (Fig. 6 line 275 `GrBScalar(1.0f0)`). */
+nbg_status nbg_scalar_new(nbg_ctx *ctx, nbg_scalar *s, int type, double value);
+/* Force materialisation and read the value as double (Fig. 6 `rdiff()`).
+ * Synchronises only on the event of the kernel that produced s. */
+nbg_status nbg_scalar_get(nbg_ctx *ctx, nbg_scalar s, double *value);
+nbg_status nbg_scalar_free(nbg_ctx *ctx, nbg_scalar s);
+
+/* ---------------------------------------------------------------- operations
+ * Each returns a new handle of output type `type` and the operand length; operands must be
+ * of equal length (NBG_DIMENSION_MISMATCH).  Full/iso operands: ewise_mult and ewise_add both
+ * apply op everywhere; with an EMPTY operand ewise_mult is empty (intersection)
+ * and ewise_add yields the other operand converted to `type` (union). */
+nbg_status nbg_apply(nbg_ctx *ctx, nbg_vector *w, int type, nbg_unop op, nbg_vector u);           /* Fig. 4 VectorApply */
+nbg_status nbg_apply_bind2nd(nbg_ctx *ctx, nbg_vector *w, int type, nbg_binop op, nbg_vector u,
+                             nbg_scalar s);                                                       /* w = op(u, s) */
+nbg_status nbg_ewise_mult(nbg_ctx *ctx, nbg_vector *w, int type, nbg_binop op, nbg_vector u, nbg_vector v);  /* Fig. 1 */
+nbg_status nbg_ewise_add(nbg_ctx *ctx, nbg_vector *w, int type, nbg_binop op, nbg_vector u, nbg_vector v);   /* Fig. 6 l.288 */
+nbg_status nbg_convert(nbg_ctx *ctx, nbg_vector *w, int type, nbg_vector u);                      /* Fig. 6 `conv` */
+
+/* w(i) = add-fold over stored A(i,j) of mul(A(i,j), u(j)), identity for an empty row (dense
+ * output); A.ncols must equal len(u) (Fig. 3, Fig. 6). */
+nbg_status nbg_mxv(nbg_ctx *ctx, nbg_vector *w, int type, nbg_semiring sr, nbg_matrix A, nbg_vector u);
+
+/* s = add-fold of u's stored values (identity if empty) (Fig. 6).  Floating PLUS is
+ * accumulated in fp64 per thread block and combined EXACTLY across blocks (order-independent
+ * fixed-point limbs), so the value is deterministic; |terms| must be < 2^127. */
+nbg_status nbg_reduce(nbg_ctx *ctx, nbg_scalar *s, int type, int monoid, nbg_vector u);
+
+/* s_out = op(s_in) evaluated in `type` (a scalar node of the DAG, e.g. the dangling constant). */
+nbg_status nbg_scalar_apply(nbg_ctx *ctx, nbg_scalar *s_out, int type, nbg_unop op, nbg_scalar s_in);
+
+/* ---------------------------------------------------------------- wait
+ * Materialise v (and every live pending node it depends on) -- the `wait` of PAPER.md:66,136
+ * and Fig. 6: signature -> plan cache -> (NVRTC compile on a miss) -> launch
+ * (PAPER.md:301-306).  Idempotent.  Returns after LAUNCHING (device work may be in flight);
+ * exports and nbg_scalar_get synchronise. */
+nbg_status nbg_vector_wait(nbg_ctx *ctx, nbg_vector v);
+nbg_status nbg_scalar_wait(nbg_ctx *ctx, nbg_scalar s);
+
+/* ---------------------------------------------------------------- PageRank (Fig. 6)
+ * Written purely on the operations above.  AT: n x n pattern CSR (edge
+ * u->v at AT[v,u]); deg: out-degrees (any numeric type).  dangling NBG_PR_UNIFORM adds the
+ * dangling mass alpha*ds/n to every rank (Google matrix, ranks sum to 1; BASELINE config 4);
+ * NBG_PR_DROP is Fig. 6 literally (no redistribution).  tol < 0 runs exactly itermax sweeps.
+ * On return *r is the rank vector (caller frees), *sweeps the number of SpMV sweeps
+ * (Fig. 6's iter = sweeps + 1), delta_hist (may be NULL, >= itermax doubles) the L1 deltas. */
+typedef enum { NBG_PR_UNIFORM = 0, NBG_PR_DROP = 1 } nbg_pr_dangling;
+typedef struct { double alpha; double tol; int itermax; int dangling; int type; } nbg_pr_params;
+
+nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, const nbg_pr_params *p,
+                        nbg_vector *r, int *sweeps, double *delta_hist);
+
+/* ---------------------------------------------------------------- multi-GPU (1-D row partition)
+ * One process per GPU; torch.distributed only broadcasts the 128-byte NCCL unique id.
+ * nbg_partition_rows is host-only (no GPU): cut points cuts[0..nparts] (cuts[0]=0,
+ * cuts[nparts]=n) of a contiguous row partition balanced by per-row bytes
+ * 4*len(i) + 8 + bytes_per_row. */
+nbg_status nbg_partition_rows(const int64_t *rowptr, int64_t n, int nparts, int64_t bytes_per_row,
+                              int64_t *cuts);
+nbg_status nbg_dist_unique_id(void *id128);
+nbg_status nbg_dist_init(nbg_ctx *ctx, int rank, int nranks, const void *id128);
+
+/* Rows [lo, hi) of A as a new matrix with all of A's columns (row pointers rebased to 0).
+ * Used to hand each rank its block of the 1-D row partition. */
+nbg_status nbg_matrix_row_block(nbg_ctx *ctx, nbg_matrix *B, nbg_matrix A, int64_t lo, int64_t hi);
+
+/* Collective operations (require nbg_dist_init; they are fusion barriers: the input is
+ * materialised, then the collective is enqueued on the context stream).
+ * allgather: every rank passes its block u_blk (length cuts[rank+1]-cuts[rank]); w is the
+ *   full vector of length cuts[nranks] on every rank (allgather-v as grouped ncclBroadcast).
+ * allreduce: s_out = the sum (PLUS reductions, combined EXACTLY on the fixed-point limbs, so
+ *   the result is independent of the rank order) or min/max of s over all ranks. */
+nbg_status nbg_vector_allgather(nbg_ctx *ctx, nbg_vector *w, nbg_vector u_blk, const int64_t *cuts);
+nbg_status nbg_scalar_allreduce(nbg_ctx *ctx, nbg_scalar *s_out, nbg_scalar s);
+
+/* Distributed PageRank: every rank holds AT_blk = rows [cuts[rank], cuts[rank+1]) of AT (all n
+ * columns) and the global out-degree vector deg (length n).  Each sweep runs the fused kernel
+ * on the local rows, then exchanges the scaled ranks with an allgather-v over NCCL and combines
+ * the delta / dangling mass exactly (integer allreduce of the fixed-point limbs).
+ * r_blk receives this rank's block of the ranks (length cuts[rank+1]-cuts[rank]). */
+nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg, const int64_t *cuts,
+                             const nbg_pr_params *p, nbg_vector *r_blk, int *sweeps, double *delta_hist);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBG_H */

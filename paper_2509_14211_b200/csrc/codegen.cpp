@@ -1,0 +1,501 @@
+// codegen.cpp -- region IR -> CUDA C++ source for NVRTC (sm_100a).
+//
+// This is the GPU form of the paper's multi-stage programming (Figs. 1,2,4,5):
+// the planner hands over a region of the DAG as a small SSA program (Prog); we splice the
+// operators inline into ONE loop over the output index space -- "one or two outer loops per
+// wait, nested methods fused into that loop" -- and, when the region contains
+// an mxv, into the epilogue of the SpMV tile loop.  Constants and iso values are runtime
+// arguments (a.imm[]), so a kernel depends only on the signature, not on values.
+//
+// Two skeletons:
+//   ewise : grid-stride loop, 4 elements per thread per step with 16-byte vector loads/stores
+//           (float4 / int4 / 2x double2 / uchar4), reductions -> fp64 per-thread partial ->
+//           fixed shuffle tree -> warp partials in order -> exact limb atomics (prelude).
+//   spmv  : persistent CTAs walk work items (long-row chunks first, then row tiles):
+//           tile:  rowptr slice -> smem offsets; gather MUL(A(i,j), x(j)) for all nonzeros of the
+//                  tile into smem with lanes on consecutive nonzeros (coalesced colidx stream,
+//                  neighbouring columns of a row share sectors); rows with > 32 entries are
+//                  reduced by a warp (lane-strided + shuffle tree), the rest sequentially by one
+//                  thread; then the epilogue program runs once per row, one thread per row.
+//           chunk: CHUNK nonzeros of one long row reduced by the CTA; the CTA that completes the
+//                  row's last chunk (atomic ticket) sums the chunk partials in chunk order and
+//                  runs the epilogue.
+//          The summation order of a row depends only on its length, so the
+//          fused and the blocking mxv -- and every row partition -- produce identical row sums.
+#include <sstream>
+
+#include "nbg_internal.hpp"
+
+namespace nbg {
+
+static const char *ctype(int t) {
+    switch (t) {
+        case NBG_BOOL: return "unsigned char";
+        case NBG_INT32: return "int";
+        case NBG_INT64: return "long long";
+        case NBG_FP32: return "float";
+        case NBG_FP64: return "double";
+    }
+    return "?";
+}
+// type in which an operator with output type t is evaluated
+static const char *ctype_compute(int t) { return t == NBG_BOOL ? "long long" : ctype(t); }
+
+std::string Prog::signature() const {
+    std::ostringstream s;
+    s << (spmv ? "S" : "E") << (vec ? "v" : "s") << "|";
+    if (spmv) s << sp.add << "," << sp.mul << "," << sp.T << "," << sp.xt << "," << sp.at << "," << sp.has_vals << "|";
+    for (const Ins &i : ins)
+        s << (int)i.k << ":" << i.t << ":" << i.code << ":" << i.a << ":" << i.b << ":" << i.imm0 << ":" << i.imm1
+          << ":" << i.slot << ":" << (int)i.fmt << ";";
+    s << "|";
+    for (const OutV &o : outs) s << o.ins << ">" << o.out << ";";
+    s << "|";
+    for (const RedOut &r : reds) s << r.ins << ">" << r.monoid << ":" << r.racc << ":" << (int)r.fmt << ";";
+    s << "|" << n_in << "," << n_out << "," << n_imm << "," << n_sin << "," << n_red;
+    return s.str();
+}
+
+namespace {
+
+struct Gen {
+    const Prog &p;
+    std::ostringstream o;
+    explicit Gen(const Prog &pp) : p(pp) {}
+
+    std::string v(int i) const { return "v" + std::to_string(i); }
+
+    std::string cvt(int to, const std::string &x) const {
+        if (to == NBG_BOOL) return "((unsigned char)((" + x + ") != 0))";
+        return "((" + std::string(ctype(to)) + ")(" + x + "))";
+    }
+
+    // expression computing instruction i (operands are already-declared variables)
+    std::string expr(const Ins &in, const std::string &accname) const {
+        const std::string C = ctype_compute(in.t);
+        auto opnd = [&](int j) { return "((" + C + ")(" + v(j) + "))"; };
+        auto k0 = [&]() { return "((" + C + ")(a.imm[" + std::to_string(in.imm0) + "]))"; };
+        auto k1 = [&]() { return "((" + C + ")(a.imm[" + std::to_string(in.imm1) + "]))"; };
+        std::string r;
+        switch (in.k) {
+            case Ins::LD_VEC:
+                return "";   // handled by the skeleton
+            case Ins::LD_ISO:
+            case Ins::LD_SHOST:
+                return cvt(in.t, "a.imm[" + std::to_string(in.slot) + "]");
+            case Ins::LD_SDEV:
+                if (is_float(in.t))
+                    return cvt(in.t, "nbg_sval(a.sin[" + std::to_string(in.slot) + "], " + std::to_string(in.fmt) + ")");
+                return cvt(in.t, "nbg_sval_i(a.sin[" + std::to_string(in.slot) + "], " + std::to_string(in.fmt) + ")");
+            case Ins::MXV_ACC:
+                return cvt(in.t, accname);
+            case Ins::CVT:
+                return cvt(in.t, v(in.a));
+            case Ins::UN: {
+                std::string x = opnd(in.a);
+                switch (in.code) {
+                    case NBG_IDENTITY: r = x; break;
+                    case NBG_AINV: r = "(-" + x + ")"; break;
+                    case NBG_ABS: r = "nbg_abs(" + x + ")"; break;
+                    case NBG_MINV: r = "nbg_div((" + C + ")1, " + x + ")"; break;
+                    case NBG_ADD_C: r = "(" + x + " + " + k0() + ")"; break;
+                    case NBG_MUL_C: r = "(" + x + " * " + k0() + ")"; break;
+                    case NBG_AXPB: r = "((" + k0() + " * " + x + ") + " + k1() + ")"; break;
+                    case NBG_ABS_SUB_C: r = "nbg_abs(" + x + " - " + k0() + ")"; break;
+                    case NBG_RECIP_SCALED:
+                        r = "((" + x + " != (" + C + ")0) ? nbg_div(" + k0() + ", " + x + ") : (" + C + ")0)";
+                        break;
+                    case NBG_ISZERO: r = "((" + x + " == (" + C + ")0) ? (" + C + ")1 : (" + C + ")0)"; break;
+                    default: fail(NBG_INVALID_VALUE, "codegen: unop code");
+                }
+                break;
+            }
+            case Ins::BIN: {
+                std::string x = opnd(in.a), y = opnd(in.b);
+                switch (in.code) {
+                    case NBG_PLUS: r = "(" + x + " + " + y + ")"; break;
+                    case NBG_MINUS: r = "(" + x + " - " + y + ")"; break;
+                    case NBG_TIMES: r = "(" + x + " * " + y + ")"; break;
+                    case NBG_DIV: r = "nbg_div(" + x + ", " + y + ")"; break;
+                    case NBG_MIN: r = "nbg_min(" + x + ", " + y + ")"; break;
+                    case NBG_MAX: r = "nbg_max(" + x + ", " + y + ")"; break;
+                    case NBG_FIRST: r = x; break;
+                    case NBG_SECOND: r = y; break;
+                    case NBG_ABSDIFF: r = "nbg_abs(" + x + " - " + y + ")"; break;
+                    case NBG_MAX_DIVX_C: r = "nbg_max(nbg_div(" + x + ", " + k0() + "), " + y + ")"; break;
+                    default: fail(NBG_INVALID_VALUE, "codegen: binop code");
+                }
+                break;
+            }
+        }
+        if (in.t == NBG_BOOL) return "((unsigned char)((" + r + ") != 0))";
+        return r;
+    }
+
+    // --- reductions
+    struct RedKind { std::string acct, ident, comb; int kind; };
+    RedKind redkind(const RedOut &r) const {
+        int t = p.ins[r.ins].t;
+        bool f = is_float(t);
+        // monoid evaluated on the term converted to the reduce output type (already done by the
+        // planner with a CVT instruction), accumulated in fp64 (floats) or int64 (ints)
+        if (r.monoid == NBG_PLUS) {
+            if (f) return {"double", "0.0", "+", 0};
+            return {"long long", "0ll", "+", 1};
+        }
+        if (r.monoid == NBG_MAX) {
+            if (f) return {"double", "(-__longlong_as_double(0x7ff0000000000000ll))", "max", 2};
+            return {"long long", "((long long)0x8000000000000000ull)", "max", 4};
+        }
+        if (f) return {"double", "(__longlong_as_double(0x7ff0000000000000ll))", "min", 3};
+        return {"long long", "0x7fffffffffffffffll", "min", 5};
+    }
+    std::string red_update(const RedOut &r, const std::string &acc, const std::string &val) const {
+        RedKind k = redkind(r);
+        std::string x = "((" + k.acct + ")(" + val + "))";
+        if (k.comb == "+") return acc + " += " + x + ";";
+        if (k.comb == "max") return acc + " = nbg_max(" + acc + ", " + x + ");";
+        return acc + " = nbg_min(" + acc + ", " + x + ");";
+    }
+    // a single term straight to the global combine (long-row epilogue)
+    std::string red_direct(const RedOut &r, const std::string &val) const {
+        RedKind k = redkind(r);
+        std::string acc = "a.racc[" + std::to_string(r.racc) + "]";
+        std::string x = "((" + k.acct + ")(" + val + "))";
+        switch (k.kind) {
+            case 0: return "nbg_xacc_add(" + acc + ", " + x + ");";
+            case 1: return "atomicAdd(&" + acc + "[11], (u64)" + x + ");";
+            case 2: return "atomicMax(&" + acc + "[11], nbg_fkey(" + x + "));";
+            case 3: return "atomicMax(&" + acc + "[11], ~nbg_fkey(" + x + "));";
+            case 4: return "atomicMax(&" + acc + "[11], nbg_ikey(" + x + "));";
+            default: return "atomicMax(&" + acc + "[11], ~nbg_ikey(" + x + "));";
+        }
+    }
+
+    void emit_uniform() {
+        for (size_t i = 0; i < p.ins.size(); i++) {
+            const Ins &in = p.ins[i];
+            if (!in.uniform) continue;
+            o << "  const " << ctype(in.t) << " " << v((int)i) << " = " << expr(in, "") << ";\n";
+        }
+    }
+    void emit_red_decl() {
+        for (size_t j = 0; j < p.reds.size(); j++) {
+            RedKind k = redkind(p.reds[j]);
+            o << "  " << k.acct << " r" << j << " = " << k.ident << ";\n";
+        }
+    }
+    void emit_red_finish() {
+        for (size_t j = 0; j < p.reds.size(); j++) {
+            RedKind k = redkind(p.reds[j]);
+            if (k.acct == "double")
+                o << "  nbg_block_finish_f(r" << j << ", " << k.kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+            else
+                o << "  nbg_block_finish_i(r" << j << ", " << k.kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+        }
+    }
+
+    // per-element body: non-uniform instructions; LD_VEC reads `ld(slot)`; outputs/reductions
+    // through the given callbacks.
+    template <class LD, class ST, class RD>
+    void emit_body(const std::string &ind, LD ld, ST st, RD rd, const std::string &accname) {
+        for (size_t i = 0; i < p.ins.size(); i++) {
+            const Ins &in = p.ins[i];
+            if (in.uniform) continue;
+            if (in.k == Ins::LD_VEC)
+                o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = " << ld(in) << ";\n";
+            else
+                o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = " << expr(in, accname) << ";\n";
+        }
+        for (const OutV &ov : p.outs) o << ind << st(ov) << "\n";
+        for (size_t j = 0; j < p.reds.size(); j++) o << ind << rd(j) << "\n";
+    }
+};
+
+// vector load / store helpers for 4 consecutive elements of type t at vector index `vi`
+std::string vload(int t, const std::string &ptr, const std::string &vi, const std::string &dst) {
+    std::ostringstream s;
+    switch (t) {
+        case NBG_FP32:
+            s << "{ const float4 q = __ldg(((const float4*)(" << ptr << ")) + " << vi << "); " << dst << "[0]=q.x; "
+              << dst << "[1]=q.y; " << dst << "[2]=q.z; " << dst << "[3]=q.w; }";
+            break;
+        case NBG_INT32:
+            s << "{ const int4 q = __ldg(((const int4*)(" << ptr << ")) + " << vi << "); " << dst << "[0]=q.x; "
+              << dst << "[1]=q.y; " << dst << "[2]=q.z; " << dst << "[3]=q.w; }";
+            break;
+        case NBG_FP64:
+            s << "{ const double2 q0 = __ldg(((const double2*)(" << ptr << ")) + 2*" << vi << "); const double2 q1 = __ldg(((const double2*)(" << ptr
+              << ")) + 2*" << vi << "+1); " << dst << "[0]=q0.x; " << dst << "[1]=q0.y; " << dst << "[2]=q1.x; " << dst
+              << "[3]=q1.y; }";
+            break;
+        case NBG_INT64:
+            s << "{ const longlong2 q0 = __ldg(((const longlong2*)(" << ptr << ")) + 2*" << vi
+              << "); const longlong2 q1 = __ldg(((const longlong2*)(" << ptr << ")) + 2*" << vi << "+1); " << dst
+              << "[0]=q0.x; " << dst << "[1]=q0.y; " << dst << "[2]=q1.x; " << dst << "[3]=q1.y; }";
+            break;
+        case NBG_BOOL:
+            s << "{ const uchar4 q = ((const uchar4*)(" << ptr << "))[" << vi << "]; " << dst << "[0]=q.x; " << dst
+              << "[1]=q.y; " << dst << "[2]=q.z; " << dst << "[3]=q.w; }";
+            break;
+    }
+    return s.str();
+}
+std::string vstore(int t, const std::string &ptr, const std::string &vi, const std::string &src) {
+    std::ostringstream s;
+    switch (t) {
+        case NBG_FP32:
+            s << "((float4*)(" << ptr << "))[" << vi << "] = make_float4(" << src << "[0], " << src << "[1], " << src << "[2], " << src << "[3]);";
+            break;
+        case NBG_INT32:
+            s << "((int4*)(" << ptr << "))[" << vi << "] = make_int4(" << src << "[0], " << src << "[1], " << src << "[2], " << src << "[3]);";
+            break;
+        case NBG_FP64:
+            s << "((double2*)(" << ptr << "))[2*" << vi << "] = make_double2(" << src << "[0], " << src << "[1]); ((double2*)(" << ptr
+              << "))[2*" << vi << "+1] = make_double2(" << src << "[2], " << src << "[3]);";
+            break;
+        case NBG_INT64:
+            s << "((longlong2*)(" << ptr << "))[2*" << vi << "] = make_longlong2(" << src << "[0], " << src << "[1]); ((longlong2*)(" << ptr
+              << "))[2*" << vi << "+1] = make_longlong2(" << src << "[2], " << src << "[3]);";
+            break;
+        case NBG_BOOL:
+            s << "((uchar4*)(" << ptr << "))[" << vi << "] = make_uchar4(" << src << "[0], " << src << "[1], " << src << "[2], " << src << "[3]);";
+            break;
+    }
+    return s.str();
+}
+
+void gen_ewise(Gen &g, const std::string &kname, bool vec) {
+    const Prog &p = g.p;
+    auto &o = g.o;
+    // which slots are loaded, with their types
+    std::vector<int> slot_type(p.n_in, -1);
+    for (const Ins &in : p.ins)
+        if (in.k == Ins::LD_VEC) slot_type[in.slot] = in.t;
+    std::vector<int> out_type(p.n_out, -1);
+    for (const OutV &ov : p.outs) out_type[ov.out] = p.ins[ov.ins].t;
+
+    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
+    o << "  __shared__ double nbg_sh[32];\n";
+    g.emit_uniform();
+    g.emit_red_decl();
+    o << "  const long long n = a.n;\n";
+    o << "  const long long stride = (long long)gridDim.x * blockDim.x;\n";
+    o << "  long long tail0 = 0;\n";
+    if (vec) {
+        o << "  const long long nv = n >> 2;\n  tail0 = nv << 2;\n";
+        o << "  for (long long vi = (long long)blockIdx.x * blockDim.x + threadIdx.x; vi < nv; vi += stride) {\n";
+        for (int s = 0; s < p.n_in; s++)
+            if (slot_type[s] >= 0) {
+                o << "    " << ctype(slot_type[s]) << " L" << s << "[4];\n";
+                o << "    " << vload(slot_type[s], "a.in[" + std::to_string(s) + "]", "vi", "L" + std::to_string(s)) << "\n";
+            }
+        for (int k = 0; k < p.n_out; k++)
+            if (out_type[k] >= 0) o << "    " << ctype(out_type[k]) << " O" << k << "[4];\n";
+        o << "    #pragma unroll\n    for (int e = 0; e < 4; e++) {\n";
+        g.emit_body(
+            "      ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
+            [&](const OutV &ov) { return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";"; },
+            [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
+        o << "    }\n";
+        for (int k = 0; k < p.n_out; k++)
+            if (out_type[k] >= 0) o << "    " << vstore(out_type[k], "a.out[" + std::to_string(k) + "]", "vi", "O" + std::to_string(k)) << "\n";
+        o << "  }\n";
+    }
+    o << "  for (long long i = tail0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {\n";
+    g.emit_body(
+        "    ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) {
+            return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[i] = " + g.v(ov.ins) + ";";
+        },
+        [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
+    o << "  }\n";
+    g.emit_red_finish();
+    o << "}\n";
+}
+
+void gen_spmv(Gen &g, const std::string &kname) {
+    const Prog &p = g.p;
+    auto &o = g.o;
+    const SpmvSig &sp = p.sp;
+    const char *T = ctype(sp.T);
+    const char *C = ctype_compute(sp.T);
+    // value type of the gathered products kept in shared memory
+    std::string VT = C;
+    // accumulator
+    std::string ACC, IDENT, ADD;
+    bool fT = is_float(sp.T);
+    if (sp.add == NBG_PLUS) {
+        ACC = fT ? "double" : "long long";
+        IDENT = fT ? "0.0" : "0ll";
+        ADD = "(A_ + B_)";
+    } else if (sp.add == NBG_MIN) {
+        ACC = C;
+        IDENT = fT ? (sp.T == NBG_FP32 ? "__int_as_float(0x7f800000)" : "__longlong_as_double(0x7ff0000000000000ll)")
+                   : (sp.T == NBG_INT32 ? "0x7fffffff" : "0x7fffffffffffffffll");
+        ADD = "nbg_min(A_, B_)";
+    } else {
+        ACC = C;
+        IDENT = fT ? (sp.T == NBG_FP32 ? "__int_as_float((int)0xff800000)" : "__longlong_as_double((long long)0xfff0000000000000ull)")
+                   : (sp.T == NBG_INT32 ? "((int)0x80000000)" : "((long long)0x8000000000000000ull)");
+        ADD = "nbg_max(A_, B_)";
+    }
+    // mul(A(i,j), x(j)) in the compute type of T
+    std::string av = sp.has_vals ? std::string("((") + C + ")(((const " + ctype(sp.at) + "*)a.aval)[P_]))"
+                                 : std::string("((") + C + ")(a.imm[0]))";
+    std::string xv = std::string("((") + C + ")(X_))";
+    std::string mul;
+    switch (sp.mul) {
+        case NBG_PLUS: mul = "(" + av + " + " + xv + ")"; break;
+        case NBG_MINUS: mul = "(" + av + " - " + xv + ")"; break;
+        case NBG_TIMES: mul = "(" + av + " * " + xv + ")"; break;
+        case NBG_DIV: mul = "nbg_div(" + av + ", " + xv + ")"; break;
+        case NBG_MIN: mul = "nbg_min(" + av + ", " + xv + ")"; break;
+        case NBG_MAX: mul = "nbg_max(" + av + ", " + xv + ")"; break;
+        case NBG_FIRST: mul = av; break;
+        case NBG_SECOND: mul = xv; break;
+        case NBG_ABSDIFF: mul = "nbg_abs(" + av + " - " + xv + ")"; break;
+        case NBG_MAX_DIVX_C: mul = "nbg_max(nbg_div(" + av + ", ((" + std::string(C) + ")(a.imm[1]))), " + xv + ")"; break;
+        default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
+    }
+    const int ACCW = (ACC == "double" || ACC == "long long") ? 2 : 1;   // 32-bit words of ACC
+
+    o << "#define NBG_D_TILE_VALS 3136\n#define NBG_D_TILE_ROWS 2080\n#define NBG_CHUNK 2048\n";
+    o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
+    o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << ctype(sp.xt) << " X_) { return "
+      << mul << "; }\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
+    o << "  __shared__ " << VT << " s_val[NBG_D_TILE_VALS];\n";
+    o << "  __shared__ int s_off[NBG_D_TILE_ROWS + 1];\n";
+    o << "  __shared__ int s_med[NBG_D_TILE_ROWS];\n";
+    o << "  __shared__ int s_nmed, s_flag;\n";
+    o << "  __shared__ double nbg_sh[32];\n";
+    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    o << "  const " << ctype(sp.xt) << "* __restrict__ X = (const " << ctype(sp.xt) << "*)a.x;\n";
+    g.emit_uniform();
+    g.emit_red_decl();
+    o << "  const long long items = a.nchunks + a.ntiles;\n";
+    o << "  for (long long it = blockIdx.x; it < items; it += gridDim.x) {\n";
+    // ---------------- chunk of a long row
+    o << "    if (it < a.nchunks) {\n";
+    o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
+    o << "      const long long pb = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
+    o << "      const int cnt = ch.w;\n";
+    o << "      " << ACC << " t = " << IDENT << ";\n";
+    o << "      for (int q0 = threadIdx.x; q0 < cnt; q0 += 1024) {\n";
+    o << "        int c_[4];\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; c_[u] = q < cnt ? __ldcs(a.colidx + pb + q) : 0; }\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; if (q < cnt) { const " << VT
+      << " m_ = nbg_mul(a, pb + q, __ldg(X + c_[u])); t = NBG_ADD(t, (" << ACC << ")m_); } }\n";
+    o << "      }\n";
+    // CTA combine of the chunk (fixed order)
+    if (ACC == "double" || ACC == "long long" || ACC == "float" || ACC == "int") {
+        o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
+    }
+    o << "      __syncthreads();\n";
+    o << "      if (lane == 0) ((" << ACC << "*)nbg_sh)[warp] = t;\n";
+    o << "      __syncthreads();\n";
+    o << "      if (threadIdx.x == 0) {\n";
+    o << "        " << ACC << " part = ((" << ACC << "*)nbg_sh)[0];\n";
+    o << "        for (int w = 1; w < (int)(blockDim.x >> 5); w++) part = NBG_ADD(part, ((" << ACC << "*)nbg_sh)[w]);\n";
+    o << "        ((" << ACC << "*)a.partials)[it] = part;\n";
+    o << "        __threadfence();\n";
+    o << "        const int4 lr = ((const int4*)a.longs)[ch.x];\n";
+    o << "        const int tk = atomicAdd(&a.counters[ch.x], 1);\n";
+    o << "        s_flag = (tk == lr.z - 1);\n";
+    o << "        if (s_flag) {\n";
+    o << "          __threadfence();\n";
+    o << "          " << ACC << " acc = " << IDENT << ";\n";
+    o << "          for (int j = 0; j < lr.z; j++) { " << ACC << " pj; const " << ACC << "* pp = ((const " << ACC
+      << "*)a.partials) + lr.y + j; pj = *(volatile const " << ACC << "*)pp; acc = NBG_ADD(acc, pj); }\n";
+    o << "          a.counters[ch.x] = 0;\n";
+    o << "          const long long i = lr.x;\n";
+    g.emit_body(
+        "          ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) {
+            return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[i] = " + g.v(ov.ins) + ";";
+        },
+        [&](size_t j) { return g.red_direct(p.reds[j], g.v(p.reds[j].ins)); }, "acc");
+    o << "        }\n";
+    o << "      }\n";
+    o << "      __syncthreads();\n";
+    o << "      continue;\n";
+    o << "    }\n";
+    // ---------------- tile of short / medium rows
+    o << "    {\n";
+    o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
+    o << "      const int rb = tl.x, R = tl.y - tl.x;\n";
+    o << "      const long long pa = a.rowptr[rb];\n";
+    o << "      for (int j = threadIdx.x; j <= R; j += 256) s_off[j] = (int)(a.rowptr[rb + j] - pa);\n";
+    o << "      if (threadIdx.x == 0) s_nmed = 0;\n";
+    o << "      __syncthreads();\n";
+    o << "      const int P = s_off[R];\n";
+    o << "      for (int q0 = threadIdx.x; q0 < P; q0 += 1024) {\n";
+    o << "        int c_[4];\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; c_[u] = q < P ? __ldcs(a.colidx + pa + q) : 0; }\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; if (q < P) s_val[q] = nbg_mul(a, pa + q, __ldg(X + c_[u])); }\n";
+    o << "      }\n";
+    o << "      for (int j = threadIdx.x; j < R; j += 256) if (s_off[j + 1] - s_off[j] > 32) s_med[atomicAdd(&s_nmed, 1)] = j;\n";
+    o << "      __syncthreads();\n";
+    o << "      const int nmed = s_nmed;\n";
+    o << "      for (int mi = warp; mi < nmed; mi += (int)(blockDim.x >> 5)) {\n";
+    o << "        const int j = s_med[mi];\n";
+    o << "        const int o0 = s_off[j], o1 = s_off[j + 1];\n";
+    o << "        " << ACC << " t = " << IDENT << ";\n";
+    o << "        for (int q = o0 + lane; q < o1; q += 32) t = NBG_ADD(t, (" << ACC << ")s_val[q]);\n";
+    o << "        for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
+    // park the row sum in the row's own (now consumed) value slots
+    if (ACCW == 2)
+        o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; const unsigned long long b_ = *(const unsigned long long*)&t; "
+             "w_[o0] = (unsigned)b_; w_[o0 + 1] = (unsigned)(b_ >> 32); }\n";
+    else
+        o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; w_[o0] = *(const unsigned*)&t; }\n";
+    o << "      }\n";
+    o << "      __syncthreads();\n";
+    o << "      for (int j = threadIdx.x; j < R; j += 256) {\n";
+    o << "        const int o0 = s_off[j], o1 = s_off[j + 1];\n";
+    o << "        " << ACC << " acc;\n";
+    o << "        if (o1 - o0 > 32) {\n";
+    if (ACCW == 2)
+        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned long long b_ = (unsigned long long)w_[o0] | ((unsigned long long)w_[o0 + 1] << 32); acc = *(const "
+          << ACC << "*)&b_;\n";
+    else
+        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned b_ = w_[o0]; acc = *(const " << ACC << "*)&b_;\n";
+    o << "        } else {\n";
+    o << "          acc = " << IDENT << ";\n";
+    o << "          for (int q = o0; q < o1; q++) acc = NBG_ADD(acc, (" << ACC << ")s_val[q]);\n";
+    o << "        }\n";
+    o << "        const long long i = (long long)rb + j;\n";
+    g.emit_body(
+        "        ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) {
+            return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[i] = " + g.v(ov.ins) + ";";
+        },
+        [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    o << "      }\n";
+    o << "      __syncthreads();\n";
+    o << "    }\n";
+    o << "  }\n";
+    g.emit_red_finish();
+    o << "}\n";
+    (void)T;
+}
+
+}  // namespace
+
+extern const char *NBG_PRELUDE_SRC;
+
+std::string codegen(const Prog &p, const std::string &kname) {
+    Gen g(p);
+    g.o << NBG_PRELUDE_SRC << "\n// ---- generated region: " << p.signature() << "\n";
+    if (p.spmv)
+        gen_spmv(g, kname);
+    else
+        gen_ewise(g, kname, p.vec);
+    return g.o.str();
+}
+
+}  // namespace nbg

@@ -1,0 +1,359 @@
+// graph.cu -- static sm_100a kernels for graph setup (once per graph):
+//   K1  gen_rmat / gen_er    counter-based edge generation (reading Q9 / Q11 of DESIGN.md)
+//   K2  build_csr            AT = CSR of the transpose: key (dst, src) radix sort (CUB),
+//                            unique + self-loop drop, rowptr by binary search, out-degree by
+//                            integer histogram (PAPER.md:266-267 `AT`, `out_degree`)
+//   K3  spmv plan            merge-path row tiles + long-row chunks for the fused SpMV
+//                            (DESIGN.md "K4 SpMV"), built once per matrix
+// Integer work only: results are bit-exact and deterministic (histogram atomics are integer).
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "nbg_internal.hpp"
+
+namespace nbg {
+
+namespace {
+
+constexpr int SP_TILE = 2048;    // merge items (rows + nonzeros) per tile
+constexpr int SP_LONG = 1024;    // rows with more nonzeros are processed as chunks
+constexpr int SP_CHUNK = 2048;   // nonzeros per chunk of a long row
+
+__device__ __forceinline__ unsigned long long sm64(unsigned long long key, unsigned long long k) {
+    unsigned long long z = key + (k + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_gen_rmat(int scale, long long m, unsigned long long seed, int *src, int *dst) {
+    const unsigned long long A = 5134103575202365ull;    // floor(0.57 * 2^53)
+    const unsigned long long AB = 6845471433603153ull;   // floor(0.76 * 2^53)
+    const unsigned long long ABC = 8556839292003942ull;  // floor(0.95 * 2^53)
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x) {
+        unsigned s = 0, d = 0;
+        for (int l = 0; l < scale; l++) {
+            unsigned long long u = sm64(seed, (unsigned long long)e * 64ull + (unsigned long long)l) >> 11;
+            unsigned sb = (u >= ABC) || (u >= AB && u < ABC);   // quadrants (1,0) and (1,1)
+            unsigned db = (u >= A && u < AB) || (u >= ABC);       // quadrants (0,1) and (1,1)
+            s |= sb << (scale - 1 - l);
+            d |= db << (scale - 1 - l);
+        }
+        src[e] = (int)s;
+        dst[e] = (int)d;
+    }
+}
+
+__global__ void k_gen_er(int logn, long long m, unsigned long long seed, int *src, int *dst) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x) {
+        src[e] = (int)(sm64(seed, 2ull * (unsigned long long)e) >> (64 - logn));
+        dst[e] = (int)(sm64(seed, 2ull * (unsigned long long)e + 1ull) >> (64 - logn));
+    }
+}
+
+__global__ void k_make_keys(long long m, long long n, int shift, const int *src, const int *dst,
+                            unsigned long long *keys, int *bad) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x) {
+        int s = src[e], d = dst[e];
+        if (s < 0 || d < 0 || s >= n || d >= n) { *bad = 1; s = 0; d = 0; }
+        keys[e] = ((unsigned long long)(unsigned)d << shift) | (unsigned long long)(unsigned)s;
+    }
+}
+
+// keep the first of equal keys and drop self-loops
+__global__ void k_flags(long long m, int shift, const unsigned long long *keys, unsigned char *flags) {
+    const unsigned long long mask = (1ull << shift) - 1ull;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long k = keys[i];
+        bool keep = (i == 0 || keys[i - 1] != k) && ((k >> shift) != (k & mask));
+        flags[i] = keep ? 1 : 0;
+    }
+}
+
+__global__ void k_colidx_deg(long long nnz, int shift, const unsigned long long *keys, int *colidx, int *deg) {
+    const unsigned long long mask = (1ull << shift) - 1ull;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (long long)gridDim.x * blockDim.x) {
+        int s = (int)(keys[i] & mask);
+        colidx[i] = s;
+        atomicAdd(&deg[s], 1);
+    }
+}
+
+// rowptr[i] = first position whose row >= i  (i in [0, n])
+__global__ void k_rowptr(long long n, long long nnz, int shift, const unsigned long long *keys, long long *rowptr) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long target = (unsigned long long)i << shift;
+        long long lo = 0, hi = nnz;
+        while (lo < hi) {
+            long long mid = (lo + hi) >> 1;
+            if (keys[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        rowptr[i] = lo;
+    }
+}
+
+// merge items per row for the tile plan: 1 + len for rows handled in tiles, 1 for long rows
+__global__ void k_eff(long long n, const long long *rowptr, long long *eff, unsigned char *is_long) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
+        if (i == n) { eff[i] = 0; continue; }
+        long long len = rowptr[i + 1] - rowptr[i];
+        bool lg = len > SP_LONG;
+        is_long[i] = lg ? 1 : 0;
+        eff[i] = lg ? 1 : 1 + len;
+    }
+}
+
+// s[k] = smallest i in [0, n] with mc[i] >= k * D
+__global__ void k_tile_bounds(long long n, long long K, const long long *mc, int *s) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k <= K; k += (long long)gridDim.x * blockDim.x) {
+        long long target = k * (long long)SP_TILE;
+        long long lo = 0, hi = n;   // answer in [0, n]
+        while (lo < hi) {
+            long long mid = (lo + hi) >> 1;
+            if (mc[mid] >= target) hi = mid; else lo = mid + 1;
+        }
+        s[k] = (int)lo;
+    }
+}
+
+__global__ void k_gather_rowptr(long long L, const int *rows, const long long *rowptr, long long *out) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L; j += (long long)gridDim.x * blockDim.x) {
+        out[2 * j] = rowptr[rows[j]];
+        out[2 * j + 1] = rowptr[rows[j] + 1];
+    }
+}
+
+__global__ void k_rebase(long long n, const long long *rp, long long base, long long *out) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        out[i] = rp[i] - base;
+}
+
+template <class T>
+__global__ void k_fill(T *d, long long n, T v) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = v;
+}
+
+int grid_for(long long n, int sms) {
+    long long g = (n + 255) / 256;
+    long long cap = (long long)sms * 8;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+int bits_for(int64_t n) {
+    int b = 1;
+    while ((1ll << b) < n) b++;
+    return b;
+}
+
+}  // namespace
+
+void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst) {
+    long long n = 1ll << g.scale;
+    long long m = (long long)g.edge_factor * n;
+    cudaEvent_t ev0;
+    timing_begin(c, "graph", &ev0);
+    if (g.kind == NBG_GRAPH_RMAT)
+        k_gen_rmat<<<grid_for(m, c.num_sms), 256, 0, c.stream>>>(g.scale, m, g.seed, d_src, d_dst);
+    else
+        k_gen_er<<<grid_for(m, c.num_sms), 256, 0, c.stream>>>(g.scale, m, g.seed, d_src, d_dst);
+    NBG_CUDA(cudaGetLastError());
+    timing_end(c, "graph", ev0);
+    c.stats.kernels_launched++;
+}
+
+MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out) {
+    cudaEvent_t ev0;
+    timing_begin(c, "graph", &ev0);
+    const int shift = bits_for(std::max<int64_t>(n, 2));
+    if (2 * shift > 64) fail(NBG_INVALID_VALUE, "graph too large for 64-bit keys");
+    BufP keys = alloc_buf(c, (size_t)std::max<int64_t>(m, 1) * 8);
+    BufP keys2 = alloc_buf(c, (size_t)std::max<int64_t>(m, 1) * 8);
+    BufP bad = alloc_buf(c, 4);
+    NBG_CUDA(cudaMemsetAsync(bad->d, 0, 4, c.stream));
+    if (m > 0)
+        k_make_keys<<<grid_for(m, c.num_sms), 256, 0, c.stream>>>(m, n, shift, d_src, d_dst, (unsigned long long *)keys->d,
+                                                                  (int *)bad->d);
+    NBG_CUDA(cudaGetLastError());
+    int hbad = 0;
+    NBG_CUDA(cudaMemcpyAsync(&hbad, bad->d, 4, cudaMemcpyDeviceToHost, c.stream));
+    // sort by (dst, src)
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, (unsigned long long *)keys->d, (unsigned long long *)keys2->d,
+                                   (int64_t)m, 0, 2 * shift, c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tmp_bytes, 16));
+    if (m > 0)
+        NBG_CUDA(cub::DeviceRadixSort::SortKeys(tmp->d, tmp_bytes, (unsigned long long *)keys->d,
+                                                (unsigned long long *)keys2->d, (int64_t)m, 0, 2 * shift, c.stream));
+    // unique + no self loops
+    BufP flags = alloc_buf(c, (size_t)std::max<int64_t>(m, 1));
+    if (m > 0)
+        k_flags<<<grid_for(m, c.num_sms), 256, 0, c.stream>>>(m, shift, (const unsigned long long *)keys2->d,
+                                                              (unsigned char *)flags->d);
+    BufP nsel = alloc_buf(c, 8);
+    NBG_CUDA(cudaMemsetAsync(nsel->d, 0, 8, c.stream));
+    size_t tb2 = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb2, (unsigned long long *)keys2->d, (unsigned char *)flags->d,
+                               (unsigned long long *)keys->d, (long long *)nsel->d, (int64_t)m, c.stream);
+    if (tb2 > tmp->bytes) tmp = alloc_buf(c, tb2);
+    if (m > 0)
+        NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb2, (unsigned long long *)keys2->d, (unsigned char *)flags->d,
+                                            (unsigned long long *)keys->d, (long long *)nsel->d, (int64_t)m, c.stream));
+    long long nnz = 0;
+    NBG_CUDA(cudaMemcpyAsync(&nnz, nsel->d, 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    if (hbad) fail(NBG_INDEX_OUT_OF_BOUNDS, "edge endpoint outside [0, n)");
+
+    auto A = std::make_shared<Mat>();
+    A->ctx = &c;
+    A->id = c.new_id();
+    A->nrows = A->ncols = n;
+    A->nnz = nnz;
+    A->type = NBG_FP32;
+    A->iso = 1.0;
+    A->rowptr = alloc_buf(c, (size_t)(n + 1) * 8);
+    A->colidx = alloc_buf(c, (size_t)std::max<long long>(nnz, 1) * 4);
+    BufP deg = alloc_buf(c, (size_t)std::max<int64_t>(n, 1) * 4);
+    NBG_CUDA(cudaMemsetAsync(deg->d, 0, (size_t)std::max<int64_t>(n, 1) * 4, c.stream));
+    if (nnz > 0)
+        k_colidx_deg<<<grid_for(nnz, c.num_sms), 256, 0, c.stream>>>(nnz, shift, (const unsigned long long *)keys->d,
+                                                                     (int *)A->colidx->d, (int *)deg->d);
+    k_rowptr<<<grid_for(n + 1, c.num_sms), 256, 0, c.stream>>>(n, nnz, shift, (const unsigned long long *)keys->d,
+                                                              (long long *)A->rowptr->d);
+    NBG_CUDA(cudaGetLastError());
+    timing_end(c, "graph", ev0);
+    c.stats.kernels_launched += 6;
+    if (deg_out) *deg_out = deg;
+    return A;
+}
+
+void gpu_build_spmv_plan(Ctx &c, Mat &A) {
+    auto P = std::make_unique<SpmvPlan>();
+    const long long n = A.nrows;
+    if (n == 0) {
+        A.plan = std::move(P);
+        return;
+    }
+    BufP eff = alloc_buf(c, (size_t)(n + 1) * 8);
+    BufP mc = alloc_buf(c, (size_t)(n + 1) * 8);
+    BufP isl = alloc_buf(c, (size_t)n);
+    k_eff<<<grid_for(n + 1, c.num_sms), 256, 0, c.stream>>>(n, (const long long *)A.rowptr->d, (long long *)eff->d,
+                                                            (unsigned char *)isl->d);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)eff->d, (long long *)mc->d, (int64_t)(n + 1), c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)eff->d, (long long *)mc->d, (int64_t)(n + 1), c.stream));
+    long long total = 0;
+    NBG_CUDA(cudaMemcpyAsync(&total, (long long *)mc->d + n, 8, cudaMemcpyDeviceToHost, c.stream));
+    // long rows
+    BufP lrows = alloc_buf(c, (size_t)n * 4);
+    BufP nl = alloc_buf(c, 8);
+    size_t tb2 = 0;
+    thrust::counting_iterator<int> cnt(0);
+    cub::DeviceSelect::Flagged(nullptr, tb2, cnt, (unsigned char *)isl->d, (int *)lrows->d, (long long *)nl->d, (int64_t)n,
+                               c.stream);
+    if (tb2 > tmp->bytes) tmp = alloc_buf(c, tb2);
+    NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb2, cnt, (unsigned char *)isl->d, (int *)lrows->d, (long long *)nl->d,
+                                        (int64_t)n, c.stream));
+    long long L = 0;
+    NBG_CUDA(cudaMemcpyAsync(&L, nl->d, 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    const long long K = (total + SP_TILE - 1) / SP_TILE;
+    BufP sb = alloc_buf(c, (size_t)(K + 1) * 4);
+    k_tile_bounds<<<grid_for(K + 1, c.num_sms), 256, 0, c.stream>>>(n, K, (const long long *)mc->d, (int *)sb->d);
+    std::vector<int> s(K + 1);
+    NBG_CUDA(cudaMemcpyAsync(s.data(), sb->d, (K + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
+    std::vector<int> lr(L);
+    std::vector<long long> lrp(2 * L);
+    if (L > 0) {
+        BufP g = alloc_buf(c, (size_t)L * 16);
+        k_gather_rowptr<<<grid_for(L, c.num_sms), 256, 0, c.stream>>>(L, (const int *)lrows->d, (const long long *)A.rowptr->d,
+                                                                      (long long *)g->d);
+        NBG_CUDA(cudaMemcpyAsync(lr.data(), lrows->d, L * 4, cudaMemcpyDeviceToHost, c.stream));
+        NBG_CUDA(cudaMemcpyAsync(lrp.data(), g->d, L * 16, cudaMemcpyDeviceToHost, c.stream));
+    }
+    NBG_CUDA(cudaGetLastError());
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+
+    // tile boundaries = merge-path cuts U {L, L+1 : L long}
+    std::vector<int> bnd(s.begin(), s.end());
+    bnd.push_back(0);
+    bnd.push_back((int)n);
+    for (int r : lr) {
+        bnd.push_back(r);
+        bnd.push_back(r + 1);
+    }
+    std::sort(bnd.begin(), bnd.end());
+    bnd.erase(std::unique(bnd.begin(), bnd.end()), bnd.end());
+    std::vector<int> tiles;
+    for (size_t j = 0; j + 1 < bnd.size(); j++) {
+        int a = bnd[j], b = bnd[j + 1];
+        if (b <= a) continue;
+        if (b == a + 1 && std::binary_search(lr.begin(), lr.end(), a)) continue;   // a long row
+        tiles.push_back(a);
+        tiles.push_back(b);
+    }
+    std::vector<int> chunks, longs;
+    long long nch_total = 0;
+    for (long long j = 0; j < L; j++) {
+        long long p0 = lrp[2 * j], p1 = lrp[2 * j + 1];
+        long long len = p1 - p0;
+        long long nch = (len + SP_CHUNK - 1) / SP_CHUNK;
+        longs.push_back(lr[j]);
+        longs.push_back((int)nch_total);
+        longs.push_back((int)nch);
+        longs.push_back(0);
+        for (long long q = 0; q < nch; q++) {
+            long long pb = p0 + q * SP_CHUNK;
+            long long cntq = std::min<long long>(SP_CHUNK, p1 - pb);
+            chunks.push_back((int)j);
+            chunks.push_back((int)(unsigned)(pb & 0xffffffffll));
+            chunks.push_back((int)(unsigned)((unsigned long long)pb >> 32));
+            chunks.push_back((int)cntq);
+        }
+        nch_total += nch;
+    }
+    P->ntiles = (int64_t)tiles.size() / 2;
+    P->nchunks = nch_total;
+    P->nlong = L;
+    if (!tiles.empty()) {
+        P->tiles = alloc_buf(c, tiles.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->tiles->d, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    }
+    if (!chunks.empty()) {
+        P->chunks = alloc_buf(c, chunks.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->chunks->d, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        P->longs = alloc_buf(c, longs.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->longs->d, longs.data(), longs.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        P->counters = alloc_buf(c, (size_t)L * 4);
+        NBG_CUDA(cudaMemsetAsync(P->counters->d, 0, (size_t)L * 4, c.stream));
+        P->partials = alloc_buf(c, (size_t)nch_total * 8);
+    }
+    NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
+    A.plan = std::move(P);
+}
+
+void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out) {
+    k_rebase<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, rp, base, out);
+    NBG_CUDA(cudaGetLastError());
+    c.stats.kernels_launched++;
+}
+
+void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v) {
+    int g = grid_for(n, c.num_sms);
+    switch (type) {
+        case NBG_BOOL: k_fill<unsigned char><<<g, 256, 0, c.stream>>>((unsigned char *)d, n, v != 0.0 ? 1 : 0); break;
+        case NBG_INT32: k_fill<int><<<g, 256, 0, c.stream>>>((int *)d, n, (int)v); break;
+        case NBG_INT64: k_fill<long long><<<g, 256, 0, c.stream>>>((long long *)d, n, (long long)v); break;
+        case NBG_FP32: k_fill<float><<<g, 256, 0, c.stream>>>((float *)d, n, (float)v); break;
+        case NBG_FP64: k_fill<double><<<g, 256, 0, c.stream>>>((double *)d, n, v); break;
+    }
+    NBG_CUDA(cudaGetLastError());
+    c.stats.kernels_launched++;
+}
+
+}  // namespace nbg

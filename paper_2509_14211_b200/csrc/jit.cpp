@@ -1,0 +1,117 @@
+// jit.cpp -- NVRTC compilation of generated regions and their launch.
+//
+// (1) signature, (2) cache lookup, (3) on a miss generate + compile + insert,
+// (4) execute.  Steps 1/2/4 live in planner.cpp; this file is step 3 and the launch of step 4.
+// Kernels are compiled for sm_100a only (--gpu-architecture=sm_100a), with --fmad=false so that
+// no multiply-add contraction changes a rounding point.  The compiled cubin is loaded with the
+// CUDA 12 library API (cudaLibraryLoadData / cudaLibraryGetKernel), so no driver-API link is
+// needed.  A persistent cubin cache keyed by a hash of the source (the paper's future-work
+// "persistent cache") is used when NBG_JIT_CACHE names a directory.
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <fstream>
+#include <sstream>
+
+#include "nbg_internal.hpp"
+
+namespace nbg {
+
+static std::string cache_dir() {
+    const char *e = getenv("NBG_JIT_CACHE");
+    if (!e || !*e) return "";
+    return e;
+}
+
+static bool read_file(const std::string &path, std::string &out) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) return false;
+    std::ostringstream ss;
+    ss << f.rdbuf();
+    out = ss.str();
+    return !out.empty();
+}
+
+static void write_file(const std::string &path, const std::string &data) {
+    std::string tmp = path + ".tmp" + std::to_string(getpid());
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        if (!f) return;
+        f.write(data.data(), (std::streamsize)data.size());
+    }
+    rename(tmp.c_str(), path.c_str());
+}
+
+static std::string nvrtc_compile(Ctx &c, const std::string &src, const std::string &kname) {
+    std::string dir = cache_dir();
+    char hbuf[40];
+    snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)hash_str(src + "|sm_100a|v1"));
+    std::string cpath = dir.empty() ? "" : dir + "/" + kname + "_" + hbuf + ".cubin";
+    std::string cubin;
+    if (!cpath.empty() && read_file(cpath, cubin)) return cubin;
+
+    double t0 = now_ns();
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), (kname + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
+        fail(NBG_PANIC, "nvrtcCreateProgram failed");
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--prec-div=true", "--prec-sqrt=true",
+                          "--ftz=false", "-std=c++17", "--generate-line-info", "-default-device"};
+    nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof opts / sizeof opts[0]), opts);
+    if (r != NVRTC_SUCCESS) {
+        size_t ls = 0;
+        nvrtcGetProgramLogSize(prog, &ls);
+        std::string log(ls, '\0');
+        nvrtcGetProgramLog(prog, &log[0]);
+        nvrtcDestroyProgram(&prog);
+        const char *dump = getenv("NBG_JIT_DUMP");
+        if (dump && *dump) write_file(std::string(dump) + "/" + kname + "_failed.cu", src);
+        fail(NBG_PANIC, std::string("NVRTC compile failed: ") + nvrtcGetErrorString(r) + "\n" + log.substr(0, 4000));
+    }
+    size_t cs = 0;
+    nvrtcGetCUBINSize(prog, &cs);
+    cubin.resize(cs);
+    nvrtcGetCUBIN(prog, &cubin[0]);
+    nvrtcDestroyProgram(&prog);
+    c.stats.jit_compiles++;
+    c.stats.jit_ms += (now_ns() - t0) * 1e-6;
+    if (!cpath.empty()) {
+        mkdir(dir.c_str(), 0755);
+        write_file(cpath, cubin);
+    }
+    return cubin;
+}
+
+KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv) {
+    const char *dump = getenv("NBG_JIT_DUMP");
+    if (dump && *dump) write_file(std::string(dump) + "/" + kname + ".cu", src);
+    std::string cubin = nvrtc_compile(c, src, kname);
+    auto k = std::make_shared<Kernel>();
+    k->name = kname;
+    NBG_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    NBG_CUDA(cudaLibraryGetKernel(&k->k, k->lib, kname.c_str()));
+    k->block = 256;
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k->k, k->block, 0);
+    if (e != cudaSuccess || per_sm <= 0) {
+        cudaGetLastError();
+        per_sm = spmv ? 4 : 8;
+    }
+    k->grid_cap = c.num_sms * per_sm;
+    return k;
+}
+
+void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls) {
+    long long g = work_items;
+    if (g > k.grid_cap) g = k.grid_cap;
+    if (g < 1) g = 1;
+    void *params[] = {(void *)&args};
+    cudaEvent_t ev0 = nullptr;
+    timing_begin(c, cls, &ev0);
+    NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, 0, c.stream));
+    timing_end(c, cls, ev0);
+    c.stats.kernels_launched++;
+}
+
+}  // namespace nbg

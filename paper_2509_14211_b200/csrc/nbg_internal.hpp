@@ -1,0 +1,344 @@
+// nbg_internal.hpp -- internal data structures of the nonblocking GraphBLAS runtime.
+//
+// Layer map:
+//   capi.cpp      C ABI: validation + DAG recording ("return once validated")
+//   planner.cpp   wait(): region collection, signature, plan cache, memo, speculation, launch
+//                 (PAPER.md:301-306 the four wait steps)
+//   codegen.cpp   region IR -> CUDA C++ source (multi-stage programming)
+//   jit.cpp       NVRTC -> cubin -> cudaLibrary, cached by signature
+//   graph.cu      generators, CSR(AT) build, SpMV tile plan (static sm_100a kernels)
+//   pagerank.cpp  Fig. 6 written on the C ABI
+//   dist.cpp      NCCL (dlopen'ed) allgather-v + exact scalar allreduce
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/nbg.h"
+
+namespace nbg {
+
+// ---------------------------------------------------------------- errors
+
+struct Error {
+    nbg_status st;
+    std::string msg;
+};
+
+[[noreturn]] void fail(nbg_status st, const std::string &msg);
+[[noreturn]] void cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define NBG_CUDA(x)                                                     \
+    do {                                                                \
+        cudaError_t e_ = (x);                                           \
+        if (e_ != cudaSuccess) ::nbg::cuda_fail(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+inline size_t type_size(int t) {
+    switch (t) {
+        case NBG_BOOL: return 1;
+        case NBG_INT32: return 4;
+        case NBG_INT64: return 8;
+        case NBG_FP32: return 4;
+        case NBG_FP64: return 8;
+    }
+    return 0;
+}
+inline bool is_float(int t) { return t == NBG_FP32 || t == NBG_FP64; }
+inline bool valid_type(int t) { return t >= NBG_BOOL && t <= NBG_FP64; }
+
+struct Ctx;
+
+// ---------------------------------------------------------------- device buffers
+
+// A device allocation.  Owned buffers are released with cudaFreeAsync on the context stream
+// (stream-ordered, so kernels already queued that read it stay valid).
+struct Buf {
+    Ctx *ctx = nullptr;
+    uint64_t id = 0;           // never reused: memo keys and hints refer to buffers by id
+    void *d = nullptr;
+    size_t bytes = 0;
+    bool owned = true;
+    uint64_t prod_sig = 0;     // signature hash of the region that wrote it (0 = none)
+    int prod_out = -1;         // output index within that region
+    ~Buf();
+};
+using BufP = std::shared_ptr<Buf>;
+
+// ---------------------------------------------------------------- device scalar slots
+// Every reduction result lives in a 128-byte slot of a zero-initialised slab; each slot has a
+// pinned host mirror for asynchronous read-back.
+//   u64[0..9]  signed 32-bit-piece limbs of the exact fixed-point accumulator (LSB = 2^-160)
+//   u64[10]    flags: bit0 NaN, bit1 +inf, bit2 -inf, bit3 out of exact range
+//   u64[11]    int64 sum (integer PLUS) or order-preserving key (MIN/MAX; 0 = no value)
+constexpr int SLOT_U64 = 16;
+constexpr int SLAB_SLOTS = 4096;
+
+struct Slab {
+    Ctx *ctx = nullptr;
+    unsigned long long *d = nullptr;   // device, SLAB_SLOTS * SLOT_U64
+    unsigned long long *h = nullptr;   // pinned host mirror
+    int used = 0;
+    ~Slab();
+};
+using SlabP = std::shared_ptr<Slab>;
+
+enum class SFmt : uint8_t { HOST = 0, XACC = 1, I64 = 2, FMAX = 3, FMIN = 4, IMAX = 5, IMIN = 6 };
+
+struct Slot {
+    SlabP slab;
+    int idx = 0;
+    uint64_t id = 0;
+    cudaEvent_t ev = nullptr;          // recorded after the D2H copy of the mirror
+    bool rb_issued = false;
+    unsigned long long *dptr() const { return slab->d + (size_t)idx * SLOT_U64; }
+    unsigned long long *hptr() const { return slab->h + (size_t)idx * SLOT_U64; }
+    ~Slot();
+};
+using SlotP = std::shared_ptr<Slot>;
+
+// decode helpers (host side; device side lives in jit/prelude.cuh)
+double xacc_to_double(const unsigned long long *limbs);
+double slot_value(const unsigned long long *s, SFmt fmt);
+
+// ---------------------------------------------------------------- matrices
+
+struct SpmvPlan {
+    // Tiles: contiguous row ranges of "short/medium" rows, balanced by merge items (rows+nnz).
+    // Long rows (len > LONG) are cut into chunks of CHUNK nonzeros processed by their own CTAs;
+    // the CTA that finishes a long row's last chunk (atomic ticket) combines the chunk partials
+    // in chunk order and runs the epilogue.  DESIGN.md "K4 SpMV".
+    int64_t ntiles = 0, nchunks = 0, nlong = 0;
+    BufP tiles;      // int2  {row_begin, row_end}
+    BufP chunks;     // int4  {long_idx, first_p_lo, first_p_hi, count}   (p = 64-bit begin)
+    BufP longs;      // int4  {row, first_chunk, nchunks, 0}
+    BufP counters;   // int[nlong], zero between launches
+    BufP partials;   // double[nchunks]
+    int max_tile_vals = 0;   // max nonzeros in one tile (shared-memory bound)
+    int max_tile_rows = 0;
+};
+
+struct Mat {
+    Ctx *ctx = nullptr;
+    uint64_t id = 0;
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int type = NBG_FP32;     // value type (iso or vals)
+    double iso = 1.0;
+    BufP rowptr, colidx, vals;   // vals null => iso
+    std::unique_ptr<SpmvPlan> plan;
+    int64_t max_row = -1;
+};
+using MatP = std::shared_ptr<Mat>;
+
+// ---------------------------------------------------------------- DAG nodes
+
+enum class Op : uint8_t { LEAF = 0, APPLY, BIND2ND, EMULT, EADD, MXV, REDUCE, SAPPLY };
+enum class VKind : uint8_t { EMPTY = 0, ISO = 1, FULL = 2 };
+
+struct Node;
+using NodeP = std::shared_ptr<Node>;
+
+struct Node {
+    Op op = Op::LEAF;
+    bool scalar = false;
+    int type = NBG_FP32;
+    int64_t n = 0;               // vector length (vectors)
+    int code = 0;                // unop / binop code, or monoid for REDUCE
+    double c0 = 0.0, c1 = 0.0;   // operator constants
+    int add = 0, mul = 0;        // MXV semiring
+    NodeP a, b;                  // operands (b: second vector, or bound scalar)
+    MatP A;                      // MXV matrix
+    uint64_t uid = 0;
+    int user_refs = 0;           // live user handles (liveness rule)
+
+    // materialised state
+    bool mat = false;
+    VKind kind = VKind::FULL;    // kind is known at record time (EMPTY/ISO folded eagerly)
+    BufP buf;                    // FULL vector
+    double iso = 0.0;            // ISO vector value (already rounded to type)
+    // scalar state
+    SFmt sfmt = SFmt::HOST;
+    double hval = 0.0;           // HOST scalar value (already rounded to type)
+    SlotP slot;                  // device scalar
+    BufP full_cache;             // ISO vector expanded to a buffer (used as an mxv input)
+};
+
+// ---------------------------------------------------------------- region IR (codegen input)
+
+struct Ins {
+    enum K : uint8_t { LD_VEC = 0, LD_ISO, LD_SHOST, LD_SDEV, MXV_ACC, UN, BIN, CVT } k;
+    int t = NBG_FP32;       // output type
+    int code = 0;
+    int a = -1, b = -1;     // operand instruction indices
+    int imm0 = -1, imm1 = -1;
+    int slot = -1;          // LD_VEC input index / LD_ISO, LD_SHOST imm index / LD_SDEV sin index
+    uint8_t fmt = 0;        // LD_SDEV format
+    bool uniform = false;   // value independent of the element index
+};
+
+struct OutV { int ins; int out; };
+struct RedOut { int ins; int monoid; int racc; uint8_t fmt; };
+
+struct SpmvSig {
+    int add = NBG_PLUS, mul = NBG_SECOND;
+    int T = NBG_FP32;       // type of the mxv node (mul evaluated in T)
+    int xt = NBG_FP32;      // x buffer type
+    int at = NBG_FP32;      // matrix value type
+    bool has_vals = false;
+};
+
+struct Prog {
+    std::vector<Ins> ins;
+    std::vector<OutV> outs;
+    std::vector<RedOut> reds;
+    bool spmv = false;
+    bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
+    SpmvSig sp;
+    int n_in = 0, n_out = 0, n_imm = 0, n_sin = 0, n_red = 0;
+    std::string signature() const;
+};
+
+// Kernel arguments (one struct passed by value; mirrored in jit/prelude.cuh).
+constexpr int MAX_IN = 16, MAX_OUT = 8, MAX_IMM = 32, MAX_SIN = 8, MAX_RED = 8;
+struct KArgs {
+    long long n;
+    const void *in[MAX_IN];
+    void *out[MAX_OUT];
+    double imm[MAX_IMM];
+    const unsigned long long *sin[MAX_SIN];
+    unsigned long long *racc[MAX_RED];
+    // spmv
+    const long long *rowptr;
+    const int *colidx;
+    const void *aval;
+    const void *x;
+    const int *tiles;        // int2 pairs
+    const int *chunks;       // int4
+    const int *longs;        // int4
+    int *counters;
+    double *partials;
+    long long ntiles, nchunks;
+    long long row_offset;    // global index of local row 0 (distributed); 0 otherwise
+};
+
+struct Kernel {
+    ~Kernel();
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t k = nullptr;
+    int block = 256;
+    int grid_cap = 0;        // persistent grid size (SMs * resident CTAs)
+    std::string name;
+};
+using KernelP = std::shared_ptr<Kernel>;
+
+struct Hint {           // speculative loop-carried side output (planner rule 3)
+    NodeP tmpl;         // pending template expression
+    Node *placeholder;  // leaf inside tmpl standing for the region output
+    NodeP ph_keep;
+};
+
+struct TimingClass {
+    double ms = 0.0;
+    int64_t launches = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+};
+
+// ---------------------------------------------------------------- context
+
+struct Dist {
+    int rank = 0, nranks = 1;
+    void *comm = nullptr;   // ncclComm_t
+    ~Dist();
+};
+
+struct Ctx {
+    int mode = NBG_NONBLOCKING;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int num_sms = 148;
+    uint64_t next_id = 1;
+    std::string last_error;
+    nbg_status latched = NBG_SUCCESS;
+    nbg_stats stats{};
+
+    // scalar slabs
+    SlabP cur_slab;
+    std::vector<cudaEvent_t> event_pool;
+
+    // plan cache: signature -> kernel ("GraphBLAS method signatures as keys")
+    std::unordered_map<std::string, KernelP> plans;
+    // memo: structural key over materialised leaves -> result (derived views)
+    struct MemoEntry {
+        std::vector<std::weak_ptr<Buf>> deps;
+        NodeP result;            // a materialised node
+    };
+    std::unordered_map<std::string, MemoEntry> memo;
+    // learned hints: producer signature hash + output index -> templates
+    std::map<std::pair<uint64_t, int>, std::vector<Hint>> hints;
+
+    // timing
+    bool timing = false;
+    std::map<std::string, TimingClass> tclass;
+
+    // distributed
+    std::unique_ptr<Dist> dist;
+
+    uint64_t new_id() { return next_id++; }
+    ~Ctx();
+};
+
+// ---------------------------------------------------------------- helpers shared by the runtime
+
+BufP alloc_buf(Ctx &c, size_t bytes);
+BufP borrow_buf(Ctx &c, void *d, size_t bytes);
+SlotP alloc_slot(Ctx &c);
+cudaEvent_t get_event(Ctx &c);
+void put_event(Ctx &c, cudaEvent_t e);
+void issue_readback(Ctx &c, Slot &s);
+
+void timing_begin(Ctx &c, const char *cls, cudaEvent_t *ev0);
+void timing_end(Ctx &c, const char *cls, cudaEvent_t ev0);
+void timing_collect(Ctx &c);
+
+// planner entry points
+void materialize(Ctx &c, const std::vector<NodeP> &roots);
+double scalar_read(Ctx &c, const NodeP &s);
+void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
+
+// codegen / jit
+std::string codegen(const Prog &p, const std::string &kname);
+KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv);
+void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);
+
+// graph (graph.cu)
+void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst);
+MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out);
+void gpu_build_spmv_plan(Ctx &c, Mat &A);
+void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
+void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out);
+void host_xacc_add(unsigned long long *limbs, double d);
+
+// host arithmetic (used for eager iso folding and host-side scalar ops)
+double host_unop(int code, int t, double x, double c0, double c1);
+double host_binop(int code, int t, double x, double y, double c0);
+double host_round(int t, double v);
+uint64_t hash_str(const std::string &s);
+
+double now_ns();
+
+}  // namespace nbg
+
+// opaque handle structs of the C ABI
+struct nbg_ctx_s : nbg::Ctx {};
+struct nbg_matrix_s { nbg_ctx *ctx; nbg::MatP m; };
+struct nbg_vector_s { nbg_ctx *ctx; nbg::NodeP node; };
+struct nbg_scalar_s { nbg_ctx *ctx; nbg::NodeP node; };

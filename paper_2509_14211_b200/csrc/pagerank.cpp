@@ -1,0 +1,268 @@
+// pagerank.cpp -- PAPER.md Fig. 6 (`pagerank_gap`, lines 266-294) written ONLY on the public C ABI,
+// which shows the ABI suffices for the paper's algorithm.
+//
+// Per sweep (t = previous ranks; all handles are immutable, so `t = r` aliases):
+//   mask  = apply(iszero, dinv)                       dangling vertices (dinv == 0 iff deg == 0)
+//   ds    = reduce(+, ewise_mult(*, t, mask))         dangling mass of t      [UNIFORM only]
+//   c     = (alpha/n) * ds + (1-alpha)/n               scalar node (Q1, Q3)     [DROP: c = (1-alpha)/n]
+//   y     = ewise_mult(*, t, dinv)                    Fig. 6 l.286 `t / d` (reading Q2)
+//   m     = mxv(+, second, AT, y)                     Fig. 6 l.287
+//   r     = apply_bind2nd(+, m, c)                    Fig. 6 l.288 `ewise_add(+, rt, r)` + dangling
+//   e     = ewise_add(|x-y|, t, r); delta = reduce(+, e)   Fig. 6 l.290-291
+//   wait(delta)   -- r is live (the driver holds it), so ONE fused kernel materialises r and delta
+//                    (Fig. 6 waits on r first; waiting on delta instead lets the planner fuse the
+//                    residual into the same pass -- the placement SPEC.md:474 leaves open).
+// Convergence (Fig. 6 l.284): sweep k+1 is recorded and launched BEFORE delta_k is read, so the
+// device never idles on the host's read-back; if delta_k <= tol the speculative sweep is dropped
+// (immutable handles keep r_k intact).  tol < 0 runs exactly itermax sweeps with no host sync.
+#include <cmath>
+#include <vector>
+
+#include "nbg_internal.hpp"
+
+#define TRY(x)                                   \
+    do {                                         \
+        nbg_status s_ = (x);                     \
+        if (s_ != NBG_SUCCESS) return s_;        \
+    } while (0)
+
+namespace {
+
+struct PR {
+    nbg_ctx *ctx;
+    nbg_matrix AT;
+    nbg_vector dinv;
+    int T;
+    bool uniform;
+    double a_n, tele;
+
+    // one sweep over t; returns the new ranks and the delta scalar (both launched)
+    nbg_status sweep(nbg_vector t, nbg_vector *r_new, nbg_scalar *delta) {
+        nbg_scalar c = nullptr;
+        if (uniform) {
+            nbg_vector mask, tm;
+            nbg_scalar ds;
+            TRY(nbg_apply(ctx, &mask, T, nbg_unop{NBG_ISZERO, 0, 0}, dinv));
+            TRY(nbg_ewise_mult(ctx, &tm, T, nbg_binop{NBG_TIMES, 0}, t, mask));
+            nbg_vector_free(ctx, mask);
+            TRY(nbg_reduce(ctx, &ds, NBG_FP64, NBG_PLUS, tm));
+            nbg_vector_free(ctx, tm);
+            TRY(nbg_scalar_apply(ctx, &c, NBG_FP64, nbg_unop{NBG_AXPB, a_n, tele}, ds));
+            nbg_scalar_free(ctx, ds);
+        } else {
+            TRY(nbg_scalar_new(ctx, &c, NBG_FP64, tele));
+        }
+        nbg_vector y, m, e;
+        TRY(nbg_ewise_mult(ctx, &y, T, nbg_binop{NBG_TIMES, 0}, t, dinv));
+        TRY(nbg_mxv(ctx, &m, T, nbg_semiring{NBG_PLUS, NBG_SECOND, 0.0}, AT, y));
+        nbg_vector_free(ctx, y);
+        TRY(nbg_apply_bind2nd(ctx, r_new, T, nbg_binop{NBG_PLUS, 0}, m, c));
+        nbg_vector_free(ctx, m);
+        nbg_scalar_free(ctx, c);
+        TRY(nbg_ewise_add(ctx, &e, T, nbg_binop{NBG_ABSDIFF, 0}, t, *r_new));
+        TRY(nbg_reduce(ctx, delta, NBG_FP64, NBG_PLUS, e));
+        nbg_vector_free(ctx, e);
+        TRY(nbg_scalar_wait(ctx, *delta));
+        return NBG_SUCCESS;
+    }
+};
+
+}  // namespace
+
+extern "C" nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, const nbg_pr_params *p, nbg_vector *r_out,
+                                   int *sweeps_out, double *delta_hist) {
+    if (!ctx || !AT || !deg || !p || !r_out) return NBG_NULL_POINTER;
+    if (!(p->alpha > 0.0 && p->alpha < 1.0) || p->itermax < 0) return NBG_INVALID_VALUE;
+    if (p->type != NBG_FP32 && p->type != NBG_FP64) return NBG_DOMAIN_MISMATCH;
+    if (p->dangling != NBG_PR_UNIFORM && p->dangling != NBG_PR_DROP) return NBG_INVALID_VALUE;
+    int64_t n = 0, nc = 0, nd = 0;
+    TRY(nbg_matrix_nrows(ctx, AT, &n));
+    TRY(nbg_matrix_ncols(ctx, AT, &nc));
+    TRY(nbg_vector_size(ctx, deg, &nd));
+    if (n != nc || nd != n) return NBG_DIMENSION_MISMATCH;
+    if (n == 0) return NBG_INVALID_VALUE;
+
+    PR pr;
+    pr.ctx = ctx;
+    pr.AT = AT;
+    pr.T = p->type;
+    pr.uniform = p->dangling == NBG_PR_UNIFORM;
+    pr.a_n = p->alpha / (double)n;
+    pr.tele = (1.0 - p->alpha) / (double)n;
+
+    // Fig. 6 l.278-281: d, then wait(d).  Reading Q2: dinv = (T)(alpha / deg) in double, 0 if deg == 0.
+    nbg_vector d64;
+    TRY(nbg_apply(ctx, &d64, NBG_FP64, nbg_unop{NBG_RECIP_SCALED, p->alpha, 0.0}, deg));
+    TRY(nbg_convert(ctx, &pr.dinv, pr.T, d64));
+    nbg_vector_free(ctx, d64);
+    TRY(nbg_vector_wait(ctx, pr.dinv));
+
+    nbg_vector t;   // Fig. 6 l.277: r = GrBVector(n, 1/n)
+    TRY(nbg_vector_new_const(ctx, &t, pr.T, n, 1.0 / (double)n));
+    if (p->itermax == 0) {
+        *r_out = t;
+        if (sweeps_out) *sweeps_out = 0;
+        nbg_vector_free(ctx, pr.dinv);
+        return NBG_SUCCESS;
+    }
+    const bool conv = p->tol >= 0.0;
+    nbg_vector rk;
+    nbg_scalar dk;
+    TRY(pr.sweep(t, &rk, &dk));
+    std::vector<nbg_scalar> deltas;   // fixed-count mode: read after the loop
+    int k = 1;
+    for (;;) {
+        nbg_vector rnext = nullptr;
+        nbg_scalar dnext = nullptr;
+        const bool more = k < p->itermax;
+        if (more) TRY(pr.sweep(rk, &rnext, &dnext));   // launched before delta_k is read
+        bool stop = !more;
+        if (conv) {
+            double v = 0.0;
+            TRY(nbg_scalar_get(ctx, dk, &v));
+            if (delta_hist) delta_hist[k - 1] = v;
+            nbg_scalar_free(ctx, dk);
+            dk = nullptr;
+            if (!(v > p->tol)) stop = true;
+        } else {
+            deltas.push_back(dk);
+            dk = nullptr;
+        }
+        if (stop) {
+            if (rnext) nbg_vector_free(ctx, rnext);
+            if (dnext) nbg_scalar_free(ctx, dnext);
+            break;
+        }
+        nbg_vector_free(ctx, t);
+        t = rk;
+        rk = rnext;
+        dk = dnext;
+        k++;
+    }
+    for (size_t j = 0; j < deltas.size(); j++) {
+        double v = 0.0;
+        TRY(nbg_scalar_get(ctx, deltas[j], &v));
+        if (delta_hist) delta_hist[j] = v;
+        nbg_scalar_free(ctx, deltas[j]);
+    }
+    if (dk) nbg_scalar_free(ctx, dk);
+    nbg_vector_free(ctx, t);
+    nbg_vector_free(ctx, pr.dinv);
+    *r_out = rk;
+    if (sweeps_out) *sweeps_out = k;
+    return NBG_SUCCESS;
+}
+
+// ---------------------------------------------------------------- distributed
+// Same sweep on this rank's row block; the gathered vector is exchanged with
+// nbg_vector_allgather and the two scalars (dangling mass, delta) with nbg_scalar_allreduce.
+extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg, const int64_t *cuts,
+                                        const nbg_pr_params *p, nbg_vector *r_out, int *sweeps_out, double *delta_hist) {
+    if (!ctx || !AT_blk || !deg || !cuts || !p || !r_out) return NBG_NULL_POINTER;
+    if (!ctx->dist) return NBG_INVALID_VALUE;
+    if (!(p->alpha > 0.0 && p->alpha < 1.0) || p->itermax < 1) return NBG_INVALID_VALUE;
+    if (p->type != NBG_FP32 && p->type != NBG_FP64) return NBG_DOMAIN_MISMATCH;
+    const int rank = ctx->dist->rank, P = ctx->dist->nranks;
+    const int64_t n = cuts[P], lo = cuts[rank], nb = cuts[rank + 1] - cuts[rank];
+    int64_t rows = 0, cols = 0, nd = 0;
+    TRY(nbg_matrix_nrows(ctx, AT_blk, &rows));
+    TRY(nbg_matrix_ncols(ctx, AT_blk, &cols));
+    TRY(nbg_vector_size(ctx, deg, &nd));
+    if (rows != nb || cols != n || nd != n) return NBG_DIMENSION_MISMATCH;
+    const int T = p->type;
+    const bool uniform = p->dangling == NBG_PR_UNIFORM;
+    const double a_n = p->alpha / (double)n, tele = (1.0 - p->alpha) / (double)n;
+
+    nbg_vector d64, dinv, dinv_blk;
+    TRY(nbg_apply(ctx, &d64, NBG_FP64, nbg_unop{NBG_RECIP_SCALED, p->alpha, 0.0}, deg));
+    TRY(nbg_convert(ctx, &dinv, T, d64));
+    nbg_vector_free(ctx, d64);
+    void *dptr = nullptr;
+    TRY(nbg_vector_device_ptr(ctx, dinv, &dptr));
+    TRY(nbg_vector_from_dense(ctx, &dinv_blk, T, nb, (char *)dptr + lo * (T == NBG_FP32 ? 4 : 8), NBG_DEVICE, NBG_BORROW));
+
+    auto sweep = [&](nbg_vector t, nbg_vector *r_new, nbg_scalar *delta) -> nbg_status {
+        nbg_scalar c = nullptr;
+        if (uniform) {
+            nbg_vector mask, tm;
+            nbg_scalar ds_loc, ds;
+            TRY(nbg_apply(ctx, &mask, T, nbg_unop{NBG_ISZERO, 0, 0}, dinv_blk));
+            TRY(nbg_ewise_mult(ctx, &tm, T, nbg_binop{NBG_TIMES, 0}, t, mask));
+            nbg_vector_free(ctx, mask);
+            TRY(nbg_reduce(ctx, &ds_loc, NBG_FP64, NBG_PLUS, tm));
+            nbg_vector_free(ctx, tm);
+            TRY(nbg_scalar_allreduce(ctx, &ds, ds_loc));
+            nbg_scalar_free(ctx, ds_loc);
+            TRY(nbg_scalar_apply(ctx, &c, NBG_FP64, nbg_unop{NBG_AXPB, a_n, tele}, ds));
+            nbg_scalar_free(ctx, ds);
+        } else {
+            TRY(nbg_scalar_new(ctx, &c, NBG_FP64, tele));
+        }
+        nbg_vector y_blk, Y, m, e;
+        nbg_scalar d_loc;
+        TRY(nbg_ewise_mult(ctx, &y_blk, T, nbg_binop{NBG_TIMES, 0}, t, dinv_blk));
+        TRY(nbg_vector_allgather(ctx, &Y, y_blk, cuts));
+        nbg_vector_free(ctx, y_blk);
+        TRY(nbg_mxv(ctx, &m, T, nbg_semiring{NBG_PLUS, NBG_SECOND, 0.0}, AT_blk, Y));
+        nbg_vector_free(ctx, Y);
+        TRY(nbg_apply_bind2nd(ctx, r_new, T, nbg_binop{NBG_PLUS, 0}, m, c));
+        nbg_vector_free(ctx, m);
+        nbg_scalar_free(ctx, c);
+        TRY(nbg_ewise_add(ctx, &e, T, nbg_binop{NBG_ABSDIFF, 0}, t, *r_new));
+        TRY(nbg_reduce(ctx, &d_loc, NBG_FP64, NBG_PLUS, e));
+        nbg_vector_free(ctx, e);
+        TRY(nbg_scalar_wait(ctx, d_loc));
+        TRY(nbg_scalar_allreduce(ctx, delta, d_loc));
+        nbg_scalar_free(ctx, d_loc);
+        return NBG_SUCCESS;
+    };
+
+    nbg_vector t;
+    TRY(nbg_vector_new_const(ctx, &t, T, nb, 1.0 / (double)n));
+    const bool conv = p->tol >= 0.0;
+    nbg_vector rk;
+    nbg_scalar dk;
+    TRY(sweep(t, &rk, &dk));
+    std::vector<nbg_scalar> deltas;
+    int k = 1;
+    for (;;) {
+        nbg_vector rnext = nullptr;
+        nbg_scalar dnext = nullptr;
+        const bool more = k < p->itermax;
+        if (more) TRY(sweep(rk, &rnext, &dnext));
+        bool stop = !more;
+        if (conv) {
+            double v = 0.0;
+            TRY(nbg_scalar_get(ctx, dk, &v));
+            if (delta_hist) delta_hist[k - 1] = v;
+            nbg_scalar_free(ctx, dk);
+            dk = nullptr;
+            if (!(v > p->tol)) stop = true;   // identical on every rank: the allreduce is exact
+        } else {
+            deltas.push_back(dk);
+            dk = nullptr;
+        }
+        if (stop) {
+            if (rnext) nbg_vector_free(ctx, rnext);
+            if (dnext) nbg_scalar_free(ctx, dnext);
+            break;
+        }
+        nbg_vector_free(ctx, t);
+        t = rk;
+        rk = rnext;
+        dk = dnext;
+        k++;
+    }
+    for (size_t j = 0; j < deltas.size(); j++) {
+        double v = 0.0;
+        TRY(nbg_scalar_get(ctx, deltas[j], &v));
+        if (delta_hist) delta_hist[j] = v;
+        nbg_scalar_free(ctx, deltas[j]);
+    }
+    nbg_vector_free(ctx, t);
+    nbg_vector_free(ctx, dinv_blk);
+    nbg_vector_free(ctx, dinv);
+    *r_out = rk;
+    if (sweeps_out) *sweeps_out = k;
+    return NBG_SUCCESS;
+}

@@ -1,0 +1,604 @@
+// planner.cpp -- materialisation at wait.
+//
+// wait(roots):
+//   1. Region: walk the pending DAG from the roots down to materialised leaves.  Every pending
+//      elementwise node (apply / ewise_mult / ewise_add / apply_bind2nd / convert) joins the
+//      region; at most ONE mxv joins it and then the whole region runs in that mxv's epilogue
+//      (per output row).  Fusion barriers: an mxv's vector input must be
+//      materialised (it is gathered), a reduction feeding a scalar operand must be materialised
+//      (every block needs its value), a second mxv is materialised separately.  Those become
+//      prerequisites, materialised first (recursively, jointly when independent).
+//   2. Memo: before computing a prerequisite, look it up by its structural key over the
+//      identities of its materialised leaves (immutable buffers) -- a derived view computed
+//      earlier is bound instead of recomputed.
+//   3. Speculation (loop-carried elision): when a prerequisite depends on exactly one buffer that
+//      an earlier region wrote, remember "region S's output o tends to be consumed through
+//      expression E"; the next time a region with signature S runs, E(output o) is emitted as an
+//      extra output of that same kernel and memoised.  For PageRank this turns y = t/d and the
+//      dangling sum of t into side outputs of the previous sweep.
+//   4. Signature of the region program -> plan cache -> (NVRTC on a miss) -> bind -> launch.
+//   Liveness ("elide unneeded objects"): besides the requested roots, only pending
+//   nodes a user still holds a handle to are stored; every other intermediate lives in registers.
+#include <algorithm>
+#include <cstdio>
+#include <functional>
+#include <unordered_set>
+
+#include "nbg_internal.hpp"
+
+namespace nbg {
+
+static std::string dbits(double v) {
+    uint64_t b;
+    memcpy(&b, &v, 8);
+    char s[24];
+    snprintf(s, sizeof s, "%llx", (unsigned long long)b);
+    return s;
+}
+
+// ---------------------------------------------------------------- structural keys
+
+static void key_rec(const Node *x, std::string &s, const Node *ph) {
+    if (x == ph) { s += "P"; return; }
+    if (x->mat) {
+        if (x->scalar) {
+            if (x->sfmt == SFmt::HOST) s += "h" + std::to_string(x->type) + ":" + dbits(x->hval);
+            else s += "d" + std::to_string(x->type) + ":" + std::to_string(x->slot->id);
+        } else if (x->kind == VKind::FULL) s += "F" + std::to_string(x->buf->id);
+        else if (x->kind == VKind::ISO) s += "I" + std::to_string(x->type) + ":" + dbits(x->iso);
+        else s += "E";
+        return;
+    }
+    s += "(" + std::to_string((int)x->op) + "," + std::to_string(x->type) + "," + std::to_string(x->n) + "," +
+         std::to_string(x->code) + "," + dbits(x->c0) + "," + dbits(x->c1) + "," + std::to_string(x->add) + "," +
+         std::to_string(x->mul) + "," + (x->A ? std::to_string(x->A->id) : "-") + ";";
+    if (x->a) key_rec(x->a.get(), s, ph);
+    s += ";";
+    if (x->b) key_rec(x->b.get(), s, ph);
+    s += ")";
+}
+
+static std::string node_key(const Node *x, const Node *ph = nullptr) {
+    std::string s;
+    key_rec(x, s, ph);
+    return s;
+}
+
+static void leaf_bufs(const Node *x, std::vector<std::weak_ptr<Buf>> &deps, std::unordered_set<const Node *> &seen) {
+    if (!seen.insert(x).second) return;
+    if (x->mat) {
+        if (!x->scalar && x->kind == VKind::FULL && x->buf) deps.push_back(x->buf);
+        return;
+    }
+    if (x->a) leaf_bufs(x->a.get(), deps, seen);
+    if (x->b) leaf_bufs(x->b.get(), deps, seen);
+}
+
+static void memo_purge(Ctx &c) {
+    for (auto it = c.memo.begin(); it != c.memo.end();) {
+        bool dead = false;
+        for (auto &w : it->second.deps)
+            if (w.expired()) { dead = true; break; }
+        if (dead) it = c.memo.erase(it);
+        else ++it;
+    }
+}
+
+static void drop_inputs(Node &x) {
+    x.a.reset();
+    x.b.reset();
+    x.A.reset();
+}
+
+static void copy_result(Node &dst, const Node &src) {
+    dst.mat = true;
+    dst.kind = src.kind;
+    dst.buf = src.buf;
+    dst.iso = src.iso;
+    dst.sfmt = src.sfmt;
+    dst.hval = src.hval;
+    dst.slot = src.slot;
+    drop_inputs(dst);
+}
+
+static bool memo_bind(Ctx &c, const NodeP &x) {
+    if (x->mat) return true;
+    auto it = c.memo.find(node_key(x.get()));
+    if (it == c.memo.end()) return false;
+    for (auto &w : it->second.deps)
+        if (w.expired()) return false;
+    copy_result(*x, *it->second.result);
+    c.stats.memo_hits++;
+    return true;
+}
+
+// ---------------------------------------------------------------- cloning (hint templates)
+
+static NodeP clone_subst(Ctx &c, const NodeP &x, const Node *from, const NodeP &to,
+                         std::unordered_map<const Node *, NodeP> &seen) {
+    if (x.get() == from) return to;
+    if (x->mat) return x;
+    auto it = seen.find(x.get());
+    if (it != seen.end()) return it->second;
+    auto y = std::make_shared<Node>(*x);
+    y->uid = c.new_id();
+    y->user_refs = 0;
+    if (x->a) y->a = clone_subst(c, x->a, from, to, seen);
+    if (x->b) y->b = clone_subst(c, x->b, from, to, seen);
+    seen[x.get()] = y;
+    return y;
+}
+
+// a template can be instantiated inside another region only if it needs no prerequisite
+static bool fusable_template(const Node *x, bool root) {
+    if (x->mat) return true;
+    if (x->op == Op::MXV) return false;
+    if (x->op == Op::REDUCE && !root) return false;
+    if (x->a && !fusable_template(x->a.get(), false)) return false;
+    if (x->b && !fusable_template(x->b.get(), false)) return false;
+    return true;
+}
+
+static void find_produced_leaves(const Node *x, std::vector<const Node *> &out, std::unordered_set<const Node *> &seen) {
+    if (!seen.insert(x).second) return;
+    if (x->mat) {
+        if (!x->scalar && x->kind == VKind::FULL && x->buf && x->buf->prod_sig) out.push_back(x);
+        return;
+    }
+    if (x->a) find_produced_leaves(x->a.get(), out, seen);
+    if (x->b) find_produced_leaves(x->b.get(), out, seen);
+}
+
+static void learn_hint(Ctx &c, const NodeP &p) {
+    if (!fusable_template(p.get(), true)) return;
+    std::vector<const Node *> prod;
+    std::unordered_set<const Node *> seen;
+    find_produced_leaves(p.get(), prod, seen);
+    if (prod.size() != 1) return;
+    const Node *L = prod[0];
+    auto key = std::make_pair(L->buf->prod_sig, L->buf->prod_out);
+    auto ph = std::make_shared<Node>();
+    ph->op = Op::LEAF;
+    ph->mat = true;
+    ph->kind = VKind::FULL;
+    ph->type = L->type;
+    ph->n = L->n;
+    ph->uid = c.new_id();
+    std::unordered_map<const Node *, NodeP> cs;
+    NodeP t = clone_subst(c, p, L, ph, cs);
+    std::string k = node_key(t.get(), ph.get());
+    auto &vec = c.hints[key];
+    for (auto &h : vec)
+        if (node_key(h.tmpl.get(), h.placeholder) == k) return;
+    if (vec.size() >= 4) return;
+    vec.push_back(Hint{t, ph.get(), ph});
+}
+
+// ---------------------------------------------------------------- region builder
+
+struct Builder {
+    Ctx &c;
+    Prog prog;
+    std::unordered_map<const Node *, int> ins_of;
+    std::unordered_map<const Node *, int> in_slot_of;
+    std::vector<NodeP> in_nodes;
+    std::vector<double> imm;
+    std::vector<SlotP> sin;
+    std::unordered_map<const Slot *, int> sin_of;
+    std::vector<NodeP> prereq;
+    std::unordered_set<const Node *> prereq_set;
+    NodeP mxv;
+    std::vector<NodeP> visited;        // pending nodes of the region
+    std::vector<NodeP> out_nodes;      // vector outputs, index = out slot
+    std::vector<NodeP> red_nodes;      // reductions, index = racc slot
+    std::unordered_set<const Node *> is_out;
+
+    explicit Builder(Ctx &cc) : c(cc) {
+        imm.push_back(0.0);   // imm[0]: iso value of the matrix (spmv)
+        imm.push_back(0.0);   // imm[1]: constant of the semiring mul (spmv)
+    }
+
+    int add(const Ins &in) {
+        prog.ins.push_back(in);
+        return (int)prog.ins.size() - 1;
+    }
+    int imm_slot(double v) {
+        imm.push_back(v);
+        return (int)imm.size() - 1;
+    }
+    void need(const NodeP &x) {
+        if (prereq_set.insert(x.get()).second) prereq.push_back(x);
+    }
+
+    static bool unop_has_c0(int code) {
+        return code == NBG_ADD_C || code == NBG_MUL_C || code == NBG_AXPB || code == NBG_ABS_SUB_C || code == NBG_RECIP_SCALED;
+    }
+
+    int emit(const NodeP &x) {
+        auto it = ins_of.find(x.get());
+        if (it != ins_of.end()) return it->second;
+        int r = -1;
+        if (x->mat) {
+            Ins in{};
+            in.t = x->type;
+            if (x->scalar) {
+                in.uniform = true;
+                if (x->sfmt == SFmt::HOST) {
+                    in.k = Ins::LD_SHOST;
+                    in.slot = imm_slot(x->hval);
+                } else {
+                    in.k = Ins::LD_SDEV;
+                    auto s = sin_of.find(x->slot.get());
+                    int si;
+                    if (s == sin_of.end()) {
+                        si = (int)sin.size();
+                        sin.push_back(x->slot);
+                        sin_of[x->slot.get()] = si;
+                    } else si = s->second;
+                    in.slot = si;
+                    in.fmt = (uint8_t)x->sfmt;
+                }
+            } else if (x->kind == VKind::ISO) {
+                in.k = Ins::LD_ISO;
+                in.uniform = true;
+                in.slot = imm_slot(x->iso);
+            } else if (x->kind == VKind::FULL) {
+                in.k = Ins::LD_VEC;
+                auto s = in_slot_of.find(x.get());
+                int si;
+                if (s == in_slot_of.end()) {
+                    si = (int)in_nodes.size();
+                    in_nodes.push_back(x);
+                    in_slot_of[x.get()] = si;
+                } else si = s->second;
+                in.slot = si;
+            } else {
+                fail(NBG_PANIC, "planner: empty vector inside a region");
+            }
+            r = add(in);
+        } else {
+            switch (x->op) {
+                case Op::APPLY:
+                case Op::SAPPLY: {
+                    int a = emit(x->a);
+                    if (a < 0) return -1;
+                    Ins in{};
+                    in.k = Ins::UN;
+                    in.t = x->type;
+                    in.code = x->code;
+                    in.a = a;
+                    if (unop_has_c0(x->code)) in.imm0 = imm_slot(x->c0);
+                    if (x->code == NBG_AXPB) in.imm1 = imm_slot(x->c1);
+                    in.uniform = prog.ins[a].uniform;
+                    r = add(in);
+                    break;
+                }
+                case Op::BIND2ND:
+                case Op::EMULT:
+                case Op::EADD: {
+                    int a = emit(x->a);
+                    int b = emit(x->b);
+                    if (a < 0 || b < 0) return -1;
+                    Ins in{};
+                    in.k = Ins::BIN;
+                    in.t = x->type;
+                    in.code = x->code;
+                    in.a = a;
+                    in.b = b;
+                    if (x->code == NBG_MAX_DIVX_C) in.imm0 = imm_slot(x->c0);
+                    in.uniform = prog.ins[a].uniform && prog.ins[b].uniform;
+                    r = add(in);
+                    break;
+                }
+                case Op::MXV: {
+                    if (mxv && mxv.get() != x.get()) { need(x); return -1; }
+                    const NodeP &u = x->a;
+                    if (!u->mat) { need(u); return -1; }
+                    if (u->kind == VKind::ISO) ensure_full(c, u);
+                    mxv = x;
+                    Ins in{};
+                    in.k = Ins::MXV_ACC;
+                    in.t = x->type;
+                    r = add(in);
+                    break;
+                }
+                case Op::REDUCE:
+                    need(x);
+                    return -1;
+                default:
+                    fail(NBG_PANIC, "planner: unexpected node");
+            }
+            visited.push_back(x);
+        }
+        ins_of[x.get()] = r;
+        return r;
+    }
+
+    // returns false if prerequisites are missing
+    bool add_vector_output(const NodeP &x) {
+        if (is_out.count(x.get())) return true;
+        int i = emit(x);
+        if (i < 0) return false;
+        prog.outs.push_back(OutV{i, (int)out_nodes.size()});
+        out_nodes.push_back(x);
+        is_out.insert(x.get());
+        return true;
+    }
+
+    bool add_reduction(const NodeP &x) {
+        if (is_out.count(x.get())) return true;
+        int i = emit(x->a);
+        if (i < 0) return false;
+        if (prog.ins[i].t != x->type) {
+            Ins cv{};
+            cv.k = Ins::CVT;
+            cv.t = x->type;
+            cv.a = i;
+            cv.uniform = prog.ins[i].uniform;
+            i = add(cv);
+        }
+        uint8_t fmt;
+        bool f = is_float(x->type);
+        if (x->code == NBG_PLUS) fmt = (uint8_t)(f ? SFmt::XACC : SFmt::I64);
+        else if (x->code == NBG_MAX) fmt = (uint8_t)(f ? SFmt::FMAX : SFmt::IMAX);
+        else fmt = (uint8_t)(f ? SFmt::FMIN : SFmt::IMIN);
+        prog.reds.push_back(RedOut{i, x->code, (int)red_nodes.size(), fmt});
+        red_nodes.push_back(x);
+        is_out.insert(x.get());
+        return true;
+    }
+};
+
+// ---------------------------------------------------------------- ISO -> FULL
+
+void ensure_full(Ctx &c, const NodeP &v) {
+    if (v->kind != VKind::ISO || v->full_cache) return;
+    size_t bytes = (size_t)v->n * type_size(v->type);
+    v->full_cache = alloc_buf(c, bytes);
+    if (v->n) gpu_fill_iso(c, v->full_cache->d, v->type, v->n, v->iso);
+}
+
+// ---------------------------------------------------------------- launch of one region
+
+struct HintOut {
+    NodeP node;       // instantiated template root (pending until launch)
+};
+
+static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int64_t n) {
+    Prog &p = B.prog;
+    p.spmv = (bool)B.mxv;
+    p.n_in = (int)B.in_nodes.size();
+    p.n_out = (int)B.out_nodes.size();
+    p.n_imm = (int)B.imm.size();
+    p.n_sin = (int)B.sin.size();
+    p.n_red = (int)B.red_nodes.size();
+    if (p.n_in > MAX_IN || p.n_out > MAX_OUT || p.n_imm > MAX_IMM || p.n_sin > MAX_SIN || p.n_red > MAX_RED)
+        fail(NBG_NOT_IMPLEMENTED, "planner: region exceeds kernel argument limits");
+
+    KArgs args;
+    memset(&args, 0, sizeof args);
+    args.n = n;
+    for (int k = 0; k < p.n_in; k++) args.in[k] = B.in_nodes[k]->buf->d;
+    // outputs
+    std::vector<BufP> obufs;
+    for (int k = 0; k < p.n_out; k++) {
+        const NodeP &x = B.out_nodes[k];
+        BufP b = alloc_buf(c, (size_t)n * type_size(x->type));
+        obufs.push_back(b);
+        args.out[k] = b->d;
+        c.stats.vectors_materialized++;
+        c.stats.bytes_materialized += b->bytes;
+    }
+    std::vector<SlotP> rslots;
+    for (int k = 0; k < p.n_red; k++) {
+        SlotP s = alloc_slot(c);
+        rslots.push_back(s);
+        args.racc[k] = s->dptr();
+    }
+    for (int k = 0; k < p.n_sin; k++) args.sin[k] = B.sin[k]->dptr();
+
+    // alignment decides the vectorised ewise skeleton
+    bool vec = true;
+    for (int k = 0; k < p.n_in; k++) vec = vec && (((uintptr_t)args.in[k]) % 16 == 0);
+    for (int k = 0; k < p.n_out; k++) vec = vec && (((uintptr_t)args.out[k]) % 16 == 0);
+    p.vec = p.spmv ? true : vec;
+
+    long long items = 0;
+    if (p.spmv) {
+        Node &mx = *B.mxv;
+        Mat &A = *mx.A;
+        if (!A.plan) gpu_build_spmv_plan(c, A);
+        const NodeP &u = mx.a;
+        p.sp.add = mx.add;
+        p.sp.mul = mx.mul;
+        p.sp.T = mx.type;
+        p.sp.xt = u->type;
+        p.sp.at = A.type;
+        p.sp.has_vals = (bool)A.vals;
+        B.imm[0] = A.iso;
+        B.imm[1] = mx.c0;
+        args.rowptr = (const long long *)A.rowptr->d;
+        args.colidx = (const int *)A.colidx->d;
+        args.aval = A.vals ? A.vals->d : nullptr;
+        args.x = (u->kind == VKind::ISO) ? u->full_cache->d : u->buf->d;
+        args.tiles = (const int *)(A.plan->tiles ? A.plan->tiles->d : nullptr);
+        args.chunks = (const int *)(A.plan->chunks ? A.plan->chunks->d : nullptr);
+        args.longs = (const int *)(A.plan->longs ? A.plan->longs->d : nullptr);
+        args.counters = (int *)(A.plan->counters ? A.plan->counters->d : nullptr);
+        args.partials = (double *)(A.plan->partials ? A.plan->partials->d : nullptr);
+        args.ntiles = A.plan->ntiles;
+        args.nchunks = A.plan->nchunks;
+        items = A.plan->ntiles + A.plan->nchunks;
+    } else {
+        items = (n + 1023) / 1024;
+    }
+    for (int k = 0; k < p.n_imm; k++) args.imm[k] = B.imm[k];
+
+    std::string sig = p.signature();
+    KernelP kern;
+    auto it = c.plans.find(sig);
+    if (it == c.plans.end()) {
+        char nm[48];
+        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.spmv ? "spmv" : "ewise", (unsigned long long)hash_str(sig));
+        kern = jit_compile(c, codegen(p, nm), nm, p.spmv);
+        c.plans[sig] = kern;
+        c.stats.plans_built++;
+    } else {
+        kern = it->second;
+        c.stats.plan_hits++;
+    }
+    if (items > 0 && n > 0) launch(c, *kern, args, items, p.spmv ? "spmv" : "ewise");
+
+    // provenance of the written buffers (for hints): base signature + output index
+    // (set by the caller through B.prog before hints were appended)
+    for (int k = 0; k < p.n_out; k++) {
+        Node &x = *B.out_nodes[k];
+        x.buf = obufs[k];
+        x.kind = VKind::FULL;
+        x.mat = true;
+    }
+    for (int k = 0; k < p.n_red; k++) {
+        Node &x = *B.red_nodes[k];
+        x.slot = rslots[k];
+        x.sfmt = (SFmt)p.reds[k].fmt;
+        x.mat = true;
+        if (x.user_refs > 0) issue_readback(c, *x.slot);   // so a later get() only waits on this kernel
+    }
+    (void)hint_outs;
+}
+
+// ---------------------------------------------------------------- materialise
+
+static int64_t root_len(const NodeP &r) {
+    if (r->scalar) return r->a ? r->a->n : 0;
+    if (r->op == Op::MXV) return r->A->nrows;
+    return r->n;
+}
+
+static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
+    const bool nb = c.mode == NBG_NONBLOCKING;
+    for (int guard = 0; guard < 256; guard++) {
+        Builder B(c);
+        bool ok = true;
+        for (const NodeP &r : roots) {
+            if (r->mat) continue;
+            if (r->scalar) ok = B.add_reduction(r) && ok;
+            else ok = B.add_vector_output(r) && ok;
+        }
+        if (!B.prereq.empty()) {
+            std::vector<NodeP> todo;
+            for (const NodeP &p : B.prereq) {
+                if (p->mat) continue;
+                if (nb && memo_bind(c, p)) continue;
+                if (nb) learn_hint(c, p);
+                todo.push_back(p);
+            }
+            if (!todo.empty()) materialize(c, todo);
+            continue;
+        }
+        if (!ok) fail(NBG_PANIC, "planner: region incomplete without prerequisites");
+        bool any = false;
+        for (const NodeP &r : roots) any = any || !r->mat;
+        if (!any) return;
+
+        // liveness: pending nodes a user still holds are stored as well (nonblocking only)
+        if (nb) {
+            std::vector<NodeP> vis = B.visited;
+            for (const NodeP &x : vis)
+                if (!x->scalar && x->user_refs > 0 && !B.is_out.count(x.get())) B.add_vector_output(x);
+        }
+        const int nbase = (int)B.out_nodes.size();
+        const uint64_t base_hash = hash_str(B.prog.signature());
+
+        // speculative side outputs learned for this signature
+        std::vector<HintOut> hint_outs;
+        if (nb) {
+            for (int o = 0; o < nbase; o++) {
+                auto h = c.hints.find({base_hash, o});
+                if (h == c.hints.end()) continue;
+                for (const Hint &hint : h->second) {
+                    std::unordered_map<const Node *, NodeP> cs;
+                    NodeP inst = clone_subst(c, hint.tmpl, hint.placeholder, B.out_nodes[o], cs);
+                    bool added = inst->scalar ? B.add_reduction(inst) : B.add_vector_output(inst);
+                    if (!added || !B.prereq.empty()) fail(NBG_PANIC, "planner: hint needs a prerequisite");
+                    hint_outs.push_back(HintOut{inst});
+                    c.stats.side_outputs++;
+                }
+            }
+        }
+
+        int64_t n = B.mxv ? B.mxv->A->nrows : root_len(roots[0]);
+        size_t nvis = B.visited.size();
+        run_region(c, B, hint_outs, n);
+        for (int k = 0; k < nbase; k++) {
+            B.out_nodes[k]->buf->prod_sig = base_hash;
+            B.out_nodes[k]->buf->prod_out = k;
+        }
+        // memoise the side outputs under their structural key (R is materialised now)
+        for (HintOut &h : hint_outs) {
+            std::vector<std::weak_ptr<Buf>> deps;
+            std::unordered_set<const Node *> seen;
+            // key over the template structure: leaves are materialised nodes
+            Node tmp = *h.node;
+            tmp.mat = false;   // the key describes the expression, not its result
+            std::string k = node_key(&tmp);
+            leaf_bufs(&tmp, deps, seen);
+            c.memo[k] = Ctx::MemoEntry{deps, h.node};
+        }
+        // elided intermediates = visited pending nodes that were not stored
+        size_t stored = 0;
+        for (const NodeP &x : B.visited)
+            if (B.is_out.count(x.get())) stored++;
+        c.stats.intermediates_elided += (nvis >= stored) ? (nvis - std::min(stored, nvis)) : 0;
+        for (const NodeP &x : B.out_nodes) drop_inputs(*x);
+        for (const NodeP &x : B.red_nodes) drop_inputs(*x);
+        c.stats.waits++;
+        return;
+    }
+    fail(NBG_PANIC, "planner did not converge");
+}
+
+void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
+    double t0 = now_ns();
+    if (c.mode == NBG_NONBLOCKING) memo_purge(c);
+    std::vector<NodeP> roots;
+    std::unordered_set<const Node *> seen;
+    for (const NodeP &r0 : roots_in) {
+        NodeP r = r0;
+        if (r->mat) continue;
+        if (r->scalar && r->op == Op::SAPPLY) {   // scalar ops are evaluated where they are used
+            while (r && !r->mat && r->op == Op::SAPPLY) r = r->a;
+            if (!r || r->mat) continue;
+        }
+        if (seen.insert(r.get()).second) roots.push_back(r);
+    }
+    if (roots.empty()) return;
+    if (c.mode == NBG_NONBLOCKING) {
+        std::vector<NodeP> left;
+        for (const NodeP &r : roots)
+            if (!memo_bind(c, r)) left.push_back(r);
+        roots.swap(left);
+    }
+    // group by index-space length (one kernel per group)
+    std::map<int64_t, std::vector<NodeP>> groups;
+    for (const NodeP &r : roots) groups[root_len(r)].push_back(r);
+    for (auto &g : groups) materialize_group(c, g.second);
+    c.stats.host_plan_ns += (uint64_t)(now_ns() - t0);
+}
+
+double scalar_read(Ctx &c, const NodeP &s) {
+    if (!s->mat) {
+        if (s->op == Op::SAPPLY) {
+            double v = scalar_read(c, s->a);
+            return host_round(s->type, host_unop(s->code, s->type, v, s->c0, s->c1));
+        }
+        materialize(c, {s});
+    }
+    if (s->sfmt == SFmt::HOST) return s->hval;
+    Slot &sl = *s->slot;
+    issue_readback(c, sl);
+    NBG_CUDA(cudaEventSynchronize(sl.ev));
+    return host_round(s->type, slot_value(sl.hptr(), s->sfmt));
+}
+
+}  // namespace nbg

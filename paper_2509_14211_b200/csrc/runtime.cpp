@@ -1,0 +1,354 @@
+// runtime.cpp -- device memory, scalar slots, events, timing, host-side arithmetic helpers.
+#include <cmath>
+#include <cstdio>
+
+#include "nbg_internal.hpp"
+
+namespace nbg {
+
+void fail(nbg_status st, const std::string &msg) { throw Error{st, msg}; }
+
+void cuda_fail(cudaError_t e, const char *what, const char *file, int line) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %d (%s) in %s at %s:%d", (int)e, cudaGetErrorString(e), what, file, line);
+    nbg_status st = (e == cudaErrorMemoryAllocation) ? NBG_OUT_OF_MEMORY : NBG_PANIC;
+    throw Error{st, buf};
+}
+
+double now_ns() {
+    return (double)std::chrono::duration_cast<std::chrono::nanoseconds>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+uint64_t hash_str(const std::string &s) {   // FNV-1a 64
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char ch : s) {
+        h ^= ch;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+// ---------------------------------------------------------------- buffers
+
+Buf::~Buf() {
+    if (owned && d && ctx) cudaFreeAsync(d, ctx->stream);
+}
+
+BufP alloc_buf(Ctx &c, size_t bytes) {
+    auto b = std::make_shared<Buf>();
+    b->ctx = &c;
+    b->id = c.new_id();
+    b->bytes = bytes;
+    b->owned = true;
+    if (bytes) NBG_CUDA(cudaMallocAsync(&b->d, bytes, c.stream));
+    return b;
+}
+
+BufP borrow_buf(Ctx &c, void *d, size_t bytes) {
+    auto b = std::make_shared<Buf>();
+    b->ctx = &c;
+    b->id = c.new_id();
+    b->bytes = bytes;
+    b->d = d;
+    b->owned = false;
+    return b;
+}
+
+// ---------------------------------------------------------------- scalar slots
+
+Slab::~Slab() {
+    if (d) cudaFreeAsync(d, ctx->stream);
+    if (h) {
+        // the host mirror may still be the target of a queued copy
+        cudaStreamSynchronize(ctx->stream);
+        cudaFreeHost(h);
+    }
+}
+
+Slot::~Slot() {
+    if (ev && slab) put_event(*slab->ctx, ev);
+}
+
+SlotP alloc_slot(Ctx &c) {
+    if (!c.cur_slab || c.cur_slab->used >= SLAB_SLOTS) {
+        auto s = std::make_shared<Slab>();
+        s->ctx = &c;
+        size_t bytes = (size_t)SLAB_SLOTS * SLOT_U64 * sizeof(unsigned long long);
+        NBG_CUDA(cudaMallocAsync((void **)&s->d, bytes, c.stream));
+        NBG_CUDA(cudaMemsetAsync(s->d, 0, bytes, c.stream));
+        NBG_CUDA(cudaMallocHost((void **)&s->h, bytes));
+        c.cur_slab = s;
+    }
+    auto sl = std::make_shared<Slot>();
+    sl->slab = c.cur_slab;
+    sl->idx = c.cur_slab->used++;
+    sl->id = c.new_id();
+    return sl;
+}
+
+cudaEvent_t get_event(Ctx &c) {
+    if (!c.event_pool.empty()) {
+        cudaEvent_t e = c.event_pool.back();
+        c.event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    NBG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return e;
+}
+
+void put_event(Ctx &c, cudaEvent_t e) { c.event_pool.push_back(e); }
+
+void issue_readback(Ctx &c, Slot &s) {
+    if (s.rb_issued) return;
+    NBG_CUDA(cudaMemcpyAsync(s.hptr(), s.dptr(), SLOT_U64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.stream));
+    if (!s.ev) s.ev = get_event(c);
+    NBG_CUDA(cudaEventRecord(s.ev, c.stream));
+    s.rb_issued = true;
+}
+
+// ---------------------------------------------------------------- exact accumulator decode (host)
+// Same arithmetic as nbg_xacc_value in jit/prelude.cuh: carry-normalise the 10 limbs of signed
+// 32-bit pieces into an 11-word two's complement integer (LSB 2^-160), then round to nearest even.
+double xacc_to_double(const unsigned long long *L) {
+    unsigned long long flags = L[10];
+    if (flags & 9ull) return NAN;
+    if ((flags & 6ull) == 6ull) return NAN;
+    if (flags & 2ull) return INFINITY;
+    if (flags & 4ull) return -INFINITY;
+    uint32_t w[11];
+    long long carry = 0;
+    for (int k = 0; k < 10; k++) {
+        long long v = (long long)L[k] + carry;
+        w[k] = (uint32_t)(v & 0xffffffffll);
+        carry = v >> 32;
+    }
+    w[10] = (uint32_t)carry;
+    bool neg = carry < 0;
+    if (neg) {
+        uint32_t cr = 1;
+        for (int k = 0; k < 11; k++) {
+            unsigned long long t = (unsigned long long)(uint32_t)(~w[k]) + cr;
+            w[k] = (uint32_t)t;
+            cr = (uint32_t)(t >> 32);
+        }
+    }
+    int h = -1;
+    for (int k = 10; k >= 0; k--)
+        if (w[k]) { h = k; break; }
+    if (h < 0) return 0.0;
+    int g = h * 32 + (31 - __builtin_clz(w[h]));
+    unsigned long long top = 0;
+    for (int j = 0; j < 64; j++) {
+        int b = g - j;
+        unsigned long long bit = (b >= 0) ? ((w[b >> 5] >> (b & 31)) & 1u) : 0u;
+        top = (top << 1) | bit;
+    }
+    bool sticky = false;
+    for (int b = g - 64; b >= 0; b--)
+        if ((w[b >> 5] >> (b & 31)) & 1u) { sticky = true; break; }
+    unsigned long long mant = top >> 11;
+    unsigned long long rb = top & 0x7ffull;
+    int lsb = g - 52;
+    if (rb > 0x400ull || (rb == 0x400ull && (sticky || (mant & 1ull)))) {
+        mant += 1;
+        if (mant == (1ull << 53)) { mant >>= 1; lsb += 1; }
+    }
+    double v = std::ldexp((double)mant, lsb - 160);
+    return neg ? -v : v;
+}
+
+// host twin of nbg_xacc_add (prelude.cuh): add one double into the limbs
+void host_xacc_add(unsigned long long *acc, double d) {
+    if (d == 0.0) return;
+    long long bits;
+    memcpy(&bits, &d, 8);
+    int e = (int)((bits >> 52) & 0x7ff);
+    if (e == 0x7ff) {
+        acc[10] |= ((bits & 0xFFFFFFFFFFFFFll) != 0) ? 1ull : (bits < 0 ? 4ull : 2ull);
+        return;
+    }
+    unsigned long long m = (unsigned long long)bits & 0xFFFFFFFFFFFFFull;
+    int ex;
+    if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
+    int pos = ex + 160;
+    if (pos < 0) {
+        int s = -pos;
+        if (s >= 64) return;
+        m >>= s;
+        pos = 0;
+        if (m == 0) return;
+    }
+    if (pos > 235) { acc[10] |= 8ull; return; }
+    int k = pos >> 5, sh = pos & 31;
+    unsigned long long lo = m << sh;
+    unsigned long long hi = sh ? (m >> (64 - sh)) : 0ull;
+    unsigned long long p0 = lo & 0xffffffffull, p1 = lo >> 32, p2 = hi;
+    if (bits < 0) { p0 = (unsigned long long)(-(long long)p0); p1 = (unsigned long long)(-(long long)p1); p2 = (unsigned long long)(-(long long)p2); }
+    acc[k] += p0;
+    acc[k + 1] += p1;
+    acc[k + 2] += p2;
+}
+
+static double fkey_dec(unsigned long long k) {
+    long long b = (k & 0x8000000000000000ull) ? (long long)(k & 0x7fffffffffffffffull) : (long long)(~k);
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+}
+
+double slot_value(const unsigned long long *s, SFmt fmt) {
+    switch (fmt) {
+        case SFmt::XACC: return xacc_to_double(s);
+        case SFmt::I64: return (double)(long long)s[11];
+        case SFmt::FMAX: return s[11] ? fkey_dec(s[11]) : -INFINITY;
+        case SFmt::FMIN: return s[11] ? fkey_dec(~s[11]) : INFINITY;
+        case SFmt::IMAX: return s[11] ? (double)(long long)(s[11] ^ 0x8000000000000000ull) : -9.2233720368547758e18;
+        case SFmt::IMIN: return s[11] ? (double)(long long)(~s[11] ^ 0x8000000000000000ull) : 9.2233720368547758e18;
+        default: return 0.0;
+    }
+}
+
+// ---------------------------------------------------------------- timing
+
+void timing_begin(Ctx &c, const char *cls, cudaEvent_t *ev0) {
+    *ev0 = nullptr;
+    if (!c.timing) return;
+    NBG_CUDA(cudaEventCreate(ev0));
+    NBG_CUDA(cudaEventRecord(*ev0, c.stream));
+    (void)cls;
+}
+
+void timing_end(Ctx &c, const char *cls, cudaEvent_t ev0) {
+    if (!c.timing || !ev0) return;
+    cudaEvent_t ev1;
+    NBG_CUDA(cudaEventCreate(&ev1));
+    NBG_CUDA(cudaEventRecord(ev1, c.stream));
+    c.tclass[cls].pending.push_back({ev0, ev1});
+}
+
+void timing_collect(Ctx &c) {
+    for (auto &kv : c.tclass) {
+        for (auto &pr : kv.second.pending) {
+            NBG_CUDA(cudaEventSynchronize(pr.second));
+            float ms = 0.f;
+            NBG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
+            kv.second.ms += ms;
+            kv.second.launches++;
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
+        kv.second.pending.clear();
+    }
+}
+
+// ---------------------------------------------------------------- host arithmetic
+// Used for eager folding of iso operands and for host-side scalar ops.  Compiled with
+// -ffp-contract=off: each line is one IEEE round-to-nearest operation in the operator's type,
+// identical to the device code generated for the same operator.
+
+template <class C>
+static C h_div(C a, C b) {
+    if constexpr (std::is_floating_point<C>::value) return a / b;
+    else return b == 0 ? (C)0 : a / b;
+}
+template <class C>
+static C h_abs(C a) {
+    if constexpr (std::is_floating_point<C>::value) return std::fabs(a);
+    else return a < 0 ? -a : a;
+}
+template <class C>
+static C h_min(C a, C b) {
+    if constexpr (std::is_floating_point<C>::value) return std::fmin(a, b);
+    else return a < b ? a : b;
+}
+template <class C>
+static C h_max(C a, C b) {
+    if constexpr (std::is_floating_point<C>::value) return std::fmax(a, b);
+    else return a > b ? a : b;
+}
+
+template <class C>
+static C h_unop(int code, C x, C k0, C k1) {
+    switch (code) {
+        case NBG_IDENTITY: return x;
+        case NBG_AINV: return -x;
+        case NBG_ABS: return h_abs(x);
+        case NBG_MINV: return h_div((C)1, x);
+        case NBG_ADD_C: return x + k0;
+        case NBG_MUL_C: return x * k0;
+        case NBG_AXPB: { C t = k0 * x; return t + k1; }
+        case NBG_ABS_SUB_C: return h_abs(x - k0);
+        case NBG_RECIP_SCALED: return x != (C)0 ? h_div(k0, x) : (C)0;
+        case NBG_ISZERO: return x == (C)0 ? (C)1 : (C)0;
+    }
+    fail(NBG_INVALID_VALUE, "unknown unop code");
+}
+
+template <class C>
+static C h_binop(int code, C x, C y, C k0) {
+    switch (code) {
+        case NBG_PLUS: return x + y;
+        case NBG_MINUS: return x - y;
+        case NBG_TIMES: return x * y;
+        case NBG_DIV: return h_div(x, y);
+        case NBG_MIN: return h_min(x, y);
+        case NBG_MAX: return h_max(x, y);
+        case NBG_FIRST: return x;
+        case NBG_SECOND: return y;
+        case NBG_ABSDIFF: return h_abs(x - y);
+        case NBG_MAX_DIVX_C: return h_max(h_div(x, k0), y);
+    }
+    fail(NBG_INVALID_VALUE, "unknown binop code");
+}
+
+// values travel as double; a double holding a value of type t converts exactly back to t
+double host_round(int t, double v) {
+    switch (t) {
+        case NBG_BOOL: return v != 0.0 ? 1.0 : 0.0;
+        case NBG_INT32: return (double)(int)v;
+        case NBG_INT64: return (double)(long long)v;
+        case NBG_FP32: return (double)(float)v;
+        default: return v;
+    }
+}
+
+double host_unop(int code, int t, double x, double c0, double c1) {
+    switch (t) {
+        case NBG_FP32: return (double)h_unop<float>(code, (float)x, (float)c0, (float)c1);
+        case NBG_FP64: return h_unop<double>(code, x, c0, c1);
+        case NBG_INT32: return (double)h_unop<int>(code, (int)x, (int)c0, (int)c1);
+        case NBG_INT64: return (double)h_unop<long long>(code, (long long)x, (long long)c0, (long long)c1);
+        case NBG_BOOL: return h_unop<long long>(code, (long long)x, (long long)c0, (long long)c1) != 0 ? 1.0 : 0.0;
+    }
+    fail(NBG_INVALID_VALUE, "bad type");
+}
+
+double host_binop(int code, int t, double x, double y, double c0) {
+    switch (t) {
+        case NBG_FP32: return (double)h_binop<float>(code, (float)x, (float)y, (float)c0);
+        case NBG_FP64: return h_binop<double>(code, x, y, c0);
+        case NBG_INT32: return (double)h_binop<int>(code, (int)x, (int)y, (int)c0);
+        case NBG_INT64: return (double)h_binop<long long>(code, (long long)x, (long long)y, (long long)c0);
+        case NBG_BOOL: return h_binop<long long>(code, (long long)x, (long long)y, (long long)c0) != 0 ? 1.0 : 0.0;
+    }
+    fail(NBG_INVALID_VALUE, "bad type");
+}
+
+Kernel::~Kernel() {
+    if (lib) cudaLibraryUnload(lib);
+}
+
+Ctx::~Ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    memo.clear();
+    hints.clear();
+    plans.clear();
+    cur_slab.reset();
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+}  // namespace nbg

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): bit-exact graph structure, out-degrees and sweep counts; ranks
+within max relative error 1e-10 (fp64) / 1e-5 (fp32) after the same sweep count; blocking ==
+nonblocking bit for bit (fused kernels keep the blocking rounding points).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import ops
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nbg():
+    from paper_2509_14211_b200 import nbg as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(nbg):
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    yield c
+    nbg.nbg_finalize(c)
+
+
+@pytest.fixture(scope="module")
+def bctx(nbg):
+    c = nbg.nbg_init(nbg.BLOCKING, 0)
+    yield c
+    nbg.nbg_finalize(c)
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.abs(b))) if a.size else 0.0
+
+
+# ------------------------------------------------------------------ a0: generation + CSR build
+
+@pytest.mark.parametrize("kind,scale,ef,seed", [("rmat", 10, 8, 1), ("rmat", 10, 8, 2), ("rmat", 10, 8, 3),
+                                                ("rmat", 14, 16, 5), ("er", 12, 16, 4)])
+def test_edges_and_csr_bit_exact(nbg, ctx, kind, scale, ef, seed):
+    k = nbg.GRAPH_RMAT if kind == "rmat" else nbg.GRAPH_ER
+    src, dst = nbg.nbg_graph_edges(ctx, k, scale, ef, seed)
+    osrc, odst = (oracle.rmat_edges if kind == "rmat" else oracle.er_edges)(scale, ef, seed)
+    assert np.array_equal(src, osrc) and np.array_equal(dst, odst)
+    A, deg = nbg.nbg_matrix_from_generator(ctx, k, scale, ef, seed)
+    rp, ci = nbg.nbg_matrix_export_csr(ctx, A)
+    orp, oci, odeg = oracle.build_csr(1 << scale, osrc, odst)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert np.array_equal(nbg.nbg_vector_export_dense(ctx, deg), odeg)
+    nbg.nbg_vector_free(ctx, deg)
+    nbg.nbg_matrix_free(ctx, A)
+
+
+def test_csr_from_host_edges_with_dups_and_loops(nbg, ctx):
+    rng = np.random.default_rng(0)
+    n = 300
+    src = rng.integers(0, n, 5000).astype(np.int32)
+    dst = rng.integers(0, n, 5000).astype(np.int32)
+    src[:50] = dst[:50]                      # self loops
+    src[50:100], dst[50:100] = src[100:150], dst[100:150]   # duplicates
+    A, deg = nbg.nbg_matrix_from_edges(ctx, n, src, dst)
+    rp, ci = nbg.nbg_matrix_export_csr(ctx, A)
+    orp, oci, odeg = oracle.build_csr(n, src, dst)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    assert np.array_equal(nbg.nbg_vector_export_dense(ctx, deg), odeg)
+
+
+def test_edges_out_of_range(nbg, ctx):
+    with pytest.raises(nbg.NbgError) as e:
+        nbg.nbg_matrix_from_edges(ctx, 10, np.array([1, 2], np.int32), np.array([3, 10], np.int32))
+    assert e.value.status == nbg.INDEX_OUT_OF_BOUNDS
+
+
+# ------------------------------------------------------------------ PageRank sweeps
+
+def _graph(nbg, ctx, kind, scale, ef, seed):
+    k = nbg.GRAPH_RMAT if kind == "rmat" else nbg.GRAPH_ER
+    A, deg = nbg.nbg_matrix_from_generator(ctx, k, scale, ef, seed)
+    src, dst = (oracle.rmat_edges if kind == "rmat" else oracle.er_edges)(scale, ef, seed)
+    orp, oci, odeg = oracle.build_csr(1 << scale, src, dst)
+    return A, deg, (orp, oci, odeg)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("uniform", [True, False])
+def test_config1_fp64_20_sweeps(nbg, ctx, seed, uniform):
+    A, deg, (orp, oci, odeg) = _graph(nbg, ctx, "rmat", 10, 8, seed)
+    r, sweeps, hist = nbg.nbg_pagerank(ctx, A, deg, tol=-1.0, itermax=20, type=nbg.FP64,
+                                       dangling=nbg.PR_UNIFORM if uniform else nbg.PR_DROP)
+    ro, so, dho, _ = oracle.pagerank(orp, oci, odeg, dtype=np.float64, uniform=uniform, itermax=20)
+    rv = nbg.nbg_vector_export_dense(ctx, r)
+    assert sweeps == so == 20
+    assert rel(rv, ro) <= 1e-10
+    assert rel(hist, dho) <= 1e-9
+    if uniform:
+        assert abs(rv.sum() - 1.0) < 1e-12
+
+
+@pytest.mark.parametrize("scale,ef,kind", [(12, 16, "rmat"), (14, 8, "er"), (16, 16, "rmat")])
+def test_fp32_fixed_sweeps(nbg, ctx, scale, ef, kind):
+    A, deg, (orp, oci, odeg) = _graph(nbg, ctx, kind, scale, ef, 1)
+    r, sweeps, hist = nbg.nbg_pagerank(ctx, A, deg, tol=-1.0, itermax=30, type=nbg.FP32)
+    ro, so, dho, _ = oracle.pagerank(orp, oci, odeg, dtype=np.float32, itermax=30)
+    rv = nbg.nbg_vector_export_dense(ctx, r)
+    assert sweeps == so
+    assert rel(rv, ro) <= 1e-5
+
+
+def test_convergence_sweep_count_exact(nbg, ctx):
+    A, deg, (orp, oci, odeg) = _graph(nbg, ctx, "rmat", 16, 16, 1)
+    r, sweeps, hist = nbg.nbg_pagerank(ctx, A, deg, tol=1e-6, itermax=100, type=nbg.FP32)
+    ro, so, dho, _ = oracle.pagerank(orp, oci, odeg, dtype=np.float32, itermax=100, tol=1e-6)
+    assert sweeps == so
+    assert rel(nbg.nbg_vector_export_dense(ctx, r), ro) <= 1e-5
+    assert rel(hist, dho) <= 1e-6
+
+
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+def test_blocking_equals_nonblocking_bitwise(nbg, ctx, bctx, T):
+    t = nbg.FP32 if T == "fp32" else nbg.FP64
+    res = []
+    for c in (ctx, bctx):
+        A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 12, 8, 9)
+        r, sweeps, hist = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=12, type=t)
+        res.append((nbg.nbg_vector_export_dense(c, r), hist))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
+
+
+def test_long_rows_star(nbg, ctx):
+    # a hub with 50k in-edges: exercises the long-row chunk path + its ticket combine
+    n = 60000
+    src = np.arange(1, n, dtype=np.int32)
+    dst = np.zeros(n - 1, np.int32)
+    src = np.concatenate([src, np.array([0, 0], np.int32)])
+    dst = np.concatenate([dst, np.array([1, 2], np.int32)])
+    A, deg = nbg.nbg_matrix_from_edges(ctx, n, src, dst)
+    orp, oci, odeg = oracle.build_csr(n, src, dst)
+    for T, np_t, tol in ((nbg.FP64, np.float64, 1e-10), (nbg.FP32, np.float32, 1e-5)):
+        r, sweeps, _ = nbg.nbg_pagerank(ctx, A, deg, tol=-1.0, itermax=10, type=T)
+        ro, _, _, _ = oracle.pagerank(orp, oci, odeg, dtype=np_t, itermax=10)
+        assert rel(nbg.nbg_vector_export_dense(ctx, r), ro) <= tol
+
+
+def test_cycle_uniform_gpu(nbg, ctx):
+    n = 1001
+    src = np.arange(n, dtype=np.int32)
+    dst = ((np.arange(n) + 1) % n).astype(np.int32)
+    A, deg = nbg.nbg_matrix_from_edges(ctx, n, src, dst)
+    r, _, _ = nbg.nbg_pagerank(ctx, A, deg, tol=-1.0, itermax=25, type=nbg.FP32)
+    rv = nbg.nbg_vector_export_dense(ctx, r)
+    assert np.all(rv == rv[0])
+    assert abs(float(rv[0]) - float(np.float32(1 / n))) <= float(np.spacing(np.float32(1 / n)))
+
+
+# ------------------------------------------------------------------ mxv semirings
+
+@pytest.mark.parametrize("add", ["PLUS", "MIN", "MAX"])
+@pytest.mark.parametrize("mul", ["TIMES", "SECOND", "FIRST", "PLUS"])
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+def test_mxv_semirings(nbg, ctx, add, mul, T):
+    rng = np.random.default_rng(hash((add, mul, T)) % 2**32)
+    n, m = 700, 900                                   # ragged, several tiles
+    lens = rng.integers(0, 40, n)
+    lens[5] = 3000                                    # a long row (chunks)
+    lens[7] = 200                                     # a medium row (warp path)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(m, int(l), replace=False)) for l in lens]).astype(np.int32)
+    npT = np.float32 if T == "fp32" else np.float64
+    vals = rng.random(ci.shape[0]).astype(npT)
+    x = rng.random(m).astype(npT)
+    t = nbg.TYPE_OF[T]
+    A = nbg.nbg_matrix_from_csr(ctx, n, m, rp, ci, vals=vals, type=t)
+    u = nbg.nbg_vector_from_dense(ctx, t, x)
+    w = nbg.nbg_mxv(ctx, t, add, mul, A, u)
+    got = nbg.nbg_vector_export_dense(ctx, w)
+    exp = ops.mxv(add, mul, rp, ci, vals, x, npT)
+    if add == "PLUS":
+        assert rel(got[lens > 0], exp[lens > 0]) <= (2e-7 if T == "fp32" else 1e-14)
+        assert np.all(got[lens == 0] == 0)
+    else:
+        assert np.array_equal(got, exp)
+
+
+def test_mxv_iso_and_empty_input(nbg, ctx):
+    rp = np.array([0, 2, 2, 5], np.int64)
+    ci = np.array([0, 3, 1, 2, 3], np.int32)
+    A = nbg.nbg_matrix_from_csr(ctx, 3, 4, rp, ci, type=nbg.FP64, iso=2.0)
+    x = nbg.nbg_vector_new_const(ctx, nbg.FP64, 4, 1.5)
+    w = nbg.nbg_mxv(ctx, nbg.FP64, "PLUS", "TIMES", A, x)
+    assert np.array_equal(nbg.nbg_vector_export_dense(ctx, w), [6.0, 0.0, 9.0])
+    e = nbg.nbg_vector_new(ctx, nbg.FP64, 4)
+    w2 = nbg.nbg_mxv(ctx, nbg.FP64, "PLUS", "TIMES", A, e)      # dense output: identity everywhere
+    assert np.array_equal(nbg.nbg_vector_export_dense(ctx, w2), [0.0, 0.0, 0.0])
+    with pytest.raises(nbg.NbgError) as ex:
+        nbg.nbg_mxv(ctx, nbg.FP64, "PLUS", "TIMES", A, nbg.nbg_vector_new_const(ctx, nbg.FP64, 5, 1.0))
+    assert ex.value.status == nbg.DIMENSION_MISMATCH
+
+
+# ------------------------------------------------------------------ elementwise chain (config 2)
+
+def _chain(nbg, c, x, y, T, free=True):
+    """z = ewise_mult(*, x, apply(v+1, y)); c1..c5; s = reduce(+)."""
+    vx = nbg.nbg_vector_from_dense(c, T, x)
+    vy = nbg.nbg_vector_from_dense(c, T, y)
+    a = nbg.nbg_apply(c, T, "ADD_C", vy, 1.0)
+    z = nbg.nbg_ewise_mult(c, T, "TIMES", vx, a)
+    c1 = nbg.nbg_apply(c, T, "MUL_C", z, 0.5)
+    c2 = nbg.nbg_ewise_add(c, T, "PLUS", c1, vx)
+    c3 = nbg.nbg_ewise_mult(c, T, "TIMES", c2, vy)
+    c4 = nbg.nbg_apply(c, T, "ABS_SUB_C", c3, 0.25)
+    c5 = nbg.nbg_ewise_add(c, T, "MAX", c4, z)
+    hs = [a, c1, c2, c3, c4]
+    if free:
+        for h in hs:
+            nbg.nbg_vector_free(c, h)
+    s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", c5)
+    return s, z, c5, vx, vy
+
+
+def _chain_oracle(x, y, npT):
+    z = ops.ewise_mult("TIMES", x, ops.unop("ADD_C", y, npT, 1.0), npT)
+    c1 = ops.unop("MUL_C", z, npT, 0.5)
+    c2 = ops.ewise_add("PLUS", c1, x, npT)
+    c3 = ops.ewise_mult("TIMES", c2, y, npT)
+    c4 = ops.unop("ABS_SUB_C", c3, npT, 0.25)
+    c5 = ops.ewise_add("MAX", c4, z, npT)
+    return ops.reduce("PLUS", c5, np.float64), z, c5
+
+
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+@pytest.mark.parametrize("n", [1, 7, 4096, 100003])
+def test_chain_fused_vs_blocking_vs_oracle(nbg, ctx, bctx, T, n):
+    import inputs
+    npT = np.float32 if T == "fp32" else np.float64
+    x, y = inputs.uniform_vectors(n, 11, npT)
+    t = nbg.TYPE_OF[T]
+    outs = []
+    for c in (ctx, bctx):
+        s, z, c5, vx, vy = _chain(nbg, c, x, y, t)
+        outs.append((nbg.nbg_scalar_get(c, s), nbg.nbg_vector_export_dense(c, z), nbg.nbg_vector_export_dense(c, c5)))
+    so, zo, c5o = _chain_oracle(x, y, npT)
+    for sv, zv, c5v in outs:
+        assert np.array_equal(zv, zo) and np.array_equal(c5v, c5o)    # every element bit-exact (P11)
+        assert abs(sv - so) <= 1e-12 * abs(so)
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_chain_fusion_counters(nbg):
+    import inputs
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        x, y = inputs.uniform_vectors(1 << 16, 3, np.float32)
+        nbg.nbg_reset_stats(c)
+        s, z, c5, vx, vy = _chain(nbg, c, x, y, nbg.FP32)
+        nbg.nbg_vector_free(c, c5)
+        nbg.nbg_vector_free(c, z)
+        nbg.nbg_scalar_get(c, s)
+        st = nbg.nbg_get_stats(c)
+        assert st["kernels_launched"] == 1            # one fused pass (Figs. 1-2)
+        assert st["vectors_materialized"] == 0        # only the scalar: every intermediate elided
+        assert st["plans_built"] == 1
+        for _ in range(5):                            # same signature: cache hits only
+            s2, z2, c52, vx2, vy2 = _chain(nbg, c, x, y, nbg.FP32)
+            for h in (z2, c52, vx2, vy2):
+                nbg.nbg_vector_free(c, h)
+            nbg.nbg_scalar_get(c, s2)
+        st = nbg.nbg_get_stats(c)
+        assert st["plans_built"] == 1 and st["plan_hits"] == 5
+    finally:
+        nbg.nbg_finalize(c)
+
+
+def test_pagerank_steady_state_one_kernel_per_sweep(nbg):
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 14, 16, 1)
+        nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=10, type=nbg.FP32)   # warm-up: plans + hints
+        nbg.nbg_reset_stats(c)
+        r, sweeps, _ = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=10, type=nbg.FP32)
+        st = nbg.nbg_get_stats(c)
+        assert st["plans_built"] == 0 and st["jit_compiles"] == 0
+        # dinv once + first sweep's prologue (y1, ds1 from the iso r0) + one fused kernel per sweep
+        assert st["kernels_launched"] <= sweeps + 2, st
+        assert st["side_outputs"] >= 2 * (sweeps - 1)
+    finally:
+        nbg.nbg_finalize(c)
