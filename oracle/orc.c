@@ -3,7 +3,7 @@
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
  * leg may load this library.  It shares no code, header, table or constant generator with
- * the CUDA path in paper_2509_14211_b200/ and never includes or links anything from it.
+ * the CUDA product package and never includes or links anything from it.
  *
  * What it computes (each function cites the passage it follows):
  *   orc_sm64            SplitMix64 output k of a stream keyed by `key` (workload generator,

@@ -360,6 +360,8 @@ void gen_spmv(Gen &g, const std::string &kname) {
         default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
     }
     const int ACCW = (ACC == "double" || ACC == "long long") ? 2 : 1;   // 32-bit words of ACC
+    const int VTW = (VT == "double" || VT == "long long") ? 2 : 1;      // 32-bit words of a value slot
+    const std::string WO = "(o0 * " + std::to_string(VTW) + ")";
 
     o << "#define NBG_D_TILE_VALS 3136\n#define NBG_D_TILE_ROWS 2080\n#define NBG_CHUNK 2048\n";
     o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
@@ -449,9 +451,9 @@ void gen_spmv(Gen &g, const std::string &kname) {
     // park the row sum in the row's own (now consumed) value slots
     if (ACCW == 2)
         o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; const unsigned long long b_ = *(const unsigned long long*)&t; "
-             "w_[o0] = (unsigned)b_; w_[o0 + 1] = (unsigned)(b_ >> 32); }\n";
+             "w_[" + WO + "] = (unsigned)b_; w_[" + WO + " + 1] = (unsigned)(b_ >> 32); }\n";
     else
-        o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; w_[o0] = *(const unsigned*)&t; }\n";
+        o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; w_[" + WO + "] = *(const unsigned*)&t; }\n";
     o << "      }\n";
     o << "      __syncthreads();\n";
     o << "      for (int j = threadIdx.x; j < R; j += 256) {\n";
@@ -459,10 +461,10 @@ void gen_spmv(Gen &g, const std::string &kname) {
     o << "        " << ACC << " acc;\n";
     o << "        if (o1 - o0 > 32) {\n";
     if (ACCW == 2)
-        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned long long b_ = (unsigned long long)w_[o0] | ((unsigned long long)w_[o0 + 1] << 32); acc = *(const "
+        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned long long b_ = (unsigned long long)w_[" + WO + "] | ((unsigned long long)w_[" + WO + " + 1] << 32); acc = *(const "
           << ACC << "*)&b_;\n";
     else
-        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned b_ = w_[o0]; acc = *(const " << ACC << "*)&b_;\n";
+        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned b_ = w_[" + WO + "]; acc = *(const " << ACC << "*)&b_;\n";
     o << "        } else {\n";
     o << "          acc = " << IDENT << ";\n";
     o << "          for (int q = o0; q < o1; q++) acc = NBG_ADD(acc, (" << ACC << ")s_val[q]);\n";
