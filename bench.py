@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""bench.py -- fused nonblocking PageRank on B200 (BASELINE.json metric, config 4 by default).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c1|c3|c5]
+    python bench.py --impl reference ...      # the CPU oracle as the reference arm
+
+A step is one whole PageRank solve through the C ABI (nbg_pagerank: every SURVEY 8(a) row --
+setup of the reciprocal out-degrees, then fused sweeps until delta <= tol or itermax) on the
+resident graph.  value = GTEPS/iter = (nnz * sweeps) / time / 1e9 summed over the job.
+N > 1: one process per GPU (torchrun), 1-D row partition balanced by bytes, NCCL allgather-v of
+the scaled ranks and exact allreduce of delta / dangling mass each sweep (nbg_pagerank_dist);
+the same graph is split across ranks ("scaling": "strong").
+Timing: W untimed warm-up steps (JIT + plan cache + speculation hints), then K
+steps bracketed by barrier + synchronize, CUDA events on the launching stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import inputs  # noqa: E402
+
+METRIC = "PageRank GTEPS/iter (fused mxv+ewise+reduce); achieved HBM GB/s vs peak"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def graph_params(w):
+    c = inputs.CONFIGS[w]
+    return c
+
+
+def algorithmic_bytes(n, nnz, w):
+    """B_ns = 4 nnz + 8 (n+1) + 2 w n (colidx, rowptr, x once, y once);
+    B_fused = B_ns + 3 w n (t read, dinv read, y_next write)."""
+    b_ns = 4 * nnz + 8 * (n + 1) + 2 * w * n
+    return b_ns, b_ns + 3 * w * n
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2509_14211_b200 import nbg
+    stream = torch.cuda.current_stream()
+    ctx = nbg.nbg_init(nbg.NONBLOCKING, local_rank, stream.cuda_stream)
+    cfg = graph_params(args.workload)
+    T = nbg.FP32 if cfg["dtype"] == "fp32" else nbg.FP64
+    w = 4 if T == nbg.FP32 else 8
+    kind = nbg.GRAPH_RMAT if cfg["graph"] == "rmat" else nbg.GRAPH_ER
+    t0 = time.time()
+    A, deg = nbg.nbg_matrix_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed)
+    n = nbg.nbg_matrix_nrows(ctx, A)
+    nnz = nbg.nbg_matrix_nnz(ctx, A)
+    cuts = None
+    if world > 1:
+        uid = nbg.nbg_dist_unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        nbg.nbg_dist_init(ctx, rank, world, obj[0])
+        rp, _ = nbg.nbg_matrix_export_csr(ctx, A)
+        cuts = nbg.nbg_partition_rows(rp, world, 5 * w)
+        Ab = nbg.nbg_matrix_row_block(ctx, A, int(cuts[rank]), int(cuts[rank + 1]))
+        nbg.nbg_matrix_free(ctx, A)
+        A = Ab
+    setup_s = time.time() - t0
+    itermax, tol = cfg["itermax"], cfg["tol"]
+    dangling = nbg.PR_UNIFORM if cfg["dangling"] == "uniform" else nbg.PR_DROP
+
+    def step():
+        if world > 1:
+            r, s, h = nbg.nbg_pagerank_dist(ctx, A, deg, cuts, alpha=cfg["alpha"], tol=tol, itermax=itermax,
+                                            dangling=dangling, type=T)
+        else:
+            r, s, h = nbg.nbg_pagerank(ctx, A, deg, alpha=cfg["alpha"], tol=tol, itermax=itermax,
+                                       dangling=dangling, type=T)
+        nbg.nbg_vector_free(ctx, r)
+        return s, h
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st0 = nbg.nbg_get_stats(ctx)
+    clocks = Clocks(local_rank)
+    clocks.start()
+    nbg.nbg_set_timing(ctx, 1)
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    sweeps_total = 0
+    hist_last = None
+    for _ in range(args.steps):
+        s, hist_last = step()
+        sweeps_total += s
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    spmv_ms, spmv_n = nbg.nbg_get_timing(ctx, "spmv")
+    ewise_ms, ewise_n = nbg.nbg_get_timing(ctx, "ewise")
+    comm_ms, comm_n = nbg.nbg_get_timing(ctx, "comm")
+    nbg.nbg_set_timing(ctx, 0)
+    ck = clocks.stop()
+    st1 = nbg.nbg_get_stats(ctx)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = st1["kernels_launched"] - st0["kernels_launched"]
+
+    # ---------------- end-to-end through the public API with HOST buffers (N = 1)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        rp_h, ci_h = nbg.nbg_matrix_export_csr(ctx, A)
+        deg_h = nbg.nbg_vector_export_dense(ctx, deg)
+        rp_p = torch.from_numpy(rp_h).pin_memory()
+        ci_p = torch.from_numpy(ci_h).pin_memory()
+        dg_p = torch.from_numpy(deg_h).pin_memory()
+        out_p = torch.empty(n, dtype=torch.float32 if T == nbg.FP32 else torch.float64).pin_memory()
+
+        def e2e_step():
+            A2 = nbg.nbg_matrix_from_csr(ctx, n, n, rp_p.numpy(), ci_p.numpy(), type=nbg.FP32)
+            d2 = nbg.nbg_vector_from_dense(ctx, nbg.INT32, dg_p.numpy())
+            r, s, _ = nbg.nbg_pagerank(ctx, A2, d2, alpha=cfg["alpha"], tol=tol, itermax=itermax, dangling=dangling,
+                                       type=T)
+            nbg.nbg_vector_export_dense(ctx, r, out_p.numpy())
+            nbg.nbg_vector_free(ctx, r)
+            nbg.nbg_vector_free(ctx, d2)
+            nbg.nbg_matrix_free(ctx, A2)
+            return s
+
+        e2e_step()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        esw = 0
+        for _ in range(args.steps):
+            esw += e2e_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        e2e = {"value": nnz * esw / (ems * 1e-3) / 1e9, "unit": "GTEPS",
+               "h2d_bytes_per_step": int(rp_h.nbytes + ci_h.nbytes + deg_h.nbytes),
+               "d2h_bytes_per_step": int(out_p.numel() * out_p.element_size())}
+
+    result = None
+    if rank == 0:
+        b_ns, b_fused = algorithmic_bytes(n, nnz, w)
+        if world > 1:
+            b_ns, b_fused = b_ns / world, b_fused / world      # rank 0's share (roofline is per GPU)
+        pk, pk_src = peaks()
+        avg_spmv_s = (spmv_ms / spmv_n) * 1e-3 if spmv_n else float("nan")
+        achieved = b_ns / avg_spmv_s / 1e9
+        traffic = load_traffic(args.workload)
+        value = nnz * sweeps_total / (ms * 1e-3) / 1e9
+        result = {
+            "metric": METRIC,
+            "value": round(value, 3),
+            "unit": "GTEPS",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32" if T == nbg.FP32 else "f64",
+            "data": "synthetic",
+            "config": {
+                "workload": f"{args.workload}: {cfg['graph']} scale {cfg['scale']} ef {cfg['edge_factor']} seed {args.seed}",
+                "n": n, "nnz": nnz, "dangling": cfg["dangling"], "alpha": cfg["alpha"], "tol": tol,
+                "itermax": itermax, "sweeps_per_step": sweeps_total / args.steps,
+                "parallelism": f"rows{world}" if world > 1 else "single",
+                "l2": "no flush: colidx stream (%.0f MB) > L2 (126 MB) each sweep; the gathered vector "
+                      "stays L2-resident by design" % (4 * nnz / 1e6),
+                "setup_s": round(setup_s, 3),
+            },
+            "roofline": {
+                "bound": "hbm", "kernel": "fused SpMV sweep (nbg_spmv_*)",
+                "achieved": round(achieved, 1), "peak": pk, "peak_source": pk_src, "unit": "GB/s",
+                "frac": round(achieved / pk, 4), "traffic": traffic,
+                "bytes_per_launch_ns": int(b_ns), "bytes_per_launch_fused": int(b_fused),
+                "achieved_fused_gbs": round(b_fused / avg_spmv_s / 1e9, 1),
+                "avg_launch_us": round(avg_spmv_s * 1e6, 2), "launches": spmv_n,
+                "share_of_step": round(spmv_ms / ms, 4) if ms else None,
+            },
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "kernel_ms": {"spmv": round(spmv_ms, 3), "ewise": round(ewise_ms, 3), "comm": round(comm_ms, 3),
+                          "ewise_launches": ewise_n, "comm_launches": comm_n},
+            "planner": {k: st1[k] - st0[k] for k in ("plans_built", "plan_hits", "memo_hits", "side_outputs",
+                                                      "intermediates_elided", "waits")},
+            "host_plan_us_per_wait": round((st1["host_plan_ns"] - st0["host_plan_ns"]) / 1e3 /
+                                           max(1, st1["waits"] - st0["waits"]), 2),
+            "clocks": ck,
+        }
+    nbg.nbg_vector_free(ctx, deg)
+    nbg.nbg_matrix_free(ctx, A)
+    nbg.nbg_finalize(ctx)
+    if dist is not None:
+        dist.destroy_process_group()
+    return result
+
+
+# ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
+
+def oracle_graph(cfg, seed):
+    import oracle
+    f = oracle.rmat_edges if cfg["graph"] == "rmat" else oracle.er_edges
+    src, dst = f(cfg["scale"], cfg["edge_factor"], seed)
+    rp, ci, deg = oracle.build_csr(1 << cfg["scale"], src, dst)
+    del src, dst
+    return rp, ci, deg
+
+
+def oracle_sample(rp, ci, deg, cfg, sweeps):
+    """Time `sweeps` fixed sweeps of the oracle (Fig. 6, single thread) -> seconds."""
+    import oracle
+    dt = np.float32 if cfg["dtype"] == "fp32" else np.float64
+    t0 = time.perf_counter()
+    oracle.pagerank(rp, ci, deg, alpha=cfg["alpha"], dtype=dt, uniform=cfg["dangling"] == "uniform",
+                    itermax=sweeps, tol=-1.0)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(args):
+    cfg = graph_params(args.workload)
+    rp, ci, deg = oracle_graph(cfg, args.seed)
+    nnz = int(ci.shape[0])
+    sweeps = max(1, min(cfg["itermax"], int(args.cpu_sweeps)))
+    t = oracle_sample(rp, ci, deg, cfg, sweeps)
+    return {"value": round(nnz * sweeps / t / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "sample": f"{sweeps} fixed Fig. 6 sweeps of the single-threaded C oracle on the same graph "
+                      f"({nnz} edges), {t:.2f} s"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cfg = graph_params(args.workload)
+    rp, ci, deg = oracle_graph(cfg, args.seed)
+    nnz = int(ci.shape[0])
+    per = max(1, int(args.ref_sweeps))
+    for _ in range(args.warmup):
+        oracle_sample(rp, ci, deg, cfg, per)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += oracle_sample(rp, ci, deg, cfg, per)
+    value = nnz * per * args.steps / tot / 1e9
+    return {
+        "metric": METRIC, "value": round(value, 5), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg["dtype"] == "fp32" else "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.workload}: {cfg['graph']} scale {cfg['scale']} ef {cfg['edge_factor']} "
+                               f"seed {args.seed}", "n": int(rp.shape[0] - 1), "nnz": nnz,
+                   "step": f"{per} fixed sweeps of the CPU oracle (bounded sample of the workload)"},
+        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                         "sample": f"{per} sweeps x {args.steps} steps, single-threaded C oracle"},
+        "e2e": {"value": round(value, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c3", "c4", "c5"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-sweeps", type=int, default=3)
+    ap.add_argument("--ref-sweeps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "--gpus N>1 must be launched with torchrun"}))
+        sys.exit(2)
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+    else:
+        res = run_ours(args, rank, world, local_rank)
+        if rank == 0 and res is not None:
+            if world == 1 and not args.no_cpu_baseline:
+                res["cpu_baseline"] = cpu_baseline(args)
+            else:
+                res["cpu_baseline"] = None
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

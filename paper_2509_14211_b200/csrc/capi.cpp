@@ -313,13 +313,6 @@ nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64
     CHECK(own == NBG_COPY || own == NBG_BORROW, NBG_INVALID_VALUE, "bad ownership");
     CHECK(!(space == NBG_HOST && own == NBG_BORROW), NBG_INVALID_VALUE, "host memory cannot be borrowed");
     check_type(type);
-    if (space == NBG_HOST) {
-        CHECK(rowptr[0] == 0 && rowptr[nrows] == nnz, NBG_INVALID_VALUE, "rowptr must start at 0 and end at nnz");
-        for (int64_t i = 0; i < nrows; i++)
-            CHECK(rowptr[i + 1] >= rowptr[i], NBG_INVALID_VALUE, "rowptr not monotone");
-        for (int64_t p = 0; p < nnz; p++)
-            CHECK(colidx[p] >= 0 && colidx[p] < ncols, NBG_INDEX_OUT_OF_BOUNDS, "column index out of range");
-    }
     auto M = std::make_shared<Mat>();
     M->ctx = ctx;
     M->id = ctx->new_id();
@@ -331,6 +324,10 @@ nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64
     M->rowptr = upload(*ctx, rowptr, (size_t)(nrows + 1) * 8, space, own);
     M->colidx = upload(*ctx, colidx, (size_t)nnz * 4, space, own);
     if (vals) M->vals = upload(*ctx, vals, (size_t)nnz * type_size(type), space, own);
+    // structural validation on the device: row pointers and column range
+    int bad = gpu_validate_csr(*ctx, nrows, ncols, nnz, (const long long *)M->rowptr->d, (const int *)M->colidx->d);
+    if (bad & 1) fail(NBG_INVALID_VALUE, "rowptr must start at 0, end at nnz and be non-decreasing");
+    if (bad & 2) fail(NBG_INDEX_OUT_OF_BOUNDS, "column index out of range");
     *A = new nbg_matrix_s{ctx, M};
     API_END(ctx)
 }

@@ -131,6 +131,19 @@ __global__ void k_rebase(long long n, const long long *rp, long long base, long 
         out[i] = rp[i] - base;
 }
 
+// structural checks of a user CSR: bit0 rowptr ends/monotone, bit1 column index out of range
+__global__ void k_validate_csr(long long n, long long ncols, long long nnz, const long long *rp, const int *ci, int *bad) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
+        long long v = rp[i];
+        if ((i == 0 && v != 0) || (i == n && v != nnz) || (i < n && rp[i + 1] < v)) atomicOr(bad, 1);
+    }
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += stride) {
+        int c = ci[p];
+        if (c < 0 || c >= ncols) atomicOr(bad, 2);
+    }
+}
+
 template <class T>
 __global__ void k_fill(T *d, long long n, T v) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = v;
@@ -335,6 +348,18 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     }
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     A.plan = std::move(P);
+}
+
+int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci) {
+    BufP bad = alloc_buf(c, 4);
+    NBG_CUDA(cudaMemsetAsync(bad->d, 0, 4, c.stream));
+    k_validate_csr<<<grid_for(std::max(n + 1, nnz), c.num_sms), 256, 0, c.stream>>>(n, ncols, nnz, rp, ci, (int *)bad->d);
+    NBG_CUDA(cudaGetLastError());
+    int h = 0;
+    NBG_CUDA(cudaMemcpyAsync(&h, bad->d, 4, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    c.stats.kernels_launched++;
+    return h;
 }
 
 void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out) {

@@ -69,6 +69,7 @@ struct Buf {
     bool owned = true;
     uint64_t prod_sig = 0;     // signature hash of the region that wrote it (0 = none)
     int prod_out = -1;         // output index within that region
+    uint64_t prod_seq = 0;     // launch sequence number of that region
     ~Buf();
 };
 using BufP = std::shared_ptr<Buf>;
@@ -266,6 +267,7 @@ struct Ctx {
     bool own_stream = false;
     int num_sms = 148;
     uint64_t next_id = 1;
+    uint64_t launch_seq = 0;
     std::string last_error;
     nbg_status latched = NBG_SUCCESS;
     nbg_stats stats{};
@@ -324,6 +326,7 @@ void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_d
 MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out);
 void gpu_build_spmv_plan(Ctx &c, Mat &A);
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
+int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);
 void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out);
 void host_xacc_add(unsigned long long *limbs, double d);
 

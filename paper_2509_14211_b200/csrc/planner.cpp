@@ -154,8 +154,14 @@ static void learn_hint(Ctx &c, const NodeP &p) {
     std::vector<const Node *> prod;
     std::unordered_set<const Node *> seen;
     find_produced_leaves(p.get(), prod, seen);
-    if (prod.size() != 1) return;
+    if (prod.empty()) return;
+    // the loop-carried operand is the most recently produced buffer (e.g. the previous sweep's
+    // ranks); older products (dinv) are loop invariants and stay leaves of the template
     const Node *L = prod[0];
+    for (const Node *q : prod)
+        if (q->buf->prod_seq > L->buf->prod_seq) L = q;
+    for (const Node *q : prod)
+        if (q != L && q->buf->prod_seq == L->buf->prod_seq) return;   // ambiguous
     auto key = std::make_pair(L->buf->prod_sig, L->buf->prod_out);
     auto ph = std::make_shared<Node>();
     ph->op = Op::LEAF;
@@ -530,9 +536,11 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
         int64_t n = B.mxv ? B.mxv->A->nrows : root_len(roots[0]);
         size_t nvis = B.visited.size();
         run_region(c, B, hint_outs, n);
+        const uint64_t seq = ++c.launch_seq;
         for (int k = 0; k < nbase; k++) {
             B.out_nodes[k]->buf->prod_sig = base_hash;
             B.out_nodes[k]->buf->prod_out = k;
+            B.out_nodes[k]->buf->prod_seq = seq;
         }
         // memoise the side outputs under their structural key (R is materialised now)
         for (HintOut &h : hint_outs) {
