@@ -244,6 +244,9 @@ struct Hint {           // speculative loop-carried side output (planner rule 3,
     NodeP tmpl;         // pending template expression
     Node *placeholder;  // leaf inside tmpl standing for the region output
     NodeP ph_keep;
+    // the template's other vector leaves, held weakly: placeholder -> original leaf
+    std::vector<std::pair<NodeP, std::weak_ptr<Node>>> fixed;
+    std::string key;    // dedupe key (expression with the loop-carried leaf as "P")
 };
 
 struct TimingClass {
@@ -282,7 +285,9 @@ struct Ctx {
     struct MemoEntry {
         std::vector<std::weak_ptr<Buf>> deps;
         NodeP result;            // a materialised node
+        uint64_t stamp = 0;      // last use (LRU bound)
     };
+    uint64_t memo_clock = 0;
     std::unordered_map<std::string, MemoEntry> memo;
     // learned hints: producer signature hash + output index -> templates
     std::map<std::pair<uint64_t, int>, std::vector<Hint>> hints;

@@ -101,32 +101,79 @@ static void copy_result(Node &dst, const Node &src) {
     drop_inputs(dst);
 }
 
+static bool dbg() {
+    static int v = -1;
+    if (v < 0) v = getenv("NBG_DEBUG") && *getenv("NBG_DEBUG") ? 1 : 0;
+    return v == 1;
+}
+
 static bool memo_bind(Ctx &c, const NodeP &x) {
     if (x->mat) return true;
+    if (dbg()) fprintf(stderr, "[nbg] memo lookup %s (%zu entries)\n", node_key(x.get()).c_str(), c.memo.size());
     auto it = c.memo.find(node_key(x.get()));
     if (it == c.memo.end()) return false;
     for (auto &w : it->second.deps)
         if (w.expired()) return false;
     copy_result(*x, *it->second.result);
+    it->second.stamp = ++c.memo_clock;
     c.stats.memo_hits++;
     return true;
 }
 
+// Results are immutable and keyed by the identities of immutable leaves, so a memo entry stays
+// valid while its leaves live; the table is bounded (LRU) so it cannot pin unbounded memory.
+static const size_t MEMO_CAP = 64;
+static void memo_insert(Ctx &c, const std::string &k, const NodeP &result) {
+    std::vector<std::weak_ptr<Buf>> deps;
+    std::unordered_set<const Node *> seen;
+    // leaves of the expression: walk the (still attached) inputs of the result node
+    Node tmp = *result;
+    tmp.mat = false;
+    leaf_bufs(&tmp, deps, seen);
+    if (c.memo.size() >= MEMO_CAP) {
+        auto victim = c.memo.begin();
+        for (auto it = c.memo.begin(); it != c.memo.end(); ++it)
+            if (it->second.stamp < victim->second.stamp) victim = it;
+        c.memo.erase(victim);
+    }
+    c.memo[k] = Ctx::MemoEntry{deps, result, ++c.memo_clock};
+}
+
 // ---------------------------------------------------------------- cloning (hint templates)
 
-static NodeP clone_subst(Ctx &c, const NodeP &x, const Node *from, const NodeP &to,
-                         std::unordered_map<const Node *, NodeP> &seen) {
-    if (x.get() == from) return to;
-    if (x->mat) return x;
+// clone the pending part of x; `subst` maps leaves to replacements (pre-seeded in `seen`)
+static NodeP clone_subst(Ctx &c, const NodeP &x, std::unordered_map<const Node *, NodeP> &seen) {
     auto it = seen.find(x.get());
     if (it != seen.end()) return it->second;
+    if (x->mat) return x;
     auto y = std::make_shared<Node>(*x);
     y->uid = c.new_id();
     y->user_refs = 0;
-    if (x->a) y->a = clone_subst(c, x->a, from, to, seen);
-    if (x->b) y->b = clone_subst(c, x->b, from, to, seen);
+    if (x->a) y->a = clone_subst(c, x->a, seen);
+    if (x->b) y->b = clone_subst(c, x->b, seen);
     seen[x.get()] = y;
     return y;
+}
+
+static NodeP make_placeholder(Ctx &c, const Node *like) {
+    auto ph = std::make_shared<Node>();
+    ph->op = Op::LEAF;
+    ph->mat = true;
+    ph->kind = VKind::FULL;
+    ph->type = like->type;
+    ph->n = like->n;
+    ph->uid = c.new_id();
+    return ph;
+}
+
+static void full_leaves(const NodeP &x, std::vector<NodeP> &out, std::unordered_set<const Node *> &seen) {
+    if (!seen.insert(x.get()).second) return;
+    if (x->mat) {
+        if (!x->scalar && x->kind == VKind::FULL) out.push_back(x);
+        return;
+    }
+    if (x->a) full_leaves(x->a, out, seen);
+    if (x->b) full_leaves(x->b, out, seen);
 }
 
 // a template can be instantiated inside another region only if it needs no prerequisite
@@ -163,21 +210,49 @@ static void learn_hint(Ctx &c, const NodeP &p) {
     for (const Node *q : prod)
         if (q != L && q->buf->prod_seq == L->buf->prod_seq) return;   // ambiguous
     auto key = std::make_pair(L->buf->prod_sig, L->buf->prod_out);
-    auto ph = std::make_shared<Node>();
-    ph->op = Op::LEAF;
-    ph->mat = true;
-    ph->kind = VKind::FULL;
-    ph->type = L->type;
-    ph->n = L->n;
-    ph->uid = c.new_id();
-    std::unordered_map<const Node *, NodeP> cs;
-    NodeP t = clone_subst(c, p, L, ph, cs);
-    std::string k = node_key(t.get(), ph.get());
+    const std::string k = node_key(p.get(), L);
     auto &vec = c.hints[key];
+    // drop hints whose loop-invariant leaves died (e.g. a previous run's dinv)
+    vec.erase(std::remove_if(vec.begin(), vec.end(),
+                             [](const Hint &h) {
+                                 for (auto &f : h.fixed)
+                                     if (f.second.expired()) return true;
+                                 return false;
+                             }),
+              vec.end());
     for (auto &h : vec)
-        if (node_key(h.tmpl.get(), h.placeholder) == k) return;
+        if (h.key == k) return;
     if (vec.size() >= 4) return;
-    vec.push_back(Hint{t, ph.get(), ph});
+    Hint h;
+    h.key = k;
+    std::unordered_map<const Node *, NodeP> cs;
+    h.ph_keep = make_placeholder(c, L);
+    h.placeholder = h.ph_keep.get();
+    cs[L] = h.ph_keep;
+    std::vector<NodeP> leaves;
+    std::unordered_set<const Node *> sl;
+    full_leaves(p, leaves, sl);
+    for (const NodeP &q : leaves) {
+        if (q.get() == L) continue;
+        NodeP px = make_placeholder(c, q.get());
+        cs[q.get()] = px;
+        h.fixed.push_back({px, std::weak_ptr<Node>(q)});
+    }
+    h.tmpl = clone_subst(c, p, cs);
+    if (dbg()) fprintf(stderr, "[nbg] learn hint sig=%llx out=%d tmpl=%s\n", (unsigned long long)key.first, key.second, k.c_str());
+    vec.push_back(std::move(h));
+}
+
+// instantiate a hint over the region output R (nullptr if a loop-invariant leaf died)
+static NodeP instantiate(Ctx &c, const Hint &h, const NodeP &R) {
+    std::unordered_map<const Node *, NodeP> cs;
+    cs[h.placeholder] = R;
+    for (auto &f : h.fixed) {
+        NodeP q = f.second.lock();
+        if (!q) return nullptr;
+        cs[f.first.get()] = q;
+    }
+    return clone_subst(c, h.tmpl, cs);
 }
 
 // ---------------------------------------------------------------- region builder
@@ -523,8 +598,8 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
                 auto h = c.hints.find({base_hash, o});
                 if (h == c.hints.end()) continue;
                 for (const Hint &hint : h->second) {
-                    std::unordered_map<const Node *, NodeP> cs;
-                    NodeP inst = clone_subst(c, hint.tmpl, hint.placeholder, B.out_nodes[o], cs);
+                    NodeP inst = instantiate(c, hint, B.out_nodes[o]);
+                    if (!inst) continue;
                     bool added = inst->scalar ? B.add_reduction(inst) : B.add_vector_output(inst);
                     if (!added || !B.prereq.empty()) fail(NBG_PANIC, "planner: hint needs a prerequisite");
                     hint_outs.push_back(HintOut{inst});
@@ -535,6 +610,11 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
 
         int64_t n = B.mxv ? B.mxv->A->nrows : root_len(roots[0]);
         size_t nvis = B.visited.size();
+        // structural keys of the base outputs (before they become leaves)
+        std::vector<std::string> base_keys;
+        if (nb) {
+            for (int k = 0; k < nbase; k++) base_keys.push_back(node_key(B.out_nodes[k].get()));
+        }
         run_region(c, B, hint_outs, n);
         const uint64_t seq = ++c.launch_seq;
         for (int k = 0; k < nbase; k++) {
@@ -542,16 +622,17 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
             B.out_nodes[k]->buf->prod_out = k;
             B.out_nodes[k]->buf->prod_seq = seq;
         }
-        // memoise the side outputs under their structural key (R is materialised now)
-        for (HintOut &h : hint_outs) {
-            std::vector<std::weak_ptr<Buf>> deps;
-            std::unordered_set<const Node *> seen;
-            // key over the template structure: leaves are materialised nodes
-            Node tmp = *h.node;
-            tmp.mat = false;   // the key describes the expression, not its result
-            std::string k = node_key(&tmp);
-            leaf_bufs(&tmp, deps, seen);
-            c.memo[k] = Ctx::MemoEntry{deps, h.node};
+        if (nb) {
+            // memoise every result (common subexpressions across waits, e.g. dinv across runs)
+            for (int k = 0; k < nbase; k++) memo_insert(c, base_keys[k], B.out_nodes[k]);
+            // side outputs are keyed with R already materialised (the next sweep's lookup key)
+            for (HintOut &h : hint_outs) {
+                Node tmp = *h.node;
+                tmp.mat = false;
+                std::string k = node_key(&tmp);
+                if (dbg()) fprintf(stderr, "[nbg] memo insert %s\n", k.c_str());
+                memo_insert(c, k, h.node);
+            }
         }
         // elided intermediates = visited pending nodes that were not stored
         size_t stored = 0;
