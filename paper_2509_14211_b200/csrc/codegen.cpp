@@ -49,7 +49,7 @@ std::string Prog::signature() const {
         s << (int)i.k << ":" << i.t << ":" << i.code << ":" << i.a << ":" << i.b << ":" << i.imm0 << ":" << i.imm1
           << ":" << i.slot << ":" << (int)i.fmt << ";";
     s << "|";
-    for (const OutV &o : outs) s << o.ins << ">" << o.out << ";";
+    for (const OutV &o : outs) s << o.ins << ">" << o.out << (o.scatter ? "s" : "") << ";";
     s << "|";
     for (const RedOut &r : reds) s << r.ins << ">" << r.monoid << ":" << r.racc << ":" << (int)r.fmt << ";";
     s << "|" << n_in << "," << n_out << "," << n_imm << "," << n_sin << "," << n_red;
@@ -64,6 +64,17 @@ struct Gen {
     explicit Gen(const Prog &pp) : p(pp) {}
 
     std::string v(int i) const { return "v" + std::to_string(i); }
+
+    // store of output ov at element index `idx` (plain, or scattered through a.oscat)
+    std::string scat(const OutV &ov, const std::string &idx) const {
+        const std::string o = std::to_string(ov.out);
+        return std::string("{ const int d_ = a.oscat[") + o + "][" + idx + "]; if (d_ >= 0) ((" + ctype(p.ins[ov.ins].t) +
+               "*)a.out[" + o + "])[d_] = " + v(ov.ins) + "; }";
+    }
+    std::string store(const OutV &ov, const std::string &idx) const {
+        if (ov.scatter) return scat(ov, idx);
+        return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[" + idx + "] = " + v(ov.ins) + ";";
+    }
 
     std::string cvt(int to, const std::string &x) const {
         if (to == NBG_BOOL) return "((unsigned char)((" + x + ") != 0))";
@@ -273,7 +284,8 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     for (const Ins &in : p.ins)
         if (in.k == Ins::LD_VEC) slot_type[in.slot] = in.t;
     std::vector<int> out_type(p.n_out, -1);
-    for (const OutV &ov : p.outs) out_type[ov.out] = p.ins[ov.ins].t;
+    for (const OutV &ov : p.outs)
+        if (!ov.scatter) out_type[ov.out] = p.ins[ov.ins].t;
 
     o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
     o << "  __shared__ double nbg_sh[32];\n";
@@ -295,7 +307,10 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
         o << "    #pragma unroll\n    for (int e = 0; e < 4; e++) {\n";
         g.emit_body(
             "      ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
-            [&](const OutV &ov) { return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";"; },
+            [&](const OutV &ov) {
+                if (ov.scatter) return g.scat(ov, "(vi * 4 + e)");
+                return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
+            },
             [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
         o << "    }\n";
         for (int k = 0; k < p.n_out; k++)
@@ -306,9 +321,7 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     g.emit_body(
         "    ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
-        [&](const OutV &ov) {
-            return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[i] = " + g.v(ov.ins) + ";";
-        },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
     o << "  }\n";
     g.emit_red_finish();
@@ -416,9 +429,7 @@ void gen_spmv(Gen &g, const std::string &kname) {
     g.emit_body(
         "          ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
-        [&](const OutV &ov) {
-            return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[i] = " + g.v(ov.ins) + ";";
-        },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_direct(p.reds[j], g.v(p.reds[j].ins)); }, "acc");
     o << "        }\n";
     o << "      }\n";
@@ -473,9 +484,7 @@ void gen_spmv(Gen &g, const std::string &kname) {
     g.emit_body(
         "        ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
-        [&](const OutV &ov) {
-            return std::string("((") + ctype(p.ins[ov.ins].t) + "*)a.out[" + std::to_string(ov.out) + "])[i] = " + g.v(ov.ins) + ";";
-        },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
     o << "      }\n";
     o << "      __syncthreads();\n";

@@ -144,6 +144,34 @@ __global__ void k_validate_csr(long long n, long long ncols, long long nnz, cons
     }
 }
 
+// ---- column relabel (gather layout)
+__global__ void k_col_count(long long nnz, const int *ci, int *cnt) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[ci[p]], 1);
+}
+// sort key: descending count, empty columns last (stable radix sort keeps ascending id on ties)
+__global__ void k_col_keys(long long nc, const int *cnt, unsigned *key, int *ids, int *nonempty) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < nc; j += (long long)gridDim.x * blockDim.x) {
+        int c = cnt[j];
+        key[j] = c > 0 ? ~(unsigned)c : 0xffffffffu;
+        ids[j] = (int)j;
+        if (c > 0) atomicAdd(nonempty, 1);
+    }
+}
+__global__ void k_perm_from_order(long long ng, const int *order, int *perm) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < ng; k += (long long)gridDim.x * blockDim.x)
+        perm[order[k]] = (int)k;
+}
+__global__ void k_map_cols(long long nnz, const int *ci, const int *perm, int *out) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x)
+        out[p] = perm[ci[p]];
+}
+template <class T>
+__global__ void k_permute(const T *x, T *xg, const int *iperm, long long ng) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < ng; k += (long long)gridDim.x * blockDim.x)
+        xg[k] = x[iperm[k]];
+}
+
 template <class T>
 __global__ void k_fill(T *d, long long n, T v) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) d[i] = v;
@@ -346,8 +374,59 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         NBG_CUDA(cudaMemsetAsync(P->counters->d, 0, (size_t)L * 4, c.stream));
         P->partials = alloc_buf(c, (size_t)nch_total * 8);
     }
+    // gather layout: relabel columns by descending count (big matrices only)
+    const char *rl = getenv("NBG_RELABEL");
+    const bool want = rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15));
+    if (want && A.nnz > 0 && !A.vals) {
+        const long long nc = A.ncols;
+        BufP cnt = alloc_buf(c, (size_t)nc * 4);
+        NBG_CUDA(cudaMemsetAsync(cnt->d, 0, (size_t)nc * 4, c.stream));
+        k_col_count<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (int *)cnt->d);
+        BufP key = alloc_buf(c, (size_t)nc * 4), key2 = alloc_buf(c, (size_t)nc * 4);
+        BufP ids = alloc_buf(c, (size_t)nc * 4), ids2 = alloc_buf(c, (size_t)nc * 4);
+        BufP ne = alloc_buf(c, 4);
+        NBG_CUDA(cudaMemsetAsync(ne->d, 0, 4, c.stream));
+        k_col_keys<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (unsigned *)key->d, (int *)ids->d,
+                                                                  (int *)ne->d);
+        size_t tb3 = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb3, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
+                                        (int *)ids2->d, (int64_t)nc, 0, 32, c.stream);
+        BufP t3 = alloc_buf(c, std::max<size_t>(tb3, 16));
+        NBG_CUDA(cub::DeviceRadixSort::SortPairs(t3->d, tb3, (const unsigned *)key->d, (unsigned *)key2->d,
+                                                 (const int *)ids->d, (int *)ids2->d, (int64_t)nc, 0, 32, c.stream));
+        int ng = 0;
+        NBG_CUDA(cudaMemcpyAsync(&ng, ne->d, 4, cudaMemcpyDeviceToHost, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+        P->perm = alloc_buf(c, (size_t)nc * 4);
+        NBG_CUDA(cudaMemsetAsync(P->perm->d, 0xff, (size_t)nc * 4, c.stream));
+        P->iperm = alloc_buf(c, (size_t)std::max(ng, 1) * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->iperm->d, ids2->d, (size_t)ng * 4, cudaMemcpyDeviceToDevice, c.stream));
+        k_perm_from_order<<<grid_for(ng, c.num_sms), 256, 0, c.stream>>>(ng, (const int *)ids2->d, (int *)P->perm->d);
+        P->colidx_g = alloc_buf(c, (size_t)A.nnz * 4);
+        k_map_cols<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (const int *)P->perm->d,
+                                                                     (int *)P->colidx_g->d);
+        NBG_CUDA(cudaGetLastError());
+        P->ncols_g = ng;
+        P->relabel = true;
+        c.stats.kernels_launched += 5;
+    }
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     A.plan = std::move(P);
+}
+
+void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng) {
+    if (ng <= 0) return;
+    int g = grid_for(ng, c.num_sms);
+    cudaEvent_t ev0;
+    timing_begin(c, "ewise", &ev0);
+    switch (type_size(type)) {
+        case 1: k_permute<unsigned char><<<g, 256, 0, c.stream>>>((const unsigned char *)x, (unsigned char *)xg, iperm, ng); break;
+        case 4: k_permute<int><<<g, 256, 0, c.stream>>>((const int *)x, (int *)xg, iperm, ng); break;
+        default: k_permute<long long><<<g, 256, 0, c.stream>>>((const long long *)x, (long long *)xg, iperm, ng); break;
+    }
+    NBG_CUDA(cudaGetLastError());
+    timing_end(c, "ewise", ev0);
+    c.stats.kernels_launched++;
 }
 
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci) {

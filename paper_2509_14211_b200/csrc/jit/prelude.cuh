@@ -30,6 +30,7 @@ struct KArgs {
     double *partials;
     long long ntiles, nchunks;
     long long row_offset;
+    const int *oscat[NBG_MAX_OUT];
 };
 
 // ------------------------------------------------------------------ operators in type T

@@ -125,6 +125,14 @@ struct SpmvPlan {
     BufP partials;   // double[nchunks]
     int max_tile_vals = 0;   // max nonzeros in one tile (shared-memory bound)
     int max_tile_rows = 0;
+    // Gather layout: columns renumbered by descending column count,
+    // empty columns dropped.  The gathered vector is stored in that order so the hot entries are
+    // dense (cache-line reuse) while every row keeps its summation order (bit-identical sums).
+    bool relabel = false;
+    int64_t ncols_g = 0;     // number of non-empty columns
+    BufP colidx_g;           // int32[nnz]  relabelled column indices
+    BufP perm;               // int32[ncols] old -> new id, -1 for an empty column
+    BufP iperm;              // int32[ncols_g] new -> old id
 };
 
 struct Mat {
@@ -185,7 +193,7 @@ struct Ins {
     bool uniform = false;   // value independent of the element index
 };
 
-struct OutV { int ins; int out; };
+struct OutV { int ins; int out; bool scatter = false; };   // scatter: out[oscat[i]] (skip < 0)
 struct RedOut { int ins; int monoid; int racc; uint8_t fmt; };
 
 struct SpmvSig {
@@ -228,6 +236,7 @@ struct KArgs {
     double *partials;
     long long ntiles, nchunks;
     long long row_offset;    // global index of local row 0 (distributed); 0 otherwise
+    const int *oscat[MAX_OUT];   // per output: scatter map (gather layout) or null
 };
 
 struct Kernel {
@@ -247,6 +256,7 @@ struct Hint {           // speculative loop-carried side output (planner rule 3,
     // the template's other vector leaves, held weakly: placeholder -> original leaf
     std::vector<std::pair<NodeP, std::weak_ptr<Node>>> fixed;
     std::string key;    // dedupe key (expression with the loop-carried leaf as "P")
+    std::weak_ptr<Mat> consumer;   // mxv whose gather input this expression was (layout of the output)
 };
 
 struct TimingClass {
@@ -331,6 +341,7 @@ void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_d
 MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out);
 void gpu_build_spmv_plan(Ctx &c, Mat &A);
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
+void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng);
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);
 void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out);
 void host_xacc_add(unsigned long long *limbs, double d);

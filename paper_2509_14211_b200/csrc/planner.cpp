@@ -130,6 +130,7 @@ static void memo_insert(Ctx &c, const std::string &k, const NodeP &result) {
     Node tmp = *result;
     tmp.mat = false;
     leaf_bufs(&tmp, deps, seen);
+    if (deps.empty() && result->a) leaf_bufs(result->a.get(), deps, seen);
     if (c.memo.size() >= MEMO_CAP) {
         auto victim = c.memo.begin();
         for (auto it = c.memo.begin(); it != c.memo.end(); ++it)
@@ -196,7 +197,7 @@ static void find_produced_leaves(const Node *x, std::vector<const Node *> &out, 
     if (x->b) find_produced_leaves(x->b.get(), out, seen);
 }
 
-static void learn_hint(Ctx &c, const NodeP &p) {
+static void learn_hint(Ctx &c, const NodeP &p, const MatP &consumer) {
     if (!fusable_template(p.get(), true)) return;
     std::vector<const Node *> prod;
     std::unordered_set<const Node *> seen;
@@ -225,6 +226,7 @@ static void learn_hint(Ctx &c, const NodeP &p) {
     if (vec.size() >= 4) return;
     Hint h;
     h.key = k;
+    h.consumer = consumer;
     std::unordered_map<const Node *, NodeP> cs;
     h.ph_keep = make_placeholder(c, L);
     h.placeholder = h.ph_keep.get();
@@ -255,6 +257,38 @@ static NodeP instantiate(Ctx &c, const Hint &h, const NodeP &R) {
     return clone_subst(c, h.tmpl, cs);
 }
 
+static NodeP memo_get(Ctx &c, const std::string &k) {
+    auto it = c.memo.find(k);
+    if (it == c.memo.end()) return nullptr;
+    for (auto &w : it->second.deps)
+        if (w.expired()) return nullptr;
+    it->second.stamp = ++c.memo_clock;
+    c.stats.memo_hits++;
+    return it->second.result;
+}
+
+static std::string perm_key(const Mat &A, const Node *u) {
+    return "PERM" + std::to_string(A.id) + "(" + node_key(u) + ")";
+}
+
+// x in the matrix's gather layout: xg[k] = x[iperm[k]] (a static permute kernel), memoised
+static NodeP permuted_view(Ctx &c, Mat &A, const NodeP &u, const std::string &pk) {
+    auto g = std::make_shared<Node>();
+    g->op = Op::LEAF;
+    g->type = u->type;
+    g->n = A.plan->ncols_g;
+    g->uid = c.new_id();
+    g->kind = VKind::FULL;
+    g->buf = alloc_buf(c, (size_t)A.plan->ncols_g * type_size(u->type));
+    if (u->kind == VKind::ISO) gpu_fill_iso(c, g->buf->d, u->type, A.plan->ncols_g, u->iso);
+    else gpu_permute(c, u->buf->d, g->buf->d, u->type, (const int *)A.plan->iperm->d, A.plan->ncols_g);
+    g->a = u;            // the memo entry depends on u's leaves
+    g->mat = true;
+    if (c.mode == NBG_NONBLOCKING) memo_insert(c, pk, g);
+    g->a.reset();
+    return g;
+}
+
 // ---------------------------------------------------------------- region builder
 
 struct Builder {
@@ -269,6 +303,8 @@ struct Builder {
     std::vector<NodeP> prereq;
     std::unordered_set<const Node *> prereq_set;
     NodeP mxv;
+    BufP mxv_x;                        // the gathered vector (in the matrix's gather layout)
+    std::unordered_map<const Node *, MatP> need_mx;   // prerequisite -> the mxv that gathers it
     std::vector<NodeP> visited;        // pending nodes of the region
     std::vector<NodeP> out_nodes;      // vector outputs, index = out slot
     std::vector<NodeP> red_nodes;      // reductions, index = racc slot
@@ -374,8 +410,22 @@ struct Builder {
                 case Op::MXV: {
                     if (mxv && mxv.get() != x.get()) { need(x); return -1; }
                     const NodeP &u = x->a;
-                    if (!u->mat) { need(u); return -1; }
-                    if (u->kind == VKind::ISO) ensure_full(c, u);
+                    Mat &A = *x->A;
+                    if (!A.plan) gpu_build_spmv_plan(c, A);
+                    if (A.plan->relabel) {
+                        // gather input in the relabelled layout: a memoised permuted view of u
+                        const std::string pk = perm_key(A, u.get());
+                        NodeP gx = memo_get(c, pk);
+                        if (!gx) {
+                            if (!u->mat) { need(u); need_mx[u.get()] = x->A; return -1; }
+                            gx = permuted_view(c, A, u, pk);
+                        }
+                        mxv_x = gx->buf;
+                    } else {
+                        if (!u->mat) { need(u); need_mx[u.get()] = x->A; return -1; }
+                        if (u->kind == VKind::ISO) ensure_full(c, u);
+                        mxv_x = u->kind == VKind::ISO ? u->full_cache : u->buf;
+                    }
                     mxv = x;
                     Ins in{};
                     in.k = Ins::MXV_ACC;
@@ -395,13 +445,17 @@ struct Builder {
         return r;
     }
 
-    // returns false if prerequisites are missing
-    bool add_vector_output(const NodeP &x) {
+    // returns false if prerequisites are missing; scatter_perm: store out[perm[i]] (gather layout)
+    std::vector<MatP> out_scatter;     // per output: matrix whose gather layout it is written in
+    bool add_vector_output(const NodeP &x, const MatP &scatter = nullptr) {
         if (is_out.count(x.get())) return true;
         int i = emit(x);
         if (i < 0) return false;
-        prog.outs.push_back(OutV{i, (int)out_nodes.size()});
+        OutV ov{i, (int)out_nodes.size()};
+        ov.scatter = (bool)scatter;
+        prog.outs.push_back(ov);
         out_nodes.push_back(x);
+        out_scatter.push_back(scatter);
         is_out.insert(x.get());
         return true;
     }
@@ -443,6 +497,7 @@ void ensure_full(Ctx &c, const NodeP &v) {
 
 struct HintOut {
     NodeP node;       // instantiated template root (pending until launch)
+    MatP scatter;     // written in this matrix's gather layout (memo key PERM<A>(...))
 };
 
 static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int64_t n) {
@@ -464,7 +519,10 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     std::vector<BufP> obufs;
     for (int k = 0; k < p.n_out; k++) {
         const NodeP &x = B.out_nodes[k];
-        BufP b = alloc_buf(c, (size_t)n * type_size(x->type));
+        const MatP &sc = B.out_scatter[k];
+        int64_t len = sc ? sc->plan->ncols_g : n;
+        BufP b = alloc_buf(c, (size_t)len * type_size(x->type));
+        if (sc) args.oscat[k] = (const int *)sc->plan->perm->d;
         obufs.push_back(b);
         args.out[k] = b->d;
         c.stats.vectors_materialized++;
@@ -499,9 +557,9 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         B.imm[0] = A.iso;
         B.imm[1] = mx.c0;
         args.rowptr = (const long long *)A.rowptr->d;
-        args.colidx = (const int *)A.colidx->d;
+        args.colidx = (const int *)(A.plan->relabel ? A.plan->colidx_g->d : A.colidx->d);
         args.aval = A.vals ? A.vals->d : nullptr;
-        args.x = (u->kind == VKind::ISO) ? u->full_cache->d : u->buf->d;
+        args.x = B.mxv_x->d;
         args.tiles = (const int *)(A.plan->tiles ? A.plan->tiles->d : nullptr);
         args.chunks = (const int *)(A.plan->chunks ? A.plan->chunks->d : nullptr);
         args.longs = (const int *)(A.plan->longs ? A.plan->longs->d : nullptr);
@@ -571,7 +629,10 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
             for (const NodeP &p : B.prereq) {
                 if (p->mat) continue;
                 if (nb && memo_bind(c, p)) continue;
-                if (nb) learn_hint(c, p);
+                if (nb) {
+                    auto cm = B.need_mx.find(p.get());
+                    learn_hint(c, p, cm == B.need_mx.end() ? nullptr : cm->second);
+                }
                 todo.push_back(p);
             }
             if (!todo.empty()) materialize(c, todo);
@@ -600,9 +661,18 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
                 for (const Hint &hint : h->second) {
                     NodeP inst = instantiate(c, hint, B.out_nodes[o]);
                     if (!inst) continue;
-                    bool added = inst->scalar ? B.add_reduction(inst) : B.add_vector_output(inst);
+                    MatP cons = hint.consumer.lock();
+                    MatP scat;
+                    if (cons && !inst->scalar) {
+                        if (!cons->plan) gpu_build_spmv_plan(c, *cons);
+                        if (cons->plan->relabel) {
+                            if (cons->ncols != inst->n) continue;
+                            scat = cons;
+                        }
+                    }
+                    bool added = inst->scalar ? B.add_reduction(inst) : B.add_vector_output(inst, scat);
                     if (!added || !B.prereq.empty()) fail(NBG_PANIC, "planner: hint needs a prerequisite");
-                    hint_outs.push_back(HintOut{inst});
+                    hint_outs.push_back(HintOut{inst, scat});
                     c.stats.side_outputs++;
                 }
             }
@@ -630,6 +700,7 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
                 Node tmp = *h.node;
                 tmp.mat = false;
                 std::string k = node_key(&tmp);
+                if (h.scatter) k = "PERM" + std::to_string(h.scatter->id) + "(" + k + ")";
                 if (dbg()) fprintf(stderr, "[nbg] memo insert %s\n", k.c_str());
                 memo_insert(c, k, h.node);
             }

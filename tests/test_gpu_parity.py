@@ -307,3 +307,32 @@ def test_pagerank_steady_state_one_kernel_per_sweep(nbg):
         assert st["side_outputs"] >= 2 * (sweeps - 1)
     finally:
         nbg.nbg_finalize(c)
+
+
+# ------------------------------------------------------------------ gather layout (column relabel)
+
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+def test_relabel_is_bit_exact(nbg, T, monkeypatch):
+    """The degree-sorted gather layout keeps every row's summation order: results with and
+    without it are identical bit for bit."""
+    t = nbg.TYPE_OF[T]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("NBG_RELABEL", flag)
+        c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+        try:
+            A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 13, 16, 4)
+            res = []
+            for _ in range(2):          # second run uses the speculative scattered side output
+                r, s, h = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=12, type=t)
+                res.append((nbg.nbg_vector_export_dense(c, r), h))
+            x = nbg.nbg_vector_from_dense(c, t, np.linspace(0, 1, 1 << 13).astype(nbg.NP_OF[t]))
+            m = nbg.nbg_mxv(c, t, "PLUS", "SECOND", A, x)
+            out[flag] = (res, nbg.nbg_vector_export_dense(c, m), nbg.nbg_get_stats(c))
+        finally:
+            nbg.nbg_finalize(c)
+    for (r0, h0), (r1, h1) in zip(out["0"][0], out["1"][0]):
+        assert np.array_equal(r0, r1)
+        assert np.array_equal(h0, h1) if T == "fp32" else rel(h0, h1) <= 1e-12
+    assert np.array_equal(out["0"][1], out["1"][1])
+    assert out["1"][2]["side_outputs"] > 0
