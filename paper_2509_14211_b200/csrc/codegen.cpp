@@ -328,15 +328,18 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     o << "}\n";
 }
 
-void gen_spmv(Gen &g, const std::string &kname) {
+// SpMV skeleton v2: one CTA per SM of NBG_GROUPS x 256 threads.  Each
+// 256-thread group works independently on its own items (named barriers), all groups share a
+// hot-column cache in shared memory: the first `hc` entries of the gathered vector, which in the
+// degree-sorted gather layout are the most frequently gathered columns.  Returns the dynamic
+// shared memory the kernel needs.
+int gen_spmv(Gen &g, const std::string &kname) {
     const Prog &p = g.p;
     auto &o = g.o;
     const SpmvSig &sp = p.sp;
-    const char *T = ctype(sp.T);
     const char *C = ctype_compute(sp.T);
-    // value type of the gathered products kept in shared memory
-    std::string VT = C;
-    // accumulator
+    const char *XT = ctype(sp.xt);
+    std::string VT = C;   // type of the gathered products kept in shared memory
     std::string ACC, IDENT, ADD;
     bool fT = is_float(sp.T);
     if (sp.add == NBG_PLUS) {
@@ -354,7 +357,6 @@ void gen_spmv(Gen &g, const std::string &kname) {
                    : (sp.T == NBG_INT32 ? "((int)0x80000000)" : "((long long)0x8000000000000000ull)");
         ADD = "nbg_max(A_, B_)";
     }
-    // mul(A(i,j), x(j)) in the compute type of T
     std::string av = sp.has_vals ? std::string("((") + C + ")(((const " + ctype(sp.at) + "*)a.aval)[P_]))"
                                  : std::string("((") + C + ")(a.imm[0]))";
     std::string xv = std::string("((") + C + ")(X_))";
@@ -375,55 +377,70 @@ void gen_spmv(Gen &g, const std::string &kname) {
     const int ACCW = (ACC == "double" || ACC == "long long") ? 2 : 1;   // 32-bit words of ACC
     const int VTW = (VT == "double" || VT == "long long") ? 2 : 1;      // 32-bit words of a value slot
     const std::string WO = "(o0 * " + std::to_string(VTW) + ")";
+    const int GROUPS = 4, VALS = 3136, ROWS = 2080;
+    const int vt_bytes = VTW * 4;
+    const int grp_bytes = VALS * vt_bytes + (ROWS + 1) * 4;
+    const int x_bytes = (int)type_size(sp.xt);
+    const int static_reserve = 2048;   // static shared memory + driver reserve
+    int hot_bytes = 227 * 1024 - static_reserve - GROUPS * grp_bytes;
+    int hot_cap = hot_bytes / x_bytes;
+    hot_cap = (hot_cap / 4) * 4;
+    if (hot_cap > 32768) hot_cap = 32768;
+    if (hot_cap < 0) hot_cap = 0;
+    const int dyn_bytes = hot_cap * x_bytes + GROUPS * grp_bytes;
 
-    o << "#define NBG_D_TILE_VALS 3136\n#define NBG_D_TILE_ROWS 2080\n#define NBG_CHUNK 2048\n";
+    o << "#define NBG_GROUPS " << GROUPS << "\n#define NBG_D_TILE_VALS " << VALS << "\n#define NBG_D_TILE_ROWS " << ROWS
+      << "\n#define NBG_HOT_CAP " << hot_cap << "\n";
     o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
-    o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << ctype(sp.xt) << " X_) { return "
-      << mul << "; }\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
-    o << "  __shared__ " << VT << " s_val[NBG_D_TILE_VALS];\n";
-    o << "  __shared__ int s_off[NBG_D_TILE_ROWS + 1];\n";
-    o << "  __shared__ int s_med[NBG_D_TILE_ROWS];\n";
-    o << "  __shared__ int s_nmed, s_flag;\n";
+    o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << XT << " X_) { return " << mul
+      << "; }\n";
+    o << "__device__ __forceinline__ void nbg_gbar(int g) { asm volatile(\"bar.sync %0, 256;\" :: \"r\"(g + 1) : \"memory\"); }\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << GROUPS * 256 << ", 1) " << kname << "(const KArgs a) {\n";
+    o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
     o << "  __shared__ double nbg_sh[32];\n";
-    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    o << "  const " << ctype(sp.xt) << "* __restrict__ X = (const " << ctype(sp.xt) << "*)a.x;\n";
+    o << "  __shared__ double nbg_shg[NBG_GROUPS][8];\n";
+    o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
+    o << "  const int g = threadIdx.x >> 8, gt = threadIdx.x & 255, lane = threadIdx.x & 31, wg = gt >> 5;\n";
+    o << "  " << VT << "* s_val = (" << VT << "*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + g * " << grp_bytes << ");\n";
+    o << "  int* s_off = (int*)((unsigned char*)s_val + NBG_D_TILE_VALS * sizeof(" << VT << "));\n";
+    o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
+    o << "  const int hc = (int)a.hc;\n";
+    // hot cache fill: the whole CTA, 16-byte vectors where possible
+    o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = __ldg(X + k);\n";
+    o << "  __syncthreads();\n";
     g.emit_uniform();
     g.emit_red_decl();
     o << "  const long long items = a.nchunks + a.ntiles;\n";
-    o << "  for (long long it = blockIdx.x; it < items; it += gridDim.x) {\n";
+    o << "  const long long GG = (long long)gridDim.x * NBG_GROUPS;\n";
+    o << "  for (long long it = (long long)blockIdx.x * NBG_GROUPS + g; it < items; it += GG) {\n";
     // ---------------- chunk of a long row
     o << "    if (it < a.nchunks) {\n";
     o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
     o << "      const long long pb = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
     o << "      const int cnt = ch.w;\n";
     o << "      " << ACC << " t = " << IDENT << ";\n";
-    o << "      for (int q0 = threadIdx.x; q0 < cnt; q0 += 1024) {\n";
+    o << "      for (int q0 = gt; q0 < cnt; q0 += 1024) {\n";
     o << "        int c_[4];\n";
     o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; c_[u] = q < cnt ? __ldcs(a.colidx + pb + q) : 0; }\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; if (q < cnt) { const " << VT
-      << " m_ = nbg_mul(a, pb + q, __ldg(X + c_[u])); t = NBG_ADD(t, (" << ACC << ")m_); } }\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; if (q < cnt) { const int c = c_[u]; const "
+      << XT << " xv_ = c < hc ? s_hot[c] : __ldg(X + c); const " << VT << " m_ = nbg_mul(a, pb + q, xv_); t = NBG_ADD(t, (" << ACC
+      << ")m_); } }\n";
     o << "      }\n";
-    // CTA combine of the chunk (fixed order)
-    if (ACC == "double" || ACC == "long long" || ACC == "float" || ACC == "int") {
-        o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
-    }
-    o << "      __syncthreads();\n";
-    o << "      if (lane == 0) ((" << ACC << "*)nbg_sh)[warp] = t;\n";
-    o << "      __syncthreads();\n";
-    o << "      if (threadIdx.x == 0) {\n";
-    o << "        " << ACC << " part = ((" << ACC << "*)nbg_sh)[0];\n";
-    o << "        for (int w = 1; w < (int)(blockDim.x >> 5); w++) part = NBG_ADD(part, ((" << ACC << "*)nbg_sh)[w]);\n";
+    o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
+    o << "      if (lane == 0) ((" << ACC << "*)nbg_shg[g])[wg] = t;\n";
+    o << "      nbg_gbar(g);\n";
+    o << "      if (gt == 0) {\n";
+    o << "        " << ACC << " part = ((" << ACC << "*)nbg_shg[g])[0];\n";
+    o << "        for (int w = 1; w < 8; w++) part = NBG_ADD(part, ((" << ACC << "*)nbg_shg[g])[w]);\n";
     o << "        ((" << ACC << "*)a.partials)[it] = part;\n";
     o << "        __threadfence();\n";
     o << "        const int4 lr = ((const int4*)a.longs)[ch.x];\n";
     o << "        const int tk = atomicAdd(&a.counters[ch.x], 1);\n";
-    o << "        s_flag = (tk == lr.z - 1);\n";
-    o << "        if (s_flag) {\n";
+    o << "        if (tk == lr.z - 1) {\n";
     o << "          __threadfence();\n";
     o << "          " << ACC << " acc = " << IDENT << ";\n";
-    o << "          for (int j = 0; j < lr.z; j++) { " << ACC << " pj; const " << ACC << "* pp = ((const " << ACC
-      << "*)a.partials) + lr.y + j; pj = *(volatile const " << ACC << "*)pp; acc = NBG_ADD(acc, pj); }\n";
+    o << "          for (int j = 0; j < lr.z; j++) { const " << ACC << " pj = *(volatile const " << ACC << "*)(((const " << ACC
+      << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
     o << "          a.counters[ch.x] = 0;\n";
     o << "          const long long i = lr.x;\n";
     g.emit_body(
@@ -433,79 +450,76 @@ void gen_spmv(Gen &g, const std::string &kname) {
         [&](size_t j) { return g.red_direct(p.reds[j], g.v(p.reds[j].ins)); }, "acc");
     o << "        }\n";
     o << "      }\n";
-    o << "      __syncthreads();\n";
+    o << "      nbg_gbar(g);\n";
     o << "      continue;\n";
     o << "    }\n";
     // ---------------- tile of short / medium rows
     o << "    {\n";
     o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
     o << "      const int rb = tl.x, R = tl.y - tl.x;\n";
-    o << "      const long long pa = a.rowptr[rb];\n";
-    o << "      for (int j = threadIdx.x; j <= R; j += 256) s_off[j] = (int)(a.rowptr[rb + j] - pa);\n";
-    o << "      if (threadIdx.x == 0) s_nmed = 0;\n";
-    o << "      __syncthreads();\n";
+    o << "      const long long pa = __ldg(a.rowptr + rb);\n";
+    o << "      for (int j = gt; j <= R; j += 256) s_off[j] = (int)(__ldg(a.rowptr + rb + j) - pa);\n";
+    o << "      nbg_gbar(g);\n";
     o << "      const int P = s_off[R];\n";
-    o << "      for (int q0 = threadIdx.x; q0 < P; q0 += 1024) {\n";
-    o << "        int c_[4];\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; c_[u] = q < P ? __ldcs(a.colidx + pa + q) : 0; }\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; if (q < P) s_val[q] = nbg_mul(a, pa + q, __ldg(X + c_[u])); }\n";
+    o << "      for (int q0 = gt; q0 < P; q0 += 2048) {\n";
+    o << "        int c_[8];\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 256; c_[u] = q < P ? __ldcs(a.colidx + pa + q) : 0; }\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 256; if (q < P) { const int c = c_[u]; const "
+      << XT << " xv_ = c < hc ? s_hot[c] : __ldg(X + c); s_val[q] = nbg_mul(a, pa + q, xv_); } }\n";
     o << "      }\n";
-    o << "      for (int j = threadIdx.x; j < R; j += 256) if (s_off[j + 1] - s_off[j] > 32) s_med[atomicAdd(&s_nmed, 1)] = j;\n";
-    o << "      __syncthreads();\n";
-    o << "      const int nmed = s_nmed;\n";
-    o << "      for (int mi = warp; mi < nmed; mi += (int)(blockDim.x >> 5)) {\n";
-    o << "        const int j = s_med[mi];\n";
-    o << "        const int o0 = s_off[j], o1 = s_off[j + 1];\n";
-    o << "        " << ACC << " t = " << IDENT << ";\n";
-    o << "        for (int q = o0 + lane; q < o1; q += 32) t = NBG_ADD(t, (" << ACC << ")s_val[q]);\n";
-    o << "        for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
-    // park the row sum in the row's own (now consumed) value slots
-    if (ACCW == 2)
-        o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; const unsigned long long b_ = *(const unsigned long long*)&t; "
-             "w_[" + WO + "] = (unsigned)b_; w_[" + WO + " + 1] = (unsigned)(b_ >> 32); }\n";
-    else
-        o << "        if (lane == 0) { unsigned* w_ = (unsigned*)s_val; w_[" + WO + "] = *(const unsigned*)&t; }\n";
-    o << "      }\n";
-    o << "      __syncthreads();\n";
-    o << "      for (int j = threadIdx.x; j < R; j += 256) {\n";
-    o << "        const int o0 = s_off[j], o1 = s_off[j + 1];\n";
-    o << "        " << ACC << " acc;\n";
-    o << "        if (o1 - o0 > 32) {\n";
-    if (ACCW == 2)
-        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned long long b_ = (unsigned long long)w_[" + WO + "] | ((unsigned long long)w_[" + WO + " + 1] << 32); acc = *(const "
-          << ACC << "*)&b_;\n";
-    else
-        o << "          const unsigned* w_ = (const unsigned*)s_val; const unsigned b_ = w_[" + WO + "]; acc = *(const " << ACC << "*)&b_;\n";
-    o << "        } else {\n";
-    o << "          acc = " << IDENT << ";\n";
-    o << "          for (int q = o0; q < o1; q++) acc = NBG_ADD(acc, (" << ACC << ")s_val[q]);\n";
+    o << "      nbg_gbar(g);\n";
+    o << "      for (int base = 0; base < R; base += 256) {\n";
+    o << "        const int j = base + gt;\n";
+    o << "        const bool valid = j < R;\n";
+    o << "        int o0 = 0, o1 = 0;\n";
+    o << "        if (valid) { o0 = s_off[j]; o1 = s_off[j + 1]; }\n";
+    o << "        " << ACC << " acc = " << IDENT << ";\n";
+    o << "        if (valid && o1 - o0 <= 32) { for (int q = o0; q < o1; q++) acc = NBG_ADD(acc, (" << ACC << ")s_val[q]); }\n";
+    o << "        unsigned mask = __ballot_sync(0xffffffffu, valid && (o1 - o0 > 32));\n";
+    o << "        while (mask) {\n";
+    o << "          const int m = __ffs(mask) - 1;\n";
+    o << "          mask &= mask - 1;\n";
+    o << "          const int jm = base + wg * 32 + m;\n";
+    o << "          const int mo0 = s_off[jm], mo1 = s_off[jm + 1];\n";
+    o << "          " << ACC << " t = " << IDENT << ";\n";
+    o << "          for (int q = mo0 + lane; q < mo1; q += 32) t = NBG_ADD(t, (" << ACC << ")s_val[q]);\n";
+    o << "          for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
+    o << "          t = __shfl_sync(0xffffffffu, t, 0);\n";
+    o << "          if (lane == m) acc = t;\n";
     o << "        }\n";
-    o << "        const long long i = (long long)rb + j;\n";
+    o << "        if (valid) {\n";
+    o << "          const long long i = (long long)rb + j;\n";
     g.emit_body(
-        "        ",
+        "          ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
         [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    o << "        }\n";
     o << "      }\n";
-    o << "      __syncthreads();\n";
+    o << "      nbg_gbar(g);\n";
     o << "    }\n";
     o << "  }\n";
+    o << "  __syncthreads();\n";
     g.emit_red_finish();
     o << "}\n";
-    (void)T;
+    (void)ACCW;
+    (void)WO;
+    return dyn_bytes;
 }
 
 }  // namespace
 
 extern const char *NBG_PRELUDE_SRC;
 
-std::string codegen(const Prog &p, const std::string &kname) {
+std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem) {
     Gen g(p);
     g.o << NBG_PRELUDE_SRC << "\n// ---- generated region: " << p.signature() << "\n";
+    int smem = 0;
     if (p.spmv)
-        gen_spmv(g, kname);
+        smem = gen_spmv(g, kname);
     else
         gen_ewise(g, kname, p.vec);
+    if (dyn_smem) *dyn_smem = smem;
     return g.o.str();
 }
 

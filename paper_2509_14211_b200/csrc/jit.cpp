@@ -83,7 +83,7 @@ static std::string nvrtc_compile(Ctx &c, const std::string &src, const std::stri
     return cubin;
 }
 
-KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv) {
+KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem) {
     const char *dump = getenv("NBG_JIT_DUMP");
     if (dump && *dump) write_file(std::string(dump) + "/" + kname + ".cu", src);
     std::string cubin = nvrtc_compile(c, src, kname);
@@ -91,12 +91,15 @@ KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bo
     k->name = kname;
     NBG_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     NBG_CUDA(cudaLibraryGetKernel(&k->k, k->lib, kname.c_str()));
-    k->block = 256;
+    k->block = spmv ? 1024 : 256;
+    k->smem = dyn_smem;
+    if (dyn_smem > 48 * 1024)
+        NBG_CUDA(cudaFuncSetAttribute((const void *)k->k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem));
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k->k, k->block, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k->k, k->block, dyn_smem);
     if (e != cudaSuccess || per_sm <= 0) {
         cudaGetLastError();
-        per_sm = spmv ? 4 : 8;
+        per_sm = spmv ? 1 : 8;
     }
     k->grid_cap = c.num_sms * per_sm;
     return k;
@@ -109,7 +112,7 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
     void *params[] = {(void *)&args};
     cudaEvent_t ev0 = nullptr;
     timing_begin(c, cls, &ev0);
-    NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, 0, c.stream));
+    NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem, c.stream));
     timing_end(c, cls, ev0);
     c.stats.kernels_launched++;
 }

@@ -31,6 +31,7 @@ struct KArgs {
     long long ntiles, nchunks;
     long long row_offset;
     const int *oscat[NBG_MAX_OUT];
+    long long hc;
 };
 
 // ------------------------------------------------------------------ operators in type T

@@ -237,6 +237,7 @@ struct KArgs {
     long long ntiles, nchunks;
     long long row_offset;    // global index of local row 0 (distributed); 0 otherwise
     const int *oscat[MAX_OUT];   // per output: scatter map (gather layout) or null
+    long long hc;                // spmv: entries of the gathered vector cached in shared memory
 };
 
 struct Kernel {
@@ -244,6 +245,7 @@ struct Kernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t k = nullptr;
     int block = 256;
+    int smem = 0;            // dynamic shared memory per CTA
     int grid_cap = 0;        // persistent grid size (SMs * resident CTAs)
     std::string name;
 };
@@ -332,8 +334,8 @@ double scalar_read(Ctx &c, const NodeP &s);
 void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
 
 // codegen / jit
-std::string codegen(const Prog &p, const std::string &kname);
-KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv);
+std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr);
+KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0);
 void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);
 
 // graph (graph.cu)

@@ -495,6 +495,14 @@ void ensure_full(Ctx &c, const NodeP &v) {
 
 // ---------------------------------------------------------------- launch of one region
 
+// hot-cache capacity (entries) of a generated SpMV kernel: its dynamic smem minus the group buffers
+static long long hot_capacity(const Kernel &k, const Prog &p) {
+    const int vtw = (p.sp.T == NBG_FP64 || p.sp.T == NBG_INT64 || p.sp.T == NBG_BOOL) ? 8 : 4;
+    const long long grp = 3136ll * vtw + 2081ll * 4;
+    long long hot = (long long)k.smem - 4 * grp;
+    return hot > 0 ? hot / (long long)type_size(p.sp.xt) : 0;
+}
+
 struct HintOut {
     NodeP node;       // instantiated template root (pending until launch)
     MatP scatter;     // written in this matrix's gather layout (memo key PERM<A>(...))
@@ -567,7 +575,8 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.partials = (double *)(A.plan->partials ? A.plan->partials->d : nullptr);
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
-        items = A.plan->ntiles + A.plan->nchunks;
+        items = (A.plan->ntiles + A.plan->nchunks + 3) / 4;   // 4 independent groups per CTA
+        args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
     } else {
         items = (n + 1023) / 1024;
     }
@@ -579,12 +588,18 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     if (it == c.plans.end()) {
         char nm[48];
         snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.spmv ? "spmv" : "ewise", (unsigned long long)hash_str(sig));
-        kern = jit_compile(c, codegen(p, nm), nm, p.spmv);
+        int smem = 0;
+        std::string src = codegen(p, nm, &smem);
+        kern = jit_compile(c, src, nm, p.spmv, smem);
         c.plans[sig] = kern;
         c.stats.plans_built++;
     } else {
         kern = it->second;
         c.stats.plan_hits++;
+    }
+    if (p.spmv) {
+        const long long cap = (long long)(kern->smem - 0) > 0 ? hot_capacity(*kern, p) : 0;
+        if (args.hc > cap) args.hc = cap;
     }
     if (items > 0 && n > 0) launch(c, *kern, args, items, p.spmv ? "spmv" : "ewise");
 

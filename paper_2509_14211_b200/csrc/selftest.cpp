@@ -11,6 +11,11 @@
 using namespace nbg;
 
 static bool compile_only(const std::string &src, const std::string &kname, std::string &log) {
+    const char *dump = getenv("NBG_JIT_DUMP");
+    if (dump && *dump) {
+        FILE *f = fopen((std::string(dump) + "/" + kname + ".cu").c_str(), "w");
+        if (f) { fputs(src.c_str(), f); fclose(f); }
+    }
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), (kname + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS) {
         log += "create failed\n";
