@@ -328,18 +328,25 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     o << "}\n";
 }
 
-// SpMV skeleton v2: one CTA per SM of NBG_GROUPS x 256 threads.  Each
-// 256-thread group works independently on its own items (named barriers), all groups share a
-// hot-column cache in shared memory: the first `hc` entries of the gathered vector, which in the
-// degree-sorted gather layout are the most frequently gathered columns.  Returns the dynamic
-// shared memory the kernel needs.
+// SpMV skeleton v3: one CTA of 1024 threads per SM; every warp works on
+// its own statically assigned tasks with no block barriers, so the gathers of 32 warps per SM
+// stay in flight.  The CTA's shared memory holds a hot-column cache: the first `hc` entries of the
+// gathered vector, which in the degree-sorted gather layout are the most gathered columns.
+//   row task  (<= 32 consecutive rows, <= 2048 nonzeros): lane j owns row rb + j.
+//             rows with <= 32 entries: the lane sums them sequentially (4 gathers in flight);
+//             rows with 33..1024 entries (ballot): the whole warp, lanes on consecutive nonzeros
+//             (coalesced index loads), lane-strided partial sums + fixed shuffle-down tree.
+//   chunk task (1024 nonzeros of a row longer than 1024): lane-strided + shuffle tree -> chunk
+//             partial; the warp that completes the row's last chunk (atomic ticket) sums the
+//             chunk partials in chunk order and runs the epilogue.
+// A row's summation order depends only on its length, never on the task layout.
 int gen_spmv(Gen &g, const std::string &kname) {
     const Prog &p = g.p;
     auto &o = g.o;
     const SpmvSig &sp = p.sp;
     const char *C = ctype_compute(sp.T);
     const char *XT = ctype(sp.xt);
-    std::string VT = C;   // type of the gathered products kept in shared memory
+    std::string VT = C;
     std::string ACC, IDENT, ADD;
     bool fT = is_float(sp.T);
     if (sp.add == NBG_PLUS) {
@@ -374,65 +381,48 @@ int gen_spmv(Gen &g, const std::string &kname) {
         case NBG_MAX_DIVX_C: mul = "nbg_max(nbg_div(" + av + ", ((" + std::string(C) + ")(a.imm[1]))), " + xv + ")"; break;
         default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
     }
-    const int ACCW = (ACC == "double" || ACC == "long long") ? 2 : 1;   // 32-bit words of ACC
-    const int VTW = (VT == "double" || VT == "long long") ? 2 : 1;      // 32-bit words of a value slot
-    const std::string WO = "(o0 * " + std::to_string(VTW) + ")";
-    const int GROUPS = 4, VALS = 3136, ROWS = 2080;
-    const int vt_bytes = VTW * 4;
-    const int grp_bytes = VALS * vt_bytes + (ROWS + 1) * 4;
     const int x_bytes = (int)type_size(sp.xt);
-    const int static_reserve = 2048;   // static shared memory + driver reserve
-    int hot_bytes = 227 * 1024 - static_reserve - GROUPS * grp_bytes;
-    int hot_cap = hot_bytes / x_bytes;
+    int hot_cap = (227 * 1024 - 2048) / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
-    if (hot_cap > 32768) hot_cap = 32768;
-    if (hot_cap < 0) hot_cap = 0;
-    const int dyn_bytes = hot_cap * x_bytes + GROUPS * grp_bytes;
+    if (hot_cap > 49152) hot_cap = 49152;
+    const int dyn_bytes = hot_cap * x_bytes;
 
-    o << "#define NBG_GROUPS " << GROUPS << "\n#define NBG_D_TILE_VALS " << VALS << "\n#define NBG_D_TILE_ROWS " << ROWS
-      << "\n#define NBG_HOT_CAP " << hot_cap << "\n";
+    o << "#define NBG_HOT_CAP " << hot_cap << "\n";
     o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
     o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << XT << " X_) { return " << mul
       << "; }\n";
-    o << "__device__ __forceinline__ void nbg_gbar(int g) { asm volatile(\"bar.sync %0, 256;\" :: \"r\"(g + 1) : \"memory\"); }\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(" << GROUPS * 256 << ", 1) " << kname << "(const KArgs a) {\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << kname << "(const KArgs a) {\n";
     o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
     o << "  __shared__ double nbg_sh[32];\n";
-    o << "  __shared__ double nbg_shg[NBG_GROUPS][8];\n";
     o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
-    o << "  const int g = threadIdx.x >> 8, gt = threadIdx.x & 255, lane = threadIdx.x & 31, wg = gt >> 5;\n";
-    o << "  " << VT << "* s_val = (" << VT << "*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + g * " << grp_bytes << ");\n";
-    o << "  int* s_off = (int*)((unsigned char*)s_val + NBG_D_TILE_VALS * sizeof(" << VT << "));\n";
+    o << "  const int lane = threadIdx.x & 31;\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
     o << "  const int hc = (int)a.hc;\n";
-    // hot cache fill: the whole CTA, 16-byte vectors where possible
     o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = __ldg(X + k);\n";
     o << "  __syncthreads();\n";
+    o << "#define NBG_GX(c_) ((c_) < hc ? s_hot[(c_)] : __ldg(X + (c_)))\n";
     g.emit_uniform();
     g.emit_red_decl();
     o << "  const long long items = a.nchunks + a.ntiles;\n";
-    o << "  const long long GG = (long long)gridDim.x * NBG_GROUPS;\n";
-    o << "  for (long long it = (long long)blockIdx.x * NBG_GROUPS + g; it < items; it += GG) {\n";
-    // ---------------- chunk of a long row
+    o << "  const long long NW = (long long)gridDim.x * (blockDim.x >> 5);\n";
+    o << "  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += NW) {\n";
+    // ---------------- chunk of a long row (one warp)
     o << "    if (it < a.nchunks) {\n";
     o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
     o << "      const long long pb = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
     o << "      const int cnt = ch.w;\n";
     o << "      " << ACC << " t = " << IDENT << ";\n";
-    o << "      for (int q0 = gt; q0 < cnt; q0 += 1024) {\n";
-    o << "        int c_[4];\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; c_[u] = q < cnt ? __ldcs(a.colidx + pb + q) : 0; }\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) { const int q = q0 + u * 256; if (q < cnt) { const int c = c_[u]; const "
-      << XT << " xv_ = c < hc ? s_hot[c] : __ldg(X + c); const " << VT << " m_ = nbg_mul(a, pb + q, xv_); t = NBG_ADD(t, (" << ACC
-      << ")m_); } }\n";
+    o << "      for (int q0 = lane; q0 < cnt; q0 += 256) {\n";
+    o << "        int c_[8];\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 32; c_[u] = q < cnt ? __ldcs(a.colidx + pb + q) : 0; }\n";
+    o << "        " << XT << " v_[8];\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 32; if (q < cnt) v_[u] = NBG_GX(c_[u]); }\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 32; if (q < cnt) t = NBG_ADD(t, (" << ACC
+      << ")nbg_mul(a, pb + q, v_[u])); }\n";
     o << "      }\n";
     o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
-    o << "      if (lane == 0) ((" << ACC << "*)nbg_shg[g])[wg] = t;\n";
-    o << "      nbg_gbar(g);\n";
-    o << "      if (gt == 0) {\n";
-    o << "        " << ACC << " part = ((" << ACC << "*)nbg_shg[g])[0];\n";
-    o << "        for (int w = 1; w < 8; w++) part = NBG_ADD(part, ((" << ACC << "*)nbg_shg[g])[w]);\n";
-    o << "        ((" << ACC << "*)a.partials)[it] = part;\n";
+    o << "      if (lane == 0) {\n";
+    o << "        ((" << ACC << "*)a.partials)[it] = t;\n";
     o << "        __threadfence();\n";
     o << "        const int4 lr = ((const int4*)a.longs)[ch.x];\n";
     o << "        const int tk = atomicAdd(&a.counters[ch.x], 1);\n";
@@ -450,60 +440,62 @@ int gen_spmv(Gen &g, const std::string &kname) {
         [&](size_t j) { return g.red_direct(p.reds[j], g.v(p.reds[j].ins)); }, "acc");
     o << "        }\n";
     o << "      }\n";
-    o << "      nbg_gbar(g);\n";
+    o << "      __syncwarp();\n";
     o << "      continue;\n";
     o << "    }\n";
-    // ---------------- tile of short / medium rows
+    // ---------------- row task: <= 32 consecutive rows, lane j owns row rb + j
     o << "    {\n";
     o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
-    o << "      const int rb = tl.x, R = tl.y - tl.x;\n";
-    o << "      const long long pa = __ldg(a.rowptr + rb);\n";
-    o << "      for (int j = gt; j <= R; j += 256) s_off[j] = (int)(__ldg(a.rowptr + rb + j) - pa);\n";
-    o << "      nbg_gbar(g);\n";
-    o << "      const int P = s_off[R];\n";
-    o << "      for (int q0 = gt; q0 < P; q0 += 2048) {\n";
-    o << "        int c_[8];\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 256; c_[u] = q < P ? __ldcs(a.colidx + pa + q) : 0; }\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 256; if (q < P) { const int c = c_[u]; const "
-      << XT << " xv_ = c < hc ? s_hot[c] : __ldg(X + c); s_val[q] = nbg_mul(a, pa + q, xv_); } }\n";
-    o << "      }\n";
-    o << "      nbg_gbar(g);\n";
-    o << "      for (int base = 0; base < R; base += 256) {\n";
-    o << "        const int j = base + gt;\n";
-    o << "        const bool valid = j < R;\n";
-    o << "        int o0 = 0, o1 = 0;\n";
-    o << "        if (valid) { o0 = s_off[j]; o1 = s_off[j + 1]; }\n";
-    o << "        " << ACC << " acc = " << IDENT << ";\n";
-    o << "        if (valid && o1 - o0 <= 32) { for (int q = o0; q < o1; q++) acc = NBG_ADD(acc, (" << ACC << ")s_val[q]); }\n";
-    o << "        unsigned mask = __ballot_sync(0xffffffffu, valid && (o1 - o0 > 32));\n";
-    o << "        while (mask) {\n";
-    o << "          const int m = __ffs(mask) - 1;\n";
-    o << "          mask &= mask - 1;\n";
-    o << "          const int jm = base + wg * 32 + m;\n";
-    o << "          const int mo0 = s_off[jm], mo1 = s_off[jm + 1];\n";
-    o << "          " << ACC << " t = " << IDENT << ";\n";
-    o << "          for (int q = mo0 + lane; q < mo1; q += 32) t = NBG_ADD(t, (" << ACC << ")s_val[q]);\n";
-    o << "          for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
-    o << "          t = __shfl_sync(0xffffffffu, t, 0);\n";
-    o << "          if (lane == m) acc = t;\n";
+    o << "      const int j = tl.x + lane;\n";
+    o << "      const bool valid = j < tl.y;\n";
+    o << "      long long o0 = 0, o1 = 0;\n";
+    o << "      if (valid) { o0 = __ldg(a.rowptr + j); o1 = __ldg(a.rowptr + j + 1); }\n";
+    o << "      const int len = (int)(o1 - o0);\n";
+    o << "      " << ACC << " acc = " << IDENT << ";\n";
+    o << "      if (valid && len <= 32) {\n";
+    o << "        long long q = o0;\n";
+    o << "        for (; q + 4 <= o1; q += 4) {\n";
+    o << "          const int c0 = __ldcs(a.colidx + q), c1 = __ldcs(a.colidx + q + 1), c2 = __ldcs(a.colidx + q + 2), c3 = __ldcs(a.colidx + q + 3);\n";
+    o << "          const " << XT << " v0 = NBG_GX(c0), v1 = NBG_GX(c1), v2 = NBG_GX(c2), v3 = NBG_GX(c3);\n";
+    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q, v0));\n";
+    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q + 1, v1));\n";
+    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q + 2, v2));\n";
+    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q + 3, v3));\n";
     o << "        }\n";
-    o << "        if (valid) {\n";
-    o << "          const long long i = (long long)rb + j;\n";
+    o << "        for (; q < o1; q++) { const int c = __ldcs(a.colidx + q); acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q, NBG_GX(c))); }\n";
+    o << "      }\n";
+    o << "      unsigned mask = __ballot_sync(0xffffffffu, valid && len > 32);\n";
+    o << "      while (mask) {\n";
+    o << "        const int m = __ffs(mask) - 1;\n";
+    o << "        mask &= mask - 1;\n";
+    o << "        const long long mo0 = __shfl_sync(0xffffffffu, o0, m), mo1 = __shfl_sync(0xffffffffu, o1, m);\n";
+    o << "        " << ACC << " t = " << IDENT << ";\n";
+    o << "        for (long long q0 = mo0 + lane; q0 < mo1; q0 += 128) {\n";
+    o << "          int c_[4];\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const long long q = q0 + u * 32; c_[u] = q < mo1 ? __ldcs(a.colidx + q) : 0; }\n";
+    o << "          " << XT << " v_[4];\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const long long q = q0 + u * 32; if (q < mo1) v_[u] = NBG_GX(c_[u]); }\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const long long q = q0 + u * 32; if (q < mo1) t = NBG_ADD(t, (" << ACC
+      << ")nbg_mul(a, q, v_[u])); }\n";
+    o << "        }\n";
+    o << "        for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
+    o << "        t = __shfl_sync(0xffffffffu, t, 0);\n";
+    o << "        if (lane == m) acc = t;\n";
+    o << "      }\n";
+    o << "      if (valid) {\n";
+    o << "        const long long i = j;\n";
     g.emit_body(
-        "          ",
+        "        ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
         [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
-    o << "        }\n";
     o << "      }\n";
-    o << "      nbg_gbar(g);\n";
     o << "    }\n";
     o << "  }\n";
     o << "  __syncthreads();\n";
     g.emit_red_finish();
+    o << "#undef NBG_GX\n";
     o << "}\n";
-    (void)ACCW;
-    (void)WO;
     return dyn_bytes;
 }
 

@@ -20,7 +20,9 @@ namespace {
 
 constexpr int SP_TILE = 2048;    // merge items (rows + nonzeros) per tile
 constexpr int SP_LONG = 1024;    // rows with more nonzeros are processed as chunks
-constexpr int SP_CHUNK = 2048;   // nonzeros per chunk of a long row
+constexpr int SP_CHUNK = 1024;   // nonzeros per chunk of a long row (one warp)
+constexpr int SP_TASK_ROWS = 32;  // rows per warp task (one per lane)
+constexpr int SP_TASK_NNZ = 2048; // nonzero budget of a warp task
 
 __device__ __forceinline__ unsigned long long sm64(unsigned long long key, unsigned long long k) {
     unsigned long long z = key + (k + 1ull) * 0x9E3779B97F4A7C15ull;
@@ -320,24 +322,28 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     NBG_CUDA(cudaGetLastError());
     NBG_CUDA(cudaStreamSynchronize(c.stream));
 
-    // tile boundaries = merge-path cuts U {L, L+1 : L long}
-    std::vector<int> bnd(s.begin(), s.end());
-    bnd.push_back(0);
-    bnd.push_back((int)n);
-    for (int r : lr) {
-        bnd.push_back(r);
-        bnd.push_back(r + 1);
-    }
-    std::sort(bnd.begin(), bnd.end());
-    bnd.erase(std::unique(bnd.begin(), bnd.end()), bnd.end());
+    // warp tasks: runs of <= 32 consecutive non-long rows with <= SP_TASK_NNZ nonzeros (greedy,
+    // on the host from the row pointers; once per matrix)
+    std::vector<long long> rph((size_t)n + 1);
+    NBG_CUDA(cudaMemcpyAsync(rph.data(), A.rowptr->d, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
     std::vector<int> tiles;
-    for (size_t j = 0; j + 1 < bnd.size(); j++) {
-        int a = bnd[j], b = bnd[j + 1];
-        if (b <= a) continue;
-        if (b == a + 1 && std::binary_search(lr.begin(), lr.end(), a)) continue;   // a long row
-        tiles.push_back(a);
-        tiles.push_back(b);
+    tiles.reserve((size_t)(n / 16 + 16));
+    for (long long i = 0; i < n;) {
+        long long len = rph[i + 1] - rph[i];
+        if (len > SP_LONG) { i++; continue; }
+        long long st = i, nz = 0;
+        while (i < n && i - st < SP_TASK_ROWS) {
+            long long l2 = rph[i + 1] - rph[i];
+            if (l2 > SP_LONG) break;
+            if (i > st && nz + l2 > SP_TASK_NNZ) break;
+            nz += l2;
+            i++;
+        }
+        tiles.push_back((int)st);
+        tiles.push_back((int)i);
     }
+    (void)s;
     std::vector<int> chunks, longs;
     long long nch_total = 0;
     for (long long j = 0; j < L; j++) {

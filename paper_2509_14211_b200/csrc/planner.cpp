@@ -495,12 +495,9 @@ void ensure_full(Ctx &c, const NodeP &v) {
 
 // ---------------------------------------------------------------- launch of one region
 
-// hot-cache capacity (entries) of a generated SpMV kernel: its dynamic smem minus the group buffers
+// hot-cache capacity (entries) of a generated SpMV kernel: its whole dynamic shared memory
 static long long hot_capacity(const Kernel &k, const Prog &p) {
-    const int vtw = (p.sp.T == NBG_FP64 || p.sp.T == NBG_INT64 || p.sp.T == NBG_BOOL) ? 8 : 4;
-    const long long grp = 3136ll * vtw + 2081ll * 4;
-    long long hot = (long long)k.smem - 4 * grp;
-    return hot > 0 ? hot / (long long)type_size(p.sp.xt) : 0;
+    return (long long)k.smem / (long long)type_size(p.sp.xt);
 }
 
 struct HintOut {
@@ -575,7 +572,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.partials = (double *)(A.plan->partials ? A.plan->partials->d : nullptr);
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
-        items = (A.plan->ntiles + A.plan->nchunks + 3) / 4;   // 4 independent groups per CTA
+        items = (A.plan->ntiles + A.plan->nchunks + 31) / 32;   // one task per warp, 32 warps per CTA
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
     } else {
         items = (n + 1023) / 1024;
