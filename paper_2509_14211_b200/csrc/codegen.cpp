@@ -22,6 +22,7 @@
 //                  runs the epilogue.
 //          The summation order of a row depends only on its length, so the
 //          fused and the blocking mxv -- and every row partition -- produce identical row sums.
+#include <algorithm>
 #include <sstream>
 
 #include "nbg_internal.hpp"
@@ -328,18 +329,24 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     o << "}\n";
 }
 
-// SpMV skeleton v3: one CTA of 1024 threads per SM; every warp works on
-// its own statically assigned tasks with no block barriers, so the gathers of 32 warps per SM
-// stay in flight.  The CTA's shared memory holds a hot-column cache: the first `hc` entries of the
-// gathered vector, which in the degree-sorted gather layout are the most gathered columns.
-//   row task  (<= 32 consecutive rows, <= 2048 nonzeros): lane j owns row rb + j.
-//             rows with <= 32 entries: the lane sums them sequentially (4 gathers in flight);
-//             rows with 33..1024 entries (ballot): the whole warp, lanes on consecutive nonzeros
-//             (coalesced index loads), lane-strided partial sums + fixed shuffle-down tree.
-//   chunk task (1024 nonzeros of a row longer than 1024): lane-strided + shuffle tree -> chunk
-//             partial; the warp that completes the row's last chunk (atomic ticket) sums the
-//             chunk partials in chunk order and runs the epilogue.
-// A row's summation order depends only on its length, never on the task layout.
+static int redkind(const Gen &g, const RedOut &r) { return g.redkind(r).kind; }
+
+// SpMV skeleton v4.  One CTA of 1024 threads per SM; the CTA owns the
+// tasks b, b + G, b + 2G, ... (G = grid size) and its 32 warps pull them from a shared-memory
+// counter, so a slow task never idles the others and no block barrier sits on the hot loop.
+//   row task  (<= 32 consecutive rows, <= 512 nonzeros): the warp stages the task's column
+//             indices into its own shared buffer with coalesced 16-byte loads, then lane j owns
+//             row rb + j: rows with <= 32 entries are summed sequentially by the lane (8 gathers in
+//             flight), rows with 33..512 entries (ballot) by the whole warp (lane-strided partial
+//             sums + fixed shuffle-down tree).
+//   chunk task (512 nonzeros of a row longer than 512): lane-strided + shuffle tree -> chunk
+//             partial; the warp that completes the row's last chunk (atomic ticket) sums the chunk
+//             partials in chunk order and runs the epilogue.
+// A row's summation order depends only on its length.  Gathers hit a hot-column cache in shared
+// memory first (the first `hc` entries of the gathered vector: the most gathered columns in the
+// degree-sorted gather layout).  Floating PLUS reductions are summed per task in fp64 (fixed
+// tree) and the task partials are added EXACTLY (fixed-point limbs), so the dynamic task order
+// cannot change any result.
 int gen_spmv(Gen &g, const std::string &kname) {
     const Prog &p = g.p;
     auto &o = g.o;
@@ -381,31 +388,51 @@ int gen_spmv(Gen &g, const std::string &kname) {
         case NBG_MAX_DIVX_C: mul = "nbg_max(nbg_div(" + av + ", ((" + std::string(C) + ")(a.imm[1]))), " + xv + ")"; break;
         default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
     }
+    // which reductions are floating PLUS (task-scoped fp64 partial + exact per-warp limbs)
+    std::vector<int> fplus;
+    for (size_t j = 0; j < p.reds.size(); j++)
+        if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
+    const int NF = (int)fplus.size();
+    const int CI = 512;                                  // staged indices per warp (task budget)
+    const int ci_bytes = 32 * (CI + 8) * 4;
+    const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
-    int hot_cap = (227 * 1024 - 2048) / x_bytes;
+    int hot_bytes = 227 * 1024 - 2048 - ci_bytes - xacc_bytes;
+    int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
-    if (hot_cap > 49152) hot_cap = 49152;
-    const int dyn_bytes = hot_cap * x_bytes;
+    if (hot_cap > 40960) hot_cap = 40960;
+    if (hot_cap < 0) hot_cap = 0;
+    const int dyn_bytes = hot_cap * x_bytes + ci_bytes + xacc_bytes;
 
-    o << "#define NBG_HOT_CAP " << hot_cap << "\n";
+    o << "#define NBG_HOT_CAP " << hot_cap << "\n#define NBG_CI " << CI << "\n#define NBG_NF " << NF << "\n";
     o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
     o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << XT << " X_) { return " << mul
       << "; }\n";
     o << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << kname << "(const KArgs a) {\n";
     o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
     o << "  __shared__ double nbg_sh[32];\n";
+    o << "  __shared__ int s_ctr;\n";
     o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
-    o << "  const int lane = threadIdx.x & 31;\n";
+    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    o << "  int* s_ci = (int*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ")) + warp * (NBG_CI + 8);\n";
+    if (NF)
+        o << "  u64* s_x = (u64*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + " << ci_bytes << ");   // [warp][NF][11]\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
     o << "  const int hc = (int)a.hc;\n";
+    o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
+    if (NF) o << "  for (int k = threadIdx.x; k < 32 * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
     o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = __ldg(X + k);\n";
     o << "  __syncthreads();\n";
     o << "#define NBG_GX(c_) ((c_) < hc ? s_hot[(c_)] : __ldg(X + (c_)))\n";
     g.emit_uniform();
     g.emit_red_decl();
     o << "  const long long items = a.nchunks + a.ntiles;\n";
-    o << "  const long long NW = (long long)gridDim.x * (blockDim.x >> 5);\n";
-    o << "  for (long long it = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < items; it += NW) {\n";
+    o << "  for (;;) {\n";
+    o << "    int l_ = 0;\n";
+    o << "    if (lane == 0) l_ = atomicAdd(&s_ctr, 1);\n";
+    o << "    l_ = __shfl_sync(0xffffffffu, l_, 0);\n";
+    o << "    const long long it = (long long)blockIdx.x + (long long)l_ * gridDim.x;\n";
+    o << "    if (it >= items) break;\n";
     // ---------------- chunk of a long row (one warp)
     o << "    if (it < a.nchunks) {\n";
     o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
@@ -446,54 +473,88 @@ int gen_spmv(Gen &g, const std::string &kname) {
     // ---------------- row task: <= 32 consecutive rows, lane j owns row rb + j
     o << "    {\n";
     o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
-    o << "      const int j = tl.x + lane;\n";
-    o << "      const bool valid = j < tl.y;\n";
-    o << "      long long o0 = 0, o1 = 0;\n";
-    o << "      if (valid) { o0 = __ldg(a.rowptr + j); o1 = __ldg(a.rowptr + j + 1); }\n";
-    o << "      const int len = (int)(o1 - o0);\n";
+    o << "      const int R = tl.y - tl.x;\n";
+    o << "      const long long rp_ = __ldg(a.rowptr + tl.x + (lane < R ? lane : R));\n";
+    o << "      const long long o0 = rp_;\n";
+    o << "      const long long o1 = __shfl_down_sync(0xffffffffu, rp_, 1);\n";
+    o << "      const long long pend = __shfl_sync(0xffffffffu, rp_, R < 31 ? R : 31);\n";
+    o << "      const long long pe = R == 32 ? __ldg(a.rowptr + tl.y) : pend;\n";
+    o << "      const long long o1f = (lane == 31) ? pe : o1;\n";
+    o << "      const long long ps = __shfl_sync(0xffffffffu, rp_, 0);\n";
+    o << "      const bool valid = lane < R;\n";
+    o << "      const int len = valid ? (int)(o1f - o0) : 0;\n";
+    // stage the task's indices (coalesced 16-byte loads where they stay inside the array)
+    o << "      const long long a0 = ps & ~3ll;\n";
+    o << "      for (long long k4 = lane; a0 + 4 * k4 < pe; k4 += 32) {\n";
+    o << "        const long long q = a0 + 4 * k4;\n";
+    o << "        if (q + 3 < a.nnz) { const int4 v4 = __ldcs((const int4*)(a.colidx + q)); ((int4*)s_ci)[k4] = v4; }\n";
+    o << "        else { for (int u = 0; u < 4; u++) if (q + u < pe) s_ci[4 * k4 + u] = __ldcs(a.colidx + q + u); }\n";
+    o << "      }\n";
+    o << "      __syncwarp();\n";
+    for (int j : fplus) o << "      r" << j << " = 0.0;\n";
     o << "      " << ACC << " acc = " << IDENT << ";\n";
     o << "      if (valid && len <= 32) {\n";
-    o << "        long long q = o0;\n";
-    o << "        for (; q + 4 <= o1; q += 4) {\n";
-    o << "          const int c0 = __ldcs(a.colidx + q), c1 = __ldcs(a.colidx + q + 1), c2 = __ldcs(a.colidx + q + 2), c3 = __ldcs(a.colidx + q + 3);\n";
-    o << "          const " << XT << " v0 = NBG_GX(c0), v1 = NBG_GX(c1), v2 = NBG_GX(c2), v3 = NBG_GX(c3);\n";
-    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q, v0));\n";
-    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q + 1, v1));\n";
-    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q + 2, v2));\n";
-    o << "          acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q + 3, v3));\n";
+    o << "        int q = (int)(o0 - a0);\n";
+    o << "        const int qe = (int)(o1f - a0);\n";
+    o << "        for (; q + 8 <= qe; q += 8) {\n";
+    o << "          " << XT << " v_[8];\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 8; u++) { const int c = s_ci[q + u]; v_[u] = NBG_GX(c); }\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 8; u++) acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, a0 + q + u, v_[u]));\n";
     o << "        }\n";
-    o << "        for (; q < o1; q++) { const int c = __ldcs(a.colidx + q); acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, q, NBG_GX(c))); }\n";
+    o << "        for (; q < qe; q++) { const int c = s_ci[q]; acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, a0 + q, NBG_GX(c))); }\n";
     o << "      }\n";
     o << "      unsigned mask = __ballot_sync(0xffffffffu, valid && len > 32);\n";
     o << "      while (mask) {\n";
     o << "        const int m = __ffs(mask) - 1;\n";
     o << "        mask &= mask - 1;\n";
-    o << "        const long long mo0 = __shfl_sync(0xffffffffu, o0, m), mo1 = __shfl_sync(0xffffffffu, o1, m);\n";
+    o << "        const int mq0 = (int)(__shfl_sync(0xffffffffu, o0, m) - a0), mq1 = (int)(__shfl_sync(0xffffffffu, o1f, m) - a0);\n";
     o << "        " << ACC << " t = " << IDENT << ";\n";
-    o << "        for (long long q0 = mo0 + lane; q0 < mo1; q0 += 128) {\n";
-    o << "          int c_[4];\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const long long q = q0 + u * 32; c_[u] = q < mo1 ? __ldcs(a.colidx + q) : 0; }\n";
+    o << "        for (int q0 = mq0 + lane; q0 < mq1; q0 += 128) {\n";
     o << "          " << XT << " v_[4];\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const long long q = q0 + u * 32; if (q < mo1) v_[u] = NBG_GX(c_[u]); }\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const long long q = q0 + u * 32; if (q < mo1) t = NBG_ADD(t, (" << ACC
-      << ")nbg_mul(a, q, v_[u])); }\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const int q = q0 + u * 32; if (q < mq1) v_[u] = NBG_GX(s_ci[q]); }\n";
+    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const int q = q0 + u * 32; if (q < mq1) t = NBG_ADD(t, (" << ACC
+      << ")nbg_mul(a, a0 + q, v_[u])); }\n";
     o << "        }\n";
     o << "        for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
     o << "        t = __shfl_sync(0xffffffffu, t, 0);\n";
     o << "        if (lane == m) acc = t;\n";
     o << "      }\n";
     o << "      if (valid) {\n";
-    o << "        const long long i = j;\n";
+    o << "        const long long i = (long long)tl.x + lane;\n";
     g.emit_body(
         "        ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
         [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
     o << "      }\n";
+    // task-scoped exact combine of the floating PLUS reductions
+    for (int f = 0; f < NF; f++) {
+        int j = fplus[f];
+        o << "      { double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f
+          << ") * 11, t_); }\n";
+    }
+    o << "      __syncwarp();\n";
     o << "    }\n";
     o << "  }\n";
     o << "  __syncthreads();\n";
-    g.emit_red_finish();
+    // per-CTA combine: float PLUS limbs (integer sums) -> global atomics; the rest as before
+    for (int f = 0; f < NF; f++) {
+        int j = fplus[f];
+        o << "  if (threadIdx.x < 11) {\n";
+        o << "    u64 v_ = 0ull;\n";
+        o << "    for (int w = 0; w < 32; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 11 + threadIdx.x]; v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
+        o << "    if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
+        o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
+        o << "  }\n";
+    }
+    for (size_t j = 0; j < p.reds.size(); j++) {
+        if (std::find(fplus.begin(), fplus.end(), (int)j) != fplus.end()) continue;
+        int kind = redkind(g, p.reds[j]);
+        if (kind == 0 || kind == 2 || kind == 3)
+            o << "  nbg_block_finish_f(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+        else
+            o << "  nbg_block_finish_i(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+    }
     o << "#undef NBG_GX\n";
     o << "}\n";
     return dyn_bytes;

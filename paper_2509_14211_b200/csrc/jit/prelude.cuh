@@ -32,6 +32,7 @@ struct KArgs {
     long long row_offset;
     const int *oscat[NBG_MAX_OUT];
     long long hc;
+    long long nnz;
 };
 
 // ------------------------------------------------------------------ operators in type T
@@ -85,6 +86,37 @@ __device__ void nbg_xacc_add(u64 *acc, double d) {
     if (p0) atomicAdd(&acc[k], p0);
     if (p1) atomicAdd(&acc[k + 1], p1);
     if (p2) atomicAdd(&acc[k + 2], p2);
+}
+
+// the same exact add into limbs the caller owns exclusively (shared memory of one warp): no atomics
+__device__ void nbg_xacc_add_local(u64 *acc, double d) {
+    if (d == 0.0) return;
+    long long bits = __double_as_longlong(d);
+    int e = (int)((bits >> 52) & 0x7ff);
+    if (e == 0x7ff) {
+        acc[10] |= ((bits & 0xFFFFFFFFFFFFFull) != 0) ? 1ull : (bits < 0 ? 4ull : 2ull);
+        return;
+    }
+    u64 m = (u64)bits & 0xFFFFFFFFFFFFFull;
+    int ex;
+    if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
+    int pos = ex + 160;
+    if (pos < 0) {
+        int s = -pos;
+        if (s >= 64) return;
+        m >>= s;
+        pos = 0;
+        if (m == 0) return;
+    }
+    if (pos > 235) { acc[10] |= 8ull; return; }
+    int k = pos >> 5, sh = pos & 31;
+    u64 lo = m << sh;
+    u64 hi = sh ? (m >> (64 - sh)) : 0ull;
+    u64 p0 = lo & 0xffffffffull, p1 = lo >> 32, p2 = hi;
+    if (bits < 0) { p0 = (u64)(-(long long)p0); p1 = (u64)(-(long long)p1); p2 = (u64)(-(long long)p2); }
+    acc[k] += p0;
+    acc[k + 1] += p1;
+    acc[k + 2] += p2;
 }
 
 __device__ double nbg_xacc_value(const u64 *L) {

@@ -238,6 +238,7 @@ struct KArgs {
     long long row_offset;    // global index of local row 0 (distributed); 0 otherwise
     const int *oscat[MAX_OUT];   // per output: scatter map (gather layout) or null
     long long hc;                // spmv: entries of the gathered vector cached in shared memory
+    long long nnz;               // spmv: number of stored entries (bounds of vector index loads)
 };
 
 struct Kernel {

@@ -573,6 +573,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
         items = (A.plan->ntiles + A.plan->nchunks + 31) / 32;   // one task per warp, 32 warps per CTA
+        args.nnz = A.nnz;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
     } else {
         items = (n + 1023) / 1024;
