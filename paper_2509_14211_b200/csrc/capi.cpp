@@ -294,7 +294,8 @@ nbg_status nbg_get_timing(nbg_ctx *ctx, const char *cls, double *total_ms, int64
 
 static BufP upload(Ctx &c, const void *p, size_t bytes, int space, int own) {
     if (bytes == 0) return alloc_buf(c, 0);
-    if (space == NBG_DEVICE && own == NBG_BORROW) return borrow_buf(c, const_cast<void *>(p), bytes);
+    // borrowed device memory is used in place when 16-byte aligned (vector loads); else copied
+    if (space == NBG_DEVICE && own == NBG_BORROW && ((uintptr_t)p % 16) == 0) return borrow_buf(c, const_cast<void *>(p), bytes);
     BufP b = alloc_buf(c, bytes);
     NBG_CUDA(cudaMemcpyAsync(b->d, p, bytes, space == NBG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream));
     if (space == NBG_HOST) NBG_CUDA(cudaStreamSynchronize(c.stream));   // caller may reuse its buffer

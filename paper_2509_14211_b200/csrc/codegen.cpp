@@ -331,23 +331,22 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
 
 static int redkind(const Gen &g, const RedOut &r) { return g.redkind(r).kind; }
 
-// SpMV skeleton v4.  One CTA of 1024 threads per SM; the CTA owns the
-// tasks b, b + G, b + 2G, ... (G = grid size) and its 32 warps pull them from a shared-memory
-// counter, so a slow task never idles the others and no block barrier sits on the hot loop.
-//   row task  (<= 32 consecutive rows, <= 512 nonzeros): the warp stages the task's column
-//             indices into its own shared buffer with coalesced 16-byte loads, then lane j owns
-//             row rb + j: rows with <= 32 entries are summed sequentially by the lane (8 gathers in
-//             flight), rows with 33..512 entries (ballot) by the whole warp (lane-strided partial
-//             sums + fixed shuffle-down tree).
-//   chunk task (512 nonzeros of a row longer than 512): lane-strided + shuffle tree -> chunk
-//             partial; the warp that completes the row's last chunk (atomic ticket) sums the chunk
-//             partials in chunk order and runs the epilogue.
-// A row's summation order depends only on its length.  Gathers hit a hot-column cache in shared
-// memory first (the first `hc` entries of the gathered vector: the most gathered columns in the
-// degree-sorted gather layout).  Floating PLUS reductions are summed per task in fp64 (fixed
-// tree) and the task partials are added EXACTLY (fixed-point limbs), so the dynamic task order
-// cannot change any result.
-int gen_spmv(Gen &g, const std::string &kname) {
+// SpMV skeleton v5.  One CTA of 1024 threads per SM; the CTA owns tasks
+// b, b + G, b + 2G, ... (G = grid size); its 32 warps pull them from a shared-memory counter.
+//   row task  (<= 32 consecutive rows, <= NBG_TASK nonzeros): the warp streams the task's
+//             nonzeros in steps of 128: lane l loads indices [base + 4l, base + 4l + 4) with one
+//             16-byte load (fully coalesced), gathers the 4 values (hot-column cache in shared
+//             memory first, else L1/L2) and reduces them by row with a segmented warp scan
+//             (row starts marked in a per-warp bitmap).  Row totals land in a per-warp array;
+//             lane j then runs the fused epilogue for row rb + j (coalesced loads/stores).
+//   chunk task (NBG_TASK nonzeros of a longer row): same 16-byte streaming, lane-sequential
+//             partials + fixed shuffle tree -> chunk partial; the warp that completes the row's
+//             last chunk (atomic ticket) sums the chunk partials in chunk order, runs the epilogue.
+// Floating PLUS reductions of the epilogue are summed per task in fp64 (fixed tree) and the task
+// partials added EXACTLY into per-warp fixed-point limbs, so the dynamic task order changes
+// nothing: every result is deterministic.  Summation order inside a row is fixed by the matrix
+// plan (the same for the fused and the per-op mxv).
+int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     const Prog &p = g.p;
     auto &o = g.o;
     const SpmvSig &sp = p.sp;
@@ -388,23 +387,24 @@ int gen_spmv(Gen &g, const std::string &kname) {
         case NBG_MAX_DIVX_C: mul = "nbg_max(nbg_div(" + av + ", ((" + std::string(C) + ")(a.imm[1]))), " + xv + ")"; break;
         default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
     }
-    // which reductions are floating PLUS (task-scoped fp64 partial + exact per-warp limbs)
     std::vector<int> fplus;
     for (size_t j = 0; j < p.reds.size(); j++)
         if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
     const int NF = (int)fplus.size();
-    const int CI = 512;                                  // staged indices per warp (task budget)
-    const int ci_bytes = 32 * (CI + 8) * 4;
+    const int accw = (ACC == "double" || ACC == "long long") ? 8 : 4;
+    const int warp_bytes = 32 * 8 + 16 + 128;                 // row totals, flag bitmap, row-of-position
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
-    int hot_bytes = 227 * 1024 - 2048 - ci_bytes - xacc_bytes;
+    int hot_bytes = 227 * 1024 - 2048 - 32 * warp_bytes - xacc_bytes;
+    if (hot_bytes > 200 * 1024) hot_bytes = 200 * 1024;
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
-    if (hot_cap > 40960) hot_cap = 40960;
     if (hot_cap < 0) hot_cap = 0;
-    const int dyn_bytes = hot_cap * x_bytes + ci_bytes + xacc_bytes;
+    const int dyn_bytes = hot_cap * x_bytes + 32 * warp_bytes + xacc_bytes;
+    if (hot_entries) *hot_entries = hot_cap;
+    (void)accw;
 
-    o << "#define NBG_HOT_CAP " << hot_cap << "\n#define NBG_CI " << CI << "\n#define NBG_NF " << NF << "\n";
+    o << "#define NBG_HOT_CAP " << hot_cap << "\n#define NBG_NF " << NF << "\n";
     o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
     o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << XT << " X_) { return " << mul
       << "; }\n";
@@ -414,13 +414,17 @@ int gen_spmv(Gen &g, const std::string &kname) {
     o << "  __shared__ int s_ctr;\n";
     o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    o << "  int* s_ci = (int*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ")) + warp * (NBG_CI + 8);\n";
+    o << "  unsigned char* s_w = nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + warp * " << warp_bytes << ";\n";
+    o << "  " << ACC << "* s_racc = (" << ACC << "*)s_w;                 // [32] row totals of the task\n";
+    o << "  unsigned* s_fl = (unsigned*)(s_w + 256);                     // [4] row-start bitmap of the step\n";
+    o << "  unsigned char* s_rof = s_w + 272;                            // [128] row of a row-start position\n";
     if (NF)
-        o << "  u64* s_x = (u64*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + " << ci_bytes << ");   // [warp][NF][11]\n";
+        o << "  u64* s_x = (u64*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + 32 * " << warp_bytes << ");   // [warp][NF][11]\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
     o << "  const int hc = (int)a.hc;\n";
     o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
     if (NF) o << "  for (int k = threadIdx.x; k < 32 * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
+    o << "  if (lane < 4) s_fl[lane] = 0u;\n";
     o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = __ldg(X + k);\n";
     o << "  __syncthreads();\n";
     o << "#define NBG_GX(c_) ((c_) < hc ? s_hot[(c_)] : __ldg(X + (c_)))\n";
@@ -433,19 +437,21 @@ int gen_spmv(Gen &g, const std::string &kname) {
     o << "    l_ = __shfl_sync(0xffffffffu, l_, 0);\n";
     o << "    const long long it = (long long)blockIdx.x + (long long)l_ * gridDim.x;\n";
     o << "    if (it >= items) break;\n";
-    // ---------------- chunk of a long row (one warp)
+    // ---------------- chunk of a long row
     o << "    if (it < a.nchunks) {\n";
     o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
     o << "      const long long pb = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
-    o << "      const int cnt = ch.w;\n";
+    o << "      const long long pe = pb + ch.w;\n";
     o << "      " << ACC << " t = " << IDENT << ";\n";
-    o << "      for (int q0 = lane; q0 < cnt; q0 += 256) {\n";
-    o << "        int c_[8];\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 32; c_[u] = q < cnt ? __ldcs(a.colidx + pb + q) : 0; }\n";
-    o << "        " << XT << " v_[8];\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 32; if (q < cnt) v_[u] = NBG_GX(c_[u]); }\n";
-    o << "        #pragma unroll\n        for (int u = 0; u < 8; u++) { const int q = q0 + u * 32; if (q < cnt) t = NBG_ADD(t, (" << ACC
-      << ")nbg_mul(a, pb + q, v_[u])); }\n";
+    o << "      for (long long base = pb & ~3ll; base < pe; base += 128) {\n";
+    o << "        const long long P0 = base + 4 * lane;\n";
+    o << "        int c_[4];\n";
+    o << "        if (P0 + 3 < a.nnz) { const int4 q4 = __ldcs((const int4*)(a.colidx + P0)); c_[0] = q4.x; c_[1] = q4.y; c_[2] = q4.z; c_[3] = q4.w; }\n";
+    o << "        else { for (int k = 0; k < 4; k++) c_[k] = (P0 + k < a.nnz) ? __ldcs(a.colidx + P0 + k) : 0; }\n";
+    o << "        " << XT << " v_[4];\n";
+    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) { const long long P = P0 + k; if (P >= pb && P < pe) v_[k] = NBG_GX(c_[k]); }\n";
+    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) { const long long P = P0 + k; if (P >= pb && P < pe) t = NBG_ADD(t, (" << ACC
+      << ")nbg_mul(a, P, v_[k])); }\n";
     o << "      }\n";
     o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
     o << "      if (lane == 0) {\n";
@@ -470,56 +476,77 @@ int gen_spmv(Gen &g, const std::string &kname) {
     o << "      __syncwarp();\n";
     o << "      continue;\n";
     o << "    }\n";
-    // ---------------- row task: <= 32 consecutive rows, lane j owns row rb + j
+    // ---------------- row task
     o << "    {\n";
     o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
     o << "      const int R = tl.y - tl.x;\n";
-    o << "      const long long rp_ = __ldg(a.rowptr + tl.x + (lane < R ? lane : R));\n";
-    o << "      const long long o0 = rp_;\n";
-    o << "      const long long o1 = __shfl_down_sync(0xffffffffu, rp_, 1);\n";
-    o << "      const long long pend = __shfl_sync(0xffffffffu, rp_, R < 31 ? R : 31);\n";
-    o << "      const long long pe = R == 32 ? __ldg(a.rowptr + tl.y) : pend;\n";
-    o << "      const long long o1f = (lane == 31) ? pe : o1;\n";
-    o << "      const long long ps = __shfl_sync(0xffffffffu, rp_, 0);\n";
+    o << "      const long long rs = __ldg(a.rowptr + tl.x + (lane < R ? lane : R));   // start of my row\n";
+    o << "      const long long re_ = (lane == 31) ? __ldg(a.rowptr + tl.x + (R < 32 ? R : 32)) : __shfl_down_sync(0xffffffffu, rs, 1);\n";
+    o << "      const long long ps = __shfl_sync(0xffffffffu, rs, 0);\n";
+    o << "      const long long pe = __shfl_sync(0xffffffffu, (lane == 31) ? re_ : rs, R < 32 ? R : 31);\n";
     o << "      const bool valid = lane < R;\n";
-    o << "      const int len = valid ? (int)(o1f - o0) : 0;\n";
-    // stage the task's indices (coalesced 16-byte loads where they stay inside the array)
-    o << "      const long long a0 = ps & ~3ll;\n";
-    o << "      for (long long k4 = lane; a0 + 4 * k4 < pe; k4 += 32) {\n";
-    o << "        const long long q = a0 + 4 * k4;\n";
-    o << "        if (q + 3 < a.nnz) { const int4 v4 = __ldcs((const int4*)(a.colidx + q)); ((int4*)s_ci)[k4] = v4; }\n";
-    o << "        else { for (int u = 0; u < 4; u++) if (q + u < pe) s_ci[4 * k4 + u] = __ldcs(a.colidx + q + u); }\n";
+    o << "      const bool nonempty = valid && re_ > rs;\n";
+    o << "      s_racc[lane] = " << IDENT << ";\n";
+    o << "      __syncwarp();\n";
+    o << "      " << ACC << " carry = " << IDENT << ";\n";
+    o << "      int crow = -1;                      // row open at the left edge of the step\n";
+    o << "      for (long long base = ps & ~3ll; base < pe; base += 128) {\n";
+    o << "        const long long P0 = base + 4 * lane;\n";
+    o << "        int c_[4];\n";
+    o << "        if (P0 + 3 < a.nnz) { const int4 q4 = __ldcs((const int4*)(a.colidx + P0)); c_[0] = q4.x; c_[1] = q4.y; c_[2] = q4.z; c_[3] = q4.w; }\n";
+    o << "        else { for (int k = 0; k < 4; k++) c_[k] = (P0 + k < a.nnz) ? __ldcs(a.colidx + P0 + k) : 0; }\n";
+    o << "        " << XT << " v_[4];\n";
+    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) { const long long P = P0 + k; if (P >= ps && P < pe) v_[k] = NBG_GX(c_[k]); }\n";
+    // mark row starts of this step
+    o << "        if (nonempty && rs >= base && rs < base + 128) { const int pos = (int)(rs - base); atomicOr(&s_fl[pos >> 5], 1u << (pos & 31)); s_rof[pos] = (unsigned char)lane; }\n";
+    o << "        __syncwarp();\n";
+    o << "        const unsigned fw = s_fl[lane >> 3];\n";
+    o << "        const int fb = (fw >> ((lane & 7) * 4)) & 15;     // flags of my 4 positions\n";
+    o << "        int rof[4];\n";
+    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) rof[k] = ((fb >> k) & 1) ? (int)s_rof[4 * lane + k] : -1;\n";
+    o << "        __syncwarp();\n";
+    o << "        if (lane < 4) s_fl[lane] = 0u;\n";
+    o << "        __syncwarp();\n";
+    // per-lane pieces: head (before the first flag), complete inner rows, tail (from the last flag)
+    o << "        " << ACC << " h = " << IDENT << ", cur = " << IDENT << ";\n";
+    o << "        int curow = -1;\n";
+    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) {\n";
+    o << "          const long long P = P0 + k;\n";
+    o << "          if (rof[k] >= 0) {\n";
+    o << "            if (curow >= 0) s_racc[curow] = cur;            // a row that started and ended in this lane\n";
+    o << "            curow = rof[k];\n";
+    o << "            cur = " << IDENT << ";\n";
+    o << "          }\n";
+    o << "          if (P >= ps && P < pe) {\n";
+    o << "            const " << ACC << " m_ = (" << ACC << ")nbg_mul(a, P, v_[k]);\n";
+    o << "            if (curow >= 0) cur = NBG_ADD(cur, m_); else h = NBG_ADD(h, m_);\n";
+    o << "          }\n";
+    o << "        }\n";
+    o << "        const bool hf = fb != 0;\n";
+    // segmented inclusive scan of (value, has-flag) over lanes; lane 0 starts from the carry
+    o << "        " << ACC << " S = hf ? cur : h;\n";
+    o << "        if (lane == 0 && !hf) S = NBG_ADD(carry, S);\n";
+    o << "        bool F = hf || lane == 0;\n";
+    o << "        int rid = hf ? curow : (lane == 0 ? crow : -1);\n";
+    o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
+    o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
+    o << "          const bool Fy = __shfl_up_sync(0xffffffffu, F, d);\n";
+    o << "          const int ry = __shfl_up_sync(0xffffffffu, rid, d);\n";
+    o << "          if (lane >= d && !F) { S = NBG_ADD(Sy, S); F = Fy; rid = ry; }\n";
+    o << "        }\n";
+    // the row that ends at my first flag: left neighbour's running value + my head
+    o << "        " << ACC << " Sl = __shfl_up_sync(0xffffffffu, S, 1);\n";
+    o << "        int rl = __shfl_up_sync(0xffffffffu, rid, 1);\n";
+    o << "        if (lane == 0) { Sl = carry; rl = crow; }\n";
+    o << "        if (hf && rl >= 0) s_racc[rl] = NBG_ADD(Sl, h);\n";
+    o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
+    o << "        crow = __shfl_sync(0xffffffffu, rid, 31);\n";
     o << "      }\n";
+    o << "      if (lane == 0 && crow >= 0) s_racc[crow] = carry;\n";
     o << "      __syncwarp();\n";
     for (int j : fplus) o << "      r" << j << " = 0.0;\n";
-    o << "      " << ACC << " acc = " << IDENT << ";\n";
-    o << "      if (valid && len <= 32) {\n";
-    o << "        int q = (int)(o0 - a0);\n";
-    o << "        const int qe = (int)(o1f - a0);\n";
-    o << "        for (; q + 8 <= qe; q += 8) {\n";
-    o << "          " << XT << " v_[8];\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 8; u++) { const int c = s_ci[q + u]; v_[u] = NBG_GX(c); }\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 8; u++) acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, a0 + q + u, v_[u]));\n";
-    o << "        }\n";
-    o << "        for (; q < qe; q++) { const int c = s_ci[q]; acc = NBG_ADD(acc, (" << ACC << ")nbg_mul(a, a0 + q, NBG_GX(c))); }\n";
-    o << "      }\n";
-    o << "      unsigned mask = __ballot_sync(0xffffffffu, valid && len > 32);\n";
-    o << "      while (mask) {\n";
-    o << "        const int m = __ffs(mask) - 1;\n";
-    o << "        mask &= mask - 1;\n";
-    o << "        const int mq0 = (int)(__shfl_sync(0xffffffffu, o0, m) - a0), mq1 = (int)(__shfl_sync(0xffffffffu, o1f, m) - a0);\n";
-    o << "        " << ACC << " t = " << IDENT << ";\n";
-    o << "        for (int q0 = mq0 + lane; q0 < mq1; q0 += 128) {\n";
-    o << "          " << XT << " v_[4];\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const int q = q0 + u * 32; if (q < mq1) v_[u] = NBG_GX(s_ci[q]); }\n";
-    o << "          #pragma unroll\n          for (int u = 0; u < 4; u++) { const int q = q0 + u * 32; if (q < mq1) t = NBG_ADD(t, (" << ACC
-      << ")nbg_mul(a, a0 + q, v_[u])); }\n";
-    o << "        }\n";
-    o << "        for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
-    o << "        t = __shfl_sync(0xffffffffu, t, 0);\n";
-    o << "        if (lane == m) acc = t;\n";
-    o << "      }\n";
     o << "      if (valid) {\n";
+    o << "        const " << ACC << " acc = s_racc[lane];\n";
     o << "        const long long i = (long long)tl.x + lane;\n";
     g.emit_body(
         "        ",
@@ -527,7 +554,6 @@ int gen_spmv(Gen &g, const std::string &kname) {
         [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
     o << "      }\n";
-    // task-scoped exact combine of the floating PLUS reductions
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
         o << "      { double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f
@@ -537,7 +563,6 @@ int gen_spmv(Gen &g, const std::string &kname) {
     o << "    }\n";
     o << "  }\n";
     o << "  __syncthreads();\n";
-    // per-CTA combine: float PLUS limbs (integer sums) -> global atomics; the rest as before
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
         o << "  if (threadIdx.x < 11) {\n";
@@ -564,12 +589,12 @@ int gen_spmv(Gen &g, const std::string &kname) {
 
 extern const char *NBG_PRELUDE_SRC;
 
-std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem) {
+std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem, int *hot_entries) {
     Gen g(p);
     g.o << NBG_PRELUDE_SRC << "\n// ---- generated region: " << p.signature() << "\n";
     int smem = 0;
     if (p.spmv)
-        smem = gen_spmv(g, kname);
+        smem = gen_spmv(g, kname, hot_entries);
     else
         gen_ewise(g, kname, p.vec);
     if (dyn_smem) *dyn_smem = smem;

@@ -19,10 +19,10 @@ namespace nbg {
 namespace {
 
 constexpr int SP_TILE = 2048;    // merge items (rows + nonzeros) per tile
-constexpr int SP_LONG = 512;     // rows with more nonzeros are processed as chunks
-constexpr int SP_CHUNK = 512;    // nonzeros per chunk of a long row (one warp)
+constexpr int SP_LONG = 2048;    // rows with more nonzeros are processed as chunks
+constexpr int SP_CHUNK = 2048;   // nonzeros per chunk of a long row (one warp)
 constexpr int SP_TASK_ROWS = 32;  // rows per warp task (one per lane)
-constexpr int SP_TASK_NNZ = 512;  // nonzero budget of a warp task (= its staging buffer)
+constexpr int SP_TASK_NNZ = 2048; // nonzero budget of a warp task
 
 __device__ __forceinline__ unsigned long long sm64(unsigned long long key, unsigned long long k) {
     unsigned long long z = key + (k + 1ull) * 0x9E3779B97F4A7C15ull;

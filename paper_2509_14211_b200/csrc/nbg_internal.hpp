@@ -247,6 +247,7 @@ struct Kernel {
     cudaKernel_t k = nullptr;
     int block = 256;
     int smem = 0;            // dynamic shared memory per CTA
+    int hot = 0;             // spmv: capacity of the hot-column cache (entries)
     int grid_cap = 0;        // persistent grid size (SMs * resident CTAs)
     std::string name;
 };
@@ -335,7 +336,7 @@ double scalar_read(Ctx &c, const NodeP &s);
 void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
 
 // codegen / jit
-std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr);
+std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
 KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0);
 void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);
 

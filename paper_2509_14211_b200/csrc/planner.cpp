@@ -495,11 +495,6 @@ void ensure_full(Ctx &c, const NodeP &v) {
 
 // ---------------------------------------------------------------- launch of one region
 
-// hot-cache capacity (entries) of a generated SpMV kernel: its whole dynamic shared memory
-static long long hot_capacity(const Kernel &k, const Prog &p) {
-    return (long long)k.smem / (long long)type_size(p.sp.xt);
-}
-
 struct HintOut {
     NodeP node;       // instantiated template root (pending until launch)
     MatP scatter;     // written in this matrix's gather layout (memo key PERM<A>(...))
@@ -586,9 +581,10 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     if (it == c.plans.end()) {
         char nm[48];
         snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.spmv ? "spmv" : "ewise", (unsigned long long)hash_str(sig));
-        int smem = 0;
-        std::string src = codegen(p, nm, &smem);
+        int smem = 0, hot = 0;
+        std::string src = codegen(p, nm, &smem, &hot);
         kern = jit_compile(c, src, nm, p.spmv, smem);
+        kern->hot = hot;
         c.plans[sig] = kern;
         c.stats.plans_built++;
     } else {
@@ -596,8 +592,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         c.stats.plan_hits++;
     }
     if (p.spmv) {
-        const long long cap = (long long)(kern->smem - 0) > 0 ? hot_capacity(*kern, p) : 0;
-        if (args.hc > cap) args.hc = cap;
+        if (args.hc > kern->hot) args.hc = kern->hot;
     }
     if (items > 0 && n > 0) launch(c, *kern, args, items, p.spmv ? "spmv" : "ewise");
 
