@@ -127,6 +127,7 @@ __device__ double nbg_xacc_value(const u64 *L) {
     if (flags & 4ull) return __longlong_as_double((long long)0xfff0000000000000ull);
     unsigned w[11];
     long long carry = 0;
+    #pragma unroll
     for (int k = 0; k < 10; k++) {
         long long v = (long long)L[k] + carry;
         w[k] = (unsigned)(v & 0xffffffffll);
@@ -136,24 +137,35 @@ __device__ double nbg_xacc_value(const u64 *L) {
     bool neg = carry < 0;
     if (neg) {
         unsigned c = 1;
+        #pragma unroll
         for (int k = 0; k < 11; k++) { unsigned long long t = (unsigned long long)(~w[k]) + c; w[k] = (unsigned)t; c = (unsigned)(t >> 32); }
     }
+    // word-level extraction of the top 64 bits (no bit loops): top word h, its top bit tb
     int h = -1;
-    for (int k = 10; k >= 0; k--) if (w[k]) { h = k; break; }
+    #pragma unroll
+    for (int k = 10; k >= 0; k--) if (h < 0 && w[k]) h = k;
     if (h < 0) return 0.0;
-    int g = h * 32 + (31 - __clz(w[h]));        // index of the top set bit
-    u64 top = 0;
-    for (int j = 0; j < 64; j++) {
-        int b = g - j;
-        u64 bit = (b >= 0) ? ((w[b >> 5] >> (b & 31)) & 1u) : 0u;
-        top = (top << 1) | bit;
-    }
+    unsigned wh = 0, wm = 0, wl = 0;
     bool sticky = false;
-    for (int b = g - 64; b >= 0; b--) if ((w[b >> 5] >> (b & 31)) & 1u) { sticky = true; break; }
+    #pragma unroll
+    for (int k = 0; k < 11; k++) {
+        if (k == h) wh = w[k];
+        else if (k == h - 1) wm = w[k];
+        else if (k == h - 2) wl = w[k];
+        else if (k < h - 2 && w[k]) sticky = true;
+    }
+    const int tb = 31 - __clz(wh);                   // top set bit inside wh
+    const int sh = 31 - tb;                          // left shift that puts it at bit 63
+    const u64 hi64 = ((u64)wh << 32) | (u64)wm;
+    u64 top = sh ? ((hi64 << sh) | ((u64)wl >> (32 - sh))) : hi64;
+    const u64 lowmask = sh ? ((1ull << (32 - sh)) - 1ull) : 0xffffffffull;
+    if ((u64)wl & lowmask) sticky = true;
+    const int g = h * 32 + tb;
     u64 mant = top >> 11;
     u64 rb = top & 0x7ffull;
+    if (rb & 0x3ffull) sticky = true;
     int lsb = g - 52;
-    if (rb > 0x400ull || (rb == 0x400ull && (sticky || (mant & 1ull)))) {
+    if ((rb & 0x400ull) && (sticky || (mant & 1ull))) {
         mant += 1;
         if (mant == (1ull << 53)) { mant >>= 1; lsb += 1; }
     }

@@ -139,20 +139,23 @@ double xacc_to_double(const unsigned long long *L) {
     for (int k = 10; k >= 0; k--)
         if (w[k]) { h = k; break; }
     if (h < 0) return 0.0;
-    int g = h * 32 + (31 - __builtin_clz(w[h]));
-    unsigned long long top = 0;
-    for (int j = 0; j < 64; j++) {
-        int b = g - j;
-        unsigned long long bit = (b >= 0) ? ((w[b >> 5] >> (b & 31)) & 1u) : 0u;
-        top = (top << 1) | bit;
-    }
+    // word-level extraction of the top 64 bits (same arithmetic as prelude.cuh)
+    const uint32_t wh = w[h], wm = h >= 1 ? w[h - 1] : 0u, wl = h >= 2 ? w[h - 2] : 0u;
     bool sticky = false;
-    for (int b = g - 64; b >= 0; b--)
-        if ((w[b >> 5] >> (b & 31)) & 1u) { sticky = true; break; }
+    for (int k = 0; k < h - 2; k++)
+        if (w[k]) sticky = true;
+    const int tb = 31 - __builtin_clz(wh);
+    const int sh = 31 - tb;
+    const unsigned long long hi64 = ((unsigned long long)wh << 32) | (unsigned long long)wm;
+    unsigned long long top = sh ? ((hi64 << sh) | ((unsigned long long)wl >> (32 - sh))) : hi64;
+    const unsigned long long lowmask = sh ? ((1ull << (32 - sh)) - 1ull) : 0xffffffffull;
+    if ((unsigned long long)wl & lowmask) sticky = true;
+    const int g = h * 32 + tb;
     unsigned long long mant = top >> 11;
     unsigned long long rb = top & 0x7ffull;
+    if (rb & 0x3ffull) sticky = true;
     int lsb = g - 52;
-    if (rb > 0x400ull || (rb == 0x400ull && (sticky || (mant & 1ull)))) {
+    if ((rb & 0x400ull) && (sticky || (mant & 1ull))) {
         mant += 1;
         if (mant == (1ull << 53)) { mant >>= 1; lsb += 1; }
     }

@@ -167,3 +167,11 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
     if (out && len) snprintf(out, len, "%s", log.c_str());
     return fails;
 }
+
+// host twin of the exact accumulator: sum of n doubles through the fixed-point limbs, decoded
+// with round-to-nearest-even (CPU-testable against math.fsum).
+extern "C" double nbg_debug_xacc_sum(const double *v, long long n) {
+    unsigned long long limbs[SLOT_U64] = {0};
+    for (long long i = 0; i < n; i++) host_xacc_add(limbs, v[i]);
+    return xacc_to_double(limbs);
+}
