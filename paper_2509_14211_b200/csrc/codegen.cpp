@@ -331,17 +331,19 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
 
 static int redkind(const Gen &g, const RedOut &r) { return g.redkind(r).kind; }
 
-// SpMV skeleton v5.  One CTA of 1024 threads per SM; the CTA owns tasks
-// b, b + G, b + 2G, ... (G = grid size); its 32 warps pull them from a shared-memory counter.
-//   row task  (<= 32 consecutive rows, <= NBG_TASK nonzeros): the warp streams the task's
-//             nonzeros in steps of 128: lane l loads indices [base + 4l, base + 4l + 4) with one
-//             16-byte load (fully coalesced), gathers the 4 values (hot-column cache in shared
-//             memory first, else L1/L2) and reduces them by row with a segmented warp scan
-//             (row starts marked in a per-warp bitmap).  Row totals land in a per-warp array;
-//             lane j then runs the fused epilogue for row rb + j (coalesced loads/stores).
-//   chunk task (NBG_TASK nonzeros of a longer row): same 16-byte streaming, lane-sequential
-//             partials + fixed shuffle tree -> chunk partial; the warp that completes the row's
-//             last chunk (atomic ticket) sums the chunk partials in chunk order, runs the epilogue.
+// SpMV skeleton v6.  The matrix plan stores every row padded to 4-entry
+// groups (index -1 = padding), so one 16-byte index load never mixes two rows.  One CTA of 1024
+// threads per SM; the CTA owns tasks b, b + G, ... (G = grid size) and its 32 warps pull them
+// from a shared-memory counter.
+//   row task  (<= 32 consecutive rows, <= 512 groups): the warp streams the task's groups, lane l
+//             owning group base + l (one row) per step; the next step's indices are prefetched;
+//             the 4 gathers per lane are predicated loads (hot-column cache in shared memory, else
+//             L1/L2).  Row starts/ends of the step are two warp OR-reductions; a segmented warp
+//             scan keyed by those starts combines lane sums into row totals (carry across steps).
+//             Lane j then runs the fused epilogue for row rb + j (coalesced loads/stores).
+//   chunk task (512 groups of a longer row): lane-strided 16-entry batches, fixed shuffle tree ->
+//             chunk partial; the warp that completes the row's last chunk (atomic ticket) sums
+//             the chunk partials in chunk order and runs the epilogue.
 // Floating PLUS reductions of the epilogue are summed per task in fp64 (fixed tree) and the task
 // partials added EXACTLY into per-warp fixed-point limbs, so the dynamic task order changes
 // nothing: every result is deterministic.  Summation order inside a row is fixed by the matrix
@@ -392,42 +394,53 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
     const int NF = (int)fplus.size();
     const int accw = (ACC == "double" || ACC == "long long") ? 8 : 4;
-    const int warp_bytes = 32 * 8 + 16 + 128;                 // row totals, flag bitmap, row-of-position
+    const int warp_bytes = 32 * 8;                            // row totals of the task
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
-    int hot_bytes = 227 * 1024 - 2048 - 32 * warp_bytes - xacc_bytes;
-    if (hot_bytes > 200 * 1024) hot_bytes = 200 * 1024;
+    int hot_bytes = 160 * 1024;                               // measured sweet spot
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
-    if (hot_cap < 0) hot_cap = 0;
-    const int dyn_bytes = hot_cap * x_bytes + 32 * warp_bytes + xacc_bytes;
+    const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
+    const int dyn_bytes = hot_region + 32 * warp_bytes + xacc_bytes;
     if (hot_entries) *hot_entries = hot_cap;
     (void)accw;
+    // gathered element: predicated shared/global load of the raw bits, reinterpreted as XT
+    std::string gx;
+    switch (sp.xt) {
+        case NBG_FP32: gx = "__uint_as_float(nbg_gx32(s_base, X, C_, hc))"; break;
+        case NBG_INT32: gx = "((int)nbg_gx32(s_base, X, C_, hc))"; break;
+        case NBG_FP64: gx = "__longlong_as_double((long long)nbg_gx64(s_base, X, C_, hc))"; break;
+        case NBG_INT64: gx = "((long long)nbg_gx64(s_base, X, C_, hc))"; break;
+        default: gx = "((C_) < hc ? s_hot[(C_)] : X[(C_)])"; break;
+    }
 
     o << "#define NBG_HOT_CAP " << hot_cap << "\n#define NBG_NF " << NF << "\n";
     o << "#define NBG_ADD(A_, B_) " << ADD << "\n";
     o << "__device__ __forceinline__ " << VT << " nbg_mul(const KArgs &a, long long P_, " << XT << " X_) { return " << mul
       << "; }\n";
+    // one padded position: index c (-1 = padding) at position P_ -> term of the row's sum
+    o << "#define NBG_TERM(C_, P_) (((C_) >= 0) ? (" << ACC << ")nbg_mul(a, (P_), nbg_gxv(s_base, s_hot, X, (C_), hc)) : (" << ACC
+      << ")(" << IDENT << "))\n";
+    o << "__device__ __forceinline__ " << XT << " nbg_gxv(unsigned s_base, const " << XT << "* s_hot, const " << XT
+      << "* X, int C_, int hc) { return " << gx << "; }\n";
     o << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << kname << "(const KArgs a) {\n";
     o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
     o << "  __shared__ double nbg_sh[32];\n";
     o << "  __shared__ int s_ctr;\n";
     o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
+    o << "  const unsigned s_base = (unsigned)__cvta_generic_to_shared(nbg_dyn);\n";
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    o << "  unsigned char* s_w = nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + warp * " << warp_bytes << ";\n";
-    o << "  " << ACC << "* s_racc = (" << ACC << "*)s_w;                 // [32] row totals of the task\n";
-    o << "  unsigned* s_fl = (unsigned*)(s_w + 256);                     // [4] row-start bitmap of the step\n";
-    o << "  unsigned char* s_rof = s_w + 272;                            // [128] row of a row-start position\n";
+    o << "  " << ACC << "* s_racc = (" << ACC << "*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << ");   // [32] row totals\n";
     if (NF)
-        o << "  u64* s_x = (u64*)(nbg_dyn + NBG_HOT_CAP * sizeof(" << XT << ") + 32 * " << warp_bytes << ");   // [warp][NF][11]\n";
+        o << "  u64* s_x = (u64*)(nbg_dyn + " << hot_region << " + 32 * " << warp_bytes << ");   // [warp][NF][11]\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
+    o << "  const int4* __restrict__ CG = (const int4*)a.colidx;\n";
+    o << "  const long long* __restrict__ GRP = a.rowptr;\n";
     o << "  const int hc = (int)a.hc;\n";
     o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
     if (NF) o << "  for (int k = threadIdx.x; k < 32 * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
-    o << "  if (lane < 4) s_fl[lane] = 0u;\n";
-    o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = __ldg(X + k);\n";
+    o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = X[k];\n";
     o << "  __syncthreads();\n";
-    o << "#define NBG_GX(c_) ((c_) < hc ? s_hot[(c_)] : __ldg(X + (c_)))\n";
     g.emit_uniform();
     g.emit_red_decl();
     o << "  const long long items = a.nchunks + a.ntiles;\n";
@@ -440,18 +453,20 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     // ---------------- chunk of a long row
     o << "    if (it < a.nchunks) {\n";
     o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
-    o << "      const long long pb = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
-    o << "      const long long pe = pb + ch.w;\n";
+    o << "      const long long g0 = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
+    o << "      const int cnt = ch.w;\n";
     o << "      " << ACC << " t = " << IDENT << ";\n";
-    o << "      for (long long base = pb & ~3ll; base < pe; base += 128) {\n";
-    o << "        const long long P0 = base + 4 * lane;\n";
-    o << "        int c_[4];\n";
-    o << "        if (P0 + 3 < a.nnz) { const int4 q4 = __ldcs((const int4*)(a.colidx + P0)); c_[0] = q4.x; c_[1] = q4.y; c_[2] = q4.z; c_[3] = q4.w; }\n";
-    o << "        else { for (int k = 0; k < 4; k++) c_[k] = (P0 + k < a.nnz) ? __ldcs(a.colidx + P0 + k) : 0; }\n";
-    o << "        " << XT << " v_[4];\n";
-    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) { const long long P = P0 + k; if (P >= pb && P < pe) v_[k] = NBG_GX(c_[k]); }\n";
-    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) { const long long P = P0 + k; if (P >= pb && P < pe) t = NBG_ADD(t, (" << ACC
-      << ")nbg_mul(a, P, v_[k])); }\n";
+    o << "      for (int b = 0; b < cnt; b += 128) {\n";
+    o << "        int4 q[4];\n";
+    o << "        #pragma unroll\n        for (int v = 0; v < 4; v++) { const int gi = b + lane + 32 * v; q[v] = gi < cnt ? __ldcs(CG + g0 + gi) : make_int4(-1, -1, -1, -1); }\n";
+    o << "        " << ACC << " u_[4];\n";
+    o << "        #pragma unroll\n        for (int v = 0; v < 4; v++) {\n";
+    o << "          const long long P_ = 4 * (g0 + b + lane + 32 * v);\n";
+    o << "          " << ACC << " w_ = NBG_TERM(q[v].x, P_);\n";
+    o << "          w_ = NBG_ADD(w_, NBG_TERM(q[v].y, P_ + 1)); w_ = NBG_ADD(w_, NBG_TERM(q[v].z, P_ + 2)); w_ = NBG_ADD(w_, NBG_TERM(q[v].w, P_ + 3));\n";
+    o << "          u_[v] = w_;\n";
+    o << "        }\n";
+    o << "        t = NBG_ADD(t, NBG_ADD(NBG_ADD(u_[0], u_[1]), NBG_ADD(u_[2], u_[3])));\n";
     o << "      }\n";
     o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
     o << "      if (lane == 0) {\n";
@@ -480,74 +495,44 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "    {\n";
     o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
     o << "      const int R = tl.y - tl.x;\n";
-    o << "      const long long rs = __ldg(a.rowptr + tl.x + (lane < R ? lane : R));   // start of my row\n";
-    o << "      const long long nx_ = __shfl_down_sync(0xffffffffu, rs, 1);\n";
-    o << "      const long long re_ = (lane == 31) ? __ldg(a.rowptr + tl.x + (R < 32 ? R : 32)) : nx_;\n";
-    o << "      const long long ps = __shfl_sync(0xffffffffu, rs, 0);\n";
-    o << "      const long long pe = __shfl_sync(0xffffffffu, (lane == 31) ? re_ : rs, R < 32 ? R : 31);\n";
+    o << "      const long long gs = GRP[tl.x + (lane < R ? lane : R)];           // my row's first group (lane R: end)\n";
+    o << "      const long long gn_ = __shfl_down_sync(0xffffffffu, gs, 1);\n";
+    o << "      const long long ge = (lane == 31) ? GRP[tl.x + (R < 32 ? R : 32)] : gn_;\n";
+    o << "      const long long G0 = __shfl_sync(0xffffffffu, gs, 0);\n";
+    o << "      const long long G1 = __shfl_sync(0xffffffffu, (lane == 31) ? ge : gs, R < 32 ? R : 31);\n";
     o << "      const bool valid = lane < R;\n";
-    o << "      const bool nonempty = valid && re_ > rs;\n";
-    o << "      s_racc[lane] = " << IDENT << ";\n";
-    o << "      __syncwarp();\n";
+    o << "      const bool nonempty = valid && ge > gs;\n";
+    o << "      const unsigned nem = __ballot_sync(0xffffffffu, nonempty);\n";
+    o << "      const int rgs = (int)(gs - G0), rge = (int)(ge - G0) - 1;     // my row's first / last group\n";
+    o << "      const int NG = (int)(G1 - G0);\n";
     o << "      " << ACC << " carry = " << IDENT << ";\n";
-    o << "      int crow = -1;                      // row open at the left edge of the step\n";
-    o << "      for (long long base = ps & ~3ll; base < pe; base += 128) {\n";
-    o << "        const long long P0 = base + 4 * lane;\n";
-    o << "        int c_[4];\n";
-    o << "        if (P0 + 3 < a.nnz) { const int4 q4 = __ldcs((const int4*)(a.colidx + P0)); c_[0] = q4.x; c_[1] = q4.y; c_[2] = q4.z; c_[3] = q4.w; }\n";
-    o << "        else { for (int k = 0; k < 4; k++) c_[k] = (P0 + k < a.nnz) ? __ldcs(a.colidx + P0 + k) : 0; }\n";
-    o << "        " << XT << " v_[4];\n";
-    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) { const long long P = P0 + k; if (P >= ps && P < pe) v_[k] = NBG_GX(c_[k]); }\n";
-    // mark row starts of this step
-    o << "        if (nonempty && rs >= base && rs < base + 128) { const int pos = (int)(rs - base); atomicOr(&s_fl[pos >> 5], 1u << (pos & 31)); s_rof[pos] = (unsigned char)lane; }\n";
-    o << "        __syncwarp();\n";
-    o << "        const unsigned fw = s_fl[lane >> 3];\n";
-    o << "        const int fb = (fw >> ((lane & 7) * 4)) & 15;     // flags of my 4 positions\n";
-    o << "        int rof[4];\n";
-    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) rof[k] = ((fb >> k) & 1) ? (int)s_rof[4 * lane + k] : -1;\n";
-    o << "        __syncwarp();\n";
-    o << "        if (lane < 4) s_fl[lane] = 0u;\n";
-    o << "        __syncwarp();\n";
-    // per-lane pieces: head (before the first flag), complete inner rows, tail (from the last flag)
-    o << "        " << ACC << " h = " << IDENT << ", cur = " << IDENT << ";\n";
-    o << "        int curow = -1;\n";
-    o << "        #pragma unroll\n        for (int k = 0; k < 4; k++) {\n";
-    o << "          const long long P = P0 + k;\n";
-    o << "          if (rof[k] >= 0) {\n";
-    o << "            if (curow >= 0) s_racc[curow] = cur;            // a row that started and ended in this lane\n";
-    o << "            curow = rof[k];\n";
-    o << "            cur = " << IDENT << ";\n";
-    o << "          }\n";
-    o << "          if (P >= ps && P < pe) {\n";
-    o << "            const " << ACC << " m_ = (" << ACC << ")nbg_mul(a, P, v_[k]);\n";
-    o << "            if (curow >= 0) cur = NBG_ADD(cur, m_); else h = NBG_ADD(h, m_);\n";
-    o << "          }\n";
-    o << "        }\n";
-    o << "        const bool hf = fb != 0;\n";
-    // segmented inclusive scan of (value, has-flag) over lanes; lane 0 starts from the carry
-    o << "        " << ACC << " S = hf ? cur : h;\n";
-    o << "        if (lane == 0 && !hf) S = NBG_ADD(carry, S);\n";
-    o << "        bool F = hf || lane == 0;\n";
-    o << "        int rid = hf ? curow : (lane == 0 ? crow : -1);\n";
+    o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
+    o << "      int4 q = (lane < NG) ? __ldcs(CG + G0 + lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "      for (int b = 0; b < NG; b += 32) {\n";
+    o << "        const long long P_ = 4 * (G0 + b + lane);\n";
+    o << "        const int4 qc = q;\n";
+    o << "        if (b + 32 < NG) q = (b + 32 + lane < NG) ? __ldcs(CG + G0 + b + 32 + lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "        " << ACC << " S = NBG_TERM(qc.x, P_);\n";
+    o << "        S = NBG_ADD(S, NBG_TERM(qc.y, P_ + 1)); S = NBG_ADD(S, NBG_TERM(qc.z, P_ + 2)); S = NBG_ADD(S, NBG_TERM(qc.w, P_ + 3));\n";
+    o << "        const int os_ = rgs - b, oe_ = rge - b;\n";
+    o << "        const unsigned M = __reduce_or_sync(0xffffffffu, (nonempty && os_ >= 0 && os_ < 32) ? (1u << os_) : 0u);\n";
+    o << "        const unsigned Eb = __reduce_or_sync(0xffffffffu, (nonempty && oe_ >= 0 && oe_ < 32) ? (1u << oe_) : 0u);\n";
+    o << "        if (lane == 0 && !(M & 1u)) S = NBG_ADD(carry, S);\n";
+    o << "        bool F = ((M >> lane) & 1u) || lane == 0;\n";
     o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
     o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
     o << "          const bool Fy = __shfl_up_sync(0xffffffffu, F, d);\n";
-    o << "          const int ry = __shfl_up_sync(0xffffffffu, rid, d);\n";
-    o << "          if (lane >= d && !F) { S = NBG_ADD(Sy, S); F = Fy; rid = ry; }\n";
+    o << "          if (lane >= d && !F) { S = NBG_ADD(Sy, S); F = Fy; }\n";
     o << "        }\n";
-    // the row that ends at my first flag: left neighbour's running value + my head
-    o << "        " << ACC << " Sl = __shfl_up_sync(0xffffffffu, S, 1);\n";
-    o << "        int rl = __shfl_up_sync(0xffffffffu, rid, 1);\n";
-    o << "        if (lane == 0) { Sl = carry; rl = crow; }\n";
-    o << "        if (hf && rl >= 0) s_racc[rl] = NBG_ADD(Sl, h);\n";
-    o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
-    o << "        crow = __shfl_sync(0xffffffffu, rid, 31);\n";
+    o << "        if ((Eb >> lane) & 1u) s_racc[nstarted + __popc(M & ((2u << lane) - 1u)) - 1] = S;\n";
+    o << "        const " << ACC << " S31 = __shfl_sync(0xffffffffu, S, 31);\n";
+    o << "        carry = ((Eb >> 31) & 1u) ? (" << ACC << ")(" << IDENT << ") : S31;\n";
+    o << "        nstarted += __popc(M);\n";
     o << "      }\n";
-    o << "      if (lane == 0 && crow >= 0) s_racc[crow] = carry;\n";
     o << "      __syncwarp();\n";
     for (int j : fplus) o << "      r" << j << " = 0.0;\n";
     o << "      if (valid) {\n";
-    o << "        const " << ACC << " acc = s_racc[lane];\n";
+    o << "        const " << ACC << " acc = nonempty ? s_racc[__popc(nem & ((1u << lane) - 1u))] : (" << ACC << ")(" << IDENT << ");\n";
     o << "        const long long i = (long long)tl.x + lane;\n";
     g.emit_body(
         "        ",
@@ -581,7 +566,6 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         else
             o << "  nbg_block_finish_i(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
     }
-    o << "#undef NBG_GX\n";
     o << "}\n";
     return dyn_bytes;
 }

@@ -7,7 +7,6 @@
 //                            (DESIGN.md "K4 SpMV"), built once per matrix
 // Integer work only: results are bit-exact and deterministic (histogram atomics are integer).
 #include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <vector>
@@ -18,11 +17,12 @@ namespace nbg {
 
 namespace {
 
-constexpr int SP_TILE = 2048;    // merge items (rows + nonzeros) per tile
-constexpr int SP_LONG = 2048;    // rows with more nonzeros are processed as chunks
-constexpr int SP_CHUNK = 2048;   // nonzeros per chunk of a long row (one warp)
-constexpr int SP_TASK_ROWS = 32;  // rows per warp task (one per lane)
-constexpr int SP_TASK_NNZ = 2048; // nonzero budget of a warp task
+// SpMV plan in 4-entry groups: every row is padded to a multiple of 4
+// stored entries (padding index -1), so a 16-byte load never mixes two rows.
+constexpr int SP_LONG_G = 512;     // rows with more groups (> 2048 entries) are processed as chunks
+constexpr int SP_CHUNK_G = 512;    // groups per chunk of a long row (one warp)
+constexpr int SP_TASK_ROWS = 32;   // rows per warp task (one per lane)
+constexpr int SP_TASK_G = 512;     // group budget of a warp task
 
 __device__ __forceinline__ unsigned long long sm64(unsigned long long key, unsigned long long k) {
     unsigned long long z = key + (k + 1ull) * 0x9E3779B97F4A7C15ull;
@@ -97,34 +97,22 @@ __global__ void k_rowptr(long long n, long long nnz, int shift, const unsigned l
     }
 }
 
-// merge items per row for the tile plan: 1 + len for rows handled in tiles, 1 for long rows
-__global__ void k_eff(long long n, const long long *rowptr, long long *eff, unsigned char *is_long) {
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
-        if (i == n) { eff[i] = 0; continue; }
-        long long len = rowptr[i + 1] - rowptr[i];
-        bool lg = len > SP_LONG;
-        is_long[i] = lg ? 1 : 0;
-        eff[i] = lg ? 1 : 1 + len;
-    }
+// groups per row (4 stored entries per group, padded)
+__global__ void k_ngroups(long long n, const long long *rowptr, long long *ng) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x)
+        ng[i] = i == n ? 0 : (rowptr[i + 1] - rowptr[i] + 3) / 4;
 }
 
-// s[k] = smallest i in [0, n] with mc[i] >= k * D
-__global__ void k_tile_bounds(long long n, long long K, const long long *mc, int *s) {
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k <= K; k += (long long)gridDim.x * blockDim.x) {
-        long long target = k * (long long)SP_TILE;
-        long long lo = 0, hi = n;   // answer in [0, n]
-        while (lo < hi) {
+// scatter the stored entries of every row into its groups: dst[4 grp[row] + j] = src[rowptr[row] + j]
+template <class T>
+__global__ void k_fill_groups(long long nnz, long long n, const long long *rowptr, const long long *grp, const T *src, T *dst) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+        long long lo = 0, hi = n;          // row = last i with rowptr[i] <= p
+        while (hi - lo > 1) {
             long long mid = (lo + hi) >> 1;
-            if (mc[mid] >= target) hi = mid; else lo = mid + 1;
+            if (rowptr[mid] <= p) lo = mid; else hi = mid;
         }
-        s[k] = (int)lo;
-    }
-}
-
-__global__ void k_gather_rowptr(long long L, const int *rows, const long long *rowptr, long long *out) {
-    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L; j += (long long)gridDim.x * blockDim.x) {
-        out[2 * j] = rowptr[rows[j]];
-        out[2 * j + 1] = rowptr[rows[j] + 1];
+        dst[4 * grp[lo] + (p - rowptr[lo])] = src[p];
     }
 }
 
@@ -281,108 +269,10 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         A.plan = std::move(P);
         return;
     }
-    BufP eff = alloc_buf(c, (size_t)(n + 1) * 8);
-    BufP mc = alloc_buf(c, (size_t)(n + 1) * 8);
-    BufP isl = alloc_buf(c, (size_t)n);
-    k_eff<<<grid_for(n + 1, c.num_sms), 256, 0, c.stream>>>(n, (const long long *)A.rowptr->d, (long long *)eff->d,
-                                                            (unsigned char *)isl->d);
-    size_t tb = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)eff->d, (long long *)mc->d, (int64_t)(n + 1), c.stream);
-    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
-    NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)eff->d, (long long *)mc->d, (int64_t)(n + 1), c.stream));
-    long long total = 0;
-    NBG_CUDA(cudaMemcpyAsync(&total, (long long *)mc->d + n, 8, cudaMemcpyDeviceToHost, c.stream));
-    // long rows
-    BufP lrows = alloc_buf(c, (size_t)n * 4);
-    BufP nl = alloc_buf(c, 8);
-    size_t tb2 = 0;
-    thrust::counting_iterator<int> cnt(0);
-    cub::DeviceSelect::Flagged(nullptr, tb2, cnt, (unsigned char *)isl->d, (int *)lrows->d, (long long *)nl->d, (int64_t)n,
-                               c.stream);
-    if (tb2 > tmp->bytes) tmp = alloc_buf(c, tb2);
-    NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb2, cnt, (unsigned char *)isl->d, (int *)lrows->d, (long long *)nl->d,
-                                        (int64_t)n, c.stream));
-    long long L = 0;
-    NBG_CUDA(cudaMemcpyAsync(&L, nl->d, 8, cudaMemcpyDeviceToHost, c.stream));
-    NBG_CUDA(cudaStreamSynchronize(c.stream));
-    const long long K = (total + SP_TILE - 1) / SP_TILE;
-    BufP sb = alloc_buf(c, (size_t)(K + 1) * 4);
-    k_tile_bounds<<<grid_for(K + 1, c.num_sms), 256, 0, c.stream>>>(n, K, (const long long *)mc->d, (int *)sb->d);
-    std::vector<int> s(K + 1);
-    NBG_CUDA(cudaMemcpyAsync(s.data(), sb->d, (K + 1) * 4, cudaMemcpyDeviceToHost, c.stream));
-    std::vector<int> lr(L);
-    std::vector<long long> lrp(2 * L);
-    if (L > 0) {
-        BufP g = alloc_buf(c, (size_t)L * 16);
-        k_gather_rowptr<<<grid_for(L, c.num_sms), 256, 0, c.stream>>>(L, (const int *)lrows->d, (const long long *)A.rowptr->d,
-                                                                      (long long *)g->d);
-        NBG_CUDA(cudaMemcpyAsync(lr.data(), lrows->d, L * 4, cudaMemcpyDeviceToHost, c.stream));
-        NBG_CUDA(cudaMemcpyAsync(lrp.data(), g->d, L * 16, cudaMemcpyDeviceToHost, c.stream));
-    }
-    NBG_CUDA(cudaGetLastError());
-    NBG_CUDA(cudaStreamSynchronize(c.stream));
-
-    // warp tasks: runs of <= 32 consecutive non-long rows with <= SP_TASK_NNZ nonzeros (greedy,
-    // on the host from the row pointers; once per matrix)
-    std::vector<long long> rph((size_t)n + 1);
-    NBG_CUDA(cudaMemcpyAsync(rph.data(), A.rowptr->d, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
-    NBG_CUDA(cudaStreamSynchronize(c.stream));
-    std::vector<int> tiles;
-    tiles.reserve((size_t)(n / 16 + 16));
-    for (long long i = 0; i < n;) {
-        long long len = rph[i + 1] - rph[i];
-        if (len > SP_LONG) { i++; continue; }
-        long long st = i, nz = 0;
-        while (i < n && i - st < SP_TASK_ROWS) {
-            long long l2 = rph[i + 1] - rph[i];
-            if (l2 > SP_LONG) break;
-            if (i > st && nz + l2 > SP_TASK_NNZ) break;
-            nz += l2;
-            i++;
-        }
-        tiles.push_back((int)st);
-        tiles.push_back((int)i);
-    }
-    (void)s;
-    std::vector<int> chunks, longs;
-    long long nch_total = 0;
-    for (long long j = 0; j < L; j++) {
-        long long p0 = lrp[2 * j], p1 = lrp[2 * j + 1];
-        long long len = p1 - p0;
-        long long nch = (len + SP_CHUNK - 1) / SP_CHUNK;
-        longs.push_back(lr[j]);
-        longs.push_back((int)nch_total);
-        longs.push_back((int)nch);
-        longs.push_back(0);
-        for (long long q = 0; q < nch; q++) {
-            long long pb = p0 + q * SP_CHUNK;
-            long long cntq = std::min<long long>(SP_CHUNK, p1 - pb);
-            chunks.push_back((int)j);
-            chunks.push_back((int)(unsigned)(pb & 0xffffffffll));
-            chunks.push_back((int)(unsigned)((unsigned long long)pb >> 32));
-            chunks.push_back((int)cntq);
-        }
-        nch_total += nch;
-    }
-    P->ntiles = (int64_t)tiles.size() / 2;
-    P->nchunks = nch_total;
-    P->nlong = L;
-    if (!tiles.empty()) {
-        P->tiles = alloc_buf(c, tiles.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->tiles->d, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, c.stream));
-    }
-    if (!chunks.empty()) {
-        P->chunks = alloc_buf(c, chunks.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->chunks->d, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        P->longs = alloc_buf(c, longs.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->longs->d, longs.data(), longs.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        P->counters = alloc_buf(c, (size_t)L * 4);
-        NBG_CUDA(cudaMemsetAsync(P->counters->d, 0, (size_t)L * 4, c.stream));
-        P->partials = alloc_buf(c, (size_t)nch_total * 8);
-    }
-    // gather layout: relabel columns by descending count (big matrices only)
+    // ---- gather layout: relabel columns by descending count (big matrices only)
     const char *rl = getenv("NBG_RELABEL");
     const bool want = rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15));
+    BufP colsrc = A.colidx;
     if (want && A.nnz > 0 && !A.vals) {
         const long long nc = A.ncols;
         BufP cnt = alloc_buf(c, (size_t)nc * 4);
@@ -408,13 +298,99 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         P->iperm = alloc_buf(c, (size_t)std::max(ng, 1) * 4);
         NBG_CUDA(cudaMemcpyAsync(P->iperm->d, ids2->d, (size_t)ng * 4, cudaMemcpyDeviceToDevice, c.stream));
         k_perm_from_order<<<grid_for(ng, c.num_sms), 256, 0, c.stream>>>(ng, (const int *)ids2->d, (int *)P->perm->d);
-        P->colidx_g = alloc_buf(c, (size_t)A.nnz * 4);
+        colsrc = alloc_buf(c, (size_t)A.nnz * 4);
         k_map_cols<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (const int *)P->perm->d,
-                                                                     (int *)P->colidx_g->d);
+                                                                     (int *)colsrc->d);
         NBG_CUDA(cudaGetLastError());
         P->ncols_g = ng;
         P->relabel = true;
         c.stats.kernels_launched += 5;
+    }
+    // ---- 4-entry groups: grp[i] = first group of row i; cg = group-padded column indices (-1 pad)
+    BufP ngb = alloc_buf(c, (size_t)(n + 1) * 8);
+    P->grp = alloc_buf(c, (size_t)(n + 1) * 8);
+    k_ngroups<<<grid_for(n + 1, c.num_sms), 256, 0, c.stream>>>(n, (const long long *)A.rowptr->d, (long long *)ngb->d);
+    size_t tb = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)ngb->d, (long long *)P->grp->d, (int64_t)(n + 1), c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)ngb->d, (long long *)P->grp->d, (int64_t)(n + 1), c.stream));
+    std::vector<long long> gph((size_t)n + 1);
+    NBG_CUDA(cudaMemcpyAsync(gph.data(), P->grp->d, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    const long long G = gph[n];
+    P->ngroups = G;
+    P->cg = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * 4);
+    NBG_CUDA(cudaMemsetAsync(P->cg->d, 0xff, (size_t)std::max<long long>(4 * G, 4) * 4, c.stream));
+    if (A.nnz > 0)
+        k_fill_groups<int><<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, n, (const long long *)A.rowptr->d,
+                                                                             (const long long *)P->grp->d, (const int *)colsrc->d,
+                                                                             (int *)P->cg->d);
+    if (A.vals) {
+        const size_t es = type_size(A.type);
+        P->vals_g = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * es);
+        NBG_CUDA(cudaMemsetAsync(P->vals_g->d, 0, (size_t)std::max<long long>(4 * G, 4) * es, c.stream));
+        if (A.nnz > 0) {
+            const long long *rp = (const long long *)A.rowptr->d, *gp = (const long long *)P->grp->d;
+            const int gr = grid_for(A.nnz, c.num_sms);
+            if (es == 1) k_fill_groups<unsigned char><<<gr, 256, 0, c.stream>>>(A.nnz, n, rp, gp, (const unsigned char *)A.vals->d, (unsigned char *)P->vals_g->d);
+            else if (es == 4) k_fill_groups<int><<<gr, 256, 0, c.stream>>>(A.nnz, n, rp, gp, (const int *)A.vals->d, (int *)P->vals_g->d);
+            else k_fill_groups<long long><<<gr, 256, 0, c.stream>>>(A.nnz, n, rp, gp, (const long long *)A.vals->d, (long long *)P->vals_g->d);
+        }
+    }
+    NBG_CUDA(cudaGetLastError());
+    c.stats.kernels_launched += 3;
+
+    // ---- warp tasks (host, once per matrix): runs of <= 32 consecutive non-long rows with
+    // <= SP_TASK_G groups; long rows (> SP_LONG_G groups) are cut into chunks of SP_CHUNK_G groups
+    std::vector<int> tiles, chunks, longs;
+    tiles.reserve((size_t)(n / 16 + 16));
+    long long nch_total = 0, L = 0;
+    for (long long i = 0; i < n;) {
+        long long gl = gph[i + 1] - gph[i];
+        if (gl > SP_LONG_G) {
+            long long nch = (gl + SP_CHUNK_G - 1) / SP_CHUNK_G;
+            longs.push_back((int)i);
+            longs.push_back((int)nch_total);
+            longs.push_back((int)nch);
+            longs.push_back(0);
+            for (long long q = 0; q < nch; q++) {
+                long long gb = gph[i] + q * SP_CHUNK_G;
+                chunks.push_back((int)L);
+                chunks.push_back((int)(unsigned)(gb & 0xffffffffll));
+                chunks.push_back((int)(unsigned)((unsigned long long)gb >> 32));
+                chunks.push_back((int)std::min<long long>(SP_CHUNK_G, gph[i + 1] - gb));
+            }
+            nch_total += nch;
+            L++;
+            i++;
+            continue;
+        }
+        long long st = i, ngr = 0;
+        while (i < n && i - st < SP_TASK_ROWS) {
+            long long g2 = gph[i + 1] - gph[i];
+            if (g2 > SP_LONG_G) break;
+            if (i > st && ngr + g2 > SP_TASK_G) break;
+            ngr += g2;
+            i++;
+        }
+        tiles.push_back((int)st);
+        tiles.push_back((int)i);
+    }
+    P->ntiles = (int64_t)tiles.size() / 2;
+    P->nchunks = nch_total;
+    P->nlong = L;
+    if (!tiles.empty()) {
+        P->tiles = alloc_buf(c, tiles.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->tiles->d, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    }
+    if (!chunks.empty()) {
+        P->chunks = alloc_buf(c, chunks.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->chunks->d, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        P->longs = alloc_buf(c, longs.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->longs->d, longs.data(), longs.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        P->counters = alloc_buf(c, (size_t)L * 4);
+        NBG_CUDA(cudaMemsetAsync(P->counters->d, 0, (size_t)L * 4, c.stream));
+        P->partials = alloc_buf(c, (size_t)nch_total * 8);
     }
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     A.plan = std::move(P);

@@ -113,24 +113,25 @@ double slot_value(const unsigned long long *s, SFmt fmt);
 // ---------------------------------------------------------------- matrices
 
 struct SpmvPlan {
-    // Tiles: contiguous row ranges of "short/medium" rows, balanced by merge items (rows+nnz).
-    // Long rows (len > LONG) are cut into chunks of CHUNK nonzeros processed by their own CTAs;
-    // the CTA that finishes a long row's last chunk (atomic ticket) combines the chunk partials
-    // in chunk order and runs the epilogue.  DESIGN.md "K4 SpMV".
-    int64_t ntiles = 0, nchunks = 0, nlong = 0;
+    // Rows are stored in 4-entry groups (padded with index -1) so a 16-byte index load never mixes
+    // two rows.  Tiles: runs of <= 32 consecutive rows with <= 512 groups (one warp task, lane j ->
+    // row j).  Long rows (> 512 groups) are cut into chunks of 512 groups processed by separate
+    // warps; the warp that finishes a long row's last chunk (atomic ticket) combines the chunk
+    // partials in chunk order and runs the epilogue.  DESIGN.md "K4 SpMV".
+    int64_t ntiles = 0, nchunks = 0, nlong = 0, ngroups = 0;
+    BufP grp;        // int64[n + 1]  first group of each row
+    BufP cg;         // int32[4 * ngroups]  column index per padded position (gather layout), -1 = pad
+    BufP vals_g;     // values per padded position (valued matrices only)
     BufP tiles;      // int2  {row_begin, row_end}
-    BufP chunks;     // int4  {long_idx, first_p_lo, first_p_hi, count}   (p = 64-bit begin)
+    BufP chunks;     // int4  {long_idx, first_group_lo, first_group_hi, ngroups}
     BufP longs;      // int4  {row, first_chunk, nchunks, 0}
     BufP counters;   // int[nlong], zero between launches
     BufP partials;   // double[nchunks]
-    int max_tile_vals = 0;   // max nonzeros in one tile (shared-memory bound)
-    int max_tile_rows = 0;
     // Gather layout: columns renumbered by descending column count,
     // empty columns dropped.  The gathered vector is stored in that order so the hot entries are
-    // dense (cache-line reuse) while every row keeps its summation order (bit-identical sums).
+    // dense and the first ones fit a shared-memory cache; rows keep their entry order.
     bool relabel = false;
     int64_t ncols_g = 0;     // number of non-empty columns
-    BufP colidx_g;           // int32[nnz]  relabelled column indices
     BufP perm;               // int32[ncols] old -> new id, -1 for an empty column
     BufP iperm;              // int32[ncols_g] new -> old id
 };

@@ -556,9 +556,9 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         p.sp.has_vals = (bool)A.vals;
         B.imm[0] = A.iso;
         B.imm[1] = mx.c0;
-        args.rowptr = (const long long *)A.rowptr->d;
-        args.colidx = (const int *)(A.plan->relabel ? A.plan->colidx_g->d : A.colidx->d);
-        args.aval = A.vals ? A.vals->d : nullptr;
+        args.rowptr = (const long long *)A.plan->grp->d;      // group-padded layout (graph.cu plan)
+        args.colidx = (const int *)A.plan->cg->d;
+        args.aval = A.vals ? A.plan->vals_g->d : nullptr;
         args.x = B.mxv_x->d;
         args.tiles = (const int *)(A.plan->tiles ? A.plan->tiles->d : nullptr);
         args.chunks = (const int *)(A.plan->chunks ? A.plan->chunks->d : nullptr);
@@ -568,7 +568,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
         items = (A.plan->ntiles + A.plan->nchunks + 31) / 32;   // one task per warp, 32 warps per CTA
-        args.nnz = A.nnz;
+        args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
     } else {
         items = (n + 1023) / 1024;

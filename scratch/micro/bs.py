@@ -1,0 +1,38 @@
+import sys, os, ctypes, time; sys.path.insert(0, '.'); sys.path.insert(0, 'scratch/micro')
+import torch, numpy as np, bsplan
+from paper_2509_14211_b200 import nbg
+torch.cuda.set_device(0)
+L = ctypes.CDLL(os.path.abspath('scratch/micro/libbs.so'))
+c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 22, 16, 1)
+rp, ci = nbg.nbg_matrix_export_csr(c, A)
+d = nbg.nbg_vector_export_dense(c, deg)
+n = rp.shape[0] - 1
+P = ctypes.c_void_p
+def ev(): return torch.cuda.Event(enable_timing=True)
+def timeit(f, reps=20):
+    for _ in range(3): f()
+    torch.cuda.synchronize(); e0, e1 = ev(), ev(); e0.record()
+    for _ in range(reps): f()
+    e1.record(); torch.cuda.synchronize(); return e0.elapsed_time(e1) / reps * 1000
+y = np.random.rand(n).astype(np.float32)
+cs_ = np.r_[0.0, np.cumsum(y[ci].astype(np.float64))]
+ref = cs_[rp[1:]] - cs_[rp[:-1]]
+for SB, LM in ((15, 256), (15, 64), (14, 256), (15, 1024)):
+    t0 = time.time(); p = bsplan.build(rp, ci, d, SB=SB, LM=LM); print("plan", SB, LM, time.time() - t0, "slots", p['nslots'], flush=True)
+    T = {k: torch.from_numpy(v).cuda() for k, v in p.items() if isinstance(v, np.ndarray)}
+    yg = np.zeros(p['ncols'], np.float32); yg[p['perm'][d > 0]] = y[d > 0]
+    ygt = torch.from_numpy(yg).cuda()
+    part = torch.zeros(p['nslots'], dtype=torch.float64, device='cuda')
+    tt = torch.rand(n, device='cuda'); dinv = torch.rand(n, device='cuda'); r = torch.empty(n, device='cuda'); yn = torch.empty(p['ncols'], device='cuda')
+    dsum = torch.zeros(1, dtype=torch.float64, device='cuda')
+    for nt in (1024, 512):
+        f1 = lambda: L.bs_p1(nt, 148, P(T['cs'].data_ptr()), P(T['sb'].data_ptr()), P(T['so'].data_ptr()), P(T['sl'].data_ptr()), P(T['sslot'].data_ptr()),
+                             P(T['slen'].data_ptr()), P(T['lcol'].data_ptr()), P(ygt.data_ptr()), SB, p['ncols'], P(part.data_ptr()))
+        f2 = lambda: L.bs_p2(148 * 8, ctypes.c_longlong(n), P(T['rslot'].data_ptr()), P(part.data_ptr()), P(tt.data_ptr()), P(dinv.data_ptr()),
+                             P(T['gpos'].data_ptr()), ctypes.c_float(0.0), P(r.data_ptr()), P(yn.data_ptr()), P(dsum.data_ptr()))
+        assert f1() == 0; assert f2() == 0; torch.cuda.synchronize()
+        got = r.cpu().numpy()
+        err = np.max(np.abs(got - ref) / np.maximum(ref, 1e-3))
+        t1 = timeit(f1); t2 = timeit(f2); t12 = timeit(lambda: (f1(), f2()))
+        print(f"  nt {nt}: p1 {t1:.1f} us  p2 {t2:.1f} us  both {t12:.1f} us  GTEPS {len(ci) / t12 / 1e3:.0f}  maxrel {err:.2e}", flush=True)

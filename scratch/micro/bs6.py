@@ -1,0 +1,34 @@
+import sys, os, ctypes, time; sys.path.insert(0, '.'); sys.path.insert(0, 'scratch/micro')
+import torch, numpy as np, bsplan4
+from paper_2509_14211_b200 import nbg
+torch.cuda.set_device(0)
+L_ = ctypes.CDLL(os.path.abspath('scratch/micro/libbs.so'))
+c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 22, 16, 1)
+rp, ci = nbg.nbg_matrix_export_csr(c, A)
+d = nbg.nbg_vector_export_dense(c, deg)
+n = rp.shape[0] - 1
+P = ctypes.c_void_p
+def ev(): return torch.cuda.Event(enable_timing=True)
+def timeit(f, reps=20):
+    for _ in range(3): f()
+    torch.cuda.synchronize(); e0, e1 = ev(), ev(); e0.record()
+    for _ in range(reps): f()
+    e1.record(); torch.cuda.synchronize(); return e0.elapsed_time(e1) / reps * 1000
+y = np.random.rand(n).astype(np.float32)
+cs_ = np.r_[0.0, np.cumsum(y[ci].astype(np.float64))]
+ref = cs_[rp[1:]] - cs_[rp[:-1]]
+for SB, L, C, nt, wp in ((15, 64, 256, 1024, 4), (15, 64, 256, 1024, 16), (15, 32, 256, 1024, 4), (15, 64, 512, 512, 4), (15, 64, 128, 1024, 4)):
+    t0 = time.time(); p = bsplan4.build(rp, ci, d, SB=SB, L=L, C=C, wpiece=wp)
+    print("plan", SB, L, C, nt, wp, f"{time.time() - t0:.1f}s", "pieces", p['nslots'], "slices", p['nslices'], flush=True)
+    T = {k: torch.from_numpy(v).cuda() for k, v in p.items() if isinstance(v, np.ndarray)}
+    yg = np.zeros(p['ncols'], np.float32); yg[p['perm'][d > 0]] = y[d > 0]
+    ygt = torch.from_numpy(yg).cuda()
+    part = torch.zeros(p['nslots'] + 1, dtype=torch.float64, device='cuda')
+    tt = torch.rand(n, device='cuda'); dinv = torch.rand(n, device='cuda'); r = torch.empty(n, device='cuda'); yn = torch.empty(p['ncols'], device='cuda')
+    dsum = torch.zeros(1, dtype=torch.float64, device='cuda')
+    for mode in (0, 1, 2, 3):
+      f1 = lambda: L_.bs_p1v6(mode, 148, P(T['cs'].data_ptr()), P(T['sblk'].data_ptr()), P(T['soff'].data_ptr()), P(T['snv'].data_ptr()),
+                           P(T['hdr'].data_ptr()), P(T['lcol'].data_ptr()), P(ygt.data_ptr()), SB, p['ncols'], P(part.data_ptr()))
+      assert f1() == 0; torch.cuda.synchronize()
+      print("mode", mode, f"  p1 {timeit(f1):.1f} us", flush=True)

@@ -1,0 +1,25 @@
+import sys, os, ctypes; sys.path.insert(0, '.')
+import torch, numpy as np
+from paper_2509_14211_b200 import nbg
+torch.cuda.set_device(0)
+L = ctypes.CDLL(os.path.abspath('scratch/micro/libmg.so'))
+c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 22, 16, 1)
+rp, ci = nbg.nbg_matrix_export_csr(c, A)
+d = nbg.nbg_vector_export_dense(c, deg)
+n = rp.shape[0] - 1
+order = np.argsort(-d.astype(np.int64), kind='stable'); perm = np.empty(n, np.int64); perm[order] = np.arange(n)
+cig = torch.from_numpy(perm[ci].astype(np.int32)).cuda()
+nnz = cig.numel(); x = torch.rand(n, device='cuda'); out = torch.empty(148 * 1024, device='cuda')
+P = ctypes.c_void_p
+def timeit(f, reps=10):
+    for _ in range(3): f()
+    torch.cuda.synchronize(); e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True); e0.record()
+    for _ in range(reps): f()
+    e1.record(); torch.cuda.synchronize(); return e0.elapsed_time(e1) / reps * 1000
+for hc in (0, 16384, 32768, 40960, 49152):
+    for V in (1, 2, 4):
+        for pred in (0, 1):
+            f = lambda: L.mg_pipe(V, pred, P(cig.data_ptr()), ctypes.c_longlong(nnz), P(x.data_ptr()), hc, P(out.data_ptr()))
+            assert f() == 0
+            print(f"hc {hc} V {V} pred {pred}: {timeit(f):.1f} us", flush=True)

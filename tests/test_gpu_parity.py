@@ -149,9 +149,10 @@ def test_blocking_equals_nonblocking_bitwise(nbg, ctx, bctx, T):
     if T == "fp32":
         assert np.array_equal(res[0][1], res[1][1])      # fp32 terms sum exactly in fp64
     else:
-        # fp64 deltas: per-block fp64 partials group differently in the fused and the
-        # per-op reduction ("nonassociativity due to rounding")
-        assert rel(res[0][1], res[1][1]) <= 1e-12
+        # fp64 deltas: the ranks differ by a few ulps (above), and Delta_k is a sum of
+        # cancelling differences, so it moves by up to sum_i ulp(r_i): the derived delta bound
+        # ("nonassociativity due to rounding")
+        assert delta_close(res[0][1], res[1][1], res[1][0], np.float64)
 
 
 def test_long_rows_star(nbg, ctx):
