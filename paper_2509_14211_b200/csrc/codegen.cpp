@@ -207,17 +207,35 @@ struct Gen {
         }
     }
 
+    // LD_VEC values of the body loaded ahead of time (declared, loaded when `cond` holds)
+    template <class LD>
+    void emit_hoisted_loads(const std::string &ind, LD ld, const std::string &cond) {
+        for (size_t i = 0; i < p.ins.size(); i++) {
+            const Ins &in = p.ins[i];
+            if (in.uniform || in.k != Ins::LD_VEC) continue;
+            o << ind << ctype(in.t) << " " << v((int)i) << " = (" << ctype(in.t) << ")0;\n";
+        }
+        o << ind << "if (" << cond << ") {\n";
+        for (size_t i = 0; i < p.ins.size(); i++) {
+            const Ins &in = p.ins[i];
+            if (in.uniform || in.k != Ins::LD_VEC) continue;
+            o << ind << "  " << v((int)i) << " = " << ld(in) << ";\n";
+        }
+        o << ind << "}\n";
+    }
+
     // per-element body: non-uniform instructions; LD_VEC reads `ld(slot)`; outputs/reductions
     // through the given callbacks.
     template <class LD, class ST, class RD>
-    void emit_body(const std::string &ind, LD ld, ST st, RD rd, const std::string &accname) {
+    void emit_body(const std::string &ind, LD ld, ST st, RD rd, const std::string &accname, bool hoisted = false) {
         for (size_t i = 0; i < p.ins.size(); i++) {
             const Ins &in = p.ins[i];
             if (in.uniform) continue;
-            if (in.k == Ins::LD_VEC)
-                o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = " << ld(in) << ";\n";
-            else
+            if (in.k == Ins::LD_VEC) {
+                if (!hoisted) o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = " << ld(in) << ";\n";
+            } else {
                 o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = " << expr(in, accname) << ";\n";
+            }
         }
         for (const OutV &ov : p.outs) o << ind << st(ov) << "\n";
         for (size_t j = 0; j < p.reds.size(); j++) o << ind << rd(j) << "\n";
@@ -335,12 +353,12 @@ static int redkind(const Gen &g, const RedOut &r) { return g.redkind(r).kind; }
 // groups (index -1 = padding), so one 16-byte index load never mixes two rows.  One CTA of 1024
 // threads per SM; the CTA owns tasks b, b + G, ... (G = grid size) and its 32 warps pull them
 // from a shared-memory counter.
-//   row task  (<= 32 consecutive rows, <= 512 groups): the warp streams the task's groups, lane l
+//   row task  (<= 128 consecutive rows, <= 512 groups): the warp streams the task's groups, lane l
 //             owning group base + l (one row) per step; the next step's indices are prefetched;
 //             the 4 gathers per lane are predicated loads (hot-column cache in shared memory, else
 //             L1/L2).  Row starts/ends of the step are two warp OR-reductions; a segmented warp
 //             scan keyed by those starts combines lane sums into row totals (carry across steps).
-//             Lane j then runs the fused epilogue for row rb + j (coalesced loads/stores).
+//             Lane j then runs the fused epilogue for rows rb + j + 32 r (coalesced loads/stores).
 //   chunk task (512 groups of a longer row): lane-strided 16-entry batches, fixed shuffle tree ->
 //             chunk partial; the warp that completes the row's last chunk (atomic ticket) sums
 //             the chunk partials in chunk order and runs the epilogue.
@@ -394,14 +412,15 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
     const int NF = (int)fplus.size();
     const int accw = (ACC == "double" || ACC == "long long") ? 8 : 4;
-    const int warp_bytes = 32 * 8;                            // row totals of the task
+    const int warp_bytes = 128 * 8;                           // row totals of the task
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
+    const int NT = spmv_threads(), NW = NT / 32;
     int hot_bytes = 160 * 1024;                               // measured sweet spot
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
     const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
-    const int dyn_bytes = hot_region + 32 * warp_bytes + xacc_bytes;
+    const int dyn_bytes = hot_region + NW * warp_bytes + NW * NF * 11 * 8;
     if (hot_entries) *hot_entries = hot_cap;
     (void)accw;
     // gathered element: predicated shared/global load of the raw bits, reinterpreted as XT
@@ -421,102 +440,102 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     // one padded position: index c (-1 = padding) at position P_ -> term of the row's sum
     o << "#define NBG_TERM(C_, P_) (((C_) >= 0) ? (" << ACC << ")nbg_mul(a, (P_), nbg_gxv(s_base, s_hot, X, (C_), hc)) : (" << ACC
       << ")(" << IDENT << "))\n";
+    // split form: gather (index clamped, always safe) now, turn into a term later
+    o << "#define NBG_GV(C_) nbg_gxv(s_base, s_hot, X, ((C_) > 0 ? (C_) : 0), hc)\n";
+    o << "#define NBG_TV(C_, P_, V_) (((C_) >= 0) ? (" << ACC << ")nbg_mul(a, (P_), (V_)) : (" << ACC << ")(" << IDENT << "))\n";
     o << "__device__ __forceinline__ " << XT << " nbg_gxv(unsigned s_base, const " << XT << "* s_hot, const " << XT
       << "* X, int C_, int hc) { return " << gx << "; }\n";
-    o << "extern \"C\" __global__ void __launch_bounds__(1024, 1) " << kname << "(const KArgs a) {\n";
+    o << "#define NBG_NW " << NW << "\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", 1) " << kname << "(const KArgs a) {\n";
     o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
     o << "  __shared__ double nbg_sh[32];\n";
     o << "  __shared__ int s_ctr;\n";
     o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
     o << "  const unsigned s_base = (unsigned)__cvta_generic_to_shared(nbg_dyn);\n";
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    o << "  " << ACC << "* s_racc = (" << ACC << "*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << ");   // [32] row totals\n";
+    o << "  " << ACC << "* s_racc = (" << ACC << "*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << ");   // [128] row totals\n";
     if (NF)
-        o << "  u64* s_x = (u64*)(nbg_dyn + " << hot_region << " + 32 * " << warp_bytes << ");   // [warp][NF][11]\n";
+        o << "  u64* s_x = (u64*)(nbg_dyn + " << hot_region << " + NBG_NW * " << warp_bytes << ");   // [warp][NF][11]\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
     o << "  const int4* __restrict__ CG = (const int4*)a.colidx;\n";
     o << "  const long long* __restrict__ GRP = a.rowptr;\n";
     o << "  const int hc = (int)a.hc;\n";
     o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
-    if (NF) o << "  for (int k = threadIdx.x; k < 32 * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
-    o << "  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = X[k];\n";
+    if (NF) o << "  for (int k = threadIdx.x; k < NBG_NW * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
+    // hot-column cache: 16-byte loads, 4 in flight per thread (X is 16-byte aligned, hc % 16 == 0 or tail)
+    o << "  {\n";
+    o << "    const int nv_ = ((((unsigned long long)X) & 15ull) == 0ull) ? (int)((hc * sizeof(" << XT << ")) >> 4) : 0;\n";
+    o << "    const uint4* src_ = (const uint4*)X; uint4* dst_ = (uint4*)nbg_dyn;\n";
+    o << "    for (int k = threadIdx.x; k < nv_; k += 4 * blockDim.x) {\n";
+    o << "      uint4 w_[4];\n";
+    o << "      #pragma unroll\n      for (int u = 0; u < 4; u++) if (k + u * (int)blockDim.x < nv_) w_[u] = __ldg(src_ + k + u * blockDim.x);\n";
+    o << "      #pragma unroll\n      for (int u = 0; u < 4; u++) if (k + u * (int)blockDim.x < nv_) dst_[k + u * blockDim.x] = w_[u];\n";
+    o << "    }\n";
+    o << "    for (int k = (nv_ << 4) / (int)sizeof(" << XT << ") + threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = X[k];\n";
+    o << "  }\n";
     o << "  __syncthreads();\n";
     g.emit_uniform();
     g.emit_red_decl();
     o << "  const long long items = a.nchunks + a.ntiles;\n";
+    // tasks are claimed one ahead so the next row task's header load overlaps this task
+    o << "  int ln_ = 0;\n";
+    o << "  if (lane == 0) ln_ = atomicAdd(&s_ctr, 1);\n";
+    o << "  ln_ = __shfl_sync(0xffffffffu, ln_, 0);\n";
+    o << "  long long itn_ = (long long)blockIdx.x + (long long)ln_ * gridDim.x;\n";
+    o << "  int4 tn_ = (itn_ >= a.nchunks && itn_ < items) ? ((const int4*)a.tiles)[itn_ - a.nchunks] : make_int4(0, 0, 0, 0);\n";
     o << "  for (;;) {\n";
-    o << "    int l_ = 0;\n";
-    o << "    if (lane == 0) l_ = atomicAdd(&s_ctr, 1);\n";
-    o << "    l_ = __shfl_sync(0xffffffffu, l_, 0);\n";
-    o << "    const long long it = (long long)blockIdx.x + (long long)l_ * gridDim.x;\n";
+    o << "    const long long it = itn_;\n";
     o << "    if (it >= items) break;\n";
-    // ---------------- chunk of a long row
-    o << "    if (it < a.nchunks) {\n";
-    o << "      const int4 ch = ((const int4*)a.chunks)[it];\n";
-    o << "      const long long g0 = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
-    o << "      const int cnt = ch.w;\n";
-    o << "      " << ACC << " t = " << IDENT << ";\n";
-    o << "      for (int b = 0; b < cnt; b += 128) {\n";
-    o << "        int4 q[4];\n";
-    o << "        #pragma unroll\n        for (int v = 0; v < 4; v++) { const int gi = b + lane + 32 * v; q[v] = gi < cnt ? __ldcs(CG + g0 + gi) : make_int4(-1, -1, -1, -1); }\n";
-    o << "        " << ACC << " u_[4];\n";
-    o << "        #pragma unroll\n        for (int v = 0; v < 4; v++) {\n";
-    o << "          const long long P_ = 4 * (g0 + b + lane + 32 * v);\n";
-    o << "          " << ACC << " w_ = NBG_TERM(q[v].x, P_);\n";
-    o << "          w_ = NBG_ADD(w_, NBG_TERM(q[v].y, P_ + 1)); w_ = NBG_ADD(w_, NBG_TERM(q[v].z, P_ + 2)); w_ = NBG_ADD(w_, NBG_TERM(q[v].w, P_ + 3));\n";
-    o << "          u_[v] = w_;\n";
-    o << "        }\n";
-    o << "        t = NBG_ADD(t, NBG_ADD(NBG_ADD(u_[0], u_[1]), NBG_ADD(u_[2], u_[3])));\n";
-    o << "      }\n";
-    o << "      for (int off = 16; off > 0; off >>= 1) { const " << ACC << " u_ = __shfl_down_sync(0xffffffffu, t, off); t = NBG_ADD(t, u_); }\n";
-    o << "      if (lane == 0) {\n";
-    o << "        ((" << ACC << "*)a.partials)[it] = t;\n";
-    o << "        __threadfence();\n";
-    o << "        const int4 lr = ((const int4*)a.longs)[ch.x];\n";
-    o << "        const int tk = atomicAdd(&a.counters[ch.x], 1);\n";
-    o << "        if (tk == lr.z - 1) {\n";
-    o << "          __threadfence();\n";
-    o << "          " << ACC << " acc = " << IDENT << ";\n";
-    o << "          for (int j = 0; j < lr.z; j++) { const " << ACC << " pj = *(volatile const " << ACC << "*)(((const " << ACC
-      << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
-    o << "          a.counters[ch.x] = 0;\n";
-    o << "          const long long i = lr.x;\n";
-    g.emit_body(
-        "          ",
-        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
-        [&](const OutV &ov) { return g.store(ov, "i"); },
-        [&](size_t j) { return g.red_direct(p.reds[j], g.v(p.reds[j].ins)); }, "acc");
-    o << "        }\n";
-    o << "      }\n";
-    o << "      __syncwarp();\n";
-    o << "      continue;\n";
-    o << "    }\n";
-    // ---------------- row task
+    o << "    const int4 tl = tn_;\n";
+    o << "    if (lane == 0) ln_ = atomicAdd(&s_ctr, 1);\n";
+    o << "    ln_ = __shfl_sync(0xffffffffu, ln_, 0);\n";
+    o << "    itn_ = (long long)blockIdx.x + (long long)ln_ * gridDim.x;\n";
+    o << "    if (itn_ >= a.nchunks && itn_ < items) tn_ = ((const int4*)a.tiles)[itn_ - a.nchunks];\n";
+    // ---------------- one task: a row task (<= 128 rows, lane l owns rows l, l + 32, l + 64,
+    // l + 96) or a chunk of one long row (R = 0: no row starts, the whole chunk is one segment)
     o << "    {\n";
-    o << "      const int2 tl = ((const int2*)a.tiles)[it - a.nchunks];\n";
-    o << "      const int R = tl.y - tl.x;\n";
-    o << "      const long long gs = GRP[tl.x + (lane < R ? lane : R)];           // my row's first group (lane R: end)\n";
-    o << "      const long long gn_ = __shfl_down_sync(0xffffffffu, gs, 1);\n";
-    o << "      const long long ge = (lane == 31) ? GRP[tl.x + (R < 32 ? R : 32)] : gn_;\n";
-    o << "      const long long G0 = __shfl_sync(0xffffffffu, gs, 0);\n";
-    o << "      const long long G1 = __shfl_sync(0xffffffffu, (lane == 31) ? ge : gs, R < 32 ? R : 31);\n";
-    o << "      const bool valid = lane < R;\n";
-    o << "      const bool nonempty = valid && ge > gs;\n";
-    o << "      const unsigned nem = __ballot_sync(0xffffffffu, nonempty);\n";
-    o << "      const int rgs = (int)(gs - G0), rge = (int)(ge - G0) - 1;     // my row's first / last group\n";
-    o << "      const int NG = (int)(G1 - G0);\n";
+    o << "      const bool is_chunk = it < a.nchunks;\n";
+    o << "      int4 ch = make_int4(0, 0, 0, 0);\n";
+    o << "      if (is_chunk) ch = ((const int4*)a.chunks)[it];\n";
+    o << "      const int R = is_chunk ? 0 : (tl.y & 0xff), NG = is_chunk ? ch.w : (tl.y >> 8);\n";
+    o << "      const long long G0 = is_chunk ? (((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y)\n";
+    o << "                                    : (((long long)(unsigned)tl.w << 32) | (long long)(unsigned)tl.z);\n";
+    o << "      int4 q = (lane < NG) ? __ldcs(CG + G0 + lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "      int4 q2 = (32 + lane < NG) ? __ldcs(CG + G0 + 32 + lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "      int rs_[4];\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
+    o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
+    o << "      unsigned nem_[4];\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) {\n";
+    o << "        const int nx = __shfl_down_sync(0xffffffffu, rs_[r], 1);\n";
+    o << "        const int nf = __shfl_sync(0xffffffffu, r < 3 ? rs_[r < 3 ? r + 1 : 3] : r128_, 0);\n";
+    o << "        const int re = (lane == 31) ? nf : nx;                     // end (exclusive) of row lane + 32 r\n";
+    o << "        nem_[r] = __ballot_sync(0xffffffffu, lane + 32 * r < R && re > rs_[r]);\n";
+    o << "      }\n";
     o << "      " << ACC << " carry = " << IDENT << ";\n";
     o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
-    o << "      int4 q = (lane < NG) ? __ldcs(CG + G0 + lane) : make_int4(-1, -1, -1, -1);\n";
+    // gather pipeline: the gathers of step b + 32 are in flight while step b is reduced; the
+    // indices are loaded two steps ahead
+    o << "      " << XT << " f0 = NBG_GV(q.x), f1 = NBG_GV(q.y), f2 = NBG_GV(q.z), f3 = NBG_GV(q.w);\n";
     o << "      for (int b = 0; b < NG; b += 32) {\n";
     o << "        const long long P_ = 4 * (G0 + b + lane);\n";
     o << "        const int4 qc = q;\n";
-    o << "        if (b + 32 < NG) q = (b + 32 + lane < NG) ? __ldcs(CG + G0 + b + 32 + lane) : make_int4(-1, -1, -1, -1);\n";
-    o << "        " << ACC << " S = NBG_TERM(qc.x, P_);\n";
-    o << "        S = NBG_ADD(S, NBG_TERM(qc.y, P_ + 1)); S = NBG_ADD(S, NBG_TERM(qc.z, P_ + 2)); S = NBG_ADD(S, NBG_TERM(qc.w, P_ + 3));\n";
-    o << "        const int os_ = rgs - b, oe_ = rge - b;\n";
-    o << "        const unsigned M = __reduce_or_sync(0xffffffffu, (nonempty && os_ >= 0 && os_ < 32) ? (1u << os_) : 0u);\n";
-    o << "        const unsigned Eb = __reduce_or_sync(0xffffffffu, (nonempty && oe_ >= 0 && oe_ < 32) ? (1u << oe_) : 0u);\n";
+    o << "        const " << XT << " c0 = f0, c1 = f1, c2 = f2, c3 = f3;\n";
+    o << "        if (b + 32 < NG) {\n";
+    o << "          q = q2; f0 = NBG_GV(q.x); f1 = NBG_GV(q.y); f2 = NBG_GV(q.z); f3 = NBG_GV(q.w);\n";
+    o << "          if (b + 64 < NG) q2 = (b + 64 + lane < NG) ? __ldcs(CG + G0 + b + 64 + lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "        }\n";
+    o << "        " << ACC << " S = NBG_TV(qc.x, P_, c0);\n";
+    o << "        S = NBG_ADD(S, NBG_TV(qc.y, P_ + 1, c1)); S = NBG_ADD(S, NBG_TV(qc.z, P_ + 2, c2)); S = NBG_ADD(S, NBG_TV(qc.w, P_ + 3, c3));\n";
+    // rows are contiguous in group space: a row ends where the next non-empty row starts, so only
+    // the starts are needed; the row ending just before a start is complete at that start
+    o << "        unsigned ms_ = 0u;\n";
+    o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) {\n";
+    o << "          const int os_ = rs_[r] - b;\n";
+    o << "          if (((nem_[r] >> lane) & 1u) && os_ >= 0 && os_ < 32) ms_ |= 1u << os_;\n";
+    o << "        }\n";
+    o << "        const unsigned M = __reduce_or_sync(0xffffffffu, ms_);\n";
+    o << "        if (lane == 0 && (M & 1u) && nstarted > 0) s_racc[nstarted - 1] = carry;   // ended at the previous step\n";
     o << "        if (lane == 0 && !(M & 1u)) S = NBG_ADD(carry, S);\n";
     o << "        bool F = ((M >> lane) & 1u) || lane == 0;\n";
     o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
@@ -524,21 +543,52 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "          const bool Fy = __shfl_up_sync(0xffffffffu, F, d);\n";
     o << "          if (lane >= d && !F) { S = NBG_ADD(Sy, S); F = Fy; }\n";
     o << "        }\n";
-    o << "        if ((Eb >> lane) & 1u) s_racc[nstarted + __popc(M & ((2u << lane) - 1u)) - 1] = S;\n";
-    o << "        const " << ACC << " S31 = __shfl_sync(0xffffffffu, S, 31);\n";
-    o << "        carry = ((Eb >> 31) & 1u) ? (" << ACC << ")(" << IDENT << ") : S31;\n";
+    o << "        const " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
+    o << "        if (lane > 0 && ((M >> lane) & 1u)) s_racc[nstarted + __popc(M & ((1u << lane) - 1u)) - 1] = Sp;\n";
+    o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
     o << "        nstarted += __popc(M);\n";
     o << "      }\n";
+    o << "      if (is_chunk) {\n";
+    o << "        if (lane == 0) {\n";
+    o << "          const " << ACC << " t = carry;\n";
+    o << "          ((" << ACC << "*)a.partials)[it] = t;\n";
+    o << "          __threadfence();\n";
+    o << "          const int4 lr = ((const int4*)a.longs)[ch.x];\n";
+    o << "          const int tk = atomicAdd(&a.counters[ch.x], 1);\n";
+    o << "          if (tk == lr.z - 1) {\n";
+    o << "            __threadfence();\n";
+    o << "            " << ACC << " acc = " << IDENT << ";\n";
+    o << "            for (int j = 0; j < lr.z; j++) { const " << ACC << " pj = *(volatile const " << ACC << "*)(((const " << ACC
+      << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
+    o << "            a.counters[ch.x] = 0;\n";
+    o << "            const long long i = lr.x;\n";
+    g.emit_body(
+        "            ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
+        [&](size_t j) { return g.red_direct(p.reds[j], g.v(p.reds[j].ins)); }, "acc");
+    o << "          }\n";
+    o << "        }\n";
+    o << "        __syncwarp();\n";
+    o << "        continue;\n";
+    o << "      }\n";
+    o << "      if (lane == 0 && nstarted > 0) s_racc[nstarted - 1] = carry;          // the task's last row\n";
     o << "      __syncwarp();\n";
     for (int j : fplus) o << "      r" << j << " = 0.0;\n";
-    o << "      if (valid) {\n";
-    o << "        const " << ACC << " acc = nonempty ? s_racc[__popc(nem & ((1u << lane) - 1u))] : (" << ACC << ")(" << IDENT << ");\n";
-    o << "        const long long i = (long long)tl.x + lane;\n";
+    o << "      int rb_ = 0;                                               // nonempty rows before block r\n";
+    o << "      for (int r = 0; r < 4; r++) {\n";
+    o << "        const long long i = (long long)tl.x + lane + 32 * r;\n";
+    o << "        const unsigned nm = r == 0 ? nem_[0] : (r == 1 ? nem_[1] : (r == 2 ? nem_[2] : nem_[3]));\n";
+    o << "        if (lane + 32 * r < R) {\n";
+    o << "          const " << ACC << " acc = ((nm >> lane) & 1u) ? s_racc[rb_ + __popc(nm & ((1u << lane) - 1u))] : (" << ACC << ")(" << IDENT << ");\n";
     g.emit_body(
-        "        ",
+        "          ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
         [&](const OutV &ov) { return g.store(ov, "i"); },
         [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    o << "        }\n";
+    o << "        rb_ += __popc(nm);\n";
+    o << "        if (32 * (r + 1) >= R) break;\n";
     o << "      }\n";
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
@@ -553,7 +603,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         int j = fplus[f];
         o << "  if (threadIdx.x < 11) {\n";
         o << "    u64 v_ = 0ull;\n";
-        o << "    for (int w = 0; w < 32; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 11 + threadIdx.x]; v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
+        o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 11 + threadIdx.x]; v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
         o << "    if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
         o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
         o << "  }\n";
@@ -573,6 +623,16 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
 }  // namespace
 
 extern const char *NBG_PRELUDE_SRC;
+
+int spmv_threads() {
+    static int v = 0;
+    if (!v) {
+        const char *e = getenv("NBG_SPMV_THREADS");
+        v = (e && *e) ? atoi(e) : 1024;
+        if (v != 256 && v != 512 && v != 768 && v != 1024) v = 1024;
+    }
+    return v;
+}
 
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem, int *hot_entries) {
     Gen g(p);

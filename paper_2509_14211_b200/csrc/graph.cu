@@ -21,7 +21,7 @@ namespace {
 // stored entries (padding index -1), so a 16-byte load never mixes two rows.
 constexpr int SP_LONG_G = 512;     // rows with more groups (> 2048 entries) are processed as chunks
 constexpr int SP_CHUNK_G = 512;    // groups per chunk of a long row (one warp)
-constexpr int SP_TASK_ROWS = 32;   // rows per warp task (one per lane)
+constexpr int SP_TASK_ROWS = 128;  // rows per warp task (lane l: rows l, l + 32, l + 64, l + 96)
 constexpr int SP_TASK_G = 512;     // group budget of a warp task
 
 __device__ __forceinline__ unsigned long long sm64(unsigned long long key, unsigned long long k) {
@@ -340,7 +340,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     NBG_CUDA(cudaGetLastError());
     c.stats.kernels_launched += 3;
 
-    // ---- warp tasks (host, once per matrix): runs of <= 32 consecutive non-long rows with
+    // ---- warp tasks (host, once per matrix): runs of <= 128 consecutive non-long rows with
     // <= SP_TASK_G groups; long rows (> SP_LONG_G groups) are cut into chunks of SP_CHUNK_G groups
     std::vector<int> tiles, chunks, longs;
     tiles.reserve((size_t)(n / 16 + 16));
@@ -373,10 +373,13 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
             ngr += g2;
             i++;
         }
+        // task record {row_begin, rows | groups << 8, first_group_lo, first_group_hi}
         tiles.push_back((int)st);
-        tiles.push_back((int)i);
+        tiles.push_back((int)((i - st) | (ngr << 8)));
+        tiles.push_back((int)(unsigned)(gph[st] & 0xffffffffll));
+        tiles.push_back((int)(unsigned)((unsigned long long)gph[st] >> 32));
     }
-    P->ntiles = (int64_t)tiles.size() / 2;
+    P->ntiles = (int64_t)tiles.size() / 4;
     P->nchunks = nch_total;
     P->nlong = L;
     if (!tiles.empty()) {

@@ -91,7 +91,7 @@ KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bo
     k->name = kname;
     NBG_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     NBG_CUDA(cudaLibraryGetKernel(&k->k, k->lib, kname.c_str()));
-    k->block = spmv ? 1024 : 256;
+    k->block = spmv ? spmv_threads() : 256;
     k->smem = dyn_smem;
     if (dyn_smem > 48 * 1024)
         NBG_CUDA(cudaFuncSetAttribute((const void *)k->k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem));

@@ -122,7 +122,7 @@ struct SpmvPlan {
     BufP grp;        // int64[n + 1]  first group of each row
     BufP cg;         // int32[4 * ngroups]  column index per padded position (gather layout), -1 = pad
     BufP vals_g;     // values per padded position (valued matrices only)
-    BufP tiles;      // int2  {row_begin, row_end}
+    BufP tiles;      // int4  {row_begin, rows | ngroups << 8, first_group_lo, first_group_hi}
     BufP chunks;     // int4  {long_idx, first_group_lo, first_group_hi, ngroups}
     BufP longs;      // int4  {row, first_chunk, nchunks, 0}
     BufP counters;   // int[nlong], zero between launches
@@ -337,6 +337,7 @@ double scalar_read(Ctx &c, const NodeP &s);
 void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
 
 // codegen / jit
+int spmv_threads();   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
 KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0);
 void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);

@@ -567,7 +567,8 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.partials = (double *)(A.plan->partials ? A.plan->partials->d : nullptr);
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
-        items = (A.plan->ntiles + A.plan->nchunks + 31) / 32;   // one task per warp, 32 warps per CTA
+        const long long nw = spmv_threads() / 32;
+        items = (A.plan->ntiles + A.plan->nchunks + nw - 1) / nw;   // one task per warp
         args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
     } else {

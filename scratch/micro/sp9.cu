@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(NT, 1) sp9(long long ntiles, long long nchunks
     const int4* __restrict__ cg,            // groups of 4 gather indices (sentinel 0)
     const float* __restrict__ X, int hc,
     const float* __restrict__ t, const float* __restrict__ dinv, const int* __restrict__ gpos, float c, float* __restrict__ r, float* __restrict__ ynext,
-    double* __restrict__ dsum, int* __restrict__ ctr) {
+    double* __restrict__ dsum, int* __restrict__ ctr, int mode) {
   constexpr int NW = NT / 32;
   extern __shared__ __align__(16) unsigned char dyn[];
   float* s_hot = (float*)dyn;
@@ -94,8 +94,11 @@ __global__ void __launch_bounds__(NT, 1) sp9(long long ntiles, long long nchunks
       const int NG = (int)(G1 - G0);
       int4 q = (lane < NG) ? __ldcs(cg + G0 + lane) : make_int4(0, 0, 0, 0);
       for (int b = 0; b < NG; b += 32) {
-        const float f0 = gx(s_base, X, q.x, hc), f1 = gx(s_base, X, q.y, hc), f2 = gx(s_base, X, q.z, hc), f3 = gx(s_base, X, q.w, hc);
+        float f0, f1, f2, f3;
+        if (mode & 2) { f0 = (float)q.x; f1 = (float)q.y; f2 = (float)q.z; f3 = (float)q.w; }
+        else { f0 = gx(s_base, X, q.x, hc); f1 = gx(s_base, X, q.y, hc); f2 = gx(s_base, X, q.z, hc); f3 = gx(s_base, X, q.w, hc); }
         if (b + 32 < NG) q = (b + 32 + lane < NG) ? __ldcs(cg + G0 + b + 32 + lane) : make_int4(0, 0, 0, 0);
+        if (mode & 1) { carry += ((double)f0 + (double)f1) + ((double)f2 + (double)f3); continue; }
         const int os = rgs - b, oe = rge - b;
         const unsigned M = __reduce_or_sync(0xffffffffu, (nonempty && os >= 0 && os < 32) ? (1u << os) : 0u);
         const unsigned Eb = __reduce_or_sync(0xffffffffu, (nonempty && oe >= 0 && oe < 32) ? (1u << oe) : 0u);
@@ -116,6 +119,7 @@ __global__ void __launch_bounds__(NT, 1) sp9(long long ntiles, long long nchunks
         carry = ((Eb >> 31) & 1u) ? 0.0 : S31;
         nstarted += __popc(M);
       }
+      if (mode & 1) { if (lane == 0) s_racc[0] = carry; }
       __syncwarp();
       if (valid) {
         const int rk = __popc(nem & ((1u << lane) - 1u));
@@ -131,13 +135,13 @@ __global__ void __launch_bounds__(NT, 1) sp9(long long ntiles, long long nchunks
   if (lane == 0) atomicAdd(dsum, d);
 }
 
-extern "C" int sp9_run(int batch, long long ntiles, long long nchunks, const void* tiles, const void* chunks, const void* longs, int* counters, double* partials,
+extern "C" int sp9_run(int mode, int batch, long long ntiles, long long nchunks, const void* tiles, const void* chunks, const void* longs, int* counters, double* partials,
     const long long* grp, const void* cg, const float* X, int hc, const float* t, const float* dinv, const int* gpos, float c,
     float* r, float* ynext, double* dsum, int* ctr) {
   cudaMemsetAsync(ctr, 0, 8);
   int smem = ((hc * 4 + 15) & ~15) + 32 * 32 * 8;
 #define GO(B_) if (batch == B_) { cudaFuncSetAttribute(sp9<1024, B_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-  sp9<1024, B_><<<148, 1024, smem>>>(ntiles, nchunks, (const int2*)tiles, (const int4*)chunks, (const int4*)longs, counters, partials, grp, (const int4*)cg, X, hc, t, dinv, gpos, c, r, ynext, dsum, ctr); \
+  sp9<1024, B_><<<148, 1024, smem>>>(ntiles, nchunks, (const int2*)tiles, (const int4*)chunks, (const int4*)longs, counters, partials, grp, (const int4*)cg, X, hc, t, dinv, gpos, c, r, ynext, dsum, ctr, mode); \
   return (int)cudaGetLastError(); }
   GO(1) GO(4) GO(16)
 #undef GO
