@@ -628,8 +628,8 @@ int spmv_threads() {
     static int v = 0;
     if (!v) {
         const char *e = getenv("NBG_SPMV_THREADS");
-        v = (e && *e) ? atoi(e) : 1024;
-        if (v != 256 && v != 512 && v != 768 && v != 1024) v = 1024;
+        v = (e && *e) ? atoi(e) : 768;
+        if (v != 256 && v != 512 && v != 768 && v != 1024) v = 768;
     }
     return v;
 }
