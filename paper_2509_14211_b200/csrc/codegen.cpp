@@ -500,8 +500,10 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "      const int R = is_chunk ? 0 : (tl.y & 0xff), NG = is_chunk ? ch.w : (tl.y >> 8);\n";
     o << "      const long long G0 = is_chunk ? (((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y)\n";
     o << "                                    : (((long long)(unsigned)tl.w << 32) | (long long)(unsigned)tl.z);\n";
-    o << "      int4 q = (lane < NG) ? __ldcs(CG + G0 + lane) : make_int4(-1, -1, -1, -1);\n";
-    o << "      int4 q2 = (32 + lane < NG) ? __ldcs(CG + G0 + 32 + lane) : make_int4(-1, -1, -1, -1);\n";
+    // step = 64 groups: lane l owns groups b + 2l and b + 2l + 1 (8 gathers in flight per lane);
+    // the next step's indices are prefetched while this step is reduced
+    o << "      int4 qa = (2 * lane < NG) ? __ldcs(CG + G0 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "      int4 qb = (2 * lane + 1 < NG) ? __ldcs(CG + G0 + 2 * lane + 1) : make_int4(-1, -1, -1, -1);\n";
     o << "      int rs_[4];\n";
     o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
     o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
@@ -514,39 +516,45 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "      }\n";
     o << "      " << ACC << " carry = " << IDENT << ";\n";
     o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
-    // gather pipeline: the gathers of step b + 32 are in flight while step b is reduced; the
-    // indices are loaded two steps ahead
-    o << "      " << XT << " f0 = NBG_GV(q.x), f1 = NBG_GV(q.y), f2 = NBG_GV(q.z), f3 = NBG_GV(q.w);\n";
-    o << "      for (int b = 0; b < NG; b += 32) {\n";
-    o << "        const long long P_ = 4 * (G0 + b + lane);\n";
-    o << "        const int4 qc = q;\n";
-    o << "        const " << XT << " c0 = f0, c1 = f1, c2 = f2, c3 = f3;\n";
-    o << "        if (b + 32 < NG) {\n";
-    o << "          q = q2; f0 = NBG_GV(q.x); f1 = NBG_GV(q.y); f2 = NBG_GV(q.z); f3 = NBG_GV(q.w);\n";
-    o << "          if (b + 64 < NG) q2 = (b + 64 + lane < NG) ? __ldcs(CG + G0 + b + 64 + lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "      for (int b = 0; b < NG; b += 64) {\n";
+    o << "        const long long P_ = 4 * (G0 + b + 2 * lane);\n";
+    o << "        const int4 ca = qa, cb = qb;\n";
+    o << "        const " << XT << " g0 = NBG_GV(ca.x), g1 = NBG_GV(ca.y), g2 = NBG_GV(ca.z), g3 = NBG_GV(ca.w);\n";
+    o << "        const " << XT << " g4 = NBG_GV(cb.x), g5 = NBG_GV(cb.y), g6 = NBG_GV(cb.z), g7 = NBG_GV(cb.w);\n";
+    o << "        if (b + 64 < NG) {\n";
+    o << "          qa = (b + 64 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "          qb = (b + 65 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
     o << "        }\n";
-    o << "        " << ACC << " S = NBG_TV(qc.x, P_, c0);\n";
-    o << "        S = NBG_ADD(S, NBG_TV(qc.y, P_ + 1, c1)); S = NBG_ADD(S, NBG_TV(qc.z, P_ + 2, c2)); S = NBG_ADD(S, NBG_TV(qc.w, P_ + 3, c3));\n";
-    // rows are contiguous in group space: a row ends where the next non-empty row starts, so only
-    // the starts are needed; the row ending just before a start is complete at that start
-    o << "        unsigned ms_ = 0u;\n";
+    // row starts of this step: two 32-bit words over positions [0, 64)
+    o << "        unsigned m0_ = 0u, m1_ = 0u;\n";
     o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) {\n";
     o << "          const int os_ = rs_[r] - b;\n";
-    o << "          if (((nem_[r] >> lane) & 1u) && os_ >= 0 && os_ < 32) ms_ |= 1u << os_;\n";
+    o << "          if (((nem_[r] >> lane) & 1u) && os_ >= 0 && os_ < 64) { if (os_ < 32) m0_ |= 1u << os_; else m1_ |= 1u << (os_ - 32); }\n";
     o << "        }\n";
-    o << "        const unsigned M = __reduce_or_sync(0xffffffffu, ms_);\n";
-    o << "        if (lane == 0 && (M & 1u) && nstarted > 0) s_racc[nstarted - 1] = carry;   // ended at the previous step\n";
-    o << "        if (lane == 0 && !(M & 1u)) S = NBG_ADD(carry, S);\n";
-    o << "        bool F = ((M >> lane) & 1u) || lane == 0;\n";
+    o << "        const unsigned M0 = __reduce_or_sync(0xffffffffu, m0_), M1 = __reduce_or_sync(0xffffffffu, m1_);\n";
+    o << "        const unsigned Mw = lane < 16 ? M0 : M1;\n";
+    o << "        const int sh_ = (2 * lane) & 31;\n";
+    o << "        const bool s0 = (Mw >> sh_) & 1u, s1 = (Mw >> (sh_ + 1)) & 1u;\n";
+    o << "        const int before = (lane < 16 ? 0 : __popc(M0)) + __popc(Mw & ((1u << sh_) - 1u));   // starts before position 2 lane\n";
+    o << "        " << ACC << " v0 = NBG_TV(ca.x, P_, g0);\n";
+    o << "        v0 = NBG_ADD(v0, NBG_TV(ca.y, P_ + 1, g1)); v0 = NBG_ADD(v0, NBG_TV(ca.z, P_ + 2, g2)); v0 = NBG_ADD(v0, NBG_TV(ca.w, P_ + 3, g3));\n";
+    o << "        " << ACC << " v1 = NBG_TV(cb.x, P_ + 4, g4);\n";
+    o << "        v1 = NBG_ADD(v1, NBG_TV(cb.y, P_ + 5, g5)); v1 = NBG_ADD(v1, NBG_TV(cb.z, P_ + 6, g6)); v1 = NBG_ADD(v1, NBG_TV(cb.w, P_ + 7, g7));\n";
+    // scan value: the segment open at the lane's end; lane 0 continues the carried row
+    o << "        " << ACC << " S = s1 ? v1 : NBG_ADD(v0, v1);\n";
+    o << "        if (lane == 0 && !s0 && !s1) S = NBG_ADD(carry, S);\n";
+    o << "        bool F = s0 || s1 || lane == 0;\n";
     o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
     o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
     o << "          const bool Fy = __shfl_up_sync(0xffffffffu, F, d);\n";
     o << "          if (lane >= d && !F) { S = NBG_ADD(Sy, S); F = Fy; }\n";
     o << "        }\n";
-    o << "        const " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
-    o << "        if (lane > 0 && ((M >> lane) & 1u)) s_racc[nstarted + __popc(M & ((1u << lane) - 1u)) - 1] = Sp;\n";
+    o << "        " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
+    o << "        if (lane == 0) Sp = carry;                                   // running total before position 0\n";
+    o << "        if (s0 && (lane > 0 || nstarted > 0)) s_racc[nstarted + before - 1] = Sp;          // row ending at 2 lane - 1\n";
+    o << "        if (s1) s_racc[nstarted + before + (s0 ? 1 : 0) - 1] = s0 ? v0 : NBG_ADD(Sp, v0);   // row ending at 2 lane\n";
     o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
-    o << "        nstarted += __popc(M);\n";
+    o << "        nstarted += __popc(M0) + __popc(M1);\n";
     o << "      }\n";
     o << "      if (is_chunk) {\n";
     o << "        if (lane == 0) {\n";
