@@ -1,0 +1,8 @@
+#!/bin/bash
+# round profile bundle: bench line, ncu launch list of the bench command, ncu --set full of one C4 SpMV launch
+set -x
+python bench.py > gpurun_out/bench_r1.json 2> gpurun_out/bench_r1.err
+python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_small.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r1.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
+python scratch/prof_c4.py > gpurun_out/prof_c4.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:nbg_spmv -s 30 -c 1 -o gpurun_out/spmv_r1 python scratch/prof_c4.py > gpurun_out/ncu_full.log 2>&1
