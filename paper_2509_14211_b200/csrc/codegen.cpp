@@ -191,6 +191,32 @@ struct Gen {
             o << "  const " << ctype(in.t) << " " << v((int)i) << " = " << expr(in, "") << ";\n";
         }
     }
+    // uniform values computed once per CTA into shared memory (spmv: keeps them out of registers
+    // across the step loop) and re-read where the epilogue needs them
+    int n_uniform() const {
+        int k = 0;
+        for (const Ins &in : p.ins) k += in.uniform ? 1 : 0;
+        return k;
+    }
+    void emit_uniform_to_smem(const std::string &arr) {
+        o << "  if (threadIdx.x == 0) {\n";
+        int k = 0;
+        for (size_t i = 0; i < p.ins.size(); i++) {
+            const Ins &in = p.ins[i];
+            if (!in.uniform) continue;
+            o << "    const " << ctype(in.t) << " " << v((int)i) << " = " << expr(in, "") << ";\n";
+            o << "    *(" << ctype(in.t) << "*)&" << arr << "[" << k++ << "] = " << v((int)i) << ";\n";
+        }
+        o << "  }\n";
+    }
+    void emit_uniform_reload(const std::string &ind, const std::string &arr) {
+        int k = 0;
+        for (size_t i = 0; i < p.ins.size(); i++) {
+            const Ins &in = p.ins[i];
+            if (!in.uniform) continue;
+            o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = *(const " << ctype(in.t) << "*)&" << arr << "[" << k++ << "];\n";
+        }
+    }
     void emit_red_decl() {
         for (size_t j = 0; j < p.reds.size(); j++) {
             RedKind k = redkind(p.reds[j]);
@@ -416,7 +442,8 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
     const int NT = spmv_threads(), NW = NT / 32;
-    int hot_bytes = 160 * 1024;                               // measured sweet spot
+    int hot_bytes = 128 * 1024;   // measured: 96-128 KB best; above ~190 KB of total smem the L1 collapses
+    if (const char *e = getenv("NBG_SPMV_HOT_KB")) if (*e) hot_bytes = std::max(0, std::min(200, atoi(e))) * 1024;
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
     const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
@@ -473,8 +500,10 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "    }\n";
     o << "    for (int k = (nv_ << 4) / (int)sizeof(" << XT << ") + threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = X[k];\n";
     o << "  }\n";
+    const int NU = std::max(1, g.n_uniform());
+    o << "  __shared__ unsigned long long s_uni[" << NU << "];\n";
+    g.emit_uniform_to_smem("s_uni");
     o << "  __syncthreads();\n";
-    g.emit_uniform();
     g.emit_red_decl();
     o << "  const long long items = a.nchunks + a.ntiles;\n";
     // tasks are claimed one ahead so the next row task's header load overlaps this task
@@ -570,6 +599,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
       << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
     o << "            a.counters[ch.x] = 0;\n";
     o << "            const long long i = lr.x;\n";
+    g.emit_uniform_reload("            ", "s_uni");
     g.emit_body(
         "            ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
@@ -589,6 +619,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "        const unsigned nm = r == 0 ? nem_[0] : (r == 1 ? nem_[1] : (r == 2 ? nem_[2] : nem_[3]));\n";
     o << "        if (lane + 32 * r < R) {\n";
     o << "          const " << ACC << " acc = ((nm >> lane) & 1u) ? s_racc[rb_ + __popc(nm & ((1u << lane) - 1u))] : (" << ACC << ")(" << IDENT << ");\n";
+    g.emit_uniform_reload("          ", "s_uni");
     g.emit_body(
         "          ",
         [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
