@@ -44,7 +44,7 @@ static const char *ctype_compute(int t) { return t == NBG_BOOL ? "long long" : c
 
 std::string Prog::signature() const {
     std::ostringstream s;
-    s << (spmv ? "S" : "E") << (vec ? "v" : "s") << "|";
+    s << (spmv ? (tp ? "T" : "S") : "E") << (vec ? "v" : "s") << "|";
     if (spmv) s << sp.add << "," << sp.mul << "," << sp.T << "," << sp.xt << "," << sp.at << "," << sp.has_vals << "|";
     for (const Ins &i : ins)
         s << (int)i.k << ":" << i.t << ":" << i.code << ":" << i.a << ":" << i.b << ":" << i.imm0 << ":" << i.imm1
@@ -659,6 +659,276 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     return dyn_bytes;
 }
 
+// ---------------------------------------------------------------- two-phase SpMV
+
+struct SemiringCode {
+    std::string C, XT, ACC, IDENT, ADD, mul;
+};
+
+SemiringCode semiring_code(const SpmvSig &sp) {
+    SemiringCode r;
+    r.C = ctype_compute(sp.T);
+    r.XT = ctype(sp.xt);
+    const bool fT = is_float(sp.T);
+    if (sp.add == NBG_PLUS) {
+        r.ACC = fT ? "double" : "long long";
+        r.IDENT = fT ? "0.0" : "0ll";
+        r.ADD = "(A_ + B_)";
+    } else if (sp.add == NBG_MIN) {
+        r.ACC = r.C;
+        r.IDENT = fT ? (sp.T == NBG_FP32 ? "__int_as_float(0x7f800000)" : "__longlong_as_double(0x7ff0000000000000ll)")
+                     : (sp.T == NBG_INT32 ? "0x7fffffff" : "0x7fffffffffffffffll");
+        r.ADD = "nbg_min(A_, B_)";
+    } else {
+        r.ACC = r.C;
+        r.IDENT = fT ? (sp.T == NBG_FP32 ? "__int_as_float((int)0xff800000)" : "__longlong_as_double((long long)0xfff0000000000000ull)")
+                     : (sp.T == NBG_INT32 ? "((int)0x80000000)" : "((long long)0x8000000000000000ull)");
+        r.ADD = "nbg_max(A_, B_)";
+    }
+    const std::string C = r.C;
+    const std::string av = sp.has_vals ? "((" + C + ")(((const " + std::string(ctype(sp.at)) + "*)a.aval)[P_]))" : "((" + C + ")(a.imm[0]))";
+    const std::string xv = "((" + C + ")(X_))";
+    switch (sp.mul) {
+        case NBG_PLUS: r.mul = "(" + av + " + " + xv + ")"; break;
+        case NBG_MINUS: r.mul = "(" + av + " - " + xv + ")"; break;
+        case NBG_TIMES: r.mul = "(" + av + " * " + xv + ")"; break;
+        case NBG_DIV: r.mul = "nbg_div(" + av + ", " + xv + ")"; break;
+        case NBG_MIN: r.mul = "nbg_min(" + av + ", " + xv + ")"; break;
+        case NBG_MAX: r.mul = "nbg_max(" + av + ", " + xv + ")"; break;
+        case NBG_FIRST: r.mul = av; break;
+        case NBG_SECOND: r.mul = xv; break;
+        case NBG_ABSDIFF: r.mul = "nbg_abs(" + av + " - " + xv + ")"; break;
+        case NBG_MAX_DIVX_C: r.mul = "nbg_max(nbg_div(" + av + ", ((" + C + ")(a.imm[1]))), " + xv + ")"; break;
+        default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
+    }
+    return r;
+}
+
+// Phase 1: per-pair partial sums with the column block in shared memory.  The CTA walks its task
+// range block by block (loads the block's slice of x, then its warps claim the block's tasks); a
+// task is the single-pass row task on pairs instead of rows (same 64-group steps, lane-local split
+// + one segmented scan), gathering only from shared memory; pair totals go to part[pslot[pair]].
+// Chunks of a long pair: the chunk total to partials[], the last chunk (ticket) combines in order.
+std::string gen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {
+    SemiringCode k = semiring_code(sp);
+    const int NT = spmv_threads(), NW = NT / 32;
+    const long long slice = (S * xsize + 15) / 16 * 16;
+    const int dyn = (int)slice + NW * 128 * 8;
+    if (dyn_smem) *dyn_smem = dyn;
+    std::ostringstream o;
+    o << "#define NBG_ADD(A_, B_) " << k.ADD << "\n";
+    o << "__device__ __forceinline__ " << k.C << " nbg_mul(const KArgs &a, long long P_, " << k.XT << " X_) { return " << k.mul << "; }\n";
+    o << "#define NBG_TV(C_, P_, V_) (((C_) >= 0) ? (" << k.ACC << ")nbg_mul(a, (P_), (V_)) : (" << k.ACC << ")(" << k.IDENT << "))\n";
+    o << "#define NBG_GS(C_) xs[(C_) > 0 ? (C_) : 0]\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", 1) " << kname << "(const KArgs a) {\n";
+    o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
+    o << "  __shared__ int s_ctr;\n";
+    o << "  " << k.XT << "* xs = (" << k.XT << "*)nbg_dyn;\n";
+    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    o << "  " << k.ACC << "* s_racc = (" << k.ACC << "*)(nbg_dyn + " << slice << " + warp * 1024);\n";
+    o << "  const int4* __restrict__ CG = (const int4*)a.colidx;\n";
+    o << "  const long long* __restrict__ GRP = a.rowptr;\n";
+    o << "  const " << k.XT << "* __restrict__ X = (const " << k.XT << "*)a.x;\n";
+    o << "  " << k.ACC << "* __restrict__ PART = (" << k.ACC << "*)a.part;\n";
+    o << "  const int q1 = a.cta[blockIdx.x + 1];\n";
+    o << "  int q = a.cta[blockIdx.x];\n";
+    o << "  while (q < q1) {\n";
+    o << "    const int blk = a.tblk[q];\n";
+    o << "    int lo = q, hi = q1;\n";
+    o << "    while (lo < hi) { const int mid = (lo + hi) >> 1; if (a.tblk[mid] <= blk) lo = mid + 1; else hi = mid; }\n";
+    o << "    const int qe = lo;\n";
+    o << "    __syncthreads();\n";
+    o << "    if (threadIdx.x == 0) s_ctr = q;\n";
+    // the block's slice of x (16-byte loads when aligned)
+    o << "    {\n";
+    o << "      const long long c0 = (long long)blk * a.S;\n";
+    o << "      const int cn = (int)((a.ncols_g - c0) < a.S ? (a.ncols_g - c0) : a.S);\n";
+    o << "      const " << k.XT << "* src = X + c0;\n";
+    o << "      const bool al = ((((unsigned long long)src) & 15ull) == 0ull);\n";
+    o << "      const int nv = al ? (int)((cn * (int)sizeof(" << k.XT << ")) >> 4) : 0;\n";
+    o << "      for (int v = threadIdx.x; v < nv; v += 4 * blockDim.x) {\n";
+    o << "        uint4 w_[4];\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) if (v + u * (int)blockDim.x < nv) w_[u] = __ldg((const uint4*)src + v + u * blockDim.x);\n";
+    o << "        #pragma unroll\n        for (int u = 0; u < 4; u++) if (v + u * (int)blockDim.x < nv) ((uint4*)xs)[v + u * blockDim.x] = w_[u];\n";
+    o << "      }\n";
+    o << "      for (int j = (nv << 4) / (int)sizeof(" << k.XT << ") + threadIdx.x; j < cn; j += blockDim.x) xs[j] = src[j];\n";
+    o << "    }\n";
+    o << "    __syncthreads();\n";
+    o << "    for (;;) {\n";
+    o << "      int t_ = 0;\n";
+    o << "      if (lane == 0) t_ = atomicAdd(&s_ctr, 1);\n";
+    o << "      t_ = __shfl_sync(0xffffffffu, t_, 0);\n";
+    o << "      if (t_ >= qe) break;\n";
+    o << "      const int4 tl = ((const int4*)a.tiles)[t_];\n";
+    o << "      const bool is_chunk = (tl.y & 0xff) == 255;\n";
+    o << "      const int R = is_chunk ? 0 : (tl.y & 0xff), NG = tl.y >> 8;\n";
+    o << "      const long long G0 = ((long long)(unsigned)tl.w << 32) | (long long)(unsigned)tl.z;\n";
+    o << "      int4 qa = (2 * lane < NG) ? __ldcs(CG + G0 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "      int4 qb = (2 * lane + 1 < NG) ? __ldcs(CG + G0 + 2 * lane + 1) : make_int4(-1, -1, -1, -1);\n";
+    o << "      int rs_[4];\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
+    o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
+    o << "      unsigned nem_[4];\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) {\n";
+    o << "        const int nx = __shfl_down_sync(0xffffffffu, rs_[r], 1);\n";
+    o << "        const int nf = __shfl_sync(0xffffffffu, r < 3 ? rs_[r < 3 ? r + 1 : 3] : r128_, 0);\n";
+    o << "        const int re = (lane == 31) ? nf : nx;\n";
+    o << "        nem_[r] = __ballot_sync(0xffffffffu, lane + 32 * r < R && re > rs_[r]);\n";
+    o << "      }\n";
+    o << "      " << k.ACC << " carry = " << k.IDENT << ";\n";
+    o << "      int nstarted = 0;\n";
+    o << "      for (int b = 0; b < NG; b += 64) {\n";
+    o << "        const long long P_ = 4 * (G0 + b + 2 * lane);\n";
+    o << "        const int4 ca = qa, cb = qb;\n";
+    o << "        if (b + 64 < NG) {\n";
+    o << "          qa = (b + 64 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "          qb = (b + 65 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+    o << "        }\n";
+    o << "        const " << k.XT << " g0 = NBG_GS(ca.x), g1 = NBG_GS(ca.y), g2 = NBG_GS(ca.z), g3 = NBG_GS(ca.w);\n";
+    o << "        const " << k.XT << " g4 = NBG_GS(cb.x), g5 = NBG_GS(cb.y), g6 = NBG_GS(cb.z), g7 = NBG_GS(cb.w);\n";
+    o << "        unsigned m0_ = 0u, m1_ = 0u;\n";
+    o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) {\n";
+    o << "          const int os_ = rs_[r] - b;\n";
+    o << "          if (((nem_[r] >> lane) & 1u) && os_ >= 0 && os_ < 64) { if (os_ < 32) m0_ |= 1u << os_; else m1_ |= 1u << (os_ - 32); }\n";
+    o << "        }\n";
+    o << "        const unsigned M0 = __reduce_or_sync(0xffffffffu, m0_), M1 = __reduce_or_sync(0xffffffffu, m1_);\n";
+    o << "        const unsigned Mw = lane < 16 ? M0 : M1;\n";
+    o << "        const int sh_ = (2 * lane) & 31;\n";
+    o << "        const bool s0 = (Mw >> sh_) & 1u, s1 = (Mw >> (sh_ + 1)) & 1u;\n";
+    o << "        const int before = (lane < 16 ? 0 : __popc(M0)) + __popc(Mw & ((1u << sh_) - 1u));\n";
+    o << "        " << k.ACC << " v0 = NBG_TV(ca.x, P_, g0);\n";
+    o << "        v0 = NBG_ADD(v0, NBG_TV(ca.y, P_ + 1, g1)); v0 = NBG_ADD(v0, NBG_TV(ca.z, P_ + 2, g2)); v0 = NBG_ADD(v0, NBG_TV(ca.w, P_ + 3, g3));\n";
+    o << "        " << k.ACC << " v1 = NBG_TV(cb.x, P_ + 4, g4);\n";
+    o << "        v1 = NBG_ADD(v1, NBG_TV(cb.y, P_ + 5, g5)); v1 = NBG_ADD(v1, NBG_TV(cb.z, P_ + 6, g6)); v1 = NBG_ADD(v1, NBG_TV(cb.w, P_ + 7, g7));\n";
+    o << "        " << k.ACC << " Sv = s1 ? v1 : NBG_ADD(v0, v1);\n";
+    o << "        if (lane == 0 && !s0 && !s1) Sv = NBG_ADD(carry, Sv);\n";
+    o << "        bool F = s0 || s1 || lane == 0;\n";
+    o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
+    o << "          const " << k.ACC << " Sy = __shfl_up_sync(0xffffffffu, Sv, d);\n";
+    o << "          const bool Fy = __shfl_up_sync(0xffffffffu, F, d);\n";
+    o << "          if (lane >= d && !F) { Sv = NBG_ADD(Sy, Sv); F = Fy; }\n";
+    o << "        }\n";
+    o << "        " << k.ACC << " Sp = __shfl_up_sync(0xffffffffu, Sv, 1);\n";
+    o << "        if (lane == 0) Sp = carry;\n";
+    o << "        if (s0 && (lane > 0 || nstarted > 0)) s_racc[nstarted + before - 1] = Sp;\n";
+    o << "        if (s1) s_racc[nstarted + before + (s0 ? 1 : 0) - 1] = s0 ? v0 : NBG_ADD(Sp, v0);\n";
+    o << "        carry = __shfl_sync(0xffffffffu, Sv, 31);\n";
+    o << "        nstarted += __popc(M0) + __popc(M1);\n";
+    o << "      }\n";
+    o << "      if (is_chunk) {\n";
+    o << "        if (lane == 0) {\n";
+    o << "          const int ci = a.chunks[t_];                              // global chunk index\n";
+    o << "          ((" << k.ACC << "*)a.partials)[ci] = carry;\n";
+    o << "          __threadfence();\n";
+    o << "          const int4 lr = ((const int4*)a.longs)[tl.x];\n";
+    o << "          const int tk = atomicAdd(&a.counters[tl.x], 1);\n";
+    o << "          if (tk == lr.z - 1) {\n";
+    o << "            __threadfence();\n";
+    o << "            " << k.ACC << " acc = " << k.IDENT << ";\n";
+    o << "            for (int j = 0; j < lr.z; j++) { const " << k.ACC << " pj = *(volatile const " << k.ACC << "*)(((const " << k.ACC
+      << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
+    o << "            a.counters[tl.x] = 0;\n";
+    o << "            PART[a.pslot[lr.x]] = acc;\n";
+    o << "          }\n";
+    o << "        }\n";
+    o << "        __syncwarp();\n";
+    o << "        continue;\n";
+    o << "      }\n";
+    o << "      if (lane == 0 && nstarted > 0) s_racc[nstarted - 1] = carry;\n";
+    o << "      __syncwarp();\n";
+    // pairs are never empty: pair j of the task -> rank j
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) {\n";
+    o << "        const int j = lane + 32 * r;\n";
+    o << "        if (j < R) PART[a.pslot[tl.x + j]] = s_racc[j];\n";
+    o << "      }\n";
+    o << "      __syncwarp();\n";
+    o << "    }\n";
+    o << "    q = qe;\n";
+    o << "  }\n";
+    o << "}\n";
+    return o.str();
+}
+
+// Phase 2: row i = its pair partials (slots rowslot[i] .. rowslot[i+1], block order) combined in
+// order, then the fused epilogue.  Warp tiles of 128 rows (lane l: rows l, l + 32, l + 64, l + 96),
+// claimed from a shared-memory counter; reductions as in the single-pass skeleton.
+int gen_tp2(Gen &g, const std::string &kname) {
+    const Prog &p = g.p;
+    auto &o = g.o;
+    SemiringCode k = semiring_code(p.sp);
+    std::vector<int> fplus;
+    for (size_t j = 0; j < p.reds.size(); j++)
+        if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
+    const int NF = (int)fplus.size();
+    const int NT = 256, NW = NT / 32;
+    o << "#define NBG_ADD(A_, B_) " << k.ADD << "\n#define NBG_NF " << NF << "\n#define NBG_NW " << NW << "\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ") " << kname << "(const KArgs a) {\n";
+    o << "  __shared__ double nbg_sh[32];\n";
+    o << "  __shared__ int s_ctr;\n";
+    if (NF) o << "  __shared__ u64 s_x[NBG_NW * NBG_NF * 11];\n";
+    const int NU = std::max(1, g.n_uniform());
+    o << "  __shared__ unsigned long long s_uni[" << NU << "];\n";
+    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    o << "  const " << k.ACC << "* __restrict__ PART = (const " << k.ACC << "*)a.part;\n";
+    o << "  const long long* __restrict__ RS = a.rowslot;\n";
+    o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
+    if (NF) o << "  for (int k = threadIdx.x; k < NBG_NW * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
+    g.emit_uniform_to_smem("s_uni");
+    o << "  __syncthreads();\n";
+    g.emit_red_decl();
+    o << "  const long long ntl = (a.n + 127) / 128;\n";
+    o << "  for (;;) {\n";
+    o << "    int l_ = 0;\n";
+    o << "    if (lane == 0) l_ = atomicAdd(&s_ctr, 1);\n";
+    o << "    l_ = __shfl_sync(0xffffffffu, l_, 0);\n";
+    o << "    const long long tt = (long long)blockIdx.x + (long long)l_ * gridDim.x;\n";
+    o << "    if (tt >= ntl) break;\n";
+    o << "    long long s0_[4], s1_[4];\n";
+    o << "    #pragma unroll\n    for (int r = 0; r < 4; r++) {\n";
+    o << "      const long long i = 128 * tt + lane + 32 * r;\n";
+    o << "      s0_[r] = (i < a.n) ? RS[i] : 0; s1_[r] = (i < a.n) ? RS[i + 1] : 0;\n";
+    o << "    }\n";
+    for (int j : fplus) o << "    r" << j << " = 0.0;\n";
+    o << "    #pragma unroll\n    for (int r = 0; r < 4; r++) {\n";
+    o << "      const long long i = 128 * tt + lane + 32 * r;\n";
+    o << "      if (i < a.n) {\n";
+    o << "        " << k.ACC << " acc = " << k.IDENT << ";\n";
+    o << "        for (long long s = s0_[r]; s < s1_[r]; s++) acc = NBG_ADD(acc, PART[s]);\n";
+    g.emit_uniform_reload("        ", "s_uni");
+    g.emit_body(
+        "        ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
+        [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    o << "      }\n";
+    o << "    }\n";
+    for (int f = 0; f < NF; f++) {
+        int j = fplus[f];
+        o << "    { double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f << ") * 11, t_); }\n";
+    }
+    o << "  }\n";
+    o << "  __syncthreads();\n";
+    for (int f = 0; f < NF; f++) {
+        int j = fplus[f];
+        o << "  if (threadIdx.x < 11) {\n";
+        o << "    u64 v_ = 0ull;\n";
+        o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 11 + threadIdx.x]; v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
+        o << "    if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
+        o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
+        o << "  }\n";
+    }
+    for (size_t j = 0; j < p.reds.size(); j++) {
+        if (std::find(fplus.begin(), fplus.end(), (int)j) != fplus.end()) continue;
+        int kind = redkind(g, p.reds[j]);
+        if (kind == 0 || kind == 2 || kind == 3)
+            o << "  nbg_block_finish_f(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+        else
+            o << "  nbg_block_finish_i(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+    }
+    o << "}\n";
+    return 0;
+}
+
 }  // namespace
 
 extern const char *NBG_PRELUDE_SRC;
@@ -673,11 +943,17 @@ int spmv_threads() {
     return v;
 }
 
+std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {
+    return std::string(NBG_PRELUDE_SRC) + "\n// ---- two-phase spmv, phase 1\n" + gen_tp1(sp, kname, xsize, S, dyn_smem);
+}
+
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem, int *hot_entries) {
     Gen g(p);
     g.o << NBG_PRELUDE_SRC << "\n// ---- generated region: " << p.signature() << "\n";
     int smem = 0;
-    if (p.spmv)
+    if (p.spmv && p.tp)
+        smem = gen_tp2(g, kname);
+    else if (p.spmv)
         smem = gen_spmv(g, kname, hot_entries);
     else
         gen_ewise(g, kname, p.vec);

@@ -181,6 +181,226 @@ int bits_for(int64_t n) {
     return b;
 }
 
+
+// ---- two-phase plan kernels
+__global__ void k_rowid(long long nnz, long long n, const long long *rowptr, int *rowid) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+        long long lo = 0, hi = n;
+        while (hi - lo > 1) {
+            long long mid = (lo + hi) >> 1;
+            if (rowptr[mid] <= p) lo = mid; else hi = mid;
+        }
+        rowid[p] = (int)lo;
+    }
+}
+__global__ void k_blk_keys(long long nnz, const int *g, long long S, unsigned *key, int *val) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+        key[p] = (unsigned)(g[p] / S);
+        val[p] = (int)p;
+    }
+}
+// sorted position k -> pair start flag
+__global__ void k_pair_flags(long long nnz, const unsigned *bk, const int *pv, const int *rowid, int *flag) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
+        flag[k] = (k == 0 || bk[k] != bk[k - 1] || rowid[pv[k]] != rowid[pv[k - 1]]) ? 1 : 0;
+}
+__global__ void k_pair_info(long long nnz, const int *flag, const int *pid, const unsigned *bk, const int *pv, const int *rowid,
+                            int *prow, int *pblk, long long *pk0) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x)
+        if (flag[k]) {
+            const int q = pid[k] - 1;
+            prow[q] = rowid[pv[k]];
+            pblk[q] = (int)bk[k];
+            pk0[q] = k;
+        }
+}
+__global__ void k_pair_groups(long long np, long long nnz, const long long *pk0, long long *ng) {
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q <= np; q += (long long)gridDim.x * blockDim.x)
+        ng[q] = q == np ? 0 : ((q + 1 < np ? pk0[q + 1] : nnz) - pk0[q] + 3) / 4;
+}
+__global__ void k_pair_fill(long long nnz, const int *pid, const long long *pk0, const long long *grp, const int *pv, const int *g,
+                            const unsigned *bk, long long S, int *cg) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (long long)gridDim.x * blockDim.x) {
+        const int q = pid[k] - 1;
+        cg[4 * grp[q] + (k - pk0[q])] = (int)(g[pv[k]] - (long long)bk[k] * S);
+    }
+}
+__global__ void k_iota(long long m, int *v) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m; k += (long long)gridDim.x * blockDim.x) v[k] = (int)k;
+}
+__global__ void k_row_count(long long np, const int *prow, long long *cnt) {
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < np; q += (long long)gridDim.x * blockDim.x)
+        atomicAdd((unsigned long long *)&cnt[prow[q]], 1ull);
+}
+__global__ void k_slot_of(long long np, const int *order, int *slot) {
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < np; r += (long long)gridDim.x * blockDim.x)
+        slot[order[r]] = (int)r;
+}
+
+}  // namespace
+
+TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta) {
+    if (!A.plan) gpu_build_spmv_plan(c, A);
+    SpmvPlan &P = *A.plan;
+    if (!P.relabel || !P.colidx_g || (xsize != 4 && xsize != 8) || A.nnz == 0) return nullptr;
+    // experimental: opt-in with NBG_SPMV_TP=1 until it beats the single pass
+    const char *e = getenv("NBG_SPMV_TP");
+    if (!(e && e[0] == '1')) return nullptr;
+    auto &slotp = P.tp[xsize == 4 ? 0 : 1];
+    if (slotp && slotp->ncta == ncta) return slotp.get();
+    auto T = std::make_unique<TpPlan>();
+    T->xsize = xsize;
+    T->S = (128 * 1024) / xsize;
+    const long long nnz = A.nnz, n = A.nrows;
+    const long long S = T->S;
+    T->nblocks = (P.ncols_g + S - 1) / S;
+    const int gr = grid_for(nnz, c.num_sms);
+    // entries sorted (stable) by column block: (block, row, position) order
+    BufP rowid = alloc_buf(c, (size_t)nnz * 4);
+    k_rowid<<<gr, 256, 0, c.stream>>>(nnz, n, (const long long *)A.rowptr->d, (int *)rowid->d);
+    BufP bk = alloc_buf(c, (size_t)nnz * 4), bk2 = alloc_buf(c, (size_t)nnz * 4);
+    BufP pv = alloc_buf(c, (size_t)nnz * 4), pv2 = alloc_buf(c, (size_t)nnz * 4);
+    k_blk_keys<<<gr, 256, 0, c.stream>>>(nnz, (const int *)P.colidx_g->d, S, (unsigned *)bk->d, (int *)pv->d);
+    const int bbits = bits_for(std::max<int64_t>(T->nblocks, 2));
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned *)bk->d, (unsigned *)bk2->d, (const int *)pv->d, (int *)pv2->d,
+                                    (int64_t)nnz, 0, bbits, c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    NBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp->d, tb, (const unsigned *)bk->d, (unsigned *)bk2->d, (const int *)pv->d,
+                                             (int *)pv2->d, (int64_t)nnz, 0, bbits, c.stream));
+    // pairs
+    BufP flag = alloc_buf(c, (size_t)nnz * 4), pid = alloc_buf(c, (size_t)nnz * 4);
+    k_pair_flags<<<gr, 256, 0, c.stream>>>(nnz, (const unsigned *)bk2->d, (const int *)pv2->d, (const int *)rowid->d, (int *)flag->d);
+    cub::DeviceScan::InclusiveSum(nullptr, tb, (const int *)flag->d, (int *)pid->d, (int64_t)nnz, c.stream);
+    if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+    NBG_CUDA(cub::DeviceScan::InclusiveSum(tmp->d, tb, (const int *)flag->d, (int *)pid->d, (int64_t)nnz, c.stream));
+    int np = 0;
+    NBG_CUDA(cudaMemcpyAsync(&np, (const int *)pid->d + nnz - 1, 4, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    T->npairs = np;
+    BufP prow = alloc_buf(c, (size_t)np * 4), pblk = alloc_buf(c, (size_t)np * 4), pk0 = alloc_buf(c, (size_t)np * 8);
+    k_pair_info<<<gr, 256, 0, c.stream>>>(nnz, (const int *)flag->d, (const int *)pid->d, (const unsigned *)bk2->d, (const int *)pv2->d,
+                                          (const int *)rowid->d, (int *)prow->d, (int *)pblk->d, (long long *)pk0->d);
+    BufP ngp = alloc_buf(c, (size_t)(np + 1) * 8);
+    T->grp = alloc_buf(c, (size_t)(np + 1) * 8);
+    k_pair_groups<<<grid_for(np + 1, c.num_sms), 256, 0, c.stream>>>(np, nnz, (const long long *)pk0->d, (long long *)ngp->d);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)ngp->d, (long long *)T->grp->d, (int64_t)(np + 1), c.stream);
+    if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+    NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)ngp->d, (long long *)T->grp->d, (int64_t)(np + 1), c.stream));
+    std::vector<long long> gph((size_t)np + 1);
+    std::vector<int> pbh((size_t)np);
+    NBG_CUDA(cudaMemcpyAsync(gph.data(), T->grp->d, (size_t)(np + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaMemcpyAsync(pbh.data(), pblk->d, (size_t)np * 4, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    const long long G = gph[np];
+    T->ngroups = G;
+    T->cg = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * 4);
+    NBG_CUDA(cudaMemsetAsync(T->cg->d, 0xff, (size_t)std::max<long long>(4 * G, 4) * 4, c.stream));
+    k_pair_fill<<<gr, 256, 0, c.stream>>>(nnz, (const int *)pid->d, (const long long *)pk0->d, (const long long *)T->grp->d,
+                                          (const int *)pv2->d, (const int *)P.colidx_g->d, (const unsigned *)bk2->d, S, (int *)T->cg->d);
+    // slots in (row, block) order: stable sort of the pairs by row
+    BufP idq = alloc_buf(c, (size_t)np * 4), ord = alloc_buf(c, (size_t)np * 4), rk2 = alloc_buf(c, (size_t)np * 4);
+    k_iota<<<grid_for(np, c.num_sms), 256, 0, c.stream>>>(np, (int *)idq->d);
+    const int rbits = bits_for(std::max<int64_t>(n, 2));
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned *)prow->d, (unsigned *)rk2->d, (const int *)idq->d, (int *)ord->d,
+                                    (int64_t)np, 0, rbits, c.stream);
+    if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+    NBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp->d, tb, (const unsigned *)prow->d, (unsigned *)rk2->d, (const int *)idq->d,
+                                             (int *)ord->d, (int64_t)np, 0, rbits, c.stream));
+    T->slot = alloc_buf(c, (size_t)np * 4);
+    k_slot_of<<<grid_for(np, c.num_sms), 256, 0, c.stream>>>(np, (const int *)ord->d, (int *)T->slot->d);
+    BufP rcnt = alloc_buf(c, (size_t)(n + 1) * 8);
+    NBG_CUDA(cudaMemsetAsync(rcnt->d, 0, (size_t)(n + 1) * 8, c.stream));
+    k_row_count<<<grid_for(np, c.num_sms), 256, 0, c.stream>>>(np, (const int *)prow->d, (long long *)rcnt->d);
+    T->rowslot = alloc_buf(c, (size_t)(n + 1) * 8);
+    cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)rcnt->d, (long long *)T->rowslot->d, (int64_t)(n + 1), c.stream);
+    if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+    NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)rcnt->d, (long long *)T->rowslot->d, (int64_t)(n + 1), c.stream));
+    T->part = alloc_buf(c, (size_t)std::max(np, 1) * 8);
+    NBG_CUDA(cudaGetLastError());
+    c.stats.kernels_launched += 14;
+
+    // ---- tasks (host): block-major runs of <= 128 pairs / <= 512 groups inside one block; pairs
+    // with > 512 groups become chunk tasks of 512 groups (same block), combined by a ticket
+    std::vector<int> tasks, tblk, chunks, longs;
+    std::vector<long long> tcost;
+    long long nch = 0, L = 0;
+    for (long long q = 0; q < np;) {
+        const long long gl = gph[q + 1] - gph[q];
+        const int b = pbh[q];
+        if (gl > SP_LONG_G) {
+            const long long nc = (gl + SP_CHUNK_G - 1) / SP_CHUNK_G;
+            longs.push_back((int)q);
+            longs.push_back((int)nch);
+            longs.push_back((int)nc);
+            longs.push_back(0);
+            for (long long u = 0; u < nc; u++) {
+                const long long gb = gph[q] + u * SP_CHUNK_G;
+                const long long cnt = std::min<long long>(SP_CHUNK_G, gph[q + 1] - gb);
+                tasks.push_back((int)L);
+                tasks.push_back((int)(255 | (cnt << 8)));          // 255 rows marks a chunk task
+                tasks.push_back((int)(unsigned)(gb & 0xffffffffll));
+                tasks.push_back((int)(unsigned)((unsigned long long)gb >> 32));
+                tblk.push_back(b);
+                tcost.push_back(cnt + 16);
+                chunks.push_back((int)nch);           // task -> global chunk index
+                nch++;
+            }
+            L++;
+            q++;
+            continue;
+        }
+        const long long st = q;
+        long long ngr = 0;
+        while (q < np && q - st < SP_TASK_ROWS && pbh[q] == b) {
+            const long long g2 = gph[q + 1] - gph[q];
+            if (g2 > SP_LONG_G) break;
+            if (q > st && ngr + g2 > SP_TASK_G) break;
+            ngr += g2;
+            q++;
+        }
+        tasks.push_back((int)st);
+        tasks.push_back((int)((q - st) | (ngr << 8)));
+        tasks.push_back((int)(unsigned)(gph[st] & 0xffffffffll));
+        tasks.push_back((int)(unsigned)((unsigned long long)gph[st] >> 32));
+        tblk.push_back(b);
+        tcost.push_back(ngr + (q - st) / 4 + 16);
+        chunks.push_back(-1);
+    }
+    T->ntasks = (int64_t)tblk.size();
+    T->nchunks = nch;
+    T->nlong = L;
+    // CTA ranges balanced by cost (block switches cost a slice load: + 2048 per block boundary)
+    std::vector<long long> pre(T->ntasks + 1, 0);
+    for (long long k = 0; k < T->ntasks; k++) pre[k + 1] = pre[k] + tcost[k];
+    std::vector<int> cta(ncta + 1, 0);
+    for (int k = 0; k <= ncta; k++) {
+        const long long target = pre[T->ntasks] * k / ncta;
+        cta[k] = (int)(std::lower_bound(pre.begin(), pre.end(), target) - pre.begin());
+    }
+    cta[ncta] = (int)T->ntasks;
+    T->ncta = ncta;
+    T->tasks = alloc_buf(c, std::max<size_t>(tasks.size(), 4) * 4);
+    NBG_CUDA(cudaMemcpyAsync(T->tasks->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    T->tblk = alloc_buf(c, std::max<size_t>(tblk.size(), 1) * 4);
+    NBG_CUDA(cudaMemcpyAsync(T->tblk->d, tblk.data(), tblk.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    T->cta = alloc_buf(c, cta.size() * 4);
+    NBG_CUDA(cudaMemcpyAsync(T->cta->d, cta.data(), cta.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    T->chunks = alloc_buf(c, std::max<size_t>(chunks.size(), 1) * 4);
+    NBG_CUDA(cudaMemcpyAsync(T->chunks->d, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    if (L > 0) {
+        T->longs = alloc_buf(c, longs.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(T->longs->d, longs.data(), longs.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        T->counters = alloc_buf(c, (size_t)L * 4);
+        NBG_CUDA(cudaMemsetAsync(T->counters->d, 0, (size_t)L * 4, c.stream));
+        T->partials = alloc_buf(c, (size_t)nch * 8);
+    }
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    slotp = std::move(T);
+    return slotp.get();
+}
+
+namespace {
 }  // namespace
 
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst) {
@@ -301,6 +521,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         colsrc = alloc_buf(c, (size_t)A.nnz * 4);
         k_map_cols<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (const int *)P->perm->d,
                                                                      (int *)colsrc->d);
+        P->colidx_g = colsrc;
         NBG_CUDA(cudaGetLastError());
         P->ncols_g = ng;
         P->relabel = true;

@@ -33,6 +33,13 @@ struct KArgs {
     const int *oscat[NBG_MAX_OUT];
     long long hc;
     long long nnz;
+    const int *tblk;
+    const int *cta;
+    const int *pslot;
+    const long long *rowslot;
+    void *part;
+    long long S;
+    long long ncols_g;
 };
 
 // ------------------------------------------------------------------ operators in type T

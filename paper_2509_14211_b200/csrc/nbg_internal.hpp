@@ -112,6 +112,8 @@ double slot_value(const unsigned long long *s, SFmt fmt);
 
 // ---------------------------------------------------------------- matrices
 
+struct TpPlan;
+
 struct SpmvPlan {
     // Rows are stored in 4-entry groups (padded with index -1) so a 16-byte index load never mixes
     // two rows.  Tiles: runs of <= 32 consecutive rows with <= 512 groups (one warp task, lane j ->
@@ -134,6 +136,34 @@ struct SpmvPlan {
     int64_t ncols_g = 0;     // number of non-empty columns
     BufP perm;               // int32[ncols] old -> new id, -1 for an empty column
     BufP iperm;              // int32[ncols_g] new -> old id
+    BufP colidx_g;           // int32[nnz] gather-layout column indices (relabelled matrices; two-phase build)
+    std::unique_ptr<TpPlan> tp[2];   // two-phase plans for 4- and 8-byte gathered elements (lazy)
+};
+
+// Two-phase column-blocked SpMV plan, one per gathered element size.
+// Phase 1: the gather layout's columns are cut into blocks of S columns (S * element size = 128 KB,
+// one block in shared memory at a time); the entries of row i in block b form a "pair" (b, i).
+// Pairs are stored block-major in the same 4-entry group layout as the single-pass plan, with
+// block-local column indices, and processed by warp tasks (<= 128 pairs, one block per task);
+// each pair's partial sum goes to part[slot], where slots are ordered (row, block).
+// Phase 2: row i's value = its slots rowslot[i] .. rowslot[i+1] combined in block order.
+struct TpPlan {
+    int xsize = 4;               // gathered element size this plan is for
+    int64_t S = 0;               // columns per block
+    int64_t nblocks = 0, npairs = 0, ngroups = 0, ntasks = 0, nchunks = 0, nlong = 0;
+    BufP grp;        // int64[npairs + 1]  first group of each pair
+    BufP cg;         // int32[4 * ngroups]  block-local column index per padded position, -1 = pad
+    BufP tasks;      // int4 {pair_begin, npairs | ngroups << 8, first_group_lo, first_group_hi}
+    BufP tblk;       // int32[ntasks]  column block of each task (tasks are block-major)
+    BufP cta;        // int32[ncta + 1]  task range of each CTA
+    int ncta = 0;
+    BufP chunks;     // int32[ntasks]  global chunk index of a chunk task, -1 for a pair task
+    BufP longs;      // int4 {pair, first_chunk, nchunks, 0}
+    BufP counters;   // int[nlong]
+    BufP partials;   // double[nchunks]
+    BufP slot;       // int32[npairs]  (row, block)-ordered slot of each pair
+    BufP rowslot;    // int64[n + 1]   first slot of each row
+    BufP part;       // double[npairs] per-pair partial sums (phase 1 -> phase 2)
 };
 
 struct Mat {
@@ -210,6 +240,7 @@ struct Prog {
     std::vector<OutV> outs;
     std::vector<RedOut> reds;
     bool spmv = false;
+    bool tp = false;        // spmv through the two-phase plan: this program is phase 2 (combine + epilogue)
     bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
     SpmvSig sp;
     int n_in = 0, n_out = 0, n_imm = 0, n_sin = 0, n_red = 0;
@@ -240,6 +271,14 @@ struct KArgs {
     const int *oscat[MAX_OUT];   // per output: scatter map (gather layout) or null
     long long hc;                // spmv: entries of the gathered vector cached in shared memory
     long long nnz;               // spmv: number of stored entries (bounds of vector index loads)
+    // two-phase spmv (TpPlan)
+    const int *tblk;             // phase 1: column block of each task
+    const int *cta;              // phase 1: task range of each CTA
+    const int *pslot;            // phase 1: (row, block) slot of each pair
+    const long long *rowslot;    // phase 2: first slot of each row
+    void *part;                  // per-slot partial sums (accumulator type)
+    long long S;                 // phase 1: columns per block
+    long long ncols_g;           // phase 1: columns of the gather layout
 };
 
 struct Kernel {
@@ -338,6 +377,7 @@ void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
 
 // codegen / jit
 int spmv_threads();   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
+std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
 KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0);
 void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);
@@ -346,6 +386,7 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst);
 MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out);
 void gpu_build_spmv_plan(Ctx &c, Mat &A);
+TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta);   // null if not applicable
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
 void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng);
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);

@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <functional>
+#include <sstream>
 #include <unordered_set>
 
 #include "nbg_internal.hpp"
@@ -571,20 +572,67 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         items = (A.plan->ntiles + A.plan->nchunks + nw - 1) / nw;   // one task per warp
         args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
+        // two-phase column-blocked plan (large relabelled matrices, 4/8-byte gathered elements)
+        TpPlan *T = (!A.vals && n > 0) ? gpu_tp_plan(c, A, (int)type_size(u->type), c.num_sms) : nullptr;
+        if (T) {
+            p.tp = true;
+            args.rowslot = (const long long *)T->rowslot->d;
+            args.part = T->part->d;
+            items = (n + 127) / 128 / 8 + 1;      // phase 2: 128-row tiles, 8 warps per CTA
+        }
     } else {
         items = (n + 1023) / 1024;
     }
     for (int k = 0; k < p.n_imm; k++) args.imm[k] = B.imm[k];
+
+    if (p.tp) {
+        // ---- phase 1: per-(row, column block) partial sums; its kernel depends on the semiring only
+        Mat &A = *B.mxv->A;
+        TpPlan *T = gpu_tp_plan(c, A, (int)type_size(p.sp.xt), c.num_sms);
+        std::ostringstream k1;
+        k1 << "TP1|" << p.sp.add << "," << p.sp.mul << "," << p.sp.T << "," << p.sp.xt << "," << p.sp.at << "|" << T->S << "|"
+           << spmv_threads();
+        KernelP kp1;
+        auto it1 = c.plans.find(k1.str());
+        if (it1 == c.plans.end()) {
+            char nm[48];
+            snprintf(nm, sizeof nm, "nbg_tp1_%016llx", (unsigned long long)hash_str(k1.str()));
+            int smem = 0;
+            std::string src = codegen_tp1(p.sp, nm, (int)type_size(p.sp.xt), T->S, &smem);
+            kp1 = jit_compile(c, src, nm, true, smem);
+            c.plans[k1.str()] = kp1;
+            c.stats.plans_built++;
+        } else {
+            kp1 = it1->second;
+            c.stats.plan_hits++;
+        }
+        KArgs a1 = args;
+        a1.rowptr = (const long long *)T->grp->d;
+        a1.colidx = (const int *)T->cg->d;
+        a1.tiles = (const int *)T->tasks->d;
+        a1.chunks = (const int *)T->chunks->d;
+        a1.longs = (const int *)(T->longs ? T->longs->d : nullptr);
+        a1.counters = (int *)(T->counters ? T->counters->d : nullptr);
+        a1.partials = (double *)(T->partials ? T->partials->d : nullptr);
+        a1.tblk = (const int *)T->tblk->d;
+        a1.cta = (const int *)T->cta->d;
+        a1.pslot = (const int *)T->slot->d;
+        a1.part = T->part->d;
+        a1.S = T->S;
+        a1.ncols_g = A.plan->ncols_g;
+        a1.nnz = 4 * T->ngroups;
+        if (T->ntasks > 0) launch(c, *kp1, a1, T->ncta, "spmv");
+    }
 
     std::string sig = p.signature();
     KernelP kern;
     auto it = c.plans.find(sig);
     if (it == c.plans.end()) {
         char nm[48];
-        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.spmv ? "spmv" : "ewise", (unsigned long long)hash_str(sig));
+        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? "spmv" : "ewise"), (unsigned long long)hash_str(sig));
         int smem = 0, hot = 0;
         std::string src = codegen(p, nm, &smem, &hot);
-        kern = jit_compile(c, src, nm, p.spmv, smem);
+        kern = jit_compile(c, src, nm, p.spmv && !p.tp, smem);
         kern->hot = hot;
         c.plans[sig] = kern;
         c.stats.plans_built++;
@@ -592,10 +640,10 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         kern = it->second;
         c.stats.plan_hits++;
     }
-    if (p.spmv) {
+    if (p.spmv && !p.tp) {
         if (args.hc > kern->hot) args.hc = kern->hot;
     }
-    if (items > 0 && n > 0) launch(c, *kern, args, items, p.spmv ? "spmv" : "ewise");
+    if (items > 0 && n > 0) launch(c, *kern, args, items, p.tp ? "spmv_p2" : (p.spmv ? "spmv" : "ewise"));
 
     // provenance of the written buffers (for hints): base signature + output index
     // (set by the caller through B.prog before hints were appended)

@@ -324,6 +324,7 @@ def test_relabel_is_bit_exact(nbg, T, monkeypatch):
     without it are identical bit for bit."""
     t = nbg.TYPE_OF[T]
     out = {}
+    monkeypatch.setenv("NBG_SPMV_TP", "0")      # the single-pass plan (the two-phase plan reorders sums)
     for flag in ("0", "1"):
         monkeypatch.setenv("NBG_RELABEL", flag)
         c = nbg.nbg_init(nbg.NONBLOCKING, 0)
@@ -343,3 +344,27 @@ def test_relabel_is_bit_exact(nbg, T, monkeypatch):
         assert np.array_equal(h0, h1) if T == "fp32" else rel(h0, h1) <= 1e-12
     assert np.array_equal(out["0"][1], out["1"][1])
     assert out["1"][2]["side_outputs"] > 0
+
+
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+def test_two_phase_matches_oracle(nbg, T, monkeypatch):
+    """The opt-in two-phase column-blocked SpMV against the oracle, and
+    deterministic: two solves give identical bits."""
+    monkeypatch.setenv("NBG_SPMV_TP", "1")
+    t = nbg.TYPE_OF[T]
+    npT = nbg.NP_OF[t]
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 16, 16, 5)
+        rp, ci = nbg.nbg_matrix_export_csr(c, A)
+        odeg = nbg.nbg_vector_export_dense(c, deg)
+        runs = []
+        for _ in range(2):
+            r, s, h = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=10, type=t)
+            runs.append((nbg.nbg_vector_export_dense(c, r), h))
+        ro, so, dho, _ = oracle.pagerank(rp, ci, odeg, dtype=npT, itermax=10)
+        assert np.array_equal(runs[0][0], runs[1][0])
+        assert rel(runs[0][0], ro) <= (1e-5 if T == "fp32" else 1e-10)
+        assert delta_close(runs[0][1], dho, ro, npT)
+    finally:
+        nbg.nbg_finalize(c)
