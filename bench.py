@@ -298,6 +298,84 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+# ------------------------------------------------------------------ config 2: fused elementwise chain
+
+def run_chain(args):
+    """BASELINE config 2: z = x * (y + 1), then c1..c5 and reduce(+) over n = 2^24 (SURVEY 8(a)
+    a13), fused (nonblocking: one pass, every intermediate elided) vs blocking (one kernel per op).
+    value = fused GB/s over the algorithmic bytes 2 w n (x and y read once)."""
+    import torch
+    from paper_2509_14211_b200 import nbg
+    torch.cuda.set_device(0)
+    n = inputs.CONFIGS["c2"]["n"]
+    npT = np.float32 if args.dtype == "fp32" else np.float64
+    t = nbg.FP32 if args.dtype == "fp32" else nbg.FP64
+    w = 4 if args.dtype == "fp32" else 8
+    x, y = inputs.uniform_vectors(n, args.seed, npT)
+    stream = torch.cuda.current_stream()
+    out = {}
+    for mode, name in ((nbg.NONBLOCKING, "fused"), (nbg.BLOCKING, "blocking")):
+        c = nbg.nbg_init(mode, 0, stream.cuda_stream)
+        vx = nbg.nbg_vector_from_dense(c, t, x)
+        vy = nbg.nbg_vector_from_dense(c, t, y)
+
+        def step():
+            a = nbg.nbg_apply(c, t, "ADD_C", vy, 1.0)
+            z = nbg.nbg_ewise_mult(c, t, "TIMES", vx, a)
+            c1 = nbg.nbg_apply(c, t, "MUL_C", z, 0.5)
+            c2 = nbg.nbg_ewise_add(c, t, "PLUS", c1, vx)
+            c3 = nbg.nbg_ewise_mult(c, t, "TIMES", c2, vy)
+            c4 = nbg.nbg_apply(c, t, "ABS_SUB_C", c3, 0.25)
+            c5 = nbg.nbg_ewise_add(c, t, "MAX", c4, z)
+            s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", c5)
+            for h in (a, z, c1, c2, c3, c4, c5):
+                nbg.nbg_vector_free(c, h)
+            v = nbg.nbg_scalar_get(c, s)
+            nbg.nbg_scalar_free(c, s)
+            return v
+
+        for _ in range(args.warmup):
+            step()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")      # > L2: inputs come from HBM
+        ms = 0.0
+        st0 = nbg.nbg_get_stats(c)
+        nbg.nbg_set_timing(c, 1)
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        st1 = nbg.nbg_get_stats(c)
+        kms, kn = nbg.nbg_get_timing(c, "ewise")          # device time of the chain's kernels
+        nbg.nbg_set_timing(c, 0)
+        out[name] = (ms / args.steps, (st1["kernels_launched"] - st0["kernels_launched"]) / args.steps, kms / args.steps)
+        nbg.nbg_vector_free(c, vx)
+        nbg.nbg_vector_free(c, vy)
+        nbg.nbg_finalize(c)
+    pk, pk_src = peaks()
+    b_alg = 2 * w * n
+    fused_ms, fused_k, fused_kms = out["fused"]
+    blk_ms, blk_k, blk_kms = out["blocking"]
+    gbs = b_alg / (fused_ms * 1e-3) / 1e9            # whole step: record 8 ops + wait + scalar read-back
+    kgbs = b_alg / (fused_kms * 1e-3) / 1e9          # the fused kernel alone (CUDA events on its stream)
+    return {"metric": "config-2 elementwise chain, fused HBM GB/s (x, y read once)", "value": round(gbs, 1), "unit": "GB/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(fused_ms, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32" if w == 4 else "f64",
+            "data": "synthetic",
+            "config": {"workload": f"c2: chain of 8 ops + reduce(+), n = 2^24, seed {args.seed}",
+                       "l2": "flushed (256 MB write) before every step"},
+            "roofline": {"bound": "hbm", "kernel": "fused chain (nbg_ewise_*)", "achieved": round(kgbs, 1), "peak": pk,
+                         "peak_source": pk_src, "unit": "GB/s", "frac": round(kgbs / pk, 4), "traffic": None,
+                         "bytes_per_launch": b_alg, "avg_launch_us": round(fused_kms * 1e3, 2)},
+            "blocking": {"ms_per_step": round(blk_ms, 4), "kernels_per_step": blk_k, "kernel_ms_per_step": round(blk_kms, 4),
+                         "speedup_fused_vs_blocking": round(blk_ms / fused_ms, 2),
+                         "kernel_speedup_fused_vs_blocking": round(blk_kms / fused_kms, 2)},
+            "gpu_launches": int(round(fused_k * args.steps))}
+
+
 # ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
 
 def oracle_graph(cfg, seed):
@@ -363,7 +441,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c1", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"], help="c2 only")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-sweeps", type=int, default=3)
     ap.add_argument("--ref-sweeps", type=int, default=2)
@@ -377,6 +456,11 @@ def main():
     if world != args.gpus and world == 1 and args.gpus > 1:
         print(json.dumps({"error": "--gpus N>1 must be launched with torchrun"}))
         sys.exit(2)
+    if args.workload == "c2":
+        res = run_chain(args) if args.impl == "ours" and rank == 0 else None
+        if rank == 0 and res is not None:
+            print(json.dumps(res), flush=True)
+        return
     if args.impl == "reference":
         res = run_reference(args, rank, world)
     else:

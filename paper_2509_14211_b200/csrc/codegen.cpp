@@ -340,26 +340,37 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     o << "  const long long stride = (long long)gridDim.x * blockDim.x;\n";
     o << "  long long tail0 = 0;\n";
     if (vec) {
+        // 4 grid-stride iterations per trip: all 16-byte loads of the trip are issued before any
+        // use, so every thread keeps 4 loads per input in flight (memory-level parallelism)
         o << "  const long long nv = n >> 2;\n  tail0 = nv << 2;\n";
-        o << "  for (long long vi = (long long)blockIdx.x * blockDim.x + threadIdx.x; vi < nv; vi += stride) {\n";
+        o << "  for (long long vb_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv; vb_ += 4 * stride) {\n";
         for (int s = 0; s < p.n_in; s++)
-            if (slot_type[s] >= 0) {
-                o << "    " << ctype(slot_type[s]) << " L" << s << "[4];\n";
-                o << "    " << vload(slot_type[s], "a.in[" + std::to_string(s) + "]", "vi", "L" + std::to_string(s)) << "\n";
-            }
+            if (slot_type[s] >= 0) o << "    " << ctype(slot_type[s]) << " L" << s << "[4][4];\n";
+        o << "    #pragma unroll\n    for (int u = 0; u < 4; u++) {\n";
+        o << "      const long long vi = vb_ + u * stride;\n";
+        o << "      if (vi < nv) {\n";
+        for (int s = 0; s < p.n_in; s++)
+            if (slot_type[s] >= 0)
+                o << "        " << vload(slot_type[s], "a.in[" + std::to_string(s) + "]", "vi", "L" + std::to_string(s) + "[u]") << "\n";
+        o << "      }\n";
+        o << "    }\n";
+        o << "    #pragma unroll\n    for (int u = 0; u < 4; u++) {\n";
+        o << "      const long long vi = vb_ + u * stride;\n";
+        o << "      if (vi >= nv) break;\n";
         for (int k = 0; k < p.n_out; k++)
-            if (out_type[k] >= 0) o << "    " << ctype(out_type[k]) << " O" << k << "[4];\n";
-        o << "    #pragma unroll\n    for (int e = 0; e < 4; e++) {\n";
+            if (out_type[k] >= 0) o << "      " << ctype(out_type[k]) << " O" << k << "[4];\n";
+        o << "      #pragma unroll\n      for (int e = 0; e < 4; e++) {\n";
         g.emit_body(
-            "      ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
+            "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[u][e]"; },
             [&](const OutV &ov) {
                 if (ov.scatter) return g.scat(ov, "(vi * 4 + e)");
                 return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
             },
             [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
-        o << "    }\n";
+        o << "      }\n";
         for (int k = 0; k < p.n_out; k++)
-            if (out_type[k] >= 0) o << "    " << vstore(out_type[k], "a.out[" + std::to_string(k) + "]", "vi", "O" + std::to_string(k)) << "\n";
+            if (out_type[k] >= 0) o << "      " << vstore(out_type[k], "a.out[" + std::to_string(k) + "]", "vi", "O" + std::to_string(k)) << "\n";
+        o << "    }\n";
         o << "  }\n";
     }
     o << "  for (long long i = tail0 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {\n";
