@@ -542,8 +542,17 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "                                    : (((long long)(unsigned)tl.w << 32) | (long long)(unsigned)tl.z);\n";
     // step = 64 groups: lane l owns groups b + 2l and b + 2l + 1 (8 gathers in flight per lane);
     // the next step's indices are prefetched while this step is reduced
+    const bool gpipe = spmv_gather_pipeline();
     o << "      int4 qa = (2 * lane < NG) ? __ldcs(CG + G0 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
     o << "      int4 qb = (2 * lane + 1 < NG) ? __ldcs(CG + G0 + 2 * lane + 1) : make_int4(-1, -1, -1, -1);\n";
+    if (gpipe) {
+        // gathers one step ahead: step b + 64's values are in flight while step b is reduced
+        o << "      int4 ca = qa, cb = qb;\n";
+        o << "      " << XT << " h0 = NBG_GV(ca.x), h1 = NBG_GV(ca.y), h2 = NBG_GV(ca.z), h3 = NBG_GV(ca.w);\n";
+        o << "      " << XT << " h4 = NBG_GV(cb.x), h5 = NBG_GV(cb.y), h6 = NBG_GV(cb.z), h7 = NBG_GV(cb.w);\n";
+        o << "      qa = (64 + 2 * lane < NG) ? __ldcs(CG + G0 + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "      qb = (65 + 2 * lane < NG) ? __ldcs(CG + G0 + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+    }
     o << "      int rs_[4];\n";
     o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
     o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
@@ -558,13 +567,29 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
     o << "      for (int b = 0; b < NG; b += 64) {\n";
     o << "        const long long P_ = 4 * (G0 + b + 2 * lane);\n";
-    o << "        const int4 ca = qa, cb = qb;\n";
-    o << "        const " << XT << " g0 = NBG_GV(ca.x), g1 = NBG_GV(ca.y), g2 = NBG_GV(ca.z), g3 = NBG_GV(ca.w);\n";
-    o << "        const " << XT << " g4 = NBG_GV(cb.x), g5 = NBG_GV(cb.y), g6 = NBG_GV(cb.z), g7 = NBG_GV(cb.w);\n";
-    o << "        if (b + 64 < NG) {\n";
-    o << "          qa = (b + 64 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-    o << "          qb = (b + 65 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-    o << "        }\n";
+    if (gpipe) {
+        o << "        const int4 ca_ = ca, cb_ = cb;\n";
+        o << "        const " << XT << " g0 = h0, g1 = h1, g2 = h2, g3 = h3, g4 = h4, g5 = h5, g6 = h6, g7 = h7;\n";
+        o << "        if (b + 64 < NG) {\n";
+        o << "          ca = qa; cb = qb;\n";
+        o << "          h0 = NBG_GV(ca.x); h1 = NBG_GV(ca.y); h2 = NBG_GV(ca.z); h3 = NBG_GV(ca.w);\n";
+        o << "          h4 = NBG_GV(cb.x); h5 = NBG_GV(cb.y); h6 = NBG_GV(cb.z); h7 = NBG_GV(cb.w);\n";
+        o << "          if (b + 128 < NG) {\n";
+        o << "            qa = (b + 128 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 128 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "            qb = (b + 129 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 129 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "          }\n";
+        o << "        }\n";
+        o << "        const int4 ca0 = ca_, cb0 = cb_;\n";
+        o << "#define ca ca0\n#define cb cb0\n";
+    } else {
+        o << "        const int4 ca = qa, cb = qb;\n";
+        o << "        const " << XT << " g0 = NBG_GV(ca.x), g1 = NBG_GV(ca.y), g2 = NBG_GV(ca.z), g3 = NBG_GV(ca.w);\n";
+        o << "        const " << XT << " g4 = NBG_GV(cb.x), g5 = NBG_GV(cb.y), g6 = NBG_GV(cb.z), g7 = NBG_GV(cb.w);\n";
+        o << "        if (b + 64 < NG) {\n";
+        o << "          qa = (b + 64 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "          qb = (b + 65 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "        }\n";
+    }
     // row starts of this step: two 32-bit words over positions [0, 64)
     o << "        unsigned m0_ = 0u, m1_ = 0u;\n";
     o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) {\n";
@@ -595,6 +620,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "        if (s1) s_racc[nstarted + before + (s0 ? 1 : 0) - 1] = s0 ? v0 : NBG_ADD(Sp, v0);   // row ending at 2 lane\n";
     o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
     o << "        nstarted += __popc(M0) + __popc(M1);\n";
+    if (gpipe) o << "#undef ca\n#undef cb\n";
     o << "      }\n";
     o << "      if (is_chunk) {\n";
     o << "        if (lane == 0) {\n";
@@ -944,12 +970,21 @@ int gen_tp2(Gen &g, const std::string &kname) {
 
 extern const char *NBG_PRELUDE_SRC;
 
+bool spmv_gather_pipeline() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NBG_SPMV_GPIPE");
+        v = (e && *e) ? (e[0] == '1') : 0;
+    }
+    return v == 1;
+}
+
 int spmv_threads() {
     static int v = 0;
     if (!v) {
         const char *e = getenv("NBG_SPMV_THREADS");
         v = (e && *e) ? atoi(e) : 768;
-        if (v != 256 && v != 512 && v != 768 && v != 1024) v = 768;
+        if (v != 256 && v != 512 && v != 640 && v != 768 && v != 1024) v = 768;
     }
     return v;
 }

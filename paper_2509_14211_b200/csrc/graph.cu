@@ -7,6 +7,7 @@
 //                            (DESIGN.md "K4 SpMV"), built once per matrix
 // Integer work only: results are bit-exact and deterministic (histogram atomics are integer).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
 #include <vector>
@@ -182,6 +183,51 @@ int bits_for(int64_t n) {
 }
 
 
+
+// ---- device-side task construction (gpu_build_spmv_plan)
+__global__ void k_short_groups(long long n, const long long *grp, long long *ngs) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (long long)gridDim.x * blockDim.x) {
+        const long long g = i < n ? grp[i + 1] - grp[i] : 0;
+        ngs[i] = (g > SP_LONG_G) ? 0 : g;
+    }
+}
+// fl[i]: a task starts at row i; fll[i]: row i is long
+__global__ void k_task_flags(long long n, const long long *grp, const long long *gs, unsigned char *fl, unsigned char *fll) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const bool lg = grp[i + 1] - grp[i] > SP_LONG_G;
+        const bool lgp = i > 0 && grp[i] - grp[i - 1] > SP_LONG_G;
+        const bool st = i == 0 || (i % SP_TASK_ROWS) == 0 || lg || lgp || (gs[i] / SP_TASK_G != gs[i - 1] / SP_TASK_G);
+        fl[i] = st ? 1 : 0;
+        fll[i] = lg ? 1 : 0;
+    }
+}
+// task k covers rows [starts[k], starts[k+1]) (n for the last); a long row start makes no task
+__global__ void k_task_records(long long nst, long long n, const int *starts, const long long *grp, int4 *rec, unsigned char *keep) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nst; k += (long long)gridDim.x * blockDim.x) {
+        const int rb = starts[k];
+        const long long re = k + 1 < nst ? starts[k + 1] : n;
+        const bool lg = grp[rb + 1] - grp[rb] > SP_LONG_G;
+        const long long g0 = grp[rb], ng = grp[re] - g0;
+        rec[k] = make_int4(rb, (int)((re - rb) | (ng << 8)), (int)(unsigned)(g0 & 0xffffffffll), (int)(unsigned)((unsigned long long)g0 >> 32));
+        keep[k] = lg ? 0 : 1;
+    }
+}
+__global__ void k_long_nchunks(long long L, const int *lrows, const long long *grp, long long *nch) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j <= L; j += (long long)gridDim.x * blockDim.x)
+        nch[j] = j < L ? (grp[lrows[j] + 1] - grp[lrows[j]] + SP_CHUNK_G - 1) / SP_CHUNK_G : 0;
+}
+__global__ void k_long_records(long long L, const int *lrows, const long long *grp, const long long *chs, int4 *longs, int4 *chunks) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < L; j += (long long)gridDim.x * blockDim.x) {
+        const int row = lrows[j];
+        const long long g0 = grp[row], g1 = grp[row + 1], c0 = chs[j], nc = chs[j + 1] - c0;
+        longs[j] = make_int4(row, (int)c0, (int)nc, 0);
+        for (long long q = 0; q < nc; q++) {
+            const long long gb = g0 + q * SP_CHUNK_G;
+            const long long cnt = (g1 - gb) < SP_CHUNK_G ? (g1 - gb) : SP_CHUNK_G;
+            chunks[c0 + q] = make_int4((int)j, (int)(unsigned)(gb & 0xffffffffll), (int)(unsigned)((unsigned long long)gb >> 32), (int)cnt);
+        }
+    }
+}
 // ---- two-phase plan kernels
 __global__ void k_rowid(long long nnz, long long n, const long long *rowptr, int *rowid) {
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
@@ -535,10 +581,9 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)ngb->d, (long long *)P->grp->d, (int64_t)(n + 1), c.stream);
     BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
     NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)ngb->d, (long long *)P->grp->d, (int64_t)(n + 1), c.stream));
-    std::vector<long long> gph((size_t)n + 1);
-    NBG_CUDA(cudaMemcpyAsync(gph.data(), P->grp->d, (size_t)(n + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    long long G = 0;
+    NBG_CUDA(cudaMemcpyAsync(&G, (const long long *)P->grp->d + n, 8, cudaMemcpyDeviceToHost, c.stream));
     NBG_CUDA(cudaStreamSynchronize(c.stream));
-    const long long G = gph[n];
     P->ngroups = G;
     P->cg = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * 4);
     NBG_CUDA(cudaMemsetAsync(P->cg->d, 0xff, (size_t)std::max<long long>(4 * G, 4) * 4, c.stream));
@@ -561,60 +606,75 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     NBG_CUDA(cudaGetLastError());
     c.stats.kernels_launched += 3;
 
-    // ---- warp tasks (host, once per matrix): runs of <= 128 consecutive non-long rows with
-    // <= SP_TASK_G groups; long rows (> SP_LONG_G groups) are cut into chunks of SP_CHUNK_G groups
-    std::vector<int> tiles, chunks, longs;
-    tiles.reserve((size_t)(n / 16 + 16));
-    long long nch_total = 0, L = 0;
-    for (long long i = 0; i < n;) {
-        long long gl = gph[i + 1] - gph[i];
-        if (gl > SP_LONG_G) {
-            long long nch = (gl + SP_CHUNK_G - 1) / SP_CHUNK_G;
-            longs.push_back((int)i);
-            longs.push_back((int)nch_total);
-            longs.push_back((int)nch);
-            longs.push_back(0);
-            for (long long q = 0; q < nch; q++) {
-                long long gb = gph[i] + q * SP_CHUNK_G;
-                chunks.push_back((int)L);
-                chunks.push_back((int)(unsigned)(gb & 0xffffffffll));
-                chunks.push_back((int)(unsigned)((unsigned long long)gb >> 32));
-                chunks.push_back((int)std::min<long long>(SP_CHUNK_G, gph[i + 1] - gb));
-            }
-            nch_total += nch;
-            L++;
-            i++;
-            continue;
+    // ---- warp tasks, built on the device (once per matrix): a task starts at every 128th row, at
+    // every crossing of a multiple of SP_TASK_G short-row groups and around every long row (> SP_LONG_G
+    // groups); long rows are cut into chunks of SP_CHUNK_G groups instead.  Tasks hold <= 128 rows and
+    // < 2 SP_TASK_G groups.
+    {
+        const int gr = grid_for(n + 1, c.num_sms);
+        BufP gshort = alloc_buf(c, (size_t)(n + 1) * 8), ngs = alloc_buf(c, (size_t)(n + 1) * 8);
+        k_short_groups<<<gr, 256, 0, c.stream>>>(n, (const long long *)P->grp->d, (long long *)ngs->d);
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)ngs->d, (long long *)gshort->d, (int64_t)(n + 1), c.stream);
+        if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+        NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)ngs->d, (long long *)gshort->d, (int64_t)(n + 1), c.stream));
+        BufP fl = alloc_buf(c, (size_t)std::max<long long>(n, 1)), fll = alloc_buf(c, (size_t)std::max<long long>(n, 1));
+        k_task_flags<<<gr, 256, 0, c.stream>>>(n, (const long long *)P->grp->d, (const long long *)gshort->d, (unsigned char *)fl->d,
+                                              (unsigned char *)fll->d);
+        BufP starts = alloc_buf(c, (size_t)std::max<long long>(n, 1) * 4), lrows = alloc_buf(c, (size_t)std::max<long long>(n, 1) * 4);
+        BufP cnts = alloc_buf(c, 16);
+        thrust::counting_iterator<int> it0(0);
+        cub::DeviceSelect::Flagged(nullptr, tb, it0, (const unsigned char *)fl->d, (int *)starts->d, (long long *)cnts->d, (int64_t)n, c.stream);
+        if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+        NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, it0, (const unsigned char *)fl->d, (int *)starts->d, (long long *)cnts->d,
+                                            (int64_t)n, c.stream));
+        cub::DeviceSelect::Flagged(nullptr, tb, it0, (const unsigned char *)fll->d, (int *)lrows->d, (long long *)cnts->d + 1, (int64_t)n,
+                                   c.stream);
+        if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+        NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, it0, (const unsigned char *)fll->d, (int *)lrows->d, (long long *)cnts->d + 1,
+                                            (int64_t)n, c.stream));
+        long long hc2[2] = {0, 0};
+        NBG_CUDA(cudaMemcpyAsync(hc2, cnts->d, 16, cudaMemcpyDeviceToHost, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+        const long long nst = hc2[0], L = hc2[1];
+        // task records (a start that is a long row makes no task: flagged by rows == 0, compacted below)
+        BufP rec = alloc_buf(c, (size_t)std::max<long long>(nst, 1) * 16), keep = alloc_buf(c, (size_t)std::max<long long>(nst, 1));
+        if (nst > 0)
+            k_task_records<<<grid_for(nst, c.num_sms), 256, 0, c.stream>>>(nst, n, (const int *)starts->d, (const long long *)P->grp->d,
+                                                                          (int4 *)rec->d, (unsigned char *)keep->d);
+        P->tiles = alloc_buf(c, (size_t)std::max<long long>(nst, 1) * 16);
+        cub::DeviceSelect::Flagged(nullptr, tb, (const int4 *)rec->d, (const unsigned char *)keep->d, (int4 *)P->tiles->d,
+                                   (long long *)cnts->d, (int64_t)nst, c.stream);
+        if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+        if (nst > 0)
+            NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, (const int4 *)rec->d, (const unsigned char *)keep->d, (int4 *)P->tiles->d,
+                                                (long long *)cnts->d, (int64_t)nst, c.stream));
+        long long nt = 0;
+        if (nst > 0) NBG_CUDA(cudaMemcpyAsync(&nt, cnts->d, 8, cudaMemcpyDeviceToHost, c.stream));
+        // long rows -> chunks
+        long long nch_total = 0;
+        if (L > 0) {
+            BufP nchb = alloc_buf(c, (size_t)(L + 1) * 8), chs = alloc_buf(c, (size_t)(L + 1) * 8);
+            k_long_nchunks<<<grid_for(L + 1, c.num_sms), 256, 0, c.stream>>>(L, (const int *)lrows->d, (const long long *)P->grp->d,
+                                                                             (long long *)nchb->d);
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, (long long *)nchb->d, (long long *)chs->d, (int64_t)(L + 1), c.stream);
+            if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+            NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)nchb->d, (long long *)chs->d, (int64_t)(L + 1), c.stream));
+            NBG_CUDA(cudaMemcpyAsync(&nch_total, (const long long *)chs->d + L, 8, cudaMemcpyDeviceToHost, c.stream));
+            NBG_CUDA(cudaStreamSynchronize(c.stream));
+            P->longs = alloc_buf(c, (size_t)L * 16);
+            P->chunks = alloc_buf(c, (size_t)nch_total * 16);
+            k_long_records<<<grid_for(L, c.num_sms), 256, 0, c.stream>>>(L, (const int *)lrows->d, (const long long *)P->grp->d,
+                                                                         (const long long *)chs->d, (int4 *)P->longs->d, (int4 *)P->chunks->d);
+            P->counters = alloc_buf(c, (size_t)L * 4);
+            NBG_CUDA(cudaMemsetAsync(P->counters->d, 0, (size_t)L * 4, c.stream));
+            P->partials = alloc_buf(c, (size_t)nch_total * 8);
         }
-        long long st = i, ngr = 0;
-        while (i < n && i - st < SP_TASK_ROWS) {
-            long long g2 = gph[i + 1] - gph[i];
-            if (g2 > SP_LONG_G) break;
-            if (i > st && ngr + g2 > SP_TASK_G) break;
-            ngr += g2;
-            i++;
-        }
-        // task record {row_begin, rows | groups << 8, first_group_lo, first_group_hi}
-        tiles.push_back((int)st);
-        tiles.push_back((int)((i - st) | (ngr << 8)));
-        tiles.push_back((int)(unsigned)(gph[st] & 0xffffffffll));
-        tiles.push_back((int)(unsigned)((unsigned long long)gph[st] >> 32));
-    }
-    P->ntiles = (int64_t)tiles.size() / 4;
-    P->nchunks = nch_total;
-    P->nlong = L;
-    if (!tiles.empty()) {
-        P->tiles = alloc_buf(c, tiles.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->tiles->d, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, c.stream));
-    }
-    if (!chunks.empty()) {
-        P->chunks = alloc_buf(c, chunks.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->chunks->d, chunks.data(), chunks.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        P->longs = alloc_buf(c, longs.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->longs->d, longs.data(), longs.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        P->counters = alloc_buf(c, (size_t)L * 4);
-        NBG_CUDA(cudaMemsetAsync(P->counters->d, 0, (size_t)L * 4, c.stream));
-        P->partials = alloc_buf(c, (size_t)nch_total * 8);
+        NBG_CUDA(cudaGetLastError());
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+        P->ntiles = nt;
+        P->nchunks = nch_total;
+        P->nlong = L;
+        c.stats.kernels_launched += 6;
     }
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     A.plan = std::move(P);
