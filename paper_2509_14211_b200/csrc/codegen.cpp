@@ -626,11 +626,12 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "        if (lane == 0) {\n";
     o << "          const " << ACC << " t = carry;\n";
     o << "          ((" << ACC << "*)a.partials)[it] = t;\n";
-    o << "          __threadfence();\n";
+    // release on the ticket (no L1 invalidation for the other chunks), acquire fence for the winner
     o << "          const int4 lr = ((const int4*)a.longs)[ch.x];\n";
-    o << "          const int tk = atomicAdd(&a.counters[ch.x], 1);\n";
+    o << "          int tk;\n";
+    o << "          asm volatile(\"atom.add.release.gpu.s32 %0, [%1], 1;\" : \"=r\"(tk) : \"l\"(&a.counters[ch.x]) : \"memory\");\n";
     o << "          if (tk == lr.z - 1) {\n";
-    o << "            __threadfence();\n";
+    o << "            asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n";
     o << "            " << ACC << " acc = " << IDENT << ";\n";
     o << "            for (int j = 0; j < lr.z; j++) { const " << ACC << " pj = *(volatile const " << ACC << "*)(((const " << ACC
       << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
@@ -856,11 +857,11 @@ std::string gen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long
     o << "        if (lane == 0) {\n";
     o << "          const int ci = a.chunks[t_];                              // global chunk index\n";
     o << "          ((" << k.ACC << "*)a.partials)[ci] = carry;\n";
-    o << "          __threadfence();\n";
     o << "          const int4 lr = ((const int4*)a.longs)[tl.x];\n";
-    o << "          const int tk = atomicAdd(&a.counters[tl.x], 1);\n";
+    o << "          int tk;\n";
+    o << "          asm volatile(\"atom.add.release.gpu.s32 %0, [%1], 1;\" : \"=r\"(tk) : \"l\"(&a.counters[tl.x]) : \"memory\");\n";
     o << "          if (tk == lr.z - 1) {\n";
-    o << "            __threadfence();\n";
+    o << "            asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n";
     o << "            " << k.ACC << " acc = " << k.IDENT << ";\n";
     o << "            for (int j = 0; j < lr.z; j++) { const " << k.ACC << " pj = *(volatile const " << k.ACC << "*)(((const " << k.ACC
       << "*)a.partials) + lr.y + j); acc = NBG_ADD(acc, pj); }\n";
