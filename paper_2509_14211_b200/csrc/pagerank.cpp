@@ -14,7 +14,9 @@
 //                    residual into the same pass -- the placement SPEC.md:474 leaves open).
 // Convergence (Fig. 6 l.284): sweep k+1 is recorded and launched BEFORE delta_k is read, so the
 // device never idles on the host's read-back; if delta_k <= tol the speculative sweep is dropped
-// (immutable handles keep r_k intact).  tol < 0 runs exactly itermax sweeps with no host sync.
+// (immutable handles keep r_k intact).  When the deltas' geometric decay predicts that sweep k is
+// the last, sweep k+1 is launched only after delta_k is read (no discarded sweep at the end).
+// tol < 0 runs exactly itermax sweeps with no host sync.
 #include <cmath>
 #include <vector>
 
@@ -111,11 +113,17 @@ extern "C" nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, 
     TRY(pr.sweep(t, &rk, &dk));
     std::vector<nbg_scalar> deltas;   // fixed-count mode: read after the loop
     int k = 1;
+    double dm1 = -1.0, dm2 = -1.0;    // delta_{k-1}, delta_{k-2} (convergence mode)
     for (;;) {
         nbg_vector rnext = nullptr;
         nbg_scalar dnext = nullptr;
         const bool more = k < p->itermax;
-        if (more) TRY(pr.sweep(rk, &rnext, &dnext));   // launched before delta_k is read
+        // speculate (launch sweep k+1 before delta_k is read) unless the geometric decay of the
+        // deltas predicts that sweep k is the last one: then the host waits for delta_k instead
+        // of paying a whole discarded sweep (results are identical either way)
+        const bool last_likely = conv && dm1 > 0.0 && dm2 > 0.0 && dm1 * (dm1 / dm2) <= 2.0 * p->tol;
+        const bool spec = more && !last_likely;
+        if (spec) TRY(pr.sweep(rk, &rnext, &dnext));   // launched before delta_k is read
         bool stop = !more;
         if (conv) {
             double v = 0.0;
@@ -124,6 +132,9 @@ extern "C" nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, 
             nbg_scalar_free(ctx, dk);
             dk = nullptr;
             if (!(v > p->tol)) stop = true;
+            dm2 = dm1;
+            dm1 = v;
+            if (!stop && more && !spec) TRY(pr.sweep(rk, &rnext, &dnext));   // mispredicted: launch now
         } else {
             deltas.push_back(dk);
             dk = nullptr;
