@@ -29,6 +29,31 @@
 
 namespace nbg {
 
+// host-side phase profile of the planner (NBG_PLAN_PROFILE=1: printed at exit)
+struct PlanProf {
+    double t[8] = {0};
+    long long n[8] = {0};
+    bool on = false;
+    PlanProf() { const char *e = getenv("NBG_PLAN_PROFILE"); on = e && e[0] == '1'; }
+    ~PlanProf() {
+        if (!on) return;
+        const char *nm[8] = {"purge+bind", "region", "hints", "keys", "run:sig+plan", "run:args+launch", "memo_insert", "total"};
+        for (int i = 0; i < 8; i++)
+            if (n[i]) fprintf(stderr, "[nbg plan] %-16s %10.2f us/call  (%lld calls)\n", nm[i], t[i] / 1e3 / n[i], n[i]);
+    }
+};
+static PlanProf g_prof;
+struct PTimer {
+    int k;
+    double t0;
+    explicit PTimer(int kk) : k(kk), t0(g_prof.on ? now_ns() : 0.0) {}
+    ~PTimer() {
+        if (!g_prof.on) return;
+        const double d = now_ns() - t0;
+        if (d < 500e3) { g_prof.t[k] += d; g_prof.n[k]++; }   // steady state only (no JIT compiles)
+    }
+};
+
 static std::string dbits(double v) {
     uint64_t b;
     memcpy(&b, &v, 8);
@@ -624,6 +649,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         if (T->ntasks > 0) launch(c, *kp1, a1, T->ncta, "spmv");
     }
 
+    double tsig0 = now_ns();
     std::string sig = p.signature();
     KernelP kern;
     auto it = c.plans.find(sig);
@@ -639,11 +665,15 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     } else {
         kern = it->second;
         c.stats.plan_hits++;
+        if (g_prof.on) { g_prof.t[4] += now_ns() - tsig0; g_prof.n[4]++; }
     }
     if (p.spmv && !p.tp) {
         if (args.hc > kern->hot) args.hc = kern->hot;
     }
-    if (items > 0 && n > 0) launch(c, *kern, args, items, p.tp ? "spmv_p2" : (p.spmv ? "spmv" : "ewise"));
+    {
+        PTimer pt(5);
+        if (items > 0 && n > 0) launch(c, *kern, args, items, p.tp ? "spmv_p2" : (p.spmv ? "spmv" : "ewise"));
+    }
 
     // provenance of the written buffers (for hints): base signature + output index
     // (set by the caller through B.prog before hints were appended)
@@ -676,10 +706,13 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
     for (int guard = 0; guard < 256; guard++) {
         Builder B(c);
         bool ok = true;
-        for (const NodeP &r : roots) {
-            if (r->mat) continue;
-            if (r->scalar) ok = B.add_reduction(r) && ok;
-            else ok = B.add_vector_output(r) && ok;
+        {
+            PTimer pt(1);
+            for (const NodeP &r : roots) {
+                if (r->mat) continue;
+                if (r->scalar) ok = B.add_reduction(r) && ok;
+                else ok = B.add_vector_output(r) && ok;
+            }
         }
         if (!B.prereq.empty()) {
             std::vector<NodeP> todo;
@@ -712,6 +745,7 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
         // speculative side outputs learned for this signature
         std::vector<HintOut> hint_outs;
         if (nb) {
+            PTimer pt_h(2);
             for (int o = 0; o < nbase; o++) {
                 auto h = c.hints.find({base_hash, o});
                 if (h == c.hints.end()) continue;
@@ -739,8 +773,11 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
         size_t nvis = B.visited.size();
         // structural keys of the base outputs (before they become leaves)
         std::vector<std::string> base_keys;
-        if (nb) {
-            for (int k = 0; k < nbase; k++) base_keys.push_back(node_key(B.out_nodes[k].get()));
+        {
+            PTimer pt(3);
+            if (nb) {
+                for (int k = 0; k < nbase; k++) base_keys.push_back(node_key(B.out_nodes[k].get()));
+            }
         }
         run_region(c, B, hint_outs, n);
         const uint64_t seq = ++c.launch_seq;
@@ -750,6 +787,7 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
             B.out_nodes[k]->buf->prod_seq = seq;
         }
         if (nb) {
+            PTimer pt_m(6);
             // memoise every result (common subexpressions across waits, e.g. dinv across runs)
             for (int k = 0; k < nbase; k++) memo_insert(c, base_keys[k], B.out_nodes[k]);
             // side outputs are keyed with R already materialised (the next sweep's lookup key)
@@ -777,7 +815,11 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
 
 void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
     double t0 = now_ns();
-    if (c.mode == NBG_NONBLOCKING) memo_purge(c);
+    PTimer pt_all(7);
+    {
+        PTimer pt_pb(0);
+        if (c.mode == NBG_NONBLOCKING) memo_purge(c);
+    }
     std::vector<NodeP> roots;
     std::unordered_set<const Node *> seen;
     for (const NodeP &r0 : roots_in) {
@@ -791,6 +833,7 @@ void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
     }
     if (roots.empty()) return;
     if (c.mode == NBG_NONBLOCKING) {
+        PTimer pt_b(0);
         std::vector<NodeP> left;
         for (const NodeP &r : roots)
             if (!memo_bind(c, r)) left.push_back(r);
