@@ -449,7 +449,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
     const int NF = (int)fplus.size();
     const int accw = (ACC == "double" || ACC == "long long") ? 8 : 4;
-    const int warp_bytes = 128 * 8;                           // row totals of the task
+    const int warp_bytes = 128 * 8 + 32 * 4;                  // row totals of the task + row-start bitmask
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
     const int NT = spmv_threads(), NW = NT / 32;
@@ -492,6 +492,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "  const unsigned s_base = (unsigned)__cvta_generic_to_shared(nbg_dyn);\n";
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
     o << "  " << ACC << "* s_racc = (" << ACC << "*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << ");   // [128] row totals\n";
+    o << "  unsigned* s_sbm = (unsigned*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << " + 1024);   // [32] row starts\n";
     if (NF)
         o << "  u64* s_x = (u64*)(nbg_dyn + " << hot_region << " + NBG_NW * " << warp_bytes << ");   // [warp][NF][11]\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
@@ -563,6 +564,12 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "        const int re = (lane == 31) ? nf : nx;                     // end (exclusive) of row lane + 32 r\n";
     o << "        nem_[r] = __ballot_sync(0xffffffffu, lane + 32 * r < R && re > rs_[r]);\n";
     o << "      }\n";
+    // the task's row starts as a bitmask over its groups (tasks hold < 1024 groups): one bit per
+    // non-empty row, set once per task instead of recomputed every step
+    o << "      s_sbm[lane] = 0u;\n";
+    o << "      __syncwarp();\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) if ((nem_[r] >> lane) & 1u) atomicOr(&s_sbm[rs_[r] >> 5], 1u << (rs_[r] & 31));\n";
+    o << "      __syncwarp();\n";
     o << "      " << ACC << " carry = " << IDENT << ";\n";
     o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
     o << "      for (int b = 0; b < NG; b += 64) {\n";
@@ -591,12 +598,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         o << "        }\n";
     }
     // row starts of this step: two 32-bit words over positions [0, 64)
-    o << "        unsigned m0_ = 0u, m1_ = 0u;\n";
-    o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) {\n";
-    o << "          const int os_ = rs_[r] - b;\n";
-    o << "          if (((nem_[r] >> lane) & 1u) && os_ >= 0 && os_ < 64) { if (os_ < 32) m0_ |= 1u << os_; else m1_ |= 1u << (os_ - 32); }\n";
-    o << "        }\n";
-    o << "        const unsigned M0 = __reduce_or_sync(0xffffffffu, m0_), M1 = __reduce_or_sync(0xffffffffu, m1_);\n";
+    o << "        const unsigned M0 = s_sbm[b >> 5], M1 = s_sbm[(b >> 5) + 1];\n";
     o << "        const unsigned Mw = lane < 16 ? M0 : M1;\n";
     o << "        const int sh_ = (2 * lane) & 31;\n";
     o << "        const bool s0 = (Mw >> sh_) & 1u, s1 = (Mw >> (sh_ + 1)) & 1u;\n";
@@ -608,11 +610,12 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     // scan value: the segment open at the lane's end; lane 0 continues the carried row
     o << "        " << ACC << " S = s1 ? v1 : NBG_ADD(v0, v1);\n";
     o << "        if (lane == 0 && !s0 && !s1) S = NBG_ADD(carry, S);\n";
-    o << "        bool F = s0 || s1 || lane == 0;\n";
+    // segmented inclusive scan bounded by the lane's segment start (highest head lane <= lane)
+    o << "        const unsigned H_ = __ballot_sync(0xffffffffu, s0 || s1) | 1u;\n";
+    o << "        const int seg_ = 31 - __clz(H_ & ((2u << lane) - 1u));\n";
     o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
     o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
-    o << "          const bool Fy = __shfl_up_sync(0xffffffffu, F, d);\n";
-    o << "          if (lane >= d && !F) { S = NBG_ADD(Sy, S); F = Fy; }\n";
+    o << "          if (lane - d >= seg_) S = NBG_ADD(Sy, S);\n";
     o << "        }\n";
     o << "        " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
     o << "        if (lane == 0) Sp = carry;                                   // running total before position 0\n";

@@ -200,3 +200,40 @@ extern "C" int mg_pipe(int V, int pred, const int* ci, long long nnz, const floa
 #undef GO
   return -1;
 }
+
+// texture-path gathers: cold columns through tex1Dfetch (TEX pipe) vs ld.global.nc (LSU pipe)
+template <int MODE>
+__global__ void __launch_bounds__(1024, 1) gtex(const int* __restrict__ ci, long long nnz, const float* __restrict__ x, cudaTextureObject_t tx, int hc, float* out) {
+  extern __shared__ float s_hot[];
+  for (int k = threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = x[k];
+  __syncthreads();
+  float acc = 0.f;
+  const long long nv = nnz >> 2;
+  for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (long long)gridDim.x * blockDim.x) {
+    const int4 c = __ldcs((const int4*)ci + v);
+    const int cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      float a;
+      if (cc[k] < hc) a = s_hot[cc[k]];
+      else if (MODE == 0) a = __ldg(x + cc[k]);
+      else if (MODE == 1) a = tex1Dfetch<float>(tx, cc[k]);
+      else a = (k & 1) ? tex1Dfetch<float>(tx, cc[k]) : __ldg(x + cc[k]);
+      acc += a;
+    }
+  }
+  out[(long long)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+extern "C" int mg_tex(int mode, const int* ci, long long nnz, const float* x, long long n, int hc, float* out) {
+  cudaResourceDesc rd = {}; rd.resType = cudaResourceTypeLinear; rd.res.linear.devPtr = (void*)x;
+  rd.res.linear.desc = cudaCreateChannelDesc<float>(); rd.res.linear.sizeInBytes = n * 4;
+  cudaTextureDesc td = {}; td.readMode = cudaReadModeElementType;
+  cudaTextureObject_t tx = 0; cudaCreateTextureObject(&tx, &rd, &td, nullptr);
+  int smem = hc * 4;
+#define GO(M_) if (mode == M_) { cudaFuncSetAttribute(gtex<M_>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); gtex<M_><<<148, 1024, smem>>>(ci, nnz, x, tx, hc, out); }
+  GO(0) GO(1) GO(2)
+#undef GO
+  int e = (int)cudaGetLastError();
+  cudaDeviceSynchronize(); cudaDestroyTextureObject(tx);
+  return e;
+}
