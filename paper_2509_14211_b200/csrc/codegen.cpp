@@ -480,7 +480,13 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
       << ")(" << IDENT << "))\n";
     // split form: gather (index clamped, always safe) now, turn into a term later
     o << "#define NBG_GV(C_) nbg_gxv(s_base, s_hot, X, ((C_) > 0 ? (C_) : 0), hc)\n";
-    o << "#define NBG_TV(C_, P_, V_) (((C_) >= 0) ? (" << ACC << ")nbg_mul(a, (P_), (V_)) : (" << ACC << ")(" << IDENT << "))\n";
+    // PLUS with SECOND (or TIMES on an iso matrix): a padding position contributes x = 0 (one select
+    // on the gathered value instead of one on the accumulator type)
+    const bool zero_pad = sp.add == NBG_PLUS && !sp.has_vals && (sp.mul == NBG_SECOND || sp.mul == NBG_TIMES);
+    if (zero_pad)
+        o << "#define NBG_TV(C_, P_, V_) ((" << ACC << ")nbg_mul(a, (P_), ((C_) >= 0) ? (V_) : (" << XT << ")0))\n";
+    else
+        o << "#define NBG_TV(C_, P_, V_) (((C_) >= 0) ? (" << ACC << ")nbg_mul(a, (P_), (V_)) : (" << ACC << ")(" << IDENT << "))\n";
     o << "__device__ __forceinline__ " << XT << " nbg_gxv(unsigned s_base, const " << XT << "* s_hot, const " << XT
       << "* X, int C_, int hc) { return " << gx << "; }\n";
     o << "#define NBG_NW " << NW << "\n";
