@@ -134,7 +134,10 @@ def run_ours(args, rank, world, local_rank):
     w = 4 if T == nbg.FP32 else 8
     kind = nbg.GRAPH_RMAT if cfg["graph"] == "rmat" else nbg.GRAPH_ER
     t0 = time.time()
-    A, deg = nbg.nbg_matrix_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed)
+    if args.mtx:       # NEXT-4: a real graph from a Matrix Market file (the paper's GAP-web run)
+        A, deg = nbg.nbg_matrix_from_mtx(ctx, args.mtx)
+    else:
+        A, deg = nbg.nbg_matrix_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed)
     n = nbg.nbg_matrix_nrows(ctx, A)
     nnz = nbg.nbg_matrix_nnz(ctx, A)
     cuts = None
@@ -245,7 +248,7 @@ def run_ours(args, rank, world, local_rank):
         # one sweep = one single-pass launch, or phase 1 + phase 2 of the two-phase SpMV
         avg_spmv_s = ((spmv_ms + p2_ms) / spmv_n) * 1e-3 if spmv_n else float("nan")
         achieved = b_ns / avg_spmv_s / 1e9
-        traffic = load_traffic(args.workload)
+        traffic = None if args.mtx else load_traffic(args.workload)
         value = nnz * sweeps_total / (ms * 1e-3) / 1e9
         result = {
             "metric": METRIC,
@@ -259,14 +262,15 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f32" if T == nbg.FP32 else "f64",
-            "data": "synthetic",
+            "data": f"file {os.path.basename(args.mtx)}" if args.mtx else "synthetic",
             "config": {
-                "workload": f"{args.workload}: {cfg['graph']} scale {cfg['scale']} ef {cfg['edge_factor']} seed {args.seed}",
+                "workload": workload_name(args, cfg),
                 "n": n, "nnz": nnz, "dangling": cfg["dangling"], "alpha": cfg["alpha"], "tol": tol,
                 "itermax": itermax, "sweeps_per_step": sweeps_total / args.steps,
                 "parallelism": f"rows{world}" if world > 1 else "single",
-                "l2": "no flush: colidx stream (%.0f MB) > L2 (126 MB) each sweep; the gathered vector "
-                      "stays L2-resident by design" % (4 * nnz / 1e6),
+                "l2": ("no flush: colidx stream (%.0f MB) > L2 (126 MB) each sweep; the gathered vector "
+                       "stays L2-resident by design" if 4 * nnz > 126e6 else
+                       "no flush; colidx (%.0f MB) fits in L2 (small file graph)") % (4 * nnz / 1e6),
                 "setup_s": round(setup_s, 3),
             },
             "roofline": {
@@ -381,8 +385,17 @@ def run_chain(args):
 
 # ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
 
-def oracle_graph(cfg, seed):
+def workload_name(args, cfg):
+    if args.mtx:
+        return f"mtx {os.path.basename(args.mtx)} (c4 solver settings)"
+    return f"{args.workload}: {cfg['graph']} scale {cfg['scale']} ef {cfg['edge_factor']} seed {args.seed}"
+
+
+def oracle_graph(cfg, seed, mtx=None):
     import oracle
+    if mtx:
+        n, src, dst = oracle.read_mtx(mtx)
+        return oracle.build_csr(n, src, dst)
     f = oracle.rmat_edges if cfg["graph"] == "rmat" else oracle.er_edges
     src, dst = f(cfg["scale"], cfg["edge_factor"], seed)
     rp, ci, deg = oracle.build_csr(1 << cfg["scale"], src, dst)
@@ -402,7 +415,7 @@ def oracle_sample(rp, ci, deg, cfg, sweeps):
 
 def cpu_baseline(args):
     cfg = graph_params(args.workload)
-    rp, ci, deg = oracle_graph(cfg, args.seed)
+    rp, ci, deg = oracle_graph(cfg, args.seed, args.mtx)
     nnz = int(ci.shape[0])
     sweeps = max(1, min(cfg["itermax"], int(args.cpu_sweeps)))
     t = oracle_sample(rp, ci, deg, cfg, sweeps)
@@ -415,7 +428,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     cfg = graph_params(args.workload)
-    rp, ci, deg = oracle_graph(cfg, args.seed)
+    rp, ci, deg = oracle_graph(cfg, args.seed, args.mtx)
     nnz = int(ci.shape[0])
     per = max(1, int(args.ref_sweeps))
     for _ in range(args.warmup):
@@ -428,9 +441,8 @@ def run_reference(args, rank, world):
         "metric": METRIC, "value": round(value, 5), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(tot / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if cfg["dtype"] == "fp32" else "f64",
-        "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.workload}: {cfg['graph']} scale {cfg['scale']} ef {cfg['edge_factor']} "
-                               f"seed {args.seed}", "n": int(rp.shape[0] - 1), "nnz": nnz,
+        "data": f"file {os.path.basename(args.mtx)}" if args.mtx else "synthetic", "impl": "reference",
+        "config": {"workload": workload_name(args, cfg), "n": int(rp.shape[0] - 1), "nnz": nnz,
                    "step": f"{per} fixed sweeps of the CPU oracle (bounded sample of the workload)"},
         "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
                          "sample": f"{per} sweeps x {args.steps} steps, single-threaded C oracle"},
@@ -451,6 +463,7 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mtx", default=None, help="Matrix Market file instead of the synthetic graph (c4 settings)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     rank = int(os.environ.get("RANK", 0))
@@ -459,6 +472,8 @@ def main():
     if world != args.gpus and world == 1 and args.gpus > 1:
         print(json.dumps({"error": "--gpus N>1 must be launched with torchrun"}))
         sys.exit(2)
+    if args.mtx:
+        args.workload = "c4"
     if args.workload == "c2":
         res = run_chain(args) if args.impl == "ours" and rank == 0 else None
         if rank == 0 and res is not None:

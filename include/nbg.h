@@ -175,6 +175,18 @@ nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64
 nbg_status nbg_matrix_from_edges(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, int64_t n, int64_t m,
                                  const int32_t *src, const int32_t *dst, int space);
 
+/* Matrix Market ingestion (the paper's experiment reads GAP-web.mtx).
+ * `path` names a coordinate-format file ("%%MatrixMarket matrix coordinate <field> <symmetry>",
+ * field pattern | real | integer, symmetry general | symmetric; '%' comment lines; a size line
+ * "M N NNZ"; NNZ lines "i j [value]" with 1-based indices).  Entry (i, j) is the edge i -> j
+ * (row = source, GAP/LAGraph convention); a symmetric file contributes both directions; values are
+ * ignored (the PageRank matrix is a pattern).  The graph has n = max(M, N)
+ * vertices and goes through nbg_matrix_from_edges (self-loops dropped, duplicates removed).
+ * Errors: NBG_INVALID_VALUE for an unreadable file or a malformed / unsupported header or line
+ * (array format, complex or hermitian fields), NBG_INDEX_OUT_OF_BOUNDS for an index outside
+ * [1, M] x [1, N]. */
+nbg_status nbg_matrix_from_mtx(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, const char *path);
+
 /* Synthetic graphs (input recipe of DESIGN.md; BASELINE configs 1,3,4,5).
  * kind NBG_GRAPH_RMAT: n = 2^scale, m = edge_factor * n, (a,b,c,d) = (0.57,0.19,0.19,0.05),
  *   edge e level l draws u = SplitMix64(seed, e*64 + l) >> 11 (reading Q9).

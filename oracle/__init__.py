@@ -100,6 +100,44 @@ def er_edges(logn: int, mean_deg: int, seed: int):
     return src, dst
 
 
+def read_mtx(path):
+    """Matrix Market coordinate file -> (n, src, dst) edge list, written from the format's own
+    definition (NIST Matrix Market exchange format): header "%%MatrixMarket matrix coordinate
+    <field> <symmetry>", '%' comments, size line "M N NNZ", NNZ 1-based lines "i j [value]".
+    Entry (i, j) is the edge i -> j; symmetric files contribute (j, i) too for i != j; values are
+    ignored.  n = max(M, N).  Plain Python line by line (test infrastructure; small files)."""
+    with open(path) as f:
+        head = f.readline().split()
+        if len(head) < 5 or head[0] != "%%MatrixMarket" or head[1].lower() != "matrix" or head[2].lower() != "coordinate":
+            raise ValueError("not a coordinate Matrix Market file")
+        field, sym = head[3].lower(), head[4].lower()
+        if field not in ("pattern", "real", "integer") or sym not in ("general", "symmetric"):
+            raise ValueError("unsupported field / symmetry")
+        line = f.readline()
+        while line.strip() == "" or line.lstrip().startswith("%"):
+            line = f.readline()
+        M, N, NZ = (int(v) for v in line.split()[:3])
+        src, dst = [], []
+        got = 0
+        while got < NZ:
+            line = f.readline()
+            if line == "":
+                raise ValueError("file ends early")
+            t = line.split()
+            if not t or t[0].startswith("%"):
+                continue
+            i, j = int(t[0]), int(t[1])
+            if not (1 <= i <= M and 1 <= j <= N):
+                raise IndexError("index out of range")
+            src.append(i - 1)
+            dst.append(j - 1)
+            if sym == "symmetric" and i != j:
+                src.append(j - 1)
+                dst.append(i - 1)
+            got += 1
+    return max(M, N), np.array(src, np.int32), np.array(dst, np.int32)
+
+
 def build_csr(n: int, src: np.ndarray, dst: np.ndarray):
     """-> (rowptr int64[n+1], colidx int32[nnz], deg int32[n]) of AT (edge u->v at AT[v,u])."""
     src = np.ascontiguousarray(src, np.int32)

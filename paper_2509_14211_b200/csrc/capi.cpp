@@ -9,6 +9,10 @@
 #include <cstdio>
 #include <new>
 
+#include <cstring>
+#include <vector>
+#include <string>
+#include <cctype>
 #include "nbg_internal.hpp"
 
 using namespace nbg;
@@ -358,6 +362,108 @@ nbg_status nbg_matrix_from_edges(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, 
     }
     BufP degb;
     MatP M = gpu_build_csr(*ctx, n, m, s, d, &degb);
+    *AT = new nbg_matrix_s{ctx, M};
+    if (deg) *deg = deg_vector(ctx, n, degb);
+    API_END(ctx)
+}
+
+// ---- Matrix Market (coordinate) reader: a buffered hand-rolled parser (fscanf is too slow for
+// billion-entry files); produces the edge list for gpu_build_csr
+static bool mtx_read(const char *path, int64_t *n_out, std::vector<int32_t> &src, std::vector<int32_t> &dst, std::string &err) {
+    FILE *f = fopen(path, "rb");
+    if (!f) { err = std::string("cannot open ") + path; return false; }
+    std::vector<char> buf(1 << 22);
+    size_t len = 0, pos = 0;
+    bool eof = false;
+    auto fill = [&]() {
+        if (pos > 0) { memmove(buf.data(), buf.data() + pos, len - pos); len -= pos; pos = 0; }
+        if (!eof) {
+            size_t r = fread(buf.data() + len, 1, buf.size() - len, f);
+            if (r == 0) eof = true;
+            len += r;
+        }
+    };
+    auto getline = [&](std::string &line) -> bool {
+        for (;;) {
+            for (size_t k = pos; k < len; k++)
+                if (buf[k] == '\n') { line.assign(buf.data() + pos, k - pos); pos = k + 1; return true; }
+            if (eof) {
+                if (pos < len) { line.assign(buf.data() + pos, len - pos); pos = len; return true; }
+                return false;
+            }
+            if (len - pos == buf.size()) buf.resize(buf.size() * 2);
+            fill();
+        }
+    };
+    std::string line;
+    bool ok = getline(line);
+    if (!ok || line.compare(0, 14, "%%MatrixMarket") != 0) { fclose(f); err = "missing %%MatrixMarket header"; return false; }
+    std::string lower = line;
+    for (char &ch : lower) ch = (char)tolower(ch);
+    if (lower.find(" matrix ") == std::string::npos || lower.find("coordinate") == std::string::npos) { fclose(f); err = "only 'matrix coordinate' files are supported"; return false; }
+    if (lower.find("complex") != std::string::npos || lower.find("hermitian") != std::string::npos || lower.find("skew") != std::string::npos) {
+        fclose(f); err = "complex / hermitian / skew-symmetric files are not supported"; return false;
+    }
+    const bool pattern = lower.find("pattern") != std::string::npos;
+    const bool symmetric = lower.find("symmetric") != std::string::npos;
+    long long M = -1, N = -1, NZ = -1;
+    while (getline(line)) {
+        size_t k = line.find_first_not_of(" \t\r");
+        if (k == std::string::npos || line[k] == '%') continue;
+        if (sscanf(line.c_str(), "%lld %lld %lld", &M, &N, &NZ) != 3) { fclose(f); err = "malformed size line"; return false; }
+        break;
+    }
+    if (M < 0 || N < 0 || NZ < 0) { fclose(f); err = "missing size line"; return false; }
+    const int64_t n = std::max(M, N);
+    if (n > MAXDIM) { fclose(f); err = "dimension exceeds int32 indices"; return false; }
+    src.reserve((size_t)NZ * (symmetric ? 2 : 1));
+    dst.reserve((size_t)NZ * (symmetric ? 2 : 1));
+    long long got = 0;
+    while (got < NZ && getline(line)) {
+        const char *c = line.c_str();
+        while (*c == ' ' || *c == '\t') c++;
+        if (*c == '\0' || *c == '\r' || *c == '%') continue;
+        char *e1 = nullptr, *e2 = nullptr;
+        long long i = strtoll(c, &e1, 10);
+        long long j = strtoll(e1, &e2, 10);
+        if (e1 == c || e2 == e1) { fclose(f); err = "malformed entry line " + std::to_string(got + 1); return false; }
+        if (!pattern) {
+            char *e3 = nullptr;
+            (void)strtod(e2, &e3);
+            if (e3 == e2) { fclose(f); err = "missing value on entry line " + std::to_string(got + 1); return false; }
+        }
+        if (i < 1 || i > M || j < 1 || j > N) { fclose(f); err = "index out of range on entry line " + std::to_string(got + 1); return false; }
+        src.push_back((int32_t)(i - 1));
+        dst.push_back((int32_t)(j - 1));
+        if (symmetric && i != j) { src.push_back((int32_t)(j - 1)); dst.push_back((int32_t)(i - 1)); }
+        got++;
+    }
+    fclose(f);
+    if (got != NZ) { err = "file ends after " + std::to_string(got) + " of " + std::to_string(NZ) + " entries"; return false; }
+    *n_out = n;
+    return true;
+}
+
+nbg_status nbg_matrix_from_mtx(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, const char *path) {
+    API_BEGIN
+    check_ctx(ctx);
+    CHECK(AT && path, NBG_NULL_POINTER, "nbg_matrix_from_mtx: NULL argument");
+    std::vector<int32_t> src, dst;
+    int64_t n = 0;
+    std::string err;
+    if (!mtx_read(path, &n, src, dst, err)) {
+        const bool oob = err.find("out of range") != std::string::npos;
+        fail(oob ? NBG_INDEX_OUT_OF_BOUNDS : NBG_INVALID_VALUE, "nbg_matrix_from_mtx: " + err);
+    }
+    const int64_t m = (int64_t)src.size();
+    BufP ds, dd;
+    if (m > 0) {
+        ds = upload(*ctx, src.data(), (size_t)m * 4, NBG_HOST, NBG_COPY);
+        dd = upload(*ctx, dst.data(), (size_t)m * 4, NBG_HOST, NBG_COPY);
+    }
+    BufP degb;
+    MatP M = gpu_build_csr(*ctx, n, m, m ? (const int32_t *)ds->d : nullptr, m ? (const int32_t *)dd->d : nullptr, &degb);
+    NBG_CUDA(cudaStreamSynchronize(ctx->stream));     // the host edge vectors go out of scope
     *AT = new nbg_matrix_s{ctx, M};
     if (deg) *deg = deg_vector(ctx, n, degb);
     API_END(ctx)

@@ -98,6 +98,7 @@ SIGNATURES = {
     "nbg_get_timing": [vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i64)],
     "nbg_matrix_from_csr": [vp, pvp, i64, i64, i64, vp, vp, vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_int],
     "nbg_matrix_from_edges": [vp, pvp, pvp, i64, i64, vp, vp, ctypes.c_int],
+    "nbg_matrix_from_mtx": [vp, pvp, pvp, ctypes.c_char_p],
     "nbg_graph_edges": [vp, ctypes.POINTER(nbg_graphgen), vp, vp, ctypes.c_int],
     "nbg_matrix_from_generator": [vp, pvp, pvp, ctypes.POINTER(nbg_graphgen)],
     "nbg_matrix_nrows": [vp, vp, ctypes.POINTER(i64)],
@@ -228,6 +229,13 @@ def nbg_matrix_from_edges(ctx, n, src, dst):
     d, _ = _ptr(dst)
     A, deg = ctypes.c_void_p(), ctypes.c_void_p()
     _call(ctx, "nbg_matrix_from_edges", ctx, ctypes.byref(A), ctypes.byref(deg), n, int(src.shape[0]), s, d, sp)
+    return A, deg
+
+
+def nbg_matrix_from_mtx(ctx, path):
+    """Matrix Market coordinate file -> (AT, out-degree) (include/nbg.h nbg_matrix_from_mtx)."""
+    A, deg = ctypes.c_void_p(), ctypes.c_void_p()
+    _call(ctx, "nbg_matrix_from_mtx", ctx, ctypes.byref(A), ctypes.byref(deg), str(path).encode())
     return A, deg
 
 
