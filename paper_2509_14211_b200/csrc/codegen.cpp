@@ -550,6 +550,24 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     // step = 64 groups: lane l owns groups b + 2l and b + 2l + 1 (8 gathers in flight per lane);
     // the next step's indices are prefetched while this step is reduced
     const bool gpipe = spmv_gather_pipeline();
+    // the epilogue's per-row inputs (and scatter maps) are prefetched into L1 when the task starts,
+    // so the epilogue does not wait a global round trip after the step loop (NBG_SPMV_PF=0: off)
+    if (spmv_epilogue_prefetch()) {
+        std::vector<int> slot_sz(p.n_in, 0);
+        for (const Ins &in : p.ins)
+            if (in.k == Ins::LD_VEC) slot_sz[in.slot] = (int)type_size(in.t);
+        std::ostringstream pf;
+        for (int s = 0; s < p.n_in; s++)
+            if (slot_sz[s] > 0)
+                pf << " asm volatile(\"prefetch.global.L1 [%0];\" :: \"l\"((const char*)a.in[" << s << "] + " << slot_sz[s] << " * i));";
+        for (const OutV &ov : p.outs)
+            if (ov.scatter) pf << " asm volatile(\"prefetch.global.L1 [%0];\" :: \"l\"(a.oscat[" << ov.out << "] + i));";
+        if (!pf.str().empty()) {
+            o << "      if (!is_chunk) {\n";
+            o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) { const long long i = (long long)tl.x + lane + 32 * r; if (lane + 32 * r < R) {" << pf.str() << " } }\n";
+            o << "      }\n";
+        }
+    }
     o << "      int4 qa = (2 * lane < NG) ? __ldcs(CG + G0 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
     o << "      int4 qb = (2 * lane + 1 < NG) ? __ldcs(CG + G0 + 2 * lane + 1) : make_int4(-1, -1, -1, -1);\n";
     if (gpipe) {
@@ -979,6 +997,15 @@ int gen_tp2(Gen &g, const std::string &kname) {
 }  // namespace
 
 extern const char *NBG_PRELUDE_SRC;
+
+bool spmv_epilogue_prefetch() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NBG_SPMV_PF");
+        v = (e && *e) ? (e[0] == '1') : 1;
+    }
+    return v == 1;
+}
 
 bool spmv_gather_pipeline() {
     static int v = -1;

@@ -377,6 +377,7 @@ void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
 
 // codegen / jit
 bool spmv_gather_pipeline();   // SpMV gathers one step ahead (NBG_SPMV_GPIPE=1)
+bool spmv_epilogue_prefetch();  // SpMV prefetches the epilogue's row inputs at task start (NBG_SPMV_PF, default on)
 int spmv_threads();   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);

@@ -1,0 +1,246 @@
+// Micro-benchmark: hybrid two-phase SpMV (v9: v8 + row-major piece slots, contiguous K_B).
+// K_A: one launch over "ranges" of work; a dense range = 2048 u16 entries of one column block
+//   (block slice of x in shared memory, loaded by a TMA bulk copy), a cold range = 1024 int32 gather
+//   indices (x gathered from L2).  Lane l of a warp owns a contiguous run (64 u16 / 32 int32) whose
+//   last entry always carries a flag, so runs are independent: every flag closes a piece whose
+//   ordinal comes from lbase (per lane run) -- no cross-lane work.  Pieces are staged per warp in
+//   shared memory and written coalesced.
+// K_B: row i = sum of its pieces P[list[rp3[i] .. rp3[i+1])].
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef STG_CAP
+#define STG_CAP 512
+#endif
+
+__device__ __forceinline__ void mbar_init(unsigned a, int cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect(unsigned a, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void *src, unsigned bytes, unsigned mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned ph) {
+    asm volatile(
+        "{ .reg .pred p; W_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W_%=; }" ::"r"(a), "r"(ph)
+        : "memory");
+}
+
+
+// one lane run: 4 uint4 = 32 u16 entries (dense, shared-memory gathers) or 16 int32 terms (cold, L2 gathers)
+template <bool DENSE, bool STAGED>
+__device__ __forceinline__ void run4(const uint4 (&w)[4], unsigned sb, const float *__restrict__ X, int o, float *P,
+                                     const int *__restrict__ slot, unsigned sdst) {
+    float r = 0.f;
+    if (DENSE) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const unsigned u[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+            for (int h = 0; h < 8; h++) {
+                const unsigned a = (h & 1) ? ((u[h >> 1] >> 14) & 0x1fffcu) : ((u[h >> 1] << 2) & 0x1fffcu);
+                float v;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(sb + a));
+                r += v;
+                const bool f = (u[h >> 1] >> (16 * (h & 1) + 15)) & 1u;
+                if (STAGED) { if (f) asm volatile("st.shared.f32 [%0], %1;" ::"r"(sdst + 4u * (unsigned)o), "f"(r) : "memory"); }
+                else { if (f) P[slot[o]] = r; }
+                o += f ? 1 : 0;
+                r = f ? 0.f : r;
+            }
+        }
+    } else {
+        float g[16];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const unsigned u[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+            for (int h = 0; h < 4; h++) g[4 * k + h] = __ldg(X + (u[h] & 0x7fffffffu));
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const unsigned u[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                r += g[4 * k + h];
+                const bool f = u[h] >> 31;
+                if (STAGED) { if (f) asm volatile("st.shared.f32 [%0], %1;" ::"r"(sdst + 4u * (unsigned)o), "f"(r) : "memory"); }
+                else { if (f) P[slot[o]] = r; }
+                o += f ? 1 : 0;
+                r = f ? 0.f : r;
+            }
+        }
+    }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) k_a(const uint4 *__restrict__ E, const uint4 *__restrict__ C,
+                                              const float *__restrict__ X, const int *__restrict__ rblk,
+                                              const int *__restrict__ bnext, const int *__restrict__ cta,
+                                              const int *__restrict__ lbase, float *__restrict__ P, int S,
+                                              long long ncols, int ndr, unsigned long long *tim,
+                                              const int *__restrict__ ccta, const int *__restrict__ slot) {
+    extern __shared__ __align__(128) unsigned char dyn[];
+    float *xs = (float *)dyn;
+    float *stg = (float *)(dyn + 32768 * 4);
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ int s_ctr;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(xs);
+    const unsigned sstg = (unsigned)__cvta_generic_to_shared(stg + warp * STG_CAP);
+    const unsigned smb = (unsigned)__cvta_generic_to_shared(&mbar);
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    if (threadIdx.x == 0) {
+        mbar_init(smb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        xs[32767] = 0.f;
+    }
+    __syncthreads();
+    unsigned phase = 0;
+    int q1 = cta[blockIdx.x + 1];
+    int q = cta[blockIdx.x];
+    bool cold_done = false;
+    while (true) {
+        if (q >= q1) {
+            if (cold_done) break;
+            cold_done = true;
+            q = ndr + ccta[blockIdx.x];
+            q1 = ndr + ccta[blockIdx.x + 1];
+            if (q >= q1) break;
+        }
+        const bool dense = q < ndr;
+        const int qe = dense ? min(q1, bnext[q]) : q1;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_ctr = q;
+            if (dense) {
+                const long long c0 = (long long)rblk[q] * S;
+                const int cn = (int)((ncols - c0) < S ? (ncols - c0) : S);
+                const unsigned bytes = (unsigned)(cn * 4 + 15) & ~15u;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect(smb, bytes);
+                const unsigned CH = 32768;
+                for (unsigned off = 0; off < bytes; off += CH)
+                    bulk_g2s(sb + off, (const char *)(X + c0) + off, bytes - off < CH ? bytes - off : CH, smb);
+            }
+        }
+        __syncthreads();
+        const uint4 *base = dense ? E : (C - (long long)ndr * 128);
+        int t = 0;
+        if (lane == 0) t = atomicAdd(&s_ctr, 1);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        uint4 w[4];
+        int o = 0, oe = 0;
+        if (t < qe) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) w[k] = __ldcs(base + (long long)t * 128 + 32 * k + lane);
+            o = __ldcs(lbase + (long long)t * 32 + lane);
+            oe = __ldcs(lbase + (long long)t * 32 + 32);
+        }
+        if (dense) {
+            mbar_wait(smb, phase);
+            phase ^= 1u;
+        }
+        while (t < qe) {
+            int tn = 0;
+            if (lane == 0) tn = atomicAdd(&s_ctr, 1);
+            tn = __shfl_sync(0xffffffffu, tn, 0);
+            uint4 wn[4];
+            int on = 0, oen = 0;
+            if (tn < qe) {
+#pragma unroll
+                for (int k = 0; k < 4; k++) wn[k] = __ldcs(base + (long long)tn * 128 + 32 * k + lane);
+                on = __ldcs(lbase + (long long)tn * 32 + lane);
+                oen = __ldcs(lbase + (long long)tn * 32 + 32);
+            }
+            const int ob = __shfl_sync(0xffffffffu, o, 0);
+            const int cnt = oe - ob;
+            if (cnt <= STG_CAP) {
+                if (dense) run4<true, true>(w, sb, X, o - ob, P, slot, sstg);
+                else run4<false, true>(w, sb, X, o - ob, P, slot, sstg);
+                __syncwarp();
+                for (int j = lane; j < cnt; j += 32) P[slot[ob + j]] = stg[warp * STG_CAP + j];
+                __syncwarp();
+            } else {
+                if (dense) run4<true, false>(w, sb, X, o, P, slot, 0);
+                else run4<false, false>(w, sb, X, o, P, slot, 0);
+            }
+            t = tn;
+#pragma unroll
+            for (int k = 0; k < 4; k++) w[k] = wn[k];
+            o = on; oe = oen;
+        }
+        q = qe;
+    }
+    if (tim) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t2;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t2));
+            tim[4 * blockIdx.x] = t_start;
+            tim[4 * blockIdx.x + 1] = t2;
+            tim[4 * blockIdx.x + 2] = 0;
+            tim[4 * blockIdx.x + 3] = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_b(long long n, const int *__restrict__ rs, const int *__restrict__ lrows, int nlong,
+                    const float *__restrict__ P, float *__restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long k = gw; k < nlong; k += nw) {          // long rows: one warp each, 4 chunks in flight
+        const int i = lrows[k];
+        const int s0 = rs[i], s1 = rs[i + 1];
+        double acc = 0;
+        for (int s = s0 + lane; s < s1; s += 128) {
+            float v0 = P[s], v1 = s + 32 < s1 ? P[s + 32] : 0.f, v2 = s + 64 < s1 ? P[s + 64] : 0.f, v3 = s + 96 < s1 ? P[s + 96] : 0.f;
+            acc += (double)v0; acc += (double)v1; acc += (double)v2; acc += (double)v3;
+        }
+        for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+        if (lane == 0) y[i] = (float)acc;
+    }
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int s0 = rs[i], s1 = rs[i + 1];
+        if (s1 - s0 > 64) continue;
+        double acc = 0;
+        int s = s0;
+        for (; s + 4 <= s1; s += 4) { const float a = P[s], b = P[s + 1], c = P[s + 2], d = P[s + 3]; acc += a; acc += b; acc += c; acc += d; }
+        for (; s < s1; s++) acc += (double)P[s];
+        y[i] = (float)acc;
+    }
+}
+
+extern "C" int tp8_a(int reps, int nt, const void *E, const void *C, const void *X, const void *rblk, const void *bnext,
+                     const void *cta, int ncta, const void *lbase, void *P, int S, long long ncols, int ndr, void *tim,
+                     const void *ccta, const void *slot) {
+    static bool init = false;
+    const int smem768 = 32768 * 4 + 24 * STG_CAP * 4, smem512 = 32768 * 4 + 16 * STG_CAP * 4;
+    if (!init) {
+        init = true;
+        cudaFuncSetAttribute(k_a<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem768);
+        cudaFuncSetAttribute(k_a<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem512);
+    }
+    for (int r = 0; r < reps; r++) {
+        if (nt == 768)
+            k_a<768><<<ncta, 768, smem768>>>((const uint4 *)E, (const uint4 *)C, (const float *)X, (const int *)rblk,
+                                              (const int *)bnext, (const int *)cta, (const int *)lbase, (float *)P, S,
+                                              ncols, ndr, (unsigned long long *)tim, (const int *)ccta, (const int *)slot);
+        else
+            k_a<512><<<ncta, 512, smem512>>>((const uint4 *)E, (const uint4 *)C, (const float *)X, (const int *)rblk,
+                                              (const int *)bnext, (const int *)cta, (const int *)lbase, (float *)P, S,
+                                              ncols, ndr, (unsigned long long *)tim, (const int *)ccta, (const int *)slot);
+    }
+    return (int)cudaGetLastError();
+}
+
+extern "C" int tp8_b(int reps, long long n, const void *rs, const void *lrows, int nlong, const void *P, void *y) {
+    for (int r = 0; r < reps; r++)
+        k_b<<<148 * 8, 256>>>(n, (const int *)rs, (const int *)lrows, nlong, (const float *)P, (float *)y);
+    return (int)cudaGetLastError();
+}
