@@ -146,6 +146,8 @@ typedef struct {
     uint64_t bytes_materialized;    /* bytes of vector buffers written by kernels             */
     uint64_t host_plan_ns;          /* host time spent planning (signature..launch)           */
     double jit_ms;                  /* host time spent in NVRTC                               */
+    uint64_t structured_regions;    /* regions over sparse / bitset vectors (NEXT-3)          */
+    uint64_t structured_index_loops;/* ... of those, run over a sparse index list (estimator)  */
 } nbg_stats;
 
 nbg_status nbg_get_stats(nbg_ctx *ctx, nbg_stats *out);
@@ -226,12 +228,14 @@ nbg_status nbg_vector_from_dense(nbg_ctx *ctx, nbg_vector *v, int type, int64_t 
                                  int space, int ownership);
 
 /* Materialise v (forces wait) and copy its n values (of v's type) to out in `space`.
- * Errors: NBG_INVALID_OBJECT if v is empty.  Synchronises. */
+ * Errors: NBG_INVALID_OBJECT if v is empty, sparse or bitset (not every entry present; use
+ * nbg_vector_export_sparse).  Synchronises. */
 nbg_status nbg_vector_export_dense(nbg_ctx *ctx, nbg_vector v, void *out, int space);
 
 nbg_status nbg_vector_size(nbg_ctx *ctx, nbg_vector v, int64_t *n);
 nbg_status nbg_vector_type(nbg_ctx *ctx, nbg_vector v, int *type);
-/* Number of stored entries (n or 0); known at record time in this subset, no wait needed. */
+/* Number of stored (present) entries.  Full / iso / empty vectors and operations over them know
+ * it at record time (n or 0); a vector over sparse or bitset operands is materialised first. */
 nbg_status nbg_vector_nvals(nbg_ctx *ctx, nbg_vector v, int64_t *nvals);
 /* 1 if v is currently materialised (FULL buffer, ISO or EMPTY), 0 if it is a pending node. */
 nbg_status nbg_vector_is_materialized(nbg_ctx *ctx, nbg_vector v, int *out);
@@ -241,6 +245,38 @@ nbg_status nbg_vector_is_materialized(nbg_ctx *ctx, nbg_vector v, int *out);
  * (e.g. torch) and to build row-block views for the multi-GPU driver. */
 nbg_status nbg_vector_device_ptr(nbg_ctx *ctx, nbg_vector v, void **ptr);
 nbg_status nbg_vector_free(nbg_ctx *ctx, nbg_vector v);
+
+/* ---------------------------------------------------------------- sparse and bitset vectors
+ * (PAPER.md:185 SparseVector / BitSetVector / FullVector, PAPER.md:234-246
+ * estimated fill ratios; GraphBLAS structure semantics: apply / bind2nd keep the operand's
+ * structure, ewise_mult = intersection, ewise_add = union with the present operand's value where
+ * only one is present, reduce = monoid over the present entries (identity if none), mxv = dense
+ * output (SPEC.md:206 reading) summing the stored entries whose x entry is present.)
+ * Representations: */
+enum { NBG_FORMAT_FULL = 0, NBG_FORMAT_ISO = 1, NBG_FORMAT_SPARSE = 2, NBG_FORMAT_BITSET = 3, NBG_FORMAT_EMPTY = 4 };
+
+/* Sparse vector of length n with nvals entries: indices (int32, strictly ascending, in [0, n))
+ * and values (nvals of `type`), both in `space`; copied.  Errors: NBG_INVALID_VALUE (bad sizes or
+ * indices not strictly ascending), NBG_INDEX_OUT_OF_BOUNDS (index outside [0, n)), NBG_NULL_POINTER. */
+nbg_status nbg_vector_from_sparse(nbg_ctx *ctx, nbg_vector *v, int type, int64_t n, int64_t nvals,
+                                  const int32_t *indices, const void *values, int space);
+
+/* Materialise v (forces wait) and export its present entries in ascending index order.  Call with
+ * indices == values == NULL to read *nvals only; otherwise both arrays must hold *nvals entries
+ * (the count from the first call) in `space`.  Works for every representation (a full vector
+ * exports all n entries, an empty one none).  Synchronises. */
+nbg_status nbg_vector_export_sparse(nbg_ctx *ctx, nbg_vector v, int64_t *nvals, int32_t *indices, void *values,
+                                    int space);
+
+/* Materialise v and return its representation (NBG_FORMAT_*): chosen by the library from the
+ * estimated fill of the result (sparse below 1/8, bitset above, full when every
+ * entry is present). */
+nbg_status nbg_vector_format(nbg_ctx *ctx, nbg_vector v, int *format);
+
+/* The naive metadata estimate of v's fill ratio (present entries / n) without materialising it
+ * (PAPER.md:236-240): materialised = nvals / n; apply, bind2nd = operand; ewise_mult = product;
+ * ewise_add = f_u + f_v - f_u f_v; mxv = 1.  Used only to choose loops and representations. */
+nbg_status nbg_vector_estimated_fill(nbg_ctx *ctx, nbg_vector v, double *fill);
 
 /* ---------------------------------------------------------------- scalars */
 

@@ -594,6 +594,7 @@ nbg_status nbg_vector_export_dense(nbg_ctx *ctx, nbg_vector v, void *out, int sp
     CHECK(out || x->n == 0, NBG_NULL_POINTER, "NULL out");
     if (!x->mat) materialize(*ctx, {x});
     if (x->kind == VKind::EMPTY) fail(NBG_INVALID_OBJECT, "export of an empty vector");
+    if (structured_kind(x->kind)) fail(NBG_INVALID_OBJECT, "vector is not full (sparse / bitset): use nbg_vector_export_sparse");
     size_t bytes = (size_t)x->n * type_size(x->type);
     if (bytes == 0) return NBG_SUCCESS;
     if (x->kind == VKind::ISO) {
@@ -635,7 +636,10 @@ nbg_status nbg_vector_nvals(nbg_ctx *ctx, nbg_vector v, int64_t *nv) {
     check_vec(ctx, v);
     CHECK(nv, NBG_NULL_POINTER, "NULL out");
     const NodeP &x = v->node;
-    *nv = (x->mat && x->kind == VKind::EMPTY) ? 0 : x->n;
+    if (!x->mat && needs_structured(x)) materialize(*ctx, {x});
+    if (x->mat && x->kind == VKind::EMPTY) *nv = 0;
+    else if (x->mat && structured_kind(x->kind)) *nv = x->nvals;
+    else *nv = x->n;
     API_END(ctx)
 }
 nbg_status nbg_vector_is_materialized(nbg_ctx *ctx, nbg_vector v, int *out) {
@@ -650,12 +654,117 @@ nbg_status nbg_vector_device_ptr(nbg_ctx *ctx, nbg_vector v, void **ptr) {
     NodeP x = v->node;
     if (!x->mat) materialize(*ctx, {x});
     if (x->kind == VKind::EMPTY) fail(NBG_INVALID_OBJECT, "empty vector has no values");
+    if (structured_kind(x->kind)) fail(NBG_INVALID_OBJECT, "vector is not full (sparse / bitset)");
     if (x->kind == VKind::ISO) {
         ensure_full(*ctx, x);
         *ptr = x->full_cache->d;
     } else {
         *ptr = x->buf->d;
     }
+    API_END(ctx)
+}
+
+// ---------------------------------------------------------------- sparse / bitset vectors (NEXT-3)
+
+nbg_status nbg_vector_from_sparse(nbg_ctx *ctx, nbg_vector *v, int type, int64_t n, int64_t nvals, const int32_t *indices,
+                                  const void *values, int space) {
+    API_BEGIN
+    check_ctx(ctx);
+    CHECK(v && ((indices && values) || nvals == 0), NBG_NULL_POINTER, "nbg_vector_from_sparse: NULL argument");
+    CHECK(n >= 0 && n <= MAXDIM && nvals >= 0 && nvals <= n, NBG_INVALID_VALUE, "nbg_vector_from_sparse: bad sizes");
+    CHECK(space == NBG_HOST || space == NBG_DEVICE, NBG_INVALID_VALUE, "bad space");
+    check_type(type);
+    NodeP x = mk(*ctx, Op::LEAF, type, n, false);
+    x->mat = true;
+    if (nvals == 0) {
+        x->kind = VKind::EMPTY;
+    } else {
+        x->idx = upload(*ctx, indices, (size_t)nvals * 4, space, NBG_COPY);
+        x->buf = upload(*ctx, values, (size_t)nvals * type_size(type), space, NBG_COPY);
+        const int bad = gpu_check_sparse(*ctx, n, nvals, (const int32_t *)x->idx->d);
+        if (bad == 2) fail(NBG_INDEX_OUT_OF_BOUNDS, "nbg_vector_from_sparse: index outside [0, n)");
+        if (bad == 1) fail(NBG_INVALID_VALUE, "nbg_vector_from_sparse: indices must be strictly ascending");
+        x->nvals = nvals;
+        if (nvals == n) {
+            x->kind = VKind::FULL;   // every entry present: the dense representation
+            x->idx.reset();
+        } else {
+            x->kind = VKind::SPARSE;
+        }
+    }
+    *v = new_vhandle(ctx, x);
+    API_END(ctx)
+}
+
+nbg_status nbg_vector_export_sparse(nbg_ctx *ctx, nbg_vector v, int64_t *nvals, int32_t *indices, void *values, int space) {
+    API_BEGIN
+    check_ctx(ctx);
+    check_vec(ctx, v);
+    CHECK(nvals, NBG_NULL_POINTER, "NULL nvals");
+    CHECK(space == NBG_HOST || space == NBG_DEVICE, NBG_INVALID_VALUE, "bad space");
+    NodeP x = v->node;
+    if (!x->mat) materialize(*ctx, {x});
+    const int64_t nv = x->kind == VKind::EMPTY ? 0 : (structured_kind(x->kind) ? x->nvals : x->n);
+    if (!indices && !values) {
+        *nvals = nv;
+        NBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        return ctx->latched;
+    }
+    CHECK(indices && values, NBG_NULL_POINTER, "nbg_vector_export_sparse: indices and values are both required");
+    CHECK(*nvals >= nv, NBG_INVALID_VALUE, "nbg_vector_export_sparse: *nvals smaller than the number of entries");
+    *nvals = nv;
+    if (nv == 0) return NBG_SUCCESS;
+    const cudaMemcpyKind dir = space == NBG_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    const size_t w = type_size(x->type);
+    BufP idx = x->idx, vals = x->buf, keep_i, keep_v;
+    if (x->kind == VKind::BITSET) {
+        gpu_bitset_to_sparse(*ctx, x->n, (const uint32_t *)x->bits->d, x->buf->d, x->type, &keep_i, &keep_v);
+        idx = keep_i;
+        vals = keep_v;
+    } else if (x->kind == VKind::FULL || x->kind == VKind::ISO) {
+        BufP bits = alloc_buf(*ctx, (size_t)((x->n + 31) / 32) * 4);
+        gpu_bitset_full(*ctx, x->n, (uint32_t *)bits->d);
+        const void *dense;
+        if (x->kind == VKind::ISO) {
+            ensure_full(*ctx, x);
+            dense = x->full_cache->d;
+        } else {
+            dense = x->buf->d;
+        }
+        gpu_bitset_to_sparse(*ctx, x->n, (const uint32_t *)bits->d, dense, x->type, &keep_i, &keep_v);
+        idx = keep_i;
+        vals = keep_v;
+    }
+    NBG_CUDA(cudaMemcpyAsync(indices, idx->d, (size_t)nv * 4, dir, ctx->stream));
+    NBG_CUDA(cudaMemcpyAsync(values, vals->d, (size_t)nv * w, dir, ctx->stream));
+    NBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->latched != NBG_SUCCESS) return ctx->latched;
+    API_END(ctx)
+}
+
+nbg_status nbg_vector_format(nbg_ctx *ctx, nbg_vector v, int *format) {
+    API_BEGIN
+    check_ctx(ctx);
+    check_vec(ctx, v);
+    CHECK(format, NBG_NULL_POINTER, "NULL out");
+    NodeP x = v->node;
+    if (!x->mat) materialize(*ctx, {x});
+    switch (x->kind) {
+        case VKind::FULL: *format = NBG_FORMAT_FULL; break;
+        case VKind::ISO: *format = NBG_FORMAT_ISO; break;
+        case VKind::SPARSE: *format = NBG_FORMAT_SPARSE; break;
+        case VKind::BITSET: *format = NBG_FORMAT_BITSET; break;
+        default: *format = NBG_FORMAT_EMPTY;
+    }
+    API_END(ctx)
+}
+
+nbg_status nbg_vector_estimated_fill(nbg_ctx *ctx, nbg_vector v, double *fill) {
+    API_BEGIN
+    check_ctx(ctx);
+    check_vec(ctx, v);
+    CHECK(fill, NBG_NULL_POINTER, "NULL out");
+    *fill = estimated_fill(v->node.get());
     API_END(ctx)
 }
 

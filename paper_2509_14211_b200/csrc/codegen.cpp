@@ -998,6 +998,149 @@ int gen_tp2(Gen &g, const std::string &kname) {
 
 extern const char *NBG_PRELUDE_SRC;
 
+// ---------------------------------------------------------------- structured regions (NEXT-3)
+//
+// A region over sparse / bitset / full leaves: every instruction carries a
+// presence bit next to its value -- leaves: full = present, bitset = bit test, sparse = binary
+// search of its sorted indices; apply / bind2nd keep the operand's presence, ewise_mult ANDs
+// (intersection), ewise_add ORs (union; the value is op(u, v) where both are present, else the
+// present operand converted to the output type).  Two loops (chosen by the
+// estimator in structured.cpp):
+//   dense : one thread per element, one warp per 32 consecutive elements; the output presence is
+//           one __ballot_sync word per warp (the output bitset, coalesced), values are dense
+//           (absent = 0) and the present count goes to a.part
+//   index : one thread per entry of a sorted driver index list (a sparse operand's indices, or the
+//           union of several); per entry a presence flag (a.out[1], bytes) and a value, compacted
+//           afterwards in index order
+// Reductions count present elements only.
+std::string SProg::signature() const {
+    std::ostringstream s;
+    s << "X" << (index_mode ? "i" : "d") << (vec_out ? "v" : "r") << "|" << p.signature() << "|";
+    for (uint8_t m : pmode) s << (int)m;
+    s << "|";
+    for (uint8_t l : leaf) s << (int)l;
+    return s.str();
+}
+
+std::string codegen_structured(const SProg &sp, const std::string &kname) {
+    const Prog &p = sp.p;
+    Gen g(p);
+    auto &o = g.o;
+    o << NBG_PRELUDE_SRC << "\n// ---- structured region: " << sp.signature() << "\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
+    o << "  __shared__ double nbg_sh[32];\n";
+    o << "  const int lane = threadIdx.x & 31;\n";
+    g.emit_uniform();
+    for (size_t k = 0; k < p.ins.size(); k++)
+        if (p.ins[k].uniform) o << "  const bool p" << k << " = true;\n";
+    g.emit_red_decl();
+    const int NI = p.n_in;
+    auto body = [&](const std::string &ind) {
+        for (size_t k = 0; k < p.ins.size(); k++) {
+            const Ins &in = p.ins[k];
+            if (in.uniform) continue;
+            const std::string T = ctype(in.t), vk = g.v((int)k), pk = "p" + std::to_string(k);
+            if (in.k == Ins::LD_VEC) {
+                const std::string vals = "((const " + T + "*)a.in[" + std::to_string(in.slot) + "])";
+                const int lk = sp.leaf[in.slot];
+                if (lk == 0) {
+                    o << ind << "const bool " << pk << " = true;\n";
+                    o << ind << "const " << T << " " << vk << " = " << vals << "[ic];\n";
+                } else if (lk == 1) {
+                    o << ind << "const bool " << pk << " = ((((const unsigned*)a.in[" << NI + in.slot << "])[ic >> 5]) >> (ic & 31)) & 1u;\n";
+                    o << ind << "const " << T << " " << vk << " = " << vals << "[ic];\n";
+                } else {
+                    o << ind << "long long lo" << k << " = 0;\n";
+                    o << ind << "{ const int* ix_ = (const int*)a.in[" << NI + in.slot << "]; long long hi_ = (long long)a.imm[" << in.imm0
+                      << "]; while (lo" << k << " < hi_) { const long long m_ = (lo" << k << " + hi_) >> 1; if ((long long)ix_[m_] < ic) lo" << k
+                      << " = m_ + 1; else hi_ = m_; } }\n";
+                    o << ind << "const bool " << pk << " = lo" << k << " < (long long)a.imm[" << in.imm0 << "] && (long long)((const int*)a.in["
+                      << NI + in.slot << "])[lo" << k << "] == ic;\n";
+                    o << ind << "const " << T << " " << vk << " = " << pk << " ? " << vals << "[lo" << k << "] : (" << T << ")0;\n";
+                }
+                continue;
+            }
+            const std::string pa = "p" + std::to_string(in.a), pb = in.b >= 0 ? "p" + std::to_string(in.b) : "true";
+            const int pm = sp.pmode[k];
+            if (pm == 2) {
+                o << ind << "const " << T << " t" << k << " = " << g.expr(in, "") << ";\n";
+                o << ind << "const " << T << " " << vk << " = (" << pa << " && " << pb << ") ? t" << k << " : (" << pa << " ? "
+                  << g.cvt(in.t, g.v(in.a)) << " : " << g.cvt(in.t, g.v(in.b)) << ");\n";
+                o << ind << "const bool " << pk << " = " << pa << " || " << pb << ";\n";
+            } else {
+                o << ind << "const " << T << " " << vk << " = " << g.expr(in, "") << ";\n";
+                o << ind << "const bool " << pk << " = " << (pm == 1 ? pa + " && " + pb : pa) << ";\n";
+            }
+        }
+    };
+    const int root = sp.vec_out ? p.outs[0].ins : p.reds[0].ins;
+    const std::string RT = ctype(p.ins[root].t);
+    if (!sp.index_mode) {
+        o << "  const long long nwords = (a.n + 31) >> 5;\n";
+        o << "  unsigned long long cnt_ = 0ull;\n";
+        o << "  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwords; w += ((long long)gridDim.x * blockDim.x) >> 5) {\n";
+        o << "    const long long i = (w << 5) + lane;\n";
+        o << "    const bool inb = i < a.n;\n";
+        o << "    const long long ic = inb ? i : 0;\n";
+        body("    ");
+        o << "    const bool P_ = inb && p" << root << ";\n";
+        if (sp.vec_out) {
+            o << "    const unsigned m_ = __ballot_sync(0xffffffffu, P_);\n";
+            o << "    if (lane == 0) { ((unsigned*)a.out[1])[w] = m_; cnt_ += (unsigned long long)__popc(m_); }\n";
+            o << "    if (inb) ((" << RT << "*)a.out[0])[i] = P_ ? " << g.v(root) << " : (" << RT << ")0;\n";
+        } else {
+            o << "    if (P_) { " << g.red_update(p.reds[0], "r0", g.v(root)) << " }\n";
+        }
+        o << "  }\n";
+        if (sp.vec_out) o << "  if (lane == 0 && cnt_) atomicAdd((unsigned long long*)a.part, cnt_);\n";
+    } else {
+        o << "  const int* __restrict__ D_ = (const int*)a.rowptr;\n";
+        o << "  for (long long k_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; k_ < a.nnz; k_ += (long long)gridDim.x * blockDim.x) {\n";
+        o << "    const long long ic = (long long)D_[k_];\n";
+        body("    ");
+        if (sp.vec_out) {
+            o << "    ((unsigned char*)a.out[1])[k_] = p" << root << " ? 1 : 0;\n";
+            o << "    ((" << RT << "*)a.out[0])[k_] = p" << root << " ? " << g.v(root) << " : (" << RT << ")0;\n";
+        } else {
+            o << "    if (p" << root << ") { " << g.red_update(p.reds[0], "r0", g.v(root)) << " }\n";
+        }
+        o << "  }\n";
+    }
+    g.emit_red_finish();
+    o << "}\n";
+    return g.o.str();
+}
+
+// mxv with a structured x (SPEC.md:206 reading: dense output, identity where no stored entry of
+// the row meets a present x entry): one warp per row of the CSR, lane-strided entries, presence by
+// bit test, fixed xor-shuffle tree -> deterministic.
+std::string codegen_smxv(const SpmvSig &sp, const std::string &kname) {
+    SemiringCode k = semiring_code(sp);
+    std::ostringstream o;
+    o << NBG_PRELUDE_SRC << "\n// ---- structured mxv\n";
+    o << "#define NBG_ADD(A_, B_) " << k.ADD << "\n";
+    o << "__device__ __forceinline__ " << k.C << " nbg_mul(const KArgs &a, long long P_, " << k.XT << " X_) { return " << k.mul << "; }\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
+    o << "  const int lane = threadIdx.x & 31;\n";
+    o << "  const long long* __restrict__ RP = a.rowptr;\n";
+    o << "  const int* __restrict__ CI = a.colidx;\n";
+    o << "  const " << k.XT << "* __restrict__ X = (const " << k.XT << "*)a.x;\n";
+    o << "  const unsigned* __restrict__ XB = (const unsigned*)a.in[0];\n";
+    o << "  for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < a.n; i += ((long long)gridDim.x * blockDim.x) >> 5) {\n";
+    o << "    " << k.ACC << " acc = " << k.IDENT << ";\n";
+    o << "    const long long s1 = RP[i + 1];\n";
+    o << "    for (long long P_ = RP[i] + lane; P_ < s1; P_ += 32) {\n";
+    o << "      const int j = CI[P_];\n";
+    o << "      if ((XB[j >> 5] >> (j & 31)) & 1u) acc = NBG_ADD(acc, (" << k.ACC << ")nbg_mul(a, P_, X[j]));\n";
+    o << "    }\n";
+    o << "    #pragma unroll\n    for (int d = 16; d >= 1; d >>= 1) { const " << k.ACC << " y_ = __shfl_xor_sync(0xffffffffu, acc, d); acc = NBG_ADD(acc, y_); }\n";
+    o << "    if (lane == 0) ((" << ctype(sp.T) << "*)a.out[0])[i] = (" << ctype(sp.T) << ")acc;\n";
+    o << "  }\n";
+    o << "}\n";
+    return o.str();
+}
+
+
 bool spmv_epilogue_prefetch() {
     static int v = -1;
     if (v < 0) {

@@ -181,7 +181,9 @@ using MatP = std::shared_ptr<Mat>;
 // ---------------------------------------------------------------- DAG nodes
 
 enum class Op : uint8_t { LEAF = 0, APPLY, BIND2ND, EMULT, EADD, MXV, REDUCE, SAPPLY };
-enum class VKind : uint8_t { EMPTY = 0, ISO = 1, FULL = 2 };
+// vector representations (PAPER.md:185 SparseVector / BitSetVector / FullVector).  EMPTY and ISO
+// are folded at record time; SPARSE and BITSET carry a structure.
+enum class VKind : uint8_t { EMPTY = 0, ISO = 1, FULL = 2, SPARSE = 3, BITSET = 4 };
 
 struct Node;
 using NodeP = std::shared_ptr<Node>;
@@ -202,7 +204,10 @@ struct Node {
     // materialised state
     bool mat = false;
     VKind kind = VKind::FULL;    // kind is known at record time (EMPTY/ISO folded eagerly)
-    BufP buf;                    // FULL vector
+    BufP buf;                    // FULL: n values; SPARSE: nvals values; BITSET: n values
+    BufP idx;                    // SPARSE: int32[nvals] strictly ascending indices
+    BufP bits;                   // BITSET: uint32[(n + 31) / 32], bit i = entry i present
+    int64_t nvals = 0;           // SPARSE / BITSET: number of present entries
     double iso = 0.0;            // ISO vector value (already rounded to type)
     // scalar state
     SFmt sfmt = SFmt::HOST;
@@ -374,6 +379,32 @@ void timing_collect(Ctx &c);
 void materialize(Ctx &c, const std::vector<NodeP> &roots);
 double scalar_read(Ctx &c, const NodeP &s);
 void ensure_full(Ctx &c, const NodeP &v);   // ISO leaf -> FULL buffer
+
+// structured (sparse / bitset) vectors: structured.cpp, sparse.cu
+bool structured_kind(VKind k);                       // SPARSE or BITSET
+bool needs_structured(const NodeP &r);               // root whose region reads a sparse/bitset leaf
+void materialize_structured(Ctx &c, const NodeP &r); // one structured region (vector or reduce root)
+double estimated_fill(const Node *x);                // naive metadata estimator
+// structured region program: Prog + presence algebra
+struct SProg {
+    Prog p;
+    std::vector<uint8_t> pmode;   // per instruction: 0 inherit a, 1 AND (ewise_mult), 2 OR (ewise_add), 3 leaf
+    std::vector<uint8_t> leaf;    // per input slot: 0 full, 1 bitset (bits in in[n_in + slot]), 2 sparse (binary search)
+    bool index_mode = false;      // iterate a sorted index list (a.rowptr as int*, a.nnz entries) instead of [0, n)
+    bool vec_out = true;          // root is a vector (else a reduction)
+    std::string signature() const;
+};
+std::string codegen_structured(const SProg &sp, const std::string &kname);
+std::string codegen_smxv(const SpmvSig &sp, const std::string &kname);
+// device helpers (sparse.cu)
+int gpu_check_sparse(Ctx &c, int64_t n, int64_t nv, const int32_t *idx);   // 0 ok, 1 not ascending, 2 out of range
+void gpu_sparse_to_bitset(Ctx &c, int64_t n, int64_t nv, const int32_t *idx, const void *vals, int type, uint32_t *bits,
+                          void *dense);
+int64_t gpu_bitset_to_sparse(Ctx &c, int64_t n, const uint32_t *bits, const void *dense, int type, BufP *idx, BufP *vals);
+int64_t gpu_select_flagged(Ctx &c, int64_t m, const int32_t *idx, const void *vals, const uint8_t *flags, int type, BufP *oidx,
+                           BufP *ovals);
+int64_t gpu_union_indices(Ctx &c, const std::vector<std::pair<const int32_t *, int64_t>> &lists, BufP *out);
+void gpu_bitset_full(Ctx &c, int64_t n, uint32_t *bits);   // all n bits set, tail bits clear
 
 // codegen / jit
 bool spmv_gather_pipeline();   // SpMV gathers one step ahead (NBG_SPMV_GPIPE=1)

@@ -72,6 +72,8 @@ static void key_rec(const Node *x, std::string &s, const Node *ph) {
             else s += "d" + std::to_string(x->type) + ":" + std::to_string(x->slot->id);
         } else if (x->kind == VKind::FULL) s += "F" + std::to_string(x->buf->id);
         else if (x->kind == VKind::ISO) s += "I" + std::to_string(x->type) + ":" + dbits(x->iso);
+        else if (x->kind == VKind::SPARSE) s += "S" + std::to_string(x->buf->id);
+        else if (x->kind == VKind::BITSET) s += "B" + std::to_string(x->buf->id);
         else s += "E";
         return;
     }
@@ -93,7 +95,7 @@ static std::string node_key(const Node *x, const Node *ph = nullptr) {
 static void leaf_bufs(const Node *x, std::vector<std::weak_ptr<Buf>> &deps, std::unordered_set<const Node *> &seen) {
     if (!seen.insert(x).second) return;
     if (x->mat) {
-        if (!x->scalar && x->kind == VKind::FULL && x->buf) deps.push_back(x->buf);
+        if (!x->scalar && (x->kind == VKind::FULL || structured_kind(x->kind)) && x->buf) deps.push_back(x->buf);
         return;
     }
     if (x->a) leaf_bufs(x->a.get(), deps, seen);
@@ -120,6 +122,9 @@ static void copy_result(Node &dst, const Node &src) {
     dst.mat = true;
     dst.kind = src.kind;
     dst.buf = src.buf;
+    dst.idx = src.idx;
+    dst.bits = src.bits;
+    dst.nvals = src.nvals;
     dst.iso = src.iso;
     dst.sfmt = src.sfmt;
     dst.hval = src.hval;
@@ -395,6 +400,8 @@ struct Builder {
                     in_slot_of[x.get()] = si;
                 } else si = s->second;
                 in.slot = si;
+            } else if (structured_kind(x->kind)) {
+                fail(NBG_PANIC, "planner: structured vector inside a dense region");
             } else {
                 fail(NBG_PANIC, "planner: empty vector inside a region");
             }
@@ -436,6 +443,8 @@ struct Builder {
                 case Op::MXV: {
                     if (mxv && mxv.get() != x.get()) { need(x); return -1; }
                     const NodeP &u = x->a;
+                    // a sparse / bitset x: the mxv runs on its own (structured.cpp), then feeds this region
+                    if (u->mat && !u->scalar && structured_kind(u->kind)) { need(x); return -1; }
                     Mat &A = *x->A;
                     if (!A.plan) gpu_build_spmv_plan(c, A);
                     if (A.plan->relabel) {
@@ -837,6 +846,15 @@ void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
         std::vector<NodeP> left;
         for (const NodeP &r : roots)
             if (!memo_bind(c, r)) left.push_back(r);
+        roots.swap(left);
+    }
+    // regions reading sparse / bitset vectors run through the structured executor, one each
+    {
+        std::vector<NodeP> left;
+        for (const NodeP &r : roots) {
+            if (needs_structured(r)) materialize_structured(c, r);
+            else left.push_back(r);
+        }
         roots.swap(left);
     }
     // group by index-space length (one kernel per group)

@@ -160,6 +160,40 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
             std::string nm2 = "selftest_bin_" + std::to_string(k++);
             if (!compile_only(codegen(q, nm2), nm2, log)) fails++;
         }
+        // (6) structured regions (NEXT-3): z = (x .* s) (+) apply(b) over full / bitset / sparse leaves,
+        // dense and index loops, vector and reduce roots; structured mxv for every monoid
+        for (int T : {NBG_INT32, NBG_FP32, NBG_FP64})
+            for (int im : {0, 1})
+                for (int vec : {0, 1}) {
+                    SProg sp;
+                    sp.index_mode = im;
+                    sp.vec_out = vec;
+                    Prog &p = sp.p;
+                    p.ins.push_back(I(Ins::LD_VEC, T, 0, -1, -1, 0));                      // 0 x (full)
+                    p.ins.push_back(I(Ins::LD_VEC, T, 0, -1, -1, 1));                      // 1 s (sparse / bitset)
+                    p.ins.push_back(I(Ins::LD_VEC, NBG_FP64, 0, -1, -1, 2));               // 2 b (bitset)
+                    p.ins.push_back(I(Ins::BIN, T, NBG_TIMES, 0, 1));                      // 3 x .* s
+                    Ins u = I(Ins::UN, T, NBG_ADD_C, 2); u.imm0 = 1; p.ins.push_back(u);   // 4 b + c
+                    p.ins.push_back(I(Ins::BIN, T, NBG_MAX, 3, 4));                        // 5 union
+                    p.ins[1].imm0 = 0;
+                    sp.pmode = {3, 3, 3, 1, 0, 2};
+                    sp.leaf = {0, (uint8_t)(im ? 2 : 1), 1};
+                    if (vec) { p.outs.push_back(OutV{5, 0}); p.n_out = 1; }
+                    else {
+                        p.reds.push_back(RedOut{5, NBG_PLUS, 0, (uint8_t)(is_float(T) ? SFmt::XACC : SFmt::I64)});
+                        p.n_red = 1;
+                    }
+                    p.n_in = 3; p.n_imm = 2;
+                    std::string nm = "selftest_sreg_" + std::to_string(k++);
+                    if (!compile_only(codegen_structured(sp, nm), nm, log)) fails++;
+                }
+        for (int add : {NBG_PLUS, NBG_MIN, NBG_MAX})
+            for (int T : {NBG_INT32, NBG_FP32, NBG_FP64}) {
+                SpmvSig sg;
+                sg.add = add; sg.mul = NBG_TIMES; sg.T = T; sg.xt = T; sg.at = NBG_FP32; sg.has_vals = true;
+                std::string nm = "selftest_smxv_" + std::to_string(k++);
+                if (!compile_only(codegen_smxv(sg, nm), nm, log)) fails++;
+            }
     } catch (const Error &e) {
         log += "exception: " + e.msg;
         fails++;

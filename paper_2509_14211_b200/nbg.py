@@ -33,6 +33,8 @@ COPY, BORROW = 0, 1
 IDENTITY, AINV, ABS, MINV, ADD_C, MUL_C, AXPB, ABS_SUB_C, RECIP_SCALED, ISZERO = range(10)
 PLUS, MINUS, TIMES, DIV, MIN, MAX, FIRST, SECOND, ABSDIFF, MAX_DIVX_C = range(10)
 GRAPH_RMAT, GRAPH_ER = 0, 1
+FORMAT_FULL, FORMAT_ISO, FORMAT_SPARSE, FORMAT_BITSET, FORMAT_EMPTY = range(5)
+FORMAT_NAMES = ["full", "iso", "sparse", "bitset", "empty"]
 PR_UNIFORM, PR_DROP = 0, 1
 
 UNOPS = {n: i for i, n in enumerate(["IDENTITY", "AINV", "ABS", "MINV", "ADD_C", "MUL_C", "AXPB", "ABS_SUB_C",
@@ -79,7 +81,7 @@ class nbg_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("waits", "plans_built", "plan_hits", "jit_compiles", "kernels_launched",
                                                 "vectors_materialized", "intermediates_elided", "memo_hits",
                                                 "side_outputs", "bytes_materialized", "host_plan_ns")] + \
-               [("jit_ms", ctypes.c_double)]
+               [("jit_ms", ctypes.c_double), ("structured_regions", ctypes.c_uint64), ("structured_index_loops", ctypes.c_uint64)]
 
 
 vp = ctypes.c_void_p
@@ -117,6 +119,10 @@ SIGNATURES = {
     "nbg_vector_is_materialized": [vp, vp, ctypes.POINTER(ctypes.c_int)],
     "nbg_vector_device_ptr": [vp, vp, pvp],
     "nbg_vector_free": [vp, vp],
+    "nbg_vector_from_sparse": [vp, pvp, ctypes.c_int, i64, i64, vp, vp, ctypes.c_int],
+    "nbg_vector_export_sparse": [vp, vp, ctypes.POINTER(i64), vp, vp, ctypes.c_int],
+    "nbg_vector_format": [vp, vp, ctypes.POINTER(ctypes.c_int)],
+    "nbg_vector_estimated_fill": [vp, vp, ctypes.POINTER(ctypes.c_double)],
     "nbg_scalar_new": [vp, pvp, ctypes.c_int, ctypes.c_double],
     "nbg_scalar_get": [vp, vp, ctypes.POINTER(ctypes.c_double)],
     "nbg_scalar_free": [vp, vp],
@@ -355,6 +361,41 @@ def nbg_vector_device_ptr(ctx, v):
 
 def nbg_vector_free(ctx, v):
     _call(ctx, "nbg_vector_free", ctx, v)
+
+
+def nbg_vector_from_sparse(ctx, type, n, indices, values):
+    """Sparse vector (include/nbg.h nbg_vector_from_sparse): int32 ascending indices + values."""
+    nv = int(indices.shape[0])
+    ip, sp = _ptr(indices)
+    vp_, sp2 = _ptr(values)
+    if sp != sp2:
+        raise ValueError("indices and values must live in the same space")
+    v = _out()
+    _call(ctx, "nbg_vector_from_sparse", ctx, ctypes.byref(v), type, int(n), nv, ip, vp_, sp)
+    return v
+
+
+def nbg_vector_export_sparse(ctx, v):
+    """-> (indices int32, values) of the present entries, ascending (two-call protocol)."""
+    nv = i64(0)
+    _call(ctx, "nbg_vector_export_sparse", ctx, v, ctypes.byref(nv), None, None, HOST)
+    idx = np.empty(nv.value, np.int32)
+    vals = np.empty(nv.value, NP_OF[nbg_vector_type(ctx, v)])
+    if nv.value:
+        _call(ctx, "nbg_vector_export_sparse", ctx, v, ctypes.byref(nv), idx.ctypes.data, vals.ctypes.data, HOST)
+    return idx, vals
+
+
+def nbg_vector_format(ctx, v):
+    t = ctypes.c_int()
+    _call(ctx, "nbg_vector_format", ctx, v, ctypes.byref(t))
+    return t.value
+
+
+def nbg_vector_estimated_fill(ctx, v):
+    f = ctypes.c_double()
+    _call(ctx, "nbg_vector_estimated_fill", ctx, v, ctypes.byref(f))
+    return f.value
 
 
 def nbg_scalar_new(ctx, type, value):
