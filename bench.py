@@ -383,6 +383,78 @@ def run_chain(args):
             "gpu_launches": int(round(fused_k * args.steps))}
 
 
+# ------------------------------------------------------------------ NEXT-3: sparse / bitset vectors
+
+def run_sparse(args):
+    """Structured regions: s = reduce(+, ewise_mult(*, u, x)) and
+    w = ewise_add(+, u, v) with u, v sparse (fill f) and x full, n = 2^24 fp32.  For each fill the
+    estimator's loop choice (auto) is timed next to the forced alternative (NBG_STRUCT_LOOP), so
+    the line shows whether the naive fill estimate picks the faster loop.
+    value = present entries of u processed per second by the mult+reduce step at f = 0.01 (auto)."""
+    import torch
+    from paper_2509_14211_b200 import nbg
+    torch.cuda.set_device(0)
+    n = 1 << 24
+    rng = np.random.default_rng(args.seed)
+    xv = rng.random(n).astype(np.float32)
+    stream = torch.cuda.current_stream()
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0, stream.cuda_stream)
+    dx = nbg.nbg_vector_from_dense(c, nbg.FP32, xv)
+    rows = []
+    pk, pk_src = peaks()
+    for fill in (0.001, 0.01, 0.03, 0.06, 0.1, 0.4):
+        iu = np.nonzero(rng.random(n) < fill)[0].astype(np.int32)
+        iv = np.nonzero(rng.random(n) < fill)[0].astype(np.int32)
+        du = nbg.nbg_vector_from_sparse(c, nbg.FP32, n, iu, rng.random(iu.shape[0]).astype(np.float32))
+        dv = nbg.nbg_vector_from_sparse(c, nbg.FP32, n, iv, rng.random(iv.shape[0]).astype(np.float32))
+        row = {"fill": fill, "nvals": int(iu.shape[0])}
+        for loop in ("auto", "index", "dense"):
+            if loop == "auto":
+                os.environ.pop("NBG_STRUCT_LOOP", None)
+            else:
+                os.environ["NBG_STRUCT_LOOP"] = loop
+
+            def step():
+                m = nbg.nbg_ewise_mult(c, nbg.FP32, "TIMES", du, dx)
+                s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", m)
+                v = nbg.nbg_scalar_get(c, s)
+                nbg.nbg_scalar_free(c, s)
+                nbg.nbg_vector_free(c, m)
+                w = nbg.nbg_ewise_add(c, nbg.FP32, "PLUS", du, dv)
+                k = nbg.nbg_vector_nvals(c, w)
+                nbg.nbg_vector_free(c, w)
+                return v, k
+
+            for _ in range(args.warmup):
+                step()
+            st0 = nbg.nbg_get_stats(c)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                step()
+            torch.cuda.synchronize()
+            ms = (time.perf_counter() - t0) * 1e3 / args.steps
+            st1 = nbg.nbg_get_stats(c)
+            row[loop + "_ms"] = round(ms, 4)
+            if loop == "auto":
+                row["auto_index_loops_per_step"] = (st1["structured_index_loops"] - st0["structured_index_loops"]) / args.steps
+        os.environ.pop("NBG_STRUCT_LOOP", None)
+        # algorithmic bytes of the mult+reduce over the index loop: u's indices and values, x at u's positions
+        row["index_bytes"] = int(iu.shape[0]) * 12
+        rows.append(row)
+        nbg.nbg_vector_free(c, du)
+        nbg.nbg_vector_free(c, dv)
+    nbg.nbg_finalize(c)
+    r01 = [r for r in rows if r["fill"] == 0.01][0]
+    return {"metric": "structured ewise_mult+reduce and ewise_add over sparse vectors (present entries/s of u)",
+            "value": round(r01["nvals"] / (r01["auto_ms"] * 1e-3) / 1e9, 4), "unit": "G entries/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r01["auto_ms"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "sparse: n = 2^24, u, v sparse with fill f (uniform random support), x full; "
+                                   "step = reduce(+, u .* x) read back + nvals(u + v)", "timing": "host wall clock per step (includes the scalar read-back and nvals syncs)"},
+            "peak_hbm_gbs": pk, "fills": rows}
+
+
 # ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
 
 def workload_name(args, cfg):
@@ -456,7 +528,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "sparse"])
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"], help="c2 only")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-sweeps", type=int, default=3)
@@ -474,8 +546,9 @@ def main():
         sys.exit(2)
     if args.mtx:
         args.workload = "c4"
-    if args.workload == "c2":
-        res = run_chain(args) if args.impl == "ours" and rank == 0 else None
+    if args.workload in ("c2", "sparse"):
+        fn = run_chain if args.workload == "c2" else run_sparse
+        res = fn(args) if args.impl == "ours" and rank == 0 else None
         if rank == 0 and res is not None:
             print(json.dumps(res), flush=True)
         return

@@ -29,7 +29,7 @@
 namespace nbg {
 
 static constexpr double SPARSE_FILL = 1.0 / 16.0;  // estimated fill at or below: sparse representation, else bitset
-static constexpr double INDEX_FILL = 0.5;           // driver entries / n at or below: loop over the driver's indices
+static constexpr double INDEX_FILL = 1.0 / 16.0;    // driver entries / n at or below: loop over the driver's indices (measured crossover, bench.py --workload sparse)
 
 bool structured_kind(VKind k) { return k == VKind::SPARSE || k == VKind::BITSET; }
 
@@ -367,7 +367,11 @@ void materialize_structured(Ctx &c, const NodeP &r) {
     const bool has_cover = !sfull && cover(R.get(), cov);
     int64_t cov_n = 0;
     for (const Node *l : cov) cov_n += l->nvals;
-    const bool index_mode = has_cover && n > 0 && (double)cov_n <= INDEX_FILL * (double)n;
+    bool index_mode = has_cover && n > 0 && (double)cov_n <= INDEX_FILL * (double)n;
+    // NBG_STRUCT_LOOP=index|dense overrides the estimator's choice (benchmarking the choice itself)
+    const char *force = getenv("NBG_STRUCT_LOOP");
+    if (force && has_cover && !strcmp(force, "index")) index_mode = true;
+    if (force && !strcmp(force, "dense")) index_mode = false;
     const bool want_sparse = f_est <= SPARSE_FILL;
 
     SBuilder B(c, index_mode);
