@@ -110,3 +110,40 @@ def test_c4_rmat22_full(nbg):
         assert delta_close(hist, dho, ro, np.float32)
     finally:
         nbg.nbg_finalize(c)
+
+
+def test_c5_rmat26_sampled(nbg):
+    """C5 (R-MAT s26, 1.06 B edges) at full size in bench.py's single-GPU launch configuration:
+    the oracle cannot run 30 sweeps of a billion edges in test time, so the check is one sweep
+    from the GPU's own sweep-1 state -- r2[i] for sampled rows (random, the 64 longest, tile
+    edges) recomputed by the C oracle's row kernel from r1 exactly as Fig. 6 defines it -- plus
+    the sweep-2 delta over all n."""
+    cfg = inputs.CONFIGS["c5"]
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, cfg["scale"], cfg["edge_factor"], 1)
+        rp, ci = nbg.nbg_matrix_export_csr(c, A)
+        d = nbg.nbg_vector_export_dense(c, deg)
+        n = rp.shape[0] - 1
+        assert rp[-1] == ci.shape[0] and np.all(d >= 0) and int(d.sum()) == ci.shape[0]
+        r1v, s1, _ = nbg.nbg_pagerank(c, A, deg, alpha=cfg["alpha"], tol=-1.0, itermax=1, type=nbg.FP32)
+        r2v, s2, h2 = nbg.nbg_pagerank(c, A, deg, alpha=cfg["alpha"], tol=-1.0, itermax=2, type=nbg.FP32)
+        assert s1 == 1 and s2 == 2
+        r1 = nbg.nbg_vector_export_dense(c, r1v)
+        r2 = nbg.nbg_vector_export_dense(c, r2v)
+        alpha = cfg["alpha"]
+        dinv = np.where(d > 0, (alpha / np.maximum(d, 1).astype(np.float64)).astype(np.float32), np.float32(0))
+        y = (r1 * dinv).astype(np.float32)                        # a4: fl_T(t * dinv)
+        ds = float(r1[d == 0].astype(np.float64).sum())           # a9 (sequential fp64 as the oracle)
+        cst = np.float32((alpha / n) * ds + (1.0 - alpha) / n)    # a6 constant, double rounded once
+        rng = np.random.default_rng(5)
+        lens = np.diff(rp)
+        rows = np.unique(np.concatenate([rng.integers(0, n, 3000), np.argsort(lens)[-64:],
+                                         np.arange(0, n, n // 64)[:64], [0, n - 1]]))
+        exp = np.array([oracle.sweep_rows_f32(int(i), int(i) + 1, rp, ci, y, cst)[0] for i in rows], np.float32)
+        got = r2[rows]
+        assert rel(got, exp) <= 1e-6, "sampled rows of sweep 2 differ from the oracle"
+        delta2 = float(np.abs(r2.astype(np.float64) - r1.astype(np.float64)).sum())
+        assert abs(h2[1] - delta2) <= 1e-9 * delta2
+    finally:
+        nbg.nbg_finalize(c)
