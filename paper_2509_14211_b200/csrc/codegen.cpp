@@ -44,7 +44,7 @@ static const char *ctype_compute(int t) { return t == NBG_BOOL ? "long long" : c
 
 std::string Prog::signature() const {
     std::ostringstream s;
-    s << (spmv ? (tp ? "T" : "S") : "E") << (vec ? "v" : "s") << "|";
+    s << (spmv ? (tp ? "T" : (lpr ? "L" : "S")) : "E") << (vec ? "v" : "s") << "|";
     if (spmv) s << sp.add << "," << sp.mul << "," << sp.T << "," << sp.xt << "," << sp.at << "," << sp.has_vals << "|";
     for (const Ins &i : ins)
         s << (int)i.k << ":" << i.t << ":" << i.code << ":" << i.a << ":" << i.b << ":" << i.imm0 << ":" << i.imm1
@@ -769,6 +769,62 @@ SemiringCode semiring_code(const SpmvSig &sp) {
     return r;
 }
 
+// Lane-per-row SpMV skeleton (SURVEY 8(a) K4 notes, "low skew": max row <= 4 x mean, mean <= 32
+// entries, e.g. C3's Erdos-Renyi rows of 8-39 entries).  A warp takes 32 consecutive rows, lane j
+// row rb + j: the row's 4-entry groups two at a time (8 gathers in flight per lane), summed in
+// order (the same per-row order as the fused and the per-op mxv), then the fused epilogue straight
+// from registers -- no tasks, scans or shared memory.  Grid-stride over 32-row tiles; epilogue
+// reductions per thread, then the block finish of the elementwise skeleton.
+int gen_spmv_lpr(Gen &g, const std::string &kname) {
+    const Prog &p = g.p;
+    auto &o = g.o;
+    SemiringCode k = semiring_code(p.sp);
+    const bool zero_pad = p.sp.add == NBG_PLUS && !p.sp.has_vals && (p.sp.mul == NBG_SECOND || p.sp.mul == NBG_TIMES);
+    o << "#define NBG_ADD(A_, B_) " << k.ADD << "\n";
+    o << "__device__ __forceinline__ " << k.C << " nbg_mul(const KArgs &a, long long P_, " << k.XT << " X_) { return " << k.mul << "; }\n";
+    if (zero_pad)
+        o << "#define NBG_TV(C_, P_, V_) ((" << k.ACC << ")nbg_mul(a, (P_), ((C_) >= 0) ? (V_) : (" << k.XT << ")0))\n";
+    else
+        o << "#define NBG_TV(C_, P_, V_) (((C_) >= 0) ? (" << k.ACC << ")nbg_mul(a, (P_), (V_)) : (" << k.ACC << ")(" << k.IDENT << "))\n";
+    o << "#define NBG_G(C_) __ldg(X + ((C_) > 0 ? (C_) : 0))\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
+    o << "  __shared__ double nbg_sh[32];\n";
+    o << "  const int lane = threadIdx.x & 31;\n";
+    o << "  const " << k.XT << "* __restrict__ X = (const " << k.XT << "*)a.x;\n";
+    o << "  const int4* __restrict__ CG = (const int4*)a.colidx;\n";
+    o << "  const long long* __restrict__ GRP = a.rowptr;\n";
+    g.emit_uniform();
+    g.emit_red_decl();
+    o << "  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;\n";
+    o << "  for (long long rb = (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 5; rb < a.n; rb += nw << 5) {\n";
+    o << "    const long long i = rb + lane;\n";
+    o << "    if (i >= a.n) continue;\n";
+    o << "    const long long g1 = GRP[i + 1];\n";
+    o << "    " << k.ACC << " acc = " << k.IDENT << ";\n";
+    o << "    for (long long gg = GRP[i]; gg < g1; gg += 2) {\n";
+    o << "      const long long P_ = 4 * gg;\n";
+    o << "      const int4 ca = __ldcs(CG + gg);\n";
+    o << "      const int4 cb = (gg + 1 < g1) ? __ldcs(CG + gg + 1) : make_int4(-1, -1, -1, -1);\n";
+    o << "      const " << k.XT << " x0 = NBG_G(ca.x), x1 = NBG_G(ca.y), x2 = NBG_G(ca.z), x3 = NBG_G(ca.w);\n";
+    o << "      const " << k.XT << " x4 = NBG_G(cb.x), x5 = NBG_G(cb.y), x6 = NBG_G(cb.z), x7 = NBG_G(cb.w);\n";
+    o << "      acc = NBG_ADD(acc, NBG_TV(ca.x, P_, x0)); acc = NBG_ADD(acc, NBG_TV(ca.y, P_ + 1, x1));\n";
+    o << "      acc = NBG_ADD(acc, NBG_TV(ca.z, P_ + 2, x2)); acc = NBG_ADD(acc, NBG_TV(ca.w, P_ + 3, x3));\n";
+    o << "      if (gg + 1 < g1) {\n";
+    o << "        acc = NBG_ADD(acc, NBG_TV(cb.x, P_ + 4, x4)); acc = NBG_ADD(acc, NBG_TV(cb.y, P_ + 5, x5));\n";
+    o << "        acc = NBG_ADD(acc, NBG_TV(cb.z, P_ + 6, x6)); acc = NBG_ADD(acc, NBG_TV(cb.w, P_ + 7, x7));\n";
+    o << "      }\n";
+    o << "    }\n";
+    g.emit_body(
+        "    ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
+        [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    o << "  }\n";
+    g.emit_red_finish();
+    o << "}\n";
+    return 0;
+}
+
 // Phase 1: per-pair partial sums with the column block in shared memory.  The CTA walks its task
 // range block by block (loads the block's slice of x, then its warps claim the block's tasks); a
 // task is the single-pass row task on pairs instead of rows (same 64-group steps, lane-local split
@@ -1159,6 +1215,11 @@ bool spmv_gather_pipeline() {
     return v == 1;
 }
 
+int spmv_lpr_mode() {   // read at every region launch (the signature records the skeleton)
+    const char *e = getenv("NBG_SPMV_LPR");
+    return (e && *e) ? (e[0] == '1' ? 1 : 0) : -1;
+}
+
 int spmv_threads() {
     static int v = 0;
     if (!v) {
@@ -1179,6 +1240,8 @@ std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem, int 
     int smem = 0;
     if (p.spmv && p.tp)
         smem = gen_tp2(g, kname);
+    else if (p.spmv && p.lpr)
+        smem = gen_spmv_lpr(g, kname);
     else if (p.spmv)
         smem = gen_spmv(g, kname, hot_entries);
     else

@@ -6,6 +6,7 @@
 //   K3  spmv plan            merge-path row tiles + long-row chunks for the fused SpMV
 //                            (DESIGN.md "K4 SpMV"), built once per matrix
 // Integer work only: results are bit-exact and deterministic (histogram atomics are integer).
+#include <cmath>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
@@ -585,6 +586,17 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     NBG_CUDA(cudaMemcpyAsync(&G, (const long long *)P->grp->d + n, 8, cudaMemcpyDeviceToHost, c.stream));
     NBG_CUDA(cudaStreamSynchronize(c.stream));
     P->ngroups = G;
+    {   // degree skew (SURVEY 8(a) K4 notes): longest row in groups -> the lane-per-row variant
+        BufP mx = alloc_buf(c, 8);
+        size_t tbm = 0;
+        cub::DeviceReduce::Max(nullptr, tbm, (const long long *)ngb->d, (long long *)mx->d, (int64_t)n, c.stream);
+        BufP tm = alloc_buf(c, std::max<size_t>(tbm, 16));
+        NBG_CUDA(cub::DeviceReduce::Max(tm->d, tbm, (const long long *)ngb->d, (long long *)mx->d, (int64_t)n, c.stream));
+        NBG_CUDA(cudaMemcpyAsync(&P->max_row_groups, mx->d, 8, cudaMemcpyDeviceToHost, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+        const double mean_g = (double)G / (double)n;
+        P->low_skew = mean_g <= 8.0 && (double)P->max_row_groups <= 4.0 * std::ceil(mean_g);
+    }
     P->cg = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * 4);
     NBG_CUDA(cudaMemsetAsync(P->cg->d, 0xff, (size_t)std::max<long long>(4 * G, 4) * 4, c.stream));
     if (A.nnz > 0)

@@ -121,6 +121,8 @@ struct SpmvPlan {
     // warps; the warp that finishes a long row's last chunk (atomic ticket) combines the chunk
     // partials in chunk order and runs the epilogue.  DESIGN.md "K4 SpMV".
     int64_t ntiles = 0, nchunks = 0, nlong = 0, ngroups = 0;
+    int64_t max_row_groups = 0;   // longest row, in 4-entry groups
+    bool low_skew = false;        // max row <= 4 x mean and mean <= 32 entries: lane-per-row SpMV
     BufP grp;        // int64[n + 1]  first group of each row
     BufP cg;         // int32[4 * ngroups]  column index per padded position (gather layout), -1 = pad
     BufP vals_g;     // values per padded position (valued matrices only)
@@ -246,6 +248,7 @@ struct Prog {
     std::vector<RedOut> reds;
     bool spmv = false;
     bool tp = false;        // spmv through the two-phase plan: this program is phase 2 (combine + epilogue)
+    bool lpr = false;       // spmv, lane-per-row skeleton (low-skew matrices)
     bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
     SpmvSig sp;
     int n_in = 0, n_out = 0, n_imm = 0, n_sin = 0, n_red = 0;
@@ -409,7 +412,8 @@ void gpu_bitset_full(Ctx &c, int64_t n, uint32_t *bits);   // all n bits set, ta
 // codegen / jit
 bool spmv_gather_pipeline();   // SpMV gathers one step ahead (NBG_SPMV_GPIPE=1)
 bool spmv_epilogue_prefetch();  // SpMV prefetches the epilogue's row inputs at task start (NBG_SPMV_PF, default on)
-int spmv_threads();   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
+int spmv_threads();
+int spmv_lpr_mode();   // NBG_SPMV_LPR: -1 auto (by skew), 0 never, 1 always   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
 KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0);

@@ -608,6 +608,12 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
         // two-phase column-blocked plan (large relabelled matrices, 4/8-byte gathered elements)
         TpPlan *T = (!A.vals && n > 0) ? gpu_tp_plan(c, A, (int)type_size(u->type), c.num_sms) : nullptr;
+        // lane-per-row skeleton for low-skew matrices (SURVEY 8(a) K4 notes), NBG_SPMV_LPR overrides
+        const int lm = spmv_lpr_mode();
+        if (!T && (lm == 1 || (lm == -1 && A.plan->low_skew))) {
+            p.lpr = true;
+            items = (n + 255) / 256;
+        }
         if (T) {
             p.tp = true;
             args.rowslot = (const long long *)T->rowslot->d;
@@ -664,10 +670,10 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     auto it = c.plans.find(sig);
     if (it == c.plans.end()) {
         char nm[48];
-        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? "spmv" : "ewise"), (unsigned long long)hash_str(sig));
+        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? (p.lpr ? "spmvl" : "spmv") : "ewise"), (unsigned long long)hash_str(sig));
         int smem = 0, hot = 0;
         std::string src = codegen(p, nm, &smem, &hot);
-        kern = jit_compile(c, src, nm, p.spmv && !p.tp, smem);
+        kern = jit_compile(c, src, nm, p.spmv && !p.tp && !p.lpr, smem);
         kern->hot = hot;
         c.plans[sig] = kern;
         c.stats.plans_built++;

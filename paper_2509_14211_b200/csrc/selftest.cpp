@@ -97,6 +97,10 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
             p.n_in = 2; p.n_out = 2; p.n_imm = 4; p.n_sin = 1; p.n_red = 2;
             std::string nm = std::string("selftest_pr_") + (T == NBG_FP32 ? "f32" : "f64");
             if (!compile_only(codegen(p, nm), nm, log)) fails++;
+            p.lpr = true;
+            p.outs[1].scatter = true;        // y_next written in the gather layout (side output)
+            nm += "_lpr";
+            if (!compile_only(codegen(p, nm), nm, log)) fails++;
         }
         // (3) plain mxv for every monoid x type x mul, iso and valued matrices
         int k = 0;
@@ -114,6 +118,19 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
                         std::string nm = "selftest_mxv_" + std::to_string(k++);
                         if (!compile_only(codegen(p, nm), nm, log)) fails++;
                     }
+        // (3b) the lane-per-row skeleton for the same semirings (low-skew matrices)
+        for (int add : {NBG_PLUS, NBG_MIN, NBG_MAX})
+            for (int T : {NBG_INT32, NBG_FP32, NBG_FP64}) {
+                Prog p;
+                p.spmv = true;
+                p.lpr = true;
+                p.sp.add = add; p.sp.mul = NBG_TIMES; p.sp.T = T; p.sp.xt = T; p.sp.at = NBG_FP32; p.sp.has_vals = add != NBG_PLUS;
+                p.ins.push_back(I(Ins::MXV_ACC, T));
+                p.outs.push_back(OutV{0, 0});
+                p.n_out = 1; p.n_imm = 2;
+                std::string nm = "selftest_mxvl_" + std::to_string(k++);
+                if (!compile_only(codegen(p, nm), nm, log)) fails++;
+            }
         // (4) reductions of every kind
         for (int T : {NBG_INT32, NBG_INT64, NBG_FP32, NBG_FP64})
             for (int mono : {NBG_PLUS, NBG_MIN, NBG_MAX}) {

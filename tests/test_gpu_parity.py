@@ -368,3 +368,37 @@ def test_two_phase_matches_oracle(nbg, T, monkeypatch):
         assert delta_close(runs[0][1], dho, ro, npT)
     finally:
         nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("kind,scale,force", [("er", 12, None), ("er", 12, "0"), ("rmat", 12, "1"), ("rmat", 10, "1")])
+def test_lane_per_row_spmv(nbg, monkeypatch, kind, scale, force):
+    """The lane-per-row SpMV skeleton (low-skew matrices) -- chosen by skew for ER,
+    forced on skewed R-MAT -- against the oracle, fused (nonblocking) and per-op (blocking)
+    results identical for fp32 and within 1e-15 for fp64 (P9), both dangling variants."""
+    if force is None:
+        monkeypatch.delenv("NBG_SPMV_LPR", raising=False)
+    else:
+        monkeypatch.setenv("NBG_SPMV_LPR", force)
+    g = nbg.GRAPH_ER if kind == "er" else nbg.GRAPH_RMAT
+    res = {}
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            A, deg = nbg.nbg_matrix_from_generator(c, g, scale, 16, 2)
+            rp, ci = nbg.nbg_matrix_export_csr(c, A)
+            d = nbg.nbg_vector_export_dense(c, deg)
+            for T, tol in (("fp32", 1e-5), ("fp64", 1e-10)):
+                for dang in (nbg.PR_UNIFORM, nbg.PR_DROP):
+                    r, s, h = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=12, dangling=dang, type=nbg.TYPE_OF[T])
+                    v = nbg.nbg_vector_export_dense(c, r)
+                    ro, so, dho, _ = oracle.pagerank(rp, ci, d, dtype=nbg.NP_OF[nbg.TYPE_OF[T]], itermax=12,
+                                                     uniform=dang == nbg.PR_UNIFORM)
+                    assert s == so == 12
+                    assert rel(v, ro) <= tol
+                    res[(mode, T, dang)] = v
+        finally:
+            nbg.nbg_finalize(c)
+    for dang in (nbg.PR_UNIFORM, nbg.PR_DROP):
+        assert np.array_equal(res[(nbg.NONBLOCKING, "fp32", dang)], res[(nbg.BLOCKING, "fp32", dang)])
+        # fp64: the dangling sum's last bit may differ (see test_blocking_equals_nonblocking_bitwise)
+        assert rel(res[(nbg.NONBLOCKING, "fp64", dang)], res[(nbg.BLOCKING, "fp64", dang)]) <= 1e-15
