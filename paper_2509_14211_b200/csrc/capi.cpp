@@ -135,7 +135,7 @@ static NodeP rec_bind2nd(Ctx &c, int type, const nbg_binop &bo, const NodeP &u, 
     return x;
 }
 
-static double monoid_identity(int monoid, int type) {
+double nbg::monoid_identity(int monoid, int type) {
     if (monoid == NBG_PLUS) return 0.0;
     if (is_float(type)) return monoid == NBG_MIN ? INFINITY : -INFINITY;
     if (type == NBG_INT32) return monoid == NBG_MIN ? 2147483647.0 : -2147483648.0;

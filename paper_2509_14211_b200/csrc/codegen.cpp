@@ -1102,6 +1102,9 @@ std::string codegen_structured(const SProg &sp, const std::string &kname) {
                 if (lk == 0) {
                     o << ind << "const bool " << pk << " = true;\n";
                     o << ind << "const " << T << " " << vk << " = " << vals << "[ic];\n";
+                } else if (lk == 3) {   // an empty operand: never present
+                    o << ind << "const bool " << pk << " = false;\n";
+                    o << ind << "const " << T << " " << vk << " = (" << T << ")0;\n";
                 } else if (lk == 1) {
                     o << ind << "const bool " << pk << " = ((((const unsigned*)a.in[" << NI + in.slot << "])[ic >> 5]) >> (ic & 31)) & 1u;\n";
                     o << ind << "const " << T << " " << vk << " = " << vals << "[ic];\n";

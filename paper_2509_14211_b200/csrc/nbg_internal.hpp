@@ -434,6 +434,7 @@ void host_xacc_add(unsigned long long *limbs, double d);
 double host_unop(int code, int t, double x, double c0, double c1);
 double host_binop(int code, int t, double x, double y, double c0);
 double host_round(int t, double v);
+double monoid_identity(int monoid, int type);   // identity of PLUS / MIN / MAX in type
 uint64_t hash_str(const std::string &s);
 
 double now_ns();

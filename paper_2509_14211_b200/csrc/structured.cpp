@@ -17,6 +17,7 @@
 //     bitset above it.
 // The estimators only select the loop and the representation; values never depend on them.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -35,7 +36,8 @@ bool structured_kind(VKind k) { return k == VKind::SPARSE || k == VKind::BITSET;
 
 static bool reaches_structured(const Node *x, std::unordered_set<const Node *> &seen) {
     if (!seen.insert(x).second) return false;
-    if (x->mat) return !x->scalar && structured_kind(x->kind);
+    // an EMPTY leaf here is a pending structured result that materialised with no entries
+    if (x->mat) return !x->scalar && (structured_kind(x->kind) || x->kind == VKind::EMPTY);
     switch (x->op) {
         case Op::APPLY:
         case Op::BIND2ND: return reaches_structured(x->a.get(), seen);
@@ -51,7 +53,7 @@ bool needs_structured(const NodeP &r) {
     if (r->op == Op::REDUCE) return reaches_structured(r->a.get(), seen);
     if (r->op == Op::MXV) {
         const Node *u = r->a.get();
-        return u->mat && !u->scalar && structured_kind(u->kind);
+        return u->mat && !u->scalar && (structured_kind(u->kind) || u->kind == VKind::EMPTY);
     }
     if (r->scalar) return false;
     return reaches_structured(r.get(), seen);
@@ -110,7 +112,7 @@ bool static_full(const Node *x) {
 bool cover(const Node *x, std::vector<const Node *> &out) {
     if (x->mat) {
         if (!x->scalar && x->kind == VKind::SPARSE) { out.push_back(x); return true; }
-        return false;
+        return !x->scalar && x->kind == VKind::EMPTY;   // no entries: covered by nothing
     }
     switch (x->op) {
         case Op::APPLY:
@@ -191,7 +193,10 @@ struct SBuilder {
                 uint8_t lk = 0;
                 const void *aux = nullptr;
                 const void *vals = x->buf ? x->buf->d : nullptr;
-                if (x->kind == VKind::BITSET) {
+                if (x->kind == VKind::EMPTY) {
+                    lk = 3;                  // never present
+                    vals = nullptr;
+                } else if (x->kind == VKind::BITSET) {
                     lk = 1;
                     aux = x->bits->d;
                 } else if (x->kind == VKind::SPARSE) {
@@ -294,6 +299,11 @@ void materialize_smxv(Ctx &c, const NodeP &r) {
     if (u->kind == VKind::BITSET) {
         bits = u->bits;
         dense = u->buf;
+    } else if (u->kind == VKind::EMPTY) {   // no x entry present: every row is the identity
+        bits = alloc_buf(c, (size_t)std::max<int64_t>((u->n + 31) / 32, 1) * 4);
+        dense = alloc_buf(c, (size_t)std::max<int64_t>(u->n, 1) * type_size(u->type));
+        NBG_CUDA(cudaMemsetAsync(bits->d, 0, bits->bytes, c.stream));
+        NBG_CUDA(cudaMemsetAsync(dense->d, 0, dense->bytes, c.stream));
     } else {
         bits = alloc_buf(c, (size_t)((u->n + 31) / 32) * 4);
         dense = alloc_buf(c, (size_t)u->n * type_size(u->type));
@@ -465,6 +475,17 @@ void materialize_structured(Ctx &c, const NodeP &r) {
         a.rowptr = (const long long *)(drv ? drv->d : nullptr);
         a.nnz = m;
         if (m > 0) launch(c, *k, a, (m + 255) / 256, "ewise");
+        else if (!vec_out) {          // no entry can be present: the monoid identity
+            r->mat = true;
+            r->sfmt = SFmt::HOST;
+            r->hval = monoid_identity(r->code, r->type);
+            r->hval = host_round(r->type, r->hval);
+            drop(*r);
+            c.stats.structured_regions++;
+            c.stats.structured_index_loops++;
+            c.stats.waits++;
+            return;
+        }
     } else if (n > 0) {
         launch(c, *k, a, (n + 255) / 256, "ewise");
     }

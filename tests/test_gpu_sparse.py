@@ -182,3 +182,28 @@ def test_empty_and_disjoint(nbg):
         assert list(i) == [0, 1, 2, 3, 4, 5] and np.all(v == 1)
     finally:
         nbg.nbg_finalize(c)
+
+
+def test_pending_result_materialised_empty(nbg):
+    """A pending structured node that materialises with no entries, used afterwards by operations
+    recorded before it was materialised (empty operand inside a region, reduce of it, mxv of it)."""
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        n = 1024
+        a = put(nbg, c, nbg.FP32, S.sparse(n, [1, 3, 5], np.ones(3, np.float32)))
+        b = put(nbg, c, nbg.FP32, S.sparse(n, [0, 2, 4], np.ones(3, np.float32)))
+        f = nbg.nbg_vector_from_dense(c, nbg.FP32, np.full(n, 2.0, np.float32))
+        m = nbg.nbg_ewise_mult(c, nbg.FP32, "TIMES", a, b)             # empty, still pending
+        u = nbg.nbg_ewise_add(c, nbg.FP32, "PLUS", m, b)               # recorded on the pending m
+        w = nbg.nbg_ewise_mult(c, nbg.FP32, "TIMES", m, f)
+        s = nbg.nbg_reduce(c, nbg.FP32, "MIN", m)
+        A, _ = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_ER, 10, 4, 1)
+        y = nbg.nbg_mxv(c, nbg.FP32, "PLUS", "TIMES", A, m)
+        assert nbg.nbg_vector_format(c, m) == nbg.FORMAT_EMPTY         # m materialised now
+        i, v = nbg.nbg_vector_export_sparse(c, u)
+        assert list(i) == [0, 2, 4] and np.all(v == 1)
+        assert nbg.nbg_vector_nvals(c, w) == 0
+        assert nbg.nbg_scalar_get(c, s) == np.inf
+        assert np.all(nbg.nbg_vector_export_dense(c, y) == 0)
+    finally:
+        nbg.nbg_finalize(c)
