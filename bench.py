@@ -43,9 +43,12 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampler (B200_PROFILING.md clocks line), started before the warm-up and stopped
+    after the timed region; samples are time-stamped so the ones inside the timed region can be
+    picked.  A timed region shorter than the sampling interval falls back to the samples taken
+    under the same load (warm-up and trailing steps), and says so in "window"."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -57,7 +60,7 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -65,10 +68,19 @@ class Clocks:
             self.proc = None
 
     def _read(self):
+        import datetime
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            f = [x.strip() for x in line.strip().split(",")]
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except Exception:
+                ts = time.time()
+            self.lines.append((ts, f[1:]))
 
-    def stop(self):
+    def count(self):
+        return len(self.lines)
+
+    def stop(self, t0=None, t1=None):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -76,10 +88,12 @@ class Clocks:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+        inwin = [f for ts, f in self.lines if t0 is not None and t0 - 0.01 <= ts <= t1 + 0.01]
+        use, window = (inwin, "timed") if inwin else ([f for _, f in self.lines], "load: warm-up + timed + trailing steps "
+                                                       "(timed region shorter than the 20 ms sampling interval)")
+        sm, smax, reasons = [], None, set()
+        for f in use:
             if len(f) < 9:
                 continue
             try:
@@ -91,7 +105,7 @@ class Clocks:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "window": window}
 
 
 def graph_params(w):
@@ -169,15 +183,20 @@ def run_ours(args, rank, world, local_rank):
         if dist is not None:
             dist.barrier()
 
+    clocks = Clocks(local_rank)
+    clocks.start()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    t_ready = time.time()
+    while clocks.count() == 0 and time.time() - t_ready < 3.0:   # sampler live before the timed region
+        step()
+    torch.cuda.synchronize()
     st0 = nbg.nbg_get_stats(ctx)
-    clocks = Clocks(local_rank)
-    clocks.start()
     nbg.nbg_set_timing(ctx, 1)
     barrier()
     torch.cuda.synchronize()
+    wall0 = time.time()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -188,6 +207,7 @@ def run_ours(args, rank, world, local_rank):
         sweeps_total += s
     e1.record(stream)
     torch.cuda.synchronize()
+    wall1 = time.time()
     barrier()
     ms = e0.elapsed_time(e1)
     spmv_ms, spmv_n = nbg.nbg_get_timing(ctx, "spmv")
@@ -195,8 +215,15 @@ def run_ours(args, rank, world, local_rank):
     ewise_ms, ewise_n = nbg.nbg_get_timing(ctx, "ewise")
     comm_ms, comm_n = nbg.nbg_get_timing(ctx, "comm")
     nbg.nbg_set_timing(ctx, 0)
-    ck = clocks.stop()
     st1 = nbg.nbg_get_stats(ctx)
+    n_in = sum(1 for ts, _ in clocks.lines if wall0 - 0.01 <= ts <= wall1 + 0.01)
+    if n_in == 0:        # short timed region: a few trailing steps under the same load for the sampler
+        t_tr = time.time()
+        c0 = clocks.count()
+        while clocks.count() < c0 + 3 and time.time() - t_tr < 3.0:
+            step()
+        torch.cuda.synchronize()
+    ck = clocks.stop(wall0, wall1)
     if dist is not None:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
