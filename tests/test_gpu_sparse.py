@@ -207,3 +207,38 @@ def test_pending_result_materialised_empty(nbg):
         assert np.all(nbg.nbg_vector_export_dense(c, y) == 0)
     finally:
         nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("mode", ["BLOCKING", "NONBLOCKING"])
+@pytest.mark.parametrize("tname", ["fp64", "int64"])
+def test_bitset_operands_chain(nbg, mode, tname):
+    """Results kept as bitsets (fill above 1/16) feeding later regions: a bitset operand in the
+    index loop (bit test at the driver's indices) and in the full-range loop, user-held
+    intermediates, int64 values."""
+    T = {"fp64": np.float64, "int64": np.int64}[tname]
+    t = nbg.TYPE_OF[tname]
+    rng = np.random.default_rng(21)
+    u, v, w = rsv(rng, N, 0.3, T), rsv(rng, N, 0.35, T), rsv(rng, N, 0.01, T)
+    c = nbg.nbg_init(getattr(nbg, mode), 0)
+    try:
+        du, dv, dw = put(nbg, c, t, u), put(nbg, c, t, v), put(nbg, c, t, w)
+        b = nbg.nbg_ewise_add(c, t, "MIN", du, dv)                          # fill ~0.55: bitset
+        eb = S.ewise_add("MIN", u, v, T)
+        same(get(nbg, c, b, N), eb)
+        assert nbg.nbg_vector_format(c, b) == nbg.FORMAT_BITSET
+        m = nbg.nbg_ewise_mult(c, t, "PLUS", b, dw)                         # driven by w (1 %)
+        e = nbg.nbg_apply(c, t, "AINV", b)
+        x = nbg.nbg_ewise_add(c, t, "MAX", e, dw)
+        s = nbg.nbg_reduce(c, nbg.INT64 if tname == "int64" else nbg.FP64, "PLUS", b)
+        same(get(nbg, c, m, N), S.ewise_mult("PLUS", eb, w, T))
+        ee = S.apply("AINV", eb, T)
+        same(get(nbg, c, e, N), ee)
+        same(get(nbg, c, x, N), S.ewise_add("MAX", ee, w, T))
+        exp = S.reduce("PLUS", eb, np.int64 if tname == "int64" else np.float64)
+        got = nbg.nbg_scalar_get(c, s)
+        if tname == "int64":
+            assert got == exp
+        else:
+            assert abs(got - exp) <= 1e-12 * float(np.abs(eb.vals).sum())
+    finally:
+        nbg.nbg_finalize(c)
