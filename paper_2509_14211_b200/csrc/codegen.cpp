@@ -343,10 +343,12 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
         // 4 grid-stride iterations per trip: all 16-byte loads of the trip are issued before any
         // use, so every thread keeps 4 loads per input in flight (memory-level parallelism)
         o << "  const long long nv = n >> 2;\n  tail0 = nv << 2;\n";
-        o << "  for (long long vb_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv; vb_ += 4 * stride) {\n";
+        const char *eu = getenv("NBG_EWISE_UNROLL");
+        const int U = (eu && (eu[0] == '1' || eu[0] == '2' || eu[0] == '4' || eu[0] == '8')) ? eu[0] - '0' : 1;
+        o << "  for (long long vb_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv; vb_ += " << U << " * stride) {\n";
         for (int s = 0; s < p.n_in; s++)
-            if (slot_type[s] >= 0) o << "    " << ctype(slot_type[s]) << " L" << s << "[4][4];\n";
-        o << "    #pragma unroll\n    for (int u = 0; u < 4; u++) {\n";
+            if (slot_type[s] >= 0) o << "    " << ctype(slot_type[s]) << " L" << s << "[" << U << "][4];\n";
+        o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
         o << "      const long long vi = vb_ + u * stride;\n";
         o << "      if (vi < nv) {\n";
         for (int s = 0; s < p.n_in; s++)
@@ -354,7 +356,7 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
                 o << "        " << vload(slot_type[s], "a.in[" + std::to_string(s) + "]", "vi", "L" + std::to_string(s) + "[u]") << "\n";
         o << "      }\n";
         o << "    }\n";
-        o << "    #pragma unroll\n    for (int u = 0; u < 4; u++) {\n";
+        o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
         o << "      const long long vi = vb_ + u * stride;\n";
         o << "      if (vi >= nv) break;\n";
         for (int k = 0; k < p.n_out; k++)
