@@ -202,14 +202,19 @@ def run_ours(args, rank, world, local_rank):
     e0.record(stream)
     sweeps_total = 0
     hist_last = None
+    marks = [e0]
     for _ in range(args.steps):
         s, hist_last = step()
         sweeps_total += s
+        ev = torch.cuda.Event(enable_timing=True)      # per-step marks (mean / median)
+        ev.record(stream)
+        marks.append(ev)
     e1.record(stream)
     torch.cuda.synchronize()
     wall1 = time.time()
     barrier()
     ms = e0.elapsed_time(e1)
+    step_ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(len(marks) - 1)]
     spmv_ms, spmv_n = nbg.nbg_get_timing(ctx, "spmv")
     p2_ms, p2_n = nbg.nbg_get_timing(ctx, "spmv_p2")      # phase 2 of the two-phase SpMV (0 launches single-pass)
     ewise_ms, ewise_n = nbg.nbg_get_timing(ctx, "ewise")
@@ -285,6 +290,8 @@ def run_ours(args, rank, world, local_rank):
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 4),
+            "step_ms": {"mean": round(statistics.mean(step_ms), 4), "median": round(statistics.median(step_ms), 4),
+                        "min": round(min(step_ms), 4), "max": round(max(step_ms), 4)},
             "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None,
@@ -512,6 +519,16 @@ def oracle_sample(rp, ci, deg, cfg, sweeps):
     return time.perf_counter() - t0
 
 
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def cpu_baseline(args):
     cfg = graph_params(args.workload)
     rp, ci, deg = oracle_graph(cfg, args.seed, args.mtx)
@@ -519,6 +536,7 @@ def cpu_baseline(args):
     sweeps = max(1, min(cfg["itermax"], int(args.cpu_sweeps)))
     t = oracle_sample(rp, ci, deg, cfg, sweeps)
     return {"value": round(nnz * sweeps / t / 1e9, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "cpu": cpu_model(), "host_cores_available": os.cpu_count(),
             "sample": f"{sweeps} fixed Fig. 6 sweeps of the single-threaded C oracle on the same graph "
                       f"({nnz} edges), {t:.2f} s"}
 
@@ -543,7 +561,7 @@ def run_reference(args, rank, world):
         "data": f"file {os.path.basename(args.mtx)}" if args.mtx else "synthetic", "impl": "reference",
         "config": {"workload": workload_name(args, cfg), "n": int(rp.shape[0] - 1), "nnz": nnz,
                    "step": f"{per} fixed sweeps of the CPU oracle (bounded sample of the workload)"},
-        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": round(value, 5), "unit": "GTEPS", "cores": 1, "kind": "oracle", "cpu": cpu_model(),
                          "sample": f"{per} sweeps x {args.steps} steps, single-threaded C oracle"},
         "e2e": {"value": round(value, 5), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
