@@ -454,8 +454,8 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     const int warp_bytes = 128 * 8 + 32 * 4;                  // row totals of the task + row-start bitmask
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
-    const int NT = spmv_threads(), NW = NT / 32;
-    int hot_bytes = 128 * 1024;   // measured: 96-128 KB best; above ~190 KB of total smem the L1 collapses
+    const int NT = spmv_threads((int)type_size(sp.xt)), NW = NT / 32;
+    int hot_bytes = 144 * 1024;   // measured: 96-128 KB best; above ~190 KB of total smem the L1 collapses
     if (const char *e = getenv("NBG_SPMV_HOT_KB")) if (*e) hot_bytes = std::max(0, std::min(200, atoi(e))) * 1024;
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
@@ -834,7 +834,7 @@ int gen_spmv_lpr(Gen &g, const std::string &kname) {
 // Chunks of a long pair: the chunk total to partials[], the last chunk (ticket) combines in order.
 std::string gen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {
     SemiringCode k = semiring_code(sp);
-    const int NT = spmv_threads(), NW = NT / 32;
+    const int NT = spmv_threads(xsize), NW = NT / 32;
     const long long slice = (S * xsize + 15) / 16 * 16;
     const int dyn = (int)slice + NW * 128 * 8;
     if (dyn_smem) *dyn_smem = dyn;
@@ -1225,14 +1225,16 @@ int spmv_lpr_mode() {   // read at every region launch (the signature records th
     return (e && *e) ? (e[0] == '1' ? 1 : 0) : -1;
 }
 
-int spmv_threads() {
-    static int v = 0;
-    if (!v) {
+int spmv_threads(int xsize) {
+    // measured (DESIGN.md §7 sweep): 1024 threads for 4-byte gathered elements; 8-byte ones spill
+    // at the 64-register cap of 1024 threads, so 768
+    static int v = -1;
+    if (v < 0) {
         const char *e = getenv("NBG_SPMV_THREADS");
-        v = (e && *e) ? atoi(e) : 768;
-        if (v != 256 && v != 512 && v != 640 && v != 768 && v != 1024) v = 768;
+        v = (e && *e) ? atoi(e) : 0;
+        if (v != 0 && v != 256 && v != 512 && v != 640 && v != 768 && v != 1024) v = 0;
     }
-    return v;
+    return v ? v : (xsize <= 4 ? 1024 : 768);
 }
 
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {

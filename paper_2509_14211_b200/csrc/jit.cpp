@@ -83,7 +83,7 @@ static std::string nvrtc_compile(Ctx &c, const std::string &src, const std::stri
     return cubin;
 }
 
-KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem) {
+KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem, int block) {
     const char *dump = getenv("NBG_JIT_DUMP");
     if (dump && *dump) write_file(std::string(dump) + "/" + kname + ".cu", src);
     std::string cubin = nvrtc_compile(c, src, kname);
@@ -91,7 +91,7 @@ KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bo
     k->name = kname;
     NBG_CUDA(cudaLibraryLoadData(&k->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     NBG_CUDA(cudaLibraryGetKernel(&k->k, k->lib, kname.c_str()));
-    k->block = spmv ? spmv_threads() : 256;
+    k->block = block > 0 ? block : (spmv ? spmv_threads(4) : 256);
     k->smem = dyn_smem;
     if (dyn_smem > 48 * 1024)
         NBG_CUDA(cudaFuncSetAttribute((const void *)k->k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem));

@@ -279,13 +279,13 @@ __device__ __forceinline__ int nbg_ld_stream(const int *p) { return __ldcs(p); }
 // caller passes c >= 0 (padding positions are clamped to 0 and masked out afterwards).
 __device__ __forceinline__ unsigned nbg_gx32(unsigned sbase, const void *X, int c, int hc) {
     unsigned r;
-    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b32 %0, [%3]; @!p ld.global.nc.b32 %0, [%4]; }"
+    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b32 %0, [%3]; @!p ld.global.cg.b32 %0, [%4]; }"
         : "=r"(r) : "r"(c), "r"(hc), "r"(sbase + 4u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned *)X + c));
     return r;
 }
 __device__ __forceinline__ unsigned long long nbg_gx64(unsigned sbase, const void *X, int c, int hc) {
     unsigned long long r;
-    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b64 %0, [%3]; @!p ld.global.nc.b64 %0, [%4]; }"
+    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b64 %0, [%3]; @!p ld.global.cg.b64 %0, [%4]; }"
         : "=l"(r) : "r"(c), "r"(hc), "r"(sbase + 8u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned long long *)X + c));
     return r;
 }

@@ -412,11 +412,11 @@ void gpu_bitset_full(Ctx &c, int64_t n, uint32_t *bits);   // all n bits set, ta
 // codegen / jit
 bool spmv_gather_pipeline();   // SpMV gathers one step ahead (NBG_SPMV_GPIPE=1)
 bool spmv_epilogue_prefetch();  // SpMV prefetches the epilogue's row inputs at task start (NBG_SPMV_PF, default on)
-int spmv_threads();
+int spmv_threads(int xsize);   // threads per SpMV CTA for a gathered element size (NBG_SPMV_THREADS overrides)
 int spmv_lpr_mode();   // NBG_SPMV_LPR: -1 auto (by skew), 0 never, 1 always   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
-KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0);
+KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0, int block = 0);
 void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);
 
 // graph (graph.cu)

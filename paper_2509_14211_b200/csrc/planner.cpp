@@ -602,7 +602,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.partials = (double *)(A.plan->partials ? A.plan->partials->d : nullptr);
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
-        const long long nw = spmv_threads() / 32;
+        const long long nw = spmv_threads((int)type_size(u->type)) / 32;
         items = (A.plan->ntiles + A.plan->nchunks + nw - 1) / nw;   // one task per warp
         args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
@@ -631,7 +631,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         TpPlan *T = gpu_tp_plan(c, A, (int)type_size(p.sp.xt), c.num_sms);
         std::ostringstream k1;
         k1 << "TP1|" << p.sp.add << "," << p.sp.mul << "," << p.sp.T << "," << p.sp.xt << "," << p.sp.at << "|" << T->S << "|"
-           << spmv_threads();
+           << spmv_threads((int)type_size(p.sp.xt));
         KernelP kp1;
         auto it1 = c.plans.find(k1.str());
         if (it1 == c.plans.end()) {
@@ -639,7 +639,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             snprintf(nm, sizeof nm, "nbg_tp1_%016llx", (unsigned long long)hash_str(k1.str()));
             int smem = 0;
             std::string src = codegen_tp1(p.sp, nm, (int)type_size(p.sp.xt), T->S, &smem);
-            kp1 = jit_compile(c, src, nm, true, smem);
+            kp1 = jit_compile(c, src, nm, true, smem, spmv_threads((int)type_size(p.sp.xt)));
             c.plans[k1.str()] = kp1;
             c.stats.plans_built++;
         } else {
@@ -673,7 +673,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? (p.lpr ? "spmvl" : "spmv") : "ewise"), (unsigned long long)hash_str(sig));
         int smem = 0, hot = 0;
         std::string src = codegen(p, nm, &smem, &hot);
-        kern = jit_compile(c, src, nm, p.spmv && !p.tp && !p.lpr, smem);
+        kern = jit_compile(c, src, nm, p.spmv && !p.tp && !p.lpr, smem, (p.spmv && !p.tp && !p.lpr) ? spmv_threads((int)type_size(p.sp.xt)) : 0);
         kern->hot = hot;
         c.plans[sig] = kern;
         c.stats.plans_built++;
