@@ -44,7 +44,7 @@ static const char *ctype_compute(int t) { return t == NBG_BOOL ? "long long" : c
 
 std::string Prog::signature() const {
     std::ostringstream s;
-    s << (spmv ? (tp ? "T" : (lpr ? "L" : "S")) : "E") << (vec ? "v" : "s") << "|";
+    s << (spmv ? (tp ? "T" : (lpr ? "L" : "S")) : "E") << (vec ? "v" : "s") << nt << "," << hot_kb << "|";
     if (spmv) s << sp.add << "," << sp.mul << "," << sp.T << "," << sp.xt << "," << sp.at << "," << sp.has_vals << "|";
     for (const Ins &i : ins)
         s << (int)i.k << ":" << i.t << ":" << i.code << ":" << i.a << ":" << i.b << ":" << i.imm0 << ":" << i.imm1
@@ -454,9 +454,10 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     const int warp_bytes = 128 * 8 + 32 * 4;                  // row totals of the task + row-start bitmask
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
-    const int NT = spmv_threads((int)type_size(sp.xt)), NW = NT / 32;
-    int hot_bytes = 144 * 1024;   // measured: 96-128 KB best; above ~190 KB of total smem the L1 collapses
-    if (const char *e = getenv("NBG_SPMV_HOT_KB")) if (*e) hot_bytes = std::max(0, std::min(200, atoi(e))) * 1024;
+    int nt_ = p.nt, hk_ = p.hot_kb;
+    if (nt_ <= 0) spmv_variant((int)type_size(sp.xt), 0, &nt_, &hk_);
+    const int NT = nt_, NW = NT / 32;
+    int hot_bytes = hk_ * 1024;
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
     const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
@@ -465,11 +466,13 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     (void)accw;
     // gathered element: predicated shared/global load of the raw bits, reinterpreted as XT
     std::string gx;
+    const char *ecold = getenv("NBG_SPMV_COLD");
+    const std::string sfx = (ecold && std::string(ecold) == "nc") ? "nc" : "";
     switch (sp.xt) {
-        case NBG_FP32: gx = "__uint_as_float(nbg_gx32(s_base, X, C_, hc))"; break;
-        case NBG_INT32: gx = "((int)nbg_gx32(s_base, X, C_, hc))"; break;
-        case NBG_FP64: gx = "__longlong_as_double((long long)nbg_gx64(s_base, X, C_, hc))"; break;
-        case NBG_INT64: gx = "((long long)nbg_gx64(s_base, X, C_, hc))"; break;
+        case NBG_FP32: gx = "__uint_as_float(nbg_gx32" + sfx + "(s_base, X, C_, hc))"; break;
+        case NBG_INT32: gx = "((int)nbg_gx32" + sfx + "(s_base, X, C_, hc))"; break;
+        case NBG_FP64: gx = "__longlong_as_double((long long)nbg_gx64" + sfx + "(s_base, X, C_, hc))"; break;
+        case NBG_INT64: gx = "((long long)nbg_gx64" + sfx + "(s_base, X, C_, hc))"; break;
         default: gx = "((C_) < hc ? s_hot[(C_)] : X[(C_)])"; break;
     }
 
@@ -1235,6 +1238,26 @@ int spmv_threads(int xsize) {
         if (v != 0 && v != 256 && v != 512 && v != 640 && v != 768 && v != 1024) v = 0;
     }
     return v ? v : (xsize <= 4 ? 1024 : 768);
+}
+
+// Launch shape of the task skeleton (DESIGN.md §7 "L2-only cold gathers"): 1024 threads for 4-byte
+// gathered elements (768 for 8-byte ones: spills); the hot cache is 144 KB when the gathered
+// vector stays L2-resident (C4: 16.8 MB) and 80 KB when it does not (C5: 108 MB), because then the
+// L1 left beside it (the shared-memory carveout steps at 132 / 164 / 196 KB) is worth more than
+// hot entries: C5 3.91 ms per sweep at 80 KB vs 4.55 ms at 96 KB and 5.79 ms at 144 KB.
+// NBG_SPMV_THREADS / NBG_SPMV_HOT_KB override both.
+void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb) {
+    const bool resident = gathered_bytes <= (48ll << 20);
+    static int et = -1, eh = -2;
+    if (et < 0) {
+        const char *e = getenv("NBG_SPMV_THREADS");
+        et = (e && *e) ? atoi(e) : 0;
+        if (et != 0 && et != 256 && et != 512 && et != 640 && et != 768 && et != 1024) et = 0;
+        const char *h = getenv("NBG_SPMV_HOT_KB");
+        eh = (h && *h) ? std::max(0, std::min(200, atoi(h))) : -1;
+    }
+    *nt = et ? et : (xsize <= 4 ? 1024 : 768);
+    *hot_kb = eh >= 0 ? eh : (resident ? 144 : 80);
 }
 
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {

@@ -274,13 +274,27 @@ __device__ void nbg_block_finish_i(long long v, int kind, u64 *acc, double *sh) 
 __device__ __forceinline__ int nbg_ld_stream(const int *p) { return __ldcs(p); }
 
 // ------------------------------------------------------------------ SpMV gathers
-// x[c] from the shared-memory hot-column cache when c < hc, else from global memory through the
-// read-only path; both loads are predicated (no divergent branch per gathered element).  The
+// x[c] from the shared-memory hot-column cache when c < hc, else from global memory cached in L2
+// only (ld.global.cg); both loads are predicated (no divergent branch per element).  The
 // caller passes c >= 0 (padding positions are clamped to 0 and masked out afterwards).
 __device__ __forceinline__ unsigned nbg_gx32(unsigned sbase, const void *X, int c, int hc) {
     unsigned r;
     asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b32 %0, [%3]; @!p ld.global.cg.b32 %0, [%4]; }"
         : "=r"(r) : "r"(c), "r"(hc), "r"(sbase + 4u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned *)X + c));
+    return r;
+}
+// the same through the read-only path with L1 allocation (matrices whose gathered vector does not
+// stay L2-resident keep the L1 hits)
+__device__ __forceinline__ unsigned nbg_gx32nc(unsigned sbase, const void *X, int c, int hc) {
+    unsigned r;
+    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b32 %0, [%3]; @!p ld.global.nc.b32 %0, [%4]; }"
+        : "=r"(r) : "r"(c), "r"(hc), "r"(sbase + 4u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned *)X + c));
+    return r;
+}
+__device__ __forceinline__ unsigned long long nbg_gx64nc(unsigned sbase, const void *X, int c, int hc) {
+    unsigned long long r;
+    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b64 %0, [%3]; @!p ld.global.nc.b64 %0, [%4]; }"
+        : "=l"(r) : "r"(c), "r"(hc), "r"(sbase + 8u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned long long *)X + c));
     return r;
 }
 __device__ __forceinline__ unsigned long long nbg_gx64(unsigned sbase, const void *X, int c, int hc) {

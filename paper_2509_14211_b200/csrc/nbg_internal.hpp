@@ -249,6 +249,7 @@ struct Prog {
     bool spmv = false;
     bool tp = false;        // spmv through the two-phase plan: this program is phase 2 (combine + epilogue)
     bool lpr = false;       // spmv, lane-per-row skeleton (low-skew matrices)
+    int nt = 0, hot_kb = 0; // spmv (task skeleton): threads per CTA and hot-cache KB, chosen per matrix
     bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
     SpmvSig sp;
     int n_in = 0, n_out = 0, n_imm = 0, n_sin = 0, n_red = 0;
@@ -412,7 +413,8 @@ void gpu_bitset_full(Ctx &c, int64_t n, uint32_t *bits);   // all n bits set, ta
 // codegen / jit
 bool spmv_gather_pipeline();   // SpMV gathers one step ahead (NBG_SPMV_GPIPE=1)
 bool spmv_epilogue_prefetch();  // SpMV prefetches the epilogue's row inputs at task start (NBG_SPMV_PF, default on)
-int spmv_threads(int xsize);   // threads per SpMV CTA for a gathered element size (NBG_SPMV_THREADS overrides)
+int spmv_threads(int xsize);
+void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb);   // per-matrix SpMV launch shape   // threads per SpMV CTA for a gathered element size (NBG_SPMV_THREADS overrides)
 int spmv_lpr_mode();   // NBG_SPMV_LPR: -1 auto (by skew), 0 never, 1 always   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);

@@ -602,7 +602,9 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         args.partials = (double *)(A.plan->partials ? A.plan->partials->d : nullptr);
         args.ntiles = A.plan->ntiles;
         args.nchunks = A.plan->nchunks;
-        const long long nw = spmv_threads((int)type_size(u->type)) / 32;
+        spmv_variant((int)type_size(u->type), (A.plan->relabel ? A.plan->ncols_g : A.ncols) * (long long)type_size(u->type), &p.nt,
+                     &p.hot_kb);
+        const long long nw = p.nt / 32;
         items = (A.plan->ntiles + A.plan->nchunks + nw - 1) / nw;   // one task per warp
         args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
@@ -612,10 +614,12 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         const int lm = spmv_lpr_mode();
         if (!T && (lm == 1 || (lm == -1 && A.plan->low_skew))) {
             p.lpr = true;
+            p.nt = p.hot_kb = 0;
             items = (n + 255) / 256;
         }
         if (T) {
             p.tp = true;
+            p.nt = p.hot_kb = 0;
             args.rowslot = (const long long *)T->rowslot->d;
             args.part = T->part->d;
             items = (n + 127) / 128 / 8 + 1;      // phase 2: 128-row tiles, 8 warps per CTA
@@ -673,7 +677,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? (p.lpr ? "spmvl" : "spmv") : "ewise"), (unsigned long long)hash_str(sig));
         int smem = 0, hot = 0;
         std::string src = codegen(p, nm, &smem, &hot);
-        kern = jit_compile(c, src, nm, p.spmv && !p.tp && !p.lpr, smem, (p.spmv && !p.tp && !p.lpr) ? spmv_threads((int)type_size(p.sp.xt)) : 0);
+        kern = jit_compile(c, src, nm, p.spmv && !p.tp && !p.lpr, smem, (p.spmv && !p.tp && !p.lpr) ? p.nt : 0);
         kern->hot = hot;
         c.plans[sig] = kern;
         c.stats.plans_built++;
