@@ -458,6 +458,12 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     if (nt_ <= 0) spmv_variant((int)type_size(sp.xt), 0, &nt_, &hk_);
     const int NT = nt_, NW = NT / 32;
     int hot_bytes = hk_ * 1024;
+    {   // keep all shared memory inside the carveout step the size aims at (132 / 164 / 196 KB):
+        // crossing a step halves the L1 left beside it (measured cliffs)
+        const int other = NW * warp_bytes + NW * NF * 11 * 8 + 1024;
+        const int step = (hk_ >= 140 ? 196 : (hk_ >= 100 ? 164 : 132)) * 1024;
+        if (hot_bytes > step - other) hot_bytes = std::max(0, step - other);
+    }
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
     const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
@@ -1241,7 +1247,7 @@ int spmv_threads(int xsize) {
 }
 
 // Launch shape of the task skeleton (DESIGN.md §7 "L2-only cold gathers"): 1024 threads for 4-byte
-// gathered elements (768 for 8-byte ones: spills); the hot cache is 144 KB when the gathered
+// gathered elements (768 for 8-byte ones: spills); the hot cache is 152 KB when the gathered
 // vector stays L2-resident (C4: 16.8 MB) and 80 KB when it does not (C5: 108 MB), because then the
 // L1 left beside it (the shared-memory carveout steps at 132 / 164 / 196 KB) is worth more than
 // hot entries: C5 3.91 ms per sweep at 80 KB vs 4.55 ms at 96 KB and 5.79 ms at 144 KB.
@@ -1257,7 +1263,7 @@ void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb) {
         eh = (h && *h) ? std::max(0, std::min(200, atoi(h))) : -1;
     }
     *nt = et ? et : (xsize <= 4 ? 1024 : 768);
-    *hot_kb = eh >= 0 ? eh : (resident ? 144 : 80);
+    *hot_kb = eh >= 0 ? eh : (resident ? 152 : 80);
 }
 
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {

@@ -1,6 +1,6 @@
-run() { env "$@" timeout 200 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null > /tmp/o.json; python -c "import json; d=json.load(open('/tmp/o.json')); print('$*', d['value'], d['roofline']['avg_launch_us'])"; }
-run NBG_SPMV_IDXLD=cs
-run NBG_SPMV_IDXLD=na
-run NBG_SPMV_IDXLD=cg
-run NBG_SPMV_IDXLD=na NBG_SPMV_HOT_KB=152
-run NBG_SPMV_IDXLD=cs
+run() { env "$@" timeout 600 python bench.py --workload $W --steps $S --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null > /tmp/o.json; python -c "import json; d=json.load(open('/tmp/o.json')); print('$W $*', d['value'], d['roofline']['avg_launch_us'])"; }
+W=c4 S=5 run NBG_X=default
+W=c4 S=5 run NBG_X=default
+W=c5 S=1 run NBG_X=default
+W=c3 S=3 run NBG_X=default
+W=c1 S=5 run NBG_X=default
