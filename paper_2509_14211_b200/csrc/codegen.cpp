@@ -451,7 +451,13 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
     const int NF = (int)fplus.size();
     const int accw = (ACC == "double" || ACC == "long long") ? 8 : 4;
-    const int warp_bytes = 128 * 8 + 32 * 4;                  // row totals of the task + row-start bitmask
+    // row totals of the task + row-start bitmask; an fp32 mxv keeps its fp64 row sums rounded to
+    // fp32 here (the epilogue rounds them to fp32 anyway: identical values, half the bytes, which
+    // leaves room for hot entries inside the shared-memory carveout step)
+    const bool rt_narrow = (ACC == "double" && sp.T == NBG_FP32);
+    const std::string RT = rt_narrow ? "float" : ACC;
+    const int rt_bytes = rt_narrow ? 4 : 8;
+    const int warp_bytes = 128 * rt_bytes + 32 * 4;
     const int xacc_bytes = 32 * NF * 11 * 8;
     const int x_bytes = (int)type_size(sp.xt);
     int nt_ = p.nt, hk_ = p.hot_kb;
@@ -460,7 +466,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     int hot_bytes = hk_ * 1024;
     {   // keep all shared memory inside the carveout step the size aims at (132 / 164 / 196 KB):
         // crossing a step halves the L1 left beside it (measured cliffs)
-        const int other = NW * warp_bytes + NW * NF * 11 * 8 + 1024;
+        const int other = NW * warp_bytes + NW * NF * 11 * 8 + 3072;   // + static smem + the driver's 1 KB per CTA
         const int step = (hk_ >= 140 ? 196 : (hk_ >= 100 ? 164 : 132)) * 1024;
         if (hot_bytes > step - other) hot_bytes = std::max(0, step - other);
     }
@@ -508,8 +514,8 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
     o << "  const unsigned s_base = (unsigned)__cvta_generic_to_shared(nbg_dyn);\n";
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
-    o << "  " << ACC << "* s_racc = (" << ACC << "*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << ");   // [128] row totals\n";
-    o << "  unsigned* s_sbm = (unsigned*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << " + 1024);   // [32] row starts\n";
+    o << "  " << RT << "* s_racc = (" << RT << "*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << ");   // [128] row totals\n";
+    o << "  unsigned* s_sbm = (unsigned*)(nbg_dyn + " << hot_region << " + warp * " << warp_bytes << " + " << 128 * rt_bytes << ");   // [32] row starts\n";
     if (NF)
         o << "  u64* s_x = (u64*)(nbg_dyn + " << hot_region << " + NBG_NW * " << warp_bytes << ");   // [warp][NF][11]\n";
     o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
@@ -694,7 +700,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "        const long long i = (long long)tl.x + lane + 32 * r;\n";
     o << "        const unsigned nm = r == 0 ? nem_[0] : (r == 1 ? nem_[1] : (r == 2 ? nem_[2] : nem_[3]));\n";
     o << "        if (lane + 32 * r < R) {\n";
-    o << "          const " << ACC << " acc = ((nm >> lane) & 1u) ? s_racc[rb_ + __popc(nm & ((1u << lane) - 1u))] : (" << ACC << ")(" << IDENT << ");\n";
+    o << "          const " << ACC << " acc = ((nm >> lane) & 1u) ? (" << ACC << ")s_racc[rb_ + __popc(nm & ((1u << lane) - 1u))] : (" << ACC << ")(" << IDENT << ");\n";
     g.emit_uniform_reload("          ", "s_uni");
     g.emit_body(
         "          ",
@@ -1247,10 +1253,10 @@ int spmv_threads(int xsize) {
 }
 
 // Launch shape of the task skeleton (DESIGN.md §7 "L2-only cold gathers"): 1024 threads for 4-byte
-// gathered elements (768 for 8-byte ones: spills); the hot cache is 152 KB when the gathered
-// vector stays L2-resident (C4: 16.8 MB) and 80 KB when it does not (C5: 108 MB), because then the
-// L1 left beside it (the shared-memory carveout steps at 132 / 164 / 196 KB) is worth more than
-// hot entries: C5 3.91 ms per sweep at 80 KB vs 4.55 ms at 96 KB and 5.79 ms at 144 KB.
+// gathered elements (768 for 8-byte ones: spills); the hot cache fills the 196 KB carveout step when
+// the gathered vector stays L2-resident (C4: 16.8 MB) and only the 132 KB step when it does not
+// (C5: 108 MB), because then the L1 left beside it is worth more than hot entries: C5 3.88 ms per
+// sweep at 99 KB vs 4.55 ms at 96 KB in the 164 KB step and 5.79 ms at 144 KB.
 // NBG_SPMV_THREADS / NBG_SPMV_HOT_KB override both.
 void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb) {
     const bool resident = gathered_bytes <= (48ll << 20);
@@ -1263,7 +1269,8 @@ void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb) {
         eh = (h && *h) ? std::max(0, std::min(200, atoi(h))) : -1;
     }
     *nt = et ? et : (xsize <= 4 ? 1024 : 768);
-    *hot_kb = eh >= 0 ? eh : (resident ? 152 : 80);
+    // targets clamped to their carveout step by gen_spmv: 192 -> fills the 196 KB step, 99 -> the 132 KB step
+    *hot_kb = eh >= 0 ? eh : (resident ? 192 : 99);
 }
 
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem) {
