@@ -818,18 +818,25 @@ int gen_spmv_lpr(Gen &g, const std::string &kname) {
     o << "    if (i >= a.n) continue;\n";
     o << "    const long long g1 = GRP[i + 1];\n";
     o << "    " << k.ACC << " acc = " << k.IDENT << ";\n";
-    o << "    for (long long gg = GRP[i]; gg < g1; gg += 2) {\n";
+    // UG groups per iteration (4 UG gathers in flight per lane); groups past the row end are
+    // padding (-1) and contribute nothing
+    const char *eug = getenv("NBG_LPR_UG");
+    const int UG = (eug && (eug[0] == '1' || eug[0] == '2' || eug[0] == '4')) ? eug[0] - '0' : 4;
+    o << "    for (long long gg = GRP[i]; gg < g1; gg += " << UG << ") {\n";
     o << "      const long long P_ = 4 * gg;\n";
-    o << "      const int4 ca = __ldcs(CG + gg);\n";
-    o << "      const int4 cb = (gg + 1 < g1) ? __ldcs(CG + gg + 1) : make_int4(-1, -1, -1, -1);\n";
-    o << "      const " << k.XT << " x0 = NBG_G(ca.x), x1 = NBG_G(ca.y), x2 = NBG_G(ca.z), x3 = NBG_G(ca.w);\n";
-    o << "      const " << k.XT << " x4 = NBG_G(cb.x), x5 = NBG_G(cb.y), x6 = NBG_G(cb.z), x7 = NBG_G(cb.w);\n";
-    o << "      acc = NBG_ADD(acc, NBG_TV(ca.x, P_, x0)); acc = NBG_ADD(acc, NBG_TV(ca.y, P_ + 1, x1));\n";
-    o << "      acc = NBG_ADD(acc, NBG_TV(ca.z, P_ + 2, x2)); acc = NBG_ADD(acc, NBG_TV(ca.w, P_ + 3, x3));\n";
-    o << "      if (gg + 1 < g1) {\n";
-    o << "        acc = NBG_ADD(acc, NBG_TV(cb.x, P_ + 4, x4)); acc = NBG_ADD(acc, NBG_TV(cb.y, P_ + 5, x5));\n";
-    o << "        acc = NBG_ADD(acc, NBG_TV(cb.z, P_ + 6, x6)); acc = NBG_ADD(acc, NBG_TV(cb.w, P_ + 7, x7));\n";
-    o << "      }\n";
+    for (int u = 0; u < UG; u++)
+        o << "      const int4 c" << u << " = (gg + " << u << " < g1) ? __ldcs(CG + gg + " << u << ") : make_int4(-1, -1, -1, -1);\n";
+    for (int u = 0; u < UG; u++)
+        o << "      const " << k.XT << " x" << u << "a = NBG_G(c" << u << ".x), x" << u << "b = NBG_G(c" << u << ".y), x" << u << "c = NBG_G(c" << u
+          << ".z), x" << u << "d = NBG_G(c" << u << ".w);\n";
+    for (int u = 0; u < UG; u++) {
+        o << "      if (gg + " << u << " < g1) {\n";
+        o << "        acc = NBG_ADD(acc, NBG_TV(c" << u << ".x, P_ + " << 4 * u << ", x" << u << "a)); acc = NBG_ADD(acc, NBG_TV(c" << u
+          << ".y, P_ + " << 4 * u + 1 << ", x" << u << "b));\n";
+        o << "        acc = NBG_ADD(acc, NBG_TV(c" << u << ".z, P_ + " << 4 * u + 2 << ", x" << u << "c)); acc = NBG_ADD(acc, NBG_TV(c" << u
+          << ".w, P_ + " << 4 * u + 3 << ", x" << u << "d));\n";
+        o << "      }\n";
+    }
     o << "    }\n";
     g.emit_body(
         "    ",
