@@ -106,15 +106,30 @@ __global__ void k_ngroups(long long n, const long long *rowptr, long long *ng) {
 }
 
 // scatter the stored entries of every row into its groups: dst[4 grp[row] + j] = src[rowptr[row] + j]
+// Each thread takes 16 consecutive entries (a warp: 512, so the src reads stay coalesced per
+// load): one binary search for the row of the first entry, then the row advances as the entries
+// cross row ends.
 template <class T>
 __global__ void k_fill_groups(long long nnz, long long n, const long long *rowptr, const long long *grp, const T *src, T *dst) {
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
-        long long lo = 0, hi = n;          // row = last i with rowptr[i] <= p
+    const long long nch = (nnz + 15) / 16;
+    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nch; q += (long long)gridDim.x * blockDim.x) {
+        const long long p0 = 16 * q;
+        long long lo = 0, hi = n;          // row = last i with rowptr[i] <= p0
         while (hi - lo > 1) {
             long long mid = (lo + hi) >> 1;
-            if (rowptr[mid] <= p) lo = mid; else hi = mid;
+            if (rowptr[mid] <= p0) lo = mid; else hi = mid;
         }
-        dst[4 * grp[lo] + (p - rowptr[lo])] = src[p];
+        long long rs = rowptr[lo], re = rowptr[lo + 1], g4 = 4 * grp[lo];
+        const long long p1 = p0 + 16 < nnz ? p0 + 16 : nnz;
+        for (long long p = p0; p < p1; p++) {
+            while (p >= re) {              // next non-empty row
+                lo++;
+                rs = re;
+                re = rowptr[lo + 1];
+                g4 = 4 * grp[lo];
+            }
+            dst[g4 + (p - rs)] = src[p];
+        }
     }
 }
 
@@ -137,9 +152,22 @@ __global__ void k_validate_csr(long long n, long long ncols, long long nnz, cons
 }
 
 // ---- column relabel (gather layout)
-__global__ void k_col_count(long long nnz, const int *ci, int *cnt) {
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x)
-        atomicAdd(&cnt[ci[p]], 1);
+// column histogram; the first CC_PRIV columns are counted in a per-CTA shared-memory copy first
+// (power-law generators put their hubs at small ids: the global atomics on those few addresses
+// serialise), then added once per CTA
+#define CC_PRIV 8192
+__global__ void k_col_count(long long nnz, long long ncols, const int *ci, int *cnt) {
+    __shared__ int h[CC_PRIV];
+    for (int j = threadIdx.x; j < CC_PRIV; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+        const int c = ci[p];
+        if (c < CC_PRIV) atomicAdd(&h[c], 1);
+        else atomicAdd(&cnt[c], 1);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < CC_PRIV && j < ncols; j += blockDim.x)
+        if (h[j]) atomicAdd(&cnt[j], h[j]);
 }
 // sort key: descending count, empty columns last (stable radix sort keeps ascending id on ties)
 __global__ void k_col_keys(long long nc, const int *cnt, unsigned *key, int *ids, int *nonempty) {
@@ -544,7 +572,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         const long long nc = A.ncols;
         BufP cnt = alloc_buf(c, (size_t)nc * 4);
         NBG_CUDA(cudaMemsetAsync(cnt->d, 0, (size_t)nc * 4, c.stream));
-        k_col_count<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (int *)cnt->d);
+        k_col_count<<<2 * c.num_sms, 1024, 0, c.stream>>>(A.nnz, nc, (const int *)A.colidx->d, (int *)cnt->d);
         BufP key = alloc_buf(c, (size_t)nc * 4), key2 = alloc_buf(c, (size_t)nc * 4);
         BufP ids = alloc_buf(c, (size_t)nc * 4), ids2 = alloc_buf(c, (size_t)nc * 4);
         BufP ne = alloc_buf(c, 4);
