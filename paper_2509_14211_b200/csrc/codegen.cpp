@@ -23,6 +23,7 @@
 //          The summation order of a row depends only on its length, so the
 //          fused and the blocking mxv -- and every row partition -- produce identical row sums.
 #include <algorithm>
+#include <charconv>
 #include <sstream>
 
 #include "nbg_internal.hpp"
@@ -42,19 +43,40 @@ static const char *ctype(int t) {
 // type in which an operator with output type t is evaluated
 static const char *ctype_compute(int t) { return t == NBG_BOOL ? "long long" : ctype(t); }
 
+// built with std::to_chars into one reserved string (it is computed at every wait: the plan-cache key)
+static inline void sig_put(std::string &s, long long v, char sep) {
+    char buf[24];
+    auto r = std::to_chars(buf, buf + sizeof buf, v);
+    s.append(buf, r.ptr);
+    s.push_back(sep);
+}
 std::string Prog::signature() const {
-    std::ostringstream s;
-    s << (spmv ? (tp ? "T" : (lpr ? "L" : "S")) : "E") << (vec ? "v" : "s") << nt << "," << hot_kb << "|";
-    if (spmv) s << sp.add << "," << sp.mul << "," << sp.T << "," << sp.xt << "," << sp.at << "," << sp.has_vals << "|";
-    for (const Ins &i : ins)
-        s << (int)i.k << ":" << i.t << ":" << i.code << ":" << i.a << ":" << i.b << ":" << i.imm0 << ":" << i.imm1
-          << ":" << i.slot << ":" << (int)i.fmt << ";";
-    s << "|";
-    for (const OutV &o : outs) s << o.ins << ">" << o.out << (o.scatter ? "s" : "") << ";";
-    s << "|";
-    for (const RedOut &r : reds) s << r.ins << ">" << r.monoid << ":" << r.racc << ":" << (int)r.fmt << ";";
-    s << "|" << n_in << "," << n_out << "," << n_imm << "," << n_sin << "," << n_red;
-    return s.str();
+    std::string s;
+    s.reserve(32 + 48 * ins.size() + 12 * (outs.size() + reds.size()));
+    s.push_back(spmv ? (tp ? 'T' : (lpr ? 'L' : 'S')) : 'E');
+    s.push_back(vec ? 'v' : 's');
+    sig_put(s, nt, ',');
+    sig_put(s, hot_kb, '|');
+    if (spmv) {
+        sig_put(s, sp.add, ','); sig_put(s, sp.mul, ','); sig_put(s, sp.T, ','); sig_put(s, sp.xt, ',');
+        sig_put(s, sp.at, ','); sig_put(s, sp.has_vals, '|');
+    }
+    for (const Ins &i : ins) {
+        sig_put(s, (int)i.k, ':'); sig_put(s, i.t, ':'); sig_put(s, i.code, ':'); sig_put(s, i.a, ':'); sig_put(s, i.b, ':');
+        sig_put(s, i.imm0, ':'); sig_put(s, i.imm1, ':'); sig_put(s, i.slot, ':'); sig_put(s, (int)i.fmt, ';');
+    }
+    s.push_back('|');
+    for (const OutV &o : outs) {
+        sig_put(s, o.ins, '>');
+        sig_put(s, o.out, o.scatter ? 's' : ';');
+    }
+    s.push_back('|');
+    for (const RedOut &r : reds) {
+        sig_put(s, r.ins, '>'); sig_put(s, r.monoid, ':'); sig_put(s, r.racc, ':'); sig_put(s, (int)r.fmt, ';');
+    }
+    s.push_back('|');
+    sig_put(s, n_in, ','); sig_put(s, n_out, ','); sig_put(s, n_imm, ','); sig_put(s, n_sin, ','); sig_put(s, n_red, '.');
+    return s;
 }
 
 namespace {

@@ -342,6 +342,11 @@ struct Ctx {
     SlabP cur_slab;
     std::vector<cudaEvent_t> event_pool;
 
+    // freed device buffers kept for reuse by size (all work is ordered on `stream`, so a buffer
+    // whose last handle died can back a later allocation without a cudaFreeAsync/MallocAsync pair)
+    std::unordered_map<size_t, std::vector<void *>> buf_pool;
+    size_t pooled_bytes = 0;
+    bool closing = false;
     // plan cache: signature -> kernel ("GraphBLAS method signatures as keys")
     std::unordered_map<std::string, KernelP> plans;
     // memo: structural key over materialised leaves -> result (derived views)

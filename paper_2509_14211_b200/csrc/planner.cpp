@@ -20,6 +20,8 @@
 //   Liveness ("elide unneeded objects"): besides the requested roots, only pending
 //   nodes a user still holds a handle to are stored; every other intermediate lives in registers.
 #include <algorithm>
+#include <charconv>
+#include <cstring>
 #include <cstdio>
 #include <functional>
 #include <sstream>
@@ -64,26 +66,46 @@ static std::string dbits(double v) {
 
 // ---------------------------------------------------------------- structural keys
 
+static inline void kput(std::string &s, long long v) {
+    char buf[24];
+    auto r = std::to_chars(buf, buf + sizeof buf, v);
+    s.append(buf, r.ptr);
+}
+static inline void kbits(std::string &s, double v) {
+    uint64_t b;
+    memcpy(&b, &v, 8);
+    char buf[24];
+    auto r = std::to_chars(buf, buf + sizeof buf, (unsigned long long)b, 16);
+    s.append(buf, r.ptr);
+}
 static void key_rec(const Node *x, std::string &s, const Node *ph) {
-    if (x == ph) { s += "P"; return; }
+    if (x == ph) { s += 'P'; return; }
     if (x->mat) {
         if (x->scalar) {
-            if (x->sfmt == SFmt::HOST) s += "h" + std::to_string(x->type) + ":" + dbits(x->hval);
-            else s += "d" + std::to_string(x->type) + ":" + std::to_string(x->slot->id);
-        } else if (x->kind == VKind::FULL) s += "F" + std::to_string(x->buf->id);
-        else if (x->kind == VKind::ISO) s += "I" + std::to_string(x->type) + ":" + dbits(x->iso);
-        else if (x->kind == VKind::SPARSE) s += "S" + std::to_string(x->buf->id);
-        else if (x->kind == VKind::BITSET) s += "B" + std::to_string(x->buf->id);
-        else s += "E";
+            if (x->sfmt == SFmt::HOST) { s += 'h'; kput(s, x->type); s += ':'; kbits(s, x->hval); }
+            else { s += 'd'; kput(s, x->type); s += ':'; kput(s, (long long)x->slot->id); }
+        } else if (x->kind == VKind::FULL) { s += 'F'; kput(s, (long long)x->buf->id); }
+        else if (x->kind == VKind::ISO) { s += 'I'; kput(s, x->type); s += ':'; kbits(s, x->iso); }
+        else if (x->kind == VKind::SPARSE) { s += 'S'; kput(s, (long long)x->buf->id); }
+        else if (x->kind == VKind::BITSET) { s += 'B'; kput(s, (long long)x->buf->id); }
+        else s += 'E';
         return;
     }
-    s += "(" + std::to_string((int)x->op) + "," + std::to_string(x->type) + "," + std::to_string(x->n) + "," +
-         std::to_string(x->code) + "," + dbits(x->c0) + "," + dbits(x->c1) + "," + std::to_string(x->add) + "," +
-         std::to_string(x->mul) + "," + (x->A ? std::to_string(x->A->id) : "-") + ";";
+    s += '(';
+    kput(s, (int)x->op); s += ',';
+    kput(s, x->type); s += ',';
+    kput(s, x->n); s += ',';
+    kput(s, x->code); s += ',';
+    kbits(s, x->c0); s += ',';
+    kbits(s, x->c1); s += ',';
+    kput(s, x->add); s += ',';
+    kput(s, x->mul); s += ',';
+    if (x->A) kput(s, (long long)x->A->id); else s += '-';
+    s += ';';
     if (x->a) key_rec(x->a.get(), s, ph);
-    s += ";";
+    s += ';';
     if (x->b) key_rec(x->b.get(), s, ph);
-    s += ")";
+    s += ')';
 }
 
 static std::string node_key(const Node *x, const Node *ph = nullptr) {

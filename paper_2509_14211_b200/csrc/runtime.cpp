@@ -32,8 +32,16 @@ uint64_t hash_str(const std::string &s) {   // FNV-1a 64
 
 // ---------------------------------------------------------------- buffers
 
+static constexpr size_t POOL_MAX_BUF = 64ull << 20, POOL_MAX_TOTAL = 512ull << 20;
+
 Buf::~Buf() {
-    if (owned && d && ctx) cudaFreeAsync(d, ctx->stream);
+    if (!(owned && d && ctx)) return;
+    if (!ctx->closing && bytes <= POOL_MAX_BUF && ctx->pooled_bytes + bytes <= POOL_MAX_TOTAL) {
+        ctx->buf_pool[bytes].push_back(d);
+        ctx->pooled_bytes += bytes;
+    } else {
+        cudaFreeAsync(d, ctx->stream);
+    }
 }
 
 BufP alloc_buf(Ctx &c, size_t bytes) {
@@ -42,7 +50,16 @@ BufP alloc_buf(Ctx &c, size_t bytes) {
     b->id = c.new_id();
     b->bytes = bytes;
     b->owned = true;
-    if (bytes) NBG_CUDA(cudaMallocAsync(&b->d, bytes, c.stream));
+    if (bytes) {
+        auto it = c.buf_pool.find(bytes);
+        if (it != c.buf_pool.end() && !it->second.empty()) {
+            b->d = it->second.back();
+            it->second.pop_back();
+            c.pooled_bytes -= bytes;
+        } else {
+            NBG_CUDA(cudaMallocAsync(&b->d, bytes, c.stream));
+        }
+    }
     return b;
 }
 
@@ -350,6 +367,11 @@ Ctx::~Ctx() {
     hints.clear();
     plans.clear();
     cur_slab.reset();
+    closing = true;
+    for (auto &kv : buf_pool)
+        for (void *p : kv.second) cudaFreeAsync(p, stream);
+    buf_pool.clear();
+    if (stream) cudaStreamSynchronize(stream);
     for (auto e : event_pool) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
