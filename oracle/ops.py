@@ -162,12 +162,23 @@ def apply_bind2nd(code, u, s, T, c0=0.0):
     return binop(code, u, np.full(u.shape[0], s), T, c0)
 
 
+def _ident(monoid, T):
+    """Identity of the monoid in T: 0 for PLUS, +/-inf for float MIN/MAX, the largest / smallest
+    value of T for integer MIN/MAX (the value an empty fold yields)."""
+    if monoid == "PLUS":
+        return _c(0, T)
+    if _is_float(T):
+        return _c(math.inf if monoid == "MIN" else -math.inf, T)
+    if np.dtype(T) == np.bool_:
+        return _c(1 if monoid == "MIN" else 0, T)
+    info = np.iinfo(np.dtype(T))
+    return np.array(info.max if monoid == "MIN" else info.min, dtype=T)[()]
+
+
 def reduce(monoid, v, T):
     """Fold of the stored values.  PLUS on floats: exact sum rounded once."""
     if v is None or v.shape[0] == 0:
-        return _c(0 if monoid == "PLUS" else (math.inf if monoid == "MIN" else -math.inf), T) \
-            if _is_float(T) else _c(0 if monoid == "PLUS" else
-                                    (np.iinfo(np.int64).max if monoid == "MIN" else np.iinfo(np.int64).min), T)
+        return _ident(monoid, T)
     if monoid == "PLUS":
         if _is_float(v.dtype) or _is_float(T):
             return _c(math.fsum(float(z) for z in v.astype(np.float64)), T)
@@ -190,8 +201,7 @@ def mxv(add, mul, rowptr, colidx, vals, x, T, iso=1.0):
     C = _compute_type(T)
     out = np.empty(n, dtype=T)
     if x is None:
-        ident = 0 if add == "PLUS" else (math.inf if add == "MIN" else -math.inf)
-        out[:] = _c(ident, T) if _is_float(T) else _c(0, T)
+        out[:] = _ident(add, T)
         return out
     xc = convert(x, C)
     for i in range(n):
@@ -208,9 +218,9 @@ def mxv(add, mul, rowptr, colidx, vals, x, T, iso=1.0):
             else:
                 out[i] = _c(int(np.asarray(prod, np.int64).sum()), T)
         elif add == "MIN":
-            out[i] = _c(np.fmin.reduce(prod) if prod.size else (math.inf if _is_float(C) else 0), T)
+            out[i] = _c(np.fmin.reduce(prod), T) if prod.size else _ident("MIN", T)
         elif add == "MAX":
-            out[i] = _c(np.fmax.reduce(prod) if prod.size else (-math.inf if _is_float(C) else 0), T)
+            out[i] = _c(np.fmax.reduce(prod), T) if prod.size else _ident("MAX", T)
         else:
             raise ValueError(add)
     return out

@@ -328,8 +328,12 @@ static C h_binop(int code, C x, C y, C k0) {
 double host_round(int t, double v) {
     switch (t) {
         case NBG_BOOL: return v != 0.0 ? 1.0 : 0.0;
-        case NBG_INT32: return (double)(int)v;
-        case NBG_INT64: return (double)(long long)v;
+        // saturating (an out-of-range double -> integer conversion is undefined; the monoid
+        // identities INT_MAX / INT64_MAX arrive here as the nearest doubles)
+        case NBG_INT32: return v >= 2147483647.0 ? 2147483647.0 : (v <= -2147483648.0 ? -2147483648.0 : (double)(int)v);
+        case NBG_INT64:
+            return v >= 9223372036854775807.0 ? 9223372036854775807.0
+                                              : (v <= -9223372036854775808.0 ? -9223372036854775808.0 : (double)(long long)v);
         case NBG_FP32: return (double)(float)v;
         default: return v;
     }

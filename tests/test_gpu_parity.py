@@ -402,3 +402,41 @@ def test_lane_per_row_spmv(nbg, monkeypatch, kind, scale, force):
         assert np.array_equal(res[(nbg.NONBLOCKING, "fp32", dang)], res[(nbg.BLOCKING, "fp32", dang)])
         # fp64: the dangling sum's last bit may differ (see test_blocking_equals_nonblocking_bitwise)
         assert rel(res[(nbg.NONBLOCKING, "fp64", dang)], res[(nbg.BLOCKING, "fp64", dang)]) <= 1e-15
+
+
+def test_mxv_degenerate_and_int(nbg, ctx):
+    """Edge cases of the SpMV plan: no stored entries, a 1 x 1 matrix, integer semirings, and a
+    wide iso matrix (>= 2^15 columns: the relabelled gather layout) against the oracle."""
+    # nnz = 0: dense output, identity everywhere
+    A0 = nbg.nbg_matrix_from_csr(ctx, 5, 3, np.zeros(6, np.int64), np.zeros(0, np.int32), type=nbg.FP32, iso=1.0)
+    w0 = nbg.nbg_mxv(ctx, nbg.FP32, "MIN", "TIMES", A0, nbg.nbg_vector_from_dense(ctx, nbg.FP32, np.ones(3, np.float32)))
+    assert np.all(nbg.nbg_vector_export_dense(ctx, w0) == np.inf)
+    # 1 x 1
+    A1 = nbg.nbg_matrix_from_csr(ctx, 1, 1, np.array([0, 1], np.int64), np.array([0], np.int32), type=nbg.FP64, iso=3.0)
+    w1 = nbg.nbg_mxv(ctx, nbg.FP64, "PLUS", "TIMES", A1, nbg.nbg_vector_from_dense(ctx, nbg.FP64, np.array([2.5])))
+    assert nbg.nbg_vector_export_dense(ctx, w1)[0] == 7.5
+    rng = np.random.default_rng(17)
+    # integer semirings on a ragged valued matrix
+    n, m = 300, 500
+    lens = rng.integers(0, 30, n)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(m, int(l), replace=False)) for l in lens]).astype(np.int32)
+    for T, npT in ((nbg.INT32, np.int32), (nbg.INT64, np.int64)):
+        vals = rng.integers(-5, 6, ci.shape[0]).astype(npT)
+        x = rng.integers(-5, 6, m).astype(npT)
+        A = nbg.nbg_matrix_from_csr(ctx, n, m, rp, ci, vals=vals, type=T)
+        u = nbg.nbg_vector_from_dense(ctx, T, x)
+        for add in ("PLUS", "MIN", "MAX"):
+            got = nbg.nbg_vector_export_dense(ctx, nbg.nbg_mxv(ctx, T, add, "TIMES", A, u))
+            assert np.array_equal(got, ops.mxv(add, "TIMES", rp, ci, vals, x, npT)), (T, add)
+    # wide iso matrix: relabelled gather layout, hot cache + L2 gathers
+    n, m = 2000, 70000
+    lens = rng.integers(0, 60, n)
+    lens[3] = 5000
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(m, int(l), replace=False)) for l in lens]).astype(np.int32)
+    x = rng.random(m).astype(np.float32)
+    A = nbg.nbg_matrix_from_csr(ctx, n, m, rp, ci, type=nbg.FP32, iso=1.0)
+    got = nbg.nbg_vector_export_dense(ctx, nbg.nbg_mxv(ctx, nbg.FP32, "PLUS", "TIMES", A, nbg.nbg_vector_from_dense(ctx, nbg.FP32, x)))
+    exp = ops.mxv("PLUS", "TIMES", rp, ci, None, x, np.float32)
+    assert rel(got[lens > 0], exp[lens > 0]) <= 2e-7 and np.all(got[lens == 0] == 0)

@@ -309,3 +309,23 @@ def test_ops_mxv_vs_dense_random():
     assert np.array_equal(ops.mxv("PLUS", "TIMES", rp, ci, None, x, np.float64), dense @ x)
     assert np.array_equal(ops.mxv("MAX", "SECOND", rp, ci, None, x, np.float64),
                           np.array([x[dense[i] > 0].max() if dense[i].any() else -np.inf for i in range(n)]))
+
+
+def test_ops_empty_fold_identities():
+    """An empty fold yields the monoid's identity in the result type (SPEC.md:206 for mxv rows,
+    SPEC.md:211-217 for reduce): 0, +/-inf for floats, the extreme values of an integer type --
+    checked against numpy's own integer limits and a brute-force min/max over the whole type."""
+    for T in (np.int32, np.int64):
+        info = np.iinfo(T)
+        assert ops.reduce("MIN", None, T) == info.max and ops.reduce("MAX", None, T) == info.min
+        assert ops.reduce("MIN", None, T).dtype == np.dtype(T)
+        # identity property: min(identity, v) == v for the extremes of the type
+        for v in (info.min, -1, 0, 1, info.max):
+            assert min(int(ops.reduce("MIN", None, T)), v) == v and max(int(ops.reduce("MAX", None, T)), v) == v
+    assert ops.reduce("MIN", None, np.float32) == np.inf and ops.reduce("PLUS", None, np.float64) == 0.0
+    # mxv: an empty row takes the identity, a non-empty one its fold
+    rp = np.array([0, 0, 2], np.int64)
+    ci = np.array([0, 1], np.int32)
+    x = np.array([4, -3], np.int32)
+    assert list(ops.mxv("MIN", "SECOND", rp, ci, None, x, np.int32)) == [np.iinfo(np.int32).max, -3]
+    assert list(ops.mxv("MAX", "SECOND", rp, ci, None, x, np.int64)) == [np.iinfo(np.int64).min, 4]
