@@ -69,10 +69,14 @@ def _div(a, b, T):
             return a / b
     out = np.zeros_like(a)
     nz = b != 0
-    q = np.zeros_like(a)
-    # C-style truncating integer division; x/0 := 0 (reading R2)
-    q[nz] = np.trunc(a[nz].astype(np.float64) / b[nz].astype(np.float64)).astype(a.dtype) if a.size else q[nz]
-    out[nz] = q[nz]
+    # C-style truncating integer division in exact integer arithmetic; x/0 := 0 (reading R2)
+    an, bn = a[nz].astype(np.int64), b[nz].astype(np.int64)
+    with np.errstate(all="ignore"):
+        # magnitudes as uint64 (|INT64_MIN| = 2^63 exactly), quotient toward zero, then the sign
+        mag = np.abs(an).astype(np.uint64) // np.abs(bn).astype(np.uint64)
+        neg = (an < 0) != (bn < 0)
+        q = np.where(neg, (np.uint64(0) - mag).astype(np.int64), mag.astype(np.int64))
+    out[nz] = q.astype(a.dtype)
     return out
 
 

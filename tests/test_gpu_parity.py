@@ -440,3 +440,41 @@ def test_mxv_degenerate_and_int(nbg, ctx):
     got = nbg.nbg_vector_export_dense(ctx, nbg.nbg_mxv(ctx, nbg.FP32, "PLUS", "TIMES", A, nbg.nbg_vector_from_dense(ctx, nbg.FP32, x)))
     exp = ops.mxv("PLUS", "TIMES", rp, ci, None, x, np.float32)
     assert rel(got[lens > 0], exp[lens > 0]) <= 2e-7 and np.all(got[lens == 0] == 0)
+
+
+@pytest.mark.parametrize("tname", ["bool", "int32", "int64", "fp32", "fp64"])
+@pytest.mark.parametrize("mode", ["NONBLOCKING", "BLOCKING"])
+def test_every_operator_every_type(nbg, tname, mode):
+    """Every unary and binary operator of the ABI in every type against the oracle, element by
+    element (one rounding in the output type on both sides; integer division by zero = 0, R2),
+    on edge values: zeros, signs, large magnitudes, the integer extremes (wrapping arithmetic)."""
+    npT = {"bool": np.bool_, "int32": np.int32, "int64": np.int64, "fp32": np.float32, "fp64": np.float64}[tname]
+    t = nbg.TYPE_OF[tname]
+    if np.dtype(npT).kind == "f":
+        base = np.array([0.0, -0.0, 1.0, -2.5, 3.0, 1e-3, 7.25, -1e30, 1e30, 0.85], np.float64)
+        c0, c1 = 2.5, -1.0
+    elif npT is np.bool_:
+        base = np.array([0, 1, 1, 0, 1], np.int64)
+        c0, c1 = 1.0, 0.0
+    else:
+        info = np.iinfo(npT)
+        base = np.array([0, 1, -1, 2, -7, 5, 1000, -1000, info.max, info.min], np.int64)
+        c0, c1 = 3.0, -2.0
+    u = np.resize(base, 97).astype(npT)
+    v = np.resize(np.roll(base, 3), 97).astype(npT)
+    dev_t = nbg.NP_OF[t]
+    c = nbg.nbg_init(getattr(nbg, mode), 0)
+    try:
+        du = nbg.nbg_vector_from_dense(c, t, u.astype(dev_t))
+        dv = nbg.nbg_vector_from_dense(c, t, v.astype(dev_t))
+        for code in nbg.UNOPS:
+            got = nbg.nbg_vector_export_dense(c, nbg.nbg_apply(c, t, code, du, c0, c1)).astype(npT)
+            exp = ops.unop(code, u, npT, c0, c1)
+            assert np.array_equal(got, exp, equal_nan=np.dtype(npT).kind == "f"), (tname, code)
+        for code in nbg.BINOPS:
+            for rec, fn in ((nbg.nbg_ewise_add, ops.ewise_add), (nbg.nbg_ewise_mult, ops.ewise_mult)):
+                got = nbg.nbg_vector_export_dense(c, rec(c, t, code, du, dv, 0.85)).astype(npT)
+                exp = fn(code, u, v, npT, 0.85)
+                assert np.array_equal(got, exp, equal_nan=np.dtype(npT).kind == "f"), (tname, code)
+    finally:
+        nbg.nbg_finalize(c)

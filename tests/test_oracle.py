@@ -329,3 +329,12 @@ def test_ops_empty_fold_identities():
     x = np.array([4, -3], np.int32)
     assert list(ops.mxv("MIN", "SECOND", rp, ci, None, x, np.int32)) == [np.iinfo(np.int32).max, -3]
     assert list(ops.mxv("MAX", "SECOND", rp, ci, None, x, np.int64)) == [np.iinfo(np.int64).min, 4]
+
+
+def test_ops_integer_division_exact():
+    """C truncating division (toward zero) for integers, x / 0 = 0 (reading R2), exact beyond 2^53."""
+    a = np.array([7, -7, 7, -7, 0, 5, 2**62 + 1, -(2**62) - 3, -2**63, 1], np.int64)
+    b = np.array([2, 2, -2, -2, 3, 0, 3, 7, 3, -2**63], np.int64)
+    exp = [3, -3, -3, 3, 0, 0, (2**62 + 1) // 3, -((2**62 + 3) // 7), -(2**63 // 3), 0]
+    assert list(ops.binop("DIV", a, b, np.int64)) == exp
+    assert list(ops.unop("MINV", np.array([1, -1, 2, 0, -2**31], np.int32), np.int32)) == [1, -1, 0, 0, 0]
