@@ -478,3 +478,38 @@ def test_every_operator_every_type(nbg, tname, mode):
                 assert np.array_equal(got, exp, equal_nan=np.dtype(npT).kind == "f"), (tname, code)
     finally:
         nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("mode", ["NONBLOCKING", "BLOCKING"])
+def test_convert_and_reduce_every_type(nbg, mode):
+    """convert between every pair of types (in-range values: C conversion rules, float -> int
+    truncates toward zero; out-of-range float -> int is undefined in C and not tested) and reduce
+    with every monoid in every type (integer sums exact, float sums within 1e-12 of the exact sum)."""
+    names = ["bool", "int32", "int64", "fp32", "fp64"]
+    npT = {"bool": np.bool_, "int32": np.int32, "int64": np.int64, "fp32": np.float32, "fp64": np.float64}
+    rng = np.random.default_rng(4)
+    src = {"bool": rng.integers(0, 2, 301).astype(np.bool_),
+           "int32": rng.integers(-100000, 100000, 301).astype(np.int32),
+           "int64": rng.integers(-100000, 100000, 301).astype(np.int64),
+           "fp32": ((rng.random(301) - 0.5) * 2e4).astype(np.float32),
+           "fp64": (rng.random(301) - 0.5) * 2e4}
+    c = nbg.nbg_init(getattr(nbg, mode), 0)
+    try:
+        for a in names:
+            ta = nbg.TYPE_OF[a]
+            du = nbg.nbg_vector_from_dense(c, ta, src[a].astype(nbg.NP_OF[ta]))
+            for b in names:
+                tb = nbg.TYPE_OF[b]
+                got = nbg.nbg_vector_export_dense(c, nbg.nbg_convert(c, tb, du)).astype(npT[b])
+                assert np.array_equal(got, ops.convert(src[a], npT[b])), (a, b)
+            for mono in ("PLUS", "MIN", "MAX"):
+                for rt in ("int64", "fp64") if mono == "PLUS" else (a,):
+                    s = nbg.nbg_reduce(c, nbg.TYPE_OF[rt], mono, du)
+                    exp = float(ops.reduce(mono, ops.convert(src[a], npT[rt]), npT[rt]))
+                    got = nbg.nbg_scalar_get(c, s)
+                    if mono == "PLUS" and rt == "fp64":
+                        assert abs(got - exp) <= 1e-12 * float(np.abs(src[a].astype(np.float64)).sum()), (a, mono, rt)
+                    else:
+                        assert got == exp, (a, mono, rt)
+    finally:
+        nbg.nbg_finalize(c)
