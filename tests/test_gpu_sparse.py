@@ -242,3 +242,35 @@ def test_bitset_operands_chain(nbg, mode, tname):
             assert abs(got - exp) <= 1e-12 * float(np.abs(eb.vals).sum())
     finally:
         nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("tname", ["bool", "int32", "fp32", "fp64"])
+def test_every_operator_structured(nbg, tname):
+    """Every unary and binary operator over sparse operands (structure and values vs the oracle),
+    both representations of the result (fills around the sparse / bitset threshold)."""
+    T = {"bool": np.bool_, "int32": np.int32, "fp32": np.float32, "fp64": np.float64}[tname]
+    t = nbg.TYPE_OF[tname]
+    rng = np.random.default_rng(33)
+    n = 5000
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        for fill in (0.02, 0.4):
+            u, v = rsv(rng, n, fill, np.float64), rsv(rng, n, fill, np.float64)
+            if T is np.bool_:
+                u.vals[:] = rng.integers(0, 2, u.vals.shape[0]); v.vals[:] = rng.integers(0, 2, v.vals.shape[0])
+            u.vals = u.vals.astype(T); v.vals = v.vals.astype(T)
+            dev = nbg.NP_OF[t]
+            du = nbg.nbg_vector_from_sparse(c, t, n, u.idx.astype(np.int32), u.vals.astype(dev))
+            dv = nbg.nbg_vector_from_sparse(c, t, n, v.idx.astype(np.int32), v.vals.astype(dev))
+            eq = (lambda a, b: np.array_equal(a, b, equal_nan=True)) if np.dtype(T).kind == "f" else np.array_equal
+            for code in nbg.UNOPS:
+                i, x = nbg.nbg_vector_export_sparse(c, nbg.nbg_apply(c, t, code, du, 2.5, -1.0))
+                e = S.apply(code, u, T, 2.5, -1.0)
+                assert np.array_equal(i, e.idx) and eq(x.astype(T), e.vals), (tname, fill, code)
+            for code in nbg.BINOPS:
+                for rec, fn in ((nbg.nbg_ewise_add, S.ewise_add), (nbg.nbg_ewise_mult, S.ewise_mult)):
+                    i, x = nbg.nbg_vector_export_sparse(c, rec(c, t, code, du, dv, 0.85))
+                    e = fn(code, u, v, T, 0.85)
+                    assert np.array_equal(i, e.idx) and eq(x.astype(T), e.vals), (tname, fill, code, fn.__name__)
+    finally:
+        nbg.nbg_finalize(c)
