@@ -713,6 +713,14 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     }
     {
         PTimer pt(5);
+        if (dbg()) {
+            fprintf(stderr, "[nbg] launch %s n=%lld items=%lld", kern->name.c_str(), (long long)n, items);
+            for (int k = 0; k < p.n_in; k++) fprintf(stderr, " in%d=%p", k, args.in[k]);
+            for (int k = 0; k < p.n_out; k++) fprintf(stderr, " out%d=%p", k, args.out[k]);
+            for (int k = 0; k < p.n_sin; k++) fprintf(stderr, " sin%d=%p", k, (const void *)args.sin[k]);
+            for (int k = 0; k < p.n_red; k++) fprintf(stderr, " racc%d=%p", k, (void *)args.racc[k]);
+            fprintf(stderr, "\n");
+        }
         if (items > 0 && n > 0) launch(c, *kern, args, items, p.tp ? "spmv_p2" : (p.spmv ? "spmv" : "ewise"));
     }
 
@@ -742,7 +750,9 @@ static int64_t root_len(const NodeP &r) {
     return r->n;
 }
 
-static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
+// `len`: the index-space length of the group (root_len at grouping time; a root materialised by a
+// prerequisite pass in the meantime has dropped its inputs, so its root_len is no longer valid)
+static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t len) {
     const bool nb = c.mode == NBG_NONBLOCKING;
     for (int guard = 0; guard < 256; guard++) {
         Builder B(c);
@@ -810,7 +820,7 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots) {
             }
         }
 
-        int64_t n = B.mxv ? B.mxv->A->nrows : root_len(roots[0]);
+        int64_t n = B.mxv ? B.mxv->A->nrows : len;
         size_t nvis = B.visited.size();
         // structural keys of the base outputs (before they become leaves)
         std::vector<std::string> base_keys;
@@ -892,7 +902,7 @@ void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
     // group by index-space length (one kernel per group)
     std::map<int64_t, std::vector<NodeP>> groups;
     for (const NodeP &r : roots) groups[root_len(r)].push_back(r);
-    for (auto &g : groups) materialize_group(c, g.second);
+    for (auto &g : groups) materialize_group(c, g.second, g.first);
     c.stats.host_plan_ns += (uint64_t)(now_ns() - t0);
 }
 

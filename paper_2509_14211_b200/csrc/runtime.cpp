@@ -34,9 +34,15 @@ uint64_t hash_str(const std::string &s) {   // FNV-1a 64
 
 static constexpr size_t POOL_MAX_BUF = 64ull << 20, POOL_MAX_TOTAL = 512ull << 20;
 
+static bool pool_enabled() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("NBG_NO_POOL"); v = (e && e[0] == '1') ? 0 : 1; }
+    return v == 1;
+}
+
 Buf::~Buf() {
     if (!(owned && d && ctx)) return;
-    if (!ctx->closing && bytes <= POOL_MAX_BUF && ctx->pooled_bytes + bytes <= POOL_MAX_TOTAL) {
+    if (pool_enabled() && !ctx->closing && bytes <= POOL_MAX_BUF && ctx->pooled_bytes + bytes <= POOL_MAX_TOTAL) {
         ctx->buf_pool[bytes].push_back(d);
         ctx->pooled_bytes += bytes;
     } else {

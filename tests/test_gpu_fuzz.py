@@ -1,0 +1,182 @@
+"""Random operation DAGs through the planner (fusion, liveness, memo, scalar operands) against the
+oracle: every requested vector element by element, every requested reduction within 1e-12 of the
+exact sum scale; nonblocking (fused) and blocking (one kernel per op) in one run per program.
+Includes sparse operands, so structured regions and dense regions meet in one DAG.
+"""
+import numpy as np
+import pytest
+
+from oracle import ops
+from oracle import sparse as S
+
+pytestmark = pytest.mark.gpu
+UN = ["IDENTITY", "AINV", "ABS", "ADD_C", "MUL_C", "AXPB", "ABS_SUB_C", "ISZERO"]
+BIN = ["PLUS", "MINUS", "TIMES", "MIN", "MAX", "FIRST", "SECOND", "ABSDIFF"]
+
+
+@pytest.fixture(scope="module")
+def nbg():
+    from paper_2509_14211_b200 import nbg as m
+    return m
+
+
+def _program(rng, n_ops):
+    """A random SSA program: ('leaf', k) | ('un', code, a, c0, c1) | ('bin', kind, code, a, b) |
+    ('bind', code, a, s) with s a reduce of an earlier vector."""
+    prog = [("leaf", 0), ("leaf", 1), ("leaf", 2)]
+    for _ in range(n_ops):
+        r = rng.random()
+        a = int(rng.integers(0, len(prog)))
+        if r < 0.35:
+            prog.append(("un", UN[rng.integers(0, len(UN))], a, float(rng.integers(-3, 4)) / 2, float(rng.integers(-3, 4)) / 4))
+        elif r < 0.85:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bin", "add" if rng.random() < 0.5 else "mult", BIN[rng.integers(0, len(BIN))], a, b))
+        else:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bind", BIN[rng.integers(0, 5)], a, b))
+    return prog
+
+
+def _oracle(prog, leaves, T):
+    vals = []
+    for ins in prog:
+        if ins[0] == "leaf":
+            vals.append(leaves[ins[1]])
+        elif ins[0] == "un":
+            vals.append(S.apply(ins[1], vals[ins[2]], T, ins[3], ins[4]))
+        elif ins[0] == "bin":
+            f = S.ewise_add if ins[1] == "add" else S.ewise_mult
+            vals.append(f(ins[2], vals[ins[3]], vals[ins[4]], T))
+        else:
+            s = S.reduce("PLUS", vals[ins[3]], np.float64)
+            vals.append(S.bind2nd(ins[1], vals[ins[2]], T.type(s) if hasattr(T, "type") else np.dtype(T).type(s), T))
+    return vals
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_dags(nbg, seed):
+    rng = np.random.default_rng(1000 + seed)
+    T = np.float64
+    n = 3001
+    leaves = [S.full((rng.integers(-8, 9, n) / 4.0).astype(T)), S.full((rng.integers(-8, 9, n) / 4.0).astype(T))]
+    sp = seed % 2 == 1                     # odd seeds: the third leaf is sparse
+    if sp:
+        idx = np.nonzero(rng.random(n) < 0.1)[0]
+        leaves.append(S.sparse(n, idx, (rng.integers(-8, 9, idx.shape[0]) / 4.0).astype(T)))
+    else:
+        leaves.append(S.full((rng.integers(-8, 9, n) / 4.0).astype(T)))
+    prog = _program(rng, 14)
+    exp = _oracle(prog, leaves, T)
+    want = sorted(set(int(k) for k in rng.integers(3, len(prog), 4)))
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            h = []
+            for ins in prog:
+                if ins[0] == "leaf":
+                    L = leaves[ins[1]]
+                    if L.idx.shape[0] == n:
+                        h.append(nbg.nbg_vector_from_dense(c, nbg.FP64, L.vals))
+                    else:
+                        h.append(nbg.nbg_vector_from_sparse(c, nbg.FP64, n, L.idx.astype(np.int32), L.vals))
+                elif ins[0] == "un":
+                    h.append(nbg.nbg_apply(c, nbg.FP64, ins[1], h[ins[2]], ins[3], ins[4]))
+                elif ins[0] == "bin":
+                    f = nbg.nbg_ewise_add if ins[1] == "add" else nbg.nbg_ewise_mult
+                    h.append(f(c, nbg.FP64, ins[2], h[ins[3]], h[ins[4]]))
+                else:
+                    s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", h[ins[3]])
+                    h.append(nbg.nbg_apply_bind2nd(c, nbg.FP64, ins[1], h[ins[2]], s))
+            # drop some handles (elided intermediates), then read the wanted ones in shuffled order
+            for k in range(3, len(prog)):
+                if k not in want and rng.random() < 0.5:
+                    nbg.nbg_vector_free(c, h[k])
+                    h[k] = None
+            for k in rng.permutation(want):
+                i, x = nbg.nbg_vector_export_sparse(c, h[k])
+                e = exp[k]
+                assert np.array_equal(i, e.idx), (seed, mode, k, prog[k])
+                scale = np.maximum(np.abs(e.vals), 1.0)
+                # values: bit-exact except where a reduce-derived scalar enters (fp64 partial sums)
+                assert np.all(np.abs(x - e.vals) <= 1e-12 * scale), (seed, mode, k, prog[k])
+        finally:
+            nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_random_dags_with_mxv_and_waits(nbg, seed):
+    """As above with mxv nodes (a fixed random matrix: the fused SpMV epilogue), waits at random
+    points in the recording (partially materialised DAGs), fp32 or fp64."""
+    rng = np.random.default_rng(5000 + seed)
+    T = np.float64 if seed % 3 else np.float32
+    t = nbg.FP64 if T is np.float64 else nbg.FP32
+    n = 2049
+    lens = rng.integers(0, 12, n)
+    lens[7] = 700
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, int(l), replace=False)) for l in lens]).astype(np.int32)
+    leaves = [S.full((rng.integers(-8, 9, n) / 4.0).astype(T)) for _ in range(3)]
+    prog = [("leaf", 0), ("leaf", 1), ("leaf", 2)]
+    for _ in range(12):
+        r = rng.random()
+        a = int(rng.integers(0, len(prog)))
+        if r < 0.15:
+            prog.append(("mxv", "SECOND" if rng.random() < 0.5 else "TIMES", a))
+        elif r < 0.4:
+            prog.append(("un", UN[rng.integers(0, len(UN))], a, float(rng.integers(-3, 4)) / 2, float(rng.integers(-3, 4)) / 4))
+        elif r < 0.85:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bin", "add" if rng.random() < 0.5 else "mult", BIN[rng.integers(0, len(BIN))], a, b))
+        else:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bind", BIN[rng.integers(0, 5)], a, b))
+    # oracle, one instruction at a time
+    exp = []
+    for ins in prog:
+        if ins[0] == "leaf":
+            exp.append(leaves[ins[1]])
+        elif ins[0] == "mxv":
+            exp.append(S.full(S.mxv("PLUS", ins[1], rp, ci, None, exp[ins[2]], T)))
+        elif ins[0] == "un":
+            exp.append(S.apply(ins[1], exp[ins[2]], T, ins[3], ins[4]))
+        elif ins[0] == "bin":
+            f = S.ewise_add if ins[1] == "add" else S.ewise_mult
+            exp.append(f(ins[2], exp[ins[3]], exp[ins[4]], T))
+        else:
+            s = S.reduce("PLUS", exp[ins[3]], np.float64)
+            exp.append(S.bind2nd(ins[1], exp[ins[2]], np.dtype(T).type(s), T))
+    want = sorted(set(int(k) for k in rng.integers(3, len(prog), 4)))
+    waits = set(int(k) for k in np.nonzero(rng.random(len(prog)) < 0.15)[0] if k >= 3)
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            A = nbg.nbg_matrix_from_csr(c, n, n, rp, ci, type=t, iso=1.0)
+            h = []
+            for k, ins in enumerate(prog):
+                if ins[0] == "leaf":
+                    h.append(nbg.nbg_vector_from_dense(c, t, leaves[ins[1]].vals))
+                elif ins[0] == "mxv":
+                    h.append(nbg.nbg_mxv(c, t, "PLUS", ins[1], A, h[ins[2]]))
+                elif ins[0] == "un":
+                    h.append(nbg.nbg_apply(c, t, ins[1], h[ins[2]], ins[3], ins[4]))
+                elif ins[0] == "bin":
+                    f = nbg.nbg_ewise_add if ins[1] == "add" else nbg.nbg_ewise_mult
+                    h.append(f(c, t, ins[2], h[ins[3]], h[ins[4]]))
+                else:
+                    s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", h[ins[3]])
+                    h.append(nbg.nbg_apply_bind2nd(c, t, ins[1], h[ins[2]], s))
+                if k in waits:
+                    nbg.nbg_vector_wait(c, h[k])
+            for k in range(3, len(prog)):
+                if k not in want and rng.random() < 0.5:
+                    nbg.nbg_vector_free(c, h[k])
+                    h[k] = None
+            for k in rng.permutation(want):
+                x = nbg.nbg_vector_export_dense(c, h[k])
+                e = exp[k].vals
+                # mxv row sums and reduce-derived scalars round in fp64 partial order: relative bound
+                tol = (1e-5 if T is np.float32 else 1e-12) * np.maximum(np.abs(e), 1.0) * 64
+                assert np.all(np.abs(x.astype(np.float64) - e.astype(np.float64)) <= tol), (seed, mode, k, prog[k])
+        finally:
+            nbg.nbg_finalize(c)
