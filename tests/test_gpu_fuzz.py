@@ -180,3 +180,86 @@ def test_random_dags_with_mxv_and_waits(nbg, seed):
                 assert np.all(np.abs(x.astype(np.float64) - e.astype(np.float64)) <= tol), (seed, mode, k, prog[k])
         finally:
             nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_structured_dags(nbg, seed):
+    """Random DAGs over two sparse leaves (fills 1-30 %) and one full leaf: structured regions,
+    structured mxv, reductions read in the middle of the recording, partial waits."""
+    rng = np.random.default_rng(9000 + seed)
+    T = np.float64
+    n = 2500
+    lens = rng.integers(0, 10, n)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, int(l), replace=False)) for l in lens]).astype(np.int32)
+    leaves = []
+    for fill in (rng.choice([0.01, 0.05, 0.3]), rng.choice([0.01, 0.05, 0.3])):
+        idx = np.nonzero(rng.random(n) < fill)[0]
+        leaves.append(S.sparse(n, idx, (rng.integers(-8, 9, idx.shape[0]) / 4.0).astype(T)))
+    leaves.append(S.full((rng.integers(-8, 9, n) / 4.0).astype(T)))
+    prog = [("leaf", 0), ("leaf", 1), ("leaf", 2)]
+    for _ in range(12):
+        r = rng.random()
+        a = int(rng.integers(0, len(prog)))
+        if r < 0.1:
+            prog.append(("mxv", "TIMES", a))
+        elif r < 0.35:
+            prog.append(("un", UN[rng.integers(0, len(UN))], a, float(rng.integers(-3, 4)) / 2, float(rng.integers(-3, 4)) / 4))
+        elif r < 0.85:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bin", "add" if rng.random() < 0.5 else "mult", BIN[rng.integers(0, len(BIN))], a, b))
+        else:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bind", BIN[rng.integers(0, 5)], a, b))
+    exp = []
+    for ins in prog:
+        if ins[0] == "leaf":
+            exp.append(leaves[ins[1]])
+        elif ins[0] == "mxv":
+            exp.append(S.full(S.mxv("PLUS", ins[1], rp, ci, None, exp[ins[2]], T)))
+        elif ins[0] == "un":
+            exp.append(S.apply(ins[1], exp[ins[2]], T, ins[3], ins[4]))
+        elif ins[0] == "bin":
+            f = S.ewise_add if ins[1] == "add" else S.ewise_mult
+            exp.append(f(ins[2], exp[ins[3]], exp[ins[4]], T))
+        else:
+            s = S.reduce("PLUS", exp[ins[3]], np.float64)
+            exp.append(S.bind2nd(ins[1], exp[ins[2]], np.dtype(T).type(s), T))
+    want = sorted(set(int(k) for k in rng.integers(3, len(prog), 4)))
+    waits = set(int(k) for k in np.nonzero(rng.random(len(prog)) < 0.15)[0] if k >= 3)
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            A = nbg.nbg_matrix_from_csr(c, n, n, rp, ci, type=nbg.FP64, iso=1.0)
+            h, sc = [], {}
+            for k, ins in enumerate(prog):
+                if ins[0] == "leaf":
+                    L = leaves[ins[1]]
+                    if L.idx.shape[0] == n:
+                        h.append(nbg.nbg_vector_from_dense(c, nbg.FP64, L.vals))
+                    else:
+                        h.append(nbg.nbg_vector_from_sparse(c, nbg.FP64, n, L.idx.astype(np.int32), L.vals))
+                elif ins[0] == "mxv":
+                    h.append(nbg.nbg_mxv(c, nbg.FP64, "PLUS", ins[1], A, h[ins[2]]))
+                elif ins[0] == "un":
+                    h.append(nbg.nbg_apply(c, nbg.FP64, ins[1], h[ins[2]], ins[3], ins[4]))
+                elif ins[0] == "bin":
+                    f = nbg.nbg_ewise_add if ins[1] == "add" else nbg.nbg_ewise_mult
+                    h.append(f(c, nbg.FP64, ins[2], h[ins[3]], h[ins[4]]))
+                else:
+                    s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", h[ins[3]])
+                    sc[k] = (s, ins[3])
+                    h.append(nbg.nbg_apply_bind2nd(c, nbg.FP64, ins[1], h[ins[2]], s))
+                    if rng.random() < 0.3:         # read the scalar now (materialises its region)
+                        v = nbg.nbg_scalar_get(c, s)
+                        ref = float(S.reduce("PLUS", exp[ins[3]], np.float64))
+                        assert abs(v - ref) <= 1e-12 * max(1.0, float(np.abs(exp[ins[3]].vals).sum())), (seed, mode, k)
+                if k in waits:
+                    nbg.nbg_vector_wait(c, h[k])
+            for k in rng.permutation(want):
+                i, x = nbg.nbg_vector_export_sparse(c, h[k])
+                e = exp[k]
+                assert np.array_equal(i, e.idx), (seed, mode, k, prog[k])
+                assert np.all(np.abs(x - e.vals) <= 64e-12 * np.maximum(np.abs(e.vals), 1.0)), (seed, mode, k, prog[k])
+        finally:
+            nbg.nbg_finalize(c)
