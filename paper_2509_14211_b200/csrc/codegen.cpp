@@ -480,7 +480,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     const std::string RT = rt_narrow ? "float" : ACC;
     const int rt_bytes = rt_narrow ? 4 : 8;
     const int warp_bytes = 128 * rt_bytes + 32 * 4;
-    const int xacc_bytes = 32 * NF * 11 * 8;
+    const int xacc_bytes = 32 * NF * 12 * 8;
     const int x_bytes = (int)type_size(sp.xt);
     int nt_ = p.nt, hk_ = p.hot_kb;
     if (nt_ <= 0) spmv_variant((int)type_size(sp.xt), 0, &nt_, &hk_);
@@ -488,14 +488,14 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     int hot_bytes = hk_ * 1024;
     {   // keep all shared memory inside the carveout step the size aims at (132 / 164 / 196 KB):
         // crossing a step halves the L1 left beside it (measured cliffs)
-        const int other = NW * warp_bytes + NW * NF * 11 * 8 + 3072;   // + static smem + the driver's 1 KB per CTA
+        const int other = NW * warp_bytes + NW * NF * 12 * 8 + 3072;   // + static smem + the driver's 1 KB per CTA
         const int step = (hk_ >= 140 ? 196 : (hk_ >= 100 ? 164 : 132)) * 1024;
         if (hot_bytes > step - other) hot_bytes = std::max(0, step - other);
     }
     int hot_cap = hot_bytes / x_bytes;
     hot_cap = (hot_cap / 4) * 4;
     const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
-    const int dyn_bytes = hot_region + NW * warp_bytes + NW * NF * 11 * 8;
+    const int dyn_bytes = hot_region + NW * warp_bytes + NW * NF * 12 * 8;
     if (hot_entries) *hot_entries = hot_cap;
     (void)accw;
     // gathered element: predicated shared/global load of the raw bits, reinterpreted as XT
@@ -545,7 +545,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "  const long long* __restrict__ GRP = a.rowptr;\n";
     o << "  const int hc = (int)a.hc;\n";
     o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
-    if (NF) o << "  for (int k = threadIdx.x; k < NBG_NW * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
+    if (NF) o << "  for (int k = threadIdx.x; k < NBG_NW * NBG_NF * 12; k += blockDim.x) s_x[k] = 0ull;\n";
     // hot-column cache: 16-byte loads, 4 in flight per thread (X is 16-byte aligned, hc % 16 == 0 or tail)
     o << "  {\n";
     o << "    const int nv_ = ((((unsigned long long)X) & 15ull) == 0ull) ? (int)((hc * sizeof(" << XT << ")) >> 4) : 0;\n";
@@ -736,7 +736,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
         o << "      { double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f
-          << ") * 11, t_); }\n";
+          << ") * 12, t_); }\n";
     }
     o << "      __syncwarp();\n";
     o << "    }\n";
@@ -744,10 +744,11 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     o << "  __syncthreads();\n";
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
-        o << "  if (threadIdx.x < 11) {\n";
-        o << "    u64 v_ = 0ull;\n";
-        o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 11 + threadIdx.x]; v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
-        o << "    if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
+        o << "  if (threadIdx.x < 12) {\n";
+        o << "    u64 v_ = 0ull; double d_ = 0.0;\n";
+        o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 12 + threadIdx.x]; if (threadIdx.x == 11) d_ += __longlong_as_double((long long)x_); else v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
+        o << "    if (threadIdx.x == 11) { if (d_ != 0.0) atomicAdd((double*)&a.racc[" << p.reds[j].racc << "][12], d_); }\n";
+        o << "    else if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
         o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
         o << "  }\n";
     }
@@ -1032,14 +1033,14 @@ int gen_tp2(Gen &g, const std::string &kname) {
     o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ") " << kname << "(const KArgs a) {\n";
     o << "  __shared__ double nbg_sh[32];\n";
     o << "  __shared__ int s_ctr;\n";
-    if (NF) o << "  __shared__ u64 s_x[NBG_NW * NBG_NF * 11];\n";
+    if (NF) o << "  __shared__ u64 s_x[NBG_NW * NBG_NF * 12];\n";
     const int NU = std::max(1, g.n_uniform());
     o << "  __shared__ unsigned long long s_uni[" << NU << "];\n";
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
     o << "  const " << k.ACC << "* __restrict__ PART = (const " << k.ACC << "*)a.part;\n";
     o << "  const long long* __restrict__ RS = a.rowslot;\n";
     o << "  if (threadIdx.x == 0) s_ctr = 0;\n";
-    if (NF) o << "  for (int k = threadIdx.x; k < NBG_NW * NBG_NF * 11; k += blockDim.x) s_x[k] = 0ull;\n";
+    if (NF) o << "  for (int k = threadIdx.x; k < NBG_NW * NBG_NF * 12; k += blockDim.x) s_x[k] = 0ull;\n";
     g.emit_uniform_to_smem("s_uni");
     o << "  __syncthreads();\n";
     g.emit_red_decl();
@@ -1071,16 +1072,17 @@ int gen_tp2(Gen &g, const std::string &kname) {
     o << "    }\n";
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
-        o << "    { double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f << ") * 11, t_); }\n";
+        o << "    { double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f << ") * 12, t_); }\n";
     }
     o << "  }\n";
     o << "  __syncthreads();\n";
     for (int f = 0; f < NF; f++) {
         int j = fplus[f];
-        o << "  if (threadIdx.x < 11) {\n";
-        o << "    u64 v_ = 0ull;\n";
-        o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 11 + threadIdx.x]; v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
-        o << "    if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
+        o << "  if (threadIdx.x < 12) {\n";
+        o << "    u64 v_ = 0ull; double d_ = 0.0;\n";
+        o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 12 + threadIdx.x]; if (threadIdx.x == 11) d_ += __longlong_as_double((long long)x_); else v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
+        o << "    if (threadIdx.x == 11) { if (d_ != 0.0) atomicAdd((double*)&a.racc[" << p.reds[j].racc << "][12], d_); }\n";
+        o << "    else if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
         o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
         o << "  }\n";
     }

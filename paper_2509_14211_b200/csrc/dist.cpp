@@ -74,6 +74,18 @@ static nbg_status to_status(nbg_ctx *ctx, const Error &e) {
     return e.st;
 }
 
+// exact allreduce of an exact-accumulator slot: the limbs are integers (sum, rank-order
+// independent), the flag word is OR-ed (split / max / join: NCCL has no bitwise OR), and the fp64
+// sum of out-of-window terms is summed in fp64
+static void xacc_allreduce(nbg_ctx *ctx, Dist &D, const unsigned long long *src, unsigned long long *dst) {
+    NBG_NCCL(nccl().AllReduce(src, dst, 10, ncclInt64, ncclSum, comm_of(D), ctx->stream));
+    SlotP f3 = alloc_slot(*ctx), g3 = alloc_slot(*ctx);
+    gpu_flags_split(*ctx, src, f3->dptr());
+    NBG_NCCL(nccl().AllReduce(f3->dptr(), g3->dptr(), 3, ncclUint64, ncclMax, comm_of(D), ctx->stream));
+    gpu_flags_join(*ctx, g3->dptr(), dst);
+    NBG_NCCL(nccl().AllReduce(src + 12, dst + 12, 1, ncclFloat64, ncclSum, comm_of(D), ctx->stream));
+}
+
 extern "C" {
 
 nbg_status nbg_partition_rows(const int64_t *rowptr, int64_t n, int nparts, int64_t bytes_per_row, int64_t *cuts) {
@@ -244,10 +256,10 @@ nbg_status nbg_scalar_allreduce(nbg_ctx *ctx, nbg_scalar *out, nbg_scalar s) {
             SlotP tmp = alloc_slot(*ctx);
             NBG_CUDA(cudaMemcpyAsync(tmp->dptr(), limbs, sizeof limbs, cudaMemcpyHostToDevice, ctx->stream));
             NBG_CUDA(cudaStreamSynchronize(ctx->stream));
-            NBG_NCCL(nccl().AllReduce(tmp->dptr(), y->slot->dptr(), 11, ncclInt64, ncclSum, comm_of(D), ctx->stream));
+            xacc_allreduce(ctx, D, tmp->dptr(), y->slot->dptr());
             y->sfmt = SFmt::XACC;
         } else if (x->sfmt == SFmt::XACC) {
-            NBG_NCCL(nccl().AllReduce(x->slot->dptr(), y->slot->dptr(), 11, ncclInt64, ncclSum, comm_of(D), ctx->stream));
+            xacc_allreduce(ctx, D, x->slot->dptr(), y->slot->dptr());
             y->sfmt = SFmt::XACC;
         } else if (x->sfmt == SFmt::I64) {
             NBG_NCCL(nccl().AllReduce(x->slot->dptr() + 11, y->slot->dptr() + 11, 1, ncclInt64, ncclSum, comm_of(D), ctx->stream));

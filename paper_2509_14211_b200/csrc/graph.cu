@@ -478,6 +478,24 @@ TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta) {
 namespace {
 }  // namespace
 
+// exact-accumulator flags across ranks (dist.cpp): NCCL has no bitwise OR, so the flag word is
+// split into one word per flag, max-reduced, and joined again
+__global__ void k_flags_split(const unsigned long long *slot, unsigned long long *three) {
+    const unsigned long long f = slot[10];
+    three[0] = f & 1ull;
+    three[1] = f & 2ull;
+    three[2] = f & 4ull;
+}
+__global__ void k_flags_join(const unsigned long long *three, unsigned long long *slot) { slot[10] = three[0] | three[1] | three[2]; }
+void gpu_flags_split(Ctx &c, const unsigned long long *slot, unsigned long long *three) {
+    k_flags_split<<<1, 1, 0, c.stream>>>(slot, three);
+    NBG_CUDA(cudaGetLastError());
+}
+void gpu_flags_join(Ctx &c, const unsigned long long *three, unsigned long long *slot) {
+    k_flags_join<<<1, 1, 0, c.stream>>>(three, slot);
+    NBG_CUDA(cudaGetLastError());
+}
+
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst) {
     long long n = 1ll << g.scale;
     long long m = (long long)g.edge_factor * n;

@@ -77,14 +77,10 @@ __device__ void nbg_xacc_add(u64 *acc, double d) {
     int ex;
     if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
     int pos = ex + 160;
-    if (pos < 0) {
-        int s = -pos;
-        if (s >= 64) return;
-        m >>= s;
-        pos = 0;
-        if (m == 0) return;
-    }
-    if (pos > 235) { atomicOr(&acc[10], 8ull); return; }
+    // terms outside the window [2^-160, 2^128) are summed in fp64 in acc[12] (arrival order); a
+    // term straddling the low edge keeps its bits >= 2^-160 (an error < 2^-160, deterministic)
+    if (pos > 235 || pos + 52 < 0) { atomicAdd((double *)&acc[12], d); return; }
+    if (pos < 0) { m >>= -pos; pos = 0; if (m == 0) return; }
     int k = pos >> 5, sh = pos & 31;
     u64 lo = m << sh;
     u64 hi = sh ? (m >> (64 - sh)) : 0ull;
@@ -95,7 +91,8 @@ __device__ void nbg_xacc_add(u64 *acc, double d) {
     if (p2) atomicAdd(&acc[k + 2], p2);
 }
 
-// the same exact add into limbs the caller owns exclusively (shared memory of one warp): no atomics
+// the same exact add into limbs the caller owns exclusively (shared memory of one warp): no atomics;
+// the caller's block has 12 words (11: fp64 sum of out-of-window terms)
 __device__ void nbg_xacc_add_local(u64 *acc, double d) {
     if (d == 0.0) return;
     long long bits = __double_as_longlong(d);
@@ -108,14 +105,9 @@ __device__ void nbg_xacc_add_local(u64 *acc, double d) {
     int ex;
     if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
     int pos = ex + 160;
-    if (pos < 0) {
-        int s = -pos;
-        if (s >= 64) return;
-        m >>= s;
-        pos = 0;
-        if (m == 0) return;
-    }
-    if (pos > 235) { acc[10] |= 8ull; return; }
+    // outside the window: the caller's acc[11] holds their fp64 sum (flushed into acc[12])
+    if (pos > 235 || pos + 52 < 0) { acc[11] = __double_as_longlong(__longlong_as_double(acc[11]) + d); return; }
+    if (pos < 0) { m >>= -pos; pos = 0; if (m == 0) return; }
     int k = pos >> 5, sh = pos & 31;
     u64 lo = m << sh;
     u64 hi = sh ? (m >> (64 - sh)) : 0ull;
@@ -126,12 +118,18 @@ __device__ void nbg_xacc_add_local(u64 *acc, double d) {
     acc[k + 2] += p2;
 }
 
+__device__ double nbg_xacc_window(const u64 *L);
 __device__ double nbg_xacc_value(const u64 *L) {
     u64 flags = L[10];
     if (flags & 9ull) return __longlong_as_double(0x7ff8000000000000ll);
     if ((flags & 6ull) == 6ull) return __longlong_as_double(0x7ff8000000000000ll);
     if (flags & 2ull) return __longlong_as_double(0x7ff0000000000000ll);
     if (flags & 4ull) return __longlong_as_double((long long)0xfff0000000000000ull);
+    const double extra = __longlong_as_double((long long)L[12]);   // out-of-window terms
+    return nbg_xacc_window(L) + extra;
+}
+
+__device__ double nbg_xacc_window(const u64 *L) {
     unsigned w[11];
     long long carry = 0;
     #pragma unroll

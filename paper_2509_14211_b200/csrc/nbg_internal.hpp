@@ -436,6 +436,8 @@ void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, in
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);
 void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out);
 void host_xacc_add(unsigned long long *limbs, double d);
+void gpu_flags_split(Ctx &c, const unsigned long long *slot, unsigned long long *three);
+void gpu_flags_join(Ctx &c, const unsigned long long *three, unsigned long long *slot);
 
 // host arithmetic (used for eager iso folding and host-side scalar ops)
 double host_unop(int code, int t, double x, double c0, double c1);

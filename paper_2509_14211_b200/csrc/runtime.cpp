@@ -1,6 +1,7 @@
 // runtime.cpp -- device memory, scalar slots, events, timing, host-side arithmetic helpers.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 
 #include "nbg_internal.hpp"
 
@@ -135,12 +136,20 @@ void issue_readback(Ctx &c, Slot &s) {
 // ---------------------------------------------------------------- exact accumulator decode (host)
 // Same arithmetic as nbg_xacc_value in jit/prelude.cuh: carry-normalise the 10 limbs of signed
 // 32-bit pieces into an 11-word two's complement integer (LSB 2^-160), then round to nearest even.
+static double xacc_window(const unsigned long long *L);
+
 double xacc_to_double(const unsigned long long *L) {
     unsigned long long flags = L[10];
     if (flags & 9ull) return NAN;
     if ((flags & 6ull) == 6ull) return NAN;
     if (flags & 2ull) return INFINITY;
     if (flags & 4ull) return -INFINITY;
+    double extra;                       // fp64 sum of the terms outside the exact window
+    memcpy(&extra, &L[12], 8);
+    return xacc_window(L) + extra;
+}
+
+static double xacc_window(const unsigned long long *L) {
     uint32_t w[11];
     long long carry = 0;
     for (int k = 0; k < 10; k++) {
@@ -200,14 +209,18 @@ void host_xacc_add(unsigned long long *acc, double d) {
     int ex;
     if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
     int pos = ex + 160;
-    if (pos < 0) {
-        int s = -pos;
-        if (s >= 64) return;
-        m >>= s;
+    if (pos > 235 || pos + 52 < 0) {     // outside the window [2^-160, 2^128): fp64 in acc[12]
+        double e12;
+        memcpy(&e12, &acc[12], 8);
+        e12 += d;
+        memcpy(&acc[12], &e12, 8);
+        return;
+    }
+    if (pos < 0) {                       // straddles the low edge: keep the bits >= 2^-160
+        m >>= -pos;
         pos = 0;
         if (m == 0) return;
     }
-    if (pos > 235) { acc[10] |= 8ull; return; }
     int k = pos >> 5, sh = pos & 31;
     unsigned long long lo = m << sh;
     unsigned long long hi = sh ? (m >> (64 - sh)) : 0ull;

@@ -263,3 +263,72 @@ def test_random_structured_dags(nbg, seed):
                 assert np.all(np.abs(x - e.vals) <= 64e-12 * np.maximum(np.abs(e.vals), 1.0)), (seed, mode, k, prog[k])
         finally:
             nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_loops_speculation(nbg, seed):
+    """Loops of a random sweep body t <- f(t) (mxv of a scaled t, random elementwise epilogue,
+    a reduce-derived constant, a delta reduction read each iteration): after the first iterations
+    the planner learns loop-carried side outputs (speculation hints) and memoised invariants; every
+    iterate and every delta must still match the oracle, in both modes."""
+    rng = np.random.default_rng(7000 + seed)
+    T = np.float64
+    n = 1500
+    lens = rng.integers(0, 9, n)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, int(l), replace=False)) for l in lens]).astype(np.int32)
+    d = (rng.integers(0, 5, n) / 8.0).astype(T)            # zeros act as a "dangling" mask
+    t0 = (rng.integers(1, 9, n) / 64.0).astype(T)
+    u1 = UN[rng.integers(0, len(UN))]
+    b1 = BIN[rng.integers(0, 5)]
+    k0, k1 = float(rng.integers(-3, 4)) / 4, float(rng.integers(-3, 4)) / 8
+    iters = 8
+
+    def body_oracle(t):
+        y = S.ewise_mult("TIMES", S.full(t), S.full(d), T)
+        m = S.full(S.mxv("PLUS", "SECOND", rp, ci, None, y, T))
+        z = S.ewise_mult("TIMES", S.full(t), S.apply("ISZERO", S.full(d), T), T)
+        s = S.reduce("PLUS", z, np.float64)
+        r = S.bind2nd(b1, S.apply(u1, m, T, k0, k1), np.dtype(T).type(s * 0.5), T)
+        delta = S.reduce("PLUS", S.ewise_add("ABSDIFF", S.full(t), r, T), np.float64)
+        return r.vals, float(delta)
+
+    ts, ds = [t0], []
+    for _ in range(iters):
+        nt, dl = body_oracle(ts[-1])
+        ts.append(nt)
+        ds.append(dl)
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            A = nbg.nbg_matrix_from_csr(c, n, n, rp, ci, type=nbg.FP64, iso=1.0)
+            dv = nbg.nbg_vector_from_dense(c, nbg.FP64, d)
+            t = nbg.nbg_vector_from_dense(c, nbg.FP64, t0)
+            for it in range(iters):
+                y = nbg.nbg_ewise_mult(c, nbg.FP64, "TIMES", t, dv)
+                m = nbg.nbg_mxv(c, nbg.FP64, "PLUS", "SECOND", A, y)
+                nbg.nbg_vector_free(c, y)
+                mask = nbg.nbg_apply(c, nbg.FP64, "ISZERO", dv)
+                z = nbg.nbg_ewise_mult(c, nbg.FP64, "TIMES", t, mask)
+                nbg.nbg_vector_free(c, mask)
+                s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", z)
+                nbg.nbg_vector_free(c, z)
+                sh = nbg.nbg_scalar_apply(c, nbg.FP64, "MUL_C", s, 0.5)
+                um = nbg.nbg_apply(c, nbg.FP64, u1, m, k0, k1)
+                nbg.nbg_vector_free(c, m)
+                r = nbg.nbg_apply_bind2nd(c, nbg.FP64, b1, um, sh)
+                nbg.nbg_vector_free(c, um)
+                e = nbg.nbg_ewise_add(c, nbg.FP64, "ABSDIFF", t, r)
+                dl = nbg.nbg_reduce(c, nbg.FP64, "PLUS", e)
+                nbg.nbg_vector_free(c, e)
+                got_d = nbg.nbg_scalar_get(c, dl)
+                assert got_d == ds[it] or abs(got_d - ds[it]) <= 1e-10 * max(1.0, abs(ds[it])), (seed, mode, it)
+                nbg.nbg_vector_free(c, t)
+                t = r
+                got = nbg.nbg_vector_export_dense(c, t)
+                ex = ts[it + 1]
+                with np.errstate(invalid="ignore"):
+                    ok = (got == ex) | (np.abs(got - ex) <= 1e-10 * np.maximum(1.0, np.abs(ex))) | (np.isnan(got) & np.isnan(ex))
+                assert np.all(ok), (seed, mode, it)
+        finally:
+            nbg.nbg_finalize(c)

@@ -50,3 +50,16 @@ def test_exact_sum_specials(xsum):
     assert math.isinf(xsum(np.array([1.0, np.inf])))
     assert math.isnan(xsum(np.array([np.inf, -np.inf])))
     assert math.isnan(xsum(np.array([1.0, np.nan])))
+
+
+def test_terms_outside_the_exact_window(xsum):
+    """Terms of magnitude >= 2^128 or < 2^-160 are outside the exact window: they are summed in
+    fp64 (arrival order) and added to the window's correctly rounded value -- no NaN, no loss."""
+    big = np.array([1e40, 2e40, -1e40, 3.0])
+    assert abs(xsum(big) - math.fsum(big)) <= 4 * np.spacing(2e40)
+    assert xsum(np.array([1e300, 1e300])) == 2e300
+    tiny = np.full(7, 1e-60)
+    assert abs(xsum(tiny) - 7e-60) <= 8 * np.spacing(7e-60)
+    # a term straddling 2^-160 keeps its bits above the edge (error < 2^-160)
+    assert abs(xsum(np.array([2.0 ** -120, 1.0])) - (1.0 + 2.0 ** -120)) <= 2.0 ** -52
+    assert math.isinf(xsum(np.array([1e308, 1e308])))
