@@ -332,3 +332,65 @@ def test_random_loops_speculation(nbg, seed):
                 assert np.all(ok), (seed, mode, it)
         finally:
             nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_dags_integer(nbg, seed):
+    """Random DAGs in int32 / int64 (wrapping arithmetic, integer division excluded by the op
+    list): every element exact, reductions (int64 PLUS) exact; sparse leaves on odd seeds."""
+    rng = np.random.default_rng(3000 + seed)
+    T = np.int32 if seed % 2 == 0 else np.int64
+    t = nbg.INT32 if T is np.int32 else nbg.INT64
+    n = 1777
+    leaves = [S.full(rng.integers(-50, 51, n).astype(T)), S.full(rng.integers(-50, 51, n).astype(T))]
+    idx = np.nonzero(rng.random(n) < (0.08 if seed % 4 == 1 else 1.0))[0]
+    leaves.append(S.sparse(n, idx, rng.integers(-50, 51, idx.shape[0]).astype(T)))
+    prog = [("leaf", 0), ("leaf", 1), ("leaf", 2)]
+    for _ in range(14):
+        r = rng.random()
+        a = int(rng.integers(0, len(prog)))
+        if r < 0.35:
+            prog.append(("un", UN[rng.integers(0, len(UN))], a, float(rng.integers(-3, 4)), float(rng.integers(-3, 4))))
+        elif r < 0.85:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bin", "add" if rng.random() < 0.5 else "mult", BIN[rng.integers(0, len(BIN))], a, b))
+        else:
+            b = int(rng.integers(0, len(prog)))
+            prog.append(("bind", BIN[rng.integers(0, 5)], a, b))
+    exp = []
+    for ins in prog:
+        if ins[0] == "leaf":
+            exp.append(leaves[ins[1]])
+        elif ins[0] == "un":
+            exp.append(S.apply(ins[1], exp[ins[2]], T, ins[3], ins[4]))
+        elif ins[0] == "bin":
+            f = S.ewise_add if ins[1] == "add" else S.ewise_mult
+            exp.append(f(ins[2], exp[ins[3]], exp[ins[4]], T))
+        else:
+            s = S.reduce("PLUS", exp[ins[3]], np.int64)
+            exp.append(S.bind2nd(ins[1], exp[ins[2]], int(s), T))
+    want = sorted(set(int(k) for k in rng.integers(3, len(prog), 4)))
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            h = []
+            for ins in prog:
+                if ins[0] == "leaf":
+                    L = leaves[ins[1]]
+                    if L.idx.shape[0] == n:
+                        h.append(nbg.nbg_vector_from_dense(c, t, L.vals))
+                    else:
+                        h.append(nbg.nbg_vector_from_sparse(c, t, n, L.idx.astype(np.int32), L.vals))
+                elif ins[0] == "un":
+                    h.append(nbg.nbg_apply(c, t, ins[1], h[ins[2]], ins[3], ins[4]))
+                elif ins[0] == "bin":
+                    f = nbg.nbg_ewise_add if ins[1] == "add" else nbg.nbg_ewise_mult
+                    h.append(f(c, t, ins[2], h[ins[3]], h[ins[4]]))
+                else:
+                    s = nbg.nbg_reduce(c, nbg.INT64, "PLUS", h[ins[3]])
+                    h.append(nbg.nbg_apply_bind2nd(c, t, ins[1], h[ins[2]], s))
+            for k in rng.permutation(want):
+                i, x = nbg.nbg_vector_export_sparse(c, h[k])
+                assert np.array_equal(i, exp[k].idx) and np.array_equal(x, exp[k].vals), (seed, mode, k, prog[k])
+        finally:
+            nbg.nbg_finalize(c)
