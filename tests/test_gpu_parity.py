@@ -513,3 +513,32 @@ def test_convert_and_reduce_every_type(nbg, mode):
                         assert got == exp, (a, mono, rt)
     finally:
         nbg.nbg_finalize(c)
+
+
+def test_degenerate_sizes(nbg):
+    """Length-0 vectors through every op (both modes), graphs with no edges / only self-loops /
+    only duplicates, and PageRank on a 1-vertex graph: bit-exact against the oracle."""
+    for mode in (nbg.NONBLOCKING, nbg.BLOCKING):
+        c = nbg.nbg_init(mode, 0)
+        try:
+            z = nbg.nbg_vector_from_dense(c, nbg.FP64, np.zeros(0, np.float64))
+            e = nbg.nbg_ewise_add(c, nbg.FP64, "PLUS", nbg.nbg_apply(c, nbg.FP64, "ABS", z), z)
+            assert nbg.nbg_vector_export_dense(c, e).shape[0] == 0
+            assert nbg.nbg_scalar_get(c, nbg.nbg_reduce(c, nbg.FP64, "PLUS", e)) == 0.0
+            assert nbg.nbg_scalar_get(c, nbg.nbg_reduce(c, nbg.FP64, "MAX", z)) == -np.inf
+            sp = nbg.nbg_vector_from_sparse(c, nbg.FP32, 0, np.zeros(0, np.int32), np.zeros(0, np.float32))
+            assert nbg.nbg_vector_nvals(c, sp) == 0
+            # graphs
+            for n, src, dst in ((5, [], []), (4, [0, 1, 2, 3], [0, 1, 2, 3]), (3, [0, 0, 0, 2], [1, 1, 1, 1]), (1, [0], [0])):
+                s = np.array(src, np.int32)
+                d = np.array(dst, np.int32)
+                A, deg = nbg.nbg_matrix_from_edges(c, n, s, d)
+                rp, ci = nbg.nbg_matrix_export_csr(c, A)
+                orp, oci, odeg = oracle.build_csr(n, s, d)
+                assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+                assert np.array_equal(nbg.nbg_vector_export_dense(c, deg), odeg)
+                r, sw, _ = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=5, type=nbg.FP64)
+                ro, so, _, _ = oracle.pagerank(orp, oci, odeg, dtype=np.float64, itermax=5)
+                assert sw == so and rel(nbg.nbg_vector_export_dense(c, r), ro) <= 1e-14, (n, src, dst)
+        finally:
+            nbg.nbg_finalize(c)
