@@ -394,3 +394,42 @@ def test_random_dags_integer(nbg, seed):
                 assert np.array_equal(i, exp[k].idx) and np.array_equal(x, exp[k].vals), (seed, mode, k, prog[k])
         finally:
             nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_pagerank(nbg, seed):
+    """nbg_pagerank on random small graphs (random sizes, duplicate edges, self-loops, isolated
+    and dangling vertices, hubs), both dangling variants, fp32 / fp64, fixed-count and converged:
+    sweep counts exact, ranks within 1e-5 / 1e-10, delta history within the derived bound."""
+    import oracle
+    rng = np.random.default_rng(1100 + seed)
+    n = int(rng.integers(1, 3000))
+    m = int(rng.integers(0, 8 * n + 1))
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = (rng.integers(0, max(1, n // 50), m) if seed % 3 == 0 else rng.integers(0, n, m)).astype(np.int32)   # hubs
+    T = np.float32 if seed % 2 else np.float64
+    t = nbg.FP32 if T is np.float32 else nbg.FP64
+    tol = -1.0 if seed % 4 < 2 else (1e-6 if T is np.float32 else 1e-12)
+    uniform = seed % 5 != 0
+    c = nbg.nbg_init(nbg.NONBLOCKING if seed % 7 else nbg.BLOCKING, 0)
+    try:
+        A, deg = nbg.nbg_matrix_from_edges(c, n, src, dst)
+        orp, oci, odeg = oracle.build_csr(n, src, dst)
+        rp, ci = nbg.nbg_matrix_export_csr(c, A)
+        assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+        r, sw, hist = nbg.nbg_pagerank(c, A, deg, tol=tol, itermax=60, type=t,
+                                       dangling=nbg.PR_UNIFORM if uniform else nbg.PR_DROP)
+        ro, so, dho, _ = oracle.pagerank(orp, oci, odeg, dtype=T, itermax=60, tol=tol, uniform=uniform)
+        assert sw == so, (seed, sw, so)
+        got = nbg.nbg_vector_export_dense(c, r)
+        assert np.max(np.abs(got - ro) / np.abs(ro)) <= (1e-5 if T is np.float32 else 1e-10), seed
+        # Delta_k moves by at most sum_i |e_k,i| + |e_k-1,i| (triangle inequality, e = rank error).
+        # When most vertices dangle, c = alpha*ds/n + (1-alpha)/n carries ds's summation-order
+        # rounding into EVERY rank with the same sign, so the rank errors are correlated and add
+        # up over n (seed 4: 2709 vertices, 1567 edges) -- the bound takes the measured final
+        # error sum (the largest over the sweeps: the errors accumulate) next to the ulp bound
+        atol = 4.0 * max(float(np.spacing(np.abs(np.asarray(ro, T))).astype(np.float64).sum()),
+                         float(np.abs(np.asarray(got, np.float64) - np.asarray(ro, np.float64)).sum()))
+        assert np.all(np.abs(np.asarray(hist) - np.asarray(dho)) <= np.maximum(1e-9 * np.abs(dho), atol)), seed
+    finally:
+        nbg.nbg_finalize(c)
