@@ -427,6 +427,84 @@ static int redkind(const Gen &g, const RedOut &r) { return g.redkind(r).kind; }
 // partials added EXACTLY into per-warp fixed-point limbs, so the dynamic task order changes
 // nothing: every result is deterministic.  Summation order inside a row is fixed by the matrix
 // plan (the same for the fused and the per-op mxv).
+// The task's step loop with G groups per lane (step = 32 G groups, 4 G gathers in flight per lane):
+// lane l owns groups b + G l .. b + G l + G - 1.  Same row bookkeeping as the G = 2 loop (row-start
+// bitmask s_sbm, one segmented warp scan per step, carry across steps), generalised over the G
+// group positions of a lane: the scan value is the sum since the lane's last row start (the whole
+// lane when none starts in it); rows that end inside the lane are written after the scan.
+static void gen_spmv_steps_g(Gen &g, int G, const std::string &ACC, const std::string &IDENT, const char *XT) {
+    auto &o = g.o;
+    const std::string gs = std::to_string(G), ss = std::to_string(32 * G);
+    for (int k = 0; k < G; k++)
+        o << "      int4 q" << k << " = (" << gs << " * lane + " << k << " < NG) ? __ldcs(CG + G0 + " << gs << " * lane + " << k
+          << ") : make_int4(-1, -1, -1, -1);\n";
+    o << "      int rs_[4];\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
+    o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
+    o << "      unsigned nem_[4];\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) {\n";
+    o << "        const int nx = __shfl_down_sync(0xffffffffu, rs_[r], 1);\n";
+    o << "        const int nf = __shfl_sync(0xffffffffu, r < 3 ? rs_[r < 3 ? r + 1 : 3] : r128_, 0);\n";
+    o << "        const int re = (lane == 31) ? nf : nx;\n";
+    o << "        nem_[r] = __ballot_sync(0xffffffffu, lane + 32 * r < R && re > rs_[r]);\n";
+    o << "      }\n";
+    o << "      s_sbm[lane] = 0u;\n";
+    o << "      __syncwarp();\n";
+    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) if ((nem_[r] >> lane) & 1u) atomicOr(&s_sbm[rs_[r] >> 5], 1u << (rs_[r] & 31));\n";
+    o << "      __syncwarp();\n";
+    o << "      " << ACC << " carry = " << IDENT << ";\n";
+    o << "      int nstarted = 0;\n";
+    o << "      for (int b = 0; b < NG; b += " << ss << ") {\n";
+    o << "        const long long P_ = 4 * (G0 + b + " << gs << " * lane);\n";
+    for (int k = 0; k < G; k++) o << "        const int4 c" << k << " = q" << k << ";\n";
+    for (int k = 0; k < G; k++)
+        o << "        const " << XT << " g" << k << "x = NBG_GV(c" << k << ".x), g" << k << "y = NBG_GV(c" << k << ".y), g" << k
+          << "z = NBG_GV(c" << k << ".z), g" << k << "w = NBG_GV(c" << k << ".w);\n";
+    o << "        if (b + " << ss << " < NG) {\n";
+    for (int k = 0; k < G; k++)
+        o << "          q" << k << " = (b + " << ss << " + " << gs << " * lane + " << k << " < NG) ? __ldcs(CG + G0 + b + " << ss << " + " << gs
+          << " * lane + " << k << ") : make_int4(-1, -1, -1, -1);\n";
+    o << "        }\n";
+    // row starts of the step: G words over positions [b, b + 32 G)
+    o << "        const int lw_ = (" << gs << " * lane) >> 5, sh_ = (" << gs << " * lane) & 31;\n";
+    o << "        int before = 0, total_ = 0;\n";
+    o << "        #pragma unroll\n        for (int w = 0; w < " << gs << "; w++) { const int pc = __popc(s_sbm[(b >> 5) + w]); total_ += pc; if (w < lw_) before += pc; }\n";
+    o << "        const unsigned Mw = s_sbm[(b >> 5) + lw_];\n";
+    o << "        before += __popc(Mw & ((1u << sh_) - 1u));\n";
+    o << "        const unsigned bits_ = (Mw >> sh_) & " << ((1u << G) - 1u) << "u;\n";
+    const char *f4[4] = {"x", "y", "z", "w"};
+    for (int k = 0; k < G; k++) {
+        o << "        " << ACC << " v" << k << " = NBG_TV(c" << k << ".x, P_ + " << 4 * k << ", g" << k << "x);";
+        for (int e = 1; e < 4; e++)
+            o << " v" << k << " = NBG_ADD(v" << k << ", NBG_TV(c" << k << "." << f4[e] << ", P_ + " << 4 * k + e << ", g" << k << f4[e] << "));";
+        o << "\n";
+    }
+    // scan value: sum since the lane's last row start (whole lane if none)
+    o << "        " << ACC << " S = " << IDENT << ";\n";
+    for (int k = 0; k < G; k++) o << "        S = ((bits_ >> " << k << ") & 1u) ? v" << k << " : NBG_ADD(S, v" << k << ");\n";
+    o << "        if (lane == 0 && bits_ == 0u) S = NBG_ADD(carry, S);\n";
+    o << "        const unsigned H_ = __ballot_sync(0xffffffffu, bits_ != 0u) | 1u;\n";
+    o << "        const int seg_ = 31 - __clz(H_ & ((2u << lane) - 1u));\n";
+    o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
+    o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
+    o << "          if (lane - d >= seg_) S = NBG_ADD(Sy, S);\n";
+    o << "        }\n";
+    o << "        " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
+    o << "        if (lane == 0) Sp = carry;\n";
+    // rows ending inside the lane: before its first start the row continues from Sp
+    o << "        {\n";
+    o << "          " << ACC << " run_ = Sp; int wi_ = nstarted + before - 1; bool st_ = false;\n";
+    for (int k = 0; k < G; k++) {
+        o << "          if ((bits_ >> " << k << ") & 1u) { if (st_ || " << (k > 0 ? "true" : "lane > 0 || nstarted > 0")
+          << ") s_racc[wi_] = run_; wi_++; st_ = true; run_ = v" << k << "; }";
+        o << (k + 1 < G ? " else run_ = NBG_ADD(run_, v" + std::to_string(k) + ");\n" : "\n");
+    }
+    o << "        }\n";
+    o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
+    o << "        nstarted += total_;\n";
+    o << "      }\n";
+}
+
 int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     const Prog &p = g.p;
     auto &o = g.o;
@@ -607,87 +685,92 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
             o << "      }\n";
         }
     }
-    o << "      int4 qa = (2 * lane < NG) ? __ldcs(CG + G0 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-    o << "      int4 qb = (2 * lane + 1 < NG) ? __ldcs(CG + G0 + 2 * lane + 1) : make_int4(-1, -1, -1, -1);\n";
-    if (gpipe) {
-        // gathers one step ahead: step b + 64's values are in flight while step b is reduced
-        o << "      int4 ca = qa, cb = qb;\n";
-        o << "      " << XT << " h0 = NBG_GV(ca.x), h1 = NBG_GV(ca.y), h2 = NBG_GV(ca.z), h3 = NBG_GV(ca.w);\n";
-        o << "      " << XT << " h4 = NBG_GV(cb.x), h5 = NBG_GV(cb.y), h6 = NBG_GV(cb.z), h7 = NBG_GV(cb.w);\n";
-        o << "      qa = (64 + 2 * lane < NG) ? __ldcs(CG + G0 + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-        o << "      qb = (65 + 2 * lane < NG) ? __ldcs(CG + G0 + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-    }
-    o << "      int rs_[4];\n";
-    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
-    o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
-    o << "      unsigned nem_[4];\n";
-    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) {\n";
-    o << "        const int nx = __shfl_down_sync(0xffffffffu, rs_[r], 1);\n";
-    o << "        const int nf = __shfl_sync(0xffffffffu, r < 3 ? rs_[r < 3 ? r + 1 : 3] : r128_, 0);\n";
-    o << "        const int re = (lane == 31) ? nf : nx;                     // end (exclusive) of row lane + 32 r\n";
-    o << "        nem_[r] = __ballot_sync(0xffffffffu, lane + 32 * r < R && re > rs_[r]);\n";
-    o << "      }\n";
-    // the task's row starts as a bitmask over its groups (tasks hold < 1024 groups): one bit per
-    // non-empty row, set once per task instead of recomputed every step
-    o << "      s_sbm[lane] = 0u;\n";
-    o << "      __syncwarp();\n";
-    o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) if ((nem_[r] >> lane) & 1u) atomicOr(&s_sbm[rs_[r] >> 5], 1u << (rs_[r] & 31));\n";
-    o << "      __syncwarp();\n";
-    o << "      " << ACC << " carry = " << IDENT << ";\n";
-    o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
-    o << "      for (int b = 0; b < NG; b += 64) {\n";
-    o << "        const long long P_ = 4 * (G0 + b + 2 * lane);\n";
-    if (gpipe) {
-        o << "        const int4 ca_ = ca, cb_ = cb;\n";
-        o << "        const " << XT << " g0 = h0, g1 = h1, g2 = h2, g3 = h3, g4 = h4, g5 = h5, g6 = h6, g7 = h7;\n";
-        o << "        if (b + 64 < NG) {\n";
-        o << "          ca = qa; cb = qb;\n";
-        o << "          h0 = NBG_GV(ca.x); h1 = NBG_GV(ca.y); h2 = NBG_GV(ca.z); h3 = NBG_GV(ca.w);\n";
-        o << "          h4 = NBG_GV(cb.x); h5 = NBG_GV(cb.y); h6 = NBG_GV(cb.z); h7 = NBG_GV(cb.w);\n";
-        o << "          if (b + 128 < NG) {\n";
-        o << "            qa = (b + 128 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 128 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-        o << "            qb = (b + 129 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 129 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-        o << "          }\n";
-        o << "        }\n";
-        o << "        const int4 ca0 = ca_, cb0 = cb_;\n";
-        o << "#define ca ca0\n#define cb cb0\n";
+    const int GPL = gpipe ? 2 : spmv_groups_per_lane();
+    if (GPL != 2) {
+        gen_spmv_steps_g(g, GPL, ACC, IDENT, XT);
     } else {
-        o << "        const int4 ca = qa, cb = qb;\n";
-        o << "        const " << XT << " g0 = NBG_GV(ca.x), g1 = NBG_GV(ca.y), g2 = NBG_GV(ca.z), g3 = NBG_GV(ca.w);\n";
-        o << "        const " << XT << " g4 = NBG_GV(cb.x), g5 = NBG_GV(cb.y), g6 = NBG_GV(cb.z), g7 = NBG_GV(cb.w);\n";
-        o << "        if (b + 64 < NG) {\n";
-        o << "          qa = (b + 64 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
-        o << "          qb = (b + 65 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "      int4 qa = (2 * lane < NG) ? __ldcs(CG + G0 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        o << "      int4 qb = (2 * lane + 1 < NG) ? __ldcs(CG + G0 + 2 * lane + 1) : make_int4(-1, -1, -1, -1);\n";
+        if (gpipe) {
+            // gathers one step ahead: step b + 64's values are in flight while step b is reduced
+            o << "      int4 ca = qa, cb = qb;\n";
+            o << "      " << XT << " h0 = NBG_GV(ca.x), h1 = NBG_GV(ca.y), h2 = NBG_GV(ca.z), h3 = NBG_GV(ca.w);\n";
+            o << "      " << XT << " h4 = NBG_GV(cb.x), h5 = NBG_GV(cb.y), h6 = NBG_GV(cb.z), h7 = NBG_GV(cb.w);\n";
+            o << "      qa = (64 + 2 * lane < NG) ? __ldcs(CG + G0 + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+            o << "      qb = (65 + 2 * lane < NG) ? __ldcs(CG + G0 + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+        }
+        o << "      int rs_[4];\n";
+        o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) { const int j = lane + 32 * r; rs_[r] = (j <= R) ? (int)(GRP[tl.x + j] - G0) : NG; }\n";
+        o << "      const int r128_ = (lane == 0 && 128 <= R) ? (int)(GRP[tl.x + 128] - G0) : NG;\n";
+        o << "      unsigned nem_[4];\n";
+        o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) {\n";
+        o << "        const int nx = __shfl_down_sync(0xffffffffu, rs_[r], 1);\n";
+        o << "        const int nf = __shfl_sync(0xffffffffu, r < 3 ? rs_[r < 3 ? r + 1 : 3] : r128_, 0);\n";
+        o << "        const int re = (lane == 31) ? nf : nx;                     // end (exclusive) of row lane + 32 r\n";
+        o << "        nem_[r] = __ballot_sync(0xffffffffu, lane + 32 * r < R && re > rs_[r]);\n";
+        o << "      }\n";
+        // the task's row starts as a bitmask over its groups (tasks hold < 1024 groups): one bit per
+        // non-empty row, set once per task instead of recomputed every step
+        o << "      s_sbm[lane] = 0u;\n";
+        o << "      __syncwarp();\n";
+        o << "      #pragma unroll\n      for (int r = 0; r < 4; r++) if ((nem_[r] >> lane) & 1u) atomicOr(&s_sbm[rs_[r] >> 5], 1u << (rs_[r] & 31));\n";
+        o << "      __syncwarp();\n";
+        o << "      " << ACC << " carry = " << IDENT << ";\n";
+        o << "      int nstarted = 0;                                          // nonempty rows started before the step\n";
+        o << "      for (int b = 0; b < NG; b += 64) {\n";
+        o << "        const long long P_ = 4 * (G0 + b + 2 * lane);\n";
+        if (gpipe) {
+            o << "        const int4 ca_ = ca, cb_ = cb;\n";
+            o << "        const " << XT << " g0 = h0, g1 = h1, g2 = h2, g3 = h3, g4 = h4, g5 = h5, g6 = h6, g7 = h7;\n";
+            o << "        if (b + 64 < NG) {\n";
+            o << "          ca = qa; cb = qb;\n";
+            o << "          h0 = NBG_GV(ca.x); h1 = NBG_GV(ca.y); h2 = NBG_GV(ca.z); h3 = NBG_GV(ca.w);\n";
+            o << "          h4 = NBG_GV(cb.x); h5 = NBG_GV(cb.y); h6 = NBG_GV(cb.z); h7 = NBG_GV(cb.w);\n";
+            o << "          if (b + 128 < NG) {\n";
+            o << "            qa = (b + 128 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 128 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+            o << "            qb = (b + 129 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 129 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+            o << "          }\n";
+            o << "        }\n";
+            o << "        const int4 ca0 = ca_, cb0 = cb_;\n";
+            o << "#define ca ca0\n#define cb cb0\n";
+        } else {
+            o << "        const int4 ca = qa, cb = qb;\n";
+            o << "        const " << XT << " g0 = NBG_GV(ca.x), g1 = NBG_GV(ca.y), g2 = NBG_GV(ca.z), g3 = NBG_GV(ca.w);\n";
+            o << "        const " << XT << " g4 = NBG_GV(cb.x), g5 = NBG_GV(cb.y), g6 = NBG_GV(cb.z), g7 = NBG_GV(cb.w);\n";
+            o << "        if (b + 64 < NG) {\n";
+            o << "          qa = (b + 64 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 64 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+            o << "          qb = (b + 65 + 2 * lane < NG) ? __ldcs(CG + G0 + b + 65 + 2 * lane) : make_int4(-1, -1, -1, -1);\n";
+            o << "        }\n";
+        }
+        // row starts of this step: two 32-bit words over positions [0, 64)
+        o << "        const unsigned M0 = s_sbm[b >> 5], M1 = s_sbm[(b >> 5) + 1];\n";
+        o << "        const unsigned Mw = lane < 16 ? M0 : M1;\n";
+        o << "        const int sh_ = (2 * lane) & 31;\n";
+        o << "        const bool s0 = (Mw >> sh_) & 1u, s1 = (Mw >> (sh_ + 1)) & 1u;\n";
+        o << "        const int before = (lane < 16 ? 0 : __popc(M0)) + __popc(Mw & ((1u << sh_) - 1u));   // starts before position 2 lane\n";
+        o << "        " << ACC << " v0 = NBG_TV(ca.x, P_, g0);\n";
+        o << "        v0 = NBG_ADD(v0, NBG_TV(ca.y, P_ + 1, g1)); v0 = NBG_ADD(v0, NBG_TV(ca.z, P_ + 2, g2)); v0 = NBG_ADD(v0, NBG_TV(ca.w, P_ + 3, g3));\n";
+        o << "        " << ACC << " v1 = NBG_TV(cb.x, P_ + 4, g4);\n";
+        o << "        v1 = NBG_ADD(v1, NBG_TV(cb.y, P_ + 5, g5)); v1 = NBG_ADD(v1, NBG_TV(cb.z, P_ + 6, g6)); v1 = NBG_ADD(v1, NBG_TV(cb.w, P_ + 7, g7));\n";
+        // scan value: the segment open at the lane's end; lane 0 continues the carried row
+        o << "        " << ACC << " S = s1 ? v1 : NBG_ADD(v0, v1);\n";
+        o << "        if (lane == 0 && !s0 && !s1) S = NBG_ADD(carry, S);\n";
+        // segmented inclusive scan bounded by the lane's segment start (highest head lane <= lane)
+        o << "        const unsigned H_ = __ballot_sync(0xffffffffu, s0 || s1) | 1u;\n";
+        o << "        const int seg_ = 31 - __clz(H_ & ((2u << lane) - 1u));\n";
+        o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
+        o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
+        o << "          if (lane - d >= seg_) S = NBG_ADD(Sy, S);\n";
         o << "        }\n";
+        o << "        " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
+        o << "        if (lane == 0) Sp = carry;                                   // running total before position 0\n";
+        o << "        if (s0 && (lane > 0 || nstarted > 0)) s_racc[nstarted + before - 1] = Sp;          // row ending at 2 lane - 1\n";
+        o << "        if (s1) s_racc[nstarted + before + (s0 ? 1 : 0) - 1] = s0 ? v0 : NBG_ADD(Sp, v0);   // row ending at 2 lane\n";
+        o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
+        o << "        nstarted += __popc(M0) + __popc(M1);\n";
+        if (gpipe) o << "#undef ca\n#undef cb\n";
+        o << "      }\n";
     }
-    // row starts of this step: two 32-bit words over positions [0, 64)
-    o << "        const unsigned M0 = s_sbm[b >> 5], M1 = s_sbm[(b >> 5) + 1];\n";
-    o << "        const unsigned Mw = lane < 16 ? M0 : M1;\n";
-    o << "        const int sh_ = (2 * lane) & 31;\n";
-    o << "        const bool s0 = (Mw >> sh_) & 1u, s1 = (Mw >> (sh_ + 1)) & 1u;\n";
-    o << "        const int before = (lane < 16 ? 0 : __popc(M0)) + __popc(Mw & ((1u << sh_) - 1u));   // starts before position 2 lane\n";
-    o << "        " << ACC << " v0 = NBG_TV(ca.x, P_, g0);\n";
-    o << "        v0 = NBG_ADD(v0, NBG_TV(ca.y, P_ + 1, g1)); v0 = NBG_ADD(v0, NBG_TV(ca.z, P_ + 2, g2)); v0 = NBG_ADD(v0, NBG_TV(ca.w, P_ + 3, g3));\n";
-    o << "        " << ACC << " v1 = NBG_TV(cb.x, P_ + 4, g4);\n";
-    o << "        v1 = NBG_ADD(v1, NBG_TV(cb.y, P_ + 5, g5)); v1 = NBG_ADD(v1, NBG_TV(cb.z, P_ + 6, g6)); v1 = NBG_ADD(v1, NBG_TV(cb.w, P_ + 7, g7));\n";
-    // scan value: the segment open at the lane's end; lane 0 continues the carried row
-    o << "        " << ACC << " S = s1 ? v1 : NBG_ADD(v0, v1);\n";
-    o << "        if (lane == 0 && !s0 && !s1) S = NBG_ADD(carry, S);\n";
-    // segmented inclusive scan bounded by the lane's segment start (highest head lane <= lane)
-    o << "        const unsigned H_ = __ballot_sync(0xffffffffu, s0 || s1) | 1u;\n";
-    o << "        const int seg_ = 31 - __clz(H_ & ((2u << lane) - 1u));\n";
-    o << "        #pragma unroll\n        for (int d = 1; d < 32; d <<= 1) {\n";
-    o << "          const " << ACC << " Sy = __shfl_up_sync(0xffffffffu, S, d);\n";
-    o << "          if (lane - d >= seg_) S = NBG_ADD(Sy, S);\n";
-    o << "        }\n";
-    o << "        " << ACC << " Sp = __shfl_up_sync(0xffffffffu, S, 1);\n";
-    o << "        if (lane == 0) Sp = carry;                                   // running total before position 0\n";
-    o << "        if (s0 && (lane > 0 || nstarted > 0)) s_racc[nstarted + before - 1] = Sp;          // row ending at 2 lane - 1\n";
-    o << "        if (s1) s_racc[nstarted + before + (s0 ? 1 : 0) - 1] = s0 ? v0 : NBG_ADD(Sp, v0);   // row ending at 2 lane\n";
-    o << "        carry = __shfl_sync(0xffffffffu, S, 31);\n";
-    o << "        nstarted += __popc(M0) + __popc(M1);\n";
-    if (gpipe) o << "#undef ca\n#undef cb\n";
-    o << "      }\n";
     o << "      if (is_chunk) {\n";
     o << "        if (lane == 0) {\n";
     o << "          const " << ACC << " t = carry;\n";
@@ -1269,6 +1352,16 @@ bool spmv_gather_pipeline() {
 int spmv_lpr_mode() {   // read at every region launch (the signature records the skeleton)
     const char *e = getenv("NBG_SPMV_LPR");
     return (e && *e) ? (e[0] == '1' ? 1 : 0) : -1;
+}
+
+int spmv_groups_per_lane() {   // NBG_SPMV_GPL: groups per lane per step of the task skeleton (2 or 4)
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("NBG_SPMV_GPL");
+        v = (e && *e) ? atoi(e) : 2;
+        if (v != 1 && v != 2 && v != 4) v = 2;
+    }
+    return v;
 }
 
 int spmv_threads(int xsize) {
