@@ -296,15 +296,23 @@ nbg_status nbg_get_timing(nbg_ctx *ctx, const char *cls, double *total_ms, int64
 
 // ---------------------------------------------------------------- matrices
 
-static BufP upload(Ctx &c, const void *p, size_t bytes, int space, int own) {
+// sync = false: the caller synchronises the stream before it returns (several host copies then
+// queue back to back instead of one round trip each), and on every error path (HostCopiesDone)
+static BufP upload(Ctx &c, const void *p, size_t bytes, int space, int own, bool sync = true) {
     if (bytes == 0) return alloc_buf(c, 0);
     // borrowed device memory is used in place when 16-byte aligned (vector loads); else copied
     if (space == NBG_DEVICE && own == NBG_BORROW && ((uintptr_t)p % 16) == 0) return borrow_buf(c, const_cast<void *>(p), bytes);
     BufP b = alloc_buf(c, bytes);
     NBG_CUDA(cudaMemcpyAsync(b->d, p, bytes, space == NBG_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream));
-    if (space == NBG_HOST) NBG_CUDA(cudaStreamSynchronize(c.stream));   // caller may reuse its buffer
+    if (space == NBG_HOST && sync) NBG_CUDA(cudaStreamSynchronize(c.stream));   // caller may reuse its buffer
     return b;
 }
+
+// the caller's host buffers may be reused once the call returns, error or not
+struct HostCopiesDone {
+    Ctx &c;
+    ~HostCopiesDone() { cudaStreamSynchronize(c.stream); }
+};
 
 nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64_t ncols, int64_t nnz,
                                const int64_t *rowptr, const int32_t *colidx, const void *vals, int type, double iso,
@@ -326,9 +334,10 @@ nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64
     M->nnz = nnz;
     M->type = type;
     M->iso = host_round(type, iso);
-    M->rowptr = upload(*ctx, rowptr, (size_t)(nrows + 1) * 8, space, own);
-    M->colidx = upload(*ctx, colidx, (size_t)nnz * 4, space, own);
-    if (vals) M->vals = upload(*ctx, vals, (size_t)nnz * type_size(type), space, own);
+    HostCopiesDone done_{*ctx};
+    M->rowptr = upload(*ctx, rowptr, (size_t)(nrows + 1) * 8, space, own, false);
+    M->colidx = upload(*ctx, colidx, (size_t)nnz * 4, space, own, false);
+    if (vals) M->vals = upload(*ctx, vals, (size_t)nnz * type_size(type), space, own, false);
     // structural validation on the device: row pointers and column range
     int bad = gpu_validate_csr(*ctx, nrows, ncols, nnz, (const long long *)M->rowptr->d, (const int *)M->colidx->d);
     if (bad & 1) fail(NBG_INVALID_VALUE, "rowptr must start at 0, end at nnz and be non-decreasing");
@@ -354,9 +363,10 @@ nbg_status nbg_matrix_from_edges(nbg_ctx *ctx, nbg_matrix *AT, nbg_vector *deg, 
     CHECK(space == NBG_HOST || space == NBG_DEVICE, NBG_INVALID_VALUE, "bad space");
     BufP ds, dd;
     const int32_t *s = src, *d = dst;
+    HostCopiesDone done_{*ctx};
     if (space == NBG_HOST && m > 0) {
-        ds = upload(*ctx, src, (size_t)m * 4, NBG_HOST, NBG_COPY);
-        dd = upload(*ctx, dst, (size_t)m * 4, NBG_HOST, NBG_COPY);
+        ds = upload(*ctx, src, (size_t)m * 4, NBG_HOST, NBG_COPY, false);
+        dd = upload(*ctx, dst, (size_t)m * 4, NBG_HOST, NBG_COPY, false);
         s = (const int32_t *)ds->d;
         d = (const int32_t *)dd->d;
     }
