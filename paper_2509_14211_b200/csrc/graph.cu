@@ -221,11 +221,12 @@ __global__ void k_short_groups(long long n, const long long *grp, long long *ngs
     }
 }
 // fl[i]: a task starts at row i; fll[i]: row i is long
-__global__ void k_task_flags(long long n, const long long *grp, const long long *gs, unsigned char *fl, unsigned char *fll) {
+__global__ void k_task_flags(long long n, const long long *grp, const long long *gs, unsigned char *fl, unsigned char *fll, int trows,
+                             long long tg) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const bool lg = grp[i + 1] - grp[i] > SP_LONG_G;
         const bool lgp = i > 0 && grp[i] - grp[i - 1] > SP_LONG_G;
-        const bool st = i == 0 || (i % SP_TASK_ROWS) == 0 || lg || lgp || (gs[i] / SP_TASK_G != gs[i - 1] / SP_TASK_G);
+        const bool st = i == 0 || (i % trows) == 0 || lg || lgp || (gs[i] / tg != gs[i - 1] / tg);
         fl[i] = st ? 1 : 0;
         fll[i] = lg ? 1 : 0;
     }
@@ -676,8 +677,14 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
         NBG_CUDA(cub::DeviceScan::ExclusiveSum(tmp->d, tb, (long long *)ngs->d, (long long *)gshort->d, (int64_t)(n + 1), c.stream));
         BufP fl = alloc_buf(c, (size_t)std::max<long long>(n, 1)), fll = alloc_buf(c, (size_t)std::max<long long>(n, 1));
+        // small matrices: shorter tasks (32 / 64 rows, group budget 4 per row) so that enough warps
+        // share the sweep -- a 128-row task is a chain of dependent steps run by one warp (C1: one
+        // CTA, 8 busy warps, 4 steps each)
+        const long long want = 4ll * c.num_sms;
+        const int trows = (n / SP_TASK_ROWS >= want) ? SP_TASK_ROWS : (n / 64 >= want ? 64 : 32);
+        const long long tg = trows == SP_TASK_ROWS ? SP_TASK_G : 4ll * trows;
         k_task_flags<<<gr, 256, 0, c.stream>>>(n, (const long long *)P->grp->d, (const long long *)gshort->d, (unsigned char *)fl->d,
-                                              (unsigned char *)fll->d);
+                                              (unsigned char *)fll->d, trows, tg);
         BufP starts = alloc_buf(c, (size_t)std::max<long long>(n, 1) * 4), lrows = alloc_buf(c, (size_t)std::max<long long>(n, 1) * 4);
         BufP cnts = alloc_buf(c, 16);
         thrust::counting_iterator<int> it0(0);

@@ -341,6 +341,7 @@ struct Ctx {
     // scalar slabs
     SlabP cur_slab;
     std::vector<cudaEvent_t> event_pool;
+    std::vector<cudaEvent_t> timing_pool;   // recycled timing events (nbg_set_timing)
 
     // freed device buffers kept for reuse by size (all work is ordered on `stream`, so a buffer
     // whose last handle died can back a later allocation without a cudaFreeAsync/MallocAsync pair)

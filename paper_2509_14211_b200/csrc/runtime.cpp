@@ -252,18 +252,29 @@ double slot_value(const unsigned long long *s, SFmt fmt) {
 
 // ---------------------------------------------------------------- timing
 
+// timing events are recycled (creating two events per launch cost ≈ 2 µs of host time per wait)
+static cudaEvent_t get_timing_event(Ctx &c) {
+    if (!c.timing_pool.empty()) {
+        cudaEvent_t e = c.timing_pool.back();
+        c.timing_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    NBG_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
 void timing_begin(Ctx &c, const char *cls, cudaEvent_t *ev0) {
     *ev0 = nullptr;
     if (!c.timing) return;
-    NBG_CUDA(cudaEventCreate(ev0));
+    *ev0 = get_timing_event(c);
     NBG_CUDA(cudaEventRecord(*ev0, c.stream));
     (void)cls;
 }
 
 void timing_end(Ctx &c, const char *cls, cudaEvent_t ev0) {
     if (!c.timing || !ev0) return;
-    cudaEvent_t ev1;
-    NBG_CUDA(cudaEventCreate(&ev1));
+    cudaEvent_t ev1 = get_timing_event(c);
     NBG_CUDA(cudaEventRecord(ev1, c.stream));
     c.tclass[cls].pending.push_back({ev0, ev1});
 }
@@ -276,8 +287,8 @@ void timing_collect(Ctx &c) {
             NBG_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
             kv.second.ms += ms;
             kv.second.launches++;
-            cudaEventDestroy(pr.first);
-            cudaEventDestroy(pr.second);
+            c.timing_pool.push_back(pr.first);
+            c.timing_pool.push_back(pr.second);
         }
         kv.second.pending.clear();
     }
@@ -396,6 +407,12 @@ Ctx::~Ctx() {
     buf_pool.clear();
     if (stream) cudaStreamSynchronize(stream);
     for (auto e : event_pool) cudaEventDestroy(e);
+    for (auto e : timing_pool) cudaEventDestroy(e);
+    for (auto &kv : tclass)
+        for (auto &pr : kv.second.pending) {
+            cudaEventDestroy(pr.first);
+            cudaEventDestroy(pr.second);
+        }
     if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
