@@ -542,3 +542,26 @@ def test_degenerate_sizes(nbg):
                 assert sw == so and rel(nbg.nbg_vector_export_dense(c, r), ro) <= 1e-14, (n, src, dst)
         finally:
             nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("n,hubs,m", [(4000, 3, 60000), (5000, 1, 40000), (9000, 2, 70000)])
+def test_small_matrix_with_long_rows(nbg, ctx, n, hubs, m):
+    """Small matrices (fewer than 4 x SMs 128-row tasks) run 32-row warp tasks; rows longer than
+    512 groups (2048 entries) are still cut into chunks combined by a ticket: both together, fp32
+    and fp64, PageRank and plain mxv against the oracle."""
+    rng = np.random.default_rng(n + m)
+    src = rng.integers(0, n, m).astype(np.int32)
+    dst = np.where(rng.random(m) < 0.8, rng.integers(0, hubs, m), rng.integers(0, n, m)).astype(np.int32)
+    A, deg = nbg.nbg_matrix_from_edges(ctx, n, src, dst)
+    orp, oci, odeg = oracle.build_csr(n, src, dst)
+    lens = np.diff(orp)
+    assert int(lens.max()) > 2048                                  # at least one chunked row
+    for T, npT, tolr in ((nbg.FP32, np.float32, 1e-5), (nbg.FP64, np.float64, 1e-12)):
+        r, sw, hist = nbg.nbg_pagerank(ctx, A, deg, tol=-1.0, itermax=15, type=T)
+        ro, so, dho, _ = oracle.pagerank(orp, oci, odeg, dtype=npT, itermax=15)
+        assert sw == so
+        assert rel(nbg.nbg_vector_export_dense(ctx, r), ro) <= tolr
+        x = rng.random(n).astype(npT)
+        got = nbg.nbg_vector_export_dense(ctx, nbg.nbg_mxv(ctx, T, "PLUS", "TIMES", A, nbg.nbg_vector_from_dense(ctx, T, x)))
+        exp = ops.mxv("PLUS", "TIMES", orp, oci, None, x, npT)
+        assert rel(got[lens > 0], exp[lens > 0]) <= (2e-7 if T == nbg.FP32 else 1e-14) and np.all(got[lens == 0] == 0)
