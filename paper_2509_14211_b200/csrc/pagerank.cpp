@@ -15,8 +15,10 @@
 // Convergence (Fig. 6 l.284): sweep k+1 is recorded and launched BEFORE delta_k is read, so the
 // device never idles on the host's read-back; if delta_k <= tol the speculative sweep is dropped
 // (immutable handles keep r_k intact).  When the deltas' geometric decay predicts that sweep k is
-// the last, sweep k+1 is launched only after delta_k is read (no discarded sweep at the end).
+// the last (within a margin set by how steady the decay ratio is), sweep k+1 is launched only
+// after delta_k is read (no discarded sweep at the end).
 // tol < 0 runs exactly itermax sweeps with no host sync.
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -113,15 +115,23 @@ extern "C" nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, 
     TRY(pr.sweep(t, &rk, &dk));
     std::vector<nbg_scalar> deltas;   // fixed-count mode: read after the loop
     int k = 1;
-    double dm1 = -1.0, dm2 = -1.0;    // delta_{k-1}, delta_{k-2} (convergence mode)
+    double dm1 = -1.0, dm2 = -1.0, dm3 = -1.0;   // delta_{k-1}, delta_{k-2}, delta_{k-3} (convergence mode)
     for (;;) {
         nbg_vector rnext = nullptr;
         nbg_scalar dnext = nullptr;
         const bool more = k < p->itermax;
         // speculate (launch sweep k+1 before delta_k is read) unless the geometric decay of the
         // deltas predicts that sweep k is the last one: then the host waits for delta_k instead
-        // of paying a whole discarded sweep (results are identical either way)
-        const bool last_likely = conv && dm1 > 0.0 && dm2 > 0.0 && dm1 * (dm1 / dm2) <= 2.0 * p->tol;
+        // of paying a whole discarded sweep (results are identical either way).  Prediction
+        // delta_k ~ delta_{k-1} q with q = delta_{k-1} / delta_{k-2}; the margin grows with the
+        // disagreement of the last two ratios (a waited sweep costs the device ~ one host round
+        // trip, a discarded one a whole sweep, so waiting pays once P(delta_k <= tol) > ~0.2)
+        bool last_likely = false;
+        if (conv && dm1 > 0.0 && dm2 > 0.0) {
+            const double q1 = dm1 / dm2;
+            const double spread = dm3 > 0.0 ? std::fabs(q1 - dm2 / dm3) / q1 : 1.0;
+            last_likely = dm1 * q1 <= p->tol * (1.0 + std::min(1.0, 3.0 * spread));
+        }
         const bool spec = more && !last_likely;
         if (spec) TRY(pr.sweep(rk, &rnext, &dnext));   // launched before delta_k is read
         bool stop = !more;
@@ -132,6 +142,7 @@ extern "C" nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, 
             nbg_scalar_free(ctx, dk);
             dk = nullptr;
             if (!(v > p->tol)) stop = true;
+            dm3 = dm2;
             dm2 = dm1;
             dm1 = v;
             if (!stop && more && !spec) TRY(pr.sweep(rk, &rnext, &dnext));   // mispredicted: launch now
