@@ -342,6 +342,8 @@ struct Ctx {
     SlabP cur_slab;
     std::vector<cudaEvent_t> event_pool;
     std::vector<cudaEvent_t> timing_pool;   // recycled timing events (nbg_set_timing)
+    cudaStream_t rb_stream = nullptr;      // scalar readbacks (issue_readback), ordered after the producer
+    cudaEvent_t rb_dep = nullptr;
 
     // freed device buffers kept for reuse by size (all work is ordered on `stream`, so a buffer
     // whose last handle died can back a later allocation without a cudaFreeAsync/MallocAsync pair)
