@@ -14,7 +14,7 @@ torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(3): solve()
     torch.cuda.synchronize()
-evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA], key=lambda e: e.time_range.start)
+evs = sorted([e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA and 'Memcpy' not in e.name], key=lambda e: e.time_range.start)
 prev = None
 for e in evs:
     st_, en = e.time_range.start, e.time_range.end
