@@ -229,6 +229,9 @@ nbg_status nbg_init(nbg_ctx **out, const nbg_config *cfg) {
         ctx->own_stream = true;
     }
     NBG_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+    // side stream of the scalar readbacks (issue_readback), on the context's device
+    NBG_CUDA(cudaStreamCreateWithFlags(&ctx->rb_stream, cudaStreamNonBlocking));
+    NBG_CUDA(cudaEventCreateWithFlags(&ctx->rb_dep, cudaEventDisableTiming));
     cudaMemPool_t pool;
     NBG_CUDA(cudaDeviceGetDefaultMemPool(&pool, cfg->device));
     uint64_t thr = UINT64_MAX;

@@ -131,10 +131,6 @@ void put_event(Ctx &c, cudaEvent_t e) { c.event_pool.push_back(e); }
 // sweep (copy-engine handoff before and after the 2 µs copy).
 void issue_readback(Ctx &c, Slot &s) {
     if (s.rb_issued) return;
-    if (!c.rb_stream) {
-        NBG_CUDA(cudaStreamCreateWithFlags(&c.rb_stream, cudaStreamNonBlocking));
-        NBG_CUDA(cudaEventCreateWithFlags(&c.rb_dep, cudaEventDisableTiming));
-    }
     NBG_CUDA(cudaEventRecord(c.rb_dep, c.stream));
     NBG_CUDA(cudaStreamWaitEvent(c.rb_stream, c.rb_dep, 0));
     NBG_CUDA(cudaMemcpyAsync(s.hptr(), s.dptr(), SLOT_U64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.rb_stream));
