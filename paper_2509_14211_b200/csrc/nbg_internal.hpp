@@ -344,6 +344,8 @@ struct Ctx {
     std::vector<cudaEvent_t> timing_pool;   // recycled timing events (nbg_set_timing)
     cudaStream_t rb_stream = nullptr;      // scalar readbacks (issue_readback), ordered after the producer
     cudaEvent_t rb_dep = nullptr;
+    long long spmv_x_bytes = 0;            // gathered vector of the SpMV being launched (L2 window, NBG_L2_PERSIST_MB)
+    bool l2_limit_set = false;
 
     // freed device buffers kept for reuse by size (all work is ordered on `stream`, so a buffer
     // whose last handle died can back a later allocation without a cudaFreeAsync/MallocAsync pair)

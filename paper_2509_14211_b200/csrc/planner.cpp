@@ -630,6 +630,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         items = (A.plan->ntiles + A.plan->nchunks + nw - 1) / nw;   // one task per warp
         args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
+        c.spmv_x_bytes = (A.plan->relabel ? A.plan->ncols_g : A.ncols) * (long long)type_size(u->type);
         // two-phase column-blocked plan (large relabelled matrices, 4/8-byte gathered elements)
         TpPlan *T = (!A.vals && n > 0) ? gpu_tp_plan(c, A, (int)type_size(u->type), c.num_sms) : nullptr;
         // lane-per-row skeleton for low-skew matrices (SURVEY 8(a) K4 notes), NBG_SPMV_LPR overrides
