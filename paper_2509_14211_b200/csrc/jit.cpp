@@ -145,8 +145,15 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
         cfg.attrs = at;
         cfg.numAttrs = 1;
         NBG_CUDA(cudaLaunchKernelExC(&cfg, (const void *)k.k, params));
-    } else
-    NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem, c.stream));
+        c.l2_window_active = true;
+    } else {
+        // lines marked persisting stay set aside until reset: release them for everything else
+        if (c.l2_window_active) {
+            NBG_CUDA(cudaCtxResetPersistingL2Cache());
+            c.l2_window_active = false;
+        }
+        NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem, c.stream));
+    }
     timing_end(c, cls, ev0);
     c.stats.kernels_launched++;
     static int dbg_sync = -1;

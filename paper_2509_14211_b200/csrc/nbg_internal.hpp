@@ -346,6 +346,7 @@ struct Ctx {
     cudaEvent_t rb_dep = nullptr;
     long long spmv_x_bytes = 0;            // gathered vector of the SpMV being launched (L2 window, NBG_L2_PERSIST_MB)
     bool l2_limit_set = false;
+    bool l2_window_active = false;         // persisting lines may be set aside (reset before other kernels)
 
     // freed device buffers kept for reuse by size (all work is ordered on `stream`, so a buffer
     // whose last handle died can back a later allocation without a cudaFreeAsync/MallocAsync pair)

@@ -414,6 +414,8 @@ Ctx::~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto e : event_pool) cudaEventDestroy(e);
     for (auto e : timing_pool) cudaEventDestroy(e);
+    if (l2_window_active) cudaCtxResetPersistingL2Cache();
+    if (l2_limit_set) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
     if (rb_stream) {
         cudaStreamSynchronize(rb_stream);
         cudaStreamDestroy(rb_stream);
