@@ -576,7 +576,7 @@ def main():
     ap.add_argument("--workload", default="c4", choices=["c1", "c2", "c3", "c4", "c5", "sparse"])
     ap.add_argument("--dtype", default="fp32", choices=["fp32", "fp64"], help="c2 only")
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-sweeps", type=int, default=3)
+    ap.add_argument("--cpu-sweeps", type=int, default=60)   # ≈ 10 s of oracle work at C4
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
