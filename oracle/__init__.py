@@ -13,8 +13,9 @@ Contents
             ewise_mult, ewise_add, mxv, reduce, convert) over full / iso / empty vectors.
 ``__init__`` a ctypes loader that compiles ``orc.c`` with gcc (``-O2 -ffp-contract=off``).
 
-Pins (what ties this oracle to something other than itself) live in ``tests/test_oracle*.py``;
-DESIGN.md lists them per function.  Functions without a pin: none.
+Pins (what ties this oracle to something other than itself) live in ``tests/test_oracle.py``,
+``tests/test_oracle_ops_pins.py`` (every operator branch of ops.py, ``convert``, the fp32 mxv, the
+R-MAT level-bit order) and ``tests/test_sparse_oracle.py``; DESIGN.md §4 lists them per function.
 """
 from __future__ import annotations
 
