@@ -25,8 +25,12 @@
  *  - Memory spaces: NBG_HOST pointers are ordinary host memory (pinned or pageable);
  *    NBG_DEVICE pointers are device memory of the context's GPU.  NBG_COPY copies the data;
  *    NBG_BORROW keeps the device pointer (it must outlive the object and stay unmodified).
- *  - All device work of a context is issued on the context's CUDA stream (config.stream, or a
- *    library-owned stream when NULL).  Exports and scalar reads synchronise that stream.
+ *  - Streams: every kernel and every host<->device copy of a context is issued on the context's
+ *    CUDA stream (config.stream, or a library-owned stream when NULL), except the device->host
+ *    readback of a reduction's value, which runs on an internal side stream ordered after the
+ *    producing kernel by an event (so the next kernels on the context stream do not wait behind
+ *    the copy).  Exports synchronise the context stream; nbg_scalar_get waits only for the
+ *    readback of that scalar; nbg_sync waits for both streams (all outstanding work).
  *  - Index types: row pointers are int64, column indices int32 ("32 bit indices");
  *    dimensions must be < 2^31 (NBG_INVALID_VALUE otherwise).
  *  - A context is single-threaded: calls on one context must not run concurrently.
@@ -68,11 +72,22 @@ typedef struct nbg_matrix_s *nbg_matrix;
 typedef struct nbg_vector_s *nbg_vector;
 typedef struct nbg_scalar_s *nbg_scalar;
 
+/* nbg_config.flags bits.
+ * NBG_FLAG_DETERMINISTIC (SURVEY 8(b) `deterministic=1`): request run-to-run bit-reproducible
+ *   results.  This library has no nondeterministic fast path, so the flag changes nothing and
+ *   results are always deterministic: floating PLUS reductions are accumulated per thread / task
+ *   in a fixed order and combined across blocks EXACTLY (order-independent fixed-point limbs;
+ *   across ranks by an integer allreduce), SpMV row sums have an order fixed by the matrix plan,
+ *   and integer MIN/MAX/PLUS are associative.  (The one exception is documented at nbg_reduce:
+ *   partials of magnitude >= 2^128 or < 2^-160 are added in arrival order.)  Other bits:
+ *   NBG_INVALID_VALUE. */
+enum { NBG_FLAG_DETERMINISTIC = 1 };
+
 typedef struct {
     int mode;        /* nbg_mode; fixed for the context's lifetime */
     int device;      /* CUDA device ordinal */
     void *stream;    /* cudaStream_t to issue work on (borrowed), or NULL for a library stream */
-    int flags;       /* reserved, must be 0 */
+    int flags;       /* 0 or NBG_FLAG_DETERMINISTIC (see above); checked before any CUDA call */
 } nbg_config;
 
 /* ---------------------------------------------------------------- operators
@@ -128,8 +143,8 @@ nbg_status nbg_finalize(nbg_ctx *ctx);
 /* Copy the last latched error message (NUL-terminated, truncated to len) into buf. */
 nbg_status nbg_last_error(nbg_ctx *ctx, char *buf, size_t len);
 
-/* Block until all work issued on the context's stream has finished; returns a latched
- * execution error if one occurred. */
+/* Block until all work of the context has finished (its stream and the scalar-readback side
+ * stream); returns a latched execution error if one occurred. */
 nbg_status nbg_sync(nbg_ctx *ctx);
 
 /* Planner / executor counters (SPEC.md:338-341 cache counters; PAPER.md:301-306 wait steps). */
@@ -318,6 +333,13 @@ nbg_status nbg_scalar_apply(nbg_ctx *ctx, nbg_scalar *s_out, int type, nbg_unop 
  * exports and nbg_scalar_get synchronise. */
 nbg_status nbg_vector_wait(nbg_ctx *ctx, nbg_vector v);
 nbg_status nbg_scalar_wait(nbg_ctx *ctx, nbg_scalar s);
+
+/* Materialise every pending vector and reduction the caller still holds a handle to, in one
+ * planning pass (the GraphBLAS `GrB_wait()` without an object): nodes that no handle
+ * reaches stay elided.  Pending scalar_apply nodes are evaluated where they are read (host
+ * arithmetic on a materialised scalar), as with nbg_scalar_wait.  Idempotent; returns after
+ * launching; execution errors as for nbg_vector_wait. */
+nbg_status nbg_wait_all(nbg_ctx *ctx);
 
 /* ---------------------------------------------------------------- PageRank (Fig. 6)
  * Written purely on the operations above.  AT: n x n pattern CSR (edge

@@ -178,14 +178,32 @@ static NodeP rec_sapply(Ctx &c, int type, const nbg_unop &op, const NodeP &s) {
     return x;
 }
 
+// every node a user handle points to is registered (weakly) for nbg_wait_all
+static void register_user_node(nbg_ctx *ctx, const NodeP &x) {
+    if (x->mat) return;
+    auto &v = ctx->user_nodes;
+    if (v.size() >= 64 && v.size() >= 2 * ctx->user_nodes_live) {   // drop dead / materialised entries
+        size_t k = 0;
+        for (auto &w : v) {
+            NodeP n = w.lock();
+            if (n && !n->mat && n->user_refs > 0) v[k++] = w;
+        }
+        v.resize(k);
+        ctx->user_nodes_live = k;
+    }
+    v.push_back(x);
+    ctx->user_nodes_live++;
+}
 static nbg_vector new_vhandle(nbg_ctx *ctx, const NodeP &x) {
     auto *h = new nbg_vector_s{ctx, x};
     x->user_refs++;
+    register_user_node(ctx, x);
     return h;
 }
 static nbg_scalar new_shandle(nbg_ctx *ctx, const NodeP &x) {
     auto *h = new nbg_scalar_s{ctx, x};
     x->user_refs++;
+    register_user_node(ctx, x);
     return h;
 }
 
@@ -213,7 +231,7 @@ nbg_status nbg_init(nbg_ctx **out, const nbg_config *cfg) {
     API_BEGIN
     CHECK(out && cfg, NBG_NULL_POINTER, "nbg_init: NULL argument");
     CHECK(cfg->mode == NBG_BLOCKING || cfg->mode == NBG_NONBLOCKING, NBG_INVALID_VALUE, "nbg_init: bad mode");
-    CHECK(cfg->flags == 0, NBG_INVALID_VALUE, "nbg_init: flags must be 0");
+    CHECK((cfg->flags & ~NBG_FLAG_DETERMINISTIC) == 0, NBG_INVALID_VALUE, "nbg_init: unknown flag bits");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess || ndev == 0) fail(NBG_PANIC, "nbg_init: no CUDA device");
@@ -261,6 +279,7 @@ nbg_status nbg_sync(nbg_ctx *ctx) {
     API_BEGIN
     check_ctx(ctx);
     NBG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->rb_stream) NBG_CUDA(cudaStreamSynchronize(ctx->rb_stream));   // scalar readbacks (side stream)
     if (ctx->latched != NBG_SUCCESS) return ctx->latched;
     API_END(ctx)
 }
@@ -922,6 +941,24 @@ nbg_status nbg_vector_wait(nbg_ctx *ctx, nbg_vector v) {
     check_ctx(ctx);
     check_vec(ctx, v);
     if (!v->node->mat) materialize(*ctx, {v->node});
+    if (ctx->latched != NBG_SUCCESS) return ctx->latched;
+    API_END(ctx)
+}
+
+nbg_status nbg_wait_all(nbg_ctx *ctx) {
+    API_BEGIN
+    check_ctx(ctx);
+    std::vector<NodeP> roots;
+    size_t k = 0;
+    for (auto &w : ctx->user_nodes) {
+        NodeP n = w.lock();
+        if (!n || n->mat || n->user_refs <= 0) continue;
+        ctx->user_nodes[k++] = w;
+        roots.push_back(n);
+    }
+    ctx->user_nodes.resize(k);
+    ctx->user_nodes_live = k;
+    if (!roots.empty()) materialize(*ctx, roots);
     if (ctx->latched != NBG_SUCCESS) return ctx->latched;
     API_END(ctx)
 }

@@ -106,13 +106,34 @@ KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bo
     return k;
 }
 
-void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls) {
+// Raise the device's persisting-L2 set-aside to `want` bytes (once per context; the previous limit
+// is saved and restored at finalize, ~Ctx).  Acts on c.device, restoring the caller's current
+// device.  Returns the granted set-aside (0 if the device refuses).
+static size_t l2_setaside(Ctx &c, size_t want) {
+    if (c.l2_limit_set) return c.l2_limit_granted;
+    c.l2_limit_set = true;   // one attempt per context
+    int prev_dev = -1, mx = 0;
+    if (cudaGetDevice(&prev_dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+    if (prev_dev != c.device && cudaSetDevice(c.device) != cudaSuccess) { cudaGetLastError(); return 0; }
+    size_t prev = 0, got = 0;
+    bool ok = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, c.device) == cudaSuccess && mx > 0 &&
+              cudaDeviceGetLimit(&prev, cudaLimitPersistingL2CacheSize) == cudaSuccess;
+    if (ok) {
+        c.l2_limit_prev = prev;
+        ok = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(want, (size_t)mx)) == cudaSuccess &&
+             cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize) == cudaSuccess;
+    }
+    if (!ok) { cudaGetLastError(); got = 0; c.l2_limit_set = false; c.l2_limit_prev = 0; }
+    c.l2_limit_granted = got;
+    if (prev_dev != c.device) cudaSetDevice(prev_dev);
+    return got;
+}
+
+void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls, long long l2_window) {
     long long g = work_items;
     if (g > k.grid_cap) g = k.grid_cap;
     if (g < 1) g = 1;
     void *params[] = {(void *)&args};
-    cudaEvent_t ev0 = nullptr;
-    timing_begin(c, cls, &ev0);
     // SpMV over a gathered vector that does not stay L2-resident (> 48 MB, C5: 108 MB): a persisting
     // L2 window over its head -- the hottest columns in the degree-sorted gather layout -- keeps
     // them in L2 against the streamed indices.  C5 sweep: no window 3.86-3.93 ms,
@@ -123,18 +144,32 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
         const char *e = getenv("NBG_L2_PERSIST_MB");
         persist = (e && *e) ? std::max(0ll, atoll(e)) << 20 : (56ll << 20);
     }
-    if (persist > 0 && args.x && c.spmv_x_bytes > (48ll << 20) && cls && cls[0] == 's' && std::string(cls) == "spmv") {
-        if (!c.l2_limit_set) {
-            int mx = 0;
-            cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, c.device);
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)std::min<long long>(persist, mx));
-            c.l2_limit_set = true;
-        }
+    size_t granted = 0;
+    if (persist > 0 && args.x && l2_window > (48ll << 20)) granted = l2_setaside(c, (size_t)persist);
+    const size_t win = granted ? (size_t)std::min<long long>(persist, l2_window) : 0;
+    if (!win && c.l2_win_base) {
+        // lines marked persisting stay set aside until demoted: touch the region once with a
+        // Normal window, in stream order after the SpMV that marked them (never while it runs)
+        cudaLaunchAttribute dm[1];
+        dm[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        dm[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(c.l2_win_base);
+        dm[0].val.accessPolicyWindow.num_bytes = c.l2_win_bytes;
+        dm[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        dm[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+        dm[0].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+        gpu_l2_touch(c, c.l2_win_base, c.l2_win_bytes, dm);
+        c.l2_win_base = nullptr;
+        c.l2_win_bytes = 0;
+    }
+    cudaEvent_t ev0 = nullptr;
+    timing_begin(c, cls, &ev0);
+    if (win) {
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeAccessPolicyWindow;
         at[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(args.x);
-        at[0].val.accessPolicyWindow.num_bytes = (size_t)std::min<long long>(persist, std::max(1ll, c.spmv_x_bytes));
-        at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+        at[0].val.accessPolicyWindow.num_bytes = win;
+        // hit ratio so that the persisting lines fit the granted set-aside (no thrashing inside it)
+        at[0].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)granted / (double)win);
         at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
         cudaLaunchConfig_t cfg = {};
@@ -145,13 +180,9 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
         cfg.attrs = at;
         cfg.numAttrs = 1;
         NBG_CUDA(cudaLaunchKernelExC(&cfg, (const void *)k.k, params));
-        c.l2_window_active = true;
+        c.l2_win_base = args.x;
+        c.l2_win_bytes = win;
     } else {
-        // lines marked persisting stay set aside until reset: release them for everything else
-        if (c.l2_window_active) {
-            NBG_CUDA(cudaCtxResetPersistingL2Cache());
-            c.l2_window_active = false;
-        }
         NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem, c.stream));
     }
     timing_end(c, cls, ev0);

@@ -344,9 +344,12 @@ struct Ctx {
     std::vector<cudaEvent_t> timing_pool;   // recycled timing events (nbg_set_timing)
     cudaStream_t rb_stream = nullptr;      // scalar readbacks (issue_readback), ordered after the producer
     cudaEvent_t rb_dep = nullptr;
-    long long spmv_x_bytes = 0;            // gathered vector of the SpMV being launched (L2 window, NBG_L2_PERSIST_MB)
-    bool l2_limit_set = false;
-    bool l2_window_active = false;         // persisting lines may be set aside (reset before other kernels)
+    // persisting-L2 window over the head of a large gathered vector (launch(), NBG_L2_PERSIST_MB)
+    bool l2_limit_set = false;             // this context raised the device's persisting set-aside
+    size_t l2_limit_prev = 0;              // ... from this value (restored at finalize)
+    size_t l2_limit_granted = 0;           // set-aside the device granted
+    const void *l2_win_base = nullptr;     // region whose lines were last marked persisting
+    size_t l2_win_bytes = 0;               // (demoted in stream order before the next other kernel)
 
     // freed device buffers kept for reuse by size (all work is ordered on `stream`, so a buffer
     // whose last handle died can back a later allocation without a cudaFreeAsync/MallocAsync pair)
@@ -365,6 +368,10 @@ struct Ctx {
     std::unordered_map<std::string, MemoEntry> memo;
     // learned hints: producer signature hash + output index -> templates
     std::map<std::pair<uint64_t, int>, std::vector<Hint>> hints;
+
+    // nodes user handles point to (weak): nbg_wait_all materialises the live pending ones
+    std::vector<std::weak_ptr<Node>> user_nodes;
+    size_t user_nodes_live = 0;
 
     // timing
     bool timing = false;
@@ -431,7 +438,10 @@ int spmv_lpr_mode();   // NBG_SPMV_LPR: -1 auto (by skew), 0 never, 1 always   /
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
 KernelP jit_compile(Ctx &c, const std::string &src, const std::string &kname, bool spmv, int dyn_smem = 0, int block = 0);
-void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls);
+// Launch k on the context stream.  l2_window > 0: an SpMV over a gathered vector args.x of that many
+// bytes; large ones get a persisting L2 access-policy window over their head.
+void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, const char *cls, long long l2_window = 0);
+void gpu_l2_touch(Ctx &c, const void *base, size_t bytes, const cudaLaunchAttribute *attr);   // graph.cu
 
 // graph (graph.cu)
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst);

@@ -183,6 +183,7 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
     if (!ctx || !AT_blk || !deg || !cuts || !p || !r_out) return NBG_NULL_POINTER;
     if (!ctx->dist) return NBG_INVALID_VALUE;
     if (!(p->alpha > 0.0 && p->alpha < 1.0) || p->itermax < 1) return NBG_INVALID_VALUE;
+    if (p->dangling != NBG_PR_UNIFORM && p->dangling != NBG_PR_DROP) return NBG_INVALID_VALUE;
     if (p->type != NBG_FP32 && p->type != NBG_FP64) return NBG_DOMAIN_MISMATCH;
     const int rank = ctx->dist->rank, P = ctx->dist->nranks;
     const int64_t n = cuts[P], lo = cuts[rank], nb = cuts[rank + 1] - cuts[rank];

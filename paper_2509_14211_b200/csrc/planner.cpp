@@ -600,6 +600,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     p.vec = p.spmv ? true : vec;
 
     long long items = 0;
+    long long xwin = 0;   // bytes of the gathered vector (persisting L2 window of large ones)
     if (p.spmv) {
         Node &mx = *B.mxv;
         Mat &A = *mx.A;
@@ -630,7 +631,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         items = (A.plan->ntiles + A.plan->nchunks + nw - 1) / nw;   // one task per warp
         args.nnz = 4 * A.plan->ngroups;
         args.hc = A.plan->relabel ? A.plan->ncols_g : A.ncols;   // clamped to the kernel's cache below
-        c.spmv_x_bytes = (A.plan->relabel ? A.plan->ncols_g : A.ncols) * (long long)type_size(u->type);
+        xwin = (A.plan->relabel ? A.plan->ncols_g : A.ncols) * (long long)type_size(u->type);
         // two-phase column-blocked plan (large relabelled matrices, 4/8-byte gathered elements)
         TpPlan *T = (!A.vals && n > 0) ? gpu_tp_plan(c, A, (int)type_size(u->type), c.num_sms) : nullptr;
         // lane-per-row skeleton for low-skew matrices (SURVEY 8(a) K4 notes), NBG_SPMV_LPR overrides
@@ -688,7 +689,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         a1.S = T->S;
         a1.ncols_g = A.plan->ncols_g;
         a1.nnz = 4 * T->ngroups;
-        if (T->ntasks > 0) launch(c, *kp1, a1, T->ncta, "spmv");
+        if (T->ntasks > 0) launch(c, *kp1, a1, T->ncta, "spmv", xwin);
     }
 
     double tsig0 = now_ns();
@@ -722,7 +723,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             for (int k = 0; k < p.n_red; k++) fprintf(stderr, " racc%d=%p", k, (void *)args.racc[k]);
             fprintf(stderr, "\n");
         }
-        if (items > 0 && n > 0) launch(c, *kern, args, items, p.tp ? "spmv_p2" : (p.spmv ? "spmv" : "ewise"));
+        if (items > 0 && n > 0) launch(c, *kern, args, items, p.tp ? "spmv_p2" : (p.spmv ? "spmv" : "ewise"), p.spmv && !p.tp ? xwin : 0);
     }
 
     // provenance of the written buffers (for hints): base signature + output index

@@ -414,8 +414,18 @@ Ctx::~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
     for (auto e : event_pool) cudaEventDestroy(e);
     for (auto e : timing_pool) cudaEventDestroy(e);
-    if (l2_window_active) cudaCtxResetPersistingL2Cache();
-    if (l2_limit_set) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+    if (l2_limit_set) {
+        // the stream is idle here: release this context's persisting lines and put the device's
+        // set-aside back to what it was before this context raised it
+        int prev_dev = -1;
+        if (cudaGetDevice(&prev_dev) == cudaSuccess) {
+            if (prev_dev != device) cudaSetDevice(device);
+            if (l2_win_base) cudaCtxResetPersistingL2Cache();
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, l2_limit_prev);
+            if (prev_dev != device) cudaSetDevice(prev_dev);
+        }
+        cudaGetLastError();
+    }
     if (rb_stream) {
         cudaStreamSynchronize(rb_stream);
         cudaStreamDestroy(rb_stream);

@@ -36,6 +36,7 @@ GRAPH_RMAT, GRAPH_ER = 0, 1
 FORMAT_FULL, FORMAT_ISO, FORMAT_SPARSE, FORMAT_BITSET, FORMAT_EMPTY = range(5)
 FORMAT_NAMES = ["full", "iso", "sparse", "bitset", "empty"]
 PR_UNIFORM, PR_DROP = 0, 1
+FLAG_DETERMINISTIC = 1
 
 UNOPS = {n: i for i, n in enumerate(["IDENTITY", "AINV", "ABS", "MINV", "ADD_C", "MUL_C", "AXPB", "ABS_SUB_C",
                                       "RECIP_SCALED", "ISZERO"])}
@@ -136,6 +137,7 @@ SIGNATURES = {
     "nbg_scalar_apply": [vp, pvp, ctypes.c_int, nbg_unop, vp],
     "nbg_vector_wait": [vp, vp],
     "nbg_scalar_wait": [vp, vp],
+    "nbg_wait_all": [vp],
     "nbg_pagerank": [vp, vp, vp, ctypes.POINTER(nbg_pr_params), pvp, ctypes.POINTER(ctypes.c_int), vp],
     "nbg_partition_rows": [vp, i64, ctypes.c_int, i64, vp],
     "nbg_dist_unique_id": [vp],
@@ -183,8 +185,8 @@ def _ptr(a):
 
 
 # ---------------------------------------------------------------- context
-def nbg_init(mode=NONBLOCKING, device=0, stream=None):
-    cfg = nbg_config(mode, device, stream, 0)
+def nbg_init(mode=NONBLOCKING, device=0, stream=None, flags=0):
+    cfg = nbg_config(mode, device, stream, flags)
     ctx = ctypes.c_void_p()
     _call(None, "nbg_init", ctypes.byref(ctx), ctypes.byref(cfg))
     return ctx
@@ -473,6 +475,10 @@ def nbg_vector_wait(ctx, v):
 
 def nbg_scalar_wait(ctx, s):
     _call(ctx, "nbg_scalar_wait", ctx, s)
+
+
+def nbg_wait_all(ctx):
+    _call(ctx, "nbg_wait_all", ctx)
 
 
 # ---------------------------------------------------------------- PageRank / distributed

@@ -60,6 +60,22 @@ def test_null_and_invalid_arguments():
     out = ctypes.c_void_p()
     assert nbg.lib.nbg_init(ctypes.byref(out), ctypes.byref(cfg)) == nbg.INVALID_VALUE
     assert nbg.lib.nbg_partition_rows(None, 0, 1, 0, None) == nbg.NULL_POINTER
+    assert nbg.lib.nbg_wait_all(None) == nbg.NULL_POINTER
+
+
+def test_config_flags_checked_before_the_device():
+    # nbg_config.flags: NBG_FLAG_DETERMINISTIC is accepted, any other bit is a validation error
+    # returned before any CUDA call (so this runs without a GPU)
+    import ctypes
+    import torch
+    from paper_2509_14211_b200 import nbg
+    out = ctypes.c_void_p()
+    for bad in (2, 4, 1 | 8, -1):
+        cfg = nbg.nbg_config(nbg.NONBLOCKING, 0, None, bad)
+        assert nbg.lib.nbg_init(ctypes.byref(out), ctypes.byref(cfg)) == nbg.INVALID_VALUE
+    if not torch.cuda.is_available():
+        cfg = nbg.nbg_config(nbg.NONBLOCKING, 0, None, nbg.FLAG_DETERMINISTIC)
+        assert nbg.lib.nbg_init(ctypes.byref(out), ctypes.byref(cfg)) == nbg.PANIC   # valid flags, no device
 
 
 def test_partition_rows_balances_bytes():

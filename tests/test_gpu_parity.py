@@ -565,3 +565,52 @@ def test_small_matrix_with_long_rows(nbg, ctx, n, hubs, m):
         got = nbg.nbg_vector_export_dense(ctx, nbg.nbg_mxv(ctx, T, "PLUS", "TIMES", A, nbg.nbg_vector_from_dense(ctx, T, x)))
         exp = ops.mxv("PLUS", "TIMES", orp, oci, None, x, npT)
         assert rel(got[lens > 0], exp[lens > 0]) <= (2e-7 if T == nbg.FP32 else 1e-14) and np.all(got[lens == 0] == 0)
+
+
+# ------------------------------------------------------------------ C ABI: wait_all, deterministic flag
+
+def test_wait_all_materialises_live_pending_nodes_only(nbg):
+    """nbg_wait_all: every pending node a handle reaches is materialised in one
+    planning pass; nodes no handle reaches stay elided; values match the oracle."""
+    import inputs
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        x, y = inputs.uniform_vectors(1 << 14, 5, np.float64)
+        vx = nbg.nbg_vector_from_dense(c, nbg.FP64, x)
+        vy = nbg.nbg_vector_from_dense(c, nbg.FP64, y)
+        a = nbg.nbg_apply(c, nbg.FP64, "ADD_C", vy, 1.0)              # freed below: elided
+        z = nbg.nbg_ewise_mult(c, nbg.FP64, "TIMES", vx, a)           # live
+        w = nbg.nbg_ewise_add(c, nbg.FP64, "MAX", z, vx)              # live
+        s = nbg.nbg_reduce(c, nbg.FP64, nbg.PLUS, w)                  # live scalar
+        nbg.nbg_vector_free(c, a)
+        assert not nbg.nbg_vector_is_materialized(c, z) and not nbg.nbg_vector_is_materialized(c, w)
+        nbg.nbg_reset_stats(c)
+        nbg.nbg_wait_all(c)
+        st = nbg.nbg_get_stats(c)
+        assert nbg.nbg_vector_is_materialized(c, z) and nbg.nbg_vector_is_materialized(c, w)
+        assert st["kernels_launched"] == 1 and st["vectors_materialized"] == 2, st   # one fused pass, `a` elided
+        nbg.nbg_wait_all(c)                                            # idempotent: nothing left
+        assert nbg.nbg_get_stats(c)["kernels_launched"] == 1
+        zo = ops.binop("TIMES", x, ops.unop("ADD_C", y, np.float64, 1.0), np.float64)
+        wo = ops.binop("MAX", zo, x, np.float64)
+        assert np.array_equal(nbg.nbg_vector_export_dense(c, z), zo)
+        assert np.array_equal(nbg.nbg_vector_export_dense(c, w), wo)
+        assert rel([nbg.nbg_scalar_get(c, s)], [ops.reduce("PLUS", wo, np.float64)]) <= 1e-12
+    finally:
+        nbg.nbg_finalize(c)
+
+
+def test_deterministic_flag_and_run_to_run_bits(nbg):
+    """nbg_config.flags = NBG_FLAG_DETERMINISTIC is accepted; results are bit-reproducible run to
+    run with or without it (exact cross-block combine, plan-fixed row order)."""
+    outs = []
+    for flags in (nbg.FLAG_DETERMINISTIC, 0, nbg.FLAG_DETERMINISTIC):
+        c = nbg.nbg_init(nbg.NONBLOCKING, 0, flags=flags)
+        try:
+            A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 14, 16, 4)
+            r, sweeps, hist = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=8, type=nbg.FP64)
+            outs.append((nbg.nbg_vector_export_dense(c, r), np.asarray(hist)))
+        finally:
+            nbg.nbg_finalize(c)
+    for o in outs[1:]:
+        assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
