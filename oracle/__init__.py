@@ -38,14 +38,41 @@ _f64p = ctypes.POINTER(ctypes.c_double)
 _f32p = ctypes.POINTER(ctypes.c_float)
 
 
-def build(force: bool = False) -> str:
-    """Compile orc.c -> liborc.so (plain gcc, no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
-        os.replace(tmp, _LIB)
-    return _LIB
+_LIB_OMP = os.path.join(_HERE, "liborc_omp.so")
+
+
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile orc.c -> liborc.so (plain gcc, no FMA contraction, no fast-math).  omp=True builds
+    the same source with -fopenmp -> liborc_omp.so (row loop over threads; identical results),
+    used only as the all-core CPU baseline of bench.py."""
+    out = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        tmp = out + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-ffp-contract=off", "-fno-fast-math"]
+                              + (["-fopenmp"] if omp else []) + ["-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
+_lib_omp = None
+
+
+def _bind(L):
+    for nm, fp in (("orc_pagerank_f64", _f64p), ("orc_pagerank_f32", _f32p)):
+        f = getattr(L, nm)
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_int64, _i64p, _i32p, _i32p, ctypes.c_double, ctypes.c_int,
+                      ctypes.c_int, ctypes.c_double, fp, _f64p, _f64p]
+    return L
+
+
+def lib_omp():
+    """The OpenMP build (threads from OMP_NUM_THREADS, default: all host cores)."""
+    global _lib_omp
+    with _lock:
+        if _lib_omp is None:
+            _lib_omp = _bind(ctypes.CDLL(build(omp=True)))
+    return _lib_omp
 
 
 def lib():
@@ -166,8 +193,10 @@ def mxv_plus(rowptr, colidx, x):
     return m
 
 
-def pagerank(rowptr, colidx, deg, *, alpha=0.85, dtype=np.float64, uniform=True, itermax=20, tol=-1.0):
-    """Fig. 6 PageRank sweep.  -> (r, sweeps, delta_hist, ds_hist)."""
+def pagerank(rowptr, colidx, deg, *, alpha=0.85, dtype=np.float64, uniform=True, itermax=20, tol=-1.0,
+             threads=False):
+    """Fig. 6 PageRank sweep.  -> (r, sweeps, delta_hist, ds_hist).
+    threads=True runs the OpenMP build (same results; bench.py's all-core baseline only)."""
     n = rowptr.shape[0] - 1
     rowptr = np.ascontiguousarray(rowptr, np.int64)
     colidx = np.ascontiguousarray(colidx, np.int32)
@@ -175,7 +204,8 @@ def pagerank(rowptr, colidx, deg, *, alpha=0.85, dtype=np.float64, uniform=True,
     r = np.empty(n, dtype)
     dh = np.zeros(max(itermax, 1), np.float64)
     sh = np.zeros(max(itermax, 1), np.float64)
-    f = lib().orc_pagerank_f64 if dtype == np.float64 else lib().orc_pagerank_f32
+    L = lib_omp() if threads else lib()
+    f = L.orc_pagerank_f64 if dtype == np.float64 else L.orc_pagerank_f32
     fp = _f64p if dtype == np.float64 else _f32p
     sweeps = f(n, _p(rowptr, _i64p), _p(colidx, _i32p), _p(deg, _i32p), float(alpha), int(uniform),
                int(itermax), float(tol), _p(r, fp), _p(dh, _f64p), _p(sh, _f64p))

@@ -187,6 +187,10 @@ int NAME(int64_t n, const int64_t *rowptr, const int32_t *colidx, const int32_t 
         for (int64_t i = 0; i < n; i++) t[i] = r[i];                                       \
         for (int64_t j = 0; j < n; j++) y[j] = t[j] * dinv[j];                             \
         const T c = uniform ? (T)(a_n * ds + tele) : (T)tele;                              \
+        /* rows are independent: the OpenMP build (liborc_omp.so, cpu_baseline only)     \
+         * splits them over threads; every row's sum keeps its ascending order, so the     \
+         * result is identical to the single-threaded build */                             \
+        _Pragma("omp parallel for schedule(static)")                                       \
         for (int64_t i = 0; i < n; i++) {                                                  \
             double acc = 0.0;                                                              \
             for (int64_t p = rowptr[i]; p < rowptr[i + 1]; p++) acc += (double)y[colidx[p]]; \

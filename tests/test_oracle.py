@@ -338,3 +338,14 @@ def test_ops_integer_division_exact():
     exp = [3, -3, -3, 3, 0, 0, (2**62 + 1) // 3, -((2**62 + 3) // 7), -(2**63 // 3), 0]
     assert list(ops.binop("DIV", a, b, np.int64)) == exp
     assert list(ops.unop("MINV", np.array([1, -1, 2, 0, -2**31], np.int32), np.int32)) == [1, -1, 0, 0, 0]
+
+
+def test_openmp_build_is_identical():
+    # bench.py's all-core baseline runs the same orc.c built with -fopenmp (rows split over
+    # threads, each row's sum in ascending order): results must equal the single-threaded build
+    src, dst = oracle.rmat_edges(12, 8, seed=2)
+    rp, ci, deg = oracle.build_csr(4096, src, dst)
+    for dt in (np.float32, np.float64):
+        a = oracle.pagerank(rp, ci, deg, dtype=dt, itermax=6)
+        b = oracle.pagerank(rp, ci, deg, dtype=dt, itermax=6, threads=True)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[2], b[2]) and a[1] == b[1]
