@@ -148,31 +148,36 @@ def run_ours(args, rank, world, local_rank):
     w = 4 if T == nbg.FP32 else 8
     kind = nbg.GRAPH_RMAT if cfg["graph"] == "rmat" else nbg.GRAPH_ER
     t0 = time.time()
-    if args.mtx:       # NEXT-4: a real graph from a Matrix Market file (the paper's GAP-web run)
-        A, deg = nbg.nbg_matrix_from_mtx(ctx, args.mtx)
-    else:
-        A, deg = nbg.nbg_matrix_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed)
-    n = nbg.nbg_matrix_nrows(ctx, A)
-    nnz = nbg.nbg_matrix_nnz(ctx, A)
-    ncols_g = int((nbg.nbg_vector_export_dense(ctx, deg) > 0).sum())   # gathered-vector length (gather layout)
     cuts = None
     if world > 1:
+        # per-rank setup: every rank regenerates the edges, keeps its share,
+        # degrees summed over NCCL, symmetric relabel, byte-balanced row block -- no rank builds the
+        # whole graph or copies a CSR to the host
         uid = nbg.nbg_dist_unique_id() if rank == 0 else None
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         nbg.nbg_dist_init(ctx, rank, world, obj[0])
-        rp, _ = nbg.nbg_matrix_export_csr(ctx, A)
-        cuts = nbg.nbg_partition_rows(rp, world, 5 * w)
-        Ab = nbg.nbg_matrix_row_block(ctx, A, int(cuts[rank]), int(cuts[rank + 1]))
-        nbg.nbg_matrix_free(ctx, A)
-        A = Ab
+        A, deg, cuts, ncols_g = nbg.nbg_dist_graph_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed,
+                                                                  nranks=world, bytes_per_row=5 * w)
+        n = int(cuts[-1])
+        t_nnz = torch.tensor([nbg.nbg_matrix_nnz(ctx, A)], device="cuda", dtype=torch.int64)
+        dist.all_reduce(t_nnz)
+        nnz = int(t_nnz.item())
+    else:
+        if args.mtx:       # NEXT-4: a real graph from a Matrix Market file (the paper's GAP-web run)
+            A, deg = nbg.nbg_matrix_from_mtx(ctx, args.mtx)
+        else:
+            A, deg = nbg.nbg_matrix_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed)
+        n = nbg.nbg_matrix_nrows(ctx, A)
+        nnz = nbg.nbg_matrix_nnz(ctx, A)
+        ncols_g = int((nbg.nbg_vector_export_dense(ctx, deg) > 0).sum())   # gathered-vector length (gather layout)
     setup_s = time.time() - t0
     itermax, tol = cfg["itermax"], cfg["tol"]
     dangling = nbg.PR_UNIFORM if cfg["dangling"] == "uniform" else nbg.PR_DROP
 
     def step():
         if world > 1:
-            r, s, h = nbg.nbg_pagerank_dist(ctx, A, deg, cuts, alpha=cfg["alpha"], tol=tol, itermax=itermax,
+            r, s, h = nbg.nbg_pagerank_dist(ctx, A, deg, cuts, ncols_g, alpha=cfg["alpha"], tol=tol, itermax=itermax,
                                             dangling=dangling, type=T)
         else:
             r, s, h = nbg.nbg_pagerank(ctx, A, deg, alpha=cfg["alpha"], tol=tol, itermax=itermax,

@@ -377,12 +377,66 @@ nbg_status nbg_matrix_row_block(nbg_ctx *ctx, nbg_matrix *B, nbg_matrix A, int64
 nbg_status nbg_vector_allgather(nbg_ctx *ctx, nbg_vector *w, nbg_vector u_blk, const int64_t *cuts);
 nbg_status nbg_scalar_allreduce(nbg_ctx *ctx, nbg_scalar *s_out, nbg_scalar s);
 
-/* Distributed PageRank: every rank holds AT_blk = rows [cuts[rank], cuts[rank+1]) of AT (all n
- * columns) and the global out-degree vector deg (length n).  Each sweep runs the fused kernel
- * on the local rows, then exchanges the scaled ranks with an allgather-v over NCCL and combines
- * the delta / dangling mass exactly (integer allreduce of the fixed-point limbs).
- * r_blk receives this rank's block of the ranks (length cuts[rank+1]-cuts[rank]). */
-nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg, const int64_t *cuts,
+/* ---- round-2 data plane
+ * Exact-accumulator slot format (the value of every floating PLUS reduction): 16 uint64 words;
+ * words 0-9 are limbs of signed 32-bit pieces (LSB weight 2^-160), word 10 counts non-finite terms
+ * (NaN: bits 0-20, +inf: 21-41, -inf: 42-62), word 12 is the fp64 sum of terms outside the exact
+ * window [2^-160, 2^128).  Slots of several ranks combine by an integer sum of words 0-10 and an
+ * fp64 sum of word 12 (what nbg_vector_allgather_reduce does over NCCL); the value is the exact sum
+ * of all terms rounded once to fp64 (window terms), so it does not depend on the rank order. */
+
+/* Host only (no GPU): encode n terms into a zeroed slot / decode a slot to its value. */
+nbg_status nbg_xacc_encode(const double *terms, int64_t n, uint64_t *slot16);
+nbg_status nbg_xacc_decode(const uint64_t *slot16, double *value);
+
+/* Materialise the floating PLUS reduction s and copy its raw 16-word slot to host memory
+ * (synchronises).  NBG_INVALID_OBJECT if s is not a device exact-accumulator scalar. */
+nbg_status nbg_scalar_export_slot(nbg_ctx *ctx, nbg_scalar s, uint64_t *slot16);
+
+/* Test transport: make the contexts ctxs[0..nranks) ranks 0..nranks-1 of one group whose
+ * collectives run inside this process (the ranks must be driven by nranks host threads, one per
+ * context, calling the same sequence of collective operations).  A collective synchronises the
+ * caller's stream, meets the other ranks at a host barrier and reads their buffers with the
+ * caller's own copies / sum kernels (all contexts on one device), so every N > 1 code path runs
+ * on one GPU without any kernel waiting on another rank.  NCCL-based runs use nbg_dist_init. */
+nbg_status nbg_dist_init_loopback(nbg_ctx **ctxs, int nranks);
+
+/* Host only: the exchange schedule of the 1-D row partition in the gather layout.  Rank q owns
+ * rows [cuts[q], cuts[q+1]) of the relabelled AT; its scaled ranks occupy positions
+ * offsets[q] .. offsets[q]+counts[q] of the gathered vector (length ncols_g), i.e. the slice of its
+ * rows clipped at ncols_g (rows >= ncols_g are dangling vertices: never gathered). */
+nbg_status nbg_dist_exchange_plan(const int64_t *cuts, int nranks, int64_t ncols_g, int64_t *offsets, int64_t *counts);
+
+/* Per-rank graph setup without building the whole graph on any rank (needs nbg_dist_init for
+ * nranks > 1; a context without it is rank 0 of 1).  Every rank regenerates the m edges of `g`
+ * (counter-based, nbg_graph_edges), deduplicates those whose destination lies in its share of the
+ * original ids to obtain exact out/in-degree contributions, sums them over the ranks (NCCL), and
+ * derives the same symmetric relabel pi on every rank: vertices by descending out-degree, ties by
+ * id, dangling vertices last (the single-GPU gather layout).  Rows are cut in pi-space balanced by
+ * bytes (4*len + 8 + bytes_per_row per row, as nbg_partition_rows).  Out: AT_blk = rows
+ * pi in [cuts[rank], cuts[rank+1]) with pi column ids (ncols = ncols_g = number of non-dangling
+ * vertices; every row keeps its original ascending-source entry order, so row sums are the
+ * single-GPU ones); deg_blk = INT32 out-degrees of those rows' vertices; cuts (nranks + 1 entries);
+ * ncols_g.  Errors: NBG_INVALID_VALUE (generator parameters), NBG_NOT_IMPLEMENTED (> 64 ranks). */
+nbg_status nbg_dist_graph_from_generator(nbg_ctx *ctx, const nbg_graphgen *g, int64_t bytes_per_row, nbg_matrix *AT_blk,
+                                         nbg_vector *deg_blk, int64_t *cuts, int64_t *ncols_g);
+
+/* The per-sweep exchange in one call: u_blk (this rank's block, length cuts[rank+1]-cuts[rank]) is
+ * materialised -- together with the pending reductions s_in[0..nscal) and every pending node the
+ * caller holds, in ONE fused kernel -- with its values written straight into positions
+ * cuts[rank] + i (< ncols_g) of a new full vector w of length ncols_g; then ONE NCCL group
+ * broadcasts every rank's slice in place and sums the scalars' exact slots (s_out[i] = global sum
+ * of s_in[i], float PLUS reductions).  u_blk itself stays pending (its values live only inside w).
+ * With one rank no collective runs.  Errors: NBG_DIMENSION_MISMATCH (u_blk length),
+ * NBG_NOT_IMPLEMENTED (sparse/bitset u_blk, non-PLUS scalars across ranks), NBG_INVALID_VALUE. */
+nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u_blk, const int64_t *cuts, int64_t ncols_g,
+                                       int nscal, const nbg_scalar *s_in, nbg_scalar *s_out);
+
+/* Distributed PageRank on the output of nbg_dist_graph_from_generator: one fused kernel and one
+ * NCCL group per sweep (nbg_vector_allgather_reduce).  r_blk receives this rank's ranks in pi order
+ * (rows [cuts[rank], cuts[rank+1])); sweeps / delta_hist as nbg_pagerank.  The ranks are
+ * bit-identical to the single-GPU nbg_pagerank of the same graph (permuted by pi), for every P. */
+nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg_blk, const int64_t *cuts, int64_t ncols_g,
                              const nbg_pr_params *p, nbg_vector *r_blk, int *sweeps, double *delta_hist);
 
 #ifdef __cplusplus

@@ -13,6 +13,10 @@
 #include <vector>
 #include <string>
 #include <cctype>
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
 #include "nbg_internal.hpp"
 
 using namespace nbg;
@@ -222,6 +226,19 @@ static void blocking_finish(nbg_ctx *ctx, const NodeP &x) {
     NBG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// NBG_SEGV_TRACE=1: print the native stack on SIGSEGV (debug aid for host crashes on GPU boxes
+// without a debugger; addresses resolve with addr2line against libnbg.so)
+static void segv_trace(int sig) {
+    void *fr[64];
+    const int k = backtrace(fr, 64);
+    const char msg[] = "[nbg] fatal signal, native stack:\n";
+    ssize_t w = write(2, msg, sizeof msg - 1);
+    (void)w;
+    backtrace_symbols_fd(fr, k, 2);
+    signal(sig, SIG_DFL);
+    raise(sig);
+}
+
 extern "C" {
 
 // ---------------------------------------------------------------- context
@@ -230,6 +247,22 @@ nbg_status nbg_init(nbg_ctx **out, const nbg_config *cfg) {
     nbg_ctx *ctx = nullptr;
     API_BEGIN
     CHECK(out && cfg, NBG_NULL_POINTER, "nbg_init: NULL argument");
+    {
+        static bool armed = false;
+        const char *e = getenv("NBG_SEGV_TRACE");
+        if (!armed && e && e[0] == '1') {
+            static char altstack[1 << 16];
+            stack_t ss{};
+            ss.ss_sp = altstack;
+            ss.ss_size = sizeof altstack;
+            sigaltstack(&ss, nullptr);
+            struct sigaction sa{};
+            sa.sa_handler = segv_trace;
+            sa.sa_flags = SA_ONSTACK;
+            sigaction(SIGSEGV, &sa, nullptr);
+            armed = true;
+        }
+    }
     CHECK(cfg->mode == NBG_BLOCKING || cfg->mode == NBG_NONBLOCKING, NBG_INVALID_VALUE, "nbg_init: bad mode");
     CHECK((cfg->flags & ~NBG_FLAG_DETERMINISTIC) == 0, NBG_INVALID_VALUE, "nbg_init: unknown flag bits");
     int ndev = 0;

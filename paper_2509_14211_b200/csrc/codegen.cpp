@@ -831,7 +831,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         o << "    u64 v_ = 0ull; double d_ = 0.0;\n";
         o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 12 + threadIdx.x]; if (threadIdx.x == 11) d_ += __longlong_as_double((long long)x_); else v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
         o << "    if (threadIdx.x == 11) { if (d_ != 0.0) atomicAdd((double*)&a.racc[" << p.reds[j].racc << "][12], d_); }\n";
-        o << "    else if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
+        o << "    else if (threadIdx.x == 10) { if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][10], nbg_xacc_flag_counts(v_)); }\n";
         o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
         o << "  }\n";
     }
@@ -1165,7 +1165,7 @@ int gen_tp2(Gen &g, const std::string &kname) {
         o << "    u64 v_ = 0ull; double d_ = 0.0;\n";
         o << "    for (int w = 0; w < NBG_NW; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 12 + threadIdx.x]; if (threadIdx.x == 11) d_ += __longlong_as_double((long long)x_); else v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
         o << "    if (threadIdx.x == 11) { if (d_ != 0.0) atomicAdd((double*)&a.racc[" << p.reds[j].racc << "][12], d_); }\n";
-        o << "    else if (threadIdx.x == 10) { if (v_) atomicOr(&a.racc[" << p.reds[j].racc << "][10], v_); }\n";
+        o << "    else if (threadIdx.x == 10) { if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][10], nbg_xacc_flag_counts(v_)); }\n";
         o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
         o << "  }\n";
     }

@@ -12,7 +12,11 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "nbg_internal.hpp"
@@ -63,6 +67,67 @@ Dist::~Dist() {
     if (comm) nccl().CommDestroy((ncclComm_t)comm);
 }
 
+// In-process transport for tests (nbg_dist_init_loopback): P contexts driven by P host threads on
+// one GPU.  A collective = sync own stream, host barrier, each rank READS the other ranks' buffers
+// with its own copies / sum kernels (same process, same device), sync, barrier.  No kernel ever
+// waits on another rank's kernel (the synchronisation is on the host).
+struct LoopGroup {
+    int P = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long long gen = 0;
+    std::vector<const void *> ptr;
+    std::vector<std::vector<const unsigned long long *>> slots;
+    explicit LoopGroup(int p) : P(p), ptr(p, nullptr), slots(p) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long long g = gen;
+        if (++arrived == P) {
+            arrived = 0;
+            gen++;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+
+static void loop_allreduce_i32(Ctx &c, Dist &D, int *d, long long n) {
+    LoopGroup &G = *D.loop;
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    G.ptr[D.rank] = d;
+    G.barrier();
+    BufP tmp = alloc_buf(c, (size_t)std::max(n, 1ll) * 4);
+    std::vector<const int *> src(G.P);
+    for (int q = 0; q < G.P; q++) src[q] = (const int *)G.ptr[q];
+    gpu_sum_i32(c, n, G.P, src.data(), (int *)tmp->d);
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    G.barrier();
+    if (n > 0) NBG_CUDA(cudaMemcpyAsync(d, tmp->d, (size_t)n * 4, cudaMemcpyDeviceToDevice, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+static void loop_exchange(Ctx &c, Dist &D, char *W, size_t ws, const std::vector<int64_t> &off, const std::vector<int64_t> &cnt,
+                          const std::vector<const unsigned long long *> &sin, const std::vector<unsigned long long *> &sout) {
+    LoopGroup &G = *D.loop;
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    G.ptr[D.rank] = W;
+    G.slots[D.rank] = sin;
+    G.barrier();
+    for (int q = 0; q < G.P; q++)
+        if (q != D.rank && cnt[q] > 0)
+            NBG_CUDA(cudaMemcpyAsync(W + off[q] * ws, (const char *)G.ptr[q] + off[q] * ws, (size_t)cnt[q] * ws,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+    for (size_t i = 0; i < sout.size(); i++) {
+        std::vector<const unsigned long long *> src(G.P);
+        for (int q = 0; q < G.P; q++) src[q] = G.slots[q][i];
+        gpu_sum_slots(c, G.P, src.data(), sout[i]);
+    }
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    G.barrier();
+}
+
 static ncclComm_t comm_of(Dist &d) { return (ncclComm_t)d.comm; }
 
 }  // namespace nbg
@@ -74,16 +139,24 @@ static nbg_status to_status(nbg_ctx *ctx, const Error &e) {
     return e.st;
 }
 
-// exact allreduce of an exact-accumulator slot: the limbs are integers (sum, rank-order
-// independent), the flag word is OR-ed (split / max / join: NCCL has no bitwise OR), and the fp64
-// sum of out-of-window terms is summed in fp64
+// exact allreduce of an exact-accumulator slot: words 0-9 (limbs) and 10 (non-finite counts) are
+// integers (one int64 sum, rank-order independent); word 12 (fp64 sum of out-of-window terms) is
+// summed in fp64.  Callers may wrap several of these in one NCCL group.
 static void xacc_allreduce(nbg_ctx *ctx, Dist &D, const unsigned long long *src, unsigned long long *dst) {
-    NBG_NCCL(nccl().AllReduce(src, dst, 10, ncclInt64, ncclSum, comm_of(D), ctx->stream));
-    SlotP f3 = alloc_slot(*ctx), g3 = alloc_slot(*ctx);
-    gpu_flags_split(*ctx, src, f3->dptr());
-    NBG_NCCL(nccl().AllReduce(f3->dptr(), g3->dptr(), 3, ncclUint64, ncclMax, comm_of(D), ctx->stream));
-    gpu_flags_join(*ctx, g3->dptr(), dst);
+    NBG_NCCL(nccl().AllReduce(src, dst, 11, ncclInt64, ncclSum, comm_of(D), ctx->stream));
     NBG_NCCL(nccl().AllReduce(src + 12, dst + 12, 1, ncclFloat64, ncclSum, comm_of(D), ctx->stream));
+}
+
+static NodeP new_full_leaf(nbg_ctx *ctx, int type, int64_t n, BufP buf) {
+    auto y = std::make_shared<Node>();
+    y->op = Op::LEAF;
+    y->type = type;
+    y->n = n;
+    y->uid = ctx->new_id();
+    y->mat = true;
+    y->kind = VKind::FULL;
+    y->buf = std::move(buf);
+    return y;
 }
 
 extern "C" {
@@ -142,6 +215,22 @@ nbg_status nbg_dist_init(nbg_ctx *ctx, int rank, int nranks, const void *id128) 
     return NBG_SUCCESS;
 }
 
+nbg_status nbg_dist_init_loopback(nbg_ctx **ctxs, int nranks) {
+    if (!ctxs) return NBG_NULL_POINTER;
+    if (nranks < 1 || nranks > 64) return NBG_INVALID_VALUE;
+    for (int q = 0; q < nranks; q++)
+        if (!ctxs[q]) return NBG_NULL_POINTER;
+    auto G = std::make_shared<LoopGroup>(nranks);
+    for (int q = 0; q < nranks; q++) {
+        auto d = std::make_unique<Dist>();
+        d->rank = q;
+        d->nranks = nranks;
+        d->loop = G;
+        ctxs[q]->dist = std::move(d);
+    }
+    return NBG_SUCCESS;
+}
+
 nbg_status nbg_matrix_row_block(nbg_ctx *ctx, nbg_matrix *B, nbg_matrix A, int64_t lo, int64_t hi) {
     if (!ctx || !B || !A) return NBG_NULL_POINTER;
     if (A->ctx != ctx) return NBG_INVALID_OBJECT;
@@ -185,6 +274,7 @@ nbg_status nbg_vector_allgather(nbg_ctx *ctx, nbg_vector *w, nbg_vector u, const
     if (!ctx || !w || !u || !cuts) return NBG_NULL_POINTER;
     if (u->ctx != ctx) return NBG_INVALID_OBJECT;
     if (!ctx->dist) return NBG_INVALID_VALUE;
+    if (ctx->dist->loop) return NBG_NOT_IMPLEMENTED;   // NCCL groups only (see nbg_vector_allgather_reduce)
     try {
         Dist &D = *ctx->dist;
         NodeP x = u->node;
@@ -229,6 +319,7 @@ nbg_status nbg_scalar_allreduce(nbg_ctx *ctx, nbg_scalar *out, nbg_scalar s) {
     if (!ctx || !out || !s) return NBG_NULL_POINTER;
     if (s->ctx != ctx) return NBG_INVALID_OBJECT;
     if (!ctx->dist) return NBG_INVALID_VALUE;
+    if (ctx->dist->loop) return NBG_NOT_IMPLEMENTED;
     try {
         Dist &D = *ctx->dist;
         NodeP x = s->node;
@@ -272,6 +363,195 @@ nbg_status nbg_scalar_allreduce(nbg_ctx *ctx, nbg_scalar *out, nbg_scalar s) {
         auto *h = new nbg_scalar_s{ctx, y};
         y->user_refs++;
         *out = h;
+    } catch (const Error &e) {
+        return to_status(ctx, e);
+    }
+    return NBG_SUCCESS;
+}
+
+
+// ---------------------------------------------------------------- round-2 data plane
+
+nbg_status nbg_dist_exchange_plan(const int64_t *cuts, int nranks, int64_t ncols_g, int64_t *offsets, int64_t *counts) {
+    if (!cuts || !offsets || !counts) return NBG_NULL_POINTER;
+    if (nranks < 1 || ncols_g < 0) return NBG_INVALID_VALUE;
+    for (int q = 0; q < nranks; q++) {
+        if (cuts[q + 1] < cuts[q] || cuts[q] < 0) return NBG_INVALID_VALUE;
+        const int64_t a = std::min(cuts[q], ncols_g), b = std::min(cuts[q + 1], ncols_g);
+        offsets[q] = a;
+        counts[q] = b - a;
+    }
+    return NBG_SUCCESS;
+}
+
+nbg_status nbg_xacc_encode(const double *terms, int64_t n, uint64_t *slot) {
+    if ((!terms && n > 0) || !slot) return NBG_NULL_POINTER;
+    if (n < 0) return NBG_INVALID_VALUE;
+    unsigned long long L[SLOT_U64] = {0};
+    for (int64_t i = 0; i < n; i++) host_xacc_add(L, terms[i]);
+    memcpy(slot, L, sizeof L);
+    return NBG_SUCCESS;
+}
+
+nbg_status nbg_xacc_decode(const uint64_t *slot, double *value) {
+    if (!slot || !value) return NBG_NULL_POINTER;
+    *value = xacc_to_double((const unsigned long long *)slot);
+    return NBG_SUCCESS;
+}
+
+nbg_status nbg_scalar_export_slot(nbg_ctx *ctx, nbg_scalar s, uint64_t *slot) {
+    if (!ctx || !s || !slot) return NBG_NULL_POINTER;
+    if (s->ctx != ctx) return NBG_INVALID_OBJECT;
+    try {
+        NodeP x = s->node;
+        if (!x->mat) materialize(*ctx, {x});
+        if (!x->mat || x->sfmt != SFmt::XACC || !x->slot) return NBG_INVALID_OBJECT;
+        NBG_CUDA(cudaMemcpyAsync(slot, x->slot->dptr(), SLOT_U64 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        NBG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (ctx->latched != NBG_SUCCESS) return ctx->latched;
+    } catch (const Error &e) {
+        return to_status(ctx, e);
+    }
+    return NBG_SUCCESS;
+}
+
+nbg_status nbg_dist_graph_from_generator(nbg_ctx *ctx, const nbg_graphgen *g, int64_t bytes_per_row, nbg_matrix *AT_blk,
+                                         nbg_vector *deg_blk, int64_t *cuts, int64_t *ncols_g) {
+    if (!ctx || !g || !AT_blk || !deg_blk || !cuts || !ncols_g) return NBG_NULL_POINTER;
+    if (g->kind != NBG_GRAPH_RMAT && g->kind != NBG_GRAPH_ER) return NBG_INVALID_VALUE;
+    if (g->scale < 1 || g->scale > 30 || g->edge_factor < 1 || bytes_per_row < 0) return NBG_INVALID_VALUE;
+    try {
+        const int rank = ctx->dist ? ctx->dist->rank : 0, P = ctx->dist ? ctx->dist->nranks : 1;
+        if (P > 64) return NBG_NOT_IMPLEMENTED;
+        auto ar = [&](int *d, long long cnt) {
+            if (ctx->dist->loop) loop_allreduce_i32(*ctx, *ctx->dist, d, cnt);
+            else NBG_NCCL(nccl().AllReduce(d, d, (size_t)cnt, ncclInt32, ncclSum, comm_of(*ctx->dist), ctx->stream));
+        };
+        DistGraph G = gpu_dist_graph(*ctx, *g, rank, P, (long long)bytes_per_row, ar);
+        for (int q = 0; q <= P; q++) cuts[q] = G.cuts[q];
+        *ncols_g = G.ncols_g;
+        const int64_t nb = G.cuts[rank + 1] - G.cuts[rank];
+        *AT_blk = new nbg_matrix_s{ctx, G.blk};
+        NodeP d = new_full_leaf(ctx, NBG_INT32, nb, G.deg_blk);
+        d->user_refs++;
+        *deg_blk = new nbg_vector_s{ctx, d};
+        if (!ctx->dist_maps) ctx->dist_maps = std::make_shared<std::map<std::pair<int64_t, int64_t>, BufP>>();
+    } catch (const Error &e) {
+        return to_status(ctx, e);
+    }
+    return NBG_SUCCESS;
+}
+
+nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u_blk, const int64_t *cuts, int64_t ncols_g,
+                                       int nscal, const nbg_scalar *s_in, nbg_scalar *s_out) {
+    if (!ctx || !w || !u_blk || !cuts || (nscal > 0 && (!s_in || !s_out))) return NBG_NULL_POINTER;
+    if (u_blk->ctx != ctx) return NBG_INVALID_OBJECT;
+    if (nscal < 0 || nscal > 8 || ncols_g < 0) return NBG_INVALID_VALUE;
+    try {
+        const int rank = ctx->dist ? ctx->dist->rank : 0, P = ctx->dist ? ctx->dist->nranks : 1;
+        if (ncols_g > cuts[P]) return NBG_INVALID_VALUE;
+        NodeP x = u_blk->node;
+        const int64_t c0 = cuts[rank], nb = cuts[rank + 1] - cuts[rank];
+        if (x->n != nb) return NBG_DIMENSION_MISMATCH;
+        if (x->scalar || structured_kind(x->kind)) return NBG_NOT_IMPLEMENTED;
+        std::vector<NodeP> sin;
+        for (int i = 0; i < nscal; i++) {
+            if (!s_in[i] || s_in[i]->ctx != ctx) return NBG_INVALID_OBJECT;
+            sin.push_back(s_in[i]->node);
+        }
+        const size_t ws = type_size(x->type);
+        BufP W = alloc_buf(*ctx, (size_t)std::max<int64_t>(ncols_g, 1) * ws + 64);
+        // ---- this rank's block, written by the producing kernel straight into W[c0 + i] (i < ncols_g - c0)
+        if (!ctx->dist_maps) ctx->dist_maps = std::make_shared<std::map<std::pair<int64_t, int64_t>, BufP>>();
+        auto key = std::make_pair(c0, nb);
+        BufP &map = (*ctx->dist_maps)[key];
+        if (!map) {
+            map = alloc_buf(*ctx, (size_t)std::max<int64_t>(nb, 1) * 4);
+            gpu_offset_map(*ctx, nb, c0, ncols_g, (int *)map->d);
+        }
+        std::vector<NodeP> roots;
+        if (!x->mat) {
+            ctx->out_targets[x.get()] = Ctx::OutTarget{W, (const int *)map->d};
+            roots.push_back(x);
+        }
+        for (const NodeP &sn : sin)
+            if (!sn->mat) roots.push_back(sn);
+        try {
+            if (!roots.empty()) materialize(*ctx, roots);
+        } catch (...) {
+            ctx->out_targets.erase(x.get());
+            throw;
+        }
+        ctx->out_targets.erase(x.get());
+        if (x->mat) {   // already materialised (or iso): copy its block into place
+            if (x->kind == VKind::EMPTY) return NBG_NOT_IMPLEMENTED;
+            ensure_full(*ctx, x);
+            const void *src = x->kind == VKind::ISO ? x->full_cache->d : x->buf->d;
+            const int64_t cnt = std::max<int64_t>(0, std::min(nb, ncols_g - c0));
+            if (cnt > 0)
+                NBG_CUDA(cudaMemcpyAsync((char *)W->d + c0 * ws, src, (size_t)cnt * ws, cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        std::vector<NodeP> sout;
+        for (const NodeP &sn : sin) {
+            if (!sn->mat) {   // a pending scalar op: evaluate on the host
+                double v = scalar_read(*ctx, sn);
+                sn->mat = true;
+                sn->sfmt = SFmt::HOST;
+                sn->hval = v;
+                sn->a.reset();
+            }
+            if (sn->sfmt != SFmt::XACC && P > 1) return NBG_NOT_IMPLEMENTED;   // float PLUS reductions only
+            auto y = std::make_shared<Node>();
+            y->op = Op::LEAF;
+            y->scalar = true;
+            y->type = sn->type;
+            y->uid = ctx->new_id();
+            y->mat = true;
+            if (P == 1) {
+                y->sfmt = sn->sfmt;
+                y->slot = sn->slot;
+                y->hval = sn->hval;
+            } else {
+                y->sfmt = SFmt::XACC;
+                y->slot = alloc_slot(*ctx);
+            }
+            sout.push_back(y);
+        }
+        // ---- one NCCL group: the P blocks broadcast in place + the exact scalar sums
+        if (P > 1 && ctx->dist->loop) {
+            std::vector<int64_t> off(P), cnt(P);
+            nbg_dist_exchange_plan(cuts, P, ncols_g, off.data(), cnt.data());
+            std::vector<const unsigned long long *> si;
+            std::vector<unsigned long long *> so;
+            for (size_t i = 0; i < sin.size(); i++) {
+                si.push_back(sin[i]->slot->dptr());
+                so.push_back(sout[i]->slot->dptr());
+            }
+            loop_exchange(*ctx, *ctx->dist, (char *)W->d, ws, off, cnt, si, so);
+        } else if (P > 1) {
+            Dist &D = *ctx->dist;
+            std::vector<int64_t> off(P), cnt(P);
+            nbg_dist_exchange_plan(cuts, P, ncols_g, off.data(), cnt.data());
+            ncclDataType_t dt = ws == 8 ? ncclInt64 : (ws == 4 ? ncclInt32 : ncclUint8);
+            char *dst = (char *)W->d;
+            cudaEvent_t ev0;
+            timing_begin(*ctx, "comm", &ev0);
+            NBG_NCCL(nccl().GroupStart());
+            for (int q = 0; q < P; q++)
+                if (cnt[q] > 0)
+                    NBG_NCCL(nccl().Broadcast(dst + off[q] * ws, dst + off[q] * ws, (size_t)cnt[q], dt, q, comm_of(D), ctx->stream));
+            for (size_t i = 0; i < sin.size(); i++) xacc_allreduce(ctx, D, sin[i]->slot->dptr(), sout[i]->slot->dptr());
+            NBG_NCCL(nccl().GroupEnd());
+            timing_end(*ctx, "comm", ev0);
+        }
+        for (size_t i = 0; i < sout.size(); i++) {
+            if (sout[i]->slot && P > 1) issue_readback(*ctx, *sout[i]->slot);
+            sout[i]->user_refs++;
+            s_out[i] = new nbg_scalar_s{ctx, sout[i]};
+        }
+        NodeP y = new_full_leaf(ctx, x->type, ncols_g, W);
+        y->user_refs++;
+        *w = new nbg_vector_s{ctx, y};
     } catch (const Error &e) {
         return to_status(ctx, e);
     }

@@ -490,22 +490,268 @@ TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta) {
 namespace {
 }  // namespace
 
-// exact-accumulator flags across ranks (dist.cpp): NCCL has no bitwise OR, so the flag word is
-// split into one word per flag, max-reduced, and joined again
-__global__ void k_flags_split(const unsigned long long *slot, unsigned long long *three) {
-    const unsigned long long f = slot[10];
-    three[0] = f & 1ull;
-    three[1] = f & 2ull;
-    three[2] = f & 4ull;
+__global__ void k_offset_map(long long nb, long long c0, long long limit, int *map) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += (long long)gridDim.x * blockDim.x)
+        map[i] = (c0 + i < limit) ? (int)(c0 + i) : -1;
 }
-__global__ void k_flags_join(const unsigned long long *three, unsigned long long *slot) { slot[10] = three[0] | three[1] | three[2]; }
-void gpu_flags_split(Ctx &c, const unsigned long long *slot, unsigned long long *three) {
-    k_flags_split<<<1, 1, 0, c.stream>>>(slot, three);
+struct PtrList { const void *p[64]; };
+__global__ void k_sum_i32(long long n, int nsrc, PtrList src, int *dst) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int s = 0;
+        for (int q = 0; q < nsrc; q++) s += ((const int *)src.p[q])[i];
+        dst[i] = s;
+    }
+}
+void gpu_sum_i32(Ctx &c, int64_t n, int nsrc, const int *const *srcs, int *dst) {
+    if (n <= 0) return;
+    if (nsrc > 64) fail(NBG_NOT_IMPLEMENTED, "more than 64 ranks");
+    PtrList l;
+    for (int q = 0; q < nsrc; q++) l.p[q] = srcs[q];
+    k_sum_i32<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, nsrc, l, dst);
     NBG_CUDA(cudaGetLastError());
 }
-void gpu_flags_join(Ctx &c, const unsigned long long *three, unsigned long long *slot) {
-    k_flags_join<<<1, 1, 0, c.stream>>>(three, slot);
+// exact-accumulator slots of several ranks: words 0-10 integer sums, word 12 fp64 sum (rank order)
+__global__ void k_sum_slots(int nsrc, PtrList src, unsigned long long *dst) {
+    const int w = threadIdx.x;
+    if (w > 12 || w == 11) return;
+    if (w == 12) {
+        double d = 0.0;
+        for (int q = 0; q < nsrc; q++) d += __longlong_as_double((long long)((const unsigned long long *)src.p[q])[12]);
+        dst[12] = (unsigned long long)__double_as_longlong(d);
+    } else {
+        unsigned long long s = 0;
+        for (int q = 0; q < nsrc; q++) s += ((const unsigned long long *)src.p[q])[w];
+        dst[w] = s;
+    }
+}
+void gpu_sum_slots(Ctx &c, int nsrc, const unsigned long long *const *slots, unsigned long long *dst) {
+    if (nsrc > 64) fail(NBG_NOT_IMPLEMENTED, "more than 64 ranks");
+    PtrList l;
+    for (int q = 0; q < nsrc; q++) l.p[q] = slots[q];
+    k_sum_slots<<<1, 32, 0, c.stream>>>(nsrc, l, dst);
     NBG_CUDA(cudaGetLastError());
+}
+
+void gpu_offset_map(Ctx &c, int64_t nb, int64_t c0, int64_t limit, int *map) {
+    if (nb <= 0) return;
+    k_offset_map<<<grid_for(nb, c.num_sms), 256, 0, c.stream>>>(nb, c0, limit, map);
+    NBG_CUDA(cudaGetLastError());
+    c.stats.kernels_launched++;
+}
+
+// ---------------------------------------------------------------- per-rank graph setup (multi-GPU)
+// every rank regenerates all edges (counter-based generator), dedups the edges whose
+// ORIGINAL destination lies in its range [lo, hi) to get exact local degree contributions, the
+// degrees are summed across ranks, every rank derives the same symmetric relabel pi (vertices by
+// descending out-degree, ties by id: the gather layout; dangling vertices last), the rows are cut
+// in pi-space by bytes, and each rank builds its row block: rows pi in [c_r, c_r+1), entries in the
+// ORIGINAL column order of each row (so every row sum is bit-identical to the one-GPU run), column
+// ids mapped to pi (all < ncols_g: a column of AT is a vertex with out-edges).
+__global__ void k_keys_in_range(long long m, int shift, const int *src, const int *dst, int lo, int hi,
+                                unsigned long long *keys, unsigned char *keep) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x) {
+        const int s = src[e], d = dst[e];
+        const bool k = d >= lo && d < hi && s != d;
+        keys[e] = ((unsigned long long)(unsigned)(d - lo) << shift) | (unsigned long long)(unsigned)s;
+        keep[e] = k ? 1 : 0;
+    }
+}
+__global__ void k_keys_in_block(long long m, int shift, const int *src, const int *dst, const int *pi, int c0, int c1,
+                                unsigned long long *keys, unsigned char *keep) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x) {
+        const int s = src[e], d = dst[e];
+        const int pd = pi[d];
+        const bool k = pd >= c0 && pd < c1 && s != d;
+        keys[e] = ((unsigned long long)(unsigned)(pd - c0) << shift) | (unsigned long long)(unsigned)s;
+        keep[e] = k ? 1 : 0;
+    }
+}
+// first of equal keys (the keys hold no self-loops)
+__global__ void k_first_of_equal(long long m, const unsigned long long *keys, unsigned char *flags) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+        flags[i] = (i == 0 || keys[i - 1] != keys[i]) ? 1 : 0;
+}
+__global__ void k_deg_counts(long long m, int shift, int lo, const unsigned long long *keys, int *outdeg, int *indeg) {
+    const unsigned long long mask = (1ull << shift) - 1ull;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        atomicAdd(&outdeg[(int)(k & mask)], 1);
+        atomicAdd(&indeg[lo + (int)(k >> shift)], 1);
+    }
+}
+__global__ void k_pi_keys(long long n, const int *deg, unsigned *key, int *ids, long long *nonempty) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+        const int d = deg[j];
+        key[j] = d > 0 ? ~(unsigned)d : 0xffffffffu;    // descending degree, dangling last (gather layout)
+        ids[j] = (int)j;
+        if (d > 0) atomicAdd((unsigned long long *)nonempty, 1ull);
+    }
+}
+// row cost in pi order: 4 * row length + 8 + bytes_per_row (nbg_partition_rows' model)
+__global__ void k_pi_cost(long long n, const int *order, const int *indeg, long long bpr, long long *cost) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        cost[k] = 4ll * indeg[order[k]] + 8 + bpr;
+}
+// cut q (1 <= q < P): the row boundary b whose exclusive prefix cost is nearest to q/P of the total
+// (inclusive prefix `incl`, n entries) -- nbg_partition_rows' rule, on the device
+__global__ void k_cuts(long long n, int P, const long long *incl, long long *cuts) {
+    const int q = threadIdx.x;
+    if (q > P) return;
+    if (q == 0) { cuts[0] = 0; return; }
+    if (q == P) { cuts[P] = n; return; }
+    const __int128 total = n ? (__int128)incl[n - 1] : 0;
+    const __int128 t = total * q;
+    // smallest b in [0, n] with excl(b) * P >= t, excl(b) = b ? incl[b - 1] : 0
+    long long lo = 0, hi = n;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        const __int128 ex = mid ? (__int128)incl[mid - 1] : 0;
+        if (ex * P >= t) hi = mid; else lo = mid + 1;
+    }
+    long long b = lo;
+    if (b > 0) {
+        const __int128 e1 = (__int128)incl[b - 1] * P - t;                       // >= 0
+        const __int128 e0 = t - (b > 1 ? (__int128)incl[b - 2] * P : (__int128)0);   // excl(b-1)
+        if (e0 <= e1) b -= 1;
+    }
+    cuts[q] = b;
+}
+__global__ void k_block_csr(long long nnz, int shift, const unsigned long long *keys, const int *pi, int *colidx) {
+    const unsigned long long mask = (1ull << shift) - 1ull;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += (long long)gridDim.x * blockDim.x)
+        colidx[i] = pi[(int)(keys[i] & mask)];
+}
+__global__ void k_gather_int(long long nb, const int *order, long long c0, const int *src, int *dst) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < nb; k += (long long)gridDim.x * blockDim.x)
+        dst[k] = src[order[c0 + k]];
+}
+
+// select the flagged keys of `keys` (m) into `out`, returning the count (synchronises)
+static long long select_keys(Ctx &c, long long m, const unsigned long long *keys, const unsigned char *keep,
+                             unsigned long long *out) {
+    BufP nsel = alloc_buf(c, 8);
+    size_t tb = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb, keys, keep, out, (long long *)nsel->d, (int64_t)m, c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, keys, keep, out, (long long *)nsel->d, (int64_t)m, c.stream));
+    long long h = 0;
+    NBG_CUDA(cudaMemcpyAsync(&h, nsel->d, 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+}
+static void sort_keys(Ctx &c, long long m, unsigned long long *keys, unsigned long long *tmpk, int bits) {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, tmpk, (int64_t)m, 0, bits, c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    if (m > 0) NBG_CUDA(cub::DeviceRadixSort::SortKeys(tmp->d, tb, keys, tmpk, (int64_t)m, 0, bits, c.stream));
+}
+
+DistGraph gpu_dist_graph(Ctx &c, const nbg_graphgen &g, int rank, int P, long long bytes_per_row,
+                         const std::function<void(int *, long long)> &allreduce_int_sum) {
+    const long long n = 1ll << g.scale;
+    const long long m = (long long)g.edge_factor * n;
+    const int shift = bits_for(std::max<long long>(n, 2));
+    if (2 * shift + 1 > 64) fail(NBG_INVALID_VALUE, "graph too large for 64-bit keys");
+    cudaEvent_t ev0;
+    timing_begin(c, "graph", &ev0);
+    BufP src = alloc_buf(c, (size_t)std::max(m, 1ll) * 4), dst = alloc_buf(c, (size_t)std::max(m, 1ll) * 4);
+    gpu_graph_edges(c, g, (int *)src->d, (int *)dst->d);
+    const int gr = grid_for(std::max(m, 1ll), c.num_sms);
+    BufP keys = alloc_buf(c, (size_t)std::max(m, 1ll) * 8), keys2 = alloc_buf(c, (size_t)std::max(m, 1ll) * 8);
+    BufP keep = alloc_buf(c, (size_t)std::max(m, 1ll));
+    // ---- 1. exact degrees: dedup the edges whose original destination is in this rank's range
+    const int lo = (int)(n * rank / P), hi = (int)(n * (rank + 1) / P);
+    k_keys_in_range<<<gr, 256, 0, c.stream>>>(m, shift, (const int *)src->d, (const int *)dst->d, lo, hi,
+                                             (unsigned long long *)keys->d, (unsigned char *)keep->d);
+    NBG_CUDA(cudaGetLastError());
+    long long ml = select_keys(c, m, (const unsigned long long *)keys->d, (const unsigned char *)keep->d,
+                               (unsigned long long *)keys2->d);
+    sort_keys(c, ml, (unsigned long long *)keys2->d, (unsigned long long *)keys->d, 2 * shift);
+    if (ml > 0) k_first_of_equal<<<grid_for(ml, c.num_sms), 256, 0, c.stream>>>(ml, (const unsigned long long *)keys->d,
+                                                                                   (unsigned char *)keep->d);
+    long long mu = ml ? select_keys(c, ml, (const unsigned long long *)keys->d, (const unsigned char *)keep->d,
+                                    (unsigned long long *)keys2->d) : 0;
+    BufP deg = alloc_buf(c, (size_t)n * 4), indeg = alloc_buf(c, (size_t)n * 4);
+    NBG_CUDA(cudaMemsetAsync(deg->d, 0, (size_t)n * 4, c.stream));
+    NBG_CUDA(cudaMemsetAsync(indeg->d, 0, (size_t)n * 4, c.stream));
+    if (mu > 0) k_deg_counts<<<grid_for(mu, c.num_sms), 256, 0, c.stream>>>(mu, shift, lo, (const unsigned long long *)keys2->d,
+                                                                              (int *)deg->d, (int *)indeg->d);
+    NBG_CUDA(cudaGetLastError());
+    if (P > 1) {
+        allreduce_int_sum((int *)deg->d, n);
+        allreduce_int_sum((int *)indeg->d, n);
+    }
+    // ---- 2. symmetric relabel pi (identical on every rank)
+    BufP key = alloc_buf(c, (size_t)n * 4), key2 = alloc_buf(c, (size_t)n * 4);
+    BufP ids = alloc_buf(c, (size_t)n * 4), order = alloc_buf(c, (size_t)n * 4), ne = alloc_buf(c, 8);
+    NBG_CUDA(cudaMemsetAsync(ne->d, 0, 8, c.stream));
+    k_pi_keys<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, (const int *)deg->d, (unsigned *)key->d, (int *)ids->d,
+                                                            (long long *)ne->d);
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
+                                    (int *)order->d, (int64_t)n, 0, 32, c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    NBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp->d, tb, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
+                                             (int *)order->d, (int64_t)n, 0, 32, c.stream));
+    BufP pi = alloc_buf(c, (size_t)n * 4);
+    k_perm_from_order<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, (const int *)order->d, (int *)pi->d);
+    // ---- 3. row cuts in pi-space, balanced by bytes
+    BufP cost = alloc_buf(c, (size_t)n * 8), incl = alloc_buf(c, (size_t)n * 8), dcuts = alloc_buf(c, (size_t)(P + 1) * 8);
+    k_pi_cost<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, (const int *)order->d, (const int *)indeg->d, bytes_per_row,
+                                                            (long long *)cost->d);
+    tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, (const long long *)cost->d, (long long *)incl->d, (int64_t)n, c.stream);
+    if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+    NBG_CUDA(cub::DeviceScan::InclusiveSum(tmp->d, tb, (const long long *)cost->d, (long long *)incl->d, (int64_t)n, c.stream));
+    k_cuts<<<1, 64, 0, c.stream>>>(n, P, (const long long *)incl->d, (long long *)dcuts->d);
+    NBG_CUDA(cudaGetLastError());
+    DistGraph G;
+    G.n = n;
+    G.cuts.resize(P + 1);
+    long long hne = 0;
+    NBG_CUDA(cudaMemcpyAsync(G.cuts.data(), dcuts->d, (size_t)(P + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaMemcpyAsync(&hne, ne->d, 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    G.ncols_g = hne;
+    const long long c0 = G.cuts[rank], c1 = G.cuts[rank + 1], nb = c1 - c0;
+    // ---- 4. this rank's row block: rows pi in [c0, c1), entries by original column order
+    k_keys_in_block<<<gr, 256, 0, c.stream>>>(m, shift, (const int *)src->d, (const int *)dst->d, (const int *)pi->d,
+                                             (int)c0, (int)c1, (unsigned long long *)keys->d, (unsigned char *)keep->d);
+    NBG_CUDA(cudaGetLastError());
+    ml = select_keys(c, m, (const unsigned long long *)keys->d, (const unsigned char *)keep->d, (unsigned long long *)keys2->d);
+    src.reset();
+    dst.reset();
+    sort_keys(c, ml, (unsigned long long *)keys2->d, (unsigned long long *)keys->d, 2 * shift + 1);
+    if (ml > 0) k_first_of_equal<<<grid_for(ml, c.num_sms), 256, 0, c.stream>>>(ml, (const unsigned long long *)keys->d,
+                                                                                   (unsigned char *)keep->d);
+    const long long nnz = ml ? select_keys(c, ml, (const unsigned long long *)keys->d, (const unsigned char *)keep->d,
+                                           (unsigned long long *)keys2->d) : 0;
+    auto A = std::make_shared<Mat>();
+    A->ctx = &c;
+    A->id = c.new_id();
+    A->nrows = nb;
+    A->ncols = G.ncols_g;           // every column id is < ncols_g (sources have out-edges)
+    A->nnz = nnz;
+    A->type = NBG_FP32;
+    A->iso = 1.0;
+    A->prelabeled = true;           // columns already in the gather layout (no second relabel)
+    A->rowptr = alloc_buf(c, (size_t)(nb + 1) * 8);
+    A->colidx = alloc_buf(c, (size_t)std::max(nnz, 1ll) * 4);
+    if (nnz > 0)
+        k_block_csr<<<grid_for(nnz, c.num_sms), 256, 0, c.stream>>>(nnz, shift, (const unsigned long long *)keys2->d,
+                                                                    (const int *)pi->d, (int *)A->colidx->d);
+    k_rowptr<<<grid_for(nb + 1, c.num_sms), 256, 0, c.stream>>>(nb, nnz, shift, (const unsigned long long *)keys2->d,
+                                                               (long long *)A->rowptr->d);
+    G.deg_blk = alloc_buf(c, (size_t)std::max(nb, 1ll) * 4);
+    if (nb > 0)
+        k_gather_int<<<grid_for(nb, c.num_sms), 256, 0, c.stream>>>(nb, (const int *)order->d, c0, (const int *)deg->d,
+                                                                    (int *)G.deg_blk->d);
+    NBG_CUDA(cudaGetLastError());
+    G.blk = A;
+    G.order = order;
+    timing_end(c, "graph", ev0);
+    c.stats.kernels_launched += 16;
+    return G;
 }
 
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst) {
@@ -596,7 +842,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     }
     // ---- gather layout: relabel columns by descending count (big matrices only)
     const char *rl = getenv("NBG_RELABEL");
-    const bool want = rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15));
+    const bool want = !A.prelabeled && (rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15)));
     BufP colsrc = A.colidx;
     if (want && A.nnz > 0 && !A.vals) {
         const long long nc = A.ncols;

@@ -64,13 +64,20 @@ __device__ __forceinline__ long long nbg_abs(long long a) { return a < 0 ? -a : 
 // A reduction's cross-block combine: 10 limbs of 32-bit pieces (LSB weight 2^-160) added with
 // 64-bit atomics.  Integer addition is associative, so the combined value does not depend on
 // the order in which thread blocks finish (deterministic).
+// Word 10 of a global slot COUNTS non-finite contributions (NaN in bits 0-20, +inf in 21-41,
+// -inf in 42-62; each block / direct term adds at most one per kind), so slots of several ranks
+// combine by one integer sum as well.  Per-warp local accumulators keep OR bits (1 NaN, 2 +inf,
+// 4 -inf) in word 10; nbg_xacc_flag_counts converts them when they are flushed.
+__device__ __forceinline__ u64 nbg_xacc_flag_counts(u64 f) {
+    return ((f & 1ull) ? 1ull : 0ull) + ((f & 2ull) ? (1ull << 21) : 0ull) + ((f & 4ull) ? (1ull << 42) : 0ull);
+}
 __device__ void nbg_xacc_add(u64 *acc, double d) {
     if (d == 0.0) return;
     long long bits = __double_as_longlong(d);
     int e = (int)((bits >> 52) & 0x7ff);
     if (e == 0x7ff) {
         u64 f = ((bits & 0xFFFFFFFFFFFFFull) != 0) ? 1ull : (bits < 0 ? 4ull : 2ull);
-        atomicOr(&acc[10], f);
+        atomicAdd(&acc[10], nbg_xacc_flag_counts(f));
         return;
     }
     u64 m = (u64)bits & 0xFFFFFFFFFFFFFull;
@@ -120,11 +127,11 @@ __device__ void nbg_xacc_add_local(u64 *acc, double d) {
 
 __device__ double nbg_xacc_window(const u64 *L);
 __device__ double nbg_xacc_value(const u64 *L) {
-    u64 flags = L[10];
-    if (flags & 9ull) return __longlong_as_double(0x7ff8000000000000ll);
-    if ((flags & 6ull) == 6ull) return __longlong_as_double(0x7ff8000000000000ll);
-    if (flags & 2ull) return __longlong_as_double(0x7ff0000000000000ll);
-    if (flags & 4ull) return __longlong_as_double((long long)0xfff0000000000000ull);
+    const u64 flags = L[10];
+    const u64 nan = flags & 0x1FFFFFull, pinf = (flags >> 21) & 0x1FFFFFull, ninf = (flags >> 42) & 0x1FFFFFull;
+    if (nan || (pinf && ninf)) return __longlong_as_double(0x7ff8000000000000ll);
+    if (pinf) return __longlong_as_double(0x7ff0000000000000ll);
+    if (ninf) return __longlong_as_double((long long)0xfff0000000000000ull);
     const double extra = __longlong_as_double((long long)L[12]);   // out-of-window terms
     return nbg_xacc_window(L) + extra;
 }

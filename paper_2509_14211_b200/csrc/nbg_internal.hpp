@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <cstring>
 #include <map>
+#include <functional>
 #include <memory>
 #include <string>
 #include <unordered_map>
@@ -177,6 +178,7 @@ struct Mat {
     BufP rowptr, colidx, vals;   // vals null => iso
     std::unique_ptr<SpmvPlan> plan;
     int64_t max_row = -1;
+    bool prelabeled = false;     // columns already in a gather layout (multi-GPU row blocks): no relabel
 };
 using MatP = std::shared_ptr<Mat>;
 
@@ -320,9 +322,11 @@ struct TimingClass {
 
 // ---------------------------------------------------------------- context
 
+struct LoopGroup;   // dist.cpp: in-process transport (P contexts in P host threads on one GPU, tests)
 struct Dist {
     int rank = 0, nranks = 1;
     void *comm = nullptr;   // ncclComm_t
+    std::shared_ptr<LoopGroup> loop;   // set instead of comm by nbg_dist_init_loopback
     ~Dist();
 };
 
@@ -369,6 +373,10 @@ struct Ctx {
     // learned hints: producer signature hash + output index -> templates
     std::map<std::pair<uint64_t, int>, std::vector<Hint>> hints;
 
+    // output targets of the current materialize call (multi-GPU: a block written straight into
+    // the exchange buffer through a scatter map); see dist.cpp nbg_vector_allgather_reduce
+    struct OutTarget { BufP buf; const int *map = nullptr; };
+    std::unordered_map<const Node *, OutTarget> out_targets;
     // nodes user handles point to (weak): nbg_wait_all materialises the live pending ones
     std::vector<std::weak_ptr<Node>> user_nodes;
     size_t user_nodes_live = 0;
@@ -379,6 +387,8 @@ struct Ctx {
 
     // distributed
     std::unique_ptr<Dist> dist;
+    // row -> position maps of this rank's block in the exchange buffer, per (first row, rows)
+    std::shared_ptr<std::map<std::pair<int64_t, int64_t>, BufP>> dist_maps;
 
     uint64_t new_id() { return next_id++; }
     ~Ctx();
@@ -447,14 +457,25 @@ void gpu_l2_touch(Ctx &c, const void *base, size_t bytes, const cudaLaunchAttrib
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst);
 MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out);
 void gpu_build_spmv_plan(Ctx &c, Mat &A);
+// per-rank multi-GPU graph setup (graph.cu)
+struct DistGraph {
+    MatP blk;                    // rows pi in [cuts[rank], cuts[rank+1]) x ncols_g columns (pi ids)
+    BufP deg_blk;                // int32 out-degrees of the block's vertices (pi order)
+    BufP order;                  // int32[n]: pi^-1 (vertex of each pi position)
+    std::vector<int64_t> cuts;   // P + 1 row cuts in pi-space
+    int64_t n = 0, ncols_g = 0;
+};
+DistGraph gpu_dist_graph(Ctx &c, const nbg_graphgen &g, int rank, int P, long long bytes_per_row,
+                         const std::function<void(int *, long long)> &allreduce_int_sum);
 TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta);   // null if not applicable
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
 void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng);
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);
 void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base, long long *out);
 void host_xacc_add(unsigned long long *limbs, double d);
-void gpu_flags_split(Ctx &c, const unsigned long long *slot, unsigned long long *three);
-void gpu_flags_join(Ctx &c, const unsigned long long *three, unsigned long long *slot);
+void gpu_offset_map(Ctx &c, int64_t nb, int64_t c0, int64_t limit, int *map);   // map[i] = c0+i < limit ? c0+i : -1
+void gpu_sum_i32(Ctx &c, int64_t n, int nsrc, const int *const *srcs, int *dst);      // dst = sum of nsrc arrays (host ptr list)
+void gpu_sum_slots(Ctx &c, int nsrc, const unsigned long long *const *slots, unsigned long long *dst);  // exact slot sum
 
 // host arithmetic (used for eager iso folding and host-side scalar ops)
 double host_unop(int code, int t, double x, double c0, double c1);

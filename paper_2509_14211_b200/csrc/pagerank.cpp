@@ -175,84 +175,100 @@ extern "C" nbg_status nbg_pagerank(nbg_ctx *ctx, nbg_matrix AT, nbg_vector deg, 
     return NBG_SUCCESS;
 }
 
-// ---------------------------------------------------------------- distributed (SURVEY 8(e))
-// Same sweep on this rank's row block; the gathered vector is exchanged with
-// nbg_vector_allgather and the two scalars (dangling mass, delta) with nbg_scalar_allreduce.
-extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg, const int64_t *cuts,
-                                        const nbg_pr_params *p, nbg_vector *r_out, int *sweeps_out, double *delta_hist) {
-    if (!ctx || !AT_blk || !deg || !cuts || !p || !r_out) return NBG_NULL_POINTER;
-    if (!ctx->dist) return NBG_INVALID_VALUE;
+// ---------------------------------------------------------------- distributed (SURVEY 8(e), DESIGN.md §8)
+// Every rank holds its row block of the symmetrically relabelled AT (nbg_dist_graph_from_generator:
+// rows and columns in the gather layout pi, so rank r's scaled ranks are the contiguous slice
+// [cuts[r], cuts[r+1]) of the next gathered vector).  One sweep = ONE fused kernel (mxv + teleport /
+// dangling epilogue + the delta and next dangling-mass reductions + the scaled ranks written straight
+// into this rank's slice of the exchange buffer) and ONE NCCL group (the P slices broadcast in place,
+// the two scalars' exact limbs summed): nbg_vector_allgather_reduce.  Row sums keep each row's
+// original entry order, so the ranks are bit-identical for every P.
+extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg_blk, const int64_t *cuts,
+                                        int64_t ncols_g, const nbg_pr_params *p, nbg_vector *r_out, int *sweeps_out,
+                                        double *delta_hist) {
+    if (!ctx || !AT_blk || !deg_blk || !cuts || !p || !r_out) return NBG_NULL_POINTER;
     if (!(p->alpha > 0.0 && p->alpha < 1.0) || p->itermax < 1) return NBG_INVALID_VALUE;
     if (p->dangling != NBG_PR_UNIFORM && p->dangling != NBG_PR_DROP) return NBG_INVALID_VALUE;
     if (p->type != NBG_FP32 && p->type != NBG_FP64) return NBG_DOMAIN_MISMATCH;
-    const int rank = ctx->dist->rank, P = ctx->dist->nranks;
-    const int64_t n = cuts[P], lo = cuts[rank], nb = cuts[rank + 1] - cuts[rank];
+    const int rank = ctx->dist ? ctx->dist->rank : 0, P = ctx->dist ? ctx->dist->nranks : 1;
+    const int64_t n = cuts[P], nb = cuts[rank + 1] - cuts[rank];
     int64_t rows = 0, cols = 0, nd = 0;
     TRY(nbg_matrix_nrows(ctx, AT_blk, &rows));
     TRY(nbg_matrix_ncols(ctx, AT_blk, &cols));
-    TRY(nbg_vector_size(ctx, deg, &nd));
-    if (rows != nb || cols != n || nd != n) return NBG_DIMENSION_MISMATCH;
+    TRY(nbg_vector_size(ctx, deg_blk, &nd));
+    if (rows != nb || cols != ncols_g || nd != nb || ncols_g > n) return NBG_DIMENSION_MISMATCH;
     const int T = p->type;
     const bool uniform = p->dangling == NBG_PR_UNIFORM;
     const double a_n = p->alpha / (double)n, tele = (1.0 - p->alpha) / (double)n;
 
-    nbg_vector d64, dinv, dinv_blk;
-    TRY(nbg_apply(ctx, &d64, NBG_FP64, nbg_unop{NBG_RECIP_SCALED, p->alpha, 0.0}, deg));
-    TRY(nbg_convert(ctx, &dinv, T, d64));
+    // Fig. 6 l.278-281 `d` (reading Q2: dinv = (T)(alpha / deg), 0 for dangling vertices)
+    nbg_vector d64, dinv_blk, mask = nullptr;
+    TRY(nbg_apply(ctx, &d64, NBG_FP64, nbg_unop{NBG_RECIP_SCALED, p->alpha, 0.0}, deg_blk));
+    TRY(nbg_convert(ctx, &dinv_blk, T, d64));
     nbg_vector_free(ctx, d64);
-    void *dptr = nullptr;
-    TRY(nbg_vector_device_ptr(ctx, dinv, &dptr));
-    TRY(nbg_vector_from_dense(ctx, &dinv_blk, T, nb, (char *)dptr + lo * (T == NBG_FP32 ? 4 : 8), NBG_DEVICE, NBG_BORROW));
+    TRY(nbg_vector_wait(ctx, dinv_blk));
+    if (uniform) TRY(nbg_apply(ctx, &mask, T, nbg_unop{NBG_ISZERO, 0, 0}, dinv_blk));
 
-    auto sweep = [&](nbg_vector t, nbg_vector *r_new, nbg_scalar *delta) -> nbg_status {
-        nbg_scalar c = nullptr;
-        if (uniform) {
-            nbg_vector mask, tm;
-            nbg_scalar ds_loc, ds;
-            TRY(nbg_apply(ctx, &mask, T, nbg_unop{NBG_ISZERO, 0, 0}, dinv_blk));
-            TRY(nbg_ewise_mult(ctx, &tm, T, nbg_binop{NBG_TIMES, 0}, t, mask));
-            nbg_vector_free(ctx, mask);
-            TRY(nbg_reduce(ctx, &ds_loc, NBG_FP64, NBG_PLUS, tm));
-            nbg_vector_free(ctx, tm);
-            TRY(nbg_scalar_allreduce(ctx, &ds, ds_loc));
-            nbg_scalar_free(ctx, ds_loc);
-            TRY(nbg_scalar_apply(ctx, &c, NBG_FP64, nbg_unop{NBG_AXPB, a_n, tele}, ds));
-            nbg_scalar_free(ctx, ds);
-        } else {
-            TRY(nbg_scalar_new(ctx, &c, NBG_FP64, tele));
-        }
-        nbg_vector y_blk, Y, m, e;
-        nbg_scalar d_loc;
-        TRY(nbg_ewise_mult(ctx, &y_blk, T, nbg_binop{NBG_TIMES, 0}, t, dinv_blk));
-        TRY(nbg_vector_allgather(ctx, &Y, y_blk, cuts));
-        nbg_vector_free(ctx, y_blk);
-        TRY(nbg_mxv(ctx, &m, T, nbg_semiring{NBG_PLUS, NBG_SECOND, 0.0}, AT_blk, Y));
-        nbg_vector_free(ctx, Y);
+    // exchange of y = t * dinv (+ the local partials of the given scalars) -> full x on every rank
+    auto exchange = [&](nbg_vector t, int ns, nbg_scalar *loc, nbg_vector *x, nbg_scalar *glob) -> nbg_status {
+        nbg_vector u;
+        TRY(nbg_ewise_mult(ctx, &u, T, nbg_binop{NBG_TIMES, 0}, t, dinv_blk));
+        nbg_status st = nbg_vector_allgather_reduce(ctx, x, u, cuts, ncols_g, ns, loc, glob);
+        nbg_vector_free(ctx, u);
+        for (int i = 0; i < ns; i++) nbg_scalar_free(ctx, loc[i]);
+        return st;
+    };
+    auto dangling_mass = [&](nbg_vector r, nbg_scalar *s) -> nbg_status {
+        nbg_vector tm;
+        TRY(nbg_ewise_mult(ctx, &tm, T, nbg_binop{NBG_TIMES, 0}, r, mask));
+        nbg_status st = nbg_reduce(ctx, s, NBG_FP64, NBG_PLUS, tm);
+        nbg_vector_free(ctx, tm);
+        return st;
+    };
+    // one sweep: t, x (gathered y), ds (global dangling mass of t) -> r, x', delta, ds'
+    auto sweep = [&](nbg_vector t, nbg_vector x, nbg_scalar ds, nbg_vector *r_new, nbg_vector *x_next, nbg_scalar *delta,
+                     nbg_scalar *ds_next) -> nbg_status {
+        nbg_scalar c;
+        if (uniform) TRY(nbg_scalar_apply(ctx, &c, NBG_FP64, nbg_unop{NBG_AXPB, a_n, tele}, ds));
+        else TRY(nbg_scalar_new(ctx, &c, NBG_FP64, tele));
+        nbg_vector m, e;
+        TRY(nbg_mxv(ctx, &m, T, nbg_semiring{NBG_PLUS, NBG_SECOND, 0.0}, AT_blk, x));
         TRY(nbg_apply_bind2nd(ctx, r_new, T, nbg_binop{NBG_PLUS, 0}, m, c));
         nbg_vector_free(ctx, m);
         nbg_scalar_free(ctx, c);
+        nbg_scalar loc[2];
         TRY(nbg_ewise_add(ctx, &e, T, nbg_binop{NBG_ABSDIFF, 0}, t, *r_new));
-        TRY(nbg_reduce(ctx, &d_loc, NBG_FP64, NBG_PLUS, e));
+        TRY(nbg_reduce(ctx, &loc[0], NBG_FP64, NBG_PLUS, e));
         nbg_vector_free(ctx, e);
-        TRY(nbg_scalar_wait(ctx, d_loc));
-        TRY(nbg_scalar_allreduce(ctx, delta, d_loc));
-        nbg_scalar_free(ctx, d_loc);
+        if (uniform) TRY(dangling_mass(*r_new, &loc[1]));
+        nbg_scalar glob[2] = {nullptr, nullptr};
+        TRY(exchange(*r_new, uniform ? 2 : 1, loc, x_next, glob));
+        *delta = glob[0];
+        *ds_next = glob[1];
         return NBG_SUCCESS;
     };
 
-    nbg_vector t;
-    TRY(nbg_vector_new_const(ctx, &t, T, nb, 1.0 / (double)n));
+    nbg_vector t, x;
+    nbg_scalar ds = nullptr;
+    TRY(nbg_vector_new_const(ctx, &t, T, nb, 1.0 / (double)n));      // Fig. 6 l.277
+    {
+        nbg_scalar loc[1];
+        if (uniform) TRY(dangling_mass(t, &loc[0]));
+        TRY(exchange(t, uniform ? 1 : 0, loc, &x, &ds));
+    }
     const bool conv = p->tol >= 0.0;
-    nbg_vector rk;
-    nbg_scalar dk;
-    TRY(sweep(t, &rk, &dk));
+    nbg_vector rk, xk;
+    nbg_scalar dk, dsk;
+    TRY(sweep(t, x, ds, &rk, &xk, &dk, &dsk));
+    nbg_vector_free(ctx, x);
+    if (ds) nbg_scalar_free(ctx, ds);
     std::vector<nbg_scalar> deltas;
     int k = 1;
     for (;;) {
-        nbg_vector rnext = nullptr;
-        nbg_scalar dnext = nullptr;
+        nbg_vector rnext = nullptr, xnext = nullptr;
+        nbg_scalar dnext = nullptr, dsnext = nullptr;
         const bool more = k < p->itermax;
-        if (more) TRY(sweep(rk, &rnext, &dnext));
+        if (more) TRY(sweep(rk, xk, dsk, &rnext, &xnext, &dnext, &dsnext));   // launched before delta_k is read
         bool stop = !more;
         if (conv) {
             double v = 0.0;
@@ -260,20 +276,26 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
             if (delta_hist) delta_hist[k - 1] = v;
             nbg_scalar_free(ctx, dk);
             dk = nullptr;
-            if (!(v > p->tol)) stop = true;   // identical on every rank: the allreduce is exact
+            if (!(v > p->tol)) stop = true;   // identical on every rank: the sum is exact
         } else {
             deltas.push_back(dk);
             dk = nullptr;
         }
+        nbg_vector_free(ctx, xk);
+        if (dsk) nbg_scalar_free(ctx, dsk);
         if (stop) {
             if (rnext) nbg_vector_free(ctx, rnext);
+            if (xnext) nbg_vector_free(ctx, xnext);
             if (dnext) nbg_scalar_free(ctx, dnext);
+            if (dsnext) nbg_scalar_free(ctx, dsnext);
             break;
         }
         nbg_vector_free(ctx, t);
         t = rk;
         rk = rnext;
+        xk = xnext;
         dk = dnext;
+        dsk = dsnext;
         k++;
     }
     for (size_t j = 0; j < deltas.size(); j++) {
@@ -283,8 +305,8 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
         nbg_scalar_free(ctx, deltas[j]);
     }
     nbg_vector_free(ctx, t);
+    if (mask) nbg_vector_free(ctx, mask);
     nbg_vector_free(ctx, dinv_blk);
-    nbg_vector_free(ctx, dinv);
     *r_out = rk;
     if (sweeps_out) *sweeps_out = k;
     return NBG_SUCCESS;

@@ -509,7 +509,9 @@ struct Builder {
         int i = emit(x);
         if (i < 0) return false;
         OutV ov{i, (int)out_nodes.size()};
-        ov.scatter = (bool)scatter;
+        // scattered store out[map[i]]: into a consumer's gather layout, or into a caller's target
+        // (multi-GPU exchange buffer, Ctx::out_targets; map < 0 skips the row)
+        ov.scatter = (bool)scatter || c.out_targets.count(x.get()) > 0;
         prog.outs.push_back(ov);
         out_nodes.push_back(x);
         out_scatter.push_back(scatter);
@@ -577,9 +579,17 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     for (int k = 0; k < p.n_out; k++) {
         const NodeP &x = B.out_nodes[k];
         const MatP &sc = B.out_scatter[k];
-        int64_t len = sc ? sc->plan->ncols_g : n;
-        BufP b = alloc_buf(c, (size_t)len * type_size(x->type));
-        if (sc) args.oscat[k] = (const int *)sc->plan->perm->d;
+        auto tg = c.out_targets.find(x.get());
+        BufP b;
+        if (tg != c.out_targets.end()) {
+            // caller-provided destination (multi-GPU exchange buffer): out[map[i]], map < 0 skips
+            b = tg->second.buf;
+            args.oscat[k] = tg->second.map;
+        } else {
+            int64_t len = sc ? sc->plan->ncols_g : n;
+            b = alloc_buf(c, (size_t)len * type_size(x->type));
+            if (sc) args.oscat[k] = (const int *)sc->plan->perm->d;
+        }
         obufs.push_back(b);
         args.out[k] = b->d;
         c.stats.vectors_materialized++;
@@ -730,6 +740,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     // (set by the caller through B.prog before hints were appended)
     for (int k = 0; k < p.n_out; k++) {
         Node &x = *B.out_nodes[k];
+        if (c.out_targets.count(&x)) continue;   // written into a target only: the node stays pending
         x.buf = obufs[k];
         x.kind = VKind::FULL;
         x.mat = true;
@@ -835,6 +846,7 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
         run_region(c, B, hint_outs, n);
         const uint64_t seq = ++c.launch_seq;
         for (int k = 0; k < nbase; k++) {
+            if (!B.out_nodes[k]->buf) continue;   // written into a caller's target only (stays pending)
             B.out_nodes[k]->buf->prod_sig = base_hash;
             B.out_nodes[k]->buf->prod_out = k;
             B.out_nodes[k]->buf->prod_seq = seq;
@@ -842,7 +854,8 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
         if (nb) {
             PTimer pt_m(6);
             // memoise every result (common subexpressions across waits, e.g. dinv across runs)
-            for (int k = 0; k < nbase; k++) memo_insert(c, base_keys[k], B.out_nodes[k]);
+            for (int k = 0; k < nbase; k++)
+                if (!c.out_targets.count(B.out_nodes[k].get())) memo_insert(c, base_keys[k], B.out_nodes[k]);
             // side outputs are keyed with R already materialised (the next sweep's lookup key)
             for (HintOut &h : hint_outs) {
                 Node tmp = *h.node;
@@ -858,7 +871,8 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
         for (const NodeP &x : B.visited)
             if (B.is_out.count(x.get())) stored++;
         c.stats.intermediates_elided += (nvis >= stored) ? (nvis - std::min(stored, nvis)) : 0;
-        for (const NodeP &x : B.out_nodes) drop_inputs(*x);
+        for (const NodeP &x : B.out_nodes)
+            if (!c.out_targets.count(x.get())) drop_inputs(*x);
         for (const NodeP &x : B.red_nodes) drop_inputs(*x);
         c.stats.waits++;
         return;

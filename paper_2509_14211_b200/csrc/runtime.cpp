@@ -145,11 +145,11 @@ void issue_readback(Ctx &c, Slot &s) {
 static double xacc_window(const unsigned long long *L);
 
 double xacc_to_double(const unsigned long long *L) {
-    unsigned long long flags = L[10];
-    if (flags & 9ull) return NAN;
-    if ((flags & 6ull) == 6ull) return NAN;
-    if (flags & 2ull) return INFINITY;
-    if (flags & 4ull) return -INFINITY;
+    const unsigned long long flags = L[10];   // counts: NaN bits 0-20, +inf 21-41, -inf 42-62 (prelude.cuh)
+    const unsigned long long nan = flags & 0x1FFFFFull, pinf = (flags >> 21) & 0x1FFFFFull, ninf = (flags >> 42) & 0x1FFFFFull;
+    if (nan || (pinf && ninf)) return NAN;
+    if (pinf) return INFINITY;
+    if (ninf) return -INFINITY;
     double extra;                       // fp64 sum of the terms outside the exact window
     memcpy(&extra, &L[12], 8);
     return xacc_window(L) + extra;
@@ -207,8 +207,8 @@ void host_xacc_add(unsigned long long *acc, double d) {
     long long bits;
     memcpy(&bits, &d, 8);
     int e = (int)((bits >> 52) & 0x7ff);
-    if (e == 0x7ff) {
-        acc[10] |= ((bits & 0xFFFFFFFFFFFFFll) != 0) ? 1ull : (bits < 0 ? 4ull : 2ull);
+    if (e == 0x7ff) {   // counted like the device's nbg_xacc_add (one per term)
+        acc[10] += ((bits & 0xFFFFFFFFFFFFFll) != 0) ? 1ull : (bits < 0 ? (1ull << 42) : (1ull << 21));
         return;
     }
     unsigned long long m = (unsigned long long)bits & 0xFFFFFFFFFFFFFull;
@@ -403,6 +403,11 @@ Kernel::~Kernel() {
 
 Ctx::~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
+    // every member that holds device buffers is released here, while the stream and the pool
+    // still exist (members are destroyed only after this body, i.e. after the stream)
+    out_targets.clear();
+    dist_maps.reset();
+    user_nodes.clear();
     memo.clear();
     hints.clear();
     plans.clear();

@@ -144,7 +144,14 @@ SIGNATURES = {
     "nbg_dist_init": [vp, ctypes.c_int, ctypes.c_int, vp],
     "nbg_vector_allgather": [vp, pvp, vp, vp],
     "nbg_scalar_allreduce": [vp, pvp, vp],
-    "nbg_pagerank_dist": [vp, vp, vp, vp, ctypes.POINTER(nbg_pr_params), pvp, ctypes.POINTER(ctypes.c_int), vp],
+    "nbg_pagerank_dist": [vp, vp, vp, vp, i64, ctypes.POINTER(nbg_pr_params), pvp, ctypes.POINTER(ctypes.c_int), vp],
+    "nbg_xacc_encode": [vp, i64, vp],
+    "nbg_xacc_decode": [vp, vp],
+    "nbg_scalar_export_slot": [vp, vp, vp],
+    "nbg_dist_exchange_plan": [vp, ctypes.c_int, i64, vp, vp],
+    "nbg_dist_init_loopback": [vp, ctypes.c_int],
+    "nbg_dist_graph_from_generator": [vp, ctypes.POINTER(nbg_graphgen), i64, pvp, pvp, vp, vp],
+    "nbg_vector_allgather_reduce": [vp, pvp, vp, vp, i64, ctypes.c_int, vp, vp],
 }
 for _n, _a in SIGNATURES.items():
     _f = getattr(lib, _n)
@@ -523,15 +530,73 @@ def nbg_scalar_allreduce(ctx, s):
     return w
 
 
-def nbg_pagerank_dist(ctx, AT_blk, deg, cuts, alpha=0.85, tol=-1.0, itermax=20, dangling=PR_UNIFORM, type=FP32):
+def nbg_pagerank_dist(ctx, AT_blk, deg_blk, cuts, ncols_g, alpha=0.85, tol=-1.0, itermax=20, dangling=PR_UNIFORM,
+                      type=FP32):
     cuts = np.ascontiguousarray(cuts, np.int64)
     p = nbg_pr_params(alpha, tol, itermax, dangling, type)
     r = _out()
     sw = ctypes.c_int()
     hist = np.zeros(max(itermax, 1), np.float64)
-    _call(ctx, "nbg_pagerank_dist", ctx, AT_blk, deg, cuts.ctypes.data, ctypes.byref(p), ctypes.byref(r),
-          ctypes.byref(sw), hist.ctypes.data)
+    _call(ctx, "nbg_pagerank_dist", ctx, AT_blk, deg_blk, cuts.ctypes.data, int(ncols_g), ctypes.byref(p),
+          ctypes.byref(r), ctypes.byref(sw), hist.ctypes.data)
     return r, sw.value, hist[:sw.value].copy()
+
+
+def nbg_xacc_encode(terms):
+    """Host only: the 16-word exact-accumulator slot of a list of float64 terms."""
+    t = np.ascontiguousarray(terms, np.float64)
+    slot = np.zeros(16, np.uint64)
+    _call(None, "nbg_xacc_encode", t.ctypes.data if t.size else None, int(t.shape[0]), slot.ctypes.data)
+    return slot
+
+
+def nbg_xacc_decode(slot):
+    slot = np.ascontiguousarray(slot, np.uint64)
+    v = ctypes.c_double()
+    _call(None, "nbg_xacc_decode", slot.ctypes.data, ctypes.byref(v))
+    return v.value
+
+
+def nbg_scalar_export_slot(ctx, s):
+    slot = np.zeros(16, np.uint64)
+    _call(ctx, "nbg_scalar_export_slot", ctx, s, slot.ctypes.data)
+    return slot
+
+
+def nbg_dist_init_loopback(ctxs):
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.value if isinstance(c, ctypes.c_void_p) else c for c in ctxs])
+    _call(None, "nbg_dist_init_loopback", ctypes.cast(arr, ctypes.c_void_p), len(ctxs))
+
+
+def nbg_dist_exchange_plan(cuts, ncols_g):
+    cuts = np.ascontiguousarray(cuts, np.int64)
+    P = cuts.shape[0] - 1
+    off = np.zeros(P, np.int64)
+    cnt = np.zeros(P, np.int64)
+    _call(None, "nbg_dist_exchange_plan", cuts.ctypes.data, P, int(ncols_g), off.ctypes.data, cnt.ctypes.data)
+    return off, cnt
+
+
+def nbg_dist_graph_from_generator(ctx, kind, scale, edge_factor, seed, nranks=1, bytes_per_row=20):
+    g = nbg_graphgen(kind, scale, edge_factor, seed)
+    A = _out()
+    d = _out()
+    cuts = np.zeros(nranks + 1, np.int64)
+    ncg = ctypes.c_int64()
+    _call(ctx, "nbg_dist_graph_from_generator", ctx, ctypes.byref(g), int(bytes_per_row), ctypes.byref(A),
+          ctypes.byref(d), cuts.ctypes.data, ctypes.byref(ncg))
+    return A, d, cuts, ncg.value
+
+
+def nbg_vector_allgather_reduce(ctx, u_blk, cuts, ncols_g, scalars=()):
+    cuts = np.ascontiguousarray(cuts, np.int64)
+    w = _out()
+    k = len(scalars)
+    sin = (ctypes.c_void_p * max(k, 1))(*scalars)
+    sout = (ctypes.c_void_p * max(k, 1))()
+    _call(ctx, "nbg_vector_allgather_reduce", ctx, ctypes.byref(w), u_blk, cuts.ctypes.data, int(ncols_g), k,
+          ctypes.cast(sin, ctypes.c_void_p), ctypes.cast(sout, ctypes.c_void_p))
+    return w, [ctypes.c_void_p(sout[i]) for i in range(k)]
 
 
 def jit_selftest():
