@@ -123,6 +123,25 @@ typedef enum {
 
 typedef struct { int code; double c0; } nbg_binop;
 
+/* User-defined operators (the paper splices the user's function into the
+ * generated loop, Fig. 2, specialising on "the concrete operations").
+ * `expr` is a CUDA C++ expression over the operand `x` (binary: `x` and `y`) and the descriptor's
+ * constants `c0`, `c1` (binary: `c0`); the prelude's helpers nbg_abs / nbg_min / nbg_max / nbg_div
+ * and CUDA math functions may be used.  Like the built-in operators it is evaluated in the
+ * operation's compute type (inputs and constants converted first; bool outputs store x != 0),
+ * IEEE round to nearest, no FMA contraction.  The expression is compiled by NVRTC (no GPU needed)
+ * for float, double, int and long long at definition time: NBG_INVALID_VALUE if it does not compile
+ * or contains ';' / unbalanced brackets (the log goes to stderr).  *code (>= NBG_USER_OP_BASE) is
+ * valid for the whole process in nbg_unop / nbg_binop descriptors of every context: apply, bind2nd,
+ * ewise_mult, ewise_add, and as the multiply of a semiring (nbg_mxv); not in nbg_scalar_apply
+ * (scalar ops are host-evaluated: NBG_NOT_IMPLEMENTED).  Operations over iso operands are not
+ * folded on the host for user operators (they run in the generated kernel).  The expression text
+ * is part of every generated kernel's source, hence of the persistent cubin cache key
+ * (NBG_JIT_CACHE). */
+enum { NBG_USER_OP_BASE = 1000 };
+nbg_status nbg_unop_define(const char *name, const char *expr, int *code);
+nbg_status nbg_binop_define(const char *name, const char *expr, int *code);
+
 /* Monoids (add of a semiring, reduce): NBG_PLUS (identity 0), NBG_MIN (+inf / INT_MAX),
  * NBG_MAX (-inf / INT_MIN).  Floating PLUS folds accumulate in fp64. */
 typedef struct {
@@ -163,6 +182,7 @@ typedef struct {
     double jit_ms;                  /* host time spent in NVRTC                               */
     uint64_t structured_regions;    /* regions over sparse / bitset vectors (NEXT-3)          */
     uint64_t structured_index_loops;/* ... of those, run over a sparse index list (estimator)  */
+    uint64_t jit_disk_hits;         /* kernels loaded from the persistent cubin cache (NBG_JIT_CACHE) */
 } nbg_stats;
 
 nbg_status nbg_get_stats(nbg_ctx *ctx, nbg_stats *out);

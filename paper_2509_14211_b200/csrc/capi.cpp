@@ -60,8 +60,23 @@ static void check_mat(nbg_ctx *ctx, nbg_matrix A) {
     CHECK(A->ctx == ctx, NBG_INVALID_OBJECT, "matrix belongs to another context");
 }
 static void check_type(int t) { CHECK(valid_type(t), NBG_INVALID_VALUE, "invalid nbg_type"); }
-static void check_unop(const nbg_unop &op) { CHECK(op.code >= NBG_IDENTITY && op.code <= NBG_ISZERO, NBG_INVALID_VALUE, "invalid unop code"); }
-static void check_binop(const nbg_binop &op) { CHECK(op.code >= NBG_PLUS && op.code <= NBG_MAX_DIVX_C, NBG_INVALID_VALUE, "invalid binop code"); }
+static bool is_user(int code) { return code >= NBG_USER_OP_BASE; }
+static void check_unop(const nbg_unop &op) {
+    if (is_user(op.code)) {
+        const UserOp *u = user_op(op.code);
+        CHECK(u && u->arity == 1, NBG_INVALID_VALUE, "invalid unop code (not a defined unary operator)");
+        return;
+    }
+    CHECK(op.code >= NBG_IDENTITY && op.code <= NBG_ISZERO, NBG_INVALID_VALUE, "invalid unop code");
+}
+static void check_binop(const nbg_binop &op) {
+    if (is_user(op.code)) {
+        const UserOp *u = user_op(op.code);
+        CHECK(u && u->arity == 2, NBG_INVALID_VALUE, "invalid binop code (not a defined binary operator)");
+        return;
+    }
+    CHECK(op.code >= NBG_PLUS && op.code <= NBG_MAX_DIVX_C, NBG_INVALID_VALUE, "invalid binop code");
+}
 static void check_monoid(int m) { CHECK(m == NBG_PLUS || m == NBG_MIN || m == NBG_MAX, NBG_INVALID_VALUE, "invalid monoid"); }
 
 static NodeP mk(Ctx &c, Op op, int type, int64_t n, bool scalar) {
@@ -101,7 +116,7 @@ static bool is_host_scalar(const NodeP &x) { return x->mat && x->scalar && x->sf
 
 static NodeP rec_apply(Ctx &c, int type, const nbg_unop &op, const NodeP &u) {
     if (is_empty(u)) return leaf_empty(c, type, u->n);
-    if (is_iso(u)) return leaf_iso(c, type, u->n, host_unop(op.code, type, u->iso, op.c0, op.c1));
+    if (is_iso(u) && !is_user(op.code)) return leaf_iso(c, type, u->n, host_unop(op.code, type, u->iso, op.c0, op.c1));
     NodeP x = mk(c, Op::APPLY, type, u->n, false);
     x->code = op.code;
     x->c0 = op.c0;
@@ -119,7 +134,7 @@ static NodeP rec_binary(Ctx &c, Op op, int type, const nbg_binop &bo, const Node
         if (is_empty(u)) return rec_apply(c, type, id, v);
         if (is_empty(v)) return rec_apply(c, type, id, u);
     }
-    if (is_iso(u) && is_iso(v)) return leaf_iso(c, type, u->n, host_binop(bo.code, type, u->iso, v->iso, bo.c0));
+    if (is_iso(u) && is_iso(v) && !is_user(bo.code)) return leaf_iso(c, type, u->n, host_binop(bo.code, type, u->iso, v->iso, bo.c0));
     NodeP x = mk(c, op, type, u->n, false);
     x->code = bo.code;
     x->c0 = bo.c0;
@@ -130,7 +145,8 @@ static NodeP rec_binary(Ctx &c, Op op, int type, const nbg_binop &bo, const Node
 
 static NodeP rec_bind2nd(Ctx &c, int type, const nbg_binop &bo, const NodeP &u, const NodeP &s) {
     if (is_empty(u)) return leaf_empty(c, type, u->n);
-    if (is_iso(u) && is_host_scalar(s)) return leaf_iso(c, type, u->n, host_binop(bo.code, type, u->iso, s->hval, bo.c0));
+    if (is_iso(u) && is_host_scalar(s) && !is_user(bo.code))
+        return leaf_iso(c, type, u->n, host_binop(bo.code, type, u->iso, s->hval, bo.c0));
     NodeP x = mk(c, Op::BIND2ND, type, u->n, false);
     x->code = bo.code;
     x->c0 = bo.c0;
@@ -963,6 +979,9 @@ nbg_status nbg_scalar_apply(nbg_ctx *ctx, nbg_scalar *out, int type, nbg_unop op
     check_scal(ctx, s);
     check_type(type);
     check_unop(op);
+    // scalar ops are evaluated on the host where they are read: a user operator (device source) is
+    // only usable on vectors and in semirings
+    CHECK(!is_user(op.code), NBG_NOT_IMPLEMENTED, "user-defined operators apply to vectors, not host-evaluated scalars");
     NodeP x = rec_sapply(*ctx, type, op, s->node);
     blocking_finish(ctx, x);
     *out = new_shandle(ctx, x);

@@ -140,7 +140,12 @@ struct Gen {
                         r = "((" + x + " != (" + C + ")0) ? nbg_div(" + k0() + ", " + x + ") : (" + C + ")0)";
                         break;
                     case NBG_ISZERO: r = "((" + x + " == (" + C + ")0) ? (" + C + ")1 : (" + C + ")0)"; break;
-                    default: fail(NBG_INVALID_VALUE, "codegen: unop code");
+                    default: {
+                        const UserOp *u = user_op(in.code);
+                        if (!u || u->arity != 1) fail(NBG_INVALID_VALUE, "codegen: unop code");
+                        r = user_op_call(*u, C, x, "", "a.imm[" + std::to_string(in.imm0) + "]",
+                                         "a.imm[" + std::to_string(in.imm1) + "]");
+                    }
                 }
                 break;
             }
@@ -157,7 +162,11 @@ struct Gen {
                     case NBG_SECOND: r = y; break;
                     case NBG_ABSDIFF: r = "nbg_abs(" + x + " - " + y + ")"; break;
                     case NBG_MAX_DIVX_C: r = "nbg_max(nbg_div(" + x + ", " + k0() + "), " + y + ")"; break;
-                    default: fail(NBG_INVALID_VALUE, "codegen: binop code");
+                    default: {
+                        const UserOp *u = user_op(in.code);
+                        if (!u || u->arity != 2) fail(NBG_INVALID_VALUE, "codegen: binop code");
+                        r = user_op_call(*u, C, x, y, in.imm0 >= 0 ? "a.imm[" + std::to_string(in.imm0) + "]" : "0", "0");
+                    }
                 }
                 break;
             }
@@ -544,7 +553,11 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
         case NBG_SECOND: mul = xv; break;
         case NBG_ABSDIFF: mul = "nbg_abs(" + av + " - " + xv + ")"; break;
         case NBG_MAX_DIVX_C: mul = "nbg_max(nbg_div(" + av + ", ((" + std::string(C) + ")(a.imm[1]))), " + xv + ")"; break;
-        default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
+        default: {
+            const UserOp *u = user_op(sp.mul);
+            if (!u || u->arity != 2) fail(NBG_INVALID_VALUE, "codegen: semiring mul");
+            mul = user_op_call(*u, C, av, xv, "a.imm[1]", "0");
+        }
     }
     std::vector<int> fplus;
     for (size_t j = 0; j < p.reds.size(); j++)
@@ -887,7 +900,11 @@ SemiringCode semiring_code(const SpmvSig &sp) {
         case NBG_SECOND: r.mul = xv; break;
         case NBG_ABSDIFF: r.mul = "nbg_abs(" + av + " - " + xv + ")"; break;
         case NBG_MAX_DIVX_C: r.mul = "nbg_max(nbg_div(" + av + ", ((" + C + ")(a.imm[1]))), " + xv + ")"; break;
-        default: fail(NBG_INVALID_VALUE, "codegen: semiring mul");
+        default: {
+            const UserOp *u = user_op(sp.mul);
+            if (!u || u->arity != 2) fail(NBG_INVALID_VALUE, "codegen: semiring mul");
+            r.mul = user_op_call(*u, C, av, xv, "a.imm[1]", "0");
+        }
     }
     return r;
 }

@@ -51,7 +51,10 @@ static std::string nvrtc_compile(Ctx &c, const std::string &src, const std::stri
     snprintf(hbuf, sizeof hbuf, "%016llx", (unsigned long long)hash_str(src + "|sm_100a|v1"));
     std::string cpath = dir.empty() ? "" : dir + "/" + kname + "_" + hbuf + ".cubin";
     std::string cubin;
-    if (!cpath.empty() && read_file(cpath, cubin)) return cubin;
+    if (!cpath.empty() && read_file(cpath, cubin)) {
+        c.stats.jit_disk_hits++;
+        return cubin;
+    }
 
     double t0 = now_ns();
     nvrtcProgram prog;

@@ -407,6 +407,13 @@ void timing_begin(Ctx &c, const char *cls, cudaEvent_t *ev0);
 void timing_end(Ctx &c, const char *cls, cudaEvent_t ev0);
 void timing_collect(Ctx &c);
 
+// user-defined operators (userops.cpp)
+struct UserOp { int arity = 1; std::string name, expr; };
+const UserOp *user_op(int code);   // null unless `code` is a registered user operator
+int user_op_define(int arity, const std::string &name, const std::string &expr, std::string *err);
+std::string user_op_call(const UserOp &op, const std::string &C, const std::string &x, const std::string &y,
+                         const std::string &k0, const std::string &k1);
+
 // planner entry points
 void materialize(Ctx &c, const std::vector<NodeP> &roots);
 double scalar_read(Ctx &c, const NodeP &s);

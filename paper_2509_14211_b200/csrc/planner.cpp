@@ -381,7 +381,8 @@ struct Builder {
     }
 
     static bool unop_has_c0(int code) {
-        return code == NBG_ADD_C || code == NBG_MUL_C || code == NBG_AXPB || code == NBG_ABS_SUB_C || code == NBG_RECIP_SCALED;
+        return code == NBG_ADD_C || code == NBG_MUL_C || code == NBG_AXPB || code == NBG_ABS_SUB_C || code == NBG_RECIP_SCALED ||
+               code >= NBG_USER_OP_BASE;
     }
 
     int emit(const NodeP &x) {
@@ -440,7 +441,7 @@ struct Builder {
                     in.code = x->code;
                     in.a = a;
                     if (unop_has_c0(x->code)) in.imm0 = imm_slot(x->c0);
-                    if (x->code == NBG_AXPB) in.imm1 = imm_slot(x->c1);
+                    if (x->code == NBG_AXPB || x->code >= NBG_USER_OP_BASE) in.imm1 = imm_slot(x->c1);
                     in.uniform = prog.ins[a].uniform;
                     r = add(in);
                     break;
@@ -457,7 +458,7 @@ struct Builder {
                     in.code = x->code;
                     in.a = a;
                     in.b = b;
-                    if (x->code == NBG_MAX_DIVX_C) in.imm0 = imm_slot(x->c0);
+                    if (x->code == NBG_MAX_DIVX_C || x->code >= NBG_USER_OP_BASE) in.imm0 = imm_slot(x->c0);
                     in.uniform = prog.ins[a].uniform && prog.ins[b].uniform;
                     r = add(in);
                     break;

@@ -232,9 +232,9 @@ struct SBuilder {
                     in.code = x->code;
                     in.a = a;
                     if (x->code == NBG_ADD_C || x->code == NBG_MUL_C || x->code == NBG_AXPB || x->code == NBG_ABS_SUB_C ||
-                        x->code == NBG_RECIP_SCALED)
+                        x->code == NBG_RECIP_SCALED || x->code >= NBG_USER_OP_BASE)
                         in.imm0 = imm_slot(x->c0);
-                    if (x->code == NBG_AXPB) in.imm1 = imm_slot(x->c1);
+                    if (x->code == NBG_AXPB || x->code >= NBG_USER_OP_BASE) in.imm1 = imm_slot(x->c1);
                     in.uniform = sp.p.ins[a].uniform;
                     r = add(in, 0);
                     break;
@@ -247,7 +247,7 @@ struct SBuilder {
                     in.code = x->code;
                     in.a = a;
                     in.b = b;
-                    if (x->code == NBG_MAX_DIVX_C) in.imm0 = imm_slot(x->c0);
+                    if (x->code == NBG_MAX_DIVX_C || x->code >= NBG_USER_OP_BASE) in.imm0 = imm_slot(x->c0);
                     in.uniform = sp.p.ins[a].uniform && sp.p.ins[b].uniform;
                     r = add(in, x->op == Op::EMULT ? 1 : (x->op == Op::EADD ? 2 : 0));
                     break;

@@ -82,7 +82,8 @@ class nbg_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("waits", "plans_built", "plan_hits", "jit_compiles", "kernels_launched",
                                                 "vectors_materialized", "intermediates_elided", "memo_hits",
                                                 "side_outputs", "bytes_materialized", "host_plan_ns")] + \
-               [("jit_ms", ctypes.c_double), ("structured_regions", ctypes.c_uint64), ("structured_index_loops", ctypes.c_uint64)]
+               [("jit_ms", ctypes.c_double), ("structured_regions", ctypes.c_uint64), ("structured_index_loops", ctypes.c_uint64),
+                ("jit_disk_hits", ctypes.c_uint64)]
 
 
 vp = ctypes.c_void_p
@@ -95,6 +96,8 @@ SIGNATURES = {
     "nbg_finalize": [vp],
     "nbg_last_error": [vp, ctypes.c_char_p, ctypes.c_size_t],
     "nbg_sync": [vp],
+    "nbg_unop_define": [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)],
+    "nbg_binop_define": [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int)],
     "nbg_get_stats": [vp, ctypes.POINTER(nbg_stats)],
     "nbg_reset_stats": [vp],
     "nbg_set_timing": [vp, ctypes.c_int],
@@ -205,6 +208,20 @@ def nbg_finalize(ctx):
 
 def nbg_sync(ctx):
     _call(ctx, "nbg_sync", ctx)
+
+
+def nbg_unop_define(name, expr):
+    """Register a user unary operator (CUDA expression over x, c0, c1) -> its code."""
+    code = ctypes.c_int()
+    _call(None, "nbg_unop_define", name.encode(), expr.encode(), ctypes.byref(code))
+    return code.value
+
+
+def nbg_binop_define(name, expr):
+    """Register a user binary operator (CUDA expression over x, y, c0) -> its code."""
+    code = ctypes.c_int()
+    _call(None, "nbg_binop_define", name.encode(), expr.encode(), ctypes.byref(code))
+    return code.value
 
 
 def nbg_get_stats(ctx):
