@@ -177,12 +177,36 @@ struct Gen {
 
     // --- reductions
     struct RedKind { std::string acct, ident, comb; int kind; };
+    // index of a float PLUS reduction over fp64 terms among the region's exact reductions (-1: none)
+    int xidx(const RedOut &r) const {
+        int k = 0;
+        for (const RedOut &q : p.reds) {
+            if (&q == &r) return exact_red(q) ? k : -1;
+            if (exact_red(q)) k++;
+        }
+        return -1;
+    }
+    int n_exact() const {
+        int k = 0;
+        for (const RedOut &q : p.reds) k += exact_red(q) ? 1 : 0;
+        return k;
+    }
+    // PLUS over fp64 TERMS (the value before the conversion to the reduce type): summed exactly per
+    // thread (prelude nbg_xt), so the value does not depend on the grouping (DESIGN.md §4 P9).  fp32
+    // terms keep the fp64 running sum (exact for the value ranges of the hot path).
+    bool exact_red(const RedOut &r) const {
+        if (r.monoid != NBG_PLUS || !is_float(p.ins[r.ins].t)) return false;
+        const Ins &in = p.ins[r.ins];
+        const int src = (in.k == Ins::CVT && in.a >= 0) ? p.ins[in.a].t : in.t;
+        return src == NBG_FP64;
+    }
     RedKind redkind(const RedOut &r) const {
         int t = p.ins[r.ins].t;
         bool f = is_float(t);
         // monoid evaluated on the term converted to the reduce output type (already done by the
         // planner with a CVT instruction), accumulated in fp64 (floats) or int64 (ints)
         if (r.monoid == NBG_PLUS) {
+            if (f && exact_red(r)) return {"nbg_xt", "nbg_xt_zero()", "xt", 6};
             if (f) return {"double", "0.0", "+", 0};
             return {"long long", "0ll", "+", 1};
         }
@@ -195,6 +219,7 @@ struct Gen {
     }
     std::string red_update(const RedOut &r, const std::string &acc, const std::string &val) const {
         RedKind k = redkind(r);
+        if (k.kind == 6) return "nbg_xt_add(" + acc + ", (double)(" + val + "), &nbg_xl[" + std::to_string(xidx(r)) + "][0]);";
         std::string x = "((" + k.acct + ")(" + val + "))";
         if (k.comb == "+") return acc + " += " + x + ";";
         if (k.comb == "max") return acc + " = nbg_max(" + acc + ", " + x + ");";
@@ -204,9 +229,10 @@ struct Gen {
     std::string red_direct(const RedOut &r, const std::string &val) const {
         RedKind k = redkind(r);
         std::string acc = "a.racc[" + std::to_string(r.racc) + "]";
-        std::string x = "((" + k.acct + ")(" + val + "))";
+        std::string x = "((" + (k.kind == 6 ? std::string("double") : k.acct) + ")(" + val + "))";
         switch (k.kind) {
-            case 0: return "nbg_xacc_add(" + acc + ", " + x + ");";
+            case 0:
+            case 6: return "nbg_xacc_add(" + acc + ", " + x + ");";
             case 1: return "atomicAdd(&" + acc + "[11], (u64)" + x + ");";
             case 2: return "atomicMax(&" + acc + "[11], nbg_fkey(" + x + "));";
             case 3: return "atomicMax(&" + acc + "[11], ~nbg_fkey(" + x + "));";
@@ -248,15 +274,27 @@ struct Gen {
             o << ind << "const " << ctype(in.t) << " " << v((int)i) << " = *(const " << ctype(in.t) << "*)&" << arr << "[" << k++ << "];\n";
         }
     }
+    // every thread must reach this (top level of the kernel): it may contain a __syncthreads
     void emit_red_decl() {
+        const int nx = n_exact();
+        if (nx) {
+            o << "  __shared__ u64 nbg_xl[" << nx << "][16];\n";
+            o << "  for (int k_ = threadIdx.x; k_ < " << 16 * nx << "; k_ += blockDim.x) (&nbg_xl[0][0])[k_] = 0ull;\n";
+            o << "  __syncthreads();\n";
+        }
         for (size_t j = 0; j < p.reds.size(); j++) {
             RedKind k = redkind(p.reds[j]);
             o << "  " << k.acct << " r" << j << " = " << k.ident << ";\n";
         }
     }
+    std::string red_finish_xt(size_t j) const {
+        return "  nbg_block_finish_xt(r" + std::to_string(j) + ", &nbg_xl[" + std::to_string(xidx(p.reds[j])) + "][0], a.racc[" +
+               std::to_string(p.reds[j].racc) + "]);\n";
+    }
     void emit_red_finish() {
         for (size_t j = 0; j < p.reds.size(); j++) {
             RedKind k = redkind(p.reds[j]);
+            if (k.kind == 6) { o << red_finish_xt(j); continue; }
             if (k.acct == "double")
                 o << "  nbg_block_finish_f(r" << j << ", " << k.kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
             else
@@ -363,7 +401,9 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     for (const OutV &ov : p.outs)
         if (!ov.scatter) out_type[ov.out] = p.ins[ov.ins].t;
 
-    o << "extern \"C\" __global__ void __launch_bounds__(256) " << kname << "(const KArgs a) {\n";
+    // an exact reduction (nbg_xt) raises register use: keep 6 blocks of 256 threads resident so the
+    // grid-stride loads keep enough bytes in flight
+    o << "extern \"C\" __global__ void __launch_bounds__(256" << (g.n_exact() ? ", 6" : "") << ") " << kname << "(const KArgs a) {\n";
     o << "  __shared__ double nbg_sh[32];\n";
     g.emit_uniform();
     g.emit_red_decl();
@@ -851,6 +891,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
     for (size_t j = 0; j < p.reds.size(); j++) {
         if (std::find(fplus.begin(), fplus.end(), (int)j) != fplus.end()) continue;
         int kind = redkind(g, p.reds[j]);
+        if (kind == 6) { o << g.red_finish_xt(j); continue; }
         if (kind == 0 || kind == 2 || kind == 3)
             o << "  nbg_block_finish_f(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
         else
@@ -1189,6 +1230,7 @@ int gen_tp2(Gen &g, const std::string &kname) {
     for (size_t j = 0; j < p.reds.size(); j++) {
         if (std::find(fplus.begin(), fplus.end(), (int)j) != fplus.end()) continue;
         int kind = redkind(g, p.reds[j]);
+        if (kind == 6) { o << g.red_finish_xt(j); continue; }
         if (kind == 0 || kind == 2 || kind == 3)
             o << "  nbg_block_finish_f(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
         else

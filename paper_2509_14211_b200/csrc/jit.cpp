@@ -61,7 +61,7 @@ static std::string nvrtc_compile(Ctx &c, const std::string &src, const std::stri
     if (nvrtcCreateProgram(&prog, src.c_str(), (kname + ".cu").c_str(), 0, nullptr, nullptr) != NVRTC_SUCCESS)
         fail(NBG_PANIC, "nvrtcCreateProgram failed");
     const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--prec-div=true", "--prec-sqrt=true",
-                          "--ftz=false", "-std=c++17", "--generate-line-info", "-default-device"};
+                          "--ftz=false", "-std=c++17", "--generate-line-info", "-default-device", "--device-int128"};
     nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof opts / sizeof opts[0]), opts);
     if (r != NVRTC_SUCCESS) {
         size_t ls = 0;

@@ -216,6 +216,129 @@ __device__ long long nbg_sval_i(const u64 *s, int fmt) {
     return (long long)nbg_sval(s, fmt);
 }
 
+// ------------------------------------------------------------------ per-thread exact accumulator
+// For PLUS reductions of fp64 terms (DESIGN.md §4 "P9"): a thread accumulates its terms EXACTLY in
+// a 128-bit two's-complement fixed-point integer V (value V * 2^L).  The anchor L is a multiple of
+// 32 chosen from the exponent of the thread's first term (its LSB lands 8..39 bits above L); a
+// term whose LSB lies more than 44 bits above L flushes V (exactly) into the block's limbs and
+// re-anchors; a term below the window goes to the block's limbs directly (exact).  |V| < 2^121 for
+// < 2^24 terms per thread, so V never overflows and 32 of them can be summed.  At the end the
+// lanes of a warp that share the anchor add their V with an exact 128-bit shuffle tree and one lane
+// flushes (no contention).  Every path is exact: the block's value is the exact sum of its terms
+// whatever the grouping, so the fused and the per-op kernels give the same bits.  Block limbs
+// `loc` use the global slot convention (nbg_xacc_add: 0-9 limbs, 10 non-finite counts, 12 fp64 sum
+// of out-of-window terms), live in shared memory, are zeroed before a __syncthreads.
+struct nbg_xt { unsigned __int128 v; int L; int init; };
+// 64-bit add into shared memory from two native 32-bit atomics (the 64-bit form is a CAS loop on
+// this part): low half first, its carry added to the high half with the value's high word.  The
+// pair is not atomic as a unit but every carry is counted, so the final value is exact.
+__device__ __forceinline__ void nbg_smem_add64(u64 *p, u64 v) {
+    unsigned *w = (unsigned *)p;
+    const unsigned lo = (unsigned)v, hi = (unsigned)(v >> 32);
+    const unsigned old = atomicAdd(w, lo);
+    const unsigned c = (old + lo < old) ? 1u : 0u;
+    if (hi + c) atomicAdd(w + 1, hi + c);
+}
+// the exact add of one term into shared block limbs (nbg_xacc_add's arithmetic, smem atomics)
+__device__ void nbg_xacc_add_smem(u64 *acc, double d) {
+    if (d == 0.0) return;
+    long long bits = __double_as_longlong(d);
+    int e = (int)((bits >> 52) & 0x7ff);
+    if (e == 0x7ff) {
+        nbg_smem_add64(&acc[10], nbg_xacc_flag_counts(((bits & 0xFFFFFFFFFFFFFull) != 0) ? 1ull : (bits < 0 ? 4ull : 2ull)));
+        return;
+    }
+    u64 m = (u64)bits & 0xFFFFFFFFFFFFFull;
+    int ex;
+    if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
+    int pos = ex + 160;
+    if (pos > 235 || pos + 52 < 0) { atomicAdd((double *)&acc[12], d); return; }
+    if (pos < 0) { m >>= -pos; pos = 0; if (m == 0) return; }
+    int k = pos >> 5, sh = pos & 31;
+    u64 lo = m << sh;
+    u64 hi = sh ? (m >> (64 - sh)) : 0ull;
+    u64 p0 = lo & 0xffffffffull, p1 = lo >> 32, p2 = hi;
+    if (bits < 0) { p0 = (u64)(-(long long)p0); p1 = (u64)(-(long long)p1); p2 = (u64)(-(long long)p2); }
+    if (p0) nbg_smem_add64(&acc[k], p0);
+    if (p1) nbg_smem_add64(&acc[k + 1], p1);
+    if (p2) nbg_smem_add64(&acc[k + 2], p2);
+}
+__device__ __forceinline__ nbg_xt nbg_xt_zero() { nbg_xt a; a.v = 0; a.L = 0; a.init = 0; return a; }
+// V * 2^L into the block limbs (by value: the caller's accumulator stays in registers)
+__device__ __noinline__ void nbg_xt_flush_v(unsigned __int128 v, int L, u64 *loc) {
+    if (v == 0) return;
+    const bool neg = (long long)(v >> 64) < 0;
+    const unsigned __int128 mag = neg ? (unsigned __int128)0 - v : v;
+    const int pos = L + 160;
+    const int hb = (mag >> 64) ? 127 - __clzll((long long)(u64)(mag >> 64)) : 63 - __clzll((long long)(u64)mag);
+    if (pos < 0 || pos + hb >= 319) {
+        // outside the limb window (wider than any PageRank value): fp64, arrival order
+        const double dv = ((double)(u64)(mag >> 64) * 18446744073709551616.0 + (double)(u64)mag) * ldexp(1.0, L);
+        atomicAdd((double *)&loc[12], neg ? -dv : dv);
+    } else {
+        const int k0 = pos >> 5, sh = pos & 31;
+        const unsigned __int128 lo = mag << sh;
+        const u64 pc[5] = {(u64)lo & 0xffffffffull, (u64)(lo >> 32) & 0xffffffffull, (u64)(lo >> 64) & 0xffffffffull,
+                           (u64)(lo >> 96) & 0xffffffffull, sh ? (u64)(mag >> (128 - sh)) : 0ull};
+        for (int i = 0; i < 5; i++)
+            if (pc[i] && k0 + i <= 9) nbg_smem_add64(&loc[k0 + i], neg ? (u64)(-(long long)pc[i]) : pc[i]);
+    }
+}
+__device__ __forceinline__ int nbg_xt_anchor(int ex) { return ((ex - 8) & ~31) - 0; }
+// everything but the common case (first term, re-anchor, below the window, non-finite, subnormal)
+__device__ __noinline__ nbg_xt nbg_xt_slow(nbg_xt a, double d, u64 *loc) {
+    if (d == 0.0) return a;
+    const long long bits = __double_as_longlong(d);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    if (e == 0x7ff) { nbg_xacc_add_smem(loc, d); return a; }   // non-finite: counted in the block limbs
+    u64 m = (u64)bits & 0xFFFFFFFFFFFFFull;
+    int ex;
+    if (e == 0) ex = -1074; else { m |= (1ull << 52); ex = e - 1075; }
+    if (!a.init) { a.L = nbg_xt_anchor(ex); a.init = 1; }
+    int sh = ex - a.L;
+    if (sh < 0) { nbg_xacc_add_smem(loc, d); return a; }     // far below the window: exact, straight to the block
+    if (sh > 44) { nbg_xt_flush_v(a.v, a.L, loc); a.v = 0; a.L = nbg_xt_anchor(ex); sh = ex - a.L; }
+    const unsigned __int128 t = ((unsigned __int128)m) << sh;
+    a.v = bits < 0 ? a.v - t : a.v + t;
+    return a;
+}
+// the common case inline: a normal term whose LSB lies in the anchored window
+__device__ __forceinline__ void nbg_xt_add(nbg_xt &a, double d, u64 *loc) {
+    const long long bits = __double_as_longlong(d);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    const int sh = e - 1075 - a.L;
+    if (a.init && (unsigned)(e - 1) < 0x7feu && (unsigned)sh <= 44u) {
+        const u64 m = ((u64)bits & 0xFFFFFFFFFFFFFull) | (1ull << 52);
+        const u64 lo = m << sh, hi = sh ? (m >> (64 - sh)) : 0ull;
+        const unsigned __int128 t = ((unsigned __int128)hi << 64) | lo;
+        a.v = bits < 0 ? a.v - t : a.v + t;
+    } else if (d != 0.0) {
+        a = nbg_xt_slow(a, d, loc);
+    }
+}
+// block finish of one exact reduction (every thread calls it; contains __syncthreads): lanes that
+// share lane 0's anchor sum their V exactly (128-bit shuffle tree) and lane 0 flushes it; the
+// others (a different anchor) flush their own
+__device__ void nbg_block_finish_xt(const nbg_xt a, u64 *loc, u64 *acc) {
+    const int lane = threadIdx.x & 31;
+    const int L0 = __shfl_sync(0xffffffffu, a.init ? a.L : 0x7fffffff, 0);
+    const bool same = a.init && a.L == L0;
+    const unsigned own = __ballot_sync(0xffffffffu, a.init && !same);
+    if (own & (1u << lane)) nbg_xt_flush_v(a.v, a.L, loc);
+    u64 lo = same ? (u64)a.v : 0ull, hi = same ? (u64)(a.v >> 64) : 0ull;
+    for (int d = 16; d >= 1; d >>= 1) {
+        const u64 l2 = __shfl_down_sync(0xffffffffu, lo, d), h2 = __shfl_down_sync(0xffffffffu, hi, d);
+        const u64 s = lo + l2;
+        hi = hi + h2 + (s < l2 ? 1ull : 0ull);
+        lo = s;
+    }
+    if (lane == 0 && L0 != 0x7fffffff) nbg_xt_flush_v(((unsigned __int128)hi << 64) | lo, L0, loc);
+    __syncthreads();
+    const int k = threadIdx.x;
+    if (k <= 10) { if (loc[k]) atomicAdd(&acc[k], loc[k]); }
+    else if (k == 12) { const double dd = __longlong_as_double((long long)loc[12]); if (dd != 0.0) atomicAdd((double *)&acc[12], dd); }
+}
+
 // ------------------------------------------------------------------ deterministic block combines
 // Fixed shuffle-down tree inside a warp, then warp partials summed in warp order by thread 0.
 __device__ __forceinline__ double nbg_warp_sum(double v) {

@@ -21,8 +21,8 @@ static bool compile_only(const std::string &src, const std::string &kname, std::
         log += "create failed\n";
         return false;
     }
-    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-default-device"};
-    nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-default-device", "--device-int128"};
+    nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
     if (r != NVRTC_SUCCESS) {
         size_t ls = 0;
         nvrtcGetProgramLogSize(prog, &ls);

@@ -10,6 +10,7 @@
 // operator code is part of the region signature (plan cache), codes are unique per process.
 #include <nvrtc.h>
 
+#include <deque>
 #include <mutex>
 
 #include "nbg_internal.hpp"
@@ -20,7 +21,7 @@ extern const char *NBG_PRELUDE_SRC;
 
 namespace {
 std::mutex g_mu;
-std::vector<UserOp> g_ops;   // code = NBG_USER_OP_BASE + index
+std::deque<UserOp> g_ops;    // code = NBG_USER_OP_BASE + index (deque: stable element addresses)
 }  // namespace
 
 const UserOp *user_op(int code) {
@@ -54,7 +55,7 @@ static std::string validate(const UserOp &op) {
     src += "}\n";
     nvrtcProgram prog;
     if (nvrtcCreateProgram(&prog, src.c_str(), "userop.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) return "nvrtcCreateProgram failed";
-    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-default-device"};
+    const char *opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-default-device", "--device-int128"};
     nvrtcResult r = nvrtcCompileProgram(prog, (int)(sizeof opts / sizeof opts[0]), opts);
     std::string log;
     if (r != NVRTC_SUCCESS) {

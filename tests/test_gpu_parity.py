@@ -139,20 +139,12 @@ def test_blocking_equals_nonblocking_bitwise(nbg, ctx, bctx, T):
         A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 12, 8, 9)
         r, sweeps, hist = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=12, type=t)
         res.append((nbg.nbg_vector_export_dense(c, r), hist))
-    if T == "fp32":
-        assert np.array_equal(res[0][0], res[1][0])      # ranks: bit for bit
-    else:
-        # the dangling mass ds is summed per block in fp64 in the fused kernel and per element
-        # block in the per-op reduce, so its last bit can differ, and c = alpha*ds/n + (1-alpha)/n
-        # with it: fp64 ranks agree to a few ulps, fp32 ranks round it away
-        assert rel(res[0][0], res[1][0]) <= 1e-15
-    if T == "fp32":
-        assert np.array_equal(res[0][1], res[1][1])      # fp32 terms sum exactly in fp64
-    else:
-        # fp64 deltas: the ranks differ by a few ulps (above), and Delta_k is a sum of
-        # cancelling differences, so it moves by up to sum_i ulp(r_i): the derived delta bound
-        # ("nonassociativity due to rounding")
-        assert delta_close(res[0][1], res[1][1], res[1][0], np.float64)
+    # ranks and deltas bit for bit in both types: the fused and the per-op kernels keep
+    # the same rounding points, and the dangling mass / delta -- summed per SpMV task in the fused
+    # kernel, per ewise thread in the per-op reduce -- are exact sums (fp64 terms: per-thread exact
+    # accumulators), so their grouping does not matter
+    assert np.array_equal(res[0][0], res[1][0])
+    assert np.array_equal(res[0][1], res[1][1])
 
 
 def test_long_rows_star(nbg, ctx):
@@ -614,3 +606,26 @@ def test_deterministic_flag_and_run_to_run_bits(nbg):
             nbg.nbg_finalize(c)
     for o in outs[1:]:
         assert np.array_equal(o[0], outs[0][0]) and np.array_equal(o[1], outs[0][1])
+
+
+@pytest.mark.parametrize("mode", ["NONBLOCKING", "BLOCKING"])
+def test_fp64_plus_reduce_is_the_exactly_rounded_sum(nbg, mode):
+    """fp64 PLUS reductions are exact sums rounded once (per-thread exact accumulators + exact
+    cross-block limbs): equal to math.fsum bit for bit, also with cancellation and wide exponent
+    ranges, standalone and fused behind elementwise operators."""
+    import math
+    c = nbg.nbg_init(getattr(nbg, mode), 0)
+    try:
+        rng = np.random.default_rng(21)
+        for n, spread in ((1, 10), (1000, 5), (100003, 60), (1 << 20, 30), (77777, 100)):   # inside [2^-160, 2^128)
+            v = np.ldexp(rng.standard_normal(n), rng.integers(-spread, spread, n))
+            if n > 10:
+                v[::7] = -v[1::7][: v[::7].shape[0]] if v[1::7].shape[0] >= v[::7].shape[0] else v[::7]
+            u = nbg.nbg_vector_from_dense(c, nbg.FP64, v)
+            s = nbg.nbg_reduce(c, nbg.FP64, nbg.PLUS, u)
+            assert nbg.nbg_scalar_get(c, s) == math.fsum(v), n
+            w = nbg.nbg_apply(c, nbg.FP64, "ABS", u)
+            s2 = nbg.nbg_reduce(c, nbg.FP64, nbg.PLUS, w)
+            assert nbg.nbg_scalar_get(c, s2) == math.fsum(np.abs(v)), n
+    finally:
+        nbg.nbg_finalize(c)
