@@ -157,6 +157,10 @@ def run_ours(args, rank, world, local_rank):
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         nbg.nbg_dist_init(ctx, rank, world, obj[0])
+        # NBG_DIST_EXCHANGE=peer: the exchange fused into the sweep kernel as NVLink peer stores
+        # (nbg_dist_set_exchange); default: one NCCL group per sweep
+        xmode = os.environ.get("NBG_DIST_EXCHANGE", "collective")
+        nbg.nbg_dist_set_exchange(ctx, nbg.DIST_EXCHANGE_PEER if xmode == "peer" else nbg.DIST_EXCHANGE_COLLECTIVE)
         A, deg, cuts, ncols_g = nbg.nbg_dist_graph_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed,
                                                                   nranks=world, bytes_per_row=5 * w)
         n = int(cuts[-1])
@@ -308,6 +312,7 @@ def run_ours(args, rank, world, local_rank):
                 "n": n, "nnz": nnz, "dangling": cfg["dangling"], "alpha": cfg["alpha"], "tol": tol,
                 "itermax": itermax, "sweeps_per_step": sweeps_total / args.steps,
                 "parallelism": f"rows{world}" if world > 1 else "single",
+                **({"exchange": os.environ.get("NBG_DIST_EXCHANGE", "collective")} if world > 1 else {}),
                 "l2": l2_note(nnz, ncols_g * w),
                 "setup_s": round(setup_s, 3),
             },

@@ -445,17 +445,37 @@ nbg_status nbg_dist_graph_from_generator(nbg_ctx *ctx, const nbg_graphgen *g, in
  * materialised -- together with the pending reductions s_in[0..nscal) and every pending node the
  * caller holds, in ONE fused kernel -- with its values written straight into positions
  * cuts[rank] + i (< ncols_g) of a new full vector w of length ncols_g; then ONE NCCL group
- * broadcasts every rank's slice in place and sums the scalars' exact slots (s_out[i] = global sum
+ * broadcasts every rank's slice in place (peer mode: the kernel already stored it on every rank,
+ * see nbg_dist_set_exchange) and sums the scalars' exact slots (s_out[i] = global sum
  * of s_in[i], float PLUS reductions).  u_blk itself stays pending (its values live only inside w).
  * With one rank no collective runs.  Errors: NBG_DIMENSION_MISMATCH (u_blk length),
  * NBG_NOT_IMPLEMENTED (sparse/bitset u_blk, non-PLUS scalars across ranks), NBG_INVALID_VALUE. */
 nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u_blk, const int64_t *cuts, int64_t ncols_g,
                                        int nscal, const nbg_scalar *s_in, nbg_scalar *s_out);
 
+/* Exchange mode of nbg_vector_allgather_reduce (per context; every rank of a group must set the
+ * same mode before its first exchange):
+ *   NBG_DIST_EXCHANGE_COLLECTIVE (default): the producing kernel writes this rank's slice of w,
+ *     then one NCCL group broadcasts the slices (loopback: device copies) and sums the slots.
+ *   NBG_DIST_EXCHANGE_PEER: the exchange is fused into the producing kernel -- every element it
+ *     computes is stored straight into ALL ranks' w buffers (peer stores over NVLink/NVSwitch:
+ *     buffers mapped with CUDA IPC handles exchanged once per (ncols_g, type) through NCCL;
+ *     loopback: plain pointers), so the data movement overlaps the SpMV row by row and only the
+ *     scalar sums (plus, with no scalars, a one-word barrier) remain as a collective.  w lives in
+ *     one of two exchange buffers per rank used alternately: it is valid until the exchange after
+ *     next of the same (ncols_g, type) overwrites it (nbg_pagerank_dist frees each gathered vector
+ *     before that).  At most 8 ranks.
+ * Errors: NBG_INVALID_VALUE (unknown mode, > 8 ranks for PEER, no nbg_dist_init / loopback). */
+enum { NBG_DIST_EXCHANGE_COLLECTIVE = 0, NBG_DIST_EXCHANGE_PEER = 1 };
+nbg_status nbg_dist_set_exchange(nbg_ctx *ctx, int mode);
+
 /* Distributed PageRank on the output of nbg_dist_graph_from_generator: one fused kernel and one
- * NCCL group per sweep (nbg_vector_allgather_reduce).  r_blk receives this rank's ranks in pi order
- * (rows [cuts[rank], cuts[rank+1])); sweeps / delta_hist as nbg_pagerank.  The ranks are
- * bit-identical to the single-GPU nbg_pagerank of the same graph (permuted by pi), for every P. */
+ * exchange per sweep (nbg_vector_allgather_reduce, in the context's exchange mode).  r_blk
+ * receives this rank's ranks in pi order (rows [cuts[rank], cuts[rank+1])); sweeps / delta_hist as
+ * nbg_pagerank.  Every row sum keeps the row's original entry order, the delta and dangling mass
+ * are exact sums over all ranks (identical on every rank); ranks agree with the single-GPU
+ * nbg_pagerank of the same graph (permuted by pi) up to the fp64 grouping of long rows' partial
+ * sums, which follows each block's SpMV task layout. */
 nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vector deg_blk, const int64_t *cuts, int64_t ncols_g,
                              const nbg_pr_params *p, nbg_vector *r_blk, int *sweeps, double *delta_hist);
 

@@ -68,7 +68,7 @@ std::string Prog::signature() const {
     s.push_back('|');
     for (const OutV &o : outs) {
         sig_put(s, o.ins, '>');
-        sig_put(s, o.out, o.scatter ? 's' : ';');
+        sig_put(s, o.out, o.multi ? 'm' : (o.scatter ? 's' : ';'));
     }
     s.push_back('|');
     for (const RedOut &r : reds) {
@@ -90,8 +90,11 @@ struct Gen {
 
     // store of output ov at element index `idx` (plain, or scattered through a.oscat)
     std::string scat(const OutV &ov, const std::string &idx) const {
-        const std::string o = std::to_string(ov.out);
-        return std::string("{ const int d_ = a.oscat[") + o + "][" + idx + "]; if (d_ >= 0) ((" + ctype(p.ins[ov.ins].t) +
+        const std::string o = std::to_string(ov.out), T = ctype(p.ins[ov.ins].t);
+        if (ov.multi)   // the exchange: the same element stored into every rank's buffer (P2P over NVLink)
+            return std::string("{ const int d_ = a.oscat[") + o + "][" + idx + "]; if (d_ >= 0) { const " + T + " v_ = " + v(ov.ins) +
+                   "; for (int q_ = 0; q_ < a.npeer; q_++) ((" + T + "*)a.peer[q_])[d_] = v_; } }";
+        return std::string("{ const int d_ = a.oscat[") + o + "][" + idx + "]; if (d_ >= 0) ((" + T +
                "*)a.out[" + o + "])[d_] = " + v(ov.ins) + "; }";
     }
     std::string store(const OutV &ov, const std::string &idx) const {

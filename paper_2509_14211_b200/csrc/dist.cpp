@@ -30,6 +30,7 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
@@ -49,6 +50,7 @@ static NcclApi &nccl() {
     NBG_SYM(CommDestroy)
     NBG_SYM(Broadcast)
     NBG_SYM(AllReduce)
+    NBG_SYM(AllGather)
     NBG_SYM(GroupStart)
     NBG_SYM(GroupEnd)
     NBG_SYM(GetErrorString)
@@ -64,6 +66,12 @@ static NcclApi &nccl() {
     } while (0)
 
 Dist::~Dist() {
+    if (!peersets.empty()) cudaDeviceSynchronize();   // no kernel may still store into the buffers
+    for (auto &kv : peersets) {
+        for (void *p : kv.second.opened) cudaIpcCloseMemHandle(p);
+        for (void *p : kv.second.own)
+            if (p) cudaFree(p);
+    }
     if (comm) nccl().CommDestroy((ncclComm_t)comm);
 }
 
@@ -79,7 +87,8 @@ struct LoopGroup {
     long long gen = 0;
     std::vector<const void *> ptr;
     std::vector<std::vector<const unsigned long long *>> slots;
-    explicit LoopGroup(int p) : P(p), ptr(p, nullptr), slots(p) {}
+    std::vector<void *> pw;   // peer mode setup: each rank's two exchange buffers
+    explicit LoopGroup(int p) : P(p), ptr(p, nullptr), slots(p), pw(2 * p, nullptr) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(mu);
         const long long g = gen;
@@ -129,6 +138,52 @@ static void loop_exchange(Ctx &c, Dist &D, char *W, size_t ws, const std::vector
 }
 
 static ncclComm_t comm_of(Dist &d) { return (ncclComm_t)d.comm; }
+
+// Peer mode (nbg_dist_set_exchange): the ping-pong pair of exchange buffers of (ncols_g, ws) on this
+// rank and every peer's, set up collectively on first use.  Buffers come from cudaMalloc (CUDA IPC
+// needs them outside the stream-ordered pool).  Under NCCL the IPC handles are all-gathered once and
+// opened with lazy peer access (NVLink/NVSwitch P2P); under loopback the ranks share one device and
+// exchange plain pointers at a host barrier.
+static Dist::PeerSet &peer_set(Ctx &c, Dist &D, int64_t ncols_g, size_t ws) {
+    auto key = std::make_pair(ncols_g, ws);
+    auto it = D.peersets.find(key);
+    if (it != D.peersets.end()) return it->second;
+    Dist::PeerSet S;
+    S.bytes = (size_t)std::max<int64_t>(ncols_g, 1) * ws + 64;
+    for (int b = 0; b < 2; b++) {
+        NBG_CUDA(cudaMalloc(&S.own[b], S.bytes));
+        S.peer[b].assign(D.nranks, nullptr);
+        S.peer[b][D.rank] = S.own[b];
+    }
+    if (D.nranks > 1 && D.loop) {
+        LoopGroup &G = *D.loop;
+        G.pw[2 * D.rank] = S.own[0];
+        G.pw[2 * D.rank + 1] = S.own[1];
+        G.barrier();
+        for (int q = 0; q < D.nranks; q++)
+            for (int b = 0; b < 2; b++) S.peer[b][q] = G.pw[2 * q + b];
+        G.barrier();
+    } else if (D.nranks > 1) {
+        const size_t hs = sizeof(cudaIpcMemHandle_t);
+        std::vector<cudaIpcMemHandle_t> h(2 * (size_t)D.nranks);
+        for (int b = 0; b < 2; b++) NBG_CUDA(cudaIpcGetMemHandle(&h[2 * D.rank + b], S.own[b]));
+        BufP hb = alloc_buf(c, 2 * hs * D.nranks);
+        char *mine = (char *)hb->d + 2 * hs * D.rank;
+        NBG_CUDA(cudaMemcpyAsync(mine, &h[2 * D.rank], 2 * hs, cudaMemcpyHostToDevice, c.stream));
+        NBG_NCCL(nccl().AllGather(mine, hb->d, 2 * hs, ncclUint8, comm_of(D), c.stream));
+        NBG_CUDA(cudaMemcpyAsync(h.data(), hb->d, 2 * hs * D.nranks, cudaMemcpyDeviceToHost, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+        for (int q = 0; q < D.nranks; q++)
+            for (int b = 0; b < 2; b++) {
+                if (q == D.rank) continue;
+                void *p = nullptr;
+                NBG_CUDA(cudaIpcOpenMemHandle(&p, h[2 * q + b], cudaIpcMemLazyEnablePeerAccess));
+                S.opened.push_back(p);
+                S.peer[b][q] = p;
+            }
+    }
+    return D.peersets.emplace(key, std::move(S)).first->second;
+}
 
 }  // namespace nbg
 
@@ -228,6 +283,14 @@ nbg_status nbg_dist_init_loopback(nbg_ctx **ctxs, int nranks) {
         d->loop = G;
         ctxs[q]->dist = std::move(d);
     }
+    return NBG_SUCCESS;
+}
+
+nbg_status nbg_dist_set_exchange(nbg_ctx *ctx, int mode) {
+    if (!ctx) return NBG_NULL_POINTER;
+    if (!ctx->dist || (mode != NBG_DIST_EXCHANGE_COLLECTIVE && mode != NBG_DIST_EXCHANGE_PEER)) return NBG_INVALID_VALUE;
+    if (mode == NBG_DIST_EXCHANGE_PEER && ctx->dist->nranks > MAX_PEER) return NBG_INVALID_VALUE;
+    ctx->dist->xmode = mode;
     return NBG_SUCCESS;
 }
 
@@ -460,7 +523,23 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
             sin.push_back(s_in[i]->node);
         }
         const size_t ws = type_size(x->type);
-        BufP W = alloc_buf(*ctx, (size_t)std::max<int64_t>(ncols_g, 1) * ws + 64);
+        const bool peer = ctx->dist && ctx->dist->xmode == NBG_DIST_EXCHANGE_PEER;
+        BufP W;
+        std::vector<void *> peers;   // peer mode: every rank's buffer for this exchange (own included)
+        if (peer) {
+            Dist::PeerSet &S = peer_set(*ctx, *ctx->dist, ncols_g, ws);
+            const int b = S.parity;
+            S.parity ^= 1;
+            W = std::make_shared<Buf>();   // a fresh buffer identity (memo keys) over the recycled memory
+            W->ctx = ctx;
+            W->id = ctx->new_id();
+            W->d = S.own[b];
+            W->bytes = S.bytes;
+            W->owned = false;
+            peers = S.peer[b];
+        } else {
+            W = alloc_buf(*ctx, (size_t)std::max<int64_t>(ncols_g, 1) * ws + 64);
+        }
         // ---- this rank's block, written by the producing kernel straight into W[c0 + i] (i < ncols_g - c0)
         if (!ctx->dist_maps) ctx->dist_maps = std::make_shared<std::map<std::pair<int64_t, int64_t>, BufP>>();
         auto key = std::make_pair(c0, nb);
@@ -471,7 +550,7 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
         }
         std::vector<NodeP> roots;
         if (!x->mat) {
-            ctx->out_targets[x.get()] = Ctx::OutTarget{W, (const int *)map->d};
+            ctx->out_targets[x.get()] = Ctx::OutTarget{W, (const int *)map->d, peers};
             roots.push_back(x);
         }
         for (const NodeP &sn : sin)
@@ -488,8 +567,11 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
             ensure_full(*ctx, x);
             const void *src = x->kind == VKind::ISO ? x->full_cache->d : x->buf->d;
             const int64_t cnt = std::max<int64_t>(0, std::min(nb, ncols_g - c0));
-            if (cnt > 0)
-                NBG_CUDA(cudaMemcpyAsync((char *)W->d + c0 * ws, src, (size_t)cnt * ws, cudaMemcpyDeviceToDevice, ctx->stream));
+            if (cnt > 0) {
+                if (!peer) peers.assign(1, W->d);
+                for (void *dst : peers)   // peer mode: into every rank's buffer (P2P copies)
+                    NBG_CUDA(cudaMemcpyAsync((char *)dst + c0 * ws, src, (size_t)cnt * ws, cudaMemcpyDeviceToDevice, ctx->stream));
+            }
         }
         std::vector<NodeP> sout;
         for (const NodeP &sn : sin) {
@@ -521,6 +603,7 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
         if (P > 1 && ctx->dist->loop) {
             std::vector<int64_t> off(P), cnt(P);
             nbg_dist_exchange_plan(cuts, P, ncols_g, off.data(), cnt.data());
+            if (peer) std::fill(cnt.begin(), cnt.end(), 0);   // data already in place: barrier + sums only
             std::vector<const unsigned long long *> si;
             std::vector<unsigned long long *> so;
             for (size_t i = 0; i < sin.size(); i++) {
@@ -536,11 +619,16 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
             char *dst = (char *)W->d;
             cudaEvent_t ev0;
             timing_begin(*ctx, "comm", &ev0);
+            SlotP bar;
             NBG_NCCL(nccl().GroupStart());
-            for (int q = 0; q < P; q++)
+            for (int q = 0; q < P && !peer; q++)
                 if (cnt[q] > 0)
                     NBG_NCCL(nccl().Broadcast(dst + off[q] * ws, dst + off[q] * ws, (size_t)cnt[q], dt, q, comm_of(D), ctx->stream));
             for (size_t i = 0; i < sin.size(); i++) xacc_allreduce(ctx, D, sin[i]->slot->dptr(), sout[i]->slot->dptr());
+            if (peer && sin.empty()) {   // the peer stores need a cross-rank barrier: a one-word allreduce
+                bar = alloc_slot(*ctx);
+                NBG_NCCL(nccl().AllReduce(bar->dptr(), bar->dptr(), 1, ncclInt64, ncclSum, comm_of(D), ctx->stream));
+            }
             NBG_NCCL(nccl().GroupEnd());
             timing_end(*ctx, "comm", ev0);
         }

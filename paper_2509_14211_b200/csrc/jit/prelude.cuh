@@ -40,6 +40,8 @@ struct KArgs {
     void *part;
     long long S;
     long long ncols_g;
+    void *peer[8];
+    int npeer;
 };
 
 // ------------------------------------------------------------------ operators in type T

@@ -233,7 +233,9 @@ struct Ins {
     bool uniform = false;   // value independent of the element index
 };
 
-struct OutV { int ins; int out; bool scatter = false; };   // scatter: out[oscat[i]] (skip < 0)
+// scatter: out[oscat[i]] (skip < 0); multi: the scattered value stored into every a.peer[q] buffer
+// (the multi-GPU exchange fused into the producing kernel, dist.cpp peer mode)
+struct OutV { int ins; int out; bool scatter = false; bool multi = false; };
 struct RedOut { int ins; int monoid; int racc; uint8_t fmt; };
 
 struct SpmvSig {
@@ -260,6 +262,7 @@ struct Prog {
 
 // Kernel arguments (one struct passed by value; mirrored in jit/prelude.cuh).
 constexpr int MAX_IN = 16, MAX_OUT = 8, MAX_IMM = 32, MAX_SIN = 8, MAX_RED = 8;
+constexpr int MAX_PEER = 8;   // ranks a multi-store output writes to (one NVSwitch node)
 struct KArgs {
     long long n;
     const void *in[MAX_IN];
@@ -290,6 +293,8 @@ struct KArgs {
     void *part;                  // per-slot partial sums (accumulator type)
     long long S;                 // phase 1: columns per block
     long long ncols_g;           // phase 1: columns of the gather layout
+    void *peer[MAX_PEER];        // multi-store output: the exchange buffers of all ranks
+    int npeer;
 };
 
 struct Kernel {
@@ -327,6 +332,17 @@ struct Dist {
     int rank = 0, nranks = 1;
     void *comm = nullptr;   // ncclComm_t
     std::shared_ptr<LoopGroup> loop;   // set instead of comm by nbg_dist_init_loopback
+    int xmode = 0;          // NBG_DIST_EXCHANGE_{COLLECTIVE,PEER} (nbg_dist_set_exchange)
+    // peer mode: per (ncols_g, element size) a ping-pong pair of exchange buffers on every rank
+    // and the peers' addresses (IPC-mapped under NCCL, plain pointers under loopback)
+    struct PeerSet {
+        size_t bytes = 0;
+        void *own[2] = {nullptr, nullptr};
+        std::vector<void *> peer[2];     // indexed by rank (own included)
+        std::vector<void *> opened;      // IPC mappings to close
+        int parity = 0;
+    };
+    std::map<std::pair<int64_t, size_t>, PeerSet> peersets;
     ~Dist();
 };
 
@@ -375,7 +391,7 @@ struct Ctx {
 
     // output targets of the current materialize call (multi-GPU: a block written straight into
     // the exchange buffer through a scatter map); see dist.cpp nbg_vector_allgather_reduce
-    struct OutTarget { BufP buf; const int *map = nullptr; };
+    struct OutTarget { BufP buf; const int *map = nullptr; std::vector<void *> peers; };   // peers: multi-store
     std::unordered_map<const Node *, OutTarget> out_targets;
     // nodes user handles point to (weak): nbg_wait_all materialises the live pending ones
     std::vector<std::weak_ptr<Node>> user_nodes;

@@ -512,7 +512,9 @@ struct Builder {
         OutV ov{i, (int)out_nodes.size()};
         // scattered store out[map[i]]: into a consumer's gather layout, or into a caller's target
         // (multi-GPU exchange buffer, Ctx::out_targets; map < 0 skips the row)
-        ov.scatter = (bool)scatter || c.out_targets.count(x.get()) > 0;
+        auto tg = c.out_targets.find(x.get());
+        ov.scatter = (bool)scatter || tg != c.out_targets.end();
+        ov.multi = tg != c.out_targets.end() && !tg->second.peers.empty();
         prog.outs.push_back(ov);
         out_nodes.push_back(x);
         out_scatter.push_back(scatter);
@@ -586,6 +588,11 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             // caller-provided destination (multi-GPU exchange buffer): out[map[i]], map < 0 skips
             b = tg->second.buf;
             args.oscat[k] = tg->second.map;
+            if (!tg->second.peers.empty()) {
+                if (args.npeer || tg->second.peers.size() > (size_t)MAX_PEER) fail(NBG_NOT_IMPLEMENTED, "planner: peer outputs");
+                args.npeer = (int)tg->second.peers.size();
+                for (int q = 0; q < args.npeer; q++) args.peer[q] = tg->second.peers[q];
+            }
         } else {
             int64_t len = sc ? sc->plan->ncols_g : n;
             b = alloc_buf(c, (size_t)len * type_size(x->type));

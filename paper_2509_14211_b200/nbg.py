@@ -37,6 +37,7 @@ FORMAT_FULL, FORMAT_ISO, FORMAT_SPARSE, FORMAT_BITSET, FORMAT_EMPTY = range(5)
 FORMAT_NAMES = ["full", "iso", "sparse", "bitset", "empty"]
 PR_UNIFORM, PR_DROP = 0, 1
 FLAG_DETERMINISTIC = 1
+DIST_EXCHANGE_COLLECTIVE, DIST_EXCHANGE_PEER = 0, 1
 
 UNOPS = {n: i for i, n in enumerate(["IDENTITY", "AINV", "ABS", "MINV", "ADD_C", "MUL_C", "AXPB", "ABS_SUB_C",
                                       "RECIP_SCALED", "ISZERO"])}
@@ -153,6 +154,7 @@ SIGNATURES = {
     "nbg_scalar_export_slot": [vp, vp, vp],
     "nbg_dist_exchange_plan": [vp, ctypes.c_int, i64, vp, vp],
     "nbg_dist_init_loopback": [vp, ctypes.c_int],
+    "nbg_dist_set_exchange": [vp, ctypes.c_int],
     "nbg_dist_graph_from_generator": [vp, ctypes.POINTER(nbg_graphgen), i64, pvp, pvp, vp, vp],
     "nbg_vector_allgather_reduce": [vp, pvp, vp, vp, i64, ctypes.c_int, vp, vp],
 }
@@ -583,6 +585,12 @@ def nbg_scalar_export_slot(ctx, s):
 def nbg_dist_init_loopback(ctxs):
     arr = (ctypes.c_void_p * len(ctxs))(*[c.value if isinstance(c, ctypes.c_void_p) else c for c in ctxs])
     _call(None, "nbg_dist_init_loopback", ctypes.cast(arr, ctypes.c_void_p), len(ctxs))
+
+
+def nbg_dist_set_exchange(ctx, mode):
+    """include/nbg.h nbg_dist_set_exchange: DIST_EXCHANGE_COLLECTIVE (default) or DIST_EXCHANGE_PEER
+    (the exchange fused into the producing kernel as peer stores)."""
+    _call(ctx, "nbg_dist_set_exchange", ctx, int(mode))
 
 
 def nbg_dist_exchange_plan(cuts, ncols_g):

@@ -95,9 +95,11 @@ def test_one_rank_pagerank_dist(nbg, T, tol, itermax):
         nbg.nbg_finalize(c)
 
 
-def _run_loopback(nbg, P, kind, scale, ef, seed, T, tol, itermax):
+def _run_loopback(nbg, P, kind, scale, ef, seed, T, tol, itermax, mode=0):
     ctxs = [nbg.nbg_init(nbg.NONBLOCKING, 0) for _ in range(P)]
     nbg.nbg_dist_init_loopback(ctxs)
+    for c in ctxs:
+        nbg.nbg_dist_set_exchange(c, mode)
     res = [None] * P
     errs = []
 
@@ -121,20 +123,23 @@ def _run_loopback(nbg, P, kind, scale, ef, seed, T, tol, itermax):
         x.start()
     for x in th:
         x.join(timeout=600)
+    assert not any(x.is_alive() for x in th), "a rank hung"
     for c in ctxs:
         nbg.nbg_finalize(c)
     assert not errs, errs
     return res
 
 
+@pytest.mark.parametrize("mode", ["collective", "peer"])
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("T", ["fp32", "fp64"])
-def test_loopback_ranks_match_one_rank(nbg, P, T):
+def test_loopback_ranks_match_one_rank(nbg, P, T, mode):
     t = nbg.TYPE_OF[T]
     npT = nbg.NP_OF[t]
+    md = nbg.DIST_EXCHANGE_PEER if mode == "peer" else nbg.DIST_EXCHANGE_COLLECTIVE
     scale, ef, seed, itermax = 12, 16, 3, 10
     one = _run_loopback(nbg, 1, nbg.GRAPH_RMAT, scale, ef, seed, t, -1.0, itermax)[0]
-    many = _run_loopback(nbg, P, nbg.GRAPH_RMAT, scale, ef, seed, t, -1.0, itermax)
+    many = _run_loopback(nbg, P, nbg.GRAPH_RMAT, scale, ef, seed, t, -1.0, itermax, md)
     rp, ci, deg = oracle_graph("rmat", scale, ef, seed)
     order, pi, rp2, ci2, ncols_g = relabel(rp, ci, deg)
     cuts = many[0]["cuts"]
@@ -155,6 +160,35 @@ def test_loopback_ranks_match_one_rank(nbg, P, T):
     assert np.allclose(many[0]["hist"], one["hist"], rtol=1e-9, atol=1e-12)
     ro, so, dho, _ = oracle.pagerank(rp, ci, deg, dtype=npT, itermax=itermax)
     assert rel(r, ro[order]) <= (1e-5 if T == "fp32" else 1e-10)
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_peer_exchange_is_bitwise_the_collective_one(nbg, P):
+    """The fused peer-store exchange (every rank's kernel stores its slice into all ranks' gathered
+    vectors) changes where the values go, not what they are: ranks, sweep counts and delta history
+    equal the collective exchange bit for bit; the ping-pong buffers survive a convergence run with
+    an odd and an even number of exchanges."""
+    for T in (nbg.FP32, nbg.FP64):
+        for tol, itermax in ((-1.0, 7), (1e-6, 100)):
+            a = _run_loopback(nbg, P, nbg.GRAPH_RMAT, 12, 16, 21, T, tol, itermax, nbg.DIST_EXCHANGE_COLLECTIVE)
+            b = _run_loopback(nbg, P, nbg.GRAPH_RMAT, 12, 16, 21, T, tol, itermax, nbg.DIST_EXCHANGE_PEER)
+            for x, y in zip(a, b):
+                assert x["sweeps"] == y["sweeps"]
+                assert np.array_equal(x["r"], y["r"]) and np.array_equal(x["hist"], y["hist"])
+                assert y["kernels"] <= y["sweeps"] + 4
+
+
+def test_set_exchange_validation(nbg):
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        with pytest.raises(nbg.NbgError):
+            nbg.nbg_dist_set_exchange(c, nbg.DIST_EXCHANGE_PEER)      # no group
+        nbg.nbg_dist_init_loopback([c])
+        with pytest.raises(nbg.NbgError):
+            nbg.nbg_dist_set_exchange(c, 7)
+        nbg.nbg_dist_set_exchange(c, nbg.DIST_EXCHANGE_PEER)
+    finally:
+        nbg.nbg_finalize(c)
 
 
 def test_loopback_convergence_sweep_count(nbg):
