@@ -43,40 +43,71 @@ static const char *ctype(int t) {
 // type in which an operator with output type t is evaluated
 static const char *ctype_compute(int t) { return t == NBG_BOOL ? "long long" : ctype(t); }
 
-// built with std::to_chars into one reserved string (it is computed at every wait: the plan-cache key)
-static inline void sig_put(std::string &s, long long v, char sep) {
-    char buf[24];
-    auto r = std::to_chars(buf, buf + sizeof buf, v);
-    s.append(buf, r.ptr);
-    s.push_back(sep);
+// The signature is emitted into a sink: a string (the plan-cache key, exact) or a 64-bit FNV-1a
+// hash of the same token stream (the region identity for learned hints, computed at every wait
+// without building the string).
+struct SigStr {
+    std::string &s;
+    void put(long long v, char sep) {
+        char buf[24];
+        auto r = std::to_chars(buf, buf + sizeof buf, v);
+        s.append(buf, r.ptr);
+        s.push_back(sep);
+    }
+    void ch(char c) { s.push_back(c); }
+};
+struct SigHash {
+    uint64_t h = 1469598103934665603ull;
+    void put(long long v, char sep) {
+        uint64_t u = (uint64_t)v;
+        for (int k = 0; k < 8; k++) {
+            h ^= (u >> (8 * k)) & 0xff;
+            h *= 1099511628211ull;
+        }
+        ch(sep);
+    }
+    void ch(char c) {
+        h ^= (unsigned char)c;
+        h *= 1099511628211ull;
+    }
+};
+template <class S>
+static void sig_emit(const Prog &p, S &s) {
+    s.ch(p.spmv ? (p.tp ? 'T' : (p.lpr ? 'L' : 'S')) : 'E');
+    s.ch(p.vec ? 'v' : 's');
+    s.put(p.nt, ',');
+    s.put(p.hot_kb, '|');
+    if (p.spmv) {
+        s.put(p.sp.add, ','); s.put(p.sp.mul, ','); s.put(p.sp.T, ','); s.put(p.sp.xt, ',');
+        s.put(p.sp.at, ','); s.put(p.sp.has_vals, '|');
+    }
+    for (const Ins &i : p.ins) {
+        s.put((int)i.k, ':'); s.put(i.t, ':'); s.put(i.code, ':'); s.put(i.a, ':'); s.put(i.b, ':');
+        s.put(i.imm0, ':'); s.put(i.imm1, ':'); s.put(i.slot, ':'); s.put((int)i.fmt, ';');
+    }
+    s.ch('|');
+    for (const OutV &o : p.outs) {
+        s.put(o.ins, '>');
+        s.put(o.out, o.multi ? 'm' : (o.scatter ? 's' : ';'));
+    }
+    s.ch('|');
+    for (const RedOut &r : p.reds) {
+        s.put(r.ins, '>'); s.put(r.monoid, ':'); s.put(r.racc, ':'); s.put((int)r.fmt, ';');
+    }
+    s.ch('|');
+    s.put(p.n_in, ','); s.put(p.n_out, ','); s.put(p.n_imm, ','); s.put(p.n_sin, ','); s.put(p.n_red, '.');
 }
 std::string Prog::signature() const {
-    std::string s;
-    s.reserve(32 + 48 * ins.size() + 12 * (outs.size() + reds.size()));
-    s.push_back(spmv ? (tp ? 'T' : (lpr ? 'L' : 'S')) : 'E');
-    s.push_back(vec ? 'v' : 's');
-    sig_put(s, nt, ',');
-    sig_put(s, hot_kb, '|');
-    if (spmv) {
-        sig_put(s, sp.add, ','); sig_put(s, sp.mul, ','); sig_put(s, sp.T, ','); sig_put(s, sp.xt, ',');
-        sig_put(s, sp.at, ','); sig_put(s, sp.has_vals, '|');
-    }
-    for (const Ins &i : ins) {
-        sig_put(s, (int)i.k, ':'); sig_put(s, i.t, ':'); sig_put(s, i.code, ':'); sig_put(s, i.a, ':'); sig_put(s, i.b, ':');
-        sig_put(s, i.imm0, ':'); sig_put(s, i.imm1, ':'); sig_put(s, i.slot, ':'); sig_put(s, (int)i.fmt, ';');
-    }
-    s.push_back('|');
-    for (const OutV &o : outs) {
-        sig_put(s, o.ins, '>');
-        sig_put(s, o.out, o.multi ? 'm' : (o.scatter ? 's' : ';'));
-    }
-    s.push_back('|');
-    for (const RedOut &r : reds) {
-        sig_put(s, r.ins, '>'); sig_put(s, r.monoid, ':'); sig_put(s, r.racc, ':'); sig_put(s, (int)r.fmt, ';');
-    }
-    s.push_back('|');
-    sig_put(s, n_in, ','); sig_put(s, n_out, ','); sig_put(s, n_imm, ','); sig_put(s, n_sin, ','); sig_put(s, n_red, '.');
-    return s;
+    std::string str;
+    str.reserve(32 + 48 * ins.size() + 12 * (outs.size() + reds.size()));
+    SigStr s{str};
+    sig_emit(*this, s);
+    return str;
+}
+uint64_t Prog::sig_hash() const {
+    SigHash h;
+    sig_emit(*this, h);
+    return h.h;
 }
 
 namespace {

@@ -422,7 +422,7 @@ nbg_status nbg_scalar_allreduce(nbg_ctx *ctx, nbg_scalar *out, nbg_scalar s) {
             NBG_NCCL(nccl().AllReduce(x->slot->dptr() + 11, y->slot->dptr() + 11, 1, ncclUint64, ncclMax, comm_of(D), ctx->stream));
             y->sfmt = x->sfmt;
         }
-        issue_readback(*ctx, *y->slot);   // a later get() waits only on this collective
+        mark_readable(*ctx, y->slot, record_prod_event(*ctx));   // a later get() waits only on this collective
         auto *h = new nbg_scalar_s{ctx, y};
         y->user_refs++;
         *out = h;
@@ -632,8 +632,12 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
             NBG_NCCL(nccl().GroupEnd());
             timing_end(*ctx, "comm", ev0);
         }
+        ProdEvP pe;
         for (size_t i = 0; i < sout.size(); i++) {
-            if (sout[i]->slot && P > 1) issue_readback(*ctx, *sout[i]->slot);
+            if (sout[i]->slot && P > 1) {
+                if (!pe) pe = record_prod_event(*ctx);
+                mark_readable(*ctx, sout[i]->slot, pe);
+            }
             sout[i]->user_refs++;
             s_out[i] = new nbg_scalar_s{ctx, sout[i]};
         }

@@ -7,6 +7,7 @@
 // CUDA 12 library API (cudaLibraryLoadData / cudaLibraryGetKernel), so no driver-API link is
 // needed.  A persistent cubin cache keyed by a hash of the source (the paper's future-work
 // "persistent cache") is used when NBG_JIT_CACHE names a directory.
+#include <cuda.h>
 #include <nvrtc.h>
 #include <algorithm>
 #include <sys/stat.h>
@@ -186,7 +187,28 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
         c.l2_win_base = args.x;
         c.l2_win_bytes = win;
     } else {
-        NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem, c.stream));
+        // the driver's cuLaunchKernel takes the library kernel handle directly (CUkernel in place of
+        // CUfunction), skipping the runtime's per-launch handle translation: ~0.5 us of host time per
+        // launch, which small graphs (C1) pay every sweep.  Resolved once through the runtime, no link
+        // against libcuda.
+        using LaunchFn = CUresult (*)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
+                                      void **, void **);
+        static LaunchFn drv = [] {
+            void *f = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuLaunchKernel", &f, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                f = nullptr;
+            return (LaunchFn)f;
+        }();
+        if (drv) {
+            const CUresult r = drv((CUfunction)(void *)k.k, (unsigned)g, 1, 1, (unsigned)k.block, 1, 1, (unsigned)k.smem,
+                                   (CUstream)c.stream, params, nullptr);
+            if (r != CUDA_SUCCESS) fail(NBG_PANIC, "cuLaunchKernel failed (" + std::to_string((int)r) + ") for " + k.name);
+        } else {
+            NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem,
+                                      c.stream));
+        }
     }
     timing_end(c, cls, ev0);
     c.stats.kernels_launched++;

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <functional>
 #include <memory>
@@ -95,12 +96,23 @@ using SlabP = std::shared_ptr<Slab>;
 
 enum class SFmt : uint8_t { HOST = 0, XACC = 1, I64 = 2, FMAX = 3, FMIN = 4, IMAX = 5, IMIN = 6 };
 
+// an event recorded on the context's stream right after the launch (or collective) that produced
+// one or more scalar slots: a deferred readback orders its copy after it (one record per launch)
+struct ProdEv {
+    Ctx *ctx = nullptr;
+    cudaEvent_t e = nullptr;
+    ~ProdEv();
+};
+using ProdEvP = std::shared_ptr<ProdEv>;
+
 struct Slot {
     SlabP slab;
     int idx = 0;
     uint64_t id = 0;
     cudaEvent_t ev = nullptr;          // recorded after the D2H copy of the mirror
     bool rb_issued = false;
+    ProdEvP pev;                       // producer position of a slot the host may read (mark_readable)
+    ProdEvP cev;                       // completion of a bulk readback that covered this slot
     unsigned long long *dptr() const { return slab->d + (size_t)idx * SLOT_U64; }
     unsigned long long *hptr() const { return slab->h + (size_t)idx * SLOT_U64; }
     ~Slot();
@@ -258,6 +270,7 @@ struct Prog {
     SpmvSig sp;
     int n_in = 0, n_out = 0, n_imm = 0, n_sin = 0, n_red = 0;
     std::string signature() const;
+    uint64_t sig_hash() const;   // hash of the signature's token stream (no string)
 };
 
 // Kernel arguments (one struct passed by value; mirrored in jit/prelude.cuh).
@@ -362,6 +375,7 @@ struct Ctx {
     SlabP cur_slab;
     std::vector<cudaEvent_t> event_pool;
     std::vector<cudaEvent_t> timing_pool;   // recycled timing events (nbg_set_timing)
+    std::deque<std::weak_ptr<Slot>> deferred;   // readable slots not yet copied, in production order
     cudaStream_t rb_stream = nullptr;      // scalar readbacks (issue_readback), ordered after the producer
     cudaEvent_t rb_dep = nullptr;
     // persisting-L2 window over the head of a large gathered vector (launch(), NBG_L2_PERSIST_MB)
@@ -418,6 +432,10 @@ SlotP alloc_slot(Ctx &c);
 cudaEvent_t get_event(Ctx &c);
 void put_event(Ctx &c, cudaEvent_t e);
 void issue_readback(Ctx &c, Slot &s);
+// record (once per producing launch: pass the same ProdEvP) the stream position after which slot s
+// is final; the D2H copy itself is issued only when the host reads it (issue_readback)
+ProdEvP record_prod_event(Ctx &c);
+void mark_readable(Ctx &c, const SlotP &s, const ProdEvP &pe);
 
 void timing_begin(Ctx &c, const char *cls, cudaEvent_t *ev0);
 void timing_end(Ctx &c, const char *cls, cudaEvent_t ev0);

@@ -64,6 +64,42 @@ static std::string dbits(double v) {
     return s;
 }
 
+// flat containers for the few-node sets of one wait (a region has tens of nodes): linear search
+// over a vector beats hashing and node allocation at this size (host time per wait)
+template <class K, class V>
+struct SmallMap {
+    std::vector<std::pair<K, V>> v;
+    using iterator = typename std::vector<std::pair<K, V>>::iterator;
+    iterator begin() { return v.begin(); }
+    iterator end() { return v.end(); }
+    iterator find(const K &k) {
+        for (auto it = v.begin(); it != v.end(); ++it)
+            if (it->first == k) return it;
+        return v.end();
+    }
+    size_t count(const K &k) { return find(k) != v.end() ? 1 : 0; }
+    V &operator[](const K &k) {
+        auto it = find(k);
+        if (it != v.end()) return it->second;
+        v.emplace_back(k, V{});
+        return v.back().second;
+    }
+};
+template <class K>
+struct SmallSet {
+    std::vector<K> v;
+    size_t count(const K &k) const {
+        for (const K &x : v)
+            if (x == k) return 1;
+        return 0;
+    }
+    std::pair<size_t, bool> insert(const K &k) {
+        if (count(k)) return {0, false};
+        v.push_back(k);
+        return {v.size() - 1, true};
+    }
+};
+
 // ---------------------------------------------------------------- structural keys
 
 static inline void kput(std::string &s, long long v) {
@@ -114,7 +150,19 @@ static std::string node_key(const Node *x, const Node *ph = nullptr) {
     return s;
 }
 
-static void leaf_bufs(const Node *x, std::vector<std::weak_ptr<Buf>> &deps, std::unordered_set<const Node *> &seen) {
+// key of x as if it were still pending (x materialised, its inputs still attached): the lookup
+// key the next wait builds for the same expression
+static std::string pending_key(const Node *x) {
+    if (!x->mat) return node_key(x);
+    Node *m = const_cast<Node *>(x);
+    m->mat = false;
+    std::string s;
+    key_rec(x, s, nullptr);
+    m->mat = true;
+    return s;
+}
+
+static void leaf_bufs(const Node *x, std::vector<std::weak_ptr<Buf>> &deps, SmallSet<const Node *> &seen) {
     if (!seen.insert(x).second) return;
     if (x->mat) {
         if (!x->scalar && (x->kind == VKind::FULL || structured_kind(x->kind)) && x->buf) deps.push_back(x->buf);
@@ -176,27 +224,26 @@ static bool memo_bind(Ctx &c, const NodeP &x) {
 // Results are immutable and keyed by the identities of immutable leaves, so a memo entry stays
 // valid while its leaves live; the table is bounded (LRU) so it cannot pin unbounded memory.
 static const size_t MEMO_CAP = 64;
-static void memo_insert(Ctx &c, const std::string &k, const NodeP &result) {
+static void memo_insert(Ctx &c, std::string k, const NodeP &result) {
     std::vector<std::weak_ptr<Buf>> deps;
-    std::unordered_set<const Node *> seen;
+    SmallSet<const Node *> seen;
     // leaves of the expression: walk the (still attached) inputs of the result node
-    Node tmp = *result;
-    tmp.mat = false;
-    leaf_bufs(&tmp, deps, seen);
-    if (deps.empty() && result->a) leaf_bufs(result->a.get(), deps, seen);
+    seen.insert(result.get());
+    if (result->a) leaf_bufs(result->a.get(), deps, seen);
+    if (result->b) leaf_bufs(result->b.get(), deps, seen);
     if (c.memo.size() >= MEMO_CAP) {
         auto victim = c.memo.begin();
         for (auto it = c.memo.begin(); it != c.memo.end(); ++it)
             if (it->second.stamp < victim->second.stamp) victim = it;
         c.memo.erase(victim);
     }
-    c.memo[k] = Ctx::MemoEntry{deps, result, ++c.memo_clock};
+    c.memo.insert_or_assign(std::move(k), Ctx::MemoEntry{std::move(deps), result, ++c.memo_clock});
 }
 
 // ---------------------------------------------------------------- cloning (hint templates)
 
 // clone the pending part of x; `subst` maps leaves to replacements (pre-seeded in `seen`)
-static NodeP clone_subst(Ctx &c, const NodeP &x, std::unordered_map<const Node *, NodeP> &seen) {
+static NodeP clone_subst(Ctx &c, const NodeP &x, SmallMap<const Node *, NodeP> &seen) {
     auto it = seen.find(x.get());
     if (it != seen.end()) return it->second;
     if (x->mat) return x;
@@ -280,7 +327,7 @@ static void learn_hint(Ctx &c, const NodeP &p, const MatP &consumer) {
     Hint h;
     h.key = k;
     h.consumer = consumer;
-    std::unordered_map<const Node *, NodeP> cs;
+    SmallMap<const Node *, NodeP> cs;
     h.ph_keep = make_placeholder(c, L);
     h.placeholder = h.ph_keep.get();
     cs[L] = h.ph_keep;
@@ -300,7 +347,7 @@ static void learn_hint(Ctx &c, const NodeP &p, const MatP &consumer) {
 
 // instantiate a hint over the region output R (nullptr if a loop-invariant leaf died)
 static NodeP instantiate(Ctx &c, const Hint &h, const NodeP &R) {
-    std::unordered_map<const Node *, NodeP> cs;
+    SmallMap<const Node *, NodeP> cs;
     cs[h.placeholder] = R;
     for (auto &f : h.fixed) {
         NodeP q = f.second.lock();
@@ -347,21 +394,21 @@ static NodeP permuted_view(Ctx &c, Mat &A, const NodeP &u, const std::string &pk
 struct Builder {
     Ctx &c;
     Prog prog;
-    std::unordered_map<const Node *, int> ins_of;
-    std::unordered_map<const Node *, int> in_slot_of;
+    SmallMap<const Node *, int> ins_of;
+    SmallMap<const Node *, int> in_slot_of;
     std::vector<NodeP> in_nodes;
     std::vector<double> imm;
     std::vector<SlotP> sin;
-    std::unordered_map<const Slot *, int> sin_of;
+    SmallMap<const Slot *, int> sin_of;
     std::vector<NodeP> prereq;
-    std::unordered_set<const Node *> prereq_set;
+    SmallSet<const Node *> prereq_set;
     NodeP mxv;
     BufP mxv_x;                        // the gathered vector (in the matrix's gather layout)
-    std::unordered_map<const Node *, MatP> need_mx;   // prerequisite -> the mxv that gathers it
+    SmallMap<const Node *, MatP> need_mx;   // prerequisite -> the mxv that gathers it
     std::vector<NodeP> visited;        // pending nodes of the region
     std::vector<NodeP> out_nodes;      // vector outputs, index = out slot
     std::vector<NodeP> red_nodes;      // reductions, index = racc slot
-    std::unordered_set<const Node *> is_out;
+    SmallSet<const Node *> is_out;
 
     explicit Builder(Ctx &cc) : c(cc) {
         imm.push_back(0.0);   // imm[0]: iso value of the matrix (spmv)
@@ -753,12 +800,16 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         x.kind = VKind::FULL;
         x.mat = true;
     }
+    ProdEvP pe;
     for (int k = 0; k < p.n_red; k++) {
         Node &x = *B.red_nodes[k];
         x.slot = rslots[k];
         x.sfmt = (SFmt)p.reds[k].fmt;
         x.mat = true;
-        if (x.user_refs > 0) issue_readback(c, *x.slot);   // so a later get() only waits on this kernel
+        if (x.user_refs > 0) {   // so a later get() only waits on this kernel (one event per launch)
+            if (!pe) pe = record_prod_event(c);
+            mark_readable(c, x.slot, pe);
+        }
     }
     (void)hint_outs;
 }
@@ -812,7 +863,7 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
                 if (!x->scalar && x->user_refs > 0 && !B.is_out.count(x.get())) B.add_vector_output(x);
         }
         const int nbase = (int)B.out_nodes.size();
-        const uint64_t base_hash = hash_str(B.prog.signature());
+        const uint64_t base_hash = B.prog.sig_hash();
 
         // speculative side outputs learned for this signature
         std::vector<HintOut> hint_outs;
@@ -863,15 +914,13 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
             PTimer pt_m(6);
             // memoise every result (common subexpressions across waits, e.g. dinv across runs)
             for (int k = 0; k < nbase; k++)
-                if (!c.out_targets.count(B.out_nodes[k].get())) memo_insert(c, base_keys[k], B.out_nodes[k]);
+                if (!c.out_targets.count(B.out_nodes[k].get())) memo_insert(c, std::move(base_keys[k]), B.out_nodes[k]);
             // side outputs are keyed with R already materialised (the next sweep's lookup key)
             for (HintOut &h : hint_outs) {
-                Node tmp = *h.node;
-                tmp.mat = false;
-                std::string k = node_key(&tmp);
+                std::string k = pending_key(h.node.get());
                 if (h.scatter) k = "PERM" + std::to_string(h.scatter->id) + "(" + k + ")";
                 if (dbg()) fprintf(stderr, "[nbg] memo insert %s\n", k.c_str());
-                memo_insert(c, k, h.node);
+                memo_insert(c, std::move(k), h.node);
             }
         }
         // elided intermediates = visited pending nodes that were not stored
@@ -893,10 +942,10 @@ void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
     PTimer pt_all(7);
     {
         PTimer pt_pb(0);
-        if (c.mode == NBG_NONBLOCKING) memo_purge(c);
+        if (c.mode == NBG_NONBLOCKING) memo_purge(c);   // dead entries release their result buffers
     }
     std::vector<NodeP> roots;
-    std::unordered_set<const Node *> seen;
+    SmallSet<const Node *> seen;
     for (const NodeP &r0 : roots_in) {
         NodeP r = r0;
         if (r->mat) continue;
@@ -941,7 +990,7 @@ double scalar_read(Ctx &c, const NodeP &s) {
     if (s->sfmt == SFmt::HOST) return s->hval;
     Slot &sl = *s->slot;
     issue_readback(c, sl);
-    NBG_CUDA(cudaEventSynchronize(sl.ev));
+    NBG_CUDA(cudaEventSynchronize(sl.cev ? sl.cev->e : sl.ev));
     return host_round(s->type, slot_value(sl.hptr(), s->sfmt));
 }
 

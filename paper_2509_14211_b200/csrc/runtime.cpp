@@ -129,14 +129,89 @@ void put_event(Ctx &c, cudaEvent_t e) { c.event_pool.push_back(e); }
 // The D2H copy of a slot's mirror runs on a side stream ordered after the producing kernel: on the
 // context stream the copy sat between consecutive sweep kernels and cost ≈ 13 µs of device time per
 // sweep (copy-engine handoff before and after the 2 µs copy).
+ProdEv::~ProdEv() {
+    if (ctx && e) put_event(*ctx, e);
+}
+
+ProdEvP record_prod_event(Ctx &c) {
+    auto p = std::make_shared<ProdEv>();
+    p->e = get_event(c);
+    p->ctx = &c;
+    NBG_CUDA(cudaEventRecord(p->e, c.stream));
+    return p;
+}
+
+void mark_readable(Ctx &c, const SlotP &s, const ProdEvP &pe) {
+    if (s->rb_issued) return;
+    s->pev = pe;
+    c.deferred.push_back(s);
+    if (c.deferred.size() > 256) {   // drop the entries of freed or already copied slots
+        std::deque<std::weak_ptr<Slot>> keep;
+        for (auto &w : c.deferred) {
+            auto q = w.lock();
+            if (q && !q->rb_issued) keep.push_back(w);
+        }
+        c.deferred.swap(keep);
+    }
+}
+
+// The D2H copy of a readable slot is issued when the host first reads it, on the side stream and
+// ordered after the slot's producer only (a speculated later launch is not waited for).  It covers,
+// in one copy per slab, every pending readable slot produced up to this one -- or all pending ones
+// when the newest producer has already finished (the end of a fixed-count loop reads its deltas in
+// one copy) -- so a scalar produced each sweep costs one event record at launch and nothing more
+// unless it is read.
 void issue_readback(Ctx &c, Slot &s) {
     if (s.rb_issued) return;
-    NBG_CUDA(cudaEventRecord(c.rb_dep, c.stream));
-    NBG_CUDA(cudaStreamWaitEvent(c.rb_stream, c.rb_dep, 0));
-    NBG_CUDA(cudaMemcpyAsync(s.hptr(), s.dptr(), SLOT_U64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.rb_stream));
-    if (!s.ev) s.ev = get_event(c);
-    NBG_CUDA(cudaEventRecord(s.ev, c.rb_stream));
-    s.rb_issued = true;
+    if (!s.pev) {
+        NBG_CUDA(cudaEventRecord(c.rb_dep, c.stream));
+        NBG_CUDA(cudaStreamWaitEvent(c.rb_stream, c.rb_dep, 0));
+        NBG_CUDA(cudaMemcpyAsync(s.hptr(), s.dptr(), SLOT_U64 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.rb_stream));
+        if (!s.ev) s.ev = get_event(c);
+        NBG_CUDA(cudaEventRecord(s.ev, c.rb_stream));
+        s.rb_issued = true;
+        return;
+    }
+    SlotP newest;
+    for (auto it = c.deferred.rbegin(); it != c.deferred.rend() && !newest; ++it) {
+        auto q = it->lock();
+        if (q && !q->rb_issued && q->pev) newest = q;
+    }
+    const bool all = newest && newest.get() != &s && cudaEventQuery(newest->pev->e) == cudaSuccess;
+    std::vector<SlotP> set;
+    for (auto &w : c.deferred) {
+        auto q = w.lock();
+        if (!q || q->rb_issued || !q->pev) continue;
+        set.push_back(q);
+        if (!all && q.get() == &s) break;
+    }
+    if (set.empty() || (!all && set.back().get() != &s)) fail(NBG_PANIC, "readback: slot not in the deferred list");
+    NBG_CUDA(cudaStreamWaitEvent(c.rb_stream, set.back()->pev->e, 0));
+    std::map<Slab *, std::pair<int, int>> rng;   // per slab: lowest and highest slot index
+    for (const SlotP &q : set) {
+        auto it = rng.find(q->slab.get());
+        if (it == rng.end()) rng[q->slab.get()] = {q->idx, q->idx};
+        else it->second = {std::min(it->second.first, q->idx), std::max(it->second.second, q->idx)};
+    }
+    for (auto &kv : rng) {
+        const size_t off = (size_t)kv.second.first * SLOT_U64, cnt = (size_t)(kv.second.second - kv.second.first + 1) * SLOT_U64;
+        NBG_CUDA(cudaMemcpyAsync(kv.first->h + off, kv.first->d + off, cnt * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 c.rb_stream));
+    }
+    auto ce = std::make_shared<ProdEv>();
+    ce->ctx = &c;
+    ce->e = get_event(c);
+    NBG_CUDA(cudaEventRecord(ce->e, c.rb_stream));
+    for (const SlotP &q : set) {
+        q->cev = ce;
+        q->rb_issued = true;
+        q->pev.reset();
+    }
+    while (!c.deferred.empty()) {
+        auto f = c.deferred.front().lock();
+        if (f && !f->rb_issued) break;
+        c.deferred.pop_front();
+    }
 }
 
 // ---------------------------------------------------------------- exact accumulator decode (host)

@@ -544,7 +544,7 @@ void materialize_structured(Ctx &c, const NodeP &r) {
         r->mat = true;
         r->slot = slot;
         r->sfmt = (SFmt)p.reds[0].fmt;
-        if (r->user_refs > 0) issue_readback(c, *slot);
+        if (r->user_refs > 0) mark_readable(c, slot, record_prod_event(c));
     }
     c.stats.intermediates_elided += B.visited.size() > 0 ? B.visited.size() - (vec_out ? 1 : 0) : 0;
     drop(*r);

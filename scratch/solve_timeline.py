@@ -6,9 +6,13 @@ from paper_2509_14211_b200 import nbg
 torch.cuda.set_device(0)
 st = torch.cuda.current_stream()
 c = nbg.nbg_init(nbg.NONBLOCKING, 0, st.cuda_stream)
-A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 22, 16, 1)
+import os
+SC = int(os.environ.get('SCALE', '22')); EF = int(os.environ.get('EF', '16'))
+A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, SC, EF, 1)
+TT = nbg.FP64 if os.environ.get('T') == 'fp64' else nbg.FP32
+KW = dict(tol=-1.0, itermax=20) if os.environ.get('FIXED') else dict(tol=1e-6, itermax=100)
 def solve():
-    r, s, h = nbg.nbg_pagerank(c, A, deg, tol=1e-6, itermax=100); nbg.nbg_vector_free(c, r)
+    r, s, h = nbg.nbg_pagerank(c, A, deg, type=TT, **KW); nbg.nbg_vector_free(c, r)
 for _ in range(3): solve()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
