@@ -120,15 +120,25 @@ def algorithmic_bytes(n, nnz, w):
     return b_ns, b_ns + 3 * w * n
 
 
-def load_traffic(workload):
+def load_ncu(workload):
+    """profiles/ncu_summary.json entry of a workload (one `ncu --set full` capture of its sweep
+    kernel): DRAM bytes and L2 sectors per launch, or {}."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
-        return None
+        return {}
     try:
-        d = json.load(open(p))
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        return json.load(open(p)).get(workload, {})
     except Exception:
-        return None
+        return {}
+
+
+def load_traffic(workload):
+    return load_ncu(workload).get("dram_bytes_per_launch")
+
+
+# L2 (LTS) random-sector throughput measured in round 1 (DESIGN.md section 7: 387 G sectors/s,
+# the microarchitecture notes' ~6300 B/clk cap at 1965 MHz): the ceiling of an L2-resident sweep
+L2_SECTORS_PEAK = 387e9
 
 
 # ------------------------------------------------------------------ our arm
@@ -334,6 +344,17 @@ def run_ours(args, rank, world, local_rank):
                 "sweep_kernels": "two-phase (phase 1 %.1f us + phase 2 %.1f us)" % (spmv_ms / spmv_n * 1e3, p2_ms / p2_n * 1e3)
                                  if p2_n else "single-pass",
                 "share_of_step": round((spmv_ms + p2_ms) / ms_instr, 4) if ms_instr else None,
+                **({"l2": {"bound_note": "L2-resident gathered vector and index stream: L2 sectors, not HBM bytes, bound "
+                                         "this sweep" if "stays L2-resident" in l2_note(nnz, ncols_g * w) and
+                                         load_ncu(args.workload).get("dram_bytes_per_launch", 1e30) < 0.5 * b_ns
+                                         else "L2 sectors of the same launch, for comparison",
+                          "sectors_per_launch": load_ncu(args.workload)["lts_sectors_per_launch"],
+                          "achieved_gsectors_s": round(load_ncu(args.workload)["lts_sectors_per_launch"] / avg_spmv_s / 1e9, 1),
+                          "peak_gsectors_s": L2_SECTORS_PEAK / 1e9,
+                          "frac": round(load_ncu(args.workload)["lts_sectors_per_launch"] / avg_spmv_s / L2_SECTORS_PEAK, 4),
+                          "source": "sectors: ncu lts__t_sectors.sum of one sweep launch (profiles/ncu_summary.json); "
+                                    "peak: measured random-sector throughput (DESIGN.md section 7)"}}
+                   if (not args.mtx and "lts_sectors_per_launch" in load_ncu(args.workload)) else {}),
                 "timing_pass": "kernel durations from an instrumented pass of the same K steps right before the "
                                "value's pass (per-launch CUDA events on the library stream); "
                                "ms_per_step with events %.4f" % (ms_instr / args.steps),

@@ -193,17 +193,25 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
         // against libcuda.
         using LaunchFn = CUresult (*)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, CUstream,
                                       void **, void **);
-        static LaunchFn drv = [] {
+        using GetFn = CUresult (*)(CUfunction *, CUkernel);
+        auto entry = [](const char *sym) -> void * {
             void *f = nullptr;
             cudaDriverEntryPointQueryResult q;
-            if (cudaGetDriverEntryPoint("cuLaunchKernel", &f, cudaEnableDefault, &q) != cudaSuccess ||
-                q != cudaDriverEntryPointSuccess)
-                f = nullptr;
-            return (LaunchFn)f;
-        }();
+            if (cudaGetDriverEntryPoint(sym, &f, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) f = nullptr;
+            return f;
+        };
+        static LaunchFn drv = (LaunchFn)entry("cuLaunchKernel");
+        static GetFn getfn = (GetFn)entry("cuKernelGetFunction");
+        Kernel &km = const_cast<Kernel &>(k);
+        if (!km.fn && getfn) {   // the kernel's function in the current context, once per kernel
+            CUfunction f = nullptr;
+            if (getfn(&f, (CUkernel)(void *)k.k) == CUDA_SUCCESS) km.fn = (void *)f;
+        }
         if (drv) {
-            const CUresult r = drv((CUfunction)(void *)k.k, (unsigned)g, 1, 1, (unsigned)k.block, 1, 1, (unsigned)k.smem,
-                                   (CUstream)c.stream, params, nullptr);
+            plan_prof_t0();
+            const CUresult r = drv(km.fn ? (CUfunction)km.fn : (CUfunction)(void *)k.k, (unsigned)g, 1, 1, (unsigned)k.block, 1, 1,
+                                   (unsigned)k.smem, (CUstream)c.stream, params, nullptr);
+            plan_prof_t1(8);
             if (r != CUDA_SUCCESS) fail(NBG_PANIC, "cuLaunchKernel failed (" + std::to_string((int)r) + ") for " + k.name);
         } else {
             NBG_CUDA(cudaLaunchKernel((const void *)k.k, dim3((unsigned)g), dim3((unsigned)k.block), params, (size_t)k.smem,

@@ -314,6 +314,7 @@ struct Kernel {
     ~Kernel();
     cudaLibrary_t lib = nullptr;
     cudaKernel_t k = nullptr;
+    void *fn = nullptr;      // CUfunction of k in the context's device (driver launch), resolved once
     int block = 256;
     int smem = 0;            // dynamic shared memory per CTA
     int hot = 0;             // spmv: capacity of the hot-column cache (entries)
@@ -524,6 +525,8 @@ double host_binop(int code, int t, double x, double y, double c0);
 double host_round(int t, double v);
 double monoid_identity(int monoid, int type);   // identity of PLUS / MIN / MAX in type
 uint64_t hash_str(const std::string &s);
+void plan_prof_t0();          // NBG_PLAN_PROFILE probes (planner.cpp)
+void plan_prof_t1(int phase);
 
 double now_ns();
 

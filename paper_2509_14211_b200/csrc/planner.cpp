@@ -33,18 +33,28 @@ namespace nbg {
 
 // host-side phase profile of the planner (NBG_PLAN_PROFILE=1: printed at exit)
 struct PlanProf {
-    double t[8] = {0};
-    long long n[8] = {0};
+    double t[10] = {0};
+    long long n[10] = {0};
     bool on = false;
     PlanProf() { const char *e = getenv("NBG_PLAN_PROFILE"); on = e && e[0] == '1'; }
     ~PlanProf() {
         if (!on) return;
-        const char *nm[8] = {"purge+bind", "region", "hints", "keys", "run:sig+plan", "run:args+launch", "memo_insert", "total"};
-        for (int i = 0; i < 8; i++)
+        const char *nm[10] = {"purge+bind", "region", "hints", "keys", "run:sig+plan", "run:args+launch", "memo_insert", "total",
+                              "  launch call", "  readable mark"};
+        for (int i = 0; i < 10; i++)
             if (n[i]) fprintf(stderr, "[nbg plan] %-16s %10.2f us/call  (%lld calls)\n", nm[i], t[i] / 1e3 / n[i], n[i]);
     }
 };
-static PlanProf g_prof;
+PlanProf g_prof;
+static thread_local double g_pp_t0 = 0.0;
+void plan_prof_t0() {
+    if (g_prof.on) g_pp_t0 = now_ns();
+}
+void plan_prof_t1(int k) {
+    if (!g_prof.on) return;
+    const double d = now_ns() - g_pp_t0;
+    if (d < 500e3) { g_prof.t[k] += d; g_prof.n[k]++; }
+}
 struct PTimer {
     int k;
     double t0;
@@ -800,6 +810,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         x.kind = VKind::FULL;
         x.mat = true;
     }
+    PTimer pt_rm(9);
     ProdEvP pe;
     for (int k = 0; k < p.n_red; k++) {
         Node &x = *B.red_nodes[k];
