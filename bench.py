@@ -284,7 +284,10 @@ def run_ours(args, rank, world, local_rank):
             nbg.nbg_matrix_free(ctx, A2)
             return s
 
-        e2e_step()
+        # warm-up: the second solve on a fresh matrix still compiles the dinv region with the side
+        # outputs learned on the first (one NVRTC compile, cached from then on)
+        for _ in range(max(2, args.warmup)):
+            e2e_step()
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
