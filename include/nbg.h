@@ -338,9 +338,16 @@ nbg_status nbg_convert(nbg_ctx *ctx, nbg_vector *w, int type, nbg_vector u);    
  * output); A.ncols must equal len(u) (Fig. 3, Fig. 6). */
 nbg_status nbg_mxv(nbg_ctx *ctx, nbg_vector *w, int type, nbg_semiring sr, nbg_matrix A, nbg_vector u);
 
-/* s = add-fold of u's stored values (identity if empty) (Fig. 6).  Floating PLUS is
- * accumulated in fp64 per thread block and combined EXACTLY across blocks (order-independent
- * fixed-point limbs), so the value is deterministic; |terms| must be < 2^127. */
+/* s = add-fold of u's stored values (identity if empty) (Fig. 6).  Floating PLUS:
+ *   - fp64 terms (a reduction of an fp64 vector, or over fp64 values of a fused region): every
+ *     term is added EXACTLY (per-thread 128-bit fixed-point accumulators flushed into the block's
+ *     limbs, limbs combined across blocks by integer atomics), so s is the exact sum of the terms
+ *     rounded once to fp64 -- independent of grouping, block count and rank count (P9);
+ *   - fp32 terms (and the per-row / per-task partials of a fused SpMV epilogue) are accumulated in
+ *     fp64 in a fixed order per thread / task, and those fp64 partials are combined exactly.
+ * Terms outside the exact window [2^-160, 2^128) are summed in fp64 on the side (slot word 12),
+ * in arrival order -- the one non-deterministic case (see NBG_FLAG_DETERMINISTIC); NaN / +inf /
+ * -inf terms are counted and decide the result (NaN, or inf of one sign). */
 nbg_status nbg_reduce(nbg_ctx *ctx, nbg_scalar *s, int type, int monoid, nbg_vector u);
 
 /* s_out = op(s_in) evaluated in `type` (a scalar node of the DAG, e.g. the dangling constant). */
