@@ -163,8 +163,17 @@ nbg_status nbg_finalize(nbg_ctx *ctx);
 nbg_status nbg_last_error(nbg_ctx *ctx, char *buf, size_t len);
 
 /* Block until all work of the context has finished (its stream and the scalar-readback side
- * stream); returns a latched execution error if one occurred. */
+ * stream); returns a latched execution error if one occurred.  With NBG_GUARD=1 in the
+ * environment it also checks the red zones of all live buffers (see nbg_guard_selftest). */
 nbg_status nbg_sync(nbg_ctx *ctx);
+
+/* Guard mode (test instrument; compute-sanitizer is unavailable on the GPU pool): with NBG_GUARD=1
+ * every pool buffer carries a 256-byte red zone after its end, checked on the device after every
+ * generated-kernel launch, at the end of every wait and when the buffer is freed; an overwritten
+ * zone fails the call with NBG_PANIC ("guard: ...").  This entry point writes one byte past the end
+ * of a fresh 1000-byte buffer and runs the check: NBG_PANIC when guard mode is on and detects it,
+ * NBG_NOT_IMPLEMENTED when NBG_GUARD is not set. */
+nbg_status nbg_guard_selftest(nbg_ctx *ctx);
 
 /* Planner / executor counters (SPEC.md:338-341 cache counters; PAPER.md:301-306 wait steps). */
 typedef struct {

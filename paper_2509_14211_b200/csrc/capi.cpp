@@ -324,11 +324,32 @@ nbg_status nbg_last_error(nbg_ctx *ctx, char *buf, size_t len) {
     return NBG_SUCCESS;
 }
 
+nbg_status nbg_guard_selftest(nbg_ctx *ctx) {
+    API_BEGIN
+    check_ctx(ctx);
+    if (!guard_enabled()) return NBG_NOT_IMPLEMENTED;
+    BufP b = alloc_buf(*ctx, 1000);
+    NBG_CUDA(cudaMemsetAsync((char *)b->d + 1000, 0, 1, ctx->stream));   // one byte past the end
+    std::string err;
+    try {
+        guard_check(*ctx, "nbg_guard_selftest");
+    } catch (const Error &e) {
+        err = e.msg;
+    }
+    // repair the zone so the buffer's release does not report it again (the context stays usable)
+    NBG_CUDA(cudaMemsetAsync((char *)b->d + 1000, 0xA5, 1, ctx->stream));
+    if (err.empty()) return NBG_SUCCESS;   // not detected: the caller's test fails on this status
+    ctx->last_error = err;
+    return NBG_PANIC;
+    API_END(ctx)
+}
+
 nbg_status nbg_sync(nbg_ctx *ctx) {
     API_BEGIN
     check_ctx(ctx);
     NBG_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctx->rb_stream) NBG_CUDA(cudaStreamSynchronize(ctx->rb_stream));   // scalar readbacks (side stream)
+    guard_check(*ctx, "nbg_sync");
     if (ctx->latched != NBG_SUCCESS) return ctx->latched;
     API_END(ctx)
 }

@@ -1035,6 +1035,33 @@ void gpu_rebase_rowptr(Ctx &c, long long n, const long long *rp, long long base,
     c.stats.kernels_launched++;
 }
 
+// NBG_GUARD=1 red-zone scan: block z checks zone z (bytes of 0xA5); the lowest bad zone index wins
+__global__ void k_guard_scan(const unsigned char *const *zones, int nz, int bytes, int *bad) {
+    for (int z = blockIdx.x; z < nz; z += gridDim.x)
+        for (int i = threadIdx.x; i < bytes; i += blockDim.x)
+            if (zones[z][i] != 0xA5) atomicMin(bad, z);
+}
+
+int gpu_guard_scan(Ctx &c, const unsigned char *const *zones, int nzones, size_t bytes) {
+    if (nzones <= 0) return -1;
+    // raw allocations: the scratch of the check must not register red zones of its own
+    void *dz = nullptr;
+    int *dbad = nullptr;
+    NBG_CUDA(cudaMallocAsync(&dz, (size_t)nzones * sizeof(void *), c.stream));
+    NBG_CUDA(cudaMallocAsync((void **)&dbad, sizeof(int), c.stream));
+    const int init = 0x7fffffff;
+    NBG_CUDA(cudaMemcpyAsync(dz, zones, (size_t)nzones * sizeof(void *), cudaMemcpyHostToDevice, c.stream));
+    NBG_CUDA(cudaMemcpyAsync(dbad, &init, sizeof(int), cudaMemcpyHostToDevice, c.stream));
+    k_guard_scan<<<std::min(nzones, 4 * c.num_sms), 256, 0, c.stream>>>((const unsigned char *const *)dz, nzones, (int)bytes, dbad);
+    NBG_CUDA(cudaGetLastError());
+    int bad = init;
+    NBG_CUDA(cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaFreeAsync(dz, c.stream));
+    NBG_CUDA(cudaFreeAsync(dbad, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    return bad == init ? -1 : bad;
+}
+
 void gpu_l2_touch(Ctx &c, const void *base, size_t bytes, const cudaLaunchAttribute *attr) {
     const long long n16 = (long long)(bytes / 16);
     if (n16 <= 0) return;

@@ -220,6 +220,7 @@ void launch(Ctx &c, const Kernel &k, const KArgs &args, long long work_items, co
     }
     timing_end(c, cls, ev0);
     c.stats.kernels_launched++;
+    if (guard_enabled()) guard_check(c, k.name.c_str());
     static int dbg_sync = -1;
     if (dbg_sync < 0) dbg_sync = (getenv("NBG_SYNC_DEBUG") && *getenv("NBG_SYNC_DEBUG")) ? 1 : 0;
     if (dbg_sync) {

@@ -376,6 +376,8 @@ struct Ctx {
     SlabP cur_slab;
     std::vector<cudaEvent_t> event_pool;
     std::vector<cudaEvent_t> timing_pool;   // recycled timing events (nbg_set_timing)
+    std::map<void *, size_t> guard_live;   // NBG_GUARD=1: live pool buffers (red zone after each)
+    std::string guard_msg;                  // a red-zone violation found at free
     std::deque<std::weak_ptr<Slot>> deferred;   // readable slots not yet copied, in production order
     cudaStream_t rb_stream = nullptr;      // scalar readbacks (issue_readback), ordered after the producer
     cudaEvent_t rb_dep = nullptr;
@@ -525,6 +527,9 @@ double host_binop(int code, int t, double x, double y, double c0);
 double host_round(int t, double v);
 double monoid_identity(int monoid, int type);   // identity of PLUS / MIN / MAX in type
 uint64_t hash_str(const std::string &s);
+bool guard_enabled();                   // NBG_GUARD=1 (runtime.cpp)
+void guard_check(Ctx &c, const char *where);
+int gpu_guard_scan(Ctx &c, const unsigned char *const *zones, int nzones, size_t bytes);   // graph.cu: first bad zone or -1
 void plan_prof_t0();          // NBG_PLAN_PROFILE probes (planner.cpp)
 void plan_prof_t1(int phase);
 

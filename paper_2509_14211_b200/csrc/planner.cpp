@@ -988,6 +988,7 @@ void materialize(Ctx &c, const std::vector<NodeP> &roots_in) {
     for (const NodeP &r : roots) groups[root_len(r)].push_back(r);
     for (auto &g : groups) materialize_group(c, g.second, g.first);
     c.stats.host_plan_ns += (uint64_t)(now_ns() - t0);
+    if (guard_enabled()) guard_check(c, "materialize (static kernels included)");
 }
 
 double scalar_read(Ctx &c, const NodeP &s) {

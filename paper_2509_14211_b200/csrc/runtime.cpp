@@ -41,8 +41,50 @@ static bool pool_enabled() {
     return v == 1;
 }
 
+// ---------------------------------------------------------------- guard mode (NBG_GUARD=1)
+// compute-sanitizer is closed on the GPU pool, so out-of-bounds WRITES are caught by red zones:
+// every pool buffer gets GUARD_BYTES of 0xA5 after its end; after every generated-kernel launch and
+// every materialisation the red zones of all live buffers are checked on the device (one kernel),
+// and a buffer's zone is checked again when it is freed.  Test-only (synchronises every launch).
+static constexpr size_t GUARD_BYTES = 256;
+bool guard_enabled() {
+    static int v = -1;
+    if (v < 0) { const char *e = getenv("NBG_GUARD"); v = (e && e[0] == '1') ? 1 : 0; }
+    return v == 1;
+}
+
+void guard_check(Ctx &c, const char *where) {
+    if (!guard_enabled()) return;
+    if (!c.guard_msg.empty()) fail(NBG_PANIC, c.guard_msg);
+    if (c.guard_live.empty()) return;
+    std::vector<const unsigned char *> zones;
+    zones.reserve(c.guard_live.size());
+    for (auto &kv : c.guard_live) zones.push_back((const unsigned char *)kv.first + kv.second);
+    const int bad = gpu_guard_scan(c, zones.data(), (int)zones.size(), GUARD_BYTES);
+    if (bad >= 0) {
+        char msg[256];
+        auto it = c.guard_live.begin();
+        std::advance(it, bad);
+        snprintf(msg, sizeof msg, "guard: red zone after a %zu-byte buffer at %p overwritten (detected after %s)", it->second,
+                 it->first, where);
+        fail(NBG_PANIC, msg);
+    }
+}
+
 Buf::~Buf() {
     if (!(owned && d && ctx)) return;
+    if (guard_enabled() && bytes) {
+        if (ctx->guard_live.count(d) && !ctx->closing) {
+            const unsigned char *z = (const unsigned char *)d + bytes;
+            if (gpu_guard_scan(*ctx, &z, 1, GUARD_BYTES) >= 0) {   // reported by the next guard_check
+                char msg[160];
+                snprintf(msg, sizeof msg, "guard: red zone after a %zu-byte buffer overwritten (detected at free)", bytes);
+                fprintf(stderr, "[nbg] %s\n", msg);
+                if (ctx->guard_msg.empty()) ctx->guard_msg = msg;
+            }
+        }
+        ctx->guard_live.erase(d);
+    }
     if (pool_enabled() && !ctx->closing && bytes <= POOL_MAX_BUF && ctx->pooled_bytes + bytes <= POOL_MAX_TOTAL) {
         ctx->buf_pool[bytes].push_back(d);
         ctx->pooled_bytes += bytes;
@@ -64,7 +106,11 @@ BufP alloc_buf(Ctx &c, size_t bytes) {
             it->second.pop_back();
             c.pooled_bytes -= bytes;
         } else {
-            NBG_CUDA(cudaMallocAsync(&b->d, bytes, c.stream));
+            NBG_CUDA(cudaMallocAsync(&b->d, bytes + (guard_enabled() ? GUARD_BYTES : 0), c.stream));
+        }
+        if (guard_enabled()) {
+            NBG_CUDA(cudaMemsetAsync((char *)b->d + bytes, 0xA5, GUARD_BYTES, c.stream));
+            c.guard_live[b->d] = bytes;
         }
     }
     return b;

@@ -155,6 +155,7 @@ SIGNATURES = {
     "nbg_dist_exchange_plan": [vp, ctypes.c_int, i64, vp, vp],
     "nbg_dist_init_loopback": [vp, ctypes.c_int],
     "nbg_dist_set_exchange": [vp, ctypes.c_int],
+    "nbg_guard_selftest": [vp],
     "nbg_dist_graph_from_generator": [vp, ctypes.POINTER(nbg_graphgen), i64, pvp, pvp, vp, vp],
     "nbg_vector_allgather_reduce": [vp, pvp, vp, vp, i64, ctypes.c_int, vp, vp],
 }
@@ -585,6 +586,11 @@ def nbg_scalar_export_slot(ctx, s):
 def nbg_dist_init_loopback(ctxs):
     arr = (ctypes.c_void_p * len(ctxs))(*[c.value if isinstance(c, ctypes.c_void_p) else c for c in ctxs])
     _call(None, "nbg_dist_init_loopback", ctypes.cast(arr, ctypes.c_void_p), len(ctxs))
+
+
+def nbg_guard_selftest(ctx):
+    """include/nbg.h nbg_guard_selftest (NBG_GUARD=1 red-zone check of an intentional overflow)."""
+    _call(ctx, "nbg_guard_selftest", ctx)
 
 
 def nbg_dist_set_exchange(ctx, mode):
