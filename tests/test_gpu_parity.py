@@ -629,3 +629,36 @@ def test_fp64_plus_reduce_is_the_exactly_rounded_sum(nbg, mode):
             assert nbg.nbg_scalar_get(c, s2) == math.fsum(np.abs(v)), n
     finally:
         nbg.nbg_finalize(c)
+
+
+def test_deferred_scalar_readbacks_any_order(nbg):
+    """Scalar readbacks are deferred to the first host read and copied in bulk (runtime.cpp
+    issue_readback): many held reductions read in reverse, interleaved with new launches, with
+    freed neighbours in the same slab and more than the deferred list's compaction threshold --
+    every value is its own exactly rounded sum (math.fsum), whatever order the copies happen in."""
+    import math
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        rng = np.random.default_rng(5)
+        vecs = [np.ldexp(rng.standard_normal(1000 + 37 * k), rng.integers(-20, 20, 1000 + 37 * k)) for k in range(300)]
+        held, expect = [], []
+        for k, v in enumerate(vecs):
+            u = nbg.nbg_vector_from_dense(c, nbg.FP64, v)
+            s = nbg.nbg_reduce(c, nbg.FP64, nbg.PLUS, u)
+            nbg.nbg_scalar_wait(c, s)                       # materialised: marked readable, not copied
+            nbg.nbg_vector_free(c, u)
+            if k % 3 == 2:
+                nbg.nbg_scalar_free(c, s)                   # a freed neighbour inside the copied range
+                continue
+            held.append(s)
+            expect.append(math.fsum(v))
+            if k % 50 == 49:                                # read a middle one while later ones exist
+                j = len(held) // 2
+                assert nbg.nbg_scalar_get(c, held[j]) == expect[j]
+        for s, e in reversed(list(zip(held, expect))):
+            assert nbg.nbg_scalar_get(c, s) == e
+        for s, e in zip(held, expect):                      # second reads hit the copied mirror
+            assert nbg.nbg_scalar_get(c, s) == e
+            nbg.nbg_scalar_free(c, s)
+    finally:
+        nbg.nbg_finalize(c)
