@@ -75,6 +75,7 @@ template <class S>
 static void sig_emit(const Prog &p, S &s) {
     s.ch(p.spmv ? (p.tp ? 'T' : (p.lpr ? 'L' : 'S')) : 'E');
     s.ch(p.vec ? 'v' : 's');
+    s.ch(p.tma ? 'T' : 'n');
     s.put(p.nt, ',');
     s.put(p.hot_kb, '|');
     if (p.spmv) {
@@ -424,7 +425,7 @@ std::string vstore(int t, const std::string &ptr, const std::string &vi, const s
     return s.str();
 }
 
-void gen_ewise(Gen &g, const std::string &kname, bool vec) {
+int gen_ewise(Gen &g, const std::string &kname, bool vec) {
     const Prog &p = g.p;
     auto &o = g.o;
     // which slots are loaded, with their types
@@ -444,13 +445,86 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     o << "  const long long n = a.n;\n";
     o << "  const long long stride = (long long)gridDim.x * blockDim.x;\n";
     o << "  long long tail0 = 0;\n";
+    int smem = 0;
+    long long v0 = 0;   // first vector index of the register skeleton (after the TMA tiles)
+    (void)v0;
+    if (vec && p.tma) {
+        // TMA skeleton: the CTA's tiles of TV 4-element vectors of every loaded input are staged
+        // in shared memory by bulk copies, NST stages deep (one thread arms each stage's mbarrier
+        // with the byte count; the copies complete on it); all threads compute from shared memory.
+        // Bytes in flight per SM no longer depend on registers per thread.  Whole tiles only; the
+        // rest goes through the register skeleton below.
+        int sumsz = 0;
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0) sumsz += (int)type_size(slot_type[s2]);
+        const int TV = sumsz <= 8 ? 512 : 256, NST = 4;
+        std::vector<int> off(p.n_in, -1);
+        int stage_bytes = 0;
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0) { off[s2] = stage_bytes; stage_bytes += TV * 4 * (int)type_size(slot_type[s2]); }
+        smem = NST * stage_bytes;
+        o << "  extern __shared__ __align__(128) unsigned char nbg_dyn[];\n";
+        o << "  __shared__ __align__(8) u64 nbg_full[" << NST << "];\n";
+        o << "  const long long ntile = (n >> 2) / " << TV << ";\n";
+        o << "  if (threadIdx.x == 0) {\n";
+        o << "    for (int s_ = 0; s_ < " << NST << "; s_++) nbg_mbar_init(&nbg_full[s_], 1);\n";
+        o << "    nbg_fence_proxy_async();\n";
+        o << "  }\n";
+        o << "  __syncthreads();\n";
+        // issue tile t into stage s_
+        o << "  auto nbg_issue = [&](int s_, long long t_) {\n";
+        o << "    nbg_mbar_expect_tx(&nbg_full[s_], " << stage_bytes << "u);\n";
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0) {
+                const int bytes = TV * 4 * (int)type_size(slot_type[s2]);
+                o << "    nbg_bulk_g2s(nbg_dyn + s_ * " << stage_bytes << " + " << off[s2] << ", (const unsigned char*)a.in[" << s2 << "] + t_ * "
+                  << bytes << "ll, " << bytes << "u, &nbg_full[s_]);\n";
+            }
+        o << "  };\n";
+        o << "  if (threadIdx.x == 0)\n";
+        o << "    for (int s_ = 0; s_ < " << NST << "; s_++) { const long long t_ = blockIdx.x + (long long)s_ * gridDim.x; if (t_ < ntile) nbg_issue(s_, t_); }\n";
+        o << "  int it_ = 0;\n";
+        o << "  for (long long t_ = blockIdx.x; t_ < ntile; t_ += gridDim.x, it_++) {\n";
+        o << "    const int s_ = it_ % " << NST << ";\n";
+        o << "    nbg_mbar_wait(&nbg_full[s_], (unsigned)((it_ / " << NST << ") & 1));\n";
+        o << "    for (int u_ = threadIdx.x; u_ < " << TV << "; u_ += blockDim.x) {\n";
+        o << "      const long long vi = t_ * " << TV << " + u_;\n";
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0) {
+                const std::string T = ctype(slot_type[s2]);
+                o << "      " << T << " L" << s2 << "[4];\n";
+                o << "      { const " << T << " *q_ = (const " << T << "*)(nbg_dyn + s_ * " << stage_bytes << " + " << off[s2]
+                  << ") + 4 * u_; L" << s2 << "[0] = q_[0]; L" << s2 << "[1] = q_[1]; L" << s2 << "[2] = q_[2]; L" << s2 << "[3] = q_[3]; }\n";
+            }
+        for (int k = 0; k < p.n_out; k++)
+            if (out_type[k] >= 0) o << "      " << ctype(out_type[k]) << " O" << k << "[4];\n";
+        o << "      #pragma unroll\n      for (int e = 0; e < 4; e++) {\n";
+        g.emit_body(
+            "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
+            [&](const OutV &ov) {
+                if (ov.scatter) return g.scat(ov, "(vi * 4 + e)");
+                return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
+            },
+            [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
+        o << "      }\n";
+        for (int k = 0; k < p.n_out; k++)
+            if (out_type[k] >= 0) o << "      " << vstore(out_type[k], "a.out[" + std::to_string(k) + "]", "vi", "O" + std::to_string(k)) << "\n";
+        o << "    }\n";
+        // every thread is done with stage s_: refill it (generic-proxy reads before async-proxy writes)
+        o << "    __syncthreads();\n";
+        o << "    if (threadIdx.x == 0) { const long long t2_ = t_ + (long long)" << NST << " * gridDim.x; if (t2_ < ntile) { nbg_fence_proxy_async(); nbg_issue(s_, t2_); } }\n";
+        o << "  }\n";
+        o << "  const long long vstart_ = ntile * " << TV << ";\n";
+    } else {
+        o << "  const long long vstart_ = 0;\n";
+    }
     if (vec) {
         // 4 grid-stride iterations per trip: all 16-byte loads of the trip are issued before any
         // use, so every thread keeps 4 loads per input in flight (memory-level parallelism)
         o << "  const long long nv = n >> 2;\n  tail0 = nv << 2;\n";
         const char *eu = getenv("NBG_EWISE_UNROLL");
         const int U = (eu && (eu[0] == '1' || eu[0] == '2' || eu[0] == '4' || eu[0] == '8')) ? eu[0] - '0' : 1;
-        o << "  for (long long vb_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv; vb_ += " << U << " * stride) {\n";
+        o << "  for (long long vb_ = vstart_ + (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv; vb_ += " << U << " * stride) {\n";
         for (int s = 0; s < p.n_in; s++)
             if (slot_type[s] >= 0) o << "    " << ctype(slot_type[s]) << " L" << s << "[" << U << "][4];\n";
         o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
@@ -489,6 +563,7 @@ void gen_ewise(Gen &g, const std::string &kname, bool vec) {
     o << "  }\n";
     g.emit_red_finish();
     o << "}\n";
+    return smem;
 }
 
 static int redkind(const Gen &g, const RedOut &r) { return g.redkind(r).kind; }
@@ -1505,7 +1580,7 @@ std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem, int 
     else if (p.spmv)
         smem = gen_spmv(g, kname, hot_entries);
     else
-        gen_ewise(g, kname, p.vec);
+        smem = gen_ewise(g, kname, p.vec);
     if (dyn_smem) *dyn_smem = smem;
     return g.o.str();
 }

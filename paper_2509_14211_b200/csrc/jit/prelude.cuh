@@ -403,6 +403,27 @@ __device__ void nbg_block_finish_i(long long v, int kind, u64 *acc, double *sh) 
 // loads that bypass / hint the caches
 __device__ __forceinline__ int nbg_ld_stream(const int *p) { return __ldcs(p); }
 
+// ------------------------------------------------------------------ TMA bulk copies + mbarriers
+// (ewise TMA skeleton, codegen.cpp gen_ewise): one thread arms a stage's mbarrier with the byte
+// count and issues 1-D bulk copies global -> shared that complete on it; consumers wait on the
+// stage's phase parity.
+__device__ __forceinline__ unsigned nbg_smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void nbg_mbar_init(u64 *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(nbg_smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nbg_mbar_expect_tx(u64 *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(nbg_smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void nbg_mbar_wait(u64 *bar, unsigned parity) {
+    asm volatile("{\n .reg .pred p_;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p_, [%0], %1;\n @!p_ bra W_%=;\n}"
+                 :: "r"(nbg_smem_addr(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void nbg_bulk_g2s(void *dst, const void *src, unsigned bytes, u64 *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(nbg_smem_addr(dst)), "l"(src), "r"(bytes), "r"(nbg_smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void nbg_fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // ------------------------------------------------------------------ SpMV gathers
 // x[c] from the shared-memory hot-column cache when c < hc, else from global memory cached in L2
 // only (ld.global.cg); both loads are predicated (no divergent branch per element).  The

@@ -267,6 +267,7 @@ struct Prog {
     bool lpr = false;       // spmv, lane-per-row skeleton (low-skew matrices)
     int nt = 0, hot_kb = 0; // spmv (task skeleton): threads per CTA and hot-cache KB, chosen per matrix
     bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
+    bool tma = false;       // ewise: inputs staged through shared memory by TMA bulk copies (large n)
     SpmvSig sp;
     int n_in = 0, n_out = 0, n_imm = 0, n_sin = 0, n_red = 0;
     std::string signature() const;
