@@ -109,27 +109,25 @@ __global__ void k_ngroups(long long n, const long long *rowptr, long long *ng) {
 // Each thread takes 16 consecutive entries (a warp: 512, so the src reads stay coalesced per
 // load): one binary search for the row of the first entry, then the row advances as the entries
 // cross row ends.
+// row of the first entry of every 16-entry chunk of the CSR (one thread per non-empty row writes
+// the chunks that start inside it); k_fill_groups starts each entry's row search there
+__global__ void k_chunk_rows(long long n, const long long *rowptr, int *crow) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long rs = rowptr[i], re = rowptr[i + 1];
+        if (rs == re) continue;
+        for (long long q = (rs + 15) >> 4; q <= (re - 1) >> 4; q++) crow[q] = (int)i;
+    }
+}
+
+// entry p of row r goes to group-padded position 4 grp[r] + (p - rowptr[r]); one thread per entry
+// (coalesced loads and, inside rows, coalesced stores), its row found from the chunk's first row
+// by a short forward walk (L1-resident rowptr)
 template <class T>
-__global__ void k_fill_groups(long long nnz, long long n, const long long *rowptr, const long long *grp, const T *src, T *dst) {
-    const long long nch = (nnz + 15) / 16;
-    for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < nch; q += (long long)gridDim.x * blockDim.x) {
-        const long long p0 = 16 * q;
-        long long lo = 0, hi = n;          // row = last i with rowptr[i] <= p0
-        while (hi - lo > 1) {
-            long long mid = (lo + hi) >> 1;
-            if (rowptr[mid] <= p0) lo = mid; else hi = mid;
-        }
-        long long rs = rowptr[lo], re = rowptr[lo + 1], g4 = 4 * grp[lo];
-        const long long p1 = p0 + 16 < nnz ? p0 + 16 : nnz;
-        for (long long p = p0; p < p1; p++) {
-            while (p >= re) {              // next non-empty row
-                lo++;
-                rs = re;
-                re = rowptr[lo + 1];
-                g4 = 4 * grp[lo];
-            }
-            dst[g4 + (p - rs)] = src[p];
-        }
+__global__ void k_fill_groups(long long nnz, const long long *rowptr, const long long *grp, const int *crow, const T *src, T *dst) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += (long long)gridDim.x * blockDim.x) {
+        long long r = crow[p >> 4];
+        while (rowptr[r + 1] <= p) r++;
+        dst[4 * grp[r] + (p - rowptr[r])] = src[p];
     }
 }
 
@@ -903,20 +901,24 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     }
     P->cg = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * 4);
     NBG_CUDA(cudaMemsetAsync(P->cg->d, 0xff, (size_t)std::max<long long>(4 * G, 4) * 4, c.stream));
-    if (A.nnz > 0)
-        k_fill_groups<int><<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, n, (const long long *)A.rowptr->d,
-                                                                             (const long long *)P->grp->d, (const int *)colsrc->d,
-                                                                             (int *)P->cg->d);
+    BufP crow = alloc_buf(c, (size_t)std::max<long long>((A.nnz + 15) / 16, 1) * 4);
+    if (A.nnz > 0) {
+        k_chunk_rows<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, (const long long *)A.rowptr->d, (int *)crow->d);
+        k_fill_groups<int><<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const long long *)A.rowptr->d,
+                                                                             (const long long *)P->grp->d, (const int *)crow->d,
+                                                                             (const int *)colsrc->d, (int *)P->cg->d);
+    }
     if (A.vals) {
         const size_t es = type_size(A.type);
         P->vals_g = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * es);
         NBG_CUDA(cudaMemsetAsync(P->vals_g->d, 0, (size_t)std::max<long long>(4 * G, 4) * es, c.stream));
         if (A.nnz > 0) {
             const long long *rp = (const long long *)A.rowptr->d, *gp = (const long long *)P->grp->d;
+            const int *cr = (const int *)crow->d;
             const int gr = grid_for(A.nnz, c.num_sms);
-            if (es == 1) k_fill_groups<unsigned char><<<gr, 256, 0, c.stream>>>(A.nnz, n, rp, gp, (const unsigned char *)A.vals->d, (unsigned char *)P->vals_g->d);
-            else if (es == 4) k_fill_groups<int><<<gr, 256, 0, c.stream>>>(A.nnz, n, rp, gp, (const int *)A.vals->d, (int *)P->vals_g->d);
-            else k_fill_groups<long long><<<gr, 256, 0, c.stream>>>(A.nnz, n, rp, gp, (const long long *)A.vals->d, (long long *)P->vals_g->d);
+            if (es == 1) k_fill_groups<unsigned char><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const unsigned char *)A.vals->d, (unsigned char *)P->vals_g->d);
+            else if (es == 4) k_fill_groups<int><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const int *)A.vals->d, (int *)P->vals_g->d);
+            else k_fill_groups<long long><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const long long *)A.vals->d, (long long *)P->vals_g->d);
         }
     }
     NBG_CUDA(cudaGetLastError());
