@@ -361,6 +361,15 @@ struct Dist {
     ~Dist();
 };
 
+// memo key: 128-bit hash of an expression's structural token stream (planner.cpp memo_key)
+struct MKey {
+    uint64_t a = 0, b = 0;
+    bool operator==(const MKey &o) const { return a == o.a && b == o.b; }
+};
+struct MKeyHash {
+    size_t operator()(const MKey &k) const { return (size_t)(k.a ^ (k.b * 0x9E3779B97F4A7C15ull)); }
+};
+
 struct Ctx {
     int mode = NBG_NONBLOCKING;
     int device = 0;
@@ -403,7 +412,7 @@ struct Ctx {
         uint64_t stamp = 0;      // last use (LRU bound)
     };
     uint64_t memo_clock = 0;
-    std::unordered_map<std::string, MemoEntry> memo;
+    std::unordered_map<MKey, MemoEntry, MKeyHash> memo;
     // learned hints: producer signature hash + output index -> templates
     std::map<std::pair<uint64_t, int>, std::vector<Hint>> hints;
 

@@ -112,64 +112,92 @@ struct SmallSet {
 
 // ---------------------------------------------------------------- structural keys
 
-static inline void kput(std::string &s, long long v) {
-    char buf[24];
-    auto r = std::to_chars(buf, buf + sizeof buf, v);
-    s.append(buf, r.ptr);
-}
-static inline void kbits(std::string &s, double v) {
-    uint64_t b;
-    memcpy(&b, &v, 8);
-    char buf[24];
-    auto r = std::to_chars(buf, buf + sizeof buf, (unsigned long long)b, 16);
-    s.append(buf, r.ptr);
-}
-static void key_rec(const Node *x, std::string &s, const Node *ph) {
-    if (x == ph) { s += 'P'; return; }
+// The key is a token stream over the expression (ops, types, sizes, operator codes and constants,
+// leaf identities); it is emitted into a sink: a string (hint templates, debug output) or a
+// 128-bit hash (the memo key, computed at every wait without building the string; two
+// independent 64-bit streams, so a collision needs both to collide).
+struct KStr {
+    std::string s;
+    void put(long long v) {
+        char buf[24];
+        auto r = std::to_chars(buf, buf + sizeof buf, v);
+        s.append(buf, r.ptr);
+    }
+    void bits(double v) {
+        uint64_t b;
+        memcpy(&b, &v, 8);
+        char buf[24];
+        auto r = std::to_chars(buf, buf + sizeof buf, (unsigned long long)b, 16);
+        s.append(buf, r.ptr);
+    }
+    void ch(char c) { s.push_back(c); }
+};
+struct KHash {
+    uint64_t a = 1469598103934665603ull, b = 0x9E3779B97F4A7C15ull;
+    void put(long long v) {
+        const uint64_t u = (uint64_t)v;
+        a = (a ^ u) * 1099511628211ull;
+        b = (b ^ (u + 0x632BE59BD9B4E019ull)) * 0xFF51AFD7ED558CCDull;
+        b ^= b >> 29;
+    }
+    void bits(double v) {
+        uint64_t u;
+        memcpy(&u, &v, 8);
+        put((long long)u);
+    }
+    void ch(char c) { put((long long)(unsigned char)c | (1ll << 40)); }
+    MKey key() const { return MKey{a, b}; }
+};
+template <class S>
+static void key_rec(const Node *x, S &s, const Node *ph) {
+    if (x == ph) { s.ch('P'); return; }
     if (x->mat) {
         if (x->scalar) {
-            if (x->sfmt == SFmt::HOST) { s += 'h'; kput(s, x->type); s += ':'; kbits(s, x->hval); }
-            else { s += 'd'; kput(s, x->type); s += ':'; kput(s, (long long)x->slot->id); }
-        } else if (x->kind == VKind::FULL) { s += 'F'; kput(s, (long long)x->buf->id); }
-        else if (x->kind == VKind::ISO) { s += 'I'; kput(s, x->type); s += ':'; kbits(s, x->iso); }
-        else if (x->kind == VKind::SPARSE) { s += 'S'; kput(s, (long long)x->buf->id); }
-        else if (x->kind == VKind::BITSET) { s += 'B'; kput(s, (long long)x->buf->id); }
-        else s += 'E';
+            if (x->sfmt == SFmt::HOST) { s.ch('h'); s.put(x->type); s.ch(':'); s.bits(x->hval); }
+            else { s.ch('d'); s.put(x->type); s.ch(':'); s.put((long long)x->slot->id); }
+        } else if (x->kind == VKind::FULL) { s.ch('F'); s.put((long long)x->buf->id); }
+        else if (x->kind == VKind::ISO) { s.ch('I'); s.put(x->type); s.ch(':'); s.bits(x->iso); }
+        else if (x->kind == VKind::SPARSE) { s.ch('S'); s.put((long long)x->buf->id); }
+        else if (x->kind == VKind::BITSET) { s.ch('B'); s.put((long long)x->buf->id); }
+        else s.ch('E');
         return;
     }
-    s += '(';
-    kput(s, (int)x->op); s += ',';
-    kput(s, x->type); s += ',';
-    kput(s, x->n); s += ',';
-    kput(s, x->code); s += ',';
-    kbits(s, x->c0); s += ',';
-    kbits(s, x->c1); s += ',';
-    kput(s, x->add); s += ',';
-    kput(s, x->mul); s += ',';
-    if (x->A) kput(s, (long long)x->A->id); else s += '-';
-    s += ';';
+    s.ch('(');
+    s.put((int)x->op); s.ch(',');
+    s.put(x->type); s.ch(',');
+    s.put(x->n); s.ch(',');
+    s.put(x->code); s.ch(',');
+    s.bits(x->c0); s.ch(',');
+    s.bits(x->c1); s.ch(',');
+    s.put(x->add); s.ch(',');
+    s.put(x->mul); s.ch(',');
+    if (x->A) s.put((long long)x->A->id); else s.ch('-');
+    s.ch(';');
     if (x->a) key_rec(x->a.get(), s, ph);
-    s += ';';
+    s.ch(';');
     if (x->b) key_rec(x->b.get(), s, ph);
-    s += ')';
+    s.ch(')');
 }
 
 static std::string node_key(const Node *x, const Node *ph = nullptr) {
-    std::string s;
+    KStr s;
     key_rec(x, s, ph);
-    return s;
+    return s.s;
 }
 
-// key of x as if it were still pending (x materialised, its inputs still attached): the lookup
-// key the next wait builds for the same expression
-static std::string pending_key(const Node *x) {
-    if (!x->mat) return node_key(x);
+// memo key of x; `pending`: as if x were still pending (x materialised, its inputs still
+// attached) -- the lookup key the next wait builds for the same expression; `perm`: the view of x
+// in matrix perm's gather layout
+static MKey memo_key(const Node *x, bool pending = false, const Mat *perm = nullptr) {
+    KHash h;
+    if (perm) { h.ch('!'); h.put((long long)perm->id); h.ch('('); }
     Node *m = const_cast<Node *>(x);
-    m->mat = false;
-    std::string s;
-    key_rec(x, s, nullptr);
-    m->mat = true;
-    return s;
+    const bool flip = pending && x->mat;
+    if (flip) m->mat = false;
+    key_rec(x, h, nullptr);
+    if (flip) m->mat = true;
+    if (perm) h.ch(')');
+    return h.key();
 }
 
 static void leaf_bufs(const Node *x, std::vector<std::weak_ptr<Buf>> &deps, SmallSet<const Node *> &seen) {
@@ -221,7 +249,7 @@ static bool dbg() {
 static bool memo_bind(Ctx &c, const NodeP &x) {
     if (x->mat) return true;
     if (dbg()) fprintf(stderr, "[nbg] memo lookup %s (%zu entries)\n", node_key(x.get()).c_str(), c.memo.size());
-    auto it = c.memo.find(node_key(x.get()));
+    auto it = c.memo.find(memo_key(x.get()));
     if (it == c.memo.end()) return false;
     for (auto &w : it->second.deps)
         if (w.expired()) return false;
@@ -234,7 +262,7 @@ static bool memo_bind(Ctx &c, const NodeP &x) {
 // Results are immutable and keyed by the identities of immutable leaves, so a memo entry stays
 // valid while its leaves live; the table is bounded (LRU) so it cannot pin unbounded memory.
 static const size_t MEMO_CAP = 64;
-static void memo_insert(Ctx &c, std::string k, const NodeP &result) {
+static void memo_insert(Ctx &c, const MKey &k, const NodeP &result) {
     std::vector<std::weak_ptr<Buf>> deps;
     SmallSet<const Node *> seen;
     // leaves of the expression: walk the (still attached) inputs of the result node
@@ -247,7 +275,7 @@ static void memo_insert(Ctx &c, std::string k, const NodeP &result) {
             if (it->second.stamp < victim->second.stamp) victim = it;
         c.memo.erase(victim);
     }
-    c.memo.insert_or_assign(std::move(k), Ctx::MemoEntry{std::move(deps), result, ++c.memo_clock});
+    c.memo.insert_or_assign(k, Ctx::MemoEntry{std::move(deps), result, ++c.memo_clock});
 }
 
 // ---------------------------------------------------------------- cloning (hint templates)
@@ -367,7 +395,7 @@ static NodeP instantiate(Ctx &c, const Hint &h, const NodeP &R) {
     return clone_subst(c, h.tmpl, cs);
 }
 
-static NodeP memo_get(Ctx &c, const std::string &k) {
+static NodeP memo_get(Ctx &c, const MKey &k) {
     auto it = c.memo.find(k);
     if (it == c.memo.end()) return nullptr;
     for (auto &w : it->second.deps)
@@ -377,12 +405,10 @@ static NodeP memo_get(Ctx &c, const std::string &k) {
     return it->second.result;
 }
 
-static std::string perm_key(const Mat &A, const Node *u) {
-    return "PERM" + std::to_string(A.id) + "(" + node_key(u) + ")";
-}
+static MKey perm_key(const Mat &A, const Node *u) { return memo_key(u, false, &A); }
 
 // x in the matrix's gather layout: xg[k] = x[iperm[k]] (a static permute kernel), memoised
-static NodeP permuted_view(Ctx &c, Mat &A, const NodeP &u, const std::string &pk) {
+static NodeP permuted_view(Ctx &c, Mat &A, const NodeP &u, const MKey &pk) {
     auto g = std::make_shared<Node>();
     g->op = Op::LEAF;
     g->type = u->type;
@@ -529,7 +555,7 @@ struct Builder {
                     if (!A.plan) gpu_build_spmv_plan(c, A);
                     if (A.plan->relabel) {
                         // gather input in the relabelled layout: a memoised permuted view of u
-                        const std::string pk = perm_key(A, u.get());
+                        const MKey pk = perm_key(A, u.get());
                         NodeP gx = memo_get(c, pk);
                         if (!gx) {
                             if (!u->mat) { need(u); need_mx[u.get()] = x->A; return -1; }
@@ -924,11 +950,11 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
         int64_t n = B.mxv ? B.mxv->A->nrows : len;
         size_t nvis = B.visited.size();
         // structural keys of the base outputs (before they become leaves)
-        std::vector<std::string> base_keys;
+        std::vector<MKey> base_keys;
         {
             PTimer pt(3);
             if (nb) {
-                for (int k = 0; k < nbase; k++) base_keys.push_back(node_key(B.out_nodes[k].get()));
+                for (int k = 0; k < nbase; k++) base_keys.push_back(memo_key(B.out_nodes[k].get()));
             }
         }
         run_region(c, B, hint_outs, n);
@@ -943,13 +969,12 @@ static void materialize_group(Ctx &c, const std::vector<NodeP> &roots, int64_t l
             PTimer pt_m(6);
             // memoise every result (common subexpressions across waits, e.g. dinv across runs)
             for (int k = 0; k < nbase; k++)
-                if (!c.out_targets.count(B.out_nodes[k].get())) memo_insert(c, std::move(base_keys[k]), B.out_nodes[k]);
+                if (!c.out_targets.count(B.out_nodes[k].get())) memo_insert(c, base_keys[k], B.out_nodes[k]);
             // side outputs are keyed with R already materialised (the next sweep's lookup key)
             for (HintOut &h : hint_outs) {
-                std::string k = pending_key(h.node.get());
-                if (h.scatter) k = "PERM" + std::to_string(h.scatter->id) + "(" + k + ")";
-                if (dbg()) fprintf(stderr, "[nbg] memo insert %s\n", k.c_str());
-                memo_insert(c, std::move(k), h.node);
+                const MKey k = memo_key(h.node.get(), true, h.scatter.get());
+                if (dbg()) fprintf(stderr, "[nbg] memo insert %s%s\n", h.scatter ? "(gather layout) " : "", node_key(h.node.get()).c_str());
+                memo_insert(c, k, h.node);
             }
         }
         // elided intermediates = visited pending nodes that were not stored
