@@ -159,23 +159,28 @@ def run_ours(args, rank, world, local_rank):
     kind = nbg.GRAPH_RMAT if cfg["graph"] == "rmat" else nbg.GRAPH_ER
     t0 = time.time()
     cuts = None
-    if world > 1:
+    # the per-rank data plane at one rank too (NBG_BENCH_DIST=1): symmetric relabel, rows in the
+    # gather layout, the next sweep's gathered vector written in row order
+    use_dist = world > 1 or os.environ.get("NBG_BENCH_DIST", "0") == "1"
+    if use_dist:
         # per-rank setup: every rank regenerates the edges, keeps its share,
         # degrees summed over NCCL, symmetric relabel, byte-balanced row block -- no rank builds the
         # whole graph or copies a CSR to the host
-        uid = nbg.nbg_dist_unique_id() if rank == 0 else None
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        nbg.nbg_dist_init(ctx, rank, world, obj[0])
-        # NBG_DIST_EXCHANGE=peer: the exchange fused into the sweep kernel as NVLink peer stores
-        # (nbg_dist_set_exchange); default: one NCCL group per sweep
-        xmode = os.environ.get("NBG_DIST_EXCHANGE", "collective")
-        nbg.nbg_dist_set_exchange(ctx, nbg.DIST_EXCHANGE_PEER if xmode == "peer" else nbg.DIST_EXCHANGE_COLLECTIVE)
+        if world > 1:
+            uid = nbg.nbg_dist_unique_id() if rank == 0 else None
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            nbg.nbg_dist_init(ctx, rank, world, obj[0])
+            # NBG_DIST_EXCHANGE=peer: the exchange fused into the sweep kernel as NVLink peer stores
+            # (nbg_dist_set_exchange); default: one NCCL group per sweep
+            xmode = os.environ.get("NBG_DIST_EXCHANGE", "collective")
+            nbg.nbg_dist_set_exchange(ctx, nbg.DIST_EXCHANGE_PEER if xmode == "peer" else nbg.DIST_EXCHANGE_COLLECTIVE)
         A, deg, cuts, ncols_g = nbg.nbg_dist_graph_from_generator(ctx, kind, cfg["scale"], cfg["edge_factor"], args.seed,
                                                                   nranks=world, bytes_per_row=5 * w)
         n = int(cuts[-1])
         t_nnz = torch.tensor([nbg.nbg_matrix_nnz(ctx, A)], device="cuda", dtype=torch.int64)
-        dist.all_reduce(t_nnz)
+        if world > 1:
+            dist.all_reduce(t_nnz)
         nnz = int(t_nnz.item())
     else:
         if args.mtx:       # NEXT-4: a real graph from a Matrix Market file (the paper's GAP-web run)
@@ -190,7 +195,7 @@ def run_ours(args, rank, world, local_rank):
     dangling = nbg.PR_UNIFORM if cfg["dangling"] == "uniform" else nbg.PR_DROP
 
     def step():
-        if world > 1:
+        if use_dist:
             r, s, h = nbg.nbg_pagerank_dist(ctx, A, deg, cuts, ncols_g, alpha=cfg["alpha"], tol=tol, itermax=itermax,
                                             dangling=dangling, type=T)
         else:

@@ -73,7 +73,7 @@ struct SigHash {
 };
 template <class S>
 static void sig_emit(const Prog &p, S &s) {
-    s.ch(p.spmv ? (p.tp ? 'T' : (p.lpr ? 'L' : 'S')) : 'E');
+    s.ch(p.spmv ? (p.tp ? 'T' : (p.lpr ? 'L' : (p.rb ? (p.rb_inline ? 'I' : 'R') : 'S'))) : 'E');
     s.ch(p.vec ? 'v' : 's');
     s.ch(p.tma ? 'T' : 'n');
     s.put(p.nt, ',');
@@ -128,6 +128,21 @@ struct Gen {
                    "; for (int q_ = 0; q_ < a.npeer; q_++) ((" + T + "*)a.peer[q_])[d_] = v_; } }";
         return std::string("{ const int d_ = a.oscat[") + o + "][" + idx + "]; if (d_ >= 0) ((" + T +
                "*)a.out[" + o + "])[d_] = " + v(ov.ins) + "; }";
+    }
+    // vector skeletons: the scatter map of 4 consecutive elements loaded once, before any store of
+    // the trip (a per-element map load after the previous element's store cannot be hoisted above
+    // it -- the compiler must assume they alias -- so each element would cost a round trip)
+    std::string scat_preload(const OutV &ov, const std::string &vi) const {
+        const std::string o = std::to_string(ov.out);
+        return "const int4 M" + o + "_ = __ldg(((const int4*)a.oscat[" + o + "]) + " + vi + ");";
+    }
+    std::string scat_pre(const OutV &ov, const std::string &e) const {
+        const std::string o = std::to_string(ov.out), T = ctype(p.ins[ov.ins].t);
+        const std::string d = "(" + e + " == 0 ? M" + o + "_.x : (" + e + " == 1 ? M" + o + "_.y : (" + e + " == 2 ? M" + o + "_.z : M" + o + "_.w)))";
+        if (ov.multi)
+            return std::string("{ const int d_ = ") + d + "; if (d_ >= 0) { const " + T + " v_ = " + v(ov.ins) +
+                   "; for (int q_ = 0; q_ < a.npeer; q_++) ((" + T + "*)a.peer[q_])[d_] = v_; } }";
+        return std::string("{ const int d_ = ") + d + "; if (d_ >= 0) ((" + T + "*)a.out[" + o + "])[d_] = " + v(ov.ins) + "; }";
     }
     std::string store(const OutV &ov, const std::string &idx) const {
         if (ov.scatter) return scat(ov, idx);
@@ -538,13 +553,15 @@ int gen_ewise(Gen &g, const std::string &kname, bool vec) {
         o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
         o << "      const long long vi = vb_ + u * stride;\n";
         o << "      if (vi >= nv) break;\n";
+        for (const OutV &ov : p.outs)
+            if (ov.scatter) o << "      " << g.scat_preload(ov, "vi") << "\n";
         for (int k = 0; k < p.n_out; k++)
             if (out_type[k] >= 0) o << "      " << ctype(out_type[k]) << " O" << k << "[4];\n";
         o << "      #pragma unroll\n      for (int e = 0; e < 4; e++) {\n";
         g.emit_body(
             "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[u][e]"; },
             [&](const OutV &ov) {
-                if (ov.scatter) return g.scat(ov, "(vi * 4 + e)");
+                if (ov.scatter) return g.scat_pre(ov, "e");
                 return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
             },
             [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
@@ -1122,6 +1139,361 @@ int gen_spmv_lpr(Gen &g, const std::string &kname) {
     return 0;
 }
 
+// Row-binned SpMV skeleton (DESIGN.md §7 "row-binned SpMV", plan RbPlan in graph.cu).  One
+// persistent CTA per SM, hot-column cache in shared memory as in the task skeleton.  Warps claim
+// tasks from one global counter (the largest first; the whole grid shares the tail):
+//   hub chunk   : 512 groups of a row > 2048 entries; lane l sums groups l, l + 32, ... in order,
+//                 fixed shuffle tree -> chunk partial; the last chunk (ticket) combines in order;
+//   long rows   : up to 32 rows of T+1..512 groups, one after another by the whole warp (same
+//                 lane-strided order + tree); the next step's indices load during this one;
+//   short slices: up to 32 slices of 32 rows, lane l owns slot l of each slice and sums its row
+//                 sequentially (entries in order); sell[base + 32 j + l] is the j-th group of the
+//                 lane's run, so every index load is one coalesced 512-byte warp load and row ends
+//                 are warp-uniform (no scans, no shuffles, no shared-memory bookkeeping);
+//   empty rows  : (inline mode) ranges of 512 rows, the epilogue of the rows without entries.
+// Epilogue, two modes:
+//   inline (default): the fused epilogue of a row runs where its total completes -- per lane at a
+//     slice end, per lane for the task's long rows at the task end, by the combining lane for a
+//     hub -- so its loads and stores overlap the gathers of other warps; floating PLUS reductions
+//     are summed per task in fp64 (fixed tree) and added exactly into per-warp limbs;
+//   barrier: row totals to tot[row]; grid barrier; the epilogue over rows in index order
+//     (coalesced, 4 rows per thread and trip).
+// A row's summation order depends on its length only, so fused / per-op mxv and every row
+// partition give identical row sums; every reduction is deterministic.
+int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
+    const Prog &p = g.p;
+    auto &o = g.o;
+    const SpmvSig &sp = p.sp;
+    const bool IE = p.rb_inline;
+    SemiringCode k = semiring_code(sp);
+    const std::string &ACC = k.ACC, &IDENT = k.IDENT;
+    const char *XT = ctype(sp.xt);
+    const bool rt_narrow = (ACC == "double" && sp.T == NBG_FP32);
+    const std::string RT = rt_narrow ? "float" : ACC;
+    const int x_bytes = (int)type_size(sp.xt);
+    int nt_ = p.nt, hk_ = p.hot_kb;
+    if (nt_ <= 0) spmv_variant(x_bytes, 0, &nt_, &hk_);
+    const int NT = nt_, NW = NT / 32;
+    // inline mode: floating PLUS reductions flushed per task into per-warp exact limbs
+    std::vector<int> fplus;
+    if (IE)
+        for (size_t j = 0; j < p.reds.size(); j++)
+            if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
+    const int NF = (int)fplus.size();
+    int hot_bytes = hk_ * 1024;
+    {
+        const int other = 4096 + NW * NF * 12 * 8;   // static shared memory + the driver's 1 KB per CTA, warp limbs
+        const int step = (hk_ >= 140 ? 196 : (hk_ >= 100 ? 164 : 132)) * 1024;
+        if (hot_bytes > step - other) hot_bytes = std::max(0, step - other);
+    }
+    int hot_cap = (hot_bytes / x_bytes / 4) * 4;
+    const int hot_region = (hot_cap * x_bytes + 15) / 16 * 16;
+    const int dyn_bytes = std::max(16, hot_region + NW * NF * 12 * 8);
+    if (hot_entries) *hot_entries = hot_cap;
+    std::string gx;
+    switch (sp.xt) {
+        case NBG_FP32: gx = "__uint_as_float(nbg_gx32(s_base, X, C_, hc))"; break;
+        case NBG_INT32: gx = "((int)nbg_gx32(s_base, X, C_, hc))"; break;
+        case NBG_FP64: gx = "__longlong_as_double((long long)nbg_gx64(s_base, X, C_, hc))"; break;
+        case NBG_INT64: gx = "((long long)nbg_gx64(s_base, X, C_, hc))"; break;
+        default: gx = "((C_) < hc ? s_hot[(C_)] : X[(C_)])"; break;
+    }
+    const bool zero_pad = sp.add == NBG_PLUS && !sp.has_vals && (sp.mul == NBG_SECOND || sp.mul == NBG_TIMES);
+    o << "#define NBG_ADD(A_, B_) " << k.ADD << "\n";
+    o << "__device__ __forceinline__ " << k.C << " nbg_mul(const KArgs &a, long long P_, " << XT << " X_) { return " << k.mul << "; }\n";
+    o << "__device__ __forceinline__ " << XT << " nbg_gxv(unsigned s_base, const " << XT << "* s_hot, const " << XT
+      << "* X, int C_, int hc) { return " << gx << "; }\n";
+    o << "#define NBG_GV(C_) nbg_gxv(s_base, s_hot, X, ((C_) > 0 ? (C_) : 0), hc)\n";
+    // term of a stored position B_ (1) or a padding position (0)
+    if (zero_pad)
+        o << "#define NBG_TV(B_, V_) ((" << ACC << ")nbg_mul(a, 0, (B_) ? (V_) : (" << XT << ")0))\n";
+    else
+        o << "#define NBG_TV(B_, V_) ((B_) ? (" << ACC << ")nbg_mul(a, 0, (V_)) : (" << ACC << ")(" << IDENT << "))\n";
+    // the 4 gathers of a group and its presence bits (the indices die here), then its 4 terms in order
+    o << "#define NBG_G4(Q_, V_) const " << XT << " V_##0 = NBG_GV(Q_.x), V_##1 = NBG_GV(Q_.y), V_##2 = NBG_GV(Q_.z), V_##3 = NBG_GV(Q_.w); "
+         "const unsigned V_##m = (unsigned)(Q_.x >= 0) | ((unsigned)(Q_.y >= 0) << 1) | ((unsigned)(Q_.z >= 0) << 2) | ((unsigned)(Q_.w >= 0) << 3)\n";
+    o << "#define NBG_A4(ACC_, V_) ACC_ = NBG_ADD(ACC_, NBG_TV(V_##m & 1u, V_##0)); ACC_ = NBG_ADD(ACC_, NBG_TV((V_##m >> 1) & 1u, V_##1)); "
+         "ACC_ = NBG_ADD(ACC_, NBG_TV((V_##m >> 2) & 1u, V_##2)); ACC_ = NBG_ADD(ACC_, NBG_TV((V_##m >> 3) & 1u, V_##3))\n";
+    o << "#define NBG_NEG make_int4(-1, -1, -1, -1)\n";
+    o << "__device__ __forceinline__ " << ACC << " nbg_tree(" << ACC << " v) {   // fixed shuffle tree, lane 0 holds the total\n";
+    o << "  for (int d = 16; d > 0; d >>= 1) { const " << ACC << " w = __shfl_down_sync(0xffffffffu, v, d); v = NBG_ADD(v, w); }\n";
+    o << "  return v;\n}\n";
+    if (NF) o << "#define NBG_NF " << NF << "\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", 1) " << kname << "(const KArgs a) {\n";
+    o << "  extern __shared__ __align__(16) unsigned char nbg_dyn[];\n";
+    o << "  __shared__ double nbg_sh[32];\n";
+    o << "  " << XT << "* s_hot = (" << XT << "*)nbg_dyn;\n";
+    o << "  const unsigned s_base = (unsigned)__cvta_generic_to_shared(nbg_dyn);\n";
+    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n";
+    if (NF) {
+        o << "  u64* s_x = (u64*)(nbg_dyn + " << hot_region << ");   // [warp][NF][12] exact limbs\n";
+        o << "  for (int k = threadIdx.x; k < " << NW * NF * 12 << "; k += blockDim.x) s_x[k] = 0ull;\n";
+    }
+    (void)NW;
+    o << "  const " << XT << "* __restrict__ X = (const " << XT << "*)a.x;\n";
+    o << "  const int4* __restrict__ CG = (const int4*)a.colidx;\n";
+    o << "  const int4* __restrict__ SELL = (const int4*)a.rb_sell;\n";
+    o << "  const long long* __restrict__ GRP = a.rowptr;\n";
+    if (!IE) o << "  " << RT << "* __restrict__ TOT = (" << RT << "*)a.rb_tot;\n";
+    o << "  const int hc = (int)a.hc;\n";
+    o << "  {\n";
+    o << "    const int nv_ = ((((unsigned long long)X) & 15ull) == 0ull) ? (int)((hc * sizeof(" << XT << ")) >> 4) : 0;\n";
+    o << "    const uint4* src_ = (const uint4*)X; uint4* dst_ = (uint4*)nbg_dyn;\n";
+    o << "    for (int k = threadIdx.x; k < nv_; k += 4 * blockDim.x) {\n";
+    o << "      uint4 w_[4];\n";
+    o << "      #pragma unroll\n      for (int u = 0; u < 4; u++) if (k + u * (int)blockDim.x < nv_) w_[u] = __ldg(src_ + k + u * blockDim.x);\n";
+    o << "      #pragma unroll\n      for (int u = 0; u < 4; u++) if (k + u * (int)blockDim.x < nv_) dst_[k + u * blockDim.x] = w_[u];\n";
+    o << "    }\n";
+    o << "    for (int k = (nv_ << 4) / (int)sizeof(" << XT << ") + threadIdx.x; k < hc; k += blockDim.x) s_hot[k] = X[k];\n";
+    o << "  }\n";
+    // uniform values (device scalars of earlier kernels, constants) read once per CTA into shared
+    // memory: re-read per use, they take no registers across the step loops
+    const int NU = std::max(1, g.n_uniform());
+    o << "  __shared__ unsigned long long s_uni[" << NU << "];\n";
+    g.emit_uniform_to_smem("s_uni");
+    o << "  __syncthreads();\n";
+    g.emit_red_decl();
+    // the fused epilogue of row `i` with row total `acc` (inline mode), in its own scope
+    auto epi = [&](const std::string &ind, const std::string &idx, const std::string &accx) {
+        o << ind << "{\n";
+        o << ind << "  const long long i = " << idx << ";\n";
+        o << ind << "  const " << ACC << " eacc_ = " << accx << ";\n";
+        g.emit_uniform_reload(ind + "  ", "s_uni");
+        g.emit_body(
+            ind + "  ",
+            [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+            [&](const OutV &ov) { return g.store(ov, "i"); },
+            [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "eacc_");
+        o << ind << "}\n";
+    };
+    // row total of a completed row: inline epilogue or tot[]
+    auto done = [&](const std::string &ind, const std::string &idx, const std::string &accx) {
+        if (IE) epi(ind, idx, accx);
+        else o << ind << "TOT[" << idx << "] = (" << RT << ")(" << accx << ");\n";
+    };
+    o << "  {\n";
+    o << "  const int items = (int)a.rb_ntasks;\n";
+    o << "  const int4* __restrict__ TK = (const int4*)a.rb_tasks;\n";
+    // tasks from one global counter (bar[2]; reset by the grid barrier's last arriver / the last CTA
+    // out), claimed one ahead
+    o << "  int itn_ = 0;\n";
+    o << "  if (lane == 0) itn_ = atomicAdd(a.rb_bar + 2, 1u);\n";
+    o << "  itn_ = __shfl_sync(0xffffffffu, itn_, 0);\n";
+    o << "  int4 tn_ = itn_ < items ? TK[itn_] : make_int4(0, 0, 0, 0);\n";
+    o << "  for (;;) {\n";
+    o << "    const int it = itn_;\n";
+    o << "    if (it >= items) break;\n";
+    o << "    const int4 tk = tn_;\n";
+    o << "    if (lane == 0) itn_ = atomicAdd(a.rb_bar + 2, 1u);\n";
+    o << "    itn_ = __shfl_sync(0xffffffffu, itn_, 0);\n";
+    o << "    if (itn_ < items) tn_ = TK[itn_];\n";
+    o << "    const int kind = tk.x & 3, cnt = tk.x >> 2;\n";
+    // ---- short slices
+    o << "    if (kind == 2) {\n";
+    o << "      const int s0 = tk.y;\n";
+    o << "      const long long base = ((long long)(unsigned)tk.w << 32) | (long long)(unsigned)tk.z;\n";
+    o << "      const int myw = lane < cnt ? a.rb_swid[s0 + lane] : 0;\n";
+    o << "      const int W = __reduce_add_sync(0xffffffffu, (unsigned)myw);\n";
+    o << "      const int4* __restrict__ Q = SELL + base + lane;\n";
+    o << "      int4 q0 = __ldcs(Q), q1 = (1 < W) ? __ldcs(Q + 32) : NBG_NEG;\n";
+    o << "      int si = 0, send = __shfl_sync(0xffffffffu, myw, 0);\n";
+    o << "      int row = a.rb_srow[32ll * s0 + lane];\n";
+    o << "      " << ACC << " acc = " << IDENT << ";\n";
+    o << "      for (int j = 0; j < W; j += 2) {\n";
+    o << "        const int4 c0 = q0, c1 = q1;\n";
+    o << "        NBG_G4(c0, u); NBG_G4(c1, v);\n";
+    o << "        if (j + 2 < W) q0 = __ldcs(Q + 32 * (j + 2));\n";
+    o << "        if (j + 3 < W) q1 = __ldcs(Q + 32 * (j + 3)); else q1 = NBG_NEG;\n";
+    o << "        NBG_A4(acc, u);\n";
+    o << "        if (j + 1 == send) {\n";
+    o << "          if (row >= 0)\n";
+    done("          ", "row", "acc");
+    o << "          acc = " << IDENT << ";\n";
+    o << "          if (++si < cnt) { send += __shfl_sync(0xffffffffu, myw, si); row = a.rb_srow[32ll * (s0 + si) + lane]; }\n";
+    o << "        }\n";
+    o << "        if (j + 1 < W) {\n";
+    o << "          NBG_A4(acc, v);\n";
+    o << "          if (j + 2 == send) {\n";
+    o << "            if (row >= 0)\n";
+    done("            ", "row", "acc");
+    o << "            acc = " << IDENT << ";\n";
+    o << "            if (++si < cnt) { send += __shfl_sync(0xffffffffu, myw, si); row = a.rb_srow[32ll * (s0 + si) + lane]; }\n";
+    o << "          }\n";
+    o << "        }\n";
+    o << "      }\n";
+    o << "    }\n";
+    if (IE) {
+        // ---- empty rows: 4 consecutive rows per lane and trip (vector loads when aligned)
+        o << "    else if (kind == 3) {\n";
+        o << "      const long long rb0_ = tk.y;\n";
+        o << "      for (int j = lane; j < cnt; j += 32) {\n";
+        o << "        const long long i_ = rb0_ + j;\n";
+        o << "        if (!((__ldg(a.rb_mask + (i_ >> 5)) >> (i_ & 31)) & 1u))\n";
+        epi("          ", "i_", "(" + ACC + ")(" + IDENT + ")");
+        o << "      }\n";
+        o << "    }\n";
+    }
+    // ---- long rows / hub chunk: lane-strided groups (lane l: l, l + 32, l + 64, ...), tree
+    o << "    else {\n";
+    o << "    int myrow = 0, myng = 0;\n";
+    o << "    long long mygb = 0;\n";
+    o << "    int nrow = 1;\n";
+    if (IE) o << "    " << ACC << " mytot = " << IDENT << ";\n";
+    o << "    if (kind == 0) {\n";
+    o << "      const int4 ch = ((const int4*)a.chunks)[tk.y];\n";
+    o << "      mygb = ((long long)(unsigned)ch.z << 32) | (long long)(unsigned)ch.y;\n";
+    o << "      myng = ch.w;\n";
+    o << "    } else {\n";
+    o << "      nrow = cnt;\n";
+    o << "      if (lane < cnt) { myrow = a.rb_lrows[tk.y + lane]; mygb = GRP[myrow]; myng = (int)(GRP[myrow + 1] - mygb); }\n";
+    o << "    }\n";
+    o << "    int r = 0, b = 0;\n";
+    o << "    long long gb = __shfl_sync(0xffffffffu, mygb, 0);\n";
+    o << "    int ng = __shfl_sync(0xffffffffu, myng, 0);\n";
+    o << "    int4 q0 = (lane < ng) ? __ldcs(CG + gb + lane) : NBG_NEG;\n";
+    o << "    int4 q1 = (32 + lane < ng) ? __ldcs(CG + gb + 32 + lane) : NBG_NEG;\n";
+    o << "    " << ACC << " acc = " << IDENT << ";\n";
+    o << "    for (;;) {\n";
+    o << "      const int4 c0 = q0, c1 = q1;\n";
+    o << "      NBG_G4(c0, u); NBG_G4(c1, v);\n";
+    o << "      int nb = b + 64, nr = r;\n";
+    o << "      long long ngb = gb; int nng = ng;\n";
+    o << "      if (nb >= ng) { nr = r + 1; nb = 0; if (nr < nrow) { ngb = __shfl_sync(0xffffffffu, mygb, nr); nng = __shfl_sync(0xffffffffu, myng, nr); } }\n";
+    o << "      if (nr < nrow) {\n";
+    o << "        q0 = (nb + lane < nng) ? __ldcs(CG + ngb + nb + lane) : NBG_NEG;\n";
+    o << "        q1 = (nb + 32 + lane < nng) ? __ldcs(CG + ngb + nb + 32 + lane) : NBG_NEG;\n";
+    o << "      }\n";
+    o << "      NBG_A4(acc, u); NBG_A4(acc, v);\n";
+    o << "      if (nr != r) {\n";
+    o << "        const " << ACC << " t = nbg_tree(acc);\n";
+    if (IE) {
+        o << "        { const " << ACC << " tt = __shfl_sync(0xffffffffu, t, 0); if (lane == r) mytot = tt; }\n";
+    } else {
+        o << "        const int orow = __shfl_sync(0xffffffffu, myrow, r);\n";
+    }
+    o << "        acc = " << IDENT << ";\n";
+    o << "        if (lane == 0) {\n";
+    if (!IE) o << "          if (kind != 0) TOT[orow] = (" << RT << ")t;\n          else {\n";
+    else o << "          if (kind == 0) {\n";
+    o << "            ((" << ACC << "*)a.partials)[tk.y] = t;\n";
+    o << "            const int cx = ((const int4*)a.chunks)[tk.y].x;\n";
+    o << "            const int4 lr = ((const int4*)a.longs)[cx];\n";
+    o << "            int tk_;\n";
+    o << "            asm volatile(\"atom.add.release.gpu.s32 %0, [%1], 1;\" : \"=r\"(tk_) : \"l\"(&a.counters[cx]) : \"memory\");\n";
+    o << "            if (tk_ == lr.z - 1) {\n";
+    o << "              asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\");\n";
+    o << "              " << ACC << " s_ = " << IDENT << ";\n";
+    o << "              for (int q = 0; q < lr.z; q++) { const " << ACC << " pq = *(volatile const " << ACC << "*)(((const " << ACC
+      << "*)a.partials) + lr.y + q); s_ = NBG_ADD(s_, pq); }\n";
+    o << "              a.counters[cx] = 0;\n";
+    done("              ", "lr.x", "s_");
+    o << "            }\n";
+    o << "          }\n";
+    o << "        }\n";
+    o << "        if (nr >= nrow) break;\n";
+    o << "      }\n";
+    o << "      r = nr; b = nb; gb = ngb; ng = nng;\n";
+    o << "    }\n";
+    if (IE) {
+        o << "    if (kind == 1 && lane < nrow)\n";
+        epi("      ", "myrow", "mytot");
+    }
+    o << "    }\n";
+    if (NF) {   // the task's floating PLUS partials: fixed tree, exact add into the warp's limbs
+        for (int f = 0; f < NF; f++) {
+            const int j = fplus[f];
+            o << "    { const double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f
+              << ") * 12, t_); r" << j << " = 0.0; }\n";
+        }
+    }
+    o << "  }\n";
+    o << "  }\n";
+    if (IE) {
+        // the last CTA out resets the task counter for the next launch (every CTA is done with it)
+        o << "  __syncthreads();\n";
+        o << "  if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(a.rb_bar, 1u) == gridDim.x - 1) { atomicExch(a.rb_bar, 0u); atomicExch(a.rb_bar + 2, 0u); } }\n";
+        for (int f = 0; f < NF; f++) {
+            const int j = fplus[f];
+            o << "  if (threadIdx.x < 12) {\n";
+            o << "    u64 v_ = 0ull; double d_ = 0.0;\n";
+            o << "    for (int w = 0; w < " << NW << "; w++) { const u64 x_ = s_x[(w * NBG_NF + " << f << ") * 12 + threadIdx.x]; if (threadIdx.x == 11) d_ += __longlong_as_double((long long)x_); else v_ = threadIdx.x == 10 ? (v_ | x_) : v_ + x_; }\n";
+            o << "    if (threadIdx.x == 11) { if (d_ != 0.0) atomicAdd((double*)&a.racc[" << p.reds[j].racc << "][12], d_); }\n";
+            o << "    else if (threadIdx.x == 10) { if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][10], nbg_xacc_flag_counts(v_)); }\n";
+            o << "    else if (v_) atomicAdd(&a.racc[" << p.reds[j].racc << "][threadIdx.x], v_);\n";
+            o << "  }\n";
+        }
+        for (size_t j = 0; j < p.reds.size(); j++) {
+            if (std::find(fplus.begin(), fplus.end(), (int)j) != fplus.end()) continue;
+            const int kind = redkind(g, p.reds[j]);
+            if (kind == 6) { o << g.red_finish_xt(j); continue; }
+            if (kind == 0 || kind == 2 || kind == 3)
+                o << "  nbg_block_finish_f(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+            else
+                o << "  nbg_block_finish_i(r" << j << ", " << kind << ", a.racc[" << p.reds[j].racc << "], nbg_sh);\n";
+        }
+        o << "}\n";
+        return dyn_bytes;
+    }
+    // ---------------- grid barrier (all CTAs are resident: one per SM, grid <= SMs)
+    o << "  nbg_grid_sync(a.rb_bar, a.rb_bar + 2);\n";
+    // ---------------- phase B: the epilogue over rows in index order.  Vector form (all buffers
+    // 16-byte aligned): 4 consecutive rows per thread and trip, every load of the trip (inputs,
+    // row totals, mask word, scatter maps) independent of the others; then the tail.
+    g.emit_uniform_reload("  ", "s_uni");
+    o << "  const long long stride_ = (long long)gridDim.x * blockDim.x;\n";
+    o << "  long long tail0_ = 0;\n";
+    if (p.vec) {
+        std::vector<int> slot_type(p.n_in, -1);
+        for (const Ins &in : p.ins)
+            if (in.k == Ins::LD_VEC) slot_type[in.slot] = in.t;
+        std::vector<int> out_type(p.n_out, -1);
+        for (const OutV &ov : p.outs)
+            if (!ov.scatter) out_type[ov.out] = p.ins[ov.ins].t;
+        const int rtt = RT == "float" ? NBG_FP32 : (RT == "double" ? NBG_FP64 : (RT == "int" ? NBG_INT32 : NBG_INT64));
+        std::string tl = vload(rtt, "a.rb_tot", "vi", "T_");
+        for (size_t q = tl.find("__ldg("); q != std::string::npos; q = tl.find("__ldg(", q)) tl.replace(q, 6, "__ldcg(");
+        o << "  const long long nv_ = a.n >> 2;\n  tail0_ = nv_ << 2;\n";
+        o << "  for (long long vi = (long long)blockIdx.x * blockDim.x + threadIdx.x; vi < nv_; vi += stride_) {\n";
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0) {
+                o << "    " << ctype(slot_type[s2]) << " L" << s2 << "[4];\n";
+                o << "    " << vload(slot_type[s2], "a.in[" + std::to_string(s2) + "]", "vi", "L" + std::to_string(s2)) << "\n";
+            }
+        o << "    " << RT << " T_[4];\n    " << tl << "\n";
+        o << "    const unsigned mb_ = (__ldcg(a.rb_mask + ((vi << 2) >> 5)) >> ((vi << 2) & 31)) & 15u;\n";
+        for (const OutV &ov : p.outs)
+            if (ov.scatter) o << "    " << g.scat_preload(ov, "vi") << "\n";
+        for (int k2 = 0; k2 < p.n_out; k2++)
+            if (out_type[k2] >= 0) o << "    " << ctype(out_type[k2]) << " O" << k2 << "[4];\n";
+        o << "    #pragma unroll\n    for (int e = 0; e < 4; e++) {\n";
+        o << "      const " << ACC << " acc = ((mb_ >> e) & 1u) ? (" << ACC << ")T_[e] : (" << ACC << ")(" << IDENT << ");\n";
+        g.emit_body(
+            "      ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
+            [&](const OutV &ov) {
+                if (ov.scatter) return g.scat_pre(ov, "e");
+                return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
+            },
+            [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+        o << "    }\n";
+        for (int k2 = 0; k2 < p.n_out; k2++)
+            if (out_type[k2] >= 0) o << "    " << vstore(out_type[k2], "a.out[" + std::to_string(k2) + "]", "vi", "O" + std::to_string(k2)) << "\n";
+        o << "  }\n";
+    }
+    o << "  for (long long i = tail0_ + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride_) {\n";
+    o << "    const unsigned mw_ = __ldcg(a.rb_mask + (i >> 5));\n";
+    o << "    const " << RT << " t_ = __ldcg(TOT + i);\n";
+    o << "    const " << ACC << " acc = ((mw_ >> (i & 31)) & 1u) ? (" << ACC << ")t_ : (" << ACC << ")(" << IDENT << ");\n";
+    g.emit_body(
+        "    ",
+        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+        [&](const OutV &ov) { return g.store(ov, "i"); },
+        [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    o << "  }\n";
+    g.emit_red_finish();
+    o << "}\n";
+    return dyn_bytes;
+}
+
 // Phase 1: per-pair partial sums with the column block in shared memory.  The CTA walks its task
 // range block by block (loads the block's slice of x, then its warps claim the block's tasks); a
 // task is the single-pass row task on pairs instead of rows (same 64-group steps, lane-local split
@@ -1577,6 +1949,8 @@ std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem, int 
         smem = gen_tp2(g, kname);
     else if (p.spmv && p.lpr)
         smem = gen_spmv_lpr(g, kname);
+    else if (p.spmv && p.rb)
+        smem = gen_spmv_rb(g, kname, hot_entries);
     else if (p.spmv)
         smem = gen_spmv(g, kname, hot_entries);
     else

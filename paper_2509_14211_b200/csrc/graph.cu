@@ -322,7 +322,234 @@ __global__ void k_slot_of(long long np, const int *order, int *slot) {
         slot[order[r]] = (int)r;
 }
 
+
+// ---- row-binned plan kernels (gpu_rb_plan)
+// per row: group count; rows with 1 <= g <= SP_LONG_G are binned (key = SP_LONG_G - g: stable radix
+// sort -> g descending, ties by row id); histogram of g; one mask word per 32 rows (non-empty)
+__global__ void k_rb_keys(long long n, const long long *grp, unsigned *key, unsigned char *flag, unsigned long long *hist,
+                          unsigned *mask) {
+    __shared__ unsigned long long h[SP_LONG_G + 1];
+    for (int j = threadIdx.x; j <= SP_LONG_G; j += blockDim.x) h[j] = 0ull;
+    __syncthreads();
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31) & ~31ll); i += (long long)gridDim.x * blockDim.x) {
+        const long long g = i < n ? grp[i + 1] - grp[i] : 0;
+        const unsigned m = __ballot_sync(0xffffffffu, g > 0);
+        if ((threadIdx.x & 31) == 0) mask[i >> 5] = m;
+        if (i < n) {
+            const bool b = g >= 1 && g <= SP_LONG_G;
+            flag[i] = b ? 1 : 0;
+            key[i] = b ? (unsigned)(SP_LONG_G - g) : 0u;
+            if (b) atomicAdd(&h[g], 1ull);
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j <= SP_LONG_G; j += blockDim.x)
+        if (h[j]) atomicAdd(&hist[j], h[j]);
+}
+// slot p of the short slices: row = sorted[nlong + p] (or none), its groups copied column-major
+__global__ void k_rb_fill(long long nslots, long long nshort, const int *sorted_short, const long long *grp, const int4 *cg,
+                          const int *swid, const long long *soff, int *srow, int4 *sell) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nslots; p += (long long)gridDim.x * blockDim.x) {
+        const long long s = p >> 5;
+        const int l = (int)(p & 31);
+        const int row = p < nshort ? sorted_short[p] : -1;
+        srow[p] = row;
+        const int w = swid[s];
+        const long long base = soff[s];
+        long long g0 = 0, g = 0;
+        if (row >= 0) { g0 = grp[row]; g = grp[row + 1] - g0; }
+        for (int k = 0; k < w; k++) sell[base + 32ll * k + l] = k < g ? cg[g0 + k] : make_int4(-1, -1, -1, -1);
+    }
+}
+
 }  // namespace
+
+bool spmv_rb_inline() {   // read at every region launch (the signature records the mode)
+    // barrier mode by default: C4 165 us per sweep vs 190 us inline (the scattered per-row epilogue
+    // costs more L2 sectors inside the gather-bound phase than the separate pass costs)
+    const char *e = getenv("NBG_RB_MODE");
+    return e && e[0] == 'i';
+}
+
+int spmv_rb_mode() {   // read at every region launch (the signature records the skeleton)
+    const char *e = getenv("NBG_SPMV_RB");
+    return (e && *e) ? (e[0] == '1' ? 1 : 0) : -1;
+}
+
+// Row-binned plan (RbPlan, DESIGN.md §7 "row-binned SpMV").  Device: group counts, mask, histogram,
+// stable radix sort of the binned rows by descending g, the column-major slice fill.  Host: from
+// the histogram alone (the sorted g sequence is determined by it) the slice widths and offsets and
+// the task list -- hub chunks first, then long-row runs, then slice runs, each run holding <= 32
+// items and about SP_TASK_G groups.
+RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
+    if (!A.plan) gpu_build_spmv_plan(c, A);
+    SpmvPlan &P = *A.plan;
+    if (A.vals || A.nrows == 0) return nullptr;
+    if (P.rb) return P.rb.get();
+    auto R = std::make_unique<RbPlan>();
+    const long long n = A.nrows;
+    {
+        const char *e = getenv("NBG_RB_T");
+        if (e && *e) R->T = std::max(1, std::min(SP_LONG_G, atoi(e)));
+    }
+    const int T = R->T;
+    long long tg = SP_TASK_G;
+    {
+        const char *e = getenv("NBG_RB_TG");
+        if (e && *e) tg = std::max(32, std::min(1 << 16, atoi(e)));
+    }
+    const int gr = grid_for(n, c.num_sms);
+    BufP key = alloc_buf(c, (size_t)n * 4), flag = alloc_buf(c, (size_t)n), hist = alloc_buf(c, (SP_LONG_G + 1) * 8);
+    R->mask = alloc_buf(c, (size_t)((n + 31) / 32) * 4);
+    NBG_CUDA(cudaMemsetAsync(hist->d, 0, (SP_LONG_G + 1) * 8, c.stream));
+    k_rb_keys<<<gr, 256, 0, c.stream>>>(n, (const long long *)P.grp->d, (unsigned *)key->d, (unsigned char *)flag->d,
+                                        (unsigned long long *)hist->d, (unsigned *)R->mask->d);
+    BufP ids = alloc_buf(c, (size_t)n * 4), keys2 = alloc_buf(c, (size_t)n * 4),
+         sorted = alloc_buf(c, (size_t)n * 4), cnt = alloc_buf(c, 8);
+    size_t tb = 0;
+    thrust::counting_iterator<int> it0(0);
+    cub::DeviceSelect::Flagged(nullptr, tb, it0, (const unsigned char *)flag->d, (int *)ids->d, (long long *)cnt->d, (int64_t)n, c.stream);
+    BufP tmp = alloc_buf(c, std::max<size_t>(tb, 16));
+    NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, it0, (const unsigned char *)flag->d, (int *)ids->d, (long long *)cnt->d, (int64_t)n,
+                                        c.stream));
+    cub::DeviceSelect::Flagged(nullptr, tb, (const unsigned *)key->d, (const unsigned char *)flag->d, (unsigned *)keys2->d,
+                               (long long *)cnt->d, (int64_t)n, c.stream);
+    if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+    NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, (const unsigned *)key->d, (const unsigned char *)flag->d, (unsigned *)keys2->d,
+                                        (long long *)cnt->d, (int64_t)n, c.stream));
+    std::vector<unsigned long long> H(SP_LONG_G + 1);
+    NBG_CUDA(cudaMemcpyAsync(H.data(), hist->d, (SP_LONG_G + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    long long m = 0;
+    for (int g = 1; g <= SP_LONG_G; g++) m += (long long)H[g];
+    if (m > 0) {
+        const int bits = bits_for(SP_LONG_G + 1);
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned *)keys2->d, (unsigned *)key->d, (const int *)ids->d, (int *)sorted->d,
+                                        (int64_t)m, 0, bits, c.stream);
+        if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
+        NBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp->d, tb, (const unsigned *)keys2->d, (unsigned *)key->d, (const int *)ids->d,
+                                                 (int *)sorted->d, (int64_t)m, 0, bits, c.stream));
+    }
+    long long nlong = 0, nshort = 0;
+    for (int g = T + 1; g <= SP_LONG_G; g++) nlong += (long long)H[g];
+    for (int g = 1; g <= T && g <= SP_LONG_G; g++) nshort += (long long)H[g];
+    R->nlong = nlong;
+    R->nshort = nshort;
+    R->nslices = (nshort + 31) / 32;
+    // slice widths: g of the first (longest) row of each slice, from the descending g sequence
+    std::vector<int> swid((size_t)std::max<long long>(R->nslices, 1));
+    std::vector<long long> soff((size_t)std::max<long long>(R->nslices, 1));
+    {
+        long long pos = 0, sl = 0, off = 0;
+        for (int g = std::min(T, SP_LONG_G); g >= 1; g--) {
+            const long long end = pos + (long long)H[g];
+            for (; sl < R->nslices && 32 * sl < end; sl++) {
+                swid[sl] = g;
+                soff[sl] = off;
+                off += 32ll * g;
+            }
+            pos = end;
+        }
+        R->sell_groups = off;
+    }
+    // tasks: {kind | count << 2, first, base_lo, base_hi}
+    std::vector<int> tasks;
+    auto push = [&](int kind, long long count, long long first, long long base) {
+        tasks.push_back((int)(kind | (count << 2)));
+        tasks.push_back((int)first);
+        tasks.push_back((int)(unsigned)(base & 0xffffffffll));
+        tasks.push_back((int)(unsigned)((unsigned long long)base >> 32));
+    };
+    for (long long q = 0; q < P.nchunks; q++) push(0, 1, q, 0);
+    {
+        std::vector<int> lg;   // the long rows' g, in plan order (descending)
+        lg.reserve((size_t)nlong);
+        for (int g = SP_LONG_G; g > T; g--)
+            for (unsigned long long q = 0; q < H[g]; q++) lg.push_back(g);
+        long long j = 0;
+        while (j < nlong) {
+            const long long first = j;
+            long long cntr = 0, sum = 0;
+            while (j < nlong && cntr < 32 && (cntr == 0 || sum + lg[j] <= tg)) {
+                sum += lg[j];
+                cntr++;
+                j++;
+            }
+            push(1, cntr, first, 0);
+        }
+    }
+    {
+        const long long tl = std::max(1ll, tg / 32);   // lane-groups per slice task
+        long long s = 0;
+        while (s < R->nslices) {
+            const long long first = s;
+            long long cntr = 0, sum = 0;
+            while (s < R->nslices && cntr < 32 && (cntr == 0 || sum + swid[s] <= tl)) {
+                sum += swid[s];
+                cntr++;
+                s++;
+            }
+            push(2, cntr, first, soff[first]);
+        }
+    }
+    // empty-row ranges (kind 3, the inline-epilogue mode only): the epilogue of the rows without
+    // stored entries, 512 rows per task, interleaved evenly into the queue (streaming work that
+    // overlaps the gathers); the barrier mode runs only the first ntasks_main tasks
+    {
+        const long long RE = 512;
+        std::vector<int> mixed;
+        const long long nmain = (long long)tasks.size() / 4, nemp = (n + RE - 1) / RE;
+        mixed.reserve((size_t)(nmain + nemp) * 4);
+        long long e = 0;
+        for (long long t = 0; t <= nmain; t++) {
+            const long long want = nmain ? (t * nemp) / std::max(1ll, nmain) : nemp;   // empties placed before task t
+            for (; e < want && e < nemp; e++) {
+                const long long r0 = e * RE, cntr = std::min(RE, n - r0);
+                mixed.push_back((int)(3 | (cntr << 2)));
+                mixed.push_back((int)r0);
+                mixed.push_back(0);
+                mixed.push_back(0);
+            }
+            if (t < nmain) mixed.insert(mixed.end(), tasks.begin() + 4 * t, tasks.begin() + 4 * t + 4);
+        }
+        for (; e < nemp; e++) {
+            const long long r0 = e * RE, cntr = std::min(RE, n - r0);
+            mixed.push_back((int)(3 | (cntr << 2)));
+            mixed.push_back((int)r0);
+            mixed.push_back(0);
+            mixed.push_back(0);
+        }
+        R->ntasks_main = nmain;
+        R->tasks_main = alloc_buf(c, std::max<size_t>(tasks.size() * 4, 16));
+        if (!tasks.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks_main->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        tasks.swap(mixed);
+    }
+    R->ntasks = (long long)tasks.size() / 4;
+    R->tasks = alloc_buf(c, std::max<size_t>(tasks.size() * 4, 16));
+    if (!tasks.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    R->lrows = alloc_buf(c, (size_t)std::max<long long>(nlong, 1) * 4);
+    if (nlong > 0) NBG_CUDA(cudaMemcpyAsync(R->lrows->d, sorted->d, (size_t)nlong * 4, cudaMemcpyDeviceToDevice, c.stream));
+    R->srow = alloc_buf(c, (size_t)std::max<long long>(32 * R->nslices, 1) * 4);
+    R->swid = alloc_buf(c, (size_t)std::max<long long>(R->nslices, 1) * 4);
+    R->sell = alloc_buf(c, (size_t)std::max<long long>(R->sell_groups, 1) * 16);
+    if (R->nslices > 0) {
+        BufP so = alloc_buf(c, (size_t)R->nslices * 8);
+        NBG_CUDA(cudaMemcpyAsync(R->swid->d, swid.data(), (size_t)R->nslices * 4, cudaMemcpyHostToDevice, c.stream));
+        NBG_CUDA(cudaMemcpyAsync(so->d, soff.data(), (size_t)R->nslices * 8, cudaMemcpyHostToDevice, c.stream));
+        k_rb_fill<<<grid_for(32 * R->nslices, c.num_sms), 256, 0, c.stream>>>(
+            32 * R->nslices, nshort, (const int *)sorted->d + nlong, (const long long *)P.grp->d, (const int4 *)P.cg->d,
+            (const int *)R->swid->d, (const long long *)so->d, (int *)R->srow->d, (int4 *)R->sell->d);
+        NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
+    }
+    R->tot = alloc_buf(c, (size_t)n * 8);
+    R->bar = alloc_buf(c, 16);
+    NBG_CUDA(cudaMemsetAsync(R->bar->d, 0, 16, c.stream));
+    NBG_CUDA(cudaGetLastError());
+    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    c.stats.kernels_launched += 5;
+    P.rb = std::move(R);
+    return P.rb.get();
+}
 
 TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta) {
     if (!A.plan) gpu_build_spmv_plan(c, A);

@@ -42,6 +42,15 @@ struct KArgs {
     long long ncols_g;
     void *peer[8];
     int npeer;
+    const int *rb_tasks;
+    const int *rb_sell;
+    const int *rb_srow;
+    const int *rb_swid;
+    const int *rb_lrows;
+    const unsigned *rb_mask;
+    void *rb_tot;
+    unsigned *rb_bar;
+    long long rb_ntasks;
 };
 
 // ------------------------------------------------------------------ operators in type T
@@ -401,6 +410,46 @@ __device__ void nbg_block_finish_i(long long v, int kind, u64 *acc, double *sh) 
 }
 
 // loads that bypass / hint the caches
+
+// Grid-wide barrier of a persistent kernel whose CTAs are all resident (one per SM, grid <= SMs):
+// bar[0] counts arrivals, bar[1] is the generation.  The generation is read before arriving, the
+// last arriver resets the count (and `reset`, a counter every CTA is done with) and releases the
+// next generation; the others spin on it.  Writes
+// before the barrier (any CTA) are visible to reads after it (fences on both sides, __syncthreads).
+__device__ __forceinline__ void nbg_grid_sync(unsigned *bar, unsigned *reset = nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned gen;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
+        __threadfence();
+        const unsigned old = atomicAdd(bar, 1u);
+        if (old == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            if (reset) atomicExch(reset, 0u);   // a counter every CTA is done with (the next launch starts from 0)
+            __threadfence();
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(bar + 1) : "memory");
+        } else {
+            unsigned cur;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+                if (cur != gen) break;
+                __nanosleep(64);
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// bulk prefetch of [p, p + bytes) into L2 (TMA engine, fire and forget); p 16-byte aligned
+__device__ __forceinline__ void nbg_prefetch_l2(const void *p, long long bytes) {
+    bytes &= ~15ll;
+    for (long long o = 0; o < bytes; o += (1ll << 20)) {
+        const unsigned b = (unsigned)((bytes - o) < (1ll << 20) ? (bytes - o) : (1ll << 20));
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"((const char *)p + o), "r"(b) : "memory");
+    }
+}
+
 __device__ __forceinline__ int nbg_ld_stream(const int *p) { return __ldcs(p); }
 
 // ------------------------------------------------------------------ TMA bulk copies + mbarriers

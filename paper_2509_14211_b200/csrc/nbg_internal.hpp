@@ -127,6 +127,7 @@ double slot_value(const unsigned long long *s, SFmt fmt);
 
 struct TpPlan;
 
+struct RbPlan;
 struct SpmvPlan {
     // Rows are stored in 4-entry groups (padded with index -1) so a 16-byte index load never mixes
     // two rows.  Tiles: runs of <= 32 consecutive rows with <= 512 groups (one warp task, lane j ->
@@ -153,6 +154,31 @@ struct SpmvPlan {
     BufP iperm;              // int32[ncols_g] new -> old id
     BufP colidx_g;           // int32[nnz] gather-layout column indices (relabelled matrices; two-phase build)
     std::unique_ptr<TpPlan> tp[2];   // two-phase plans for 4- and 8-byte gathered elements (lazy)
+    std::unique_ptr<RbPlan> rb;   // row-binned plan (lazy, DESIGN.md §7 "row-binned SpMV")
+};
+
+// Row-binned SpMV plan (DESIGN.md §7 "row-binned SpMV"), built once per matrix on top of the
+// group-padded plan.  Rows are binned by length in 4-entry groups g:
+//   short (1 <= g <= T): sorted by g descending (ties by row id), cut into 32-row slices; a slice
+//        is stored column-major (group k of its lane-l row at soff + 32 k + l, -1 padded to the
+//        slice width), so one warp sums 32 rows lane-per-row with coalesced 512-byte index loads;
+//   long  (T < g <= 512): g descending, one warp per row over the group-padded CSR;
+//   hub   (g > 512): the group-padded plan's chunks (one warp each, combined in chunk order).
+// Every row total goes to tot[row]; after a grid barrier the same kernel runs the fused epilogue
+// over the rows in index order.  A row's summation order depends on its length only.
+struct RbPlan {
+    int T = 16;                  // short-row bound in groups
+    int64_t nshort = 0, nslices = 0, nlong = 0, ntasks = 0, ntasks_main = 0, sell_groups = 0;
+    BufP sell;      // int4[sell_groups]  short slices, column-major, -1 padded
+    BufP srow;      // int32[32 * nslices]  destination row of each slice slot (-1: none)
+    BufP swid;      // int32[nslices]  slice width in groups
+    BufP lrows;     // int32[nlong]  long rows, g descending
+    BufP tasks;     // int4[ntasks]  {kind | count << 2, first, base_lo, base_hi}: 0 hub chunk, 1 long rows, 2 short slices,
+                    //   3 empty-row range (inline-epilogue mode), interleaved
+    BufP tasks_main;   // int4[ntasks_main]  the same without kind 3 (barrier mode)
+    BufP mask;      // u32[(n + 31) / 32]  bit i: row i is non-empty
+    BufP tot;       // 8 bytes per row: row totals (the kernel's row-total type)
+    BufP bar;       // u32[2]  grid barrier {arrivals, generation}
 };
 
 // Two-phase column-blocked SpMV plan, one per gathered element size.
@@ -265,6 +291,8 @@ struct Prog {
     bool spmv = false;
     bool tp = false;        // spmv through the two-phase plan: this program is phase 2 (combine + epilogue)
     bool lpr = false;       // spmv, lane-per-row skeleton (low-skew matrices)
+    bool rb = false;        // spmv, row-binned skeleton (RbPlan)
+    bool rb_inline = false; // row-binned: epilogue at each row's completion (no barrier); else totals + grid barrier + epilogue pass
     int nt = 0, hot_kb = 0; // spmv (task skeleton): threads per CTA and hot-cache KB, chosen per matrix
     bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
     bool tma = false;       // ewise: inputs staged through shared memory by TMA bulk copies (large n)
@@ -309,6 +337,16 @@ struct KArgs {
     long long ncols_g;           // phase 1: columns of the gather layout
     void *peer[MAX_PEER];        // multi-store output: the exchange buffers of all ranks
     int npeer;
+    // row-binned spmv (RbPlan)
+    const int *rb_tasks;         // int4 task records
+    const int *rb_sell;          // int4 short-slice groups
+    const int *rb_srow;
+    const int *rb_swid;
+    const int *rb_lrows;
+    const unsigned *rb_mask;
+    void *rb_tot;
+    unsigned *rb_bar;
+    long long rb_ntasks;
 };
 
 struct Kernel {
@@ -498,6 +536,8 @@ bool spmv_epilogue_prefetch();  // SpMV prefetches the epilogue's row inputs at 
 int spmv_threads(int xsize);
 int spmv_groups_per_lane();   // SpMV task skeleton: groups per lane per step (NBG_SPMV_GPL, default 2)
 void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb);   // per-matrix SpMV launch shape   // threads per SpMV CTA for a gathered element size (NBG_SPMV_THREADS overrides)
+int spmv_rb_mode();    // NBG_SPMV_RB: -1 auto (skewed matrices), 0 never, 1 always
+bool spmv_rb_inline(); // NBG_RB_MODE: b (default) totals + grid barrier + epilogue pass, i epilogue at each row's completion
 int spmv_lpr_mode();   // NBG_SPMV_LPR: -1 auto (by skew), 0 never, 1 always   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);
@@ -522,6 +562,7 @@ struct DistGraph {
 DistGraph gpu_dist_graph(Ctx &c, const nbg_graphgen &g, int rank, int P, long long bytes_per_row,
                          const std::function<void(int *, long long)> &allreduce_int_sum);
 TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta);   // null if not applicable
+RbPlan *gpu_rb_plan(Ctx &c, Mat &A);                         // null if not applicable (valued matrices)
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
 void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng);
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);

@@ -698,6 +698,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     bool vec = true;
     for (int k = 0; k < p.n_in; k++) vec = vec && (((uintptr_t)args.in[k]) % 16 == 0);
     for (int k = 0; k < p.n_out; k++) vec = vec && (((uintptr_t)args.out[k]) % 16 == 0);
+    for (int k = 0; k < p.n_out; k++) vec = vec && (((uintptr_t)args.oscat[k]) % 16 == 0);   // scatter maps: int4 loads
     p.vec = p.spmv ? true : vec;
     // TMA-staged elementwise skeleton (codegen gen_ewise), opt-in: NBG_EWISE_TMA=1.  Measured on
     // C2: fp32 29.8 us vs 29.1 with the register skeleton, fp64 56.1 vs 56.4 -- the
@@ -760,6 +761,29 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             p.nt = p.hot_kb = 0;
             items = (n + 255) / 256;
         }
+        // row-binned skeleton (DESIGN.md §7 "row-binned SpMV") for skewed matrices without values
+        // (the choice does not depend on the gather layout, so relabelled and plain layouts keep
+        // identical sums); NBG_SPMV_RB overrides (1: any matrix without values, 0: never)
+        p.rb = false;
+        const int rbm = spmv_rb_mode();
+        if (!T && !p.lpr && !A.vals && (rbm == 1 || (rbm == -1 && !A.plan->low_skew))) {
+            RbPlan *R = gpu_rb_plan(c, A);
+            if (R) {
+                p.rb = true;
+                p.vec = vec;   // the epilogue uses 16-byte vector loads when every buffer allows them
+                p.rb_inline = spmv_rb_inline();
+                args.rb_tasks = (const int *)(p.rb_inline ? R->tasks->d : R->tasks_main->d);
+                args.rb_sell = (const int *)R->sell->d;
+                args.rb_srow = (const int *)R->srow->d;
+                args.rb_swid = (const int *)R->swid->d;
+                args.rb_lrows = (const int *)R->lrows->d;
+                args.rb_mask = (const unsigned *)R->mask->d;
+                args.rb_tot = R->tot->d;
+                args.rb_bar = (unsigned *)R->bar->d;
+                args.rb_ntasks = p.rb_inline ? R->ntasks : R->ntasks_main;
+                items = 1ll << 40;   // persistent: one CTA per SM (clamped to the kernel's grid_cap)
+            }
+        }
         if (T) {
             p.tp = true;
             p.nt = p.hot_kb = 0;
@@ -817,7 +841,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     auto it = c.plans.find(sig);
     if (it == c.plans.end()) {
         char nm[48];
-        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? (p.lpr ? "spmvl" : "spmv") : "ewise"), (unsigned long long)hash_str(sig));
+        snprintf(nm, sizeof nm, "nbg_%s_%016llx", p.tp ? "tp2" : (p.spmv ? (p.lpr ? "spmvl" : (p.rb ? "spmvr" : "spmv")) : "ewise"), (unsigned long long)hash_str(sig));
         int smem = 0, hot = 0;
         std::string src = codegen(p, nm, &smem, &hot);
         kern = jit_compile(c, src, nm, p.spmv && !p.tp && !p.lpr, smem, (p.spmv && !p.tp && !p.lpr) ? p.nt : 0);

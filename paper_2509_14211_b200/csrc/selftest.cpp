@@ -99,8 +99,12 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
             if (!compile_only(codegen(p, nm), nm, log)) fails++;
             p.lpr = true;
             p.outs[1].scatter = true;        // y_next written in the gather layout (side output)
-            nm += "_lpr";
-            if (!compile_only(codegen(p, nm), nm, log)) fails++;
+            if (!compile_only(codegen(p, nm + "_lpr"), nm + "_lpr", log)) fails++;
+            p.lpr = false;
+            p.rb = true;                     // row-binned skeleton (the C4 default), both epilogue modes
+            if (!compile_only(codegen(p, nm + "_rb"), nm + "_rb", log)) fails++;
+            p.rb_inline = true;
+            if (!compile_only(codegen(p, nm + "_rbi"), nm + "_rbi", log)) fails++;
         }
         // (3) plain mxv for every monoid x type x mul, iso and valued matrices
         int k = 0;
@@ -131,6 +135,21 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
                 std::string nm = "selftest_mxvl_" + std::to_string(k++);
                 if (!compile_only(codegen(p, nm), nm, log)) fails++;
             }
+        // (3c) the row-binned skeleton for every monoid x type (iso matrices)
+        for (int add : {NBG_PLUS, NBG_MIN, NBG_MAX})
+            for (int T : {NBG_BOOL, NBG_INT32, NBG_INT64, NBG_FP32, NBG_FP64})
+                for (int mul : {NBG_TIMES, NBG_SECOND}) {
+                    Prog p;
+                    p.spmv = true;
+                    p.rb = true;
+                    p.rb_inline = (k & 1) != 0;
+                    p.sp.add = add; p.sp.mul = mul; p.sp.T = T; p.sp.xt = T == NBG_BOOL ? NBG_FP32 : T; p.sp.at = NBG_INT32;
+                    p.ins.push_back(I(Ins::MXV_ACC, T));
+                    p.outs.push_back(OutV{0, 0});
+                    p.n_out = 1; p.n_imm = 2;
+                    std::string nm = "selftest_mxvr_" + std::to_string(k++);
+                    if (!compile_only(codegen(p, nm), nm, log)) fails++;
+                }
         // (4) reductions of every kind
         for (int T : {NBG_INT32, NBG_INT64, NBG_FP32, NBG_FP64})
             for (int mono : {NBG_PLUS, NBG_MIN, NBG_MAX}) {
