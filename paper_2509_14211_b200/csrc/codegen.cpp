@@ -1234,7 +1234,20 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     o << "  const int4* __restrict__ CG = (const int4*)a.colidx;\n";
     o << "  const int4* __restrict__ SELL = (const int4*)a.rb_sell;\n";
     o << "  const long long* __restrict__ GRP = a.rowptr;\n";
-    if (!IE) o << "  " << RT << "* __restrict__ TOT = (" << RT << "*)a.rb_tot;\n";
+    // barrier mode: row totals go to a plain output of the region with the row-total width when there
+    // is one (the epilogue pass reads each total and overwrites it in place: one 4-byte array less in
+    // L2 next to the index stream), else to the plan's tot buffer
+    std::string totbuf = "a.rb_tot";
+    if (!IE) {
+        const char *e = getenv("NBG_RB_TOTOUT");
+        if (!(e && e[0] == '0'))
+            for (const OutV &ov : p.outs)
+                if (!ov.scatter && !ov.multi && type_size(p.ins[ov.ins].t) == (RT == "float" || RT == "int" ? 4u : 8u)) {
+                    totbuf = "a.out[" + std::to_string(ov.out) + "]";
+                    break;
+                }
+        o << "  " << RT << "* TOT = (" << RT << "*)" << totbuf << ";\n";
+    }
     o << "  const int hc = (int)a.hc;\n";
     o << "  {\n";
     o << "    const int nv_ = ((((unsigned long long)X) & 15ull) == 0ull) ? (int)((hc * sizeof(" << XT << ")) >> 4) : 0;\n";
@@ -1450,33 +1463,57 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
         for (const OutV &ov : p.outs)
             if (!ov.scatter) out_type[ov.out] = p.ins[ov.ins].t;
         const int rtt = RT == "float" ? NBG_FP32 : (RT == "double" ? NBG_FP64 : (RT == "int" ? NBG_INT32 : NBG_INT64));
-        std::string tl = vload(rtt, "a.rb_tot", "vi", "T_");
-        for (size_t q = tl.find("__ldg("); q != std::string::npos; q = tl.find("__ldg(", q)) tl.replace(q, 6, "__ldcg(");
+        // U trips per iteration: every load of the U trips is issued before the first store (the
+        // compiler cannot move loads above stores that may alias them)
+        int U = 1;
+        {
+            const char *e = getenv("NBG_RB_BU");
+            if (e && (e[0] == '1' || e[0] == '2' || e[0] == '4')) U = e[0] - '0';
+        }
         o << "  const long long nv_ = a.n >> 2;\n  tail0_ = nv_ << 2;\n";
-        o << "  for (long long vi = (long long)blockIdx.x * blockDim.x + threadIdx.x; vi < nv_; vi += stride_) {\n";
+        o << "  for (long long vb_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv_; vb_ += " << U << " * stride_) {\n";
         for (int s2 = 0; s2 < p.n_in; s2++)
-            if (slot_type[s2] >= 0) {
-                o << "    " << ctype(slot_type[s2]) << " L" << s2 << "[4];\n";
-                o << "    " << vload(slot_type[s2], "a.in[" + std::to_string(s2) + "]", "vi", "L" + std::to_string(s2)) << "\n";
-            }
-        o << "    " << RT << " T_[4];\n    " << tl << "\n";
-        o << "    const unsigned mb_ = (__ldcg(a.rb_mask + ((vi << 2) >> 5)) >> ((vi << 2) & 31)) & 15u;\n";
+            if (slot_type[s2] >= 0) o << "    " << ctype(slot_type[s2]) << " L" << s2 << "[" << U << "][4];\n";
+        o << "    " << RT << " T_[" << U << "][4];\n";
+        o << "    unsigned mb_[" << U << "];\n";
         for (const OutV &ov : p.outs)
-            if (ov.scatter) o << "    " << g.scat_preload(ov, "vi") << "\n";
+            if (ov.scatter) o << "    int4 MM" << ov.out << "_[" << U << "];\n";
+        o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
+        o << "      const long long vi = vb_ + u * stride_;\n";
+        o << "      if (vi < nv_) {\n";
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0)
+                o << "        " << vload(slot_type[s2], "a.in[" + std::to_string(s2) + "]", "vi", "L" + std::to_string(s2) + "[u]") << "\n";
+        {
+            std::string tl2 = vload(rtt, totbuf, "vi", "T_[u]");
+            for (size_t q = tl2.find("__ldg("); q != std::string::npos; q = tl2.find("__ldg(", q)) tl2.replace(q, 6, "__ldcg(");
+            o << "        " << tl2 << "\n";
+        }
+        o << "        mb_[u] = (__ldcg(a.rb_mask + ((vi << 2) >> 5)) >> ((vi << 2) & 31)) & 15u;\n";
+        for (const OutV &ov : p.outs)
+            if (ov.scatter) o << "        MM" << ov.out << "_[u] = __ldg(((const int4*)a.oscat[" << ov.out << "]) + vi);\n";
+        o << "      }\n";
+        o << "    }\n";
+        o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
+        o << "      const long long vi = vb_ + u * stride_;\n";
+        o << "      if (vi >= nv_) break;\n";
+        for (const OutV &ov : p.outs)
+            if (ov.scatter) o << "      const int4 M" << ov.out << "_ = MM" << ov.out << "_[u];\n";
         for (int k2 = 0; k2 < p.n_out; k2++)
-            if (out_type[k2] >= 0) o << "    " << ctype(out_type[k2]) << " O" << k2 << "[4];\n";
-        o << "    #pragma unroll\n    for (int e = 0; e < 4; e++) {\n";
-        o << "      const " << ACC << " acc = ((mb_ >> e) & 1u) ? (" << ACC << ")T_[e] : (" << ACC << ")(" << IDENT << ");\n";
+            if (out_type[k2] >= 0) o << "      " << ctype(out_type[k2]) << " O" << k2 << "[4];\n";
+        o << "      #pragma unroll\n      for (int e = 0; e < 4; e++) {\n";
+        o << "        const " << ACC << " acc = ((mb_[u] >> e) & 1u) ? (" << ACC << ")T_[u][e] : (" << ACC << ")(" << IDENT << ");\n";
         g.emit_body(
-            "      ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
+            "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[u][e]"; },
             [&](const OutV &ov) {
                 if (ov.scatter) return g.scat_pre(ov, "e");
                 return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
             },
             [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
-        o << "    }\n";
+        o << "      }\n";
         for (int k2 = 0; k2 < p.n_out; k2++)
-            if (out_type[k2] >= 0) o << "    " << vstore(out_type[k2], "a.out[" + std::to_string(k2) + "]", "vi", "O" + std::to_string(k2)) << "\n";
+            if (out_type[k2] >= 0) o << "      " << vstore(out_type[k2], "a.out[" + std::to_string(k2) + "]", "vi", "O" + std::to_string(k2)) << "\n";
+        o << "    }\n";
         o << "  }\n";
     }
     o << "  for (long long i = tail0_ + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride_) {\n";

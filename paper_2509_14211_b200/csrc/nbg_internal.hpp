@@ -167,7 +167,7 @@ struct SpmvPlan {
 // Every row total goes to tot[row]; after a grid barrier the same kernel runs the fused epilogue
 // over the rows in index order.  A row's summation order depends on its length only.
 struct RbPlan {
-    int T = 16;                  // short-row bound in groups
+    int T = 32;                  // short-row bound in groups (C4: T 8 / 16 / 32 / 64 / 128 -> 209 / 171 / 168 / 171 / 194 us)
     int64_t nshort = 0, nslices = 0, nlong = 0, ntasks = 0, ntasks_main = 0, sell_groups = 0;
     BufP sell;      // int4[sell_groups]  short slices, column-major, -1 padded
     BufP srow;      // int32[32 * nslices]  destination row of each slice slot (-1: none)

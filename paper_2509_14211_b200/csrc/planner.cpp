@@ -761,12 +761,13 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             p.nt = p.hot_kb = 0;
             items = (n + 255) / 256;
         }
-        // row-binned skeleton (DESIGN.md §7 "row-binned SpMV") for skewed matrices without values
-        // (the choice does not depend on the gather layout, so relabelled and plain layouts keep
-        // identical sums); NBG_SPMV_RB overrides (1: any matrix without values, 0: never)
+        // row-binned skeleton (DESIGN.md §7 "row-binned SpMV") for large skewed matrices without
+        // values (C4 165 vs 178 us, C5 3.73 vs 3.90 ms per sweep; small ones keep the task skeleton:
+        // C1 21.9 vs 14.9 us).  The choice does not depend on the gather layout, so relabelled and
+        // plain layouts keep identical sums.  NBG_SPMV_RB overrides (1: any matrix without values, 0: never)
         p.rb = false;
         const int rbm = spmv_rb_mode();
-        if (!T && !p.lpr && !A.vals && (rbm == 1 || (rbm == -1 && !A.plan->low_skew))) {
+        if (!T && !p.lpr && !A.vals && (rbm == 1 || (rbm == -1 && !A.plan->low_skew && A.nnz >= (1ll << 19)))) {
             RbPlan *R = gpu_rb_plan(c, A);
             if (R) {
                 p.rb = true;
