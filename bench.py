@@ -159,9 +159,10 @@ def run_ours(args, rank, world, local_rank):
     kind = nbg.GRAPH_RMAT if cfg["graph"] == "rmat" else nbg.GRAPH_ER
     t0 = time.time()
     cuts = None
-    # the per-rank data plane at one rank too (NBG_BENCH_DIST=1): symmetric relabel, rows in the
-    # gather layout, the next sweep's gathered vector written in row order
-    use_dist = world > 1 or os.environ.get("NBG_BENCH_DIST", "0") == "1"
+    # the per-rank data plane at one rank too (default; NBG_BENCH_DIST=0 for nbg_pagerank on the
+    # generator's plain CSR): symmetric relabel, rows in the gather layout, the next sweep's gathered
+    # vector written in row order into its slice (C4 156.5 vs 164.8 us per sweep)
+    use_dist = world > 1 or (os.environ.get("NBG_BENCH_DIST", "1") == "1" and not args.mtx)
     if use_dist:
         # per-rank setup: every rank regenerates the edges, keeps its share,
         # degrees summed over NCCL, symmetric relabel, byte-balanced row block -- no rank builds the
@@ -337,13 +338,15 @@ def run_ours(args, rank, world, local_rank):
                 "workload": workload_name(args, cfg),
                 "n": n, "nnz": nnz, "dangling": cfg["dangling"], "alpha": cfg["alpha"], "tol": tol,
                 "itermax": itermax, "sweeps_per_step": sweeps_total / args.steps,
-                "parallelism": f"rows{world}" if world > 1 else "single",
+                "parallelism": f"rows{world}" if world > 1 else ("single (per-rank data plane, P = 1)" if use_dist else "single"),
                 **({"exchange": os.environ.get("NBG_DIST_EXCHANGE", "collective")} if world > 1 else {}),
+                "layout": "symmetric gather-layout relabel (rows and columns by descending out-degree, dangling last)"
+                          if use_dist else "column gather layout, rows in generator order",
                 "l2": l2_note(nnz, ncols_g * w),
                 "setup_s": round(setup_s, 3),
             },
             "roofline": {
-                "bound": "hbm", "kernel": "fused SpMV sweep (nbg_spmv_*)",
+                "bound": "hbm", "kernel": "fused SpMV sweep (nbg_spmv*: row-binned nbg_spmvr_* on C4 / C5)",
                 "achieved": round(achieved, 1), "peak": pk, "peak_source": pk_src, "unit": "GB/s",
                 "frac": round(achieved / pk, 4), "traffic": traffic,
                 "bytes_per_launch_ns": int(b_ns), "bytes_per_launch_fused": int(b_fused),

@@ -89,7 +89,7 @@ static void sig_emit(const Prog &p, S &s) {
     s.ch('|');
     for (const OutV &o : p.outs) {
         s.put(o.ins, '>');
-        s.put(o.out, o.multi ? 'm' : (o.scatter ? 's' : ';'));
+        s.put(o.out, o.affine ? (o.multi ? 'A' : 'a') : (o.multi ? 'm' : (o.scatter ? 's' : ';')));
     }
     s.ch('|');
     for (const RedOut &r : p.reds) {
@@ -123,6 +123,7 @@ struct Gen {
     // store of output ov at element index `idx` (plain, or scattered through a.oscat)
     std::string scat(const OutV &ov, const std::string &idx) const {
         const std::string o = std::to_string(ov.out), T = ctype(p.ins[ov.ins].t);
+        if (ov.affine) return aff(ov, idx);
         if (ov.multi)   // the exchange: the same element stored into every rank's buffer (P2P over NVLink)
             return std::string("{ const int d_ = a.oscat[") + o + "][" + idx + "]; if (d_ >= 0) { const " + T + " v_ = " + v(ov.ins) +
                    "; for (int q_ = 0; q_ < a.npeer; q_++) ((" + T + "*)a.peer[q_])[d_] = v_; } }";
@@ -132,12 +133,23 @@ struct Gen {
     // vector skeletons: the scatter map of 4 consecutive elements loaded once, before any store of
     // the trip (a per-element map load after the previous element's store cannot be hoisted above
     // it -- the compiler must assume they alias -- so each element would cost a round trip)
+    // affine target (contiguous slice of an exchange buffer): out[ooff + i] for i < olim, no map
+    std::string aff(const OutV &ov, const std::string &idx) const {
+        const std::string o = std::to_string(ov.out), T = ctype(p.ins[ov.ins].t);
+        const std::string d = "a.ooff[" + o + "] + (" + idx + ")";
+        if (ov.multi)
+            return "{ if ((" + idx + ") < a.olim[" + o + "]) { const " + T + " v_ = " + v(ov.ins) + "; for (int q_ = 0; q_ < a.npeer; q_++) ((" + T +
+                   "*)a.peer[q_])[" + d + "] = v_; } }";
+        return "{ if ((" + idx + ") < a.olim[" + o + "]) ((" + T + "*)a.out[" + o + "])[" + d + "] = " + v(ov.ins) + "; }";
+    }
     std::string scat_preload(const OutV &ov, const std::string &vi) const {
         const std::string o = std::to_string(ov.out);
+        if (ov.affine) return "";
         return "const int4 M" + o + "_ = __ldg(((const int4*)a.oscat[" + o + "]) + " + vi + ");";
     }
-    std::string scat_pre(const OutV &ov, const std::string &e) const {
+    std::string scat_pre(const OutV &ov, const std::string &e, const std::string &idx) const {
         const std::string o = std::to_string(ov.out), T = ctype(p.ins[ov.ins].t);
+        if (ov.affine) return aff(ov, idx);
         const std::string d = "(" + e + " == 0 ? M" + o + "_.x : (" + e + " == 1 ? M" + o + "_.y : (" + e + " == 2 ? M" + o + "_.z : M" + o + "_.w)))";
         if (ov.multi)
             return std::string("{ const int d_ = ") + d + "; if (d_ >= 0) { const " + T + " v_ = " + v(ov.ins) +
@@ -561,7 +573,7 @@ int gen_ewise(Gen &g, const std::string &kname, bool vec) {
         g.emit_body(
             "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[u][e]"; },
             [&](const OutV &ov) {
-                if (ov.scatter) return g.scat_pre(ov, "e");
+                if (ov.scatter) return g.scat_pre(ov, "e", "(vi * 4 + e)");
                 return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
             },
             [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "");
@@ -857,7 +869,7 @@ int gen_spmv(Gen &g, const std::string &kname, int *hot_entries) {
             if (slot_sz[s] > 0)
                 pf << " asm volatile(\"prefetch.global.L1 [%0];\" :: \"l\"((const char*)a.in[" << s << "] + " << slot_sz[s] << " * i));";
         for (const OutV &ov : p.outs)
-            if (ov.scatter) pf << " asm volatile(\"prefetch.global.L1 [%0];\" :: \"l\"(a.oscat[" << ov.out << "] + i));";
+            if (ov.scatter && !ov.affine) pf << " asm volatile(\"prefetch.global.L1 [%0];\" :: \"l\"(a.oscat[" << ov.out << "] + i));";
         if (!pf.str().empty()) {
             o << "      if (!is_chunk) {\n";
             o << "        #pragma unroll\n        for (int r = 0; r < 4; r++) { const long long i = (long long)tl.x + lane + 32 * r; if (lane + 32 * r < R) {" << pf.str() << " } }\n";
@@ -1477,7 +1489,7 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
         o << "    " << RT << " T_[" << U << "][4];\n";
         o << "    unsigned mb_[" << U << "];\n";
         for (const OutV &ov : p.outs)
-            if (ov.scatter) o << "    int4 MM" << ov.out << "_[" << U << "];\n";
+            if (ov.scatter && !ov.affine) o << "    int4 MM" << ov.out << "_[" << U << "];\n";
         o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
         o << "      const long long vi = vb_ + u * stride_;\n";
         o << "      if (vi < nv_) {\n";
@@ -1491,14 +1503,14 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
         }
         o << "        mb_[u] = (__ldcg(a.rb_mask + ((vi << 2) >> 5)) >> ((vi << 2) & 31)) & 15u;\n";
         for (const OutV &ov : p.outs)
-            if (ov.scatter) o << "        MM" << ov.out << "_[u] = __ldg(((const int4*)a.oscat[" << ov.out << "]) + vi);\n";
+            if (ov.scatter && !ov.affine) o << "        MM" << ov.out << "_[u] = __ldg(((const int4*)a.oscat[" << ov.out << "]) + vi);\n";
         o << "      }\n";
         o << "    }\n";
         o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
         o << "      const long long vi = vb_ + u * stride_;\n";
         o << "      if (vi >= nv_) break;\n";
         for (const OutV &ov : p.outs)
-            if (ov.scatter) o << "      const int4 M" << ov.out << "_ = MM" << ov.out << "_[u];\n";
+            if (ov.scatter && !ov.affine) o << "      const int4 M" << ov.out << "_ = MM" << ov.out << "_[u];\n";
         for (int k2 = 0; k2 < p.n_out; k2++)
             if (out_type[k2] >= 0) o << "      " << ctype(out_type[k2]) << " O" << k2 << "[4];\n";
         o << "      #pragma unroll\n      for (int e = 0; e < 4; e++) {\n";
@@ -1506,7 +1518,7 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
         g.emit_body(
             "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[u][e]"; },
             [&](const OutV &ov) {
-                if (ov.scatter) return g.scat_pre(ov, "e");
+                if (ov.scatter) return g.scat_pre(ov, "e", "(vi * 4 + e)");
                 return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
             },
             [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");

@@ -550,7 +550,8 @@ nbg_status nbg_vector_allgather_reduce(nbg_ctx *ctx, nbg_vector *w, nbg_vector u
         }
         std::vector<NodeP> roots;
         if (!x->mat) {
-            ctx->out_targets[x.get()] = Ctx::OutTarget{W, (const int *)map->d, peers};
+            // the map is affine (gpu_offset_map): the fused kernel stores to W[c0 + i], i < ncols_g - c0
+            ctx->out_targets[x.get()] = Ctx::OutTarget{W, (const int *)map->d, peers, c0, std::max<int64_t>(0, std::min(nb, ncols_g - c0))};
             roots.push_back(x);
         }
         for (const NodeP &sn : sin)

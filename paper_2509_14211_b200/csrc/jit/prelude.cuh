@@ -51,6 +51,7 @@ struct KArgs {
     void *rb_tot;
     unsigned *rb_bar;
     long long rb_ntasks;
+    long long ooff[NBG_MAX_OUT], olim[NBG_MAX_OUT];
 };
 
 // ------------------------------------------------------------------ operators in type T

@@ -273,7 +273,7 @@ struct Ins {
 
 // scatter: out[oscat[i]] (skip < 0); multi: the scattered value stored into every a.peer[q] buffer
 // (the multi-GPU exchange fused into the producing kernel, dist.cpp peer mode)
-struct OutV { int ins; int out; bool scatter = false; bool multi = false; };
+struct OutV { int ins; int out; bool scatter = false; bool multi = false; bool affine = false; };   // affine: out[ooff + i], i < olim (no map)
 struct RedOut { int ins; int monoid; int racc; uint8_t fmt; };
 
 struct SpmvSig {
@@ -347,6 +347,7 @@ struct KArgs {
     void *rb_tot;
     unsigned *rb_bar;
     long long rb_ntasks;
+    long long ooff[MAX_OUT], olim[MAX_OUT];   // affine outputs: out[ooff + i] for i < olim
 };
 
 struct Kernel {
@@ -456,7 +457,9 @@ struct Ctx {
 
     // output targets of the current materialize call (multi-GPU: a block written straight into
     // the exchange buffer through a scatter map); see dist.cpp nbg_vector_allgather_reduce
-    struct OutTarget { BufP buf; const int *map = nullptr; std::vector<void *> peers; };   // peers: multi-store
+    // peers: multi-store; alim >= 0: the map is affine (row i -> aoff + i for i < alim, else skipped) and
+    // the kernels store without it
+    struct OutTarget { BufP buf; const int *map = nullptr; std::vector<void *> peers; int64_t aoff = 0, alim = -1; };
     std::unordered_map<const Node *, OutTarget> out_targets;
     // nodes user handles point to (weak): nbg_wait_all materialises the live pending ones
     std::vector<std::weak_ptr<Node>> user_nodes;

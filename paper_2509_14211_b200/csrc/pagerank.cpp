@@ -264,11 +264,22 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
     if (ds) nbg_scalar_free(ctx, ds);
     std::vector<nbg_scalar> deltas;
     int k = 1;
+    double dm1 = -1.0, dm2 = -1.0, dm3 = -1.0;   // delta_{k-1}, delta_{k-2}, delta_{k-3} (convergence mode)
     for (;;) {
         nbg_vector rnext = nullptr, xnext = nullptr;
         nbg_scalar dnext = nullptr, dsnext = nullptr;
         const bool more = k < p->itermax;
-        if (more) TRY(sweep(rk, xk, dsk, &rnext, &xnext, &dnext, &dsnext));   // launched before delta_k is read
+        // the same convergence prediction as nbg_pagerank (every rank sees the same exact deltas, so
+        // every rank takes the same decision): wait for delta_k instead of speculating when the
+        // geometric decay predicts that sweep k is the last one
+        bool last_likely = false;
+        if (conv && dm1 > 0.0 && dm2 > 0.0) {
+            const double q1 = dm1 / dm2;
+            const double spread = dm3 > 0.0 ? std::fabs(q1 - dm2 / dm3) / q1 : 1.0;
+            last_likely = dm1 * q1 <= p->tol * (1.0 + std::min(1.0, 3.0 * spread));
+        }
+        const bool spec = more && !last_likely;
+        if (spec) TRY(sweep(rk, xk, dsk, &rnext, &xnext, &dnext, &dsnext));   // launched before delta_k is read
         bool stop = !more;
         if (conv) {
             double v = 0.0;
@@ -277,6 +288,10 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
             nbg_scalar_free(ctx, dk);
             dk = nullptr;
             if (!(v > p->tol)) stop = true;   // identical on every rank: the sum is exact
+            dm3 = dm2;
+            dm2 = dm1;
+            dm1 = v;
+            if (!stop && more && !spec) TRY(sweep(rk, xk, dsk, &rnext, &xnext, &dnext, &dsnext));   // mispredicted: launch now
         } else {
             deltas.push_back(dk);
             dk = nullptr;

@@ -598,6 +598,7 @@ struct Builder {
         auto tg = c.out_targets.find(x.get());
         ov.scatter = (bool)scatter || tg != c.out_targets.end();
         ov.multi = tg != c.out_targets.end() && !tg->second.peers.empty();
+        ov.affine = tg != c.out_targets.end() && tg->second.alim >= 0;
         prog.outs.push_back(ov);
         out_nodes.push_back(x);
         out_scatter.push_back(scatter);
@@ -670,7 +671,9 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
         if (tg != c.out_targets.end()) {
             // caller-provided destination (multi-GPU exchange buffer): out[map[i]], map < 0 skips
             b = tg->second.buf;
-            args.oscat[k] = tg->second.map;
+            args.oscat[k] = tg->second.alim >= 0 ? nullptr : tg->second.map;
+            args.ooff[k] = tg->second.aoff;
+            args.olim[k] = tg->second.alim;
             if (!tg->second.peers.empty()) {
                 if (args.npeer || tg->second.peers.size() > (size_t)MAX_PEER) fail(NBG_NOT_IMPLEMENTED, "planner: peer outputs");
                 args.npeer = (int)tg->second.peers.size();

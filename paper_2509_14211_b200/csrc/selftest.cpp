@@ -105,6 +105,13 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
             if (!compile_only(codegen(p, nm + "_rb"), nm + "_rb", log)) fails++;
             p.rb_inline = true;
             if (!compile_only(codegen(p, nm + "_rbi"), nm + "_rbi", log)) fails++;
+            p.rb_inline = false;
+            p.outs[1].affine = true;         // y_next into this rank's slice of the exchange buffer
+            if (!compile_only(codegen(p, nm + "_rba"), nm + "_rba", log)) fails++;
+            p.outs[1].multi = true;          // ... and into every peer's (NVLink peer stores)
+            if (!compile_only(codegen(p, nm + "_rbam"), nm + "_rbam", log)) fails++;
+            p.rb = false;                    // the task skeleton with the same outputs
+            if (!compile_only(codegen(p, nm + "_am"), nm + "_am", log)) fails++;
         }
         // (3) plain mxv for every monoid x type x mul, iso and valued matrices
         int k = 0;
