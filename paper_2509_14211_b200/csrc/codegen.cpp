@@ -73,7 +73,7 @@ struct SigHash {
 };
 template <class S>
 static void sig_emit(const Prog &p, S &s) {
-    s.ch(p.spmv ? (p.tp ? 'T' : (p.lpr ? 'L' : (p.rb ? (p.rb_inline ? 'I' : 'R') : 'S'))) : 'E');
+    s.ch(p.spmv ? (p.tp ? 'T' : (p.lpr ? 'L' : (p.rb ? (p.rb_inline ? 'I' : (p.rb_pipe ? 'P' : 'R')) : 'S'))) : 'E');
     s.ch(p.vec ? 'v' : 's');
     s.ch(p.tma ? 'T' : 'n');
     s.put(p.nt, ',');
@@ -1176,7 +1176,8 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     const Prog &p = g.p;
     auto &o = g.o;
     const SpmvSig &sp = p.sp;
-    const bool IE = p.rb_inline;
+    const bool IE = p.rb_inline, PIPE = p.rb_pipe && !IE;
+    const bool PT = IE || PIPE;   // reductions summed per task (dynamic task order) rather than per thread
     SemiringCode k = semiring_code(sp);
     const std::string &ACC = k.ACC, &IDENT = k.IDENT;
     const char *XT = ctype(sp.xt);
@@ -1188,7 +1189,7 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     const int NT = nt_, NW = NT / 32;
     // inline mode: floating PLUS reductions flushed per task into per-warp exact limbs
     std::vector<int> fplus;
-    if (IE)
+    if (PT)
         for (size_t j = 0; j < p.reds.size(); j++)
             if (redkind(g, p.reds[j]) == 0) fplus.push_back((int)j);
     const int NF = (int)fplus.size();
@@ -1251,7 +1252,8 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     // L2 next to the index stream), else to the plan's tot buffer
     std::string totbuf = "a.rb_tot";
     if (!IE) {
-        const char *e = getenv("NBG_RB_TOTOUT");
+        const char *e = PIPE ? "0" : getenv("NBG_RB_TOTOUT");   // pipelined: epilogue chunks of a group run while other
+                                                                  // groups still write totals -- keep them apart from the outputs
         if (!(e && e[0] == '0'))
             for (const OutV &ov : p.outs)
                 if (!ov.scatter && !ov.multi && type_size(p.ins[ov.ins].t) == (RT == "float" || RT == "int" ? 4u : 8u)) {
@@ -1296,27 +1298,139 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
         if (IE) epi(ind, idx, accx);
         else o << ind << "TOT[" << idx << "] = (" << RT << ")(" << accx << ");\n";
     };
+    // one trip of the vector epilogue: rows 4 vi .. 4 vi + 3, every load of the trip (inputs, totals,
+    // non-empty mask word, scatter map) before any store
+    std::vector<int> slot_type(p.n_in, -1);
+    for (const Ins &in : p.ins)
+        if (in.k == Ins::LD_VEC) slot_type[in.slot] = in.t;
+    std::vector<int> out_type(p.n_out, -1);
+    for (const OutV &ov : p.outs)
+        if (!ov.scatter) out_type[ov.out] = p.ins[ov.ins].t;
+    const int rtt = RT == "float" ? NBG_FP32 : (RT == "double" ? NBG_FP64 : (RT == "int" ? NBG_INT32 : NBG_INT64));
+    auto red_of = [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); };
+    auto vec_trip = [&](const std::string &ind) {
+        o << ind << "{\n";
+        for (int s2 = 0; s2 < p.n_in; s2++)
+            if (slot_type[s2] >= 0) {
+                o << ind << "  " << ctype(slot_type[s2]) << " L" << s2 << "[4];\n";
+                o << ind << "  " << vload(slot_type[s2], "a.in[" + std::to_string(s2) + "]", "vi", "L" + std::to_string(s2)) << "\n";
+            }
+        std::string tl = vload(rtt, totbuf, "vi", "T_");
+        for (size_t q = tl.find("__ldg("); q != std::string::npos; q = tl.find("__ldg(", q)) tl.replace(q, 6, "__ldcg(");
+        o << ind << "  " << RT << " T_[4];\n" << ind << "  " << tl << "\n";
+        o << ind << "  const unsigned mb_ = (__ldcg(a.rb_mask + ((vi << 2) >> 5)) >> ((vi << 2) & 31)) & 15u;\n";
+        for (const OutV &ov : p.outs)
+            if (ov.scatter && !ov.affine) o << ind << "  " << g.scat_preload(ov, "vi") << "\n";
+        for (int k2 = 0; k2 < p.n_out; k2++)
+            if (out_type[k2] >= 0) o << ind << "  " << ctype(out_type[k2]) << " O" << k2 << "[4];\n";
+        g.emit_uniform_reload(ind + "  ", "s_uni");
+        o << ind << "  #pragma unroll\n" << ind << "  for (int e = 0; e < 4; e++) {\n";
+        o << ind << "    const " << ACC << " acc = ((mb_ >> e) & 1u) ? (" << ACC << ")T_[e] : (" << ACC << ")(" << IDENT << ");\n";
+        g.emit_body(
+            ind + "    ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[e]"; },
+            [&](const OutV &ov) {
+                if (ov.scatter) return g.scat_pre(ov, "e", "(vi * 4 + e)");
+                return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
+            },
+            red_of, "acc");
+        o << ind << "  }\n";
+        for (int k2 = 0; k2 < p.n_out; k2++)
+            if (out_type[k2] >= 0) o << ind << "  " << vstore(out_type[k2], "a.out[" + std::to_string(k2) + "]", "vi", "O" + std::to_string(k2)) << "\n";
+        o << ind << "}\n";
+    };
+    // the epilogue of row i from its total (tail rows and unaligned buffers)
+    auto row_epi = [&](const std::string &ind) {
+        o << ind << "const unsigned mw_ = __ldcg(a.rb_mask + (i >> 5));\n";
+        o << ind << "const " << RT << " t_ = __ldcg(((const " << RT << "*)" << totbuf << ") + i);\n";
+        o << ind << "const " << ACC << " acc = ((mw_ >> (i & 31)) & 1u) ? (" << ACC << ")t_ : (" << ACC << ")(" << IDENT << ");\n";
+        g.emit_uniform_reload(ind, "s_uni");
+        g.emit_body(
+            ind,
+            [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
+            [&](const OutV &ov) { return g.store(ov, "i"); }, red_of, "acc");
+    };
     o << "  {\n";
     o << "  const int items = (int)a.rb_ntasks;\n";
     o << "  const int4* __restrict__ TK = (const int4*)a.rb_tasks;\n";
     // tasks from one global counter (bar[2]; reset by the grid barrier's last arriver / the last CTA
     // out), claimed one ahead
+    const std::string claim = PIPE ? "(int)atomicAdd(a.rb_done + 1 + 2 * a.rb_ngrp, 1ull)" : "(int)atomicAdd(a.rb_bar + 2, 1u)";
     o << "  int itn_ = 0;\n";
-    o << "  if (lane == 0) itn_ = atomicAdd(a.rb_bar + 2, 1u);\n";
+    o << "  if (lane == 0) itn_ = " << claim << ";\n";
     o << "  itn_ = __shfl_sync(0xffffffffu, itn_, 0);\n";
     o << "  int4 tn_ = itn_ < items ? TK[itn_] : make_int4(0, 0, 0, 0);\n";
+    if (PIPE) {
+        o << "  int qlo_ = 0;          // lane 0: first row group whose epilogue chunks are not all taken\n";
+        o << "  bool hd_ = false;      // lane 0: every hub / long task has completed\n";
+        o << "  const int ngk_ = (int)a.rb_ngrp;\n";
+    }
     o << "  for (;;) {\n";
+    if (PIPE) {
+        // an epilogue chunk (512 rows) of a row group whose totals are complete -- every hub / long task
+        // and every slice run of the group done (acquire loads of the completion counters) -- before
+        // the next row task: the DRAM-bound epilogue overlaps the gather-bound rows of later groups
+        o << "    int eq_ = -1; long long ec_ = 0;\n";
+        // polled only once every slice run of group qlo_ has been claimed (before that it cannot be complete)
+        // while row tasks remain, only every NBG_RB_EW-th warp takes epilogue chunks (the rest keep the
+        // gathers going); once the queue is empty every warp does
+        int ew = 4;
+        {
+            const char *e = getenv("NBG_RB_EW");
+            if (e && *e) ew = std::max(1, std::min(32, atoi(e)));
+        }
+        o << "    if (lane == 0 && qlo_ < ngk_ && itn_ >= a.rb_gcnt[1 + ngk_ + qlo_] && (itn_ >= items || (warp % " << ew << ") == 0)) {\n";
+        o << "      unsigned long long d_;\n";
+        // relaxed polls (an acquire load invalidates the SM's L1 each time); one acquire fence once a chunk is taken
+        o << "      if (!hd_) { asm volatile(\"ld.relaxed.gpu.global.u64 %0, [%1];\" : \"=l\"(d_) : \"l\"(a.rb_done) : \"memory\"); hd_ = d_ >= (unsigned long long)a.rb_gcnt[0]; }\n";
+        o << "      if (hd_)\n";
+        o << "        for (int q = qlo_; q < ngk_; q++) {\n";
+        o << "          asm volatile(\"ld.relaxed.gpu.global.u64 %0, [%1];\" : \"=l\"(d_) : \"l\"(a.rb_done + 1 + q) : \"memory\");\n";
+        o << "          if (d_ < (unsigned long long)a.rb_gcnt[1 + q]) break;\n";
+        o << "          const long long r0q_ = (long long)q * a.rb_gsize, r1q_ = min(a.n, r0q_ + a.rb_gsize);\n";
+        o << "          const unsigned long long c_ = atomicAdd(a.rb_done + 1 + ngk_ + q, 1ull);\n";
+        o << "          if ((long long)c_ < (r1q_ - r0q_ + 511) / 512) { eq_ = q; ec_ = (long long)c_; asm volatile(\"fence.acq_rel.gpu;\" ::: \"memory\"); break; }\n";
+        o << "          if (q == qlo_) qlo_++;\n";
+        o << "        }\n";
+        o << "    }\n";
+        o << "    eq_ = __shfl_sync(0xffffffffu, eq_, 0);\n";
+        o << "    ec_ = __shfl_sync(0xffffffffu, ec_, 0);\n";
+        o << "    if (eq_ >= 0) {\n";
+        o << "      const long long rb0_ = (long long)eq_ * a.rb_gsize + 512 * ec_;\n";
+        o << "      const long long re_ = min(min(a.n, (long long)(eq_ + 1) * a.rb_gsize), rb0_ + 512);\n";
+        if (p.vec) {
+            o << "      for (long long vi = (rb0_ >> 2) + lane; vi < (re_ >> 2); vi += 32)\n";
+            vec_trip("      ");
+            o << "      for (long long i = (re_ & ~3ll) + lane; i < re_; i += 32) {\n";
+        } else {
+            o << "      for (long long i = rb0_ + lane; i < re_; i += 32) {\n";
+        }
+        row_epi("        ");
+        o << "      }\n";
+        for (int f = 0; f < NF; f++) {
+            const int j = fplus[f];
+            o << "      { const double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f
+              << ") * 12, t_); r" << j << " = 0.0; }\n";
+        }
+        o << "      continue;\n";
+        o << "    }\n";
+    }
     o << "    const int it = itn_;\n";
-    o << "    if (it >= items) break;\n";
+    if (PIPE)
+        o << "    if (it >= items) { if (__shfl_sync(0xffffffffu, qlo_, 0) >= ngk_) break; __nanosleep(200); continue; }\n";
+    else
+        o << "    if (it >= items) break;\n";
     o << "    const int4 tk = tn_;\n";
-    o << "    if (lane == 0) itn_ = atomicAdd(a.rb_bar + 2, 1u);\n";
+    o << "    if (lane == 0) itn_ = " << claim << ";\n";
     o << "    itn_ = __shfl_sync(0xffffffffu, itn_, 0);\n";
     o << "    if (itn_ < items) tn_ = TK[itn_];\n";
     o << "    const int kind = tk.x & 3, cnt = tk.x >> 2;\n";
     // ---- short slices
     o << "    if (kind == 2) {\n";
     o << "      const int s0 = tk.y;\n";
-    o << "      const long long base = ((long long)(unsigned)tk.w << 32) | (long long)(unsigned)tk.z;\n";
+    if (PIPE)   // pipelined records: 32-bit slice offset, .w = the row group
+        o << "      const long long base = (long long)(unsigned)tk.z;\n";
+    else
+        o << "      const long long base = ((long long)(unsigned)tk.w << 32) | (long long)(unsigned)tk.z;\n";
     o << "      const int myw = lane < cnt ? a.rb_swid[s0 + lane] : 0;\n";
     o << "      const int W = __reduce_add_sync(0xffffffffu, (unsigned)myw);\n";
     o << "      const int4* __restrict__ Q = SELL + base + lane;\n";
@@ -1424,7 +1538,13 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
         epi("      ", "myrow", "mytot");
     }
     o << "    }\n";
-    if (NF) {   // the task's floating PLUS partials: fixed tree, exact add into the warp's limbs
+    if (PIPE) {   // a slice / long / hub task is complete: its totals are visible before the count
+        // release by lane 0 after the warp barrier (which orders the other lanes' total stores before it):
+        // no full fence and no L1 invalidation per task
+        o << "    __syncwarp();\n";
+        o << "    if (lane == 0) asm volatile(\"red.release.gpu.global.add.u64 [%0], 1;\" :: \"l\"(a.rb_done + (kind == 2 ? 1 + tk.w : 0)) : \"memory\");\n";
+    }
+    if (NF && IE) {   // the task's floating PLUS partials: fixed tree, exact add into the warp's limbs
         for (int f = 0; f < NF; f++) {
             const int j = fplus[f];
             o << "    { const double t_ = nbg_warp_sum(r" << j << "); if (lane == 0) nbg_xacc_add_local(s_x + (warp * NBG_NF + " << f
@@ -1433,10 +1553,14 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     }
     o << "  }\n";
     o << "  }\n";
-    if (IE) {
-        // the last CTA out resets the task counter for the next launch (every CTA is done with it)
+    if (PT) {
         o << "  __syncthreads();\n";
-        o << "  if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(a.rb_bar, 1u) == gridDim.x - 1) { atomicExch(a.rb_bar, 0u); atomicExch(a.rb_bar + 2, 0u); } }\n";
+        // inline: the last CTA out resets the task counter for the next launch (every CTA is done with it);
+        // pipelined: monotonic counters, nothing to reset
+        if (IE)
+            o << "  if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(a.rb_bar, 1u) == gridDim.x - 1) { atomicExch(a.rb_bar, 0u); atomicExch(a.rb_bar + 2, 0u); } }\n";
+        else   // pipelined: the last CTA out zeroes every counter for the next launch
+            o << "  if (threadIdx.x == 0) { __threadfence(); if (atomicAdd(a.rb_done + 2 + 2 * a.rb_ngrp, 1ull) == gridDim.x - 1) { for (long long k_ = 0; k_ < 3 + 2 * a.rb_ngrp; k_++) atomicExch(a.rb_done + k_, 0ull); } }\n";
         for (int f = 0; f < NF; f++) {
             const int j = fplus[f];
             o << "  if (threadIdx.x < 12) {\n";
@@ -1462,81 +1586,17 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     // ---------------- grid barrier (all CTAs are resident: one per SM, grid <= SMs)
     o << "  nbg_grid_sync(a.rb_bar, a.rb_bar + 2);\n";
     // ---------------- phase B: the epilogue over rows in index order.  Vector form (all buffers
-    // 16-byte aligned): 4 consecutive rows per thread and trip, every load of the trip (inputs,
-    // row totals, mask word, scatter maps) independent of the others; then the tail.
-    g.emit_uniform_reload("  ", "s_uni");
+    // 16-byte aligned): 4 consecutive rows per thread and trip (vec_trip); then the tail.  (Two or four
+    // trips per iteration measured slower: 167.0 / 178.8 vs 165.0 us at C4.)
     o << "  const long long stride_ = (long long)gridDim.x * blockDim.x;\n";
     o << "  long long tail0_ = 0;\n";
     if (p.vec) {
-        std::vector<int> slot_type(p.n_in, -1);
-        for (const Ins &in : p.ins)
-            if (in.k == Ins::LD_VEC) slot_type[in.slot] = in.t;
-        std::vector<int> out_type(p.n_out, -1);
-        for (const OutV &ov : p.outs)
-            if (!ov.scatter) out_type[ov.out] = p.ins[ov.ins].t;
-        const int rtt = RT == "float" ? NBG_FP32 : (RT == "double" ? NBG_FP64 : (RT == "int" ? NBG_INT32 : NBG_INT64));
-        // U trips per iteration: every load of the U trips is issued before the first store (the
-        // compiler cannot move loads above stores that may alias them)
-        int U = 1;
-        {
-            const char *e = getenv("NBG_RB_BU");
-            if (e && (e[0] == '1' || e[0] == '2' || e[0] == '4')) U = e[0] - '0';
-        }
         o << "  const long long nv_ = a.n >> 2;\n  tail0_ = nv_ << 2;\n";
-        o << "  for (long long vb_ = (long long)blockIdx.x * blockDim.x + threadIdx.x; vb_ < nv_; vb_ += " << U << " * stride_) {\n";
-        for (int s2 = 0; s2 < p.n_in; s2++)
-            if (slot_type[s2] >= 0) o << "    " << ctype(slot_type[s2]) << " L" << s2 << "[" << U << "][4];\n";
-        o << "    " << RT << " T_[" << U << "][4];\n";
-        o << "    unsigned mb_[" << U << "];\n";
-        for (const OutV &ov : p.outs)
-            if (ov.scatter && !ov.affine) o << "    int4 MM" << ov.out << "_[" << U << "];\n";
-        o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
-        o << "      const long long vi = vb_ + u * stride_;\n";
-        o << "      if (vi < nv_) {\n";
-        for (int s2 = 0; s2 < p.n_in; s2++)
-            if (slot_type[s2] >= 0)
-                o << "        " << vload(slot_type[s2], "a.in[" + std::to_string(s2) + "]", "vi", "L" + std::to_string(s2) + "[u]") << "\n";
-        {
-            std::string tl2 = vload(rtt, totbuf, "vi", "T_[u]");
-            for (size_t q = tl2.find("__ldg("); q != std::string::npos; q = tl2.find("__ldg(", q)) tl2.replace(q, 6, "__ldcg(");
-            o << "        " << tl2 << "\n";
-        }
-        o << "        mb_[u] = (__ldcg(a.rb_mask + ((vi << 2) >> 5)) >> ((vi << 2) & 31)) & 15u;\n";
-        for (const OutV &ov : p.outs)
-            if (ov.scatter && !ov.affine) o << "        MM" << ov.out << "_[u] = __ldg(((const int4*)a.oscat[" << ov.out << "]) + vi);\n";
-        o << "      }\n";
-        o << "    }\n";
-        o << "    #pragma unroll\n    for (int u = 0; u < " << U << "; u++) {\n";
-        o << "      const long long vi = vb_ + u * stride_;\n";
-        o << "      if (vi >= nv_) break;\n";
-        for (const OutV &ov : p.outs)
-            if (ov.scatter && !ov.affine) o << "      const int4 M" << ov.out << "_ = MM" << ov.out << "_[u];\n";
-        for (int k2 = 0; k2 < p.n_out; k2++)
-            if (out_type[k2] >= 0) o << "      " << ctype(out_type[k2]) << " O" << k2 << "[4];\n";
-        o << "      #pragma unroll\n      for (int e = 0; e < 4; e++) {\n";
-        o << "        const " << ACC << " acc = ((mb_[u] >> e) & 1u) ? (" << ACC << ")T_[u][e] : (" << ACC << ")(" << IDENT << ");\n";
-        g.emit_body(
-            "        ", [&](const Ins &in) { return "L" + std::to_string(in.slot) + "[u][e]"; },
-            [&](const OutV &ov) {
-                if (ov.scatter) return g.scat_pre(ov, "e", "(vi * 4 + e)");
-                return "O" + std::to_string(ov.out) + "[e] = " + g.v(ov.ins) + ";";
-            },
-            [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
-        o << "      }\n";
-        for (int k2 = 0; k2 < p.n_out; k2++)
-            if (out_type[k2] >= 0) o << "      " << vstore(out_type[k2], "a.out[" + std::to_string(k2) + "]", "vi", "O" + std::to_string(k2)) << "\n";
-        o << "    }\n";
-        o << "  }\n";
+        o << "  for (long long vi = (long long)blockIdx.x * blockDim.x + threadIdx.x; vi < nv_; vi += stride_)\n";
+        vec_trip("  ");
     }
     o << "  for (long long i = tail0_ + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride_) {\n";
-    o << "    const unsigned mw_ = __ldcg(a.rb_mask + (i >> 5));\n";
-    o << "    const " << RT << " t_ = __ldcg(TOT + i);\n";
-    o << "    const " << ACC << " acc = ((mw_ >> (i & 31)) & 1u) ? (" << ACC << ")t_ : (" << ACC << ")(" << IDENT << ");\n";
-    g.emit_body(
-        "    ",
-        [&](const Ins &in) { return std::string("((const ") + ctype(in.t) + "*)a.in[" + std::to_string(in.slot) + "])[i]"; },
-        [&](const OutV &ov) { return g.store(ov, "i"); },
-        [&](size_t j) { return g.red_update(p.reds[j], "r" + std::to_string(j), g.v(p.reds[j].ins)); }, "acc");
+    row_epi("    ");
     o << "  }\n";
     g.emit_red_finish();
     o << "}\n";

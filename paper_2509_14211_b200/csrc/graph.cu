@@ -324,35 +324,33 @@ __global__ void k_slot_of(long long np, const int *order, int *slot) {
 
 
 // ---- row-binned plan kernels (gpu_rb_plan)
-// per row: group count; rows with 1 <= g <= SP_LONG_G are binned (key = SP_LONG_G - g: stable radix
-// sort -> g descending, ties by row id); histogram of g; one mask word per 32 rows (non-empty)
-__global__ void k_rb_keys(long long n, const long long *grp, unsigned *key, unsigned char *flag, unsigned long long *hist,
-                          unsigned *mask) {
-    __shared__ unsigned long long h[SP_LONG_G + 1];
-    for (int j = threadIdx.x; j <= SP_LONG_G; j += blockDim.x) h[j] = 0ull;
-    __syncthreads();
+// per row: group count g; rows with 1 <= g <= SP_LONG_G are binned.  Sort key (stable radix sort):
+// long rows (g > T) first, then the short rows of row group 0, 1, ... (row group = i / gsize), each
+// class by g descending, ties by row id.  Histogram per class and g; one mask word per 32 rows.
+__global__ void k_rb_keys(long long n, const long long *grp, int T, long long gsize, int nclass, unsigned *key, unsigned char *flag,
+                          unsigned long long *hist, unsigned *mask) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < ((n + 31) & ~31ll); i += (long long)gridDim.x * blockDim.x) {
         const long long g = i < n ? grp[i + 1] - grp[i] : 0;
         const unsigned m = __ballot_sync(0xffffffffu, g > 0);
         if ((threadIdx.x & 31) == 0) mask[i >> 5] = m;
         if (i < n) {
             const bool b = g >= 1 && g <= SP_LONG_G;
+            const int cls = g > T ? 0 : 1 + (int)min((long long)(nclass - 2), i / gsize);
             flag[i] = b ? 1 : 0;
-            key[i] = b ? (unsigned)(SP_LONG_G - g) : 0u;
-            if (b) atomicAdd(&h[g], 1ull);
+            key[i] = b ? (((unsigned)cls << 10) | (unsigned)(SP_LONG_G - g)) : 0u;
+            if (b) atomicAdd(&hist[(long long)cls * (SP_LONG_G + 1) + g], 1ull);
         }
     }
-    __syncthreads();
-    for (int j = threadIdx.x; j <= SP_LONG_G; j += blockDim.x)
-        if (h[j]) atomicAdd(&hist[j], h[j]);
 }
-// slot p of the short slices: row = sorted[nlong + p] (or none), its groups copied column-major
-__global__ void k_rb_fill(long long nslots, long long nshort, const int *sorted_short, const long long *grp, const int4 *cg,
-                          const int *swid, const long long *soff, int *srow, int4 *sell) {
+// slot p of the short slices: row = sorted[sfirst[s] + l] for l < scnt[s] (or none), its groups
+// copied column-major
+__global__ void k_rb_fill(long long nslots, const int *sorted, const int2 *sfc, const long long *grp, const int4 *cg, const int *swid,
+                          const long long *soff, int *srow, int4 *sell) {
     for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nslots; p += (long long)gridDim.x * blockDim.x) {
         const long long s = p >> 5;
         const int l = (int)(p & 31);
-        const int row = p < nshort ? sorted_short[p] : -1;
+        const int2 fc = sfc[s];
+        const int row = l < fc.y ? sorted[fc.x + l] : -1;
         srow[p] = row;
         const int w = swid[s];
         const long long base = soff[s];
@@ -364,11 +362,11 @@ __global__ void k_rb_fill(long long nslots, long long nshort, const int *sorted_
 
 }  // namespace
 
-bool spmv_rb_inline() {   // read at every region launch (the signature records the mode)
-    // barrier mode by default: C4 165 us per sweep vs 190 us inline (the scattered per-row epilogue
-    // costs more L2 sectors inside the gather-bound phase than the separate pass costs)
+char spmv_rb_epi_mode() {   // read at every region launch (the signature records the mode)
+    // barrier mode by default (DESIGN.md §7 table: C4 156.9 us per sweep); the inline (189.8 us) and
+    // pipelined (239 - 336 us) modes measured slower and stay opt-in
     const char *e = getenv("NBG_RB_MODE");
-    return e && e[0] == 'i';
+    return (e && (e[0] == 'i' || e[0] == 'p')) ? e[0] : 'b';
 }
 
 int spmv_rb_mode() {   // read at every region launch (the signature records the skeleton)
@@ -376,11 +374,16 @@ int spmv_rb_mode() {   // read at every region launch (the signature records the
     return (e && *e) ? (e[0] == '1' ? 1 : 0) : -1;
 }
 
-// Row-binned plan (RbPlan, DESIGN.md §7 "row-binned SpMV").  Device: group counts, mask, histogram,
-// stable radix sort of the binned rows by descending g, the column-major slice fill.  Host: from
-// the histogram alone (the sorted g sequence is determined by it) the slice widths and offsets and
-// the task list -- hub chunks first, then long-row runs, then slice runs, each run holding <= 32
-// items and about SP_TASK_G groups.
+// Row-binned plan (RbPlan, DESIGN.md §7 "row-binned SpMV").  Device: group counts, mask, histogram
+// per class, stable radix sort of the binned rows, the column-major slice fill.  Host: from the
+// histograms alone (the sorted g sequence of each class is determined by them) the slices (per row
+// group, never across one), their widths and offsets, and three task lists -- every list: hub chunks,
+// long-row runs, slice runs (largest first), each run <= 32 items and about SP_TASK_G groups:
+//   main      (barrier mode) exactly that;
+//   inline    + 512-row empty-row tasks interleaved evenly;
+//   pipelined slice runs grouped by row group, and after the slices of group q + 1 the epilogue
+//             tasks of group q (512-row chunks), which wait until every long / hub task and every
+//             slice task of group q has completed.
 RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
     if (!A.plan) gpu_build_spmv_plan(c, A);
     SpmvPlan &P = *A.plan;
@@ -398,14 +401,24 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
         const char *e = getenv("NBG_RB_TG");
         if (e && *e) tg = std::max(32, std::min(1 << 16, atoi(e)));
     }
+    int NG = 8;
+    {
+        const char *e = getenv("NBG_RB_NG");
+        if (e && *e) NG = std::max(1, std::min(64, atoi(e)));
+    }
+    const long long RE = 512;                                          // rows per epilogue / empty-row task
+    const long long gsize = std::max(RE, (((n + NG - 1) / NG) + RE - 1) / RE * RE);   // rows per row group (multiple of RE)
+    NG = (int)std::max(1ll, (n + gsize - 1) / gsize);
+    R->ngrp = NG;
+    const int NC = NG + 1;                                             // classes: long, then short per row group
     const int gr = grid_for(n, c.num_sms);
-    BufP key = alloc_buf(c, (size_t)n * 4), flag = alloc_buf(c, (size_t)n), hist = alloc_buf(c, (SP_LONG_G + 1) * 8);
+    BufP key = alloc_buf(c, (size_t)n * 4), flag = alloc_buf(c, (size_t)n), hist = alloc_buf(c, (size_t)NC * (SP_LONG_G + 1) * 8);
     R->mask = alloc_buf(c, (size_t)((n + 31) / 32) * 4);
-    NBG_CUDA(cudaMemsetAsync(hist->d, 0, (SP_LONG_G + 1) * 8, c.stream));
-    k_rb_keys<<<gr, 256, 0, c.stream>>>(n, (const long long *)P.grp->d, (unsigned *)key->d, (unsigned char *)flag->d,
+    NBG_CUDA(cudaMemsetAsync(hist->d, 0, (size_t)NC * (SP_LONG_G + 1) * 8, c.stream));
+    k_rb_keys<<<gr, 256, 0, c.stream>>>(n, (const long long *)P.grp->d, T, gsize, NC, (unsigned *)key->d, (unsigned char *)flag->d,
                                         (unsigned long long *)hist->d, (unsigned *)R->mask->d);
-    BufP ids = alloc_buf(c, (size_t)n * 4), keys2 = alloc_buf(c, (size_t)n * 4),
-         sorted = alloc_buf(c, (size_t)n * 4), cnt = alloc_buf(c, 8);
+    BufP ids = alloc_buf(c, (size_t)n * 4), keys2 = alloc_buf(c, (size_t)n * 4), sorted = alloc_buf(c, (size_t)n * 4),
+         cnt = alloc_buf(c, 8);
     size_t tb = 0;
     thrust::counting_iterator<int> it0(0);
     cub::DeviceSelect::Flagged(nullptr, tb, it0, (const unsigned char *)flag->d, (int *)ids->d, (long long *)cnt->d, (int64_t)n, c.stream);
@@ -417,13 +430,15 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
     if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
     NBG_CUDA(cub::DeviceSelect::Flagged(tmp->d, tb, (const unsigned *)key->d, (const unsigned char *)flag->d, (unsigned *)keys2->d,
                                         (long long *)cnt->d, (int64_t)n, c.stream));
-    std::vector<unsigned long long> H(SP_LONG_G + 1);
-    NBG_CUDA(cudaMemcpyAsync(H.data(), hist->d, (SP_LONG_G + 1) * 8, cudaMemcpyDeviceToHost, c.stream));
+    std::vector<unsigned long long> H((size_t)NC * (SP_LONG_G + 1));
+    NBG_CUDA(cudaMemcpyAsync(H.data(), hist->d, H.size() * 8, cudaMemcpyDeviceToHost, c.stream));
     NBG_CUDA(cudaStreamSynchronize(c.stream));
+    auto h = [&](int cls, int g) { return (long long)H[(size_t)cls * (SP_LONG_G + 1) + g]; };
     long long m = 0;
-    for (int g = 1; g <= SP_LONG_G; g++) m += (long long)H[g];
+    for (int cl = 0; cl < NC; cl++)
+        for (int g = 1; g <= SP_LONG_G; g++) m += h(cl, g);
     if (m > 0) {
-        const int bits = bits_for(SP_LONG_G + 1);
+        const int bits = 10 + bits_for(NC + 1);
         cub::DeviceRadixSort::SortPairs(nullptr, tb, (const unsigned *)keys2->d, (unsigned *)key->d, (const int *)ids->d, (int *)sorted->d,
                                         (int64_t)m, 0, bits, c.stream);
         if (tb > tmp->bytes) tmp = alloc_buf(c, tb);
@@ -431,41 +446,53 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
                                                  (int *)sorted->d, (int64_t)m, 0, bits, c.stream));
     }
     long long nlong = 0, nshort = 0;
-    for (int g = T + 1; g <= SP_LONG_G; g++) nlong += (long long)H[g];
-    for (int g = 1; g <= T && g <= SP_LONG_G; g++) nshort += (long long)H[g];
+    for (int g = 1; g <= SP_LONG_G; g++) nlong += h(0, g);
+    for (int cl = 1; cl < NC; cl++)
+        for (int g = 1; g <= SP_LONG_G; g++) nshort += h(cl, g);
     R->nlong = nlong;
     R->nshort = nshort;
-    R->nslices = (nshort + 31) / 32;
-    // slice widths: g of the first (longest) row of each slice, from the descending g sequence
-    std::vector<int> swid((size_t)std::max<long long>(R->nslices, 1));
-    std::vector<long long> soff((size_t)std::max<long long>(R->nslices, 1));
+    // slices, per row group: width = g of the slice's first (longest) row
+    std::vector<int> swid, sgrp, sfc;   // sfc: int2 {first sorted index, count}
+    std::vector<long long> soff;
     {
-        long long pos = 0, sl = 0, off = 0;
-        for (int g = std::min(T, SP_LONG_G); g >= 1; g--) {
-            const long long end = pos + (long long)H[g];
-            for (; sl < R->nslices && 32 * sl < end; sl++) {
-                swid[sl] = g;
-                soff[sl] = off;
+        long long pos = nlong, off = 0;
+        for (int q = 0; q < NG; q++) {
+            long long nq = 0;
+            for (int g = 1; g <= SP_LONG_G; g++) nq += h(1 + q, g);
+            const long long ns = (nq + 31) / 32;
+            long long k = 0;   // rows of the group with g larger than the current g
+            int g = SP_LONG_G;
+            long long left = h(1 + q, g);
+            for (long long sl = 0; sl < ns; sl++) {
+                const long long want = 32 * sl;   // index of the slice's first row inside the group
+                while (k + left <= want && g > 1) { k += left; left = h(1 + q, --g); }
+                swid.push_back(g);
+                soff.push_back(off);
+                sgrp.push_back(q);
+                sfc.push_back((int)(pos + 32 * sl));
+                sfc.push_back((int)std::min(32ll, nq - 32 * sl));
                 off += 32ll * g;
             }
-            pos = end;
+            pos += nq;
         }
         R->sell_groups = off;
     }
-    // tasks: {kind | count << 2, first, base_lo, base_hi}
-    std::vector<int> tasks;
-    auto push = [&](int kind, long long count, long long first, long long base) {
-        tasks.push_back((int)(kind | (count << 2)));
-        tasks.push_back((int)first);
-        tasks.push_back((int)(unsigned)(base & 0xffffffffll));
-        tasks.push_back((int)(unsigned)((unsigned long long)base >> 32));
+    R->nslices = (long long)swid.size();
+    // task records {kind | count << 2, first, z, w}: short runs z/w = slice offset lo/hi (main, inline)
+    // or lo/row group (pipelined); epilogue chunks (pipelined) {3, row0, group}; empty-row ranges (inline) {3, row0}
+    std::vector<int> head, tasks;   // head: hub + long tasks
+    auto push = [&](std::vector<int> &v, int kind, long long count, long long first, long long z, long long w) {
+        v.push_back((int)(kind | (count << 2)));
+        v.push_back((int)first);
+        v.push_back((int)(unsigned)(z & 0xffffffffll));
+        v.push_back((int)(unsigned)((unsigned long long)w & 0xffffffffull));
     };
-    for (long long q = 0; q < P.nchunks; q++) push(0, 1, q, 0);
+    for (long long q = 0; q < P.nchunks; q++) push(head, 0, 1, q, 0, 0);
     {
         std::vector<int> lg;   // the long rows' g, in plan order (descending)
         lg.reserve((size_t)nlong);
-        for (int g = SP_LONG_G; g > T; g--)
-            for (unsigned long long q = 0; q < H[g]; q++) lg.push_back(g);
+        for (int g = SP_LONG_G; g >= 1; g--)
+            for (long long q = 0; q < h(0, g); q++) lg.push_back(g);
         long long j = 0;
         while (j < nlong) {
             const long long first = j;
@@ -475,77 +502,97 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
                 cntr++;
                 j++;
             }
-            push(1, cntr, first, 0);
+            push(head, 1, cntr, first, 0, 0);
         }
     }
+    // slice runs per row group (a run never crosses a group)
+    std::vector<std::vector<int>> sruns((size_t)NG), sruns_p((size_t)NG);
     {
         const long long tl = std::max(1ll, tg / 32);   // lane-groups per slice task
         long long s = 0;
         while (s < R->nslices) {
             const long long first = s;
+            const int q = sgrp[s];
             long long cntr = 0, sum = 0;
-            while (s < R->nslices && cntr < 32 && (cntr == 0 || sum + swid[s] <= tl)) {
+            while (s < R->nslices && sgrp[s] == q && cntr < 32 && (cntr == 0 || sum + swid[s] <= tl)) {
                 sum += swid[s];
                 cntr++;
                 s++;
             }
-            push(2, cntr, first, soff[first]);
+            push(sruns[q], 2, cntr, first, soff[first], (long long)((unsigned long long)soff[first] >> 32));
+            push(sruns_p[q], 2, cntr, first, soff[first], q);
         }
     }
-    // empty-row ranges (kind 3, the inline-epilogue mode only): the epilogue of the rows without
-    // stored entries, 512 rows per task, interleaved evenly into the queue (streaming work that
-    // overlaps the gathers); the barrier mode runs only the first ntasks_main tasks
+    // main list (barrier mode)
+    tasks = head;
+    for (int q = 0; q < NG; q++) tasks.insert(tasks.end(), sruns[q].begin(), sruns[q].end());
+    R->ntasks_main = (long long)tasks.size() / 4;
+    R->tasks_main = alloc_buf(c, std::max<size_t>(tasks.size() * 4, 16));
+    if (!tasks.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks_main->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    // inline list: + empty-row ranges (kind 3) interleaved evenly
+    std::vector<int> mixed;
     {
-        const long long RE = 512;
-        std::vector<int> mixed;
         const long long nmain = (long long)tasks.size() / 4, nemp = (n + RE - 1) / RE;
         mixed.reserve((size_t)(nmain + nemp) * 4);
         long long e = 0;
-        for (long long t = 0; t <= nmain; t++) {
-            const long long want = nmain ? (t * nemp) / std::max(1ll, nmain) : nemp;   // empties placed before task t
-            for (; e < want && e < nemp; e++) {
-                const long long r0 = e * RE, cntr = std::min(RE, n - r0);
-                mixed.push_back((int)(3 | (cntr << 2)));
-                mixed.push_back((int)r0);
-                mixed.push_back(0);
-                mixed.push_back(0);
-            }
-            if (t < nmain) mixed.insert(mixed.end(), tasks.begin() + 4 * t, tasks.begin() + 4 * t + 4);
+        auto emp = [&](long long e2) { const long long r0 = e2 * RE; push(mixed, 3, std::min(RE, n - r0), r0, 0, 0); };
+        for (long long t = 0; t < nmain; t++) {
+            const long long want = (t * nemp) / std::max(1ll, nmain);   // empties placed before task t
+            for (; e < want; e++) emp(e);
+            mixed.insert(mixed.end(), tasks.begin() + 4 * t, tasks.begin() + 4 * t + 4);
         }
-        for (; e < nemp; e++) {
-            const long long r0 = e * RE, cntr = std::min(RE, n - r0);
-            mixed.push_back((int)(3 | (cntr << 2)));
-            mixed.push_back((int)r0);
-            mixed.push_back(0);
-            mixed.push_back(0);
-        }
-        R->ntasks_main = nmain;
-        R->tasks_main = alloc_buf(c, std::max<size_t>(tasks.size() * 4, 16));
-        if (!tasks.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks_main->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        tasks.swap(mixed);
+        for (; e < nemp; e++) emp(e);
+        R->ntasks = (long long)mixed.size() / 4;
+        R->tasks = alloc_buf(c, std::max<size_t>(mixed.size() * 4, 16));
+        if (!mixed.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks->d, mixed.data(), mixed.size() * 4, cudaMemcpyHostToDevice, c.stream));
     }
-    R->ntasks = (long long)tasks.size() / 4;
-    R->tasks = alloc_buf(c, std::max<size_t>(tasks.size() * 4, 16));
-    if (!tasks.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
+    // pipelined list: head, then the slice runs of row group 0, 1, ...; the epilogue chunks of a row
+    // group are not queued: warps take them (gsize / RE per group) once the group's totals are complete
+    std::vector<int> pl = head, gcnt((size_t)NG + 1, 0);
+    {
+        gcnt[0] = (int)(head.size() / 4);
+        for (int q = 0; q < NG; q++) {
+            pl.insert(pl.end(), sruns_p[q].begin(), sruns_p[q].end());
+            gcnt[1 + q] = (int)(sruns_p[q].size() / 4);
+        }
+        R->gsize = gsize;
+        R->ntasks_pipe = (long long)pl.size() / 4;
+        R->tasks_pipe = alloc_buf(c, std::max<size_t>(pl.size() * 4, 16));
+        if (!pl.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks_pipe->d, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        // + [NG + 1 + q]: end (exclusive) of group q's slice runs in the list -- once the claims pass it,
+        // the group can complete and the kernel starts polling its counter
+        {
+            int end = gcnt[0];
+            for (int q = 0; q < NG; q++) { end += gcnt[1 + q]; gcnt.push_back(end); }
+        }
+        R->gcnt = alloc_buf(c, gcnt.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(R->gcnt->d, gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        R->pipe_ok = R->sell_groups < (1ll << 31);   // pipelined short records keep 32 bits of the slice offset
+        // counters, zero between launches (the last CTA out resets them): [0] hub + long tasks done,
+        // [1 + q] slice runs of group q done, [1 + NG + q] epilogue chunks of group q taken, [1 + 2 NG]
+        // task claims, [2 + 2 NG] CTAs out
+        R->done = alloc_buf(c, (2 * (size_t)NG + 3) * 8);
+        NBG_CUDA(cudaMemsetAsync(R->done->d, 0, (2 * (size_t)NG + 3) * 8, c.stream));
+    }
     R->lrows = alloc_buf(c, (size_t)std::max<long long>(nlong, 1) * 4);
     if (nlong > 0) NBG_CUDA(cudaMemcpyAsync(R->lrows->d, sorted->d, (size_t)nlong * 4, cudaMemcpyDeviceToDevice, c.stream));
     R->srow = alloc_buf(c, (size_t)std::max<long long>(32 * R->nslices, 1) * 4);
     R->swid = alloc_buf(c, (size_t)std::max<long long>(R->nslices, 1) * 4);
     R->sell = alloc_buf(c, (size_t)std::max<long long>(R->sell_groups, 1) * 16);
     if (R->nslices > 0) {
-        BufP so = alloc_buf(c, (size_t)R->nslices * 8);
+        BufP so = alloc_buf(c, (size_t)R->nslices * 8), fc = alloc_buf(c, (size_t)R->nslices * 8);
         NBG_CUDA(cudaMemcpyAsync(R->swid->d, swid.data(), (size_t)R->nslices * 4, cudaMemcpyHostToDevice, c.stream));
         NBG_CUDA(cudaMemcpyAsync(so->d, soff.data(), (size_t)R->nslices * 8, cudaMemcpyHostToDevice, c.stream));
+        NBG_CUDA(cudaMemcpyAsync(fc->d, sfc.data(), (size_t)R->nslices * 8, cudaMemcpyHostToDevice, c.stream));
         k_rb_fill<<<grid_for(32 * R->nslices, c.num_sms), 256, 0, c.stream>>>(
-            32 * R->nslices, nshort, (const int *)sorted->d + nlong, (const long long *)P.grp->d, (const int4 *)P.cg->d,
+            32 * R->nslices, (const int *)sorted->d, (const int2 *)fc->d, (const long long *)P.grp->d, (const int4 *)P.cg->d,
             (const int *)R->swid->d, (const long long *)so->d, (int *)R->srow->d, (int4 *)R->sell->d);
-        NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     }
     R->tot = alloc_buf(c, (size_t)n * 8);
     R->bar = alloc_buf(c, 16);
     NBG_CUDA(cudaMemsetAsync(R->bar->d, 0, 16, c.stream));
     NBG_CUDA(cudaGetLastError());
-    NBG_CUDA(cudaStreamSynchronize(c.stream));
+    NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     c.stats.kernels_launched += 5;
     P.rb = std::move(R);
     return P.rb.get();

@@ -52,6 +52,9 @@ struct KArgs {
     unsigned *rb_bar;
     long long rb_ntasks;
     long long ooff[NBG_MAX_OUT], olim[NBG_MAX_OUT];
+    unsigned long long *rb_done;
+    const int *rb_gcnt;
+    long long rb_ngrp, rb_gsize;
 };
 
 // ------------------------------------------------------------------ operators in type T

@@ -176,6 +176,13 @@ struct RbPlan {
     BufP tasks;     // int4[ntasks]  {kind | count << 2, first, base_lo, base_hi}: 0 hub chunk, 1 long rows, 2 short slices,
                     //   3 empty-row range (inline-epilogue mode), interleaved
     BufP tasks_main;   // int4[ntasks_main]  the same without kind 3 (barrier mode)
+    BufP tasks_pipe;   // int4[ntasks_pipe]  pipelined mode: hub + long tasks, then slice runs by row group (.w = group)
+    int64_t ntasks_pipe = 0;
+    int ngrp = 1;      // row groups: rows [q gsize, (q + 1) gsize)
+    int64_t gsize = 0;
+    bool pipe_ok = false;
+    BufP gcnt;      // int[2 ngrp + 1]  tasks per counter: [0] hub + long, [1 + q] slice runs of group q; [1 + ngrp + q] end of group q's runs
+    BufP done;      // u64[2 ngrp + 3]  pipelined counters (zero between launches; see gpu_rb_plan)
     BufP mask;      // u32[(n + 31) / 32]  bit i: row i is non-empty
     BufP tot;       // 8 bytes per row: row totals (the kernel's row-total type)
     BufP bar;       // u32[2]  grid barrier {arrivals, generation}
@@ -292,7 +299,9 @@ struct Prog {
     bool tp = false;        // spmv through the two-phase plan: this program is phase 2 (combine + epilogue)
     bool lpr = false;       // spmv, lane-per-row skeleton (low-skew matrices)
     bool rb = false;        // spmv, row-binned skeleton (RbPlan)
-    bool rb_inline = false; // row-binned: epilogue at each row's completion (no barrier); else totals + grid barrier + epilogue pass
+    bool rb_inline = false; // row-binned: epilogue at each row's completion (no barrier)
+    bool rb_pipe = false;   // row-binned: epilogue chunks of a row group once its totals are complete (no barrier)
+                            // neither: totals + grid barrier + epilogue pass
     int nt = 0, hot_kb = 0; // spmv (task skeleton): threads per CTA and hot-cache KB, chosen per matrix
     bool vec = true;        // 16-byte vector loads/stores (all buffers aligned)
     bool tma = false;       // ewise: inputs staged through shared memory by TMA bulk copies (large n)
@@ -348,6 +357,10 @@ struct KArgs {
     unsigned *rb_bar;
     long long rb_ntasks;
     long long ooff[MAX_OUT], olim[MAX_OUT];   // affine outputs: out[ooff + i] for i < olim
+    // row-binned, pipelined mode: counters (gpu_rb_plan), tasks per completion counter, row groups
+    unsigned long long *rb_done;
+    const int *rb_gcnt;
+    long long rb_ngrp, rb_gsize;
 };
 
 struct Kernel {
@@ -540,7 +553,7 @@ int spmv_threads(int xsize);
 int spmv_groups_per_lane();   // SpMV task skeleton: groups per lane per step (NBG_SPMV_GPL, default 2)
 void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb);   // per-matrix SpMV launch shape   // threads per SpMV CTA for a gathered element size (NBG_SPMV_THREADS overrides)
 int spmv_rb_mode();    // NBG_SPMV_RB: -1 auto (skewed matrices), 0 never, 1 always
-bool spmv_rb_inline(); // NBG_RB_MODE: b (default) totals + grid barrier + epilogue pass, i epilogue at each row's completion
+char spmv_rb_epi_mode(); // NBG_RB_MODE: b (default) totals + grid barrier + epilogue pass, p pipelined epilogue chunks, i epilogue at each row's completion
 int spmv_lpr_mode();   // NBG_SPMV_LPR: -1 auto (by skew), 0 never, 1 always   // threads per SpMV CTA (NBG_SPMV_THREADS, default 1024)
 std::string codegen_tp1(const SpmvSig &sp, const std::string &kname, int xsize, long long S, int *dyn_smem);
 std::string codegen(const Prog &p, const std::string &kname, int *dyn_smem = nullptr, int *hot_entries = nullptr);

@@ -775,8 +775,14 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             if (R) {
                 p.rb = true;
                 p.vec = vec;   // the epilogue uses 16-byte vector loads when every buffer allows them
-                p.rb_inline = spmv_rb_inline();
-                args.rb_tasks = (const int *)(p.rb_inline ? R->tasks->d : R->tasks_main->d);
+                const char md = spmv_rb_epi_mode();
+                p.rb_inline = md == 'i';
+                p.rb_pipe = md == 'p' && R->pipe_ok;
+                args.rb_tasks = (const int *)(p.rb_inline ? R->tasks->d : (p.rb_pipe ? R->tasks_pipe->d : R->tasks_main->d));
+                args.rb_done = (unsigned long long *)R->done->d;
+                args.rb_gcnt = (const int *)R->gcnt->d;
+                args.rb_ngrp = R->ngrp;
+                args.rb_gsize = R->gsize;
                 args.rb_sell = (const int *)R->sell->d;
                 args.rb_srow = (const int *)R->srow->d;
                 args.rb_swid = (const int *)R->swid->d;
@@ -784,7 +790,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
                 args.rb_mask = (const unsigned *)R->mask->d;
                 args.rb_tot = R->tot->d;
                 args.rb_bar = (unsigned *)R->bar->d;
-                args.rb_ntasks = p.rb_inline ? R->ntasks : R->ntasks_main;
+                args.rb_ntasks = p.rb_inline ? R->ntasks : (p.rb_pipe ? R->ntasks_pipe : R->ntasks_main);
                 items = 1ll << 40;   // persistent: one CTA per SM (clamped to the kernel's grid_cap)
             }
         }
@@ -860,6 +866,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
     if (p.spmv && !p.tp) {
         if (args.hc > kern->hot) args.hc = kern->hot;
     }
+
     {
         PTimer pt(5);
         if (dbg()) {

@@ -106,6 +106,8 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
             p.rb_inline = true;
             if (!compile_only(codegen(p, nm + "_rbi"), nm + "_rbi", log)) fails++;
             p.rb_inline = false;
+            p.rb_pipe = true;                // pipelined epilogue chunks
+            if (!compile_only(codegen(p, nm + "_rbp"), nm + "_rbp", log)) fails++;
             p.outs[1].affine = true;         // y_next into this rank's slice of the exchange buffer
             if (!compile_only(codegen(p, nm + "_rba"), nm + "_rba", log)) fails++;
             p.outs[1].multi = true;          // ... and into every peer's (NVLink peer stores)
@@ -149,7 +151,8 @@ extern "C" int nbg_debug_jit_selftest(char *out, size_t len) {
                     Prog p;
                     p.spmv = true;
                     p.rb = true;
-                    p.rb_inline = (k & 1) != 0;
+                    p.rb_inline = (k % 3) == 1;
+                    p.rb_pipe = (k % 3) == 2;
                     p.sp.add = add; p.sp.mul = mul; p.sp.T = T; p.sp.xt = T == NBG_BOOL ? NBG_FP32 : T; p.sp.at = NBG_INT32;
                     p.ins.push_back(I(Ins::MXV_ACC, T));
                     p.outs.push_back(OutV{0, 0});

@@ -21,10 +21,11 @@ from oracle import ops
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["b", "i"])
+@pytest.fixture(autouse=True, params=["b", "p", "i"])
 def rb_mode(request, monkeypatch):
-    """Both epilogue modes: b = row totals + grid barrier + epilogue pass (default), i = the
-    epilogue where each row's total completes."""
+    """Every epilogue mode: b = row totals + grid barrier + epilogue pass (default), p = epilogue
+    chunks of a row group taken once its totals are complete, i = the epilogue where each row's
+    total completes."""
     monkeypatch.setenv("NBG_RB_MODE", request.param)
     return request.param
 
@@ -236,5 +237,29 @@ def test_rb_degenerate(nbg, monkeypatch, n, src, dst):
         r, sw, _ = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=5, type=nbg.FP64)
         ro, so, _, _ = oracle.pagerank(orp, oci, odeg, dtype=np.float64, itermax=5)
         assert sw == so and rel(nbg.nbg_vector_export_dense(c, r), ro) <= 1e-10
+    finally:
+        nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("ng", [1, 3, 64])
+def test_rb_row_groups(nbg, monkeypatch, ng):
+    """Row groups of the pipelined mode (NBG_RB_NG): one group, an uneven count, more groups than
+    rows per group allows (clamped) -- PageRank against the oracle and repeated solves bit-identical
+    (the monotonic completion counters carry over between launches)."""
+    monkeypatch.setenv("NBG_SPMV_RB", "1")
+    monkeypatch.setenv("NBG_RB_NG", str(ng))
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 13, 16, 7)
+        rp, ci = nbg.nbg_matrix_export_csr(c, A)
+        d = nbg.nbg_vector_export_dense(c, deg)
+        runs = []
+        for _ in range(3):
+            r, s, h = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=9, type=nbg.FP32)
+            runs.append((nbg.nbg_vector_export_dense(c, r), h))
+        ro, so, dho, _ = oracle.pagerank(rp, ci, d, dtype=np.float32, itermax=9)
+        assert rel(runs[0][0], ro) <= 1e-5
+        for v, h in runs[1:]:
+            assert np.array_equal(v, runs[0][0]) and np.array_equal(h, runs[0][1])
     finally:
         nbg.nbg_finalize(c)
