@@ -176,6 +176,10 @@ __global__ void k_col_keys(long long nc, const int *cnt, unsigned *key, int *ids
         if (c > 0) atomicAdd(nonempty, 1);
     }
 }
+__global__ void k_not_identity(long long n, const int *order, int *bad) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        if (order[k] != (int)k) *bad = 1;
+}
 __global__ void k_perm_from_order(long long ng, const int *order, int *perm) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < ng; k += (long long)gridDim.x * blockDim.x)
         perm[order[k]] = (int)k;
@@ -1116,6 +1120,9 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     const char *rl = getenv("NBG_RELABEL");
     const bool want = !A.prelabeled && (rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15)));
     BufP colsrc = A.colidx;
+    bool want_id = false;   // the column order is already the gather layout
+    BufP sorted_ids;
+    int sorted_ng = 0;
     if (want && A.nnz > 0 && !A.vals) {
         const long long nc = A.ncols;
         BufP cnt = alloc_buf(c, (size_t)nc * 4);
@@ -1135,7 +1142,23 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
                                                  (const int *)ids->d, (int *)ids2->d, (int64_t)nc, 0, 32, c.stream));
         int ng = 0;
         NBG_CUDA(cudaMemcpyAsync(&ng, ne->d, 4, cudaMemcpyDeviceToHost, c.stream));
+        // already in the gather layout (a symmetrically relabelled matrix: columns by descending count,
+        // ties by id, empty columns last)?  Then no relabel: the gathered vector is the plain vector and
+        // side outputs in its layout are plain row-order stores (no scatter map)
+        BufP notid = alloc_buf(c, 4);
+        NBG_CUDA(cudaMemsetAsync(notid->d, 0, 4, c.stream));
+        k_not_identity<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)ids2->d, (int *)notid->d);
+        int nid = 1;
+        NBG_CUDA(cudaMemcpyAsync(&nid, notid->d, 4, cudaMemcpyDeviceToHost, c.stream));
         NBG_CUDA(cudaStreamSynchronize(c.stream));
+        if (!nid) want_id = true;
+        sorted_ids = ids2;
+        sorted_ng = ng;
+    }
+    if (want && A.nnz > 0 && !A.vals && !want_id) {
+        const long long nc = A.ncols;
+        BufP ids2 = sorted_ids;
+        const int ng = sorted_ng;
         P->perm = alloc_buf(c, (size_t)nc * 4);
         NBG_CUDA(cudaMemsetAsync(P->perm->d, 0xff, (size_t)nc * 4, c.stream));
         P->iperm = alloc_buf(c, (size_t)std::max(ng, 1) * 4);

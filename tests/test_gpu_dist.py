@@ -241,3 +241,32 @@ def test_two_slot_exact_combine_on_device(nbg):
         assert math.isnan(nbg.nbg_xacc_decode(combine(slot(a_ninf), slot(b_inf))))
     finally:
         nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+def test_csr_already_in_gather_layout(nbg, T):
+    """A CSR whose columns are already in the gather layout (the one-rank symmetric relabel,
+    exported and loaded back through nbg_matrix_from_csr): the plan keeps the column order (no
+    relabel, y_next stored in row order) and nbg_pagerank matches the distributed solve of the same
+    matrix and the oracle."""
+    t = nbg.TYPE_OF[T]
+    npT = nbg.NP_OF[t]
+    c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        A, d, cuts, ncg = nbg.nbg_dist_graph_from_generator(c, nbg.GRAPH_RMAT, 14, 16, 3, nranks=1)
+        rp, ci = nbg.nbg_matrix_export_csr(c, A)
+        deg = nbg.nbg_vector_export_dense(c, d)
+        n = rp.shape[0] - 1
+        B = nbg.nbg_matrix_from_csr(c, n, n, rp, ci, type=nbg.FP32)
+        bdeg = nbg.nbg_vector_from_dense(c, nbg.INT32, deg.astype(np.int32))
+        for _ in range(2):      # the second solve runs the hinted (side-output) kernels
+            r1, s1, h1 = nbg.nbg_pagerank(c, B, bdeg, tol=-1.0, itermax=10, type=t)
+        r2, s2, h2 = nbg.nbg_pagerank_dist(c, A, d, cuts, ncg, tol=-1.0, itermax=10, type=t)
+        v1 = nbg.nbg_vector_export_dense(c, r1)
+        v2 = nbg.nbg_vector_export_dense(c, r2)
+        assert s1 == s2 == 10
+        assert rel(v1, v2) <= (1e-6 if T == "fp32" else 1e-13)
+        ro, so, dho, _ = oracle.pagerank(rp, ci, deg, dtype=npT, itermax=10)
+        assert rel(v1, ro) <= (1e-5 if T == "fp32" else 1e-10)
+    finally:
+        nbg.nbg_finalize(c)
