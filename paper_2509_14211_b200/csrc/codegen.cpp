@@ -1489,20 +1489,30 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     o << "    int r = 0, b = 0;\n";
     o << "    long long gb = __shfl_sync(0xffffffffu, mygb, 0);\n";
     o << "    int ng = __shfl_sync(0xffffffffu, myng, 0);\n";
-    o << "    int4 q0 = (lane < ng) ? __ldcs(CG + gb + lane) : NBG_NEG;\n";
-    o << "    int4 q1 = (32 + lane < ng) ? __ldcs(CG + gb + 32 + lane) : NBG_NEG;\n";
+    // LG groups per lane per step (steps of 32 LG groups): lane l sums groups l, l + 32, l + 64, ...
+    // whatever LG is -- the order (and every bit of the result) does not depend on it
+    int LG = 2;
+    {
+        const char *e = getenv("NBG_RB_LG");
+        if (e && (e[0] == '1' || e[0] == '2' || e[0] == '3' || e[0] == '4')) LG = e[0] - '0';
+    }
+    const char *gv[4] = {"u", "v", "w", "z"};
+    for (int k2 = 0; k2 < LG; k2++)
+        o << "    int4 q" << k2 << " = (" << 32 * k2 << " + lane < ng) ? __ldcs(CG + gb + " << 32 * k2 << " + lane) : NBG_NEG;\n";
     o << "    " << ACC << " acc = " << IDENT << ";\n";
     o << "    for (;;) {\n";
-    o << "      const int4 c0 = q0, c1 = q1;\n";
-    o << "      NBG_G4(c0, u); NBG_G4(c1, v);\n";
-    o << "      int nb = b + 64, nr = r;\n";
+    for (int k2 = 0; k2 < LG; k2++) o << "      const int4 c" << k2 << " = q" << k2 << ";\n";
+    for (int k2 = 0; k2 < LG; k2++) o << "      NBG_G4(c" << k2 << ", " << gv[k2] << ");\n";
+    o << "      int nb = b + " << 32 * LG << ", nr = r;\n";
     o << "      long long ngb = gb; int nng = ng;\n";
     o << "      if (nb >= ng) { nr = r + 1; nb = 0; if (nr < nrow) { ngb = __shfl_sync(0xffffffffu, mygb, nr); nng = __shfl_sync(0xffffffffu, myng, nr); } }\n";
     o << "      if (nr < nrow) {\n";
-    o << "        q0 = (nb + lane < nng) ? __ldcs(CG + ngb + nb + lane) : NBG_NEG;\n";
-    o << "        q1 = (nb + 32 + lane < nng) ? __ldcs(CG + ngb + nb + 32 + lane) : NBG_NEG;\n";
+    for (int k2 = 0; k2 < LG; k2++)
+        o << "        q" << k2 << " = (nb + " << 32 * k2 << " + lane < nng) ? __ldcs(CG + ngb + nb + " << 32 * k2 << " + lane) : NBG_NEG;\n";
     o << "      }\n";
-    o << "      NBG_A4(acc, u); NBG_A4(acc, v);\n";
+    o << "      ";
+    for (int k2 = 0; k2 < LG; k2++) o << "NBG_A4(acc, " << gv[k2] << "); ";
+    o << "\n";
     o << "      if (nr != r) {\n";
     o << "        const " << ACC << " t = nbg_tree(acc);\n";
     if (IE) {

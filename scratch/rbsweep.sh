@@ -3,7 +3,7 @@ set -u
 T=$1; shift; O=gpurun_out/$T; mkdir -p $O
 for e in "$@"; do
   f=$O/$(echo "$e" | tr ' =' '_-').json
-  env NBG_SPMV_RB=1 $e timeout 300 python bench.py --steps 20 --no-cpu-baseline --no-e2e > $f 2> $f.err
+  env NBG_SPMV_RB=1 $e timeout 600 python bench.py --workload ${WL:-c4} --steps ${STEPS:-20} --no-cpu-baseline --no-e2e > $f 2> $f.err
   python -c "
 import json,sys
 d=json.load(open('$f')); r=d['roofline']
