@@ -176,9 +176,9 @@ __global__ void k_col_keys(long long nc, const int *cnt, unsigned *key, int *ids
         if (c > 0) atomicAdd(nonempty, 1);
     }
 }
-__global__ void k_not_identity(long long n, const int *order, int *bad) {
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
-        if (order[k] != (int)k) *bad = 1;
+__global__ void k_increasing_pair(long long n, const int *cnt, int *bad) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k + 1 < n; k += (long long)gridDim.x * blockDim.x)
+        if (cnt[k] < cnt[k + 1]) *bad = 1;
 }
 __global__ void k_perm_from_order(long long ng, const int *order, int *perm) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < ng; k += (long long)gridDim.x * blockDim.x)
@@ -378,6 +378,21 @@ int spmv_rb_mode() {   // read at every region launch (the signature records the
     return (e && *e) ? (e[0] == '1' ? 1 : 0) : -1;
 }
 
+// NBG_PLAN_BUILD_PROFILE=1: device-synchronised phase times of the plan builders on stderr
+struct BuildProf {
+    Ctx &c;
+    bool on;
+    double t;
+    explicit BuildProf(Ctx &cc) : c(cc), on(getenv("NBG_PLAN_BUILD_PROFILE") != nullptr), t(0) { if (on) { cudaStreamSynchronize(c.stream); t = now_ns(); } }
+    void mark(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(c.stream);
+        const double u = now_ns();
+        fprintf(stderr, "[nbg plan build] %-28s %8.3f ms\n", what, (u - t) * 1e-6);
+        t = u;
+    }
+};
+
 // Row-binned plan (RbPlan, DESIGN.md §7 "row-binned SpMV").  Device: group counts, mask, histogram
 // per class, stable radix sort of the binned rows, the column-major slice fill.  Host: from the
 // histograms alone (the sorted g sequence of each class is determined by them) the slices (per row
@@ -415,6 +430,7 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
     NG = (int)std::max(1ll, (n + gsize - 1) / gsize);
     R->ngrp = NG;
     const int NC = NG + 1;                                             // classes: long, then short per row group
+    BuildProf bp(c);
     const int gr = grid_for(n, c.num_sms);
     BufP key = alloc_buf(c, (size_t)n * 4), flag = alloc_buf(c, (size_t)n), hist = alloc_buf(c, (size_t)NC * (SP_LONG_G + 1) * 8);
     R->mask = alloc_buf(c, (size_t)((n + 31) / 32) * 4);
@@ -449,6 +465,7 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
         NBG_CUDA(cub::DeviceRadixSort::SortPairs(tmp->d, tb, (const unsigned *)keys2->d, (unsigned *)key->d, (const int *)ids->d,
                                                  (int *)sorted->d, (int64_t)m, 0, bits, c.stream));
     }
+    bp.mark("rb: keys, selects, sort");
     long long nlong = 0, nshort = 0;
     for (int g = 1; g <= SP_LONG_G; g++) nlong += h(0, g);
     for (int cl = 1; cl < NC; cl++)
@@ -459,6 +476,11 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
     std::vector<int> swid, sgrp, sfc;   // sfc: int2 {first sorted index, count}
     std::vector<long long> soff;
     {
+        const size_t ns_max = (size_t)(nshort / 32 + NG + 1);
+        swid.reserve(ns_max);
+        sgrp.reserve(ns_max);
+        soff.reserve(ns_max);
+        sfc.reserve(2 * ns_max);
         long long pos = nlong, off = 0;
         for (int q = 0; q < NG; q++) {
             long long nq = 0;
@@ -482,9 +504,11 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
         R->sell_groups = off;
     }
     R->nslices = (long long)swid.size();
+    bp.mark("rb: host slices");
     // task records {kind | count << 2, first, z, w}: short runs z/w = slice offset lo/hi (main, inline)
     // or lo/row group (pipelined); epilogue chunks (pipelined) {3, row0, group}; empty-row ranges (inline) {3, row0}
     std::vector<int> head, tasks;   // head: hub + long tasks
+    head.reserve((size_t)(P.nchunks + nlong + 1) * 4);
     auto push = [&](std::vector<int> &v, int kind, long long count, long long first, long long z, long long w) {
         v.push_back((int)(kind | (count << 2)));
         v.push_back((int)first);
@@ -495,8 +519,7 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
     {
         std::vector<int> lg;   // the long rows' g, in plan order (descending)
         lg.reserve((size_t)nlong);
-        for (int g = SP_LONG_G; g >= 1; g--)
-            for (long long q = 0; q < h(0, g); q++) lg.push_back(g);
+        for (int g = SP_LONG_G; g >= 1; g--) lg.insert(lg.end(), (size_t)h(0, g), g);
         long long j = 0;
         while (j < nlong) {
             const long long first = j;
@@ -510,7 +533,8 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
         }
     }
     // slice runs per row group (a run never crosses a group)
-    std::vector<std::vector<int>> sruns((size_t)NG), sruns_p((size_t)NG);
+    std::vector<std::vector<int>> sruns((size_t)NG);
+    for (auto &v : sruns) v.reserve((size_t)(R->nslices / std::max(1, NG) + 8) * 4);
     {
         const long long tl = std::max(1ll, tg / 32);   // lane-groups per slice task
         long long s = 0;
@@ -524,60 +548,21 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
                 s++;
             }
             push(sruns[q], 2, cntr, first, soff[first], (long long)((unsigned long long)soff[first] >> 32));
-            push(sruns_p[q], 2, cntr, first, soff[first], q);
         }
     }
+    bp.mark("rb: host runs");
     // main list (barrier mode)
     tasks = head;
     for (int q = 0; q < NG; q++) tasks.insert(tasks.end(), sruns[q].begin(), sruns[q].end());
     R->ntasks_main = (long long)tasks.size() / 4;
     R->tasks_main = alloc_buf(c, std::max<size_t>(tasks.size() * 4, 16));
     if (!tasks.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks_main->d, tasks.data(), tasks.size() * 4, cudaMemcpyHostToDevice, c.stream));
-    // inline list: + empty-row ranges (kind 3) interleaved evenly
-    std::vector<int> mixed;
-    {
-        const long long nmain = (long long)tasks.size() / 4, nemp = (n + RE - 1) / RE;
-        mixed.reserve((size_t)(nmain + nemp) * 4);
-        long long e = 0;
-        auto emp = [&](long long e2) { const long long r0 = e2 * RE; push(mixed, 3, std::min(RE, n - r0), r0, 0, 0); };
-        for (long long t = 0; t < nmain; t++) {
-            const long long want = (t * nemp) / std::max(1ll, nmain);   // empties placed before task t
-            for (; e < want; e++) emp(e);
-            mixed.insert(mixed.end(), tasks.begin() + 4 * t, tasks.begin() + 4 * t + 4);
-        }
-        for (; e < nemp; e++) emp(e);
-        R->ntasks = (long long)mixed.size() / 4;
-        R->tasks = alloc_buf(c, std::max<size_t>(mixed.size() * 4, 16));
-        if (!mixed.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks->d, mixed.data(), mixed.size() * 4, cudaMemcpyHostToDevice, c.stream));
-    }
-    // pipelined list: head, then the slice runs of row group 0, 1, ...; the epilogue chunks of a row
-    // group are not queued: warps take them (gsize / RE per group) once the group's totals are complete
-    std::vector<int> pl = head, gcnt((size_t)NG + 1, 0);
-    {
-        gcnt[0] = (int)(head.size() / 4);
-        for (int q = 0; q < NG; q++) {
-            pl.insert(pl.end(), sruns_p[q].begin(), sruns_p[q].end());
-            gcnt[1 + q] = (int)(sruns_p[q].size() / 4);
-        }
-        R->gsize = gsize;
-        R->ntasks_pipe = (long long)pl.size() / 4;
-        R->tasks_pipe = alloc_buf(c, std::max<size_t>(pl.size() * 4, 16));
-        if (!pl.empty()) NBG_CUDA(cudaMemcpyAsync(R->tasks_pipe->d, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        // + [NG + 1 + q]: end (exclusive) of group q's slice runs in the list -- once the claims pass it,
-        // the group can complete and the kernel starts polling its counter
-        {
-            int end = gcnt[0];
-            for (int q = 0; q < NG; q++) { end += gcnt[1 + q]; gcnt.push_back(end); }
-        }
-        R->gcnt = alloc_buf(c, gcnt.size() * 4);
-        NBG_CUDA(cudaMemcpyAsync(R->gcnt->d, gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice, c.stream));
-        R->pipe_ok = R->sell_groups < (1ll << 31);   // pipelined short records keep 32 bits of the slice offset
-        // counters, zero between launches (the last CTA out resets them): [0] hub + long tasks done,
-        // [1 + q] slice runs of group q done, [1 + NG + q] epilogue chunks of group q taken, [1 + 2 NG]
-        // task claims, [2 + 2 NG] CTAs out
-        R->done = alloc_buf(c, (2 * (size_t)NG + 3) * 8);
-        NBG_CUDA(cudaMemsetAsync(R->done->d, 0, (2 * (size_t)NG + 3) * 8, c.stream));
-    }
+    // the inline and pipelined lists are built on first use (rb_task_list)
+    R->h_head = std::move(head);
+    R->h_sruns = std::move(sruns);
+    R->gsize = gsize;
+    R->pipe_ok = R->sell_groups < (1ll << 31);   // pipelined short records keep 32 bits of the slice offset
+    bp.mark("rb: host slices + task lists");
     R->lrows = alloc_buf(c, (size_t)std::max<long long>(nlong, 1) * 4);
     if (nlong > 0) NBG_CUDA(cudaMemcpyAsync(R->lrows->d, sorted->d, (size_t)nlong * 4, cudaMemcpyDeviceToDevice, c.stream));
     R->srow = alloc_buf(c, (size_t)std::max<long long>(32 * R->nslices, 1) * 4);
@@ -597,9 +582,75 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
     NBG_CUDA(cudaMemsetAsync(R->bar->d, 0, 16, c.stream));
     NBG_CUDA(cudaGetLastError());
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
+    bp.mark("rb: slice fill");
     c.stats.kernels_launched += 5;
     P.rb = std::move(R);
     return P.rb.get();
+}
+
+// The task list of an epilogue mode ('b' main, 'i' inline, 'p' pipelined), built on first use from
+// the plan's host-side runs (gpu_rb_plan): the inline list interleaves 512-row empty-row tasks
+// (kind 3) evenly into the main list; the pipelined one is hub + long tasks, then the slice runs of
+// row group 0, 1, ... with the group in .w, plus per-group task counts and run ends (gcnt) and the
+// zeroed counters.  Returns the task buffer and sets *ntasks.
+const int *rb_task_list(Ctx &c, RbPlan &R, char mode, long long n, int64_t *ntasks) {
+    const long long RE = 512;
+    const int NG = R.ngrp;
+    auto push = [](std::vector<int> &v, int kind, long long count, long long first, long long z, long long w) {
+        v.push_back((int)(kind | (count << 2)));
+        v.push_back((int)first);
+        v.push_back((int)(unsigned)(z & 0xffffffffll));
+        v.push_back((int)(unsigned)((unsigned long long)w & 0xffffffffull));
+    };
+    if (mode == 'i' && !R.tasks) {
+        std::vector<int> main = R.h_head;
+        for (int q = 0; q < NG; q++) main.insert(main.end(), R.h_sruns[q].begin(), R.h_sruns[q].end());
+        std::vector<int> mixed;
+        const long long nmain = (long long)main.size() / 4, nemp = (n + RE - 1) / RE;
+        mixed.reserve((size_t)(nmain + nemp) * 4);
+        long long e = 0;
+        auto emp = [&](long long e2) { const long long r0 = e2 * RE; push(mixed, 3, std::min(RE, n - r0), r0, 0, 0); };
+        for (long long t = 0; t < nmain; t++) {
+            const long long want = (t * nemp) / std::max(1ll, nmain);   // empties placed before task t
+            for (; e < want; e++) emp(e);
+            mixed.insert(mixed.end(), main.begin() + 4 * t, main.begin() + 4 * t + 4);
+        }
+        for (; e < nemp; e++) emp(e);
+        R.ntasks = (long long)mixed.size() / 4;
+        R.tasks = alloc_buf(c, std::max<size_t>(mixed.size() * 4, 16));
+        if (!mixed.empty()) NBG_CUDA(cudaMemcpyAsync(R.tasks->d, mixed.data(), mixed.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    if (mode == 'p' && !R.tasks_pipe) {
+        std::vector<int> pl = R.h_head, gcnt((size_t)NG + 1, 0);
+        gcnt[0] = (int)(R.h_head.size() / 4);
+        for (int q = 0; q < NG; q++) {
+            for (size_t t = 0; t < R.h_sruns[q].size(); t += 4) {   // .w = the row group (offsets < 2^31: pipe_ok)
+                pl.insert(pl.end(), R.h_sruns[q].begin() + t, R.h_sruns[q].begin() + t + 3);
+                pl.push_back(q);
+            }
+            gcnt[1 + q] = (int)(R.h_sruns[q].size() / 4);
+        }
+        // + [NG + 1 + q]: end (exclusive) of group q's slice runs in the list -- once the claims pass it,
+        // the group can complete and the kernel starts polling its counter
+        int end = gcnt[0];
+        for (int q = 0; q < NG; q++) { end += gcnt[1 + q]; gcnt.push_back(end); }
+        R.ntasks_pipe = (long long)pl.size() / 4;
+        R.tasks_pipe = alloc_buf(c, std::max<size_t>(pl.size() * 4, 16));
+        if (!pl.empty()) NBG_CUDA(cudaMemcpyAsync(R.tasks_pipe->d, pl.data(), pl.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        R.gcnt = alloc_buf(c, gcnt.size() * 4);
+        NBG_CUDA(cudaMemcpyAsync(R.gcnt->d, gcnt.data(), gcnt.size() * 4, cudaMemcpyHostToDevice, c.stream));
+        // counters, zero between launches (the last CTA out resets them): [0] hub + long tasks done,
+        // [1 + q] slice runs of group q done, [1 + NG + q] epilogue chunks of group q taken, [1 + 2 NG]
+        // task claims, [2 + 2 NG] CTAs out
+        R.done = alloc_buf(c, (2 * (size_t)NG + 3) * 8);
+        NBG_CUDA(cudaMemsetAsync(R.done->d, 0, (2 * (size_t)NG + 3) * 8, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    if (mode == 'i') { *ntasks = R.ntasks; return (const int *)R.tasks->d; }
+    if (mode == 'p') { *ntasks = R.ntasks_pipe; return (const int *)R.tasks_pipe->d; }
+    *ntasks = R.ntasks_main;
+    return (const int *)R.tasks_main->d;
 }
 
 TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta) {
@@ -1110,6 +1161,7 @@ MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int
 }
 
 void gpu_build_spmv_plan(Ctx &c, Mat &A) {
+    BuildProf bp(c);
     auto P = std::make_unique<SpmvPlan>();
     const long long n = A.nrows;
     if (n == 0) {
@@ -1128,32 +1180,37 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         BufP cnt = alloc_buf(c, (size_t)nc * 4);
         NBG_CUDA(cudaMemsetAsync(cnt->d, 0, (size_t)nc * 4, c.stream));
         k_col_count<<<2 * c.num_sms, 1024, 0, c.stream>>>(A.nnz, nc, (const int *)A.colidx->d, (int *)cnt->d);
-        BufP key = alloc_buf(c, (size_t)nc * 4), key2 = alloc_buf(c, (size_t)nc * 4);
-        BufP ids = alloc_buf(c, (size_t)nc * 4), ids2 = alloc_buf(c, (size_t)nc * 4);
-        BufP ne = alloc_buf(c, 4);
-        NBG_CUDA(cudaMemsetAsync(ne->d, 0, 4, c.stream));
-        k_col_keys<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (unsigned *)key->d, (int *)ids->d,
-                                                                  (int *)ne->d);
-        size_t tb3 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb3, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
-                                        (int *)ids2->d, (int64_t)nc, 0, 32, c.stream);
-        BufP t3 = alloc_buf(c, std::max<size_t>(tb3, 16));
-        NBG_CUDA(cub::DeviceRadixSort::SortPairs(t3->d, tb3, (const unsigned *)key->d, (unsigned *)key2->d,
-                                                 (const int *)ids->d, (int *)ids2->d, (int64_t)nc, 0, 32, c.stream));
-        int ng = 0;
-        NBG_CUDA(cudaMemcpyAsync(&ng, ne->d, 4, cudaMemcpyDeviceToHost, c.stream));
-        // already in the gather layout (a symmetrically relabelled matrix: columns by descending count,
-        // ties by id, empty columns last)?  Then no relabel: the gathered vector is the plain vector and
-        // side outputs in its layout are plain row-order stores (no scatter map)
+        // already in the gather layout (a symmetrically relabelled matrix)?  The stable sort by
+        // descending count is the identity exactly when the counts never increase with the id (empty
+        // columns last).  Then no relabel: the gathered vector is the plain vector and side outputs in
+        // its layout are plain row-order stores (no scatter map)
         BufP notid = alloc_buf(c, 4);
         NBG_CUDA(cudaMemsetAsync(notid->d, 0, 4, c.stream));
-        k_not_identity<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)ids2->d, (int *)notid->d);
+        k_increasing_pair<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (int *)notid->d);
         int nid = 1;
         NBG_CUDA(cudaMemcpyAsync(&nid, notid->d, 4, cudaMemcpyDeviceToHost, c.stream));
         NBG_CUDA(cudaStreamSynchronize(c.stream));
-        if (!nid) want_id = true;
-        sorted_ids = ids2;
-        sorted_ng = ng;
+        if (!nid) {
+            want_id = true;
+        } else {
+            BufP key = alloc_buf(c, (size_t)nc * 4), key2 = alloc_buf(c, (size_t)nc * 4);
+            BufP ids = alloc_buf(c, (size_t)nc * 4), ids2 = alloc_buf(c, (size_t)nc * 4);
+            BufP ne = alloc_buf(c, 4);
+            NBG_CUDA(cudaMemsetAsync(ne->d, 0, 4, c.stream));
+            k_col_keys<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (unsigned *)key->d, (int *)ids->d,
+                                                                      (int *)ne->d);
+            size_t tb3 = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb3, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
+                                            (int *)ids2->d, (int64_t)nc, 0, 32, c.stream);
+            BufP t3 = alloc_buf(c, std::max<size_t>(tb3, 16));
+            NBG_CUDA(cub::DeviceRadixSort::SortPairs(t3->d, tb3, (const unsigned *)key->d, (unsigned *)key2->d,
+                                                     (const int *)ids->d, (int *)ids2->d, (int64_t)nc, 0, 32, c.stream));
+            int ng = 0;
+            NBG_CUDA(cudaMemcpyAsync(&ng, ne->d, 4, cudaMemcpyDeviceToHost, c.stream));
+            NBG_CUDA(cudaStreamSynchronize(c.stream));
+            sorted_ids = ids2;
+            sorted_ng = ng;
+        }
     }
     if (want && A.nnz > 0 && !A.vals && !want_id) {
         const long long nc = A.ncols;
@@ -1173,6 +1230,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         P->relabel = true;
         c.stats.kernels_launched += 5;
     }
+    bp.mark("base: column relabel");
     // ---- 4-entry groups: grp[i] = first group of row i; cg = group-padded column indices (-1 pad)
     BufP ngb = alloc_buf(c, (size_t)(n + 1) * 8);
     P->grp = alloc_buf(c, (size_t)(n + 1) * 8);
@@ -1221,6 +1279,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     NBG_CUDA(cudaGetLastError());
     c.stats.kernels_launched += 3;
 
+    bp.mark("base: groups + fill");
     // ---- warp tasks, built on the device (once per matrix): a task starts at every 128th row, at
     // every crossing of a multiple of SP_TASK_G short-row groups and around every long row (> SP_LONG_G
     // groups); long rows are cut into chunks of SP_CHUNK_G groups instead.  Tasks hold <= 128 rows and
@@ -1298,6 +1357,7 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
         c.stats.kernels_launched += 6;
     }
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
+    bp.mark("base: tasks + chunks");
     A.plan = std::move(P);
 }
 

@@ -182,7 +182,9 @@ struct RbPlan {
     int64_t gsize = 0;
     bool pipe_ok = false;
     BufP gcnt;      // int[2 ngrp + 1]  tasks per counter: [0] hub + long, [1 + q] slice runs of group q; [1 + ngrp + q] end of group q's runs
-    BufP done;      // u64[2 ngrp + 3]  pipelined counters (zero between launches; see gpu_rb_plan)
+    BufP done;      // u64[2 ngrp + 3]  pipelined counters (zero between launches; see rb_task_list)
+    std::vector<int> h_head;                  // host copies for the lazily built lists: hub + long task records,
+    std::vector<std::vector<int>> h_sruns;    // and the slice runs per row group (pipelined form, .w = group)
     BufP mask;      // u32[(n + 31) / 32]  bit i: row i is non-empty
     BufP tot;       // 8 bytes per row: row totals (the kernel's row-total type)
     BufP bar;       // u32[2]  grid barrier {arrivals, generation}
@@ -579,6 +581,7 @@ DistGraph gpu_dist_graph(Ctx &c, const nbg_graphgen &g, int rank, int P, long lo
                          const std::function<void(int *, long long)> &allreduce_int_sum);
 TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta);   // null if not applicable
 RbPlan *gpu_rb_plan(Ctx &c, Mat &A);                         // null if not applicable (valued matrices)
+const int *rb_task_list(Ctx &c, RbPlan &R, char mode, long long n, int64_t *ntasks);   // task list of an epilogue mode (lazy)
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
 void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng);
 int gpu_validate_csr(Ctx &c, long long n, long long ncols, long long nnz, const long long *rp, const int *ci);

@@ -775,12 +775,15 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             if (R) {
                 p.rb = true;
                 p.vec = vec;   // the epilogue uses 16-byte vector loads when every buffer allows them
-                const char md = spmv_rb_epi_mode();
+                char md = spmv_rb_epi_mode();
+                if (md == 'p' && !R->pipe_ok) md = 'b';
                 p.rb_inline = md == 'i';
-                p.rb_pipe = md == 'p' && R->pipe_ok;
-                args.rb_tasks = (const int *)(p.rb_inline ? R->tasks->d : (p.rb_pipe ? R->tasks_pipe->d : R->tasks_main->d));
-                args.rb_done = (unsigned long long *)R->done->d;
-                args.rb_gcnt = (const int *)R->gcnt->d;
+                p.rb_pipe = md == 'p';
+                int64_t nt = 0;
+                args.rb_tasks = rb_task_list(c, *R, md, n, &nt);
+                args.rb_ntasks = nt;
+                args.rb_done = R->done ? (unsigned long long *)R->done->d : nullptr;
+                args.rb_gcnt = R->gcnt ? (const int *)R->gcnt->d : nullptr;
                 args.rb_ngrp = R->ngrp;
                 args.rb_gsize = R->gsize;
                 args.rb_sell = (const int *)R->sell->d;
@@ -790,7 +793,7 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
                 args.rb_mask = (const unsigned *)R->mask->d;
                 args.rb_tot = R->tot->d;
                 args.rb_bar = (unsigned *)R->bar->d;
-                args.rb_ntasks = p.rb_inline ? R->ntasks : (p.rb_pipe ? R->ntasks_pipe : R->ntasks_main);
+
                 items = 1ll << 40;   // persistent: one CTA per SM (clamped to the kernel's grid_cap)
             }
         }
