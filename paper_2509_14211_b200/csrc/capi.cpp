@@ -400,11 +400,26 @@ static BufP upload(Ctx &c, const void *p, size_t bytes, int space, int own, bool
     return b;
 }
 
-// the caller's host buffers may be reused once the call returns, error or not
+// the caller's host buffers may be reused once the call returns, error or not (the side stream
+// carries the overlapped column-index upload of nbg_matrix_from_csr)
 struct HostCopiesDone {
     Ctx &c;
-    ~HostCopiesDone() { cudaStreamSynchronize(c.stream); }
+    ~HostCopiesDone() {
+        cudaStreamSynchronize(c.stream);
+        if (c.rb_stream) cudaStreamSynchronize(c.rb_stream);
+    }
 };
+
+// Eager ingestion of a large host CSR without values (NBG_EAGER_PLAN=0 turns it off): the SpMV plan's
+// structure (row pointers only: groups, skew, tasks, and the row-binned bins / slices / task lists)
+// is built while the column indices travel over PCIe on a side stream; the column-dependent fill
+// (relabel, padded indices, slice fill) follows the copy.  C4: upload 5.8 ms + plan 3.4 ms at the
+// first solve -> ingestion ≈ 7.x ms with the plan done (DESIGN.md §7 "e2e").
+static bool eager_plan_wanted(int64_t nrows, int64_t nnz, const void *vals, int space) {
+    const char *e = getenv("NBG_EAGER_PLAN");
+    if (e && e[0] == '0') return false;
+    return space == NBG_HOST && !vals && nrows > 0 && nnz >= (1ll << 19);
+}
 
 nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64_t ncols, int64_t nnz,
                                const int64_t *rowptr, const int32_t *colidx, const void *vals, int type, double iso,
@@ -427,6 +442,31 @@ nbg_status nbg_matrix_from_csr(nbg_ctx *ctx, nbg_matrix *A, int64_t nrows, int64
     M->type = type;
     M->iso = host_round(type, iso);
     HostCopiesDone done_{*ctx};
+    if (eager_plan_wanted(nrows, nnz, vals, space)) {
+        Ctx &c = *ctx;
+        M->rowptr = upload(c, rowptr, (size_t)(nrows + 1) * 8, space, own, false);
+        // the structure is built from the row pointers: validate them first
+        int bad = gpu_validate_csr(c, nrows, ncols, nnz, (const long long *)M->rowptr->d, nullptr);
+        if (bad & 1) fail(NBG_INVALID_VALUE, "rowptr must start at 0, end at nnz and be non-decreasing");
+        M->colidx = alloc_buf(c, (size_t)nnz * 4);
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        NBG_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        NBG_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        struct EvGuard { cudaEvent_t *e; ~EvGuard() { cudaEventDestroy(e[0]); cudaEventDestroy(e[1]); } } evg{ev};
+        NBG_CUDA(cudaEventRecord(ev[0], c.stream));            // the buffer's allocation, in stream order
+        NBG_CUDA(cudaStreamWaitEvent(c.rb_stream, ev[0], 0));
+        NBG_CUDA(cudaMemcpyAsync(M->colidx->d, colidx, (size_t)nnz * 4, cudaMemcpyHostToDevice, c.rb_stream));
+        NBG_CUDA(cudaEventRecord(ev[1], c.rb_stream));
+        gpu_build_spmv_plan(c, *M, 1);
+        if (!M->plan->low_skew) gpu_rb_plan(c, *M, false);
+        NBG_CUDA(cudaStreamWaitEvent(c.stream, ev[1], 0));
+        bad = gpu_validate_csr(c, nrows, ncols, nnz, nullptr, (const int *)M->colidx->d);
+        if (bad & 2) fail(NBG_INDEX_OUT_OF_BOUNDS, "column index out of range");
+        gpu_build_spmv_plan(c, *M, 2);
+        if (M->plan->rb) gpu_rb_fill(c, *M);
+        *A = new nbg_matrix_s{ctx, M};
+        return NBG_SUCCESS;
+    }
     M->rowptr = upload(*ctx, rowptr, (size_t)(nrows + 1) * 8, space, own, false);
     M->colidx = upload(*ctx, colidx, (size_t)nnz * 4, space, own, false);
     if (vals) M->vals = upload(*ctx, vals, (size_t)nnz * type_size(type), space, own, false);

@@ -139,11 +139,11 @@ __global__ void k_rebase(long long n, const long long *rp, long long base, long 
 // structural checks of a user CSR: bit0 rowptr ends/monotone, bit1 column index out of range
 __global__ void k_validate_csr(long long n, long long ncols, long long nnz, const long long *rp, const int *ci, int *bad) {
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += stride) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; rp && i <= n; i += stride) {
         long long v = rp[i];
         if ((i == 0 && v != 0) || (i == n && v != nnz) || (i < n && rp[i + 1] < v)) atomicOr(bad, 1);
     }
-    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; p < nnz; p += stride) {
+    for (long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x; ci && p < nnz; p += stride) {
         int c = ci[p];
         if (c < 0 || c >= ncols) atomicOr(bad, 2);
     }
@@ -403,11 +403,14 @@ struct BuildProf {
 //   pipelined slice runs grouped by row group, and after the slices of group q + 1 the epilogue
 //             tasks of group q (512-row chunks), which wait until every long / hub task and every
 //             slice task of group q has completed.
-RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
+RbPlan *gpu_rb_plan(Ctx &c, Mat &A, bool fill) {
     if (!A.plan) gpu_build_spmv_plan(c, A);
     SpmvPlan &P = *A.plan;
     if (A.vals || A.nrows == 0) return nullptr;
-    if (P.rb) return P.rb.get();
+    if (P.rb) {
+        if (fill && !P.rb->filled) gpu_rb_fill(c, A);
+        return P.rb.get();
+    }
     auto R = std::make_unique<RbPlan>();
     const long long n = A.nrows;
     {
@@ -573,19 +576,38 @@ RbPlan *gpu_rb_plan(Ctx &c, Mat &A) {
         NBG_CUDA(cudaMemcpyAsync(R->swid->d, swid.data(), (size_t)R->nslices * 4, cudaMemcpyHostToDevice, c.stream));
         NBG_CUDA(cudaMemcpyAsync(so->d, soff.data(), (size_t)R->nslices * 8, cudaMemcpyHostToDevice, c.stream));
         NBG_CUDA(cudaMemcpyAsync(fc->d, sfc.data(), (size_t)R->nslices * 8, cudaMemcpyHostToDevice, c.stream));
-        k_rb_fill<<<grid_for(32 * R->nslices, c.num_sms), 256, 0, c.stream>>>(
-            32 * R->nslices, (const int *)sorted->d, (const int2 *)fc->d, (const long long *)P.grp->d, (const int4 *)P.cg->d,
-            (const int *)R->swid->d, (const long long *)so->d, (int *)R->srow->d, (int4 *)R->sell->d);
+        R->pend_sorted = sorted;
+        R->pend_fc = fc;
+        R->pend_so = so;
     }
     R->tot = alloc_buf(c, (size_t)n * 8);
     R->bar = alloc_buf(c, 16);
     NBG_CUDA(cudaMemsetAsync(R->bar->d, 0, 16, c.stream));
     NBG_CUDA(cudaGetLastError());
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
-    bp.mark("rb: slice fill");
-    c.stats.kernels_launched += 5;
+    c.stats.kernels_launched += 4;
     P.rb = std::move(R);
+    if (fill) gpu_rb_fill(c, A);
+    bp.mark("rb: slice fill");
     return P.rb.get();
+}
+
+// the column-major slice fill (needs the plan's group-padded indices, stage 2 of the plan)
+void gpu_rb_fill(Ctx &c, Mat &A) {
+    SpmvPlan &P = *A.plan;
+    RbPlan &R = *P.rb;
+    if (R.filled) return;
+    if (R.nslices > 0) {
+        k_rb_fill<<<grid_for(32 * R.nslices, c.num_sms), 256, 0, c.stream>>>(
+            32 * R.nslices, (const int *)R.pend_sorted->d, (const int2 *)R.pend_fc->d, (const long long *)P.grp->d,
+            (const int4 *)P.cg->d, (const int *)R.swid->d, (const long long *)R.pend_so->d, (int *)R.srow->d, (int4 *)R.sell->d);
+        NBG_CUDA(cudaGetLastError());
+        c.stats.kernels_launched++;
+    }
+    R.pend_sorted.reset();   // stream-ordered release after the fill
+    R.pend_fc.reset();
+    R.pend_so.reset();
+    R.filled = true;
 }
 
 // The task list of an epilogue mode ('b' main, 'i' inline, 'p' pipelined), built on first use from
@@ -1160,77 +1182,12 @@ MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int
     return A;
 }
 
-void gpu_build_spmv_plan(Ctx &c, Mat &A) {
-    BuildProf bp(c);
-    auto P = std::make_unique<SpmvPlan>();
+// SpMV plan, in two stages so that matrix ingestion can overlap them with the column-index upload
+// (nbg_matrix_from_csr): the structure needs the row pointers only -- 4-entry groups, degree skew,
+// the padded index array (allocated, -1), warp tasks and long-row chunks --; the fill needs the
+// column indices -- the gather-layout relabel and the group-padded copy of the indices (and values).
+static void plan_structure(Ctx &c, Mat &A, SpmvPlan *P, BuildProf &bp) {
     const long long n = A.nrows;
-    if (n == 0) {
-        A.plan = std::move(P);
-        return;
-    }
-    // ---- gather layout: relabel columns by descending count (big matrices only; DESIGN.md)
-    const char *rl = getenv("NBG_RELABEL");
-    const bool want = !A.prelabeled && (rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15)));
-    BufP colsrc = A.colidx;
-    bool want_id = false;   // the column order is already the gather layout
-    BufP sorted_ids;
-    int sorted_ng = 0;
-    if (want && A.nnz > 0 && !A.vals) {
-        const long long nc = A.ncols;
-        BufP cnt = alloc_buf(c, (size_t)nc * 4);
-        NBG_CUDA(cudaMemsetAsync(cnt->d, 0, (size_t)nc * 4, c.stream));
-        k_col_count<<<2 * c.num_sms, 1024, 0, c.stream>>>(A.nnz, nc, (const int *)A.colidx->d, (int *)cnt->d);
-        // already in the gather layout (a symmetrically relabelled matrix)?  The stable sort by
-        // descending count is the identity exactly when the counts never increase with the id (empty
-        // columns last).  Then no relabel: the gathered vector is the plain vector and side outputs in
-        // its layout are plain row-order stores (no scatter map)
-        BufP notid = alloc_buf(c, 4);
-        NBG_CUDA(cudaMemsetAsync(notid->d, 0, 4, c.stream));
-        k_increasing_pair<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (int *)notid->d);
-        int nid = 1;
-        NBG_CUDA(cudaMemcpyAsync(&nid, notid->d, 4, cudaMemcpyDeviceToHost, c.stream));
-        NBG_CUDA(cudaStreamSynchronize(c.stream));
-        if (!nid) {
-            want_id = true;
-        } else {
-            BufP key = alloc_buf(c, (size_t)nc * 4), key2 = alloc_buf(c, (size_t)nc * 4);
-            BufP ids = alloc_buf(c, (size_t)nc * 4), ids2 = alloc_buf(c, (size_t)nc * 4);
-            BufP ne = alloc_buf(c, 4);
-            NBG_CUDA(cudaMemsetAsync(ne->d, 0, 4, c.stream));
-            k_col_keys<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (unsigned *)key->d, (int *)ids->d,
-                                                                      (int *)ne->d);
-            size_t tb3 = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb3, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
-                                            (int *)ids2->d, (int64_t)nc, 0, 32, c.stream);
-            BufP t3 = alloc_buf(c, std::max<size_t>(tb3, 16));
-            NBG_CUDA(cub::DeviceRadixSort::SortPairs(t3->d, tb3, (const unsigned *)key->d, (unsigned *)key2->d,
-                                                     (const int *)ids->d, (int *)ids2->d, (int64_t)nc, 0, 32, c.stream));
-            int ng = 0;
-            NBG_CUDA(cudaMemcpyAsync(&ng, ne->d, 4, cudaMemcpyDeviceToHost, c.stream));
-            NBG_CUDA(cudaStreamSynchronize(c.stream));
-            sorted_ids = ids2;
-            sorted_ng = ng;
-        }
-    }
-    if (want && A.nnz > 0 && !A.vals && !want_id) {
-        const long long nc = A.ncols;
-        BufP ids2 = sorted_ids;
-        const int ng = sorted_ng;
-        P->perm = alloc_buf(c, (size_t)nc * 4);
-        NBG_CUDA(cudaMemsetAsync(P->perm->d, 0xff, (size_t)nc * 4, c.stream));
-        P->iperm = alloc_buf(c, (size_t)std::max(ng, 1) * 4);
-        NBG_CUDA(cudaMemcpyAsync(P->iperm->d, ids2->d, (size_t)ng * 4, cudaMemcpyDeviceToDevice, c.stream));
-        k_perm_from_order<<<grid_for(ng, c.num_sms), 256, 0, c.stream>>>(ng, (const int *)ids2->d, (int *)P->perm->d);
-        colsrc = alloc_buf(c, (size_t)A.nnz * 4);
-        k_map_cols<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (const int *)P->perm->d,
-                                                                     (int *)colsrc->d);
-        P->colidx_g = colsrc;
-        NBG_CUDA(cudaGetLastError());
-        P->ncols_g = ng;
-        P->relabel = true;
-        c.stats.kernels_launched += 5;
-    }
-    bp.mark("base: column relabel");
     // ---- 4-entry groups: grp[i] = first group of row i; cg = group-padded column indices (-1 pad)
     BufP ngb = alloc_buf(c, (size_t)(n + 1) * 8);
     P->grp = alloc_buf(c, (size_t)(n + 1) * 8);
@@ -1256,30 +1213,6 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     }
     P->cg = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * 4);
     NBG_CUDA(cudaMemsetAsync(P->cg->d, 0xff, (size_t)std::max<long long>(4 * G, 4) * 4, c.stream));
-    BufP crow = alloc_buf(c, (size_t)std::max<long long>((A.nnz + 15) / 16, 1) * 4);
-    if (A.nnz > 0) {
-        k_chunk_rows<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, (const long long *)A.rowptr->d, (int *)crow->d);
-        k_fill_groups<int><<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const long long *)A.rowptr->d,
-                                                                             (const long long *)P->grp->d, (const int *)crow->d,
-                                                                             (const int *)colsrc->d, (int *)P->cg->d);
-    }
-    if (A.vals) {
-        const size_t es = type_size(A.type);
-        P->vals_g = alloc_buf(c, (size_t)std::max<long long>(4 * G, 4) * es);
-        NBG_CUDA(cudaMemsetAsync(P->vals_g->d, 0, (size_t)std::max<long long>(4 * G, 4) * es, c.stream));
-        if (A.nnz > 0) {
-            const long long *rp = (const long long *)A.rowptr->d, *gp = (const long long *)P->grp->d;
-            const int *cr = (const int *)crow->d;
-            const int gr = grid_for(A.nnz, c.num_sms);
-            if (es == 1) k_fill_groups<unsigned char><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const unsigned char *)A.vals->d, (unsigned char *)P->vals_g->d);
-            else if (es == 4) k_fill_groups<int><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const int *)A.vals->d, (int *)P->vals_g->d);
-            else k_fill_groups<long long><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const long long *)A.vals->d, (long long *)P->vals_g->d);
-        }
-    }
-    NBG_CUDA(cudaGetLastError());
-    c.stats.kernels_launched += 3;
-
-    bp.mark("base: groups + fill");
     // ---- warp tasks, built on the device (once per matrix): a task starts at every 128th row, at
     // every crossing of a multiple of SP_TASK_G short-row groups and around every long row (> SP_LONG_G
     // groups); long rows are cut into chunks of SP_CHUNK_G groups instead.  Tasks hold <= 128 rows and
@@ -1358,6 +1291,118 @@ void gpu_build_spmv_plan(Ctx &c, Mat &A) {
     }
     NBG_CUDA(cudaStreamSynchronize(c.stream));   // host vectors go out of scope
     bp.mark("base: tasks + chunks");
+}
+
+static void plan_fill(Ctx &c, Mat &A, SpmvPlan *P, BuildProf &bp) {
+    const long long n = A.nrows;
+    // ---- gather layout: relabel columns by descending count (big matrices only; DESIGN.md)
+    const char *rl = getenv("NBG_RELABEL");
+    const bool want = !A.prelabeled && (rl ? (rl[0] == '1') : (A.ncols >= (1ll << 15)));
+    BufP colsrc = A.colidx;
+    bool want_id = false;   // the column order is already the gather layout
+    BufP sorted_ids;
+    int sorted_ng = 0;
+    if (want && A.nnz > 0 && !A.vals) {
+        const long long nc = A.ncols;
+        BufP cnt = alloc_buf(c, (size_t)nc * 4);
+        NBG_CUDA(cudaMemsetAsync(cnt->d, 0, (size_t)nc * 4, c.stream));
+        k_col_count<<<2 * c.num_sms, 1024, 0, c.stream>>>(A.nnz, nc, (const int *)A.colidx->d, (int *)cnt->d);
+        // already in the gather layout (a symmetrically relabelled matrix)?  The stable sort by
+        // descending count is the identity exactly when the counts never increase with the id (empty
+        // columns last).  Then no relabel: the gathered vector is the plain vector and side outputs in
+        // its layout are plain row-order stores (no scatter map)
+        BufP notid = alloc_buf(c, 4);
+        NBG_CUDA(cudaMemsetAsync(notid->d, 0, 4, c.stream));
+        k_increasing_pair<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (int *)notid->d);
+        int nid = 1;
+        NBG_CUDA(cudaMemcpyAsync(&nid, notid->d, 4, cudaMemcpyDeviceToHost, c.stream));
+        NBG_CUDA(cudaStreamSynchronize(c.stream));
+        if (!nid) {
+            want_id = true;
+        } else {
+            BufP key = alloc_buf(c, (size_t)nc * 4), key2 = alloc_buf(c, (size_t)nc * 4);
+            BufP ids = alloc_buf(c, (size_t)nc * 4), ids2 = alloc_buf(c, (size_t)nc * 4);
+            BufP ne = alloc_buf(c, 4);
+            NBG_CUDA(cudaMemsetAsync(ne->d, 0, 4, c.stream));
+            k_col_keys<<<grid_for(nc, c.num_sms), 256, 0, c.stream>>>(nc, (const int *)cnt->d, (unsigned *)key->d, (int *)ids->d,
+                                                                      (int *)ne->d);
+            size_t tb3 = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb3, (const unsigned *)key->d, (unsigned *)key2->d, (const int *)ids->d,
+                                            (int *)ids2->d, (int64_t)nc, 0, 32, c.stream);
+            BufP t3 = alloc_buf(c, std::max<size_t>(tb3, 16));
+            NBG_CUDA(cub::DeviceRadixSort::SortPairs(t3->d, tb3, (const unsigned *)key->d, (unsigned *)key2->d,
+                                                     (const int *)ids->d, (int *)ids2->d, (int64_t)nc, 0, 32, c.stream));
+            int ng = 0;
+            NBG_CUDA(cudaMemcpyAsync(&ng, ne->d, 4, cudaMemcpyDeviceToHost, c.stream));
+            NBG_CUDA(cudaStreamSynchronize(c.stream));
+            sorted_ids = ids2;
+            sorted_ng = ng;
+        }
+    }
+    if (want && A.nnz > 0 && !A.vals && !want_id) {
+        const long long nc = A.ncols;
+        BufP ids2 = sorted_ids;
+        const int ng = sorted_ng;
+        P->perm = alloc_buf(c, (size_t)nc * 4);
+        NBG_CUDA(cudaMemsetAsync(P->perm->d, 0xff, (size_t)nc * 4, c.stream));
+        P->iperm = alloc_buf(c, (size_t)std::max(ng, 1) * 4);
+        NBG_CUDA(cudaMemcpyAsync(P->iperm->d, ids2->d, (size_t)ng * 4, cudaMemcpyDeviceToDevice, c.stream));
+        k_perm_from_order<<<grid_for(ng, c.num_sms), 256, 0, c.stream>>>(ng, (const int *)ids2->d, (int *)P->perm->d);
+        colsrc = alloc_buf(c, (size_t)A.nnz * 4);
+        k_map_cols<<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const int *)A.colidx->d, (const int *)P->perm->d,
+                                                                     (int *)colsrc->d);
+        P->colidx_g = colsrc;
+        NBG_CUDA(cudaGetLastError());
+        P->ncols_g = ng;
+        P->relabel = true;
+        c.stats.kernels_launched += 5;
+    }
+    bp.mark("base: column relabel");
+    BufP crow = alloc_buf(c, (size_t)std::max<long long>((A.nnz + 15) / 16, 1) * 4);
+    if (A.nnz > 0) {
+        k_chunk_rows<<<grid_for(n, c.num_sms), 256, 0, c.stream>>>(n, (const long long *)A.rowptr->d, (int *)crow->d);
+        k_fill_groups<int><<<grid_for(A.nnz, c.num_sms), 256, 0, c.stream>>>(A.nnz, (const long long *)A.rowptr->d,
+                                                                             (const long long *)P->grp->d, (const int *)crow->d,
+                                                                             (const int *)colsrc->d, (int *)P->cg->d);
+    }
+    if (A.vals) {
+        const size_t es = type_size(A.type);
+        P->vals_g = alloc_buf(c, (size_t)std::max<long long>(4 * P->ngroups, 4) * es);
+        NBG_CUDA(cudaMemsetAsync(P->vals_g->d, 0, (size_t)std::max<long long>(4 * P->ngroups, 4) * es, c.stream));
+        if (A.nnz > 0) {
+            const long long *rp = (const long long *)A.rowptr->d, *gp = (const long long *)P->grp->d;
+            const int *cr = (const int *)crow->d;
+            const int gr = grid_for(A.nnz, c.num_sms);
+            if (es == 1) k_fill_groups<unsigned char><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const unsigned char *)A.vals->d, (unsigned char *)P->vals_g->d);
+            else if (es == 4) k_fill_groups<int><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const int *)A.vals->d, (int *)P->vals_g->d);
+            else k_fill_groups<long long><<<gr, 256, 0, c.stream>>>(A.nnz, rp, gp, cr, (const long long *)A.vals->d, (long long *)P->vals_g->d);
+        }
+    }
+    NBG_CUDA(cudaGetLastError());
+    c.stats.kernels_launched += 2;
+
+    bp.mark("base: groups + fill");
+}
+
+void gpu_build_spmv_plan(Ctx &c, Mat &A, int stage) {
+    BuildProf bp(c);
+    if (stage == 2) {   // the fill of a plan whose structure was built before
+        plan_fill(c, A, A.plan.get(), bp);
+        A.plan->filled = true;
+        return;
+    }
+    auto P = std::make_unique<SpmvPlan>();
+    const long long n = A.nrows;
+    if (n == 0) {
+        P->filled = true;
+        A.plan = std::move(P);
+        return;
+    }
+    plan_structure(c, A, P.get(), bp);
+    if (stage == 0) {
+        plan_fill(c, A, P.get(), bp);
+        P->filled = true;
+    }
     A.plan = std::move(P);
 }
 

@@ -155,6 +155,7 @@ struct SpmvPlan {
     BufP colidx_g;           // int32[nnz] gather-layout column indices (relabelled matrices; two-phase build)
     std::unique_ptr<TpPlan> tp[2];   // two-phase plans for 4- and 8-byte gathered elements (lazy)
     std::unique_ptr<RbPlan> rb;   // row-binned plan (lazy, DESIGN.md §7 "row-binned SpMV")
+    bool filled = false;          // stage 2 (column indices) done
 };
 
 // Row-binned SpMV plan (DESIGN.md §7 "row-binned SpMV"), built once per matrix on top of the
@@ -183,6 +184,8 @@ struct RbPlan {
     bool pipe_ok = false;
     BufP gcnt;      // int[2 ngrp + 1]  tasks per counter: [0] hub + long, [1 + q] slice runs of group q; [1 + ngrp + q] end of group q's runs
     BufP done;      // u64[2 ngrp + 3]  pipelined counters (zero between launches; see rb_task_list)
+    bool filled = false;                      // slices filled (sell / srow); before: pend_* hold the fill's inputs
+    BufP pend_sorted, pend_fc, pend_so;
     std::vector<int> h_head;                  // host copies for the lazily built lists: hub + long task records,
     std::vector<std::vector<int>> h_sruns;    // and the slice runs per row group (pipelined form, .w = group)
     BufP mask;      // u32[(n + 31) / 32]  bit i: row i is non-empty
@@ -568,7 +571,9 @@ void gpu_l2_touch(Ctx &c, const void *base, size_t bytes, const cudaLaunchAttrib
 // graph (graph.cu)
 void gpu_graph_edges(Ctx &c, const nbg_graphgen &g, int32_t *d_src, int32_t *d_dst);
 MatP gpu_build_csr(Ctx &c, int64_t n, int64_t m, const int32_t *d_src, const int32_t *d_dst, BufP *deg_out);
-void gpu_build_spmv_plan(Ctx &c, Mat &A);
+// stage 0: the whole plan; 1: the structure (row pointers only); 2: the fill of a stage-1 plan
+// (column indices) -- nbg_matrix_from_csr overlaps stage 1 with the column-index upload
+void gpu_build_spmv_plan(Ctx &c, Mat &A, int stage = 0);
 // per-rank multi-GPU graph setup (graph.cu)
 struct DistGraph {
     MatP blk;                    // rows pi in [cuts[rank], cuts[rank+1]) x ncols_g columns (pi ids)
@@ -580,7 +585,9 @@ struct DistGraph {
 DistGraph gpu_dist_graph(Ctx &c, const nbg_graphgen &g, int rank, int P, long long bytes_per_row,
                          const std::function<void(int *, long long)> &allreduce_int_sum);
 TpPlan *gpu_tp_plan(Ctx &c, Mat &A, int xsize, int ncta);   // null if not applicable
-RbPlan *gpu_rb_plan(Ctx &c, Mat &A);                         // null if not applicable (valued matrices)
+RbPlan *gpu_rb_plan(Ctx &c, Mat &A, bool fill = true);      // null if not applicable (valued matrices); fill = false:
+                                                             // everything but the slice fill (needs the plan's fill)
+void gpu_rb_fill(Ctx &c, Mat &A);                            // the slice fill of a gpu_rb_plan(.., false) plan
 const int *rb_task_list(Ctx &c, RbPlan &R, char mode, long long n, int64_t *ntasks);   // task list of an epilogue mode (lazy)
 void gpu_fill_iso(Ctx &c, void *d, int type, int64_t n, double v);
 void gpu_permute(Ctx &c, const void *x, void *xg, int type, const int *iperm, int64_t ng);
