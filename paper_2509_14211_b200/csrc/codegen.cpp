@@ -2030,9 +2030,16 @@ int spmv_threads(int xsize) {
     if (v < 0) {
         const char *e = getenv("NBG_SPMV_THREADS");
         v = (e && *e) ? atoi(e) : 0;
-        if (v != 0 && v != 256 && v != 512 && v != 640 && v != 768 && v != 1024) v = 0;
+        if (v != 0 && v != 32 && v != 64 && v != 128 && v != 256 && v != 512 && v != 640 && v != 768 && v != 1024) v = 0;
     }
     return v ? v : (xsize <= 4 ? 1024 : 768);
+}
+
+bool spmv_threads_overridden() {
+    const char *e = getenv("NBG_SPMV_THREADS");
+    if (!(e && *e)) return false;
+    const int v = atoi(e);
+    return v == 32 || v == 64 || v == 128 || v == 256 || v == 512 || v == 640 || v == 768 || v == 1024;
 }
 
 // Launch shape of the task skeleton (DESIGN.md §7 "L2-only cold gathers"): 1024 threads for 4-byte
@@ -2047,7 +2054,7 @@ void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb) {
     if (et < 0) {
         const char *e = getenv("NBG_SPMV_THREADS");
         et = (e && *e) ? atoi(e) : 0;
-        if (et != 0 && et != 256 && et != 512 && et != 640 && et != 768 && et != 1024) et = 0;
+        if (et != 0 && et != 32 && et != 64 && et != 128 && et != 256 && et != 512 && et != 640 && et != 768 && et != 1024) et = 0;
         const char *h = getenv("NBG_SPMV_HOT_KB");
         eh = (h && *h) ? std::max(0, std::min(200, atoi(h))) : -1;
     }

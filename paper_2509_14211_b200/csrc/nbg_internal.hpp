@@ -555,6 +555,7 @@ void gpu_bitset_full(Ctx &c, int64_t n, uint32_t *bits);   // all n bits set, ta
 bool spmv_gather_pipeline();   // SpMV gathers one step ahead (NBG_SPMV_GPIPE=1)
 bool spmv_epilogue_prefetch();  // SpMV prefetches the epilogue's row inputs at task start (NBG_SPMV_PF, default on)
 int spmv_threads(int xsize);
+bool spmv_threads_overridden();   // NBG_SPMV_THREADS set to a valid CTA size
 int spmv_groups_per_lane();   // SpMV task skeleton: groups per lane per step (NBG_SPMV_GPL, default 2)
 void spmv_variant(int xsize, long long gathered_bytes, int *nt, int *hot_kb);   // per-matrix SpMV launch shape   // threads per SpMV CTA for a gathered element size (NBG_SPMV_THREADS overrides)
 int spmv_rb_mode();    // NBG_SPMV_RB: -1 auto (skewed matrices), 0 never, 1 always

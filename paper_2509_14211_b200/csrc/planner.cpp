@@ -804,6 +804,16 @@ static void run_region(Ctx &c, Builder &B, std::vector<HintOut> &hint_outs, int6
             args.part = T->part->d;
             items = (n + 127) / 128 / 8 + 1;      // phase 2: 128-row tiles, 8 warps per CTA
         }
+        // task skeleton on a matrix whose warp tasks would not fill the SMs at the default CTA size
+        // (C1: 48 tasks in 2 CTAs of 768 threads): 256-thread CTAs spread them over more SMs and
+        // shorten each CTA's block-level finish (C1 sweep kernel 14.8 -> 12.7 us, 0.43 -> 0.49
+        // GTEPS/iter; 32 / 64 / 128 threads measured no better).  The task order and every row's
+        // summation order are those of the task plan, independent of the CTA size.
+        if (!p.tp && !p.lpr && !p.rb && !spmv_threads_overridden() && p.nt > 256 &&
+            A.plan->ntiles + A.plan->nchunks < (long long)c.num_sms * (p.nt / 32)) {
+            p.nt = 256;
+            items = (A.plan->ntiles + A.plan->nchunks + 7) / 8;
+        }
     } else {
         items = (n + 1023) / 1024;
     }
