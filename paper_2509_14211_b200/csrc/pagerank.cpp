@@ -202,12 +202,11 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
     const double a_n = p->alpha / (double)n, tele = (1.0 - p->alpha) / (double)n;
 
     // Fig. 6 l.278-281 `d` (reading Q2: dinv = (T)(alpha / deg), 0 for dangling vertices)
-    nbg_vector d64, dinv_blk, mask = nullptr;
+    nbg_vector d64, dinv_blk;
     TRY(nbg_apply(ctx, &d64, NBG_FP64, nbg_unop{NBG_RECIP_SCALED, p->alpha, 0.0}, deg_blk));
     TRY(nbg_convert(ctx, &dinv_blk, T, d64));
     nbg_vector_free(ctx, d64);
     TRY(nbg_vector_wait(ctx, dinv_blk));
-    if (uniform) TRY(nbg_apply(ctx, &mask, T, nbg_unop{NBG_ISZERO, 0, 0}, dinv_blk));
 
     // exchange of y = t * dinv (+ the local partials of the given scalars) -> full x on every rank
     auto exchange = [&](nbg_vector t, int ns, nbg_scalar *loc, nbg_vector *x, nbg_scalar *glob) -> nbg_status {
@@ -218,10 +217,16 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
         for (int i = 0; i < ns; i++) nbg_scalar_free(ctx, loc[i]);
         return st;
     };
+    // the dangling mask is recorded afresh per sweep and released at once (as in nbg_pagerank): not
+    // user-live at the wait, it is elided and fused as iszero(dinv[i]) on the dinv the epilogue loads
+    // anyway -- a held mask would be materialised and read as a third n-vector every sweep
     auto dangling_mass = [&](nbg_vector r, nbg_scalar *s) -> nbg_status {
-        nbg_vector tm;
-        TRY(nbg_ewise_mult(ctx, &tm, T, nbg_binop{NBG_TIMES, 0}, r, mask));
-        nbg_status st = nbg_reduce(ctx, s, NBG_FP64, NBG_PLUS, tm);
+        nbg_vector mask, tm;
+        TRY(nbg_apply(ctx, &mask, T, nbg_unop{NBG_ISZERO, 0, 0}, dinv_blk));
+        nbg_status st = nbg_ewise_mult(ctx, &tm, T, nbg_binop{NBG_TIMES, 0}, r, mask);
+        nbg_vector_free(ctx, mask);
+        if (st != NBG_SUCCESS) return st;
+        st = nbg_reduce(ctx, s, NBG_FP64, NBG_PLUS, tm);
         nbg_vector_free(ctx, tm);
         return st;
     };
@@ -320,7 +325,6 @@ extern "C" nbg_status nbg_pagerank_dist(nbg_ctx *ctx, nbg_matrix AT_blk, nbg_vec
         nbg_scalar_free(ctx, deltas[j]);
     }
     nbg_vector_free(ctx, t);
-    if (mask) nbg_vector_free(ctx, mask);
     nbg_vector_free(ctx, dinv_blk);
     *r_out = rk;
     if (sweeps_out) *sweeps_out = k;
