@@ -270,3 +270,47 @@ def test_csr_already_in_gather_layout(nbg, T):
         assert rel(v1, ro) <= (1e-5 if T == "fp32" else 1e-10)
     finally:
         nbg.nbg_finalize(c)
+
+
+def test_nccl_transport_one_rank(nbg):
+    """The NCCL transport itself -- the one bench.py --gpus N uses under torchrun -- at one rank (the
+    pool gives one GPU per call, and NCCL refuses two ranks on one device): the library dlopens the
+    NCCL that torch already loaded, all-gathers the unique id (here: one rank), and runs the
+    per-sweep group (the slice broadcast and the exact slot sums) in both exchange modes, plus the
+    NCCL-only entry points nbg_vector_allgather and nbg_scalar_allreduce.  Every result equals the
+    same solve without a group bit for bit (a one-rank broadcast and integer limb sum are exact)."""
+    import torch  # noqa: F401  (loads torch's libnccl.so.2 first, as bench.py's process group does)
+    T = nbg.FP32
+    ref = nbg.nbg_init(nbg.NONBLOCKING, 0)
+    try:
+        A, d, cuts, ncg = nbg.nbg_dist_graph_from_generator(ref, nbg.GRAPH_RMAT, 12, 16, 3, nranks=1)
+        r0, s0, h0 = nbg.nbg_pagerank_dist(ref, A, d, cuts, ncg, tol=1e-7, itermax=100, type=T)
+        v0 = nbg.nbg_vector_export_dense(ref, r0)
+    finally:
+        nbg.nbg_finalize(ref)
+    for mode in (nbg.DIST_EXCHANGE_COLLECTIVE, nbg.DIST_EXCHANGE_PEER):
+        c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+        try:
+            nbg.nbg_dist_init(c, 0, 1, nbg.nbg_dist_unique_id())
+            nbg.nbg_dist_set_exchange(c, mode)
+            A, d, cuts1, ncg1 = nbg.nbg_dist_graph_from_generator(c, nbg.GRAPH_RMAT, 12, 16, 3, nranks=1)
+            assert np.array_equal(cuts1, cuts) and ncg1 == ncg
+            for _ in range(2):     # the second solve reuses the plans (and, in peer mode, the exchange buffers)
+                r1, s1, h1 = nbg.nbg_pagerank_dist(c, A, d, cuts1, ncg1, tol=1e-7, itermax=100, type=T)
+                assert s1 == s0
+                assert np.array_equal(nbg.nbg_vector_export_dense(c, r1), v0)
+                assert np.array_equal(h1[:s1], h0[:s0])
+                nbg.nbg_vector_free(c, r1)
+            x = np.random.default_rng(5).random(1000).astype(np.float32)
+            u = nbg.nbg_vector_from_dense(c, T, x)
+            w = nbg.nbg_vector_allgather(c, u, np.array([0, x.size], np.int64))
+            assert np.array_equal(nbg.nbg_vector_export_dense(c, w), x)
+            s = nbg.nbg_reduce(c, nbg.FP64, "PLUS", u)
+            sa = nbg.nbg_scalar_allreduce(c, s)
+            assert nbg.nbg_scalar_get(c, sa) == nbg.nbg_scalar_get(c, s) == math.fsum(x.astype(np.float64))
+            for v in (u, w):
+                nbg.nbg_vector_free(c, v)
+            for v in (s, sa):
+                nbg.nbg_scalar_free(c, v)
+        finally:
+            nbg.nbg_finalize(c)
