@@ -1204,11 +1204,16 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     const int dyn_bytes = std::max(16, hot_region + NW * NF * 12 * 8);
     if (hot_entries) *hot_entries = hot_cap;
     std::string gx;
+    // cold-gather qualifier: ld.global.cg (L2 only, default) or, NBG_SPMV_COLD=nc / el, the read-only path
+    // with L1 allocation (plain / L1::evict_last); DESIGN.md section 7 has the measured sweep
+    const char *ecold = getenv("NBG_SPMV_COLD");
+    const std::string ec = ecold ? ecold : "";
+    const std::string sfx = ec == "nc" ? "nc" : (ec == "el" ? "el" : "");
     switch (sp.xt) {
-        case NBG_FP32: gx = "__uint_as_float(nbg_gx32(s_base, X, C_, hc))"; break;
-        case NBG_INT32: gx = "((int)nbg_gx32(s_base, X, C_, hc))"; break;
-        case NBG_FP64: gx = "__longlong_as_double((long long)nbg_gx64(s_base, X, C_, hc))"; break;
-        case NBG_INT64: gx = "((long long)nbg_gx64(s_base, X, C_, hc))"; break;
+        case NBG_FP32: gx = "__uint_as_float(nbg_gx32" + sfx + "(s_base, X, C_, hc))"; break;
+        case NBG_INT32: gx = "((int)nbg_gx32" + sfx + "(s_base, X, C_, hc))"; break;
+        case NBG_FP64: gx = "__longlong_as_double((long long)nbg_gx64" + sfx + "(s_base, X, C_, hc))"; break;
+        case NBG_INT64: gx = "((long long)nbg_gx64" + sfx + "(s_base, X, C_, hc))"; break;
         default: gx = "((C_) < hc ? s_hot[(C_)] : X[(C_)])"; break;
     }
     const bool zero_pad = sp.add == NBG_PLUS && !sp.has_vals && (sp.mul == NBG_SECOND || sp.mul == NBG_TIMES);

@@ -495,6 +495,18 @@ __device__ __forceinline__ unsigned nbg_gx32nc(unsigned sbase, const void *X, in
         : "=r"(r) : "r"(c), "r"(hc), "r"(sbase + 4u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned *)X + c));
     return r;
 }
+__device__ __forceinline__ unsigned nbg_gx32el(unsigned sbase, const void *X, int c, int hc) {
+    unsigned r;
+    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b32 %0, [%3]; @!p ld.global.nc.L1::evict_last.b32 %0, [%4]; }"
+        : "=r"(r) : "r"(c), "r"(hc), "r"(sbase + 4u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned *)X + c));
+    return r;
+}
+__device__ __forceinline__ unsigned long long nbg_gx64el(unsigned sbase, const void *X, int c, int hc) {
+    unsigned long long r;
+    asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b64 %0, [%3]; @!p ld.global.nc.L1::evict_last.b64 %0, [%4]; }"
+        : "=l"(r) : "r"(c), "r"(hc), "r"(sbase + 8u * (unsigned)(c < hc ? c : 0)), "l"((const unsigned long long *)X + c));
+    return r;
+}
 __device__ __forceinline__ unsigned long long nbg_gx64nc(unsigned sbase, const void *X, int c, int hc) {
     unsigned long long r;
     asm("{ .reg .pred p; setp.lt.s32 p, %1, %2; @p ld.shared.b64 %0, [%3]; @!p ld.global.nc.b64 %0, [%4]; }"

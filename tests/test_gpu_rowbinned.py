@@ -263,3 +263,34 @@ def test_rb_row_groups(nbg, monkeypatch, ng):
             assert np.array_equal(v, runs[0][0]) and np.array_equal(h, runs[0][1])
     finally:
         nbg.nbg_finalize(c)
+
+
+@pytest.mark.parametrize("T", ["fp32", "fp64"])
+def test_rb_cold_gather_qualifiers_same_bits(nbg, monkeypatch, T):
+    """NBG_SPMV_COLD picks the load the cold gathers use (ld.global.cg by default, the read-only path
+    with L1 allocation for nc / el; DESIGN.md §7 has the measured sweep): the qualifier is a cache
+    hint only, so every variant must return the same bits.  The matrix has more non-empty columns
+    than the shared-memory hot cache holds (≈ 43 K fp32 / 21 K fp64 entries), so cold gathers run."""
+    monkeypatch.setenv("NBG_SPMV_RB", "1")
+    rng = np.random.default_rng(11)
+    n, m = 3000, 400000
+    lens = _lens(rng, n)
+    lens[rng.choice(n, 40, replace=False)] = 4000
+    rp, ci = _matrix(rng, n, m, lens)
+    assert np.unique(ci).size > 60000
+    t = nbg.TYPE_OF[T]
+    npT = nbg.NP_OF[t]
+    x = rng.random(m).astype(npT)
+    res = {}
+    for q in ["cg", "nc", "el"]:
+        monkeypatch.setenv("NBG_SPMV_COLD", q)
+        c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+        try:
+            A = nbg.nbg_matrix_from_csr(c, n, m, rp, ci, type=t)
+            res[q] = nbg.nbg_vector_export_dense(c, nbg.nbg_mxv(c, t, "PLUS", "SECOND", A, nbg.nbg_vector_from_dense(c, t, x)))
+        finally:
+            nbg.nbg_finalize(c)
+    exp = ops.mxv("PLUS", "SECOND", rp, ci, None, x, npT)
+    assert rel(res["cg"][lens > 0], exp[lens > 0]) <= (2e-7 if T == "fp32" else 1e-14)
+    assert np.array_equal(res["nc"], res["cg"])
+    assert np.array_equal(res["el"], res["cg"])
