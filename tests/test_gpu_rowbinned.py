@@ -294,3 +294,31 @@ def test_rb_cold_gather_qualifiers_same_bits(nbg, monkeypatch, T):
     assert rel(res["cg"][lens > 0], exp[lens > 0]) <= (2e-7 if T == "fp32" else 1e-14)
     assert np.array_equal(res["nc"], res["cg"])
     assert np.array_equal(res["el"], res["cg"])
+
+
+def test_rb_epilogue_cache_hints_same_bits(nbg, monkeypatch, rb_mode):
+    """NBG_RB_EPI_HINT puts an L2 cache policy on the epilogue pass's fp32 vector loads / stores
+    (default: evict_first input loads): a hint only -- ranks and the delta history
+    must equal the hint-free kernel's bit for bit, and the oracle within the north-star tolerance."""
+    monkeypatch.setenv("NBG_SPMV_RB", "1")
+    res = {}
+    rp = ci = d = None
+    for hint in ["0", "ef", "efs", "el", "els", ""]:
+        if hint:
+            monkeypatch.setenv("NBG_RB_EPI_HINT", hint)
+        else:
+            monkeypatch.delenv("NBG_RB_EPI_HINT", raising=False)     # the default choice
+        c = nbg.nbg_init(nbg.NONBLOCKING, 0)
+        try:
+            A, deg = nbg.nbg_matrix_from_generator(c, nbg.GRAPH_RMAT, 13, 16, 5)
+            if rp is None:
+                rp, ci = nbg.nbg_matrix_export_csr(c, A)
+                d = nbg.nbg_vector_export_dense(c, deg)
+            r, s, h = nbg.nbg_pagerank(c, A, deg, tol=-1.0, itermax=10, dangling=nbg.PR_UNIFORM, type=nbg.FP32)
+            res[hint] = (nbg.nbg_vector_export_dense(c, r), s, np.asarray(h))
+        finally:
+            nbg.nbg_finalize(c)
+    ro, so, _, _ = oracle.pagerank(rp, ci, d, dtype=np.float32, itermax=10, uniform=True)
+    assert res["0"][1] == so == 10 and rel(res["0"][0], ro) <= 1e-5
+    for hint in ["ef", "efs", "el", "els", ""]:
+        assert np.array_equal(res[hint][0], res["0"][0]) and np.array_equal(res[hint][2], res["0"][2])
