@@ -1322,12 +1322,15 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
     // off when it does not (C5: 3.53 ms without, 3.58 ms with).  NBG_RB_EPI_HINT=0 turns it off.
     const char *ehint = getenv("NBG_RB_EPI_HINT");
     const std::string eh = PIPE ? "" : (ehint && *ehint ? std::string(ehint) : std::string(hk_ >= 140 ? "ef" : ""));
-    const bool hint_ld = eh == "el" || eh == "els" || eh == "ef" || eh == "efs", hint_st = eh == "els" || eh == "efs";
+    // "efl": evict_first loads, evict_last stores (the stored r is the next sweep's t)
+    const bool hint_ld = eh == "el" || eh == "els" || eh == "ef" || eh == "efs" || eh == "efl", hint_st = eh == "els" || eh == "efs" || eh == "efl";
     auto vec_trip = [&](const std::string &ind) {
         o << ind << "{\n";
         if (hint_ld)
             o << ind << "  unsigned long long pol_; asm(\"createpolicy.fractional.L2::" << (eh[1] == 'f' ? "evict_first" : "evict_last")
               << ".b64 %0, 1.0;\" : \"=l\"(pol_));\n";
+        if (eh == "efl")
+            o << ind << "  unsigned long long pols_; asm(\"createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\" : \"=l\"(pols_));\n";
         for (int s2 = 0; s2 < p.n_in; s2++)
             if (slot_type[s2] >= 0) {
                 o << ind << "  " << ctype(slot_type[s2]) << " L" << s2 << "[4];\n";
@@ -1363,7 +1366,7 @@ int gen_spmv_rb(Gen &g, const std::string &kname, int *hot_entries) {
                 if (hint_st && out_type[k2] == NBG_FP32) {
                     const std::string O = "O" + std::to_string(k2);
                     o << ind << "  asm volatile(\"st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;\" :: \"l\"(((float4*)(a.out[" << k2
-                      << "])) + vi), \"f\"(" << O << "[0]), \"f\"(" << O << "[1]), \"f\"(" << O << "[2]), \"f\"(" << O << "[3]), \"l\"(pol_) : \"memory\");\n";
+                      << "])) + vi), \"f\"(" << O << "[0]), \"f\"(" << O << "[1]), \"f\"(" << O << "[2]), \"f\"(" << O << "[3]), \"l\"(" << (eh == "efl" ? "pols_" : "pol_") << ") : \"memory\");\n";
                     continue;
                 }
                 o << ind << "  " << vstore(out_type[k2], "a.out[" + std::to_string(k2) + "]", "vi", "O" + std::to_string(k2)) << "\n";

@@ -303,7 +303,7 @@ def test_rb_epilogue_cache_hints_same_bits(nbg, monkeypatch, rb_mode):
     monkeypatch.setenv("NBG_SPMV_RB", "1")
     res = {}
     rp = ci = d = None
-    for hint in ["0", "ef", "efs", "el", "els", ""]:
+    for hint in ["0", "ef", "efs", "efl", "el", "els", ""]:
         if hint:
             monkeypatch.setenv("NBG_RB_EPI_HINT", hint)
         else:
@@ -320,5 +320,5 @@ def test_rb_epilogue_cache_hints_same_bits(nbg, monkeypatch, rb_mode):
             nbg.nbg_finalize(c)
     ro, so, _, _ = oracle.pagerank(rp, ci, d, dtype=np.float32, itermax=10, uniform=True)
     assert res["0"][1] == so == 10 and rel(res["0"][0], ro) <= 1e-5
-    for hint in ["ef", "efs", "el", "els", ""]:
+    for hint in ["ef", "efs", "efl", "el", "els", ""]:
         assert np.array_equal(res[hint][0], res["0"][0]) and np.array_equal(res[hint][2], res["0"][2])
